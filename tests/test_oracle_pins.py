@@ -1,0 +1,551 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU).
+
+Each test names the passage (P:n = PAPER.md line) or DESIGN.md reading (Qn) it
+pins, and checks the oracle against something other than itself: printed /
+hand-computed worked examples (tests/golden), closed forms, brute force on tiny
+inputs, library routines, invariants.
+"""
+import itertools
+import json
+import math
+import os
+from math import comb
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1805_08166_b200 import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+ANN = {"serial": 0, "unroll": 1, "vectorize": 2, "parallel": 3, "blockIdx": 4, "vthread": 5, "threadIdx": 6}
+
+
+def W(d):
+    return O.workload(**d)
+
+
+def space(*ws):
+    return O.OracleSpace([W(w) for w in ws])
+
+
+# ---------------------------------------------------------------- RNG / exp_det
+def test_philox_known_answers():
+    """Q28: Philox4x32-10 must reproduce Random123's published KAT vectors."""
+    kat = json.load(open(os.path.join(GOLD, "philox_kat.json")))
+    for v in kat["vectors"]:
+        ctr = [int(x, 16) for x in v["ctr"]]
+        key = [int(x, 16) for x in v["key"]]
+        assert O.philox(ctr, key) == [int(x, 16) for x in v["out"]]
+
+
+def test_mulhi64_against_bigint():
+    g = np.random.default_rng(1)
+    for _ in range(2000):
+        a = int(g.integers(0, 2**63)) * 2 + int(g.integers(0, 2))
+        b = int(g.integers(1, 2**62))
+        assert O.mulhi64(a, b) == (a * b) >> 64
+
+
+def test_exp_det_special_values_and_accuracy():
+    """Q22: exp_det(0) = 1, clamps at -87 / 88, and is within 2 ulp of fp64 exp on [-87, 88]."""
+    assert O.exp_det(0.0) == 1.0
+    assert O.exp_det(-0.0) == 1.0
+    assert O.exp_det(-87.5) == 0.0
+    assert O.exp_det(88.5) == math.inf
+    xs = np.concatenate([np.linspace(-87, 88, 20001), np.linspace(-1, 1, 5001)]).astype(np.float32)
+    got = O.exp_det_array(xs).astype(np.float64)
+    ref = np.exp(xs.astype(np.float64))
+    ulp = np.spacing(ref.astype(np.float32)).astype(np.float64)
+    assert np.max(np.abs(got - ref) / ulp) <= 2.0
+    # monotone non-decreasing over the grid
+    s = np.sort(xs)
+    v = O.exp_det_array(s)
+    assert np.all(np.diff(v.astype(np.float64)) >= 0)
+
+
+# ---------------------------------------------------------------- space (a1, a2)
+def _closed_form_factorizations(n, L):
+    """Number of ordered L-factorizations of n = prod_p C(e_p + L - 1, L - 1)."""
+    out, p, m = 1, 2, n
+    while p * p <= m:
+        e = 0
+        while m % p == 0:
+            m //= p
+            e += 1
+        out *= comb(e + L - 1, L - 1)
+        p += 1
+    if m > 1:
+        out *= L
+    return out
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 12, 28, 56, 64, 112, 128, 224, 512, 1024])
+@pytest.mark.parametrize("L", [2, 3, 4])
+def test_factorization_counts_closed_form(n, L):
+    assert O.count_factorizations(n, L) == _closed_form_factorizations(n, L)
+
+
+def test_factor_tables_lexicographic_and_exhaustive():
+    """O2: a split knob's domain is every ordered L-tuple with product = extent, lexicographic."""
+    sp = space(synth.CFG2A)
+    for j, (ext, L) in enumerate([(128, 4), (28, 4), (28, 4), (128, 2), (3, 2), (3, 2)]):
+        tab = sp.factors(0, j)
+        brute = sorted(t for t in itertools.product(range(1, ext + 1), repeat=L) if math.prod(t) == ext) \
+            if ext <= 28 else None
+        if brute is not None:
+            assert tab == brute
+        assert tab == sorted(tab)
+        assert all(math.prod(t) == ext for t in tab)
+        assert len(set(tab)) == len(tab) == _closed_form_factorizations(ext, L)
+
+
+def test_space_cardinalities():
+    """|S_e| = prod_j r_j (north_star pin); sizes quoted in DESIGN.md section 4."""
+    assert space(synth.MATMUL_512).size() == 55 * 55 * 10 * 5 == 151_250
+    assert space(synth.MATMUL_8).size() == 10 * 10 * 4 * 5 == 2000
+    assert space(synth.CFG2A).size() == 221_184_000
+    assert space(synth.CFG2B).size() == 48_660_480
+    u = space(*synth.ALL_RESNET)
+    assert u.size() == 1_740_983_040
+    expect_dw = [158_054_400, 77_414_400, 110_592_000, 27_648_000, 38_016_000,
+                 6_082_560, 8_110_080, 506_880, 658_944]
+    d = space(*synth.ALL_DW)
+    assert [d.size(w) for w in range(9)] == expect_dw
+    for w in range(9):
+        assert d.size(w) == math.prod(d.radices(w))
+
+
+def test_mixed_radix_roundtrip():
+    """S:138-146 mixed-radix bijection: 0 -> zeros, size-1 -> maxima, round trip."""
+    for wl in (synth.MATMUL_512, synth.CFG2A, synth.ALL_DW[0]):
+        sp = space(wl)
+        r = sp.radices()
+        assert sp.decode(0) == [0] * len(r)
+        assert sp.decode(sp.size() - 1) == [x - 1 for x in r]
+        for idx in synth.uniform_indices(sp.size(), 500, seed=3):
+            ch = sp.decode(int(idx))
+            assert all(0 <= c < x for c, x in zip(ch, r))
+            assert sp.encode(ch) == int(idx)
+            # knob 0 fastest
+            assert int(idx) == sum(c * math.prod(r[:j]) for j, c in enumerate(ch))
+
+
+# ---------------------------------------------------------------- features (a3, a4)
+def _check_rows(sp, choices, gold, n_rows):
+    ns, rows = sp.context(choices)
+    assert ns.n == n_rows
+    for k, (r, g) in enumerate(zip(rows, gold["rows"])):
+        got = [r.length, r.top_down, r.bottom_up]
+        for b in range(3):
+            got += [r.touch[b], r.reuse[b], r.stride[b]]
+        assert got == pytest.approx(g, abs=0), f"loop {gold['loops'][k]}"
+        assert r.ann == ANN[gold["annotations"][k]], gold["loops"][k]
+
+
+def test_appendix_c_matmul_example():
+    """Fig. 1 matmul lowered with the tiled 8^3 schedule: every context column of P:630-637."""
+    gold = json.load(open(os.path.join(GOLD, "appendix_c_matmul.json")))
+    sp = space(gold["workload"])
+    s = gold["splits"]
+    ch = [sp.factors(0, 0).index(tuple(s["i"])), sp.factors(0, 1).index(tuple(s["j"])),
+          sp.factors(0, 2).index(tuple(s["k"])), [1, 2, 4, 8, 16].index(gold["unroll"])]
+    _check_rows(sp, ch, gold, 8)
+    x = sp.features([sp.encode(ch)])[0]
+    rel = gold["relation_t1_6"]
+    for b, name in enumerate("CAB"):
+        assert list(x[342 + 40 * b: 342 + 40 * b + 6]) == rel[f"{name}_reuse"]
+        assert list(x[362 + 40 * b: 362 + 40 * b + 6]) == rel[f"{name}_topdown"]
+    assert list(x[462:468]) == [512, 64, 64, 64, 0, 0]
+    assert np.all(x[8 * 19:342] == 0)          # absent rows are zero (Q15)
+
+
+def test_appendix_c2_conv_example():
+    """T_CONV worked example: thread binding, distinct-element touch (Q5), fractional reuse."""
+    gold = json.load(open(os.path.join(GOLD, "appendix_c2_conv.json")))
+    sp = space(gold["workload"])
+    t = gold["tiles"]
+    ch = [sp.factors(0, j).index(tuple(t[a])) for j, a in enumerate(["f", "y", "x", "rc", "ry", "rx"])]
+    ch += [gold["reorder"], [0, 512, 1500].index(gold["unroll"]), gold["vectorize"]]
+    _check_rows(sp, ch, gold, 18)
+    x = sp.features([sp.encode(ch)])[0]
+    assert x[462] == gold["total_iters"]
+
+
+def test_naive_matmul_innermost_k():
+    """SPEC S:231 example: naive 4^3, innermost k: C touch 1 reuse 4 stride 0; A touch 4 reuse 1 stride 4."""
+    sp = space(dict(kind=0, n=4, m=4, k=4))
+    ch = [sp.factors(0, 0).index((4, 1, 1)), sp.factors(0, 1).index((4, 1, 1)), sp.factors(0, 2).index((4, 1)), 0]
+    ns, rows = sp.context(ch)
+    k = 2                                       # k0 is the innermost non-unit loop of i0 j0 k0
+    assert (rows[k].touch[0], rows[k].reuse[0], rows[k].stride[0]) == (1, 4.0, 0)
+    assert (rows[k].touch[1], rows[k].reuse[1], rows[k].stride[1]) == (4, 1.0, 4)
+
+
+def _random_choices(sp, n, seed):
+    return [sp.decode(int(i)) for i in synth.uniform_indices(sp.size(), n, seed=seed)]
+
+
+@pytest.mark.parametrize("wl", [synth.MATMUL_8, synth.CONV_TINY, dict(kind=1, h=6, w=6, ic=2, oc=4, ksize=3, stride=2, pad=1),
+                                dict(kind=2, h=6, w=6, ic=4, oc=4, ksize=3, stride=2, pad=1),
+                                dict(kind=1, h=5, w=5, ic=2, oc=2, ksize=1, stride=1, pad=0)])
+def test_touch_equals_flat_bruteforce(wl):
+    """P:635 literal: per-dimension enumeration == enumeration of the whole flat buffer on tiny nests."""
+    sp = space(wl)
+    for ch in _random_choices(sp, 30, seed=7):
+        ns = sp.lower(ch)
+        for k in range(ns.n):
+            for b in range(3):
+                assert sp.touch(ns, b, k) == sp.touch(ns, b, k, brute=True)
+
+
+def _closed_touch(sp, ns, b, k):
+    """Independent closed form: per-dim product of active extents, min(YR,(Y-1)S+R) for y*S+ry."""
+    w = sp.workloads[0]
+    act = {}
+    for l in range(k, ns.n):
+        act[ns.axis[l]] = act.get(ns.axis[l], 1) * ns.ext[l]
+    A = lambda a: act.get(a, 1)
+    S = w.stride
+    comp = lambda Y, R: min(Y * R, (Y - 1) * S + R)
+    if sp.s.sp[0].tmpl == 1:
+        dims = {0: [A(0), A(1), A(2)], 1: [A(3), comp(A(1), A(4)), comp(A(2), A(5))], 2: [A(0), A(3), A(4), A(5)]}
+    elif sp.s.sp[0].tmpl == 2:
+        dims = {0: [A(0), A(1), A(2)], 1: [A(0), comp(A(1), A(3)), comp(A(2), A(4))], 2: [A(0), A(3), A(4)]}
+    else:
+        dims = {0: [A(0), A(1)], 1: [A(2), A(0)], 2: [A(2), A(1)]}
+    return math.prod(dims[b])
+
+
+@pytest.mark.parametrize("wl", [synth.CFG2A, synth.CFG2B, synth.resnet("C1"), synth.ALL_DW[1], synth.MATMUL_512])
+def test_touch_closed_form_agrees(wl):
+    sp = space(wl)
+    for ch in _random_choices(sp, 25, seed=11):
+        ns = sp.lower(ch)
+        for k in range(ns.n):
+            for b in range(3):
+                assert sp.touch(ns, b, k) == _closed_touch(sp, ns, b, k)
+
+
+@pytest.mark.parametrize("wl", [synth.MATMUL_512, synth.CFG2A, synth.ALL_DW[3], synth.resnet("C11")])
+def test_feature_invariants(wl):
+    """top_down * bottom_up = total; top_down(0) = 1; bottom_up(last) = extent;
+    touch(b, 0) = full output / kernel buffer; R_t non-decreasing in t; exactly one annotation."""
+    sp = space(wl)
+    ss = sp.s.sp[0]
+    full = [math.prod(ss.shape[b][d] for d in range(ss.n_dims[b])) for b in range(3)]
+    idx = synth.uniform_indices(sp.size(), 40, seed=5)
+    X = sp.features(idx)
+    for i, x in zip(idx, X):
+        ns, rows = sp.context(sp.decode(int(i)))
+        total = math.prod(ns.ext[k] for k in range(ns.n))
+        assert rows[0].top_down == 1 and rows[-1].bottom_up == rows[-1].length
+        for k, r in enumerate(rows):
+            assert r.top_down * r.bottom_up == total
+            assert sum(x[19 * k + 1: 19 * k + 8]) == 1
+        assert rows[0].touch[0] == full[0]
+        if ss.tmpl == 0:
+            assert rows[0].touch[1] == full[1] and rows[0].touch[2] == full[2]
+        else:
+            assert rows[0].touch[2] == full[2]
+        for b in range(3):
+            for p in range(2):
+                R = x[342 + 40 * b + 20 * p: 342 + 40 * b + 20 * p + 20]
+                assert np.all(np.diff(R) >= 0)
+        assert x[462] == np.float32(total)
+        assert x[466] == 0 and x[467] == 0
+
+
+def test_relation_feature_spec_example():
+    """touch column [100, 10] with reuse [4, 8] and beta = 32 -> 8 (only the inner loop qualifies).
+    Realised as a 2-loop matmul-like nest: the relation value at t = 5 is the inner loop's reuse."""
+    sp = space(dict(kind=0, n=100, m=1, k=1))
+    # i = (1, 10, 10) -> loops i0(1) j0 k0 i1(10) j1 k1 i2(10) j2; pick the row values directly
+    ch = [sp.factors(0, 0).index((1, 10, 10)), 0, 0, 0]
+    x = sp.features([sp.encode(ch)])[0]
+    ns, rows = sp.context(ch)
+    t = 5
+    qual = [r for r in rows if r.touch[0] < 2 ** t]
+    assert x[342 + t - 1] == max(r.reuse[0] for r in qual)
+    assert all(r.touch[0] >= 2 ** t for r in rows if r not in qual)
+
+
+# ---------------------------------------------------------------- GBT (a5)
+def test_hand_ensemble_predictions():
+    """north_star pin: a tiny hand-built ensemble yields known predictions and leaf slots (Q18)."""
+    e = O.OracleGbt(**synth.hand_ensemble())
+    X = np.array([[1, 0], [2.5, 1.5], [3, 0.7]], np.float32)
+    s, sl = e.predict(X, slots=True)
+    assert list(s) == [1.25, 3.5, 3.25]
+    assert sl.T.tolist() == [[0, 0], [3, 2], [2, 0]]
+
+
+def test_gbt_canonical_sum_close_to_fp64_and_batch_equals_single():
+    ens = synth.ensemble(333, 6, seed=9)
+    e = O.OracleGbt(**ens)
+    sp = space(synth.CFG2A)
+    X = sp.features(synth.uniform_indices(sp.size(), 64, seed=2))
+    s, sl = e.predict(X, slots=True)
+    ni = 63
+    ref = np.zeros(len(X))
+    for i in range(len(X)):   # independent pointer-walk in fp64
+        tot = 0.0
+        for t in range(333):
+            node = 0
+            for _ in range(6):
+                node = 2 * node + (1 if X[i, ens["feat"][t, node]] < ens["thresh"][t, node] else 2)
+            assert sl[t, i] == node - ni
+            tot += float(ens["leaf"][t, node - ni])
+        ref[i] = tot
+    assert np.allclose(s, ref, rtol=1e-6, atol=1e-6)
+    for i in range(0, 64, 9):
+        assert e.predict(X[i:i + 1])[0] == s[i]
+
+
+# ---------------------------------------------------------------- SA + top-k (a6, a7)
+def _tiny():
+    sp = space(synth.MATMUL_8)
+    ens = synth.ensemble(40, 6, seed=4)
+    return sp, O.OracleGbt(**ens), ens
+
+
+def test_sa_infinite_temperature_accepts_everything():
+    sp, e, _ = _tiny()
+    r = sp.sa_explore(e, 16, 40, seed=1805, round_=0, temps=np.full(40, np.inf, np.float32))
+    assert np.all(r["accept_bits"][:, 0] == 0xFFFFFFFF)
+    assert np.all(r["accept_bits"][:, 1] == (1 << 8) - 1)
+    assert np.all(r["chain_idx"] == r["visited_idx"][:, -1])
+
+
+def test_sa_zero_temperature_is_greedy_and_proposals_are_single_knob():
+    sp, e, _ = _tiny()
+    steps = 64
+    r = sp.sa_explore(e, 24, steps, seed=7, round_=2, temps=np.zeros(steps, np.float32))
+    X = sp.features(r["visited_idx"].ravel())
+    E = e.predict(X).reshape(24, steps + 1)
+    assert np.array_equal(E, r["visited_E"])
+    for c in range(24):
+        cur_i, cur_E = r["visited_idx"][c, 0], E[c, 0]
+        for s in range(steps):
+            prop = r["visited_idx"][c, s + 1]
+            a, b = sp.decode(int(cur_i)), sp.decode(int(prop))
+            assert sum(x != y for x, y in zip(a, b)) == 1        # S:151 single-knob move
+            acc = (r["accept_bits"][c, s // 32] >> (s % 32)) & 1
+            assert acc == (1 if E[c, s + 1] <= cur_E else 0)     # T = 0: accept iff E' <= E
+            if acc:
+                cur_i, cur_E = prop, E[c, s + 1]
+        assert r["chain_idx"][c] == cur_i and r["chain_energy"][c] == cur_E
+
+
+def test_sa_topk_equals_exhaustive_ranking_on_tiny_space():
+    """north_star pin: SA top-k on a tiny space == brute-force exhaustive ranking."""
+    sp, e, _ = _tiny()
+    N = sp.size()
+    allidx = np.arange(N, dtype=np.uint64)
+    E_all = e.predict(sp.features(allidx))
+    order = np.lexsort((allidx, E_all))
+    r = sp.sa_explore(e, N, 3, seed=5, round_=0, temps=np.full(3, 0.05, np.float32), chain_idx=allidx)
+    (ti, tE), = sp.topk(r["visited_E"], r["visited_idx"], 64)
+    assert np.array_equal(ti, allidx[order[:64]])
+    assert np.array_equal(tE, E_all[order[:64]])
+    # measured configs are excluded
+    meas = allidx[order[:10]]
+    (ti2, _), = sp.topk(r["visited_E"], r["visited_idx"], 64, measured=meas)
+    assert np.array_equal(ti2, allidx[order[10:74]])
+
+
+def test_sa_deterministic_and_persistent():
+    sp, e, _ = _tiny()
+    T = synth.temperatures(30, 0.3)
+    r1 = sp.sa_explore(e, 8, 30, seed=11, round_=0, temps=T)
+    r2 = sp.sa_explore(e, 8, 30, seed=11, round_=0, temps=T)
+    assert np.array_equal(r1["accept_bits"], r2["accept_bits"])
+    r3 = sp.sa_explore(e, 8, 30, seed=11, round_=1, temps=T, chain_idx=r1["chain_idx"])
+    assert np.array_equal(r3["visited_idx"][:, 0], r1["chain_idx"])          # P:187 persistence
+    # chain ids are global: chains 4..7 alone reproduce the same trajectories (rank invariance)
+    r4 = sp.sa_explore(e, 4, 30, seed=11, round_=0, temps=T, chain_id_base=4)
+    assert np.array_equal(r4["visited_idx"], r1["visited_idx"][4:])
+
+
+def test_sa_knob_frequencies_uniform():
+    """each non-singleton knob is mutated with frequency 1/#non-singleton (+-5%)."""
+    sp, e, _ = _tiny()
+    r = sp.sa_explore(e, 64, 200, seed=3, round_=0, temps=np.full(200, np.inf, np.float32))
+    cnt = np.zeros(4)
+    for c in range(64):
+        for s in range(200):
+            a, b = sp.decode(int(r["visited_idx"][c, s])), sp.decode(int(r["visited_idx"][c, s + 1]))
+            cnt[[i for i in range(4) if a[i] != b[i]][0]] += 1
+    assert np.all(np.abs(cnt / cnt.sum() - 0.25) < 0.05 * 0.25 * 4)
+
+
+# ---------------------------------------------------------------- select (a8)
+def test_select_alpha0_eps0_is_plain_topb():
+    sp = space(synth.CFG2A)
+    idx = synth.uniform_indices(sp.size(), 128, seed=8)
+    E = np.random.default_rng(0).random(128).astype(np.float32)
+    E[5] = E[6]                                  # a tie, broken by idx
+    order = np.lexsort((idx, E))
+    got = sp.select(0, idx[order], E[order], b=64, eps=0.0, alpha=0.0, seed=1, round_=0)
+    assert np.array_equal(got, idx[order[:64]])
+
+
+def test_select_epsilon_picks():
+    """exactly ceil(eps b) random picks, never measured, never duplicated; greedy first."""
+    sp = space(synth.CFG2B)
+    idx = synth.uniform_indices(sp.size(), 128, seed=9)
+    E = np.random.default_rng(1).random(128).astype(np.float32)
+    order = np.lexsort((idx, E))
+    meas = synth.uniform_indices(sp.size(), 50, seed=10)
+    got = sp.select(0, idx[order], E[order], b=64, eps=0.05, alpha=0.1, seed=3, round_=4, measured=meas)
+    assert len(got) == 64 and len(set(got.tolist())) == 64
+    assert set(got[:60].tolist()) <= set(idx.tolist())
+    assert not set(got.tolist()) & set(meas.tolist())
+
+
+def test_select_exhausted_space_stops():
+    sp = space(dict(kind=0, n=1, m=1, k=2))     # |S| = 1*1*2*5 = 10
+    assert sp.size() == 10
+    meas = np.array([0, 1, 2, 3], np.uint64)
+    got = sp.select(0, np.array([4, 5], np.uint64), np.array([0.1, 0.2], np.float32), b=20, eps=0.5,
+                    alpha=0.0, seed=1, round_=0, measured=meas)
+    assert sorted(got.tolist()) == [4, 5, 6, 7, 8, 9]
+
+
+def test_select_greedy_vs_bruteforce_subsets():
+    """greedy L(S) >= (1 - 1/e) max_S L(S) (L shifted non-negative on singletons), pools of 8, b = 4."""
+    sp = space(synth.CFG2A)
+    g = np.random.default_rng(2)
+    for trial in range(20):
+        idx = synth.uniform_indices(sp.size(), 8, seed=100 + trial)
+        E = g.random(8).astype(np.float32)
+        alpha = 1.0
+        got = sp.select(0, idx, E, b=4, eps=0.0, alpha=alpha, seed=1, round_=0)
+        mu, sd = E.astype(np.float64).mean(), E.astype(np.float64).std()
+        z = (E - mu) / sd
+        ch = [sp.decode(int(i)) for i in idx]
+        shift = max(0.0, max(z))                 # makes -z + shift >= 0 per element
+
+        def L(S):
+            cov = sum(len({ch[i][j] for i in S}) for j in range(9))
+            return sum(-z[i] + shift for i in S) + alpha * cov
+
+        best = max(L(S) for S in itertools.combinations(range(8), 4))
+        mine = L([list(idx).index(i) for i in got])
+        assert mine >= (1 - 1 / math.e) * best - 1e-12
+
+
+# ---------------------------------------------------------------- refit (a9)
+def test_rank_loss_closed_forms():
+    """Eq. 2: each ordered pair contributes log(1 + e^{-sign (f_i - f_j)})."""
+    c = np.array([1, 2], np.float32)
+    assert O.rank_loss(c, np.array([0, 0], np.float32)) == pytest.approx(2 * math.log(2), rel=1e-12)
+    assert O.rank_loss(c, np.array([3, 1], np.float32)) == pytest.approx(2 * math.log(1 + math.e ** 2), rel=1e-12)
+
+
+def test_pair_gradients_match_finite_difference():
+    """g_i, h_i are the first/second derivatives of Eq. 2 summed over ordered pairs inside a group."""
+    g = np.random.default_rng(5)
+    n = 40                                       # one group (group_size 64)
+    cost = g.random(n).astype(np.float32)
+    pred = (g.random(n) - 0.5).astype(np.float32)
+    key = np.zeros(n, np.uint16)
+    G, H = O.pair_gradients(cost, pred, key, seed=1, tree=0, group_size=64)
+    for i in range(0, n, 7):
+        eps = 1e-3
+        p1, p2 = pred.astype(np.float64).copy(), pred.astype(np.float64).copy()
+        p1[i] += eps
+        p2[i] -= eps
+        # finite difference of Eq. 2 (libm exp, fp64) -- independent of exp_det
+        def L(p):
+            s = 0.0
+            for a in range(n):
+                for b in range(n):
+                    if a != b:
+                        sg = np.sign(cost[a] - cost[b])
+                        s += math.log1p(math.exp(-sg * (p[a] - p[b])))
+            return s
+        fd = (L(p1) - L(p2)) / (2 * eps)
+        fd2 = (L(p1) - 2 * L(pred.astype(np.float64)) + L(p2)) / eps ** 2
+        assert G[i] / 2 ** 32 == pytest.approx(fd, rel=1e-4, abs=1e-6)
+        assert H[i] / 2 ** 32 == pytest.approx(fd2, rel=2e-3, abs=1e-4)
+
+
+def test_group_positions_are_permutations_within_workloads():
+    key = synth.group_keys(3001, 5, seed=2)
+    for tree in (0, 1, 7):
+        pos = O.group_positions(key, seed=1805, tree=tree)
+        for w in range(5):
+            p = pos[key == w]
+            assert sorted(p.tolist()) == list(range(len(p)))
+    assert not np.array_equal(O.group_positions(key, 1805, 0), O.group_positions(key, 1805, 1))
+
+
+def _fit_data(n=600, seed=3, nw=2):
+    sp = space(synth.MATMUL_512, synth.CFG2B)
+    key = synth.group_keys(n, nw, seed=seed)
+    idx = np.array([sp.offset(int(w)) + int(synth.uniform_indices(sp.size(int(w)), 1, seed=seed * 1000 + i)[0])
+                    for i, w in enumerate(key)], np.uint64)
+    X = sp.features(idx)
+    return X, synth.labels(X, seed=seed), key
+
+
+def test_fit_label_affine_invariance():
+    """only sign(c_i - c_j) enters Eq. 2, so labels c and 2c + 5 give a bit-identical ensemble."""
+    X, c, key = _fit_data(300)
+    a = O.fit_hist(X, c, key, n_trees=4, depth=4)
+    b = O.fit_hist(X, (2 * c.astype(np.float64) + 5).astype(np.float32), key, n_trees=4, depth=4)
+    for k in ("feat", "thresh", "leaf"):
+        assert np.array_equal(a[k], b[k])
+
+
+def test_fit_root_split_equals_exact_greedy():
+    """Every feature here has <= 256 unique values, so histogram splits == exact greedy over all thresholds."""
+    X, c, key = _fit_data(400)
+    Xs = X[:, :120]                               # rows 0..5 of the context block
+    out = O.fit_hist(Xs, c, key, n_trees=1, depth=1)
+    G, H = O.pair_gradients(c, np.zeros(len(c), np.float32), key, seed=1805, tree=0)
+    G, H = G.astype(np.float64) / 2 ** 32, H.astype(np.float64) / 2 ** 32
+    lam = 1.0
+    best = (-1, None, 0.0)
+    for f in range(Xs.shape[1]):
+        vals = np.unique(Xs[:, f])
+        if len(vals) > 256:
+            pytest.skip("feature with > 256 unique values")
+        for th in vals[1:]:
+            left = Xs[:, f] < th
+            gl, hl, gr, hr = G[left].sum(), H[left].sum(), G[~left].sum(), H[~left].sum()
+            if hl < 1 or hr < 1:
+                continue
+            gain = gl * gl / (hl + lam) + gr * gr / (hr + lam) - G.sum() ** 2 / (H.sum() + lam)
+            if gain > best[2] * (1 + 1e-12) + 1e-300:
+                best = (f, th, gain)
+    assert out["feat"][0, 0] == best[0]
+    assert out["thresh"][0, 0] == best[1]
+    # leaves are -eta G / (H + lambda) of the two children
+    left = Xs[:, best[0]] < best[1]
+    for slot, m in ((0, left), (1, ~left)):
+        w = -0.1 * (G[m].sum() / (H[m].sum() + lam))
+        assert out["leaf"][0, slot] == pytest.approx(w, rel=1e-6)
+
+
+def test_fit_reduces_rank_loss():
+    X, c, key = _fit_data(400, seed=4, nw=1)
+    key = np.zeros_like(key)
+    out = O.fit_hist(X, c, key, n_trees=15, depth=4)
+    assert O.rank_loss(c, out["pred"]) < 0.9 * O.rank_loss(c, np.zeros(len(c), np.float32))
+    # the fit's own predictions equal re-scoring the training set with the ensemble (up to order)
+    e = O.OracleGbt(out["feat"], out["thresh"], out["leaf"])
+    assert np.allclose(e.predict(X), out["pred"], rtol=1e-5, atol=1e-6)
+
+
+def test_fit_cuts_rule():
+    """Q36: <= max_bins unique values -> cuts are the unique values but the minimum; else quantiles."""
+    g = np.random.default_rng(0)
+    X = np.stack([g.integers(0, 10, 1000), g.random(1000) * 100], axis=1).astype(np.float32)
+    cuts, nc = O.fit_cuts(X, 256)
+    assert nc[0] == 9 and list(cuts[0, :9]) == list(range(1, 10))
+    s = np.sort(X[:, 1])
+    q = [s[((b + 1) * 1000) // 256] for b in range(255)]
+    uq = [v for i, v in enumerate(q) if v != s[0] and (i == 0 or v != q[i - 1])]
+    assert list(cuts[1, :nc[1]]) == uq
