@@ -1,0 +1,252 @@
+// features.cuh -- knob decode + closed-form lowering + loop-context / relation features
+// for one candidate, as a device function shared by features_extract and sa_explore.
+//
+// Paper: x = g(e, s); loop context per loop (Appendix table): length,
+// one-hot annotation, top-down (product of outer lengths), bottom-up (this loop and
+// inner), per buffer touch count ("number of touched elements"), reuse ratio
+// (bottom-up / touch), stride (coefficient of the loop variable);
+// relation features R_t = max_{k : touch_b(k) < 2^t} Z_k,i.
+//
+// GPU design (differs from the oracle's literal enumeration): one pass from the
+// innermost loop outward keeps the active extent product A_a of every axis; then
+//   touch of a dimension indexed by one axis       = A_a
+//   touch of a dimension indexed by y*S + ry       = min(A_y A_ry, (A_y - 1) S + A_ry)
+// (the active levels of every split chain are a suffix of the nest, so each chain
+// covers a contiguous range), the stride of loop k is coef_k x rowstride where
+// coef_k = A_axis before loop k is folded in, and the relation max over the
+// qualifying loops {k : touch_b(k) < 2^t} -- an inner suffix, because touch only
+// grows outward -- is emitted for each t the moment the pass reaches the first loop
+// whose touch reaches 2^t.  All integers are u32 (space_create guarantees no overflow);
+// the float conversions and the reuse division are single IEEE RN operations.
+#pragma once
+#include "at_common.cuh"
+
+namespace at {
+
+// lexicographic permutations of 3 items: item at slot q of permutation p
+// (0,1,2) (0,2,1) (1,0,2) (1,2,0) (2,0,1) (2,1,0), packed 2 bits per slot
+__host__ __device__ __forceinline__ uint32_t perm3(uint32_t p, uint32_t q)
+{
+    const uint32_t t = (p == 0) ? 0x24u : (p == 1) ? 0x18u : (p == 2) ? 0x21u : (p == 3) ? 0x09u : (p == 4) ? 0x12u : 0x06u;
+    return (t >> (2 * q)) & 3u;
+}
+
+template <int TMPL> struct Tmpl;
+template <> struct Tmpl<0> { static constexpr int NK = 4, NL = 8, NA = 3; };
+template <> struct Tmpl<1> { static constexpr int NK = 9, NL = 18, NA = 6; };
+template <> struct Tmpl<2> { static constexpr int NK = 8, NL = 16, NA = 5; };
+
+__device__ __forceinline__ uint32_t comp_touch(uint32_t Y, uint32_t R, uint32_t S)
+{
+    uint32_t a = Y * R, b = (Y - 1u) * S + R;
+    return a < b ? a : b;
+}
+
+// decode local flat index (knob 0 fastest)
+template <int TMPL>
+__device__ __forceinline__ void decode_knobs(const WlDev &W, uint32_t local, uint32_t *ch)
+{
+#pragma unroll
+    for (int j = 0; j < Tmpl<TMPL>::NK; ++j) {
+        uint32_t r = W.radix[j];
+        uint32_t q = local / r;
+        ch[j] = local - q * r;
+        local = q;
+    }
+}
+
+// Compute all 468 features of the loop nest given by knob choices `ch`.
+// Sink: put(int f, float v) for every column (static f after unrolling except relation).
+template <int TMPL, class Sink>
+__device__ __forceinline__ void features_one(const WlDev &W, const uint16_t *__restrict__ fact,
+                                             const uint32_t *ch, Sink &sk)
+{
+    constexpr int NL = Tmpl<TMPL>::NL;
+    constexpr int NA = Tmpl<TMPL>::NA;
+    uint32_t ext[NL];
+    int axis_[NL];
+    int level_[NL];
+    uint32_t unroll_max, vec;
+    // ---- lowering (DESIGN Q3 templates): loop extents, axes, levels of the nest, outer -> inner
+    if (TMPL == 0) {
+        // i0 j0 k0 i1 j1 k1 i2 j2
+        uint32_t Fi[3], Fj[3], Fk[2];
+        const uint16_t *ti = fact + W.fact_off[0] + ch[0] * 3;
+        const uint16_t *tj = fact + W.fact_off[1] + ch[1] * 3;
+        const uint16_t *tk = fact + W.fact_off[2] + ch[2] * 2;
+#pragma unroll
+        for (int l = 0; l < 3; ++l) { Fi[l] = __ldg(ti + l); Fj[l] = __ldg(tj + l); }
+        Fk[0] = __ldg(tk); Fk[1] = __ldg(tk + 1);
+        const int ax[8] = {0, 1, 2, 0, 1, 2, 0, 1};
+        const int lv[8] = {0, 0, 0, 1, 1, 1, 2, 2};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            axis_[k] = ax[k];
+            level_[k] = lv[k];
+            ext[k] = ax[k] == 0 ? Fi[lv[k]] : ax[k] == 1 ? Fj[lv[k]] : Fk[lv[k]];
+        }
+        unroll_max = W.unroll_vals[ch[3]];
+        vec = 0;
+    } else {
+        constexpr int NSPLIT = (TMPL == 1) ? 6 : 5;
+        uint32_t F[NSPLIT][4];
+#pragma unroll
+        for (int a = 0; a < NSPLIT; ++a) {
+            const int L = (a < 3) ? 4 : 2;
+            const uint16_t *t = fact + W.fact_off[a] + ch[a] * L;
+#pragma unroll
+            for (int l = 0; l < 4; ++l) F[a][l] = (l < L) ? (uint32_t)__ldg(t + l) : 1u;
+        }
+        const uint32_t p = ch[NSPLIT];
+        unroll_max = W.unroll_vals[ch[NSPLIT + 1]];
+        vec = ch[NSPLIT + 2];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) { axis_[k] = k % 3; level_[k] = k / 3; }
+        if (TMPL == 1) {
+            // f0 y0 x0 f1 y1 x1 f2 y2 x2 | perm(rc0 ry0 rx0) | rc1 ry1 rx1 | f3 y3 x3
+#pragma unroll
+            for (int q = 0; q < 3; ++q) { axis_[9 + q] = 3 + (int)perm3(p, q); level_[9 + q] = 0; }
+#pragma unroll
+            for (int q = 0; q < 3; ++q) { axis_[12 + q] = 3 + q; level_[12 + q] = 1; }
+#pragma unroll
+            for (int q = 0; q < 3; ++q) { axis_[15 + q] = q; level_[15 + q] = 3; }
+        } else {
+            // c0 y0 x0 c1 y1 x1 c2 y2 x2 | ry0 rx0 ry1 rx1 | perm(c3 y3 x3)
+            axis_[9] = 3; level_[9] = 0; axis_[10] = 4; level_[10] = 0;
+            axis_[11] = 3; level_[11] = 1; axis_[12] = 4; level_[12] = 1;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) { axis_[13 + q] = (int)perm3(p, q); level_[13 + q] = 3; }
+        }
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            uint32_t e = 1;
+#pragma unroll
+            for (int a = 0; a < NSPLIT; ++a)
+#pragma unroll
+                for (int l = 0; l < 4; ++l)
+                    if (axis_[k] == a && level_[k] == l) e = F[a][l];
+            ext[k] = e;
+        }
+    }
+
+    // ---- top-down prefix products
+    uint32_t td[NL];
+    td[0] = 1;
+#pragma unroll
+    for (int k = 1; k < NL; ++k) td[k] = td[k - 1] * ext[k - 1];
+
+    // ---- inner -> outer pass
+    uint32_t A[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) A[a] = 1;
+    uint32_t bu = 1;
+    float smax_r[3], smax_t[3];
+    int tnext[3];
+    bool has[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) { smax_r[b] = 0.f; smax_t[b] = 0.f; tnext[b] = 1; has[b] = false; }
+    const uint32_t S = W.S;
+
+#pragma unroll
+    for (int k = NL - 1; k >= 0; --k) {
+        const int a = axis_[k];
+        uint32_t coef = 1;
+#pragma unroll
+        for (int q = 0; q < NA; ++q) if (a == q) coef = A[q];
+#pragma unroll
+        for (int q = 0; q < NA; ++q) if (a == q) A[q] *= ext[k];
+        bu *= ext[k];
+        uint32_t T[3];
+        uint32_t st[3];
+        if (TMPL == 0) {
+            T[0] = A[0] * A[1];                // C[i][j]
+            T[1] = A[2] * A[0];                // A[k][i]
+            T[2] = A[2] * A[1];                // B[k][j]
+            st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : 0u;
+            st[1] = (a == 2) ? coef * W.str_in[0] : (a == 0) ? coef * W.str_in[1] : 0u;
+            st[2] = (a == 2) ? coef * W.str_ker[0] : (a == 1) ? coef * W.str_ker[1] : 0u;
+        } else if (TMPL == 1) {
+            T[0] = A[0] * A[1] * A[2];                                             // Out[f][y][x]
+            T[1] = A[3] * comp_touch(A[1], A[4], S) * comp_touch(A[2], A[5], S);   // Data[rc][yS+ry][xS+rx]
+            T[2] = A[0] * A[3] * A[4] * A[5];                                      // Ker[f][rc][ry][rx]
+            st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : (a == 2) ? coef * W.str_out[2] : 0u;
+            st[1] = (a == 3) ? coef * W.str_in[0] : (a == 1) ? coef * S * W.str_in[1] : (a == 4) ? coef * W.str_in[1]
+                  : (a == 2) ? coef * S * W.str_in[2] : (a == 5) ? coef * W.str_in[2] : 0u;
+            st[2] = (a == 0) ? coef * W.str_ker[0] : (a == 3) ? coef * W.str_ker[1] : (a == 4) ? coef * W.str_ker[2]
+                  : (a == 5) ? coef * W.str_ker[3] : 0u;
+        } else {
+            T[0] = A[0] * A[1] * A[2];                                             // Out[c][y][x]
+            T[1] = A[0] * comp_touch(A[1], A[3], S) * comp_touch(A[2], A[4], S);   // Data[c][yS+ry][xS+rx]
+            T[2] = A[0] * A[3] * A[4];                                             // Ker[c][ry][rx]
+            st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : (a == 2) ? coef * W.str_out[2] : 0u;
+            st[1] = (a == 0) ? coef * W.str_in[0] : (a == 1) ? coef * S * W.str_in[1] : (a == 3) ? coef * W.str_in[1]
+                  : (a == 2) ? coef * S * W.str_in[2] : (a == 4) ? coef * W.str_in[2] : 0u;
+            st[2] = (a == 0) ? coef * W.str_ker[0] : (a == 3) ? coef * W.str_ker[1] : (a == 4) ? coef * W.str_ker[2] : 0u;
+        }
+        // annotation: 0 serial 1 unroll 2 vectorize 3 parallel 4 blockIdx 5 vthread 6 threadIdx
+        int ann;
+        if (TMPL != 0 && k < 9) {
+            ann = 4 + level_[k];
+        } else {
+            ann = (bu <= unroll_max) ? 1 : 0;
+            if (k == NL - 1 && vec) ann = 2;
+        }
+        const float fbu = __uint2float_rn(bu);
+        float reuse[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) reuse[b] = __fdiv_rn(fbu, __uint2float_rn(T[b]));
+        const float ftd = __uint2float_rn(td[k]);
+        // relation emission (before loop k joins the qualifying suffix)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            while (tnext[b] <= 20 && (T[b] >> tnext[b]) != 0u) {
+                sk.put_rel(342 + 40 * b + tnext[b] - 1, has[b] ? smax_r[b] : 0.f);
+                sk.put_rel(362 + 40 * b + tnext[b] - 1, has[b] ? smax_t[b] : 0.f);
+                ++tnext[b];
+            }
+            smax_r[b] = has[b] ? fmaxf(smax_r[b], reuse[b]) : reuse[b];
+            smax_t[b] = has[b] ? fmaxf(smax_t[b], ftd) : ftd;
+            has[b] = true;
+        }
+        // the 19 context columns of row k
+        const int base = 19 * k;
+        sk.put(base + 0, __uint2float_rn(ext[k]));
+#pragma unroll
+        for (int q = 0; q < 7; ++q) sk.put(base + 1 + q, ann == q ? 1.0f : 0.0f);
+        sk.put(base + 8, ftd);
+        sk.put(base + 9, fbu);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            sk.put(base + 10 + 3 * b, __uint2float_rn(T[b]));
+            sk.put(base + 11 + 3 * b, reuse[b]);
+            sk.put(base + 12 + 3 * b, __uint2float_rn(st[b]));
+        }
+        if (k == 0) {
+            // scalars: total iterations and footprints touch(b, 0)
+            sk.put(462, fbu);
+#pragma unroll
+            for (int b = 0; b < 3; ++b) sk.put(463 + b, __uint2float_rn(T[b]));
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        while (tnext[b] <= 20) {
+            sk.put_rel(342 + 40 * b + tnext[b] - 1, smax_r[b]);
+            sk.put_rel(362 + 40 * b + tnext[b] - 1, smax_t[b]);
+            ++tnext[b];
+        }
+    }
+}
+
+// columns that are zero for every candidate of a template (absent loop rows + padding)
+template <int TMPL, class Sink>
+__device__ __forceinline__ void features_zero_cols(Sink &sk)
+{
+    constexpr int NL = Tmpl<TMPL>::NL;
+#pragma unroll 4
+    for (int f = 19 * NL; f < 342; ++f) sk.put(f, 0.0f);
+    sk.put(466, 0.0f);
+    sk.put(467, 0.0f);
+}
+
+}  // namespace at

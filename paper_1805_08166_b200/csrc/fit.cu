@@ -1,0 +1,667 @@
+// fit.cu -- gbt_fit_hist: histogram GBT refit under the pairwise rank loss
+// (Alg. 1 P:163 "update f-hat using D"; Eq. 2; readings Q16, Q17, Q34-Q37).
+//
+// Pipeline (all on `stream`, one process per GPU, histograms summed across ranks by
+// the caller's all-reduce between levels):
+//   1. cuts: per feature an LSD radix sort (4 x 8-bit passes, one block per feature,
+//      stable warp-match ranking) of the order-preserving u32 keys, then the unique
+//      values (<= max_bins) or the max_bins-quantile order statistics;  bins u8 [F][n].
+//   2. per-workload dense ranks and group tables (once per fit).
+//   3. per tree: Feistel/Philox positions -> group members; one block per group of
+//      <= 64 computes both orders of every pair's Eq. 2 gradient / curvature, quantised
+//      to int64 2^-32 fixed point (order-free sums -> bit-identical at any rank count);
+//      per level: int64 histograms [node][F][bins] of the rank's sample slice
+//      (shared-memory atomics, one block per feature), all-reduce, fp64 split search
+//      (one block per node), partition of every sample; leaves -eta G / (H + lambda);
+//      fp32 prediction update in tree order.
+#include <cmath>
+#include <vector>
+
+#include "at_common.cuh"
+
+namespace at {
+
+constexpr int FIT_MAXKEYS = 1024;
+constexpr double FX = 1.0 / 4294967296.0;   // 2^-32
+
+// ------------------------------------------------------------------ 1. cuts
+__global__ void __launch_bounds__(1024) sort_feature_kernel(const float *__restrict__ X, int64_t ld, int64_t n,
+                                                            uint32_t *__restrict__ bufA, uint32_t *__restrict__ bufB)
+{
+    __shared__ uint32_t wcount[32][257];
+    __shared__ uint32_t base[256];
+    __shared__ uint32_t tile_total[256];
+    const int f = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t *src = bufA + (int64_t)f * n, *dst = bufB + (int64_t)f * n;
+    for (int64_t i = tid; i < n; i += 1024) src[i] = fkey(X[(int64_t)f * ld + i]);
+    __syncthreads();
+    for (int pass = 0; pass < 4; ++pass) {
+        const int sh = 8 * pass;
+        if (tid < 256) base[tid] = 0;
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += 1024) atomicAdd(&base[(src[i] >> sh) & 255u], 1u);
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t run = 0;
+            for (int d = 0; d < 256; ++d) { const uint32_t c = base[d]; base[d] = run; run += c; }
+        }
+        __syncthreads();
+        for (int64_t t0 = 0; t0 < n; t0 += 1024) {
+            for (int q = tid; q < 32 * 257; q += 1024) (&wcount[0][0])[q] = 0;
+            __syncthreads();
+            const int64_t i = t0 + tid;
+            const bool ok = i < n;
+            const uint32_t key = ok ? src[i] : 0u;
+            const uint32_t dg = ok ? ((key >> sh) & 255u) : 256u;
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dg);
+            const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+            if (ok && rank == 0) wcount[warp][dg] = __popc(peers);
+            __syncthreads();
+            if (tid < 256) {
+                uint32_t run = 0;
+                for (int w = 0; w < 32; ++w) { const uint32_t c = wcount[w][tid]; wcount[w][tid] = run; run += c; }
+                tile_total[tid] = run;
+            }
+            __syncthreads();
+            if (ok) dst[base[dg] + wcount[warp][dg] + rank] = key;
+            __syncthreads();
+            if (tid < 256) base[tid] += tile_total[tid];
+            __syncthreads();
+        }
+        uint32_t *t = src; src = dst; dst = t;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) cuts_kernel(const uint32_t *__restrict__ sorted, int64_t n, int B,
+                                                    float *__restrict__ cuts, int32_t *__restrict__ ncuts)
+{
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t s_run;
+    __shared__ int64_t s_U;
+    const int f = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t *k = sorted + (int64_t)f * n;
+    float *c = cuts + (int64_t)f * (B - 1);
+    // number of unique values U
+    int64_t cnt = 0;
+    for (int64_t i = tid; i < n; i += 1024) cnt += (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
+    if (lane == 0) wsum[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        int64_t U = 0;
+        for (int w = 0; w < 32; ++w) U += wsum[w];
+        s_U = U;
+        s_run = 0;
+    }
+    __syncthreads();
+    const int64_t U = s_U;
+    if (U <= B) {
+        // cuts = u_2 .. u_U: the unique values in order, without the minimum
+        for (int64_t t0 = 0; t0 < n; t0 += 1024) {
+            const int64_t i = t0 + tid;
+            const int flag = (i < n && (i == 0 || k[i] != k[i - 1])) ? 1 : 0;
+            int incl = flag;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            __syncthreads();
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            if (tid == 0) {
+                int64_t r = 0;
+                for (int w = 0; w < 32; ++w) { const int64_t x = wsum[w]; wsum[w] = r; r += x; }
+            }
+            __syncthreads();
+            const int64_t before = s_run + wsum[warp] + incl - flag;   // uniques in [0, i)
+            if (flag && i > 0) c[before - 1] = fkey_inv(k[i]);
+            __syncthreads();
+            if (tid == 1023) s_run = before + flag;
+            __syncthreads();
+        }
+        if (tid == 0) ncuts[f] = (int32_t)(U - 1);
+    } else if (tid == 0) {
+        int nc = 0;
+        for (int q = 0; q < B - 1; ++q) {
+            const uint32_t v = k[((int64_t)(q + 1) * n) / B];
+            if (v == k[0]) continue;
+            if (nc > 0 && fkey(c[nc - 1]) == v) continue;
+            c[nc++] = fkey_inv(v);
+        }
+        ncuts[f] = nc;
+    }
+}
+
+__global__ void bins_kernel(const float *__restrict__ X, int64_t ld, int64_t n, int F, int B,
+                            const float *__restrict__ cuts, const int32_t *__restrict__ ncuts,
+                            uint8_t *__restrict__ bins)
+{
+    const int f = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float x = X[(int64_t)f * ld + i];
+    const float *c = cuts + (int64_t)f * (B - 1);
+    int lo = 0, hi = ncuts[f];   // upper_bound: number of cuts <= x
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (c[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    bins[(int64_t)f * n + i] = (uint8_t)lo;
+}
+
+// ------------------------------------------------------------------ 2. groups
+__global__ void __launch_bounds__(1024) ranks_kernel(const uint16_t *__restrict__ key, int64_t n,
+                                                     int32_t *__restrict__ rank, int32_t *__restrict__ counts,
+                                                     int32_t *__restrict__ woff, int32_t *__restrict__ gprefix,
+                                                     int group_size)
+{
+    __shared__ int32_t cnt[FIT_MAXKEYS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int k = tid; k < FIT_MAXKEYS; k += 1024) cnt[k] = 0;
+    __syncthreads();
+    for (int64_t t0 = 0; t0 < n; t0 += 1024) {
+        const int64_t i = t0 + tid;
+        const bool ok = i < n;
+        const uint32_t k = ok ? (uint32_t)key[i] : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, k);
+        const int r = __popc(peers & ((1u << lane) - 1u));
+        for (int w = 0; w < 32; ++w) {
+            if (warp == w && ok) {
+                rank[i] = cnt[k] + r;
+                __syncwarp(peers);
+                if (r == 0) cnt[k] += __popc(peers);
+            }
+            __syncthreads();
+        }
+    }
+    if (tid == 0) {
+        int32_t o = 0, g = 0;
+        for (int k = 0; k < FIT_MAXKEYS; ++k) {
+            counts[k] = cnt[k];
+            woff[k] = o;
+            gprefix[k] = g;
+            o += cnt[k];
+            g += (cnt[k] + group_size - 1) / group_size;
+        }
+        gprefix[FIT_MAXKEYS] = g;
+    }
+}
+
+__device__ __forceinline__ uint32_t feistel(uint32_t x, int h, uint64_t seed, uint32_t tree, uint32_t wkey)
+{
+    const uint32_t mask = (1u << h) - 1u;
+    uint32_t L = x >> h, R = x & mask;
+#pragma unroll
+    for (uint32_t r = 0; r < 4; ++r) {
+        const U4 o = philox(seed, R, tree, (wkey << 2) | r, TAG_GROUP_PERM);
+        const uint32_t nL = R, nR = L ^ (o.x & mask);
+        L = nL;
+        R = nR;
+    }
+    return (L << h) | R;
+}
+
+__global__ void positions_kernel(const uint16_t *__restrict__ key, const int32_t *__restrict__ rank,
+                                 const int32_t *__restrict__ counts, const int32_t *__restrict__ woff, int64_t n,
+                                 uint64_t seed, uint32_t tree, int32_t *__restrict__ member)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = key[i];
+    const uint32_t nw = (uint32_t)counts[k];
+    int bits = 0;
+    while ((1ull << bits) < nw) ++bits;
+    int h = (bits + 1) / 2;
+    if (h < 1) h = 1;
+    uint32_t y = feistel((uint32_t)rank[i], h, seed, tree, k);
+    while (y >= nw) y = feistel(y, h, seed, tree, k);
+    member[woff[k] + y] = (int32_t)i;
+}
+
+__global__ void __launch_bounds__(256) grads_kernel(const int32_t *__restrict__ member,
+                                                    const int32_t *__restrict__ counts,
+                                                    const int32_t *__restrict__ woff,
+                                                    const int32_t *__restrict__ gprefix, int group_size,
+                                                    const float *__restrict__ cost, const float *__restrict__ pred,
+                                                    int64_t *__restrict__ g, int64_t *__restrict__ h)
+{
+    extern __shared__ unsigned char smraw[];
+    int64_t *sg = (int64_t *)smraw;
+    int64_t *sh = sg + group_size;
+    float *sc = (float *)(sh + group_size);
+    float *sp = sc + group_size;
+    int32_t *si = (int32_t *)(sp + group_size);
+    __shared__ int s_w;
+    const int b = blockIdx.x;
+    if (b >= gprefix[FIT_MAXKEYS]) return;
+    if (threadIdx.x == 0) {
+        int lo = 0, hi = FIT_MAXKEYS;   // largest w with gprefix[w] <= b
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (gprefix[mid] <= b) lo = mid; else hi = mid;
+        }
+        while (lo + 1 <= FIT_MAXKEYS && gprefix[lo + 1] <= b) ++lo;
+        s_w = lo;
+    }
+    __syncthreads();
+    const int w = s_w;
+    const int gi = b - gprefix[w];
+    const int start = gi * group_size;
+    int m = counts[w] - start;
+    if (m > group_size) m = group_size;
+    for (int a = threadIdx.x; a < m; a += blockDim.x) {
+        const int i = member[woff[w] + start + a];
+        si[a] = i;
+        sc[a] = cost[i];
+        sp[a] = pred[i];
+        sg[a] = 0;
+        sh[a] = 0;
+    }
+    __syncthreads();
+    const int npairs = m * (m - 1) / 2;
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        // unordered pair (a, c), a < c, from the linear pair index
+        int a = 0, rem = p;
+        while (rem >= m - 1 - a) { rem -= m - 1 - a; ++a; }
+        int c = a + 1 + rem;
+        if (sc[a] == sc[c]) continue;                 // sign(c_i - c_j) = 0
+        if (sc[a] < sc[c]) { const int t = a; a = c; c = t; }   // now cost[a] > cost[c]
+        const float d = __fsub_rn(sp[c], sp[a]);
+        const float e = exp_det(-d);
+        const float rho = __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
+        const float hh = __fmul_rn(rho, __fsub_rn(1.0f, rho));
+        const long long q = __double2ll_rn((double)rho * 4294967296.0);
+        const long long qh = __double2ll_rn((double)hh * 4294967296.0);
+        atomicAdd((unsigned long long *)&sg[a], (unsigned long long)(-2 * q));
+        atomicAdd((unsigned long long *)&sg[c], (unsigned long long)(2 * q));
+        atomicAdd((unsigned long long *)&sh[a], (unsigned long long)(2 * qh));
+        atomicAdd((unsigned long long *)&sh[c], (unsigned long long)(2 * qh));
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < m; a += blockDim.x) {
+        g[si[a]] = sg[a];
+        h[si[a]] = sh[a];
+    }
+}
+
+// ------------------------------------------------------------------ 3. levels
+template <bool SMEM>
+__global__ void __launch_bounds__(512) hist_kernel(const uint8_t *__restrict__ bins, const int32_t *__restrict__ node,
+                                                   const int64_t *__restrict__ g, const int64_t *__restrict__ h,
+                                                   int64_t hb, int64_t he, int64_t n, int F, int B, int first, int nn,
+                                                   int64_t *__restrict__ hist)
+{
+    extern __shared__ unsigned long long shist[];
+    const int f = blockIdx.x;
+    const int64_t cells = (int64_t)nn * B * 2;
+    if (SMEM) {
+        for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) shist[q] = 0ull;
+        __syncthreads();
+    }
+    const uint8_t *bf = bins + (int64_t)f * n;
+    for (int64_t i = hb + threadIdx.x; i < he; i += blockDim.x) {
+        const int nd = node[i] - first;
+        const int b = bf[i];
+        const unsigned long long gv = (unsigned long long)g[i], hv = (unsigned long long)h[i];
+        if (SMEM) {
+            atomicAdd(&shist[((int64_t)nd * B + b) * 2], gv);
+            atomicAdd(&shist[((int64_t)nd * B + b) * 2 + 1], hv);
+        } else {
+            int64_t *cell = hist + (((int64_t)nd * F + f) * B + b) * 2;
+            atomicAdd((unsigned long long *)cell, gv);
+            atomicAdd((unsigned long long *)cell + 1, hv);
+        }
+    }
+    if (SMEM) {
+        __syncthreads();
+        for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) {
+            const int64_t nd = q / (2 * B), rem = q - nd * 2 * B;
+            hist[(nd * F + f) * B * 2 + rem] = (int64_t)shist[q];
+        }
+    }
+}
+
+struct SplitBest {
+    double gain;
+    int f, s;
+};
+
+__device__ __forceinline__ bool split_better(const SplitBest &a, const SplitBest &b)
+{
+    if (a.f < 0) return false;
+    if (b.f < 0) return true;
+    if (a.gain != b.gain) return a.gain > b.gain;
+    return a.f < b.f;
+}
+
+__global__ void __launch_bounds__(256) split_kernel(const int64_t *__restrict__ hist, int F, int B, int first,
+                                                    const float *__restrict__ cuts, const int32_t *__restrict__ ncuts,
+                                                    double lam, double mcw, uint8_t *__restrict__ dead,
+                                                    int32_t *__restrict__ split_f, int32_t *__restrict__ split_s,
+                                                    uint16_t *__restrict__ tree_feat, float *__restrict__ tree_thr)
+{
+    __shared__ long long s_sum[2][8];
+    __shared__ SplitBest s_best[8];
+    const int q = blockIdx.x, nd = first + q;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (dead[nd]) {
+        if (tid == 0) {
+            tree_feat[nd] = 0;
+            tree_thr[nd] = __int_as_float(0x7f800000);
+            split_f[nd] = -1;
+            dead[2 * nd + 1] = 1;
+            dead[2 * nd + 2] = 1;
+        }
+        return;
+    }
+    const int64_t *hn = hist + (int64_t)q * F * B * 2;
+    // node totals from feature 0 (every sample sits in exactly one of its bins)
+    long long G0 = 0, H0 = 0;
+    for (int b = tid; b < B; b += 256) { G0 += hn[2 * b]; H0 += hn[2 * b + 1]; }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        G0 += __shfl_xor_sync(0xFFFFFFFFu, G0, off);
+        H0 += __shfl_xor_sync(0xFFFFFFFFu, H0, off);
+    }
+    if (lane == 0) { s_sum[0][warp] = G0; s_sum[1][warp] = H0; }
+    __syncthreads();
+    long long Gi = 0, Hi = 0;
+    for (int w = 0; w < 8; ++w) { Gi += s_sum[0][w]; Hi += s_sum[1][w]; }
+    const double G = (double)Gi * FX, H = (double)Hi * FX;
+    const double parent = G * G / (H + lam);
+    SplitBest best{0.0, -1, 0};
+    for (int f = tid; f < F; f += 256) {
+        const int64_t *hf = hn + (int64_t)f * B * 2;
+        const int nc = ncuts[f];
+        long long GLi = 0, HLi = 0;
+        for (int s = 1; s <= nc; ++s) {
+            GLi += hf[2 * (s - 1)];
+            HLi += hf[2 * (s - 1) + 1];
+            const double GL = (double)GLi * FX, HL = (double)HLi * FX;
+            const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
+            if (HL < mcw || HR < mcw) continue;
+            const double gain = (GL * GL / (HL + lam) + GR * GR / (HR + lam)) - parent;
+            if (!(gain > 0.0)) continue;
+            if (best.f < 0 || gain > best.gain) { best.gain = gain; best.f = f; best.s = s; }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        SplitBest o;
+        o.gain = __shfl_xor_sync(0xFFFFFFFFu, best.gain, off);
+        o.f = __shfl_xor_sync(0xFFFFFFFFu, best.f, off);
+        o.s = __shfl_xor_sync(0xFFFFFFFFu, best.s, off);
+        if (split_better(o, best)) best = o;
+    }
+    if (lane == 0) s_best[warp] = best;
+    __syncthreads();
+    if (tid == 0) {
+        SplitBest b = s_best[0];
+        for (int w = 1; w < 8; ++w)
+            if (split_better(s_best[w], b)) b = s_best[w];
+        if (b.f < 0) {
+            tree_feat[nd] = 0;
+            tree_thr[nd] = __int_as_float(0x7f800000);
+            split_f[nd] = -1;
+            dead[2 * nd + 1] = 1;
+            dead[2 * nd + 2] = 1;
+        } else {
+            tree_feat[nd] = (uint16_t)b.f;
+            tree_thr[nd] = cuts[(int64_t)b.f * (B - 1) + b.s - 1];
+            split_f[nd] = b.f;
+            split_s[nd] = b.s;
+        }
+    }
+}
+
+__global__ void partition_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ split_f,
+                                 const int32_t *__restrict__ split_s, int32_t *__restrict__ node)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nd = node[i];
+    const int sf = split_f[nd];
+    int child = 2 * nd + 1;
+    if (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= split_s[nd]) child = 2 * nd + 2;
+    node[i] = child;
+}
+
+__global__ void leafsum_kernel(const int32_t *__restrict__ node, const int64_t *__restrict__ g,
+                               const int64_t *__restrict__ h, int64_t hb, int64_t he, int n_int,
+                               int64_t *__restrict__ sums)
+{
+    const int64_t i = hb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= he) return;
+    const int l = node[i] - n_int;
+    atomicAdd((unsigned long long *)&sums[2 * l], (unsigned long long)g[i]);
+    atomicAdd((unsigned long long *)&sums[2 * l + 1], (unsigned long long)h[i]);
+}
+
+__global__ void leaf_kernel(const int64_t *__restrict__ sums, int n_leaf, double eta, double lam,
+                            float *__restrict__ leaf)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= n_leaf) return;
+    const double G = (double)sums[2 * l] * FX, H = (double)sums[2 * l + 1] * FX;
+    leaf[l] = (float)(-(eta * (G / (H + lam))));
+}
+
+__global__ void pred_update_kernel(const int32_t *__restrict__ node, int64_t n, int n_int,
+                                   const float *__restrict__ leaf, float *__restrict__ pred)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    pred[i] = __fadd_rn(pred[i], leaf[node[i] - n_int]);
+}
+
+__global__ void pack_nodes_kernel(const uint16_t *__restrict__ feat, const float *__restrict__ thr, int64_t m,
+                                  uint2 *__restrict__ nodes)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    nodes[i] = make_uint2(feat[i], __float_as_uint(thr[i]));
+}
+
+__global__ void finite_check_kernel(const float *__restrict__ c, int64_t n, int *__restrict__ bad)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && !isfinite(c[i])) *bad = 1;
+}
+
+__global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int *__restrict__ bad)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && k[i] >= FIT_MAXKEYS) *bad = 2;
+}
+
+}  // namespace at
+
+namespace {
+
+struct Ws {
+    cudaStream_t s;
+    std::vector<void *> ptrs;
+    int err = 0;
+    template <class T> T *get(size_t count)
+    {
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, count * sizeof(T) + 16, s) != cudaSuccess) {
+            cudaGetLastError();
+            err = AT_ENOMEM;
+            return nullptr;
+        }
+        ptrs.push_back(p);
+        return (T *)p;
+    }
+    ~Ws()
+    {
+        for (void *p : ptrs) cudaFreeAsync(p, s);
+    }
+};
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t F, const float *d_cost,
+                            const uint16_t *d_group_key, int64_t hb, int64_t he, const at_fit_opts *o, at_gbt *out,
+                            void *stream)
+{
+    using namespace at;
+    if (!o || !out) return fail(AT_EINVAL, "gbt_fit_hist: null options/output");
+    if (n == 0) return fail(AT_EEMPTY, "gbt_fit_hist: empty training set");
+    if (n < 0 || n > 0x7FFFFFFF) return fail(AT_EINVAL, "gbt_fit_hist: bad n");
+    if (!d_feat || !d_cost || !d_group_key) return fail(AT_EINVAL, "gbt_fit_hist: null buffer");
+    if (ld < n || F < 1 || F > 65535) return fail(AT_EMISMATCH, "gbt_fit_hist: bad ld / n_features");
+    if (o->depth < 1 || o->depth > 8) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: depth must be in [1, 8]");
+    if (o->max_bins < 2 || o->max_bins > 256) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: max_bins must be in [2, 256]");
+    if (o->n_trees < 1 || o->group_size < 2 || o->group_size > 1024) return fail(AT_EINVAL, "gbt_fit_hist: bad n_trees / group_size");
+    if (hb < 0 || he < hb || he > n) return fail(AT_EINVAL, "gbt_fit_hist: bad histogram slice");
+    if (!o->allreduce && (hb != 0 || he != n)) return fail(AT_EINVAL, "gbt_fit_hist: a slice needs an allreduce");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int D = o->depth, B = o->max_bins, GS = o->group_size;
+    const int n_int = (1 << D) - 1, n_leaf = 1 << D;
+    const double lam = (double)o->lambda, mcw = (double)o->min_child_weight, eta = (double)o->eta;
+
+    Ws ws;
+    ws.s = s;
+    int *d_bad = ws.get<int>(1);
+    uint32_t *sortA = ws.get<uint32_t>((size_t)F * n);
+    uint32_t *sortB = ws.get<uint32_t>((size_t)F * n);
+    float *cuts = ws.get<float>((size_t)F * (B - 1));
+    int32_t *ncuts = ws.get<int32_t>(F);
+    uint8_t *bins = ws.get<uint8_t>((size_t)F * n);
+    int32_t *rank = ws.get<int32_t>(n);
+    int32_t *counts = ws.get<int32_t>(FIT_MAXKEYS);
+    int32_t *woff = ws.get<int32_t>(FIT_MAXKEYS);
+    int32_t *gpre = ws.get<int32_t>(FIT_MAXKEYS + 1);
+    int32_t *member = ws.get<int32_t>(n);
+    int64_t *g = ws.get<int64_t>(n);
+    int64_t *h = ws.get<int64_t>(n);
+    float *pred = ws.get<float>(n);
+    int32_t *node = ws.get<int32_t>(n);
+    const int max_nn = 1 << (D - 1);
+    int64_t *hist = ws.get<int64_t>((size_t)max_nn * F * B * 2);
+    int64_t *lsum = ws.get<int64_t>((size_t)n_leaf * 2);
+    uint8_t *dead = ws.get<uint8_t>(n_int + n_leaf);
+    int32_t *split_f = ws.get<int32_t>(n_int);
+    int32_t *split_s = ws.get<int32_t>(n_int);
+    uint16_t *t_feat = ws.get<uint16_t>((size_t)o->n_trees * n_int);
+    float *t_thr = ws.get<float>((size_t)o->n_trees * n_int);
+    float *t_leaf = ws.get<float>((size_t)o->n_trees * n_leaf);
+    if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+
+    // input checks (one sync): finite costs, group keys < 1024
+    {
+        int bad = 0;
+        AT_CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+        finite_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, n, d_bad);
+        key_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, n, d_bad);
+        AT_LAUNCH_CHECK("fit input checks");
+        AT_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AT_CUDA_TRY(cudaStreamSynchronize(s));
+        if (bad == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
+        if (bad == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
+    }
+    {
+        ProfScope ps(AT_K_FIT_PREP, s);
+        sort_feature_kernel<<<F, 1024, 0, s>>>(d_feat, ld, n, sortA, sortB);
+        cuts_kernel<<<F, 1024, 0, s>>>(sortA, n, B, cuts, ncuts);
+        bins_kernel<<<dim3(nblk(n, 256), F), 256, 0, s>>>(d_feat, ld, n, F, B, cuts, ncuts, bins);
+        ranks_kernel<<<1, 1024, 0, s>>>(d_group_key, n, rank, counts, woff, gpre, GS);
+        AT_CUDA_TRY(cudaMemsetAsync(pred, 0, sizeof(float) * n, s));
+        AT_LAUNCH_CHECK("fit prep");
+    }
+    const size_t grad_smem = (size_t)GS * (2 * sizeof(int64_t) + 2 * sizeof(float) + sizeof(int32_t));
+    const unsigned grad_blocks = nblk(n, GS) + FIT_MAXKEYS;
+    static size_t hist_attr = 0;
+    for (int t = 0; t < o->n_trees; ++t) {
+        {
+            ProfScope ps(AT_K_FIT_GRAD, s);
+            positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, (uint32_t)t,
+                                                          member);
+            grads_kernel<<<grad_blocks, 256, grad_smem, s>>>(member, counts, woff, gpre, GS, d_cost, pred, g, h);
+            AT_LAUNCH_CHECK("fit gradients");
+        }
+        AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
+        AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
+        uint16_t *tf = t_feat + (size_t)t * n_int;
+        float *tt = t_thr + (size_t)t * n_int;
+        for (int d = 0; d < D; ++d) {
+            const int first = (1 << d) - 1, nn = 1 << d;
+            const size_t cells = (size_t)nn * B * 2;
+            const size_t smem = cells * sizeof(int64_t);
+            {
+                ProfScope ps(AT_K_FIT_HIST, s);
+                if (smem <= 160 * 1024) {
+                    if (smem > hist_attr) {
+                        AT_CUDA_TRY(cudaFuncSetAttribute(hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         160 * 1024));
+                        hist_attr = 160 * 1024;
+                    }
+                    hist_kernel<true><<<F, 512, smem, s>>>(bins, node, g, h, hb, he, n, F, B, first, nn, hist);
+                } else {
+                    AT_CUDA_TRY(cudaMemsetAsync(hist, 0, cells * F * sizeof(int64_t), s));
+                    hist_kernel<false><<<F, 512, 0, s>>>(bins, node, g, h, hb, he, n, F, B, first, nn, hist);
+                }
+                AT_LAUNCH_CHECK("hist_kernel");
+            }
+            if (o->allreduce) {
+                const int rc = o->allreduce(hist, (int64_t)(cells * F), o->ctx, stream);
+                if (rc) return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
+            }
+            if (t == 0 && d == 0 && o->d_hist0_out)
+                AT_CUDA_TRY(cudaMemcpyAsync(o->d_hist0_out, hist, (size_t)F * B * 2 * sizeof(int64_t),
+                                            cudaMemcpyDeviceToDevice, s));
+            {
+                ProfScope ps(AT_K_FIT_SPLIT, s);
+                split_kernel<<<nn, 256, 0, s>>>(hist, F, B, first, cuts, ncuts, lam, mcw, dead, split_f, split_s, tf, tt);
+                partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
+                AT_LAUNCH_CHECK("split/partition");
+            }
+        }
+        {
+            ProfScope ps(AT_K_FIT_UPDATE, s);
+            AT_CUDA_TRY(cudaMemsetAsync(lsum, 0, sizeof(int64_t) * 2 * n_leaf, s));
+            if (he > hb) leafsum_kernel<<<nblk(he - hb, 256), 256, 0, s>>>(node, g, h, hb, he, n_int, lsum);
+            AT_LAUNCH_CHECK("leafsum");
+        }
+        if (o->allreduce) {
+            const int rc = o->allreduce(lsum, (int64_t)2 * n_leaf, o->ctx, stream);
+            if (rc) return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
+        }
+        {
+            ProfScope ps(AT_K_FIT_UPDATE, s);
+            float *tl = t_leaf + (size_t)t * n_leaf;
+            leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(lsum, n_leaf, eta, lam, tl);
+            pred_update_kernel<<<nblk(n, 256), 256, 0, s>>>(node, n, n_int, tl, pred);
+            AT_LAUNCH_CHECK("leaf/pred update");
+        }
+    }
+    // the fitted ensemble handle
+    at_gbt gm = new at_gbt_s();
+    gm->n_trees = o->n_trees;
+    gm->depth = D;
+    gm->n_features = F;
+    gm->base = 0.0f;
+    if (cudaMalloc(&gm->d_nodes, sizeof(uint2) * (size_t)o->n_trees * n_int) != cudaSuccess ||
+        cudaMalloc(&gm->d_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(gm->d_nodes);
+        delete gm;
+        return fail(AT_ENOMEM, "gbt_fit_hist: model allocation failed");
+    }
+    pack_nodes_kernel<<<nblk((int64_t)o->n_trees * n_int, 256), 256, 0, s>>>(t_feat, t_thr, (int64_t)o->n_trees * n_int,
+                                                                             gm->d_nodes);
+    AT_CUDA_TRY(cudaMemcpyAsync(gm->d_leaf, t_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf,
+                                cudaMemcpyDeviceToDevice, s));
+    if (o->d_pred_out) AT_CUDA_TRY(cudaMemcpyAsync(o->d_pred_out, pred, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+    AT_LAUNCH_CHECK("fit finish");
+    *out = gm;
+    return AT_OK;
+}

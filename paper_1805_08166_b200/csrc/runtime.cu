@@ -1,0 +1,126 @@
+// runtime.cu -- error state, launch accounting / event profiling, scratch memory.
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "at_common.cuh"
+
+namespace at {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where)
+{
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return AT_ECUDA;
+}
+
+// ---------------------------------------------------------------- profiling
+static std::atomic<int64_t> g_launches{0};
+static std::atomic<int> g_prof_on{0};
+static std::mutex g_prof_mu;
+struct EvPair { cudaEvent_t a, b; };
+static std::vector<EvPair> g_ev[AT_K_NCLASSES];
+static std::vector<EvPair> g_pool;
+static cudaEvent_t g_open[AT_K_NCLASSES];
+
+static cudaEvent_t take_event()
+{
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(int cls, cudaStream_t s)
+{
+    g_launches.fetch_add(1);
+    if (!g_prof_on.load()) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t e;
+    if (!g_pool.empty()) { e = g_pool.back().a; g_pool.pop_back(); } else e = take_event();
+    cudaEventRecord(e, s);
+    g_open[cls] = e;
+}
+
+void prof_end(int cls, cudaStream_t s)
+{
+    if (!g_prof_on.load()) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t e;
+    if (!g_pool.empty()) { e = g_pool.back().a; g_pool.pop_back(); } else e = take_event();
+    cudaEventRecord(e, s);
+    g_ev[cls].push_back(EvPair{g_open[cls], e});
+}
+
+int scratch_reserve(at_space sp, size_t bytes, cudaStream_t s)
+{
+    if (sp->scratch_bytes >= bytes) return AT_OK;
+    if (sp->d_scratch) {
+        AT_CUDA_TRY(cudaStreamSynchronize(s));
+        cudaFree(sp->d_scratch);
+        sp->d_scratch = nullptr;
+        sp->scratch_bytes = 0;
+    }
+    size_t want = bytes + bytes / 4;
+    if (cudaMalloc(&sp->d_scratch, want) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(AT_ENOMEM, "scratch allocation of " + std::to_string(want) + " bytes failed");
+    }
+    sp->scratch_bytes = want;
+    return AT_OK;
+}
+
+}  // namespace at
+
+extern "C" {
+
+const char *at_last_error(void) { return at::g_err.c_str(); }
+
+int64_t at_launch_count(void) { return at::g_launches.load(); }
+
+int at_prof_enable(int on)
+{
+    at::g_prof_on.store(on ? 1 : 0);
+    return AT_OK;
+}
+
+int at_prof_reset(void)
+{
+    std::lock_guard<std::mutex> lk(at::g_prof_mu);
+    for (int c = 0; c < AT_K_NCLASSES; ++c) {
+        for (auto &p : at::g_ev[c]) {
+            cudaEventSynchronize(p.b);
+            at::g_pool.push_back(at::EvPair{p.a, nullptr});
+            at::g_pool.push_back(at::EvPair{p.b, nullptr});
+        }
+        at::g_ev[c].clear();
+    }
+    return AT_OK;
+}
+
+int at_prof_query(int32_t cls, int64_t *launches, double *total_ms)
+{
+    if (cls < 0 || cls >= AT_K_NCLASSES) return at::fail(AT_EINVAL, "at_prof_query: bad kernel class");
+    std::lock_guard<std::mutex> lk(at::g_prof_mu);
+    double tot = 0.0;
+    for (auto &p : at::g_ev[cls]) {
+        cudaError_t e = cudaEventSynchronize(p.b);
+        if (e != cudaSuccess) return at::cuda_fail(e, "at_prof_query");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        tot += ms;
+    }
+    if (launches) *launches = (int64_t)at::g_ev[cls].size();
+    if (total_ms) *total_ms = tot;
+    return AT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,281 @@
+// sa.cu -- sa_explore: fused proposal -> features -> GBT -> Metropolis over many chains
+// (Alg. 1 P:152-153 "run parallel simulated annealing ... using energy function f-hat";
+// P:187 "a batch of parallel Markov chains", persistent states; readings Q20-Q23, Q28).
+//
+// Block = 32 chains (lane = chain) x SA_NW warps.  Per step, warp 0 draws the
+// Philox proposal of each chain, applies the single-knob move to the chain's knob
+// vector (kept in registers: no decode after the start state) and writes the
+// proposal's 468 features into the block's shared tile [468][32]; then all SA_NW
+// warps walk the ensemble (each a residue class of trees, gbt.cuh) and warp 0 folds
+// the partials in the canonical order, takes the Metropolis decision and records the
+// proposal's key for the distinct top-K.  Chain state never leaves the SM between
+// steps; only 8 bytes per chain-step (the visited key) go to HBM.
+#include "features.cuh"
+#include "gbt.cuh"
+#include "topk.cuh"
+
+namespace at {
+
+constexpr int SA_NW = 8;
+
+struct TileSink {
+    float *tile;
+    int lane;
+    __device__ __forceinline__ void put(int f, float v) { tile[f * 32 + lane] = v; }
+    __device__ __forceinline__ void put_rel(int f, float v) { tile[f * 32 + lane] = v; }
+};
+
+template <int TMPL>
+__device__ __forceinline__ void feats_into_tile(const WlDev &W, const uint16_t *fact, const uint32_t *ch, float *tile,
+                                                int lane)
+{
+    TileSink sk{tile, lane};
+    features_one<TMPL>(W, fact, ch, sk);
+}
+
+__device__ __forceinline__ void feats_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, float *tile,
+                                          int lane)
+{
+    switch (W.tmpl) {
+    case 0: feats_into_tile<0>(W, fact, ch, tile, lane); break;
+    case 1: feats_into_tile<1>(W, fact, ch, tile, lane); break;
+    default: feats_into_tile<2>(W, fact, ch, tile, lane); break;
+    }
+}
+
+__device__ __forceinline__ void zero_cols_any(int tmpl, float *tile, int lane)
+{
+    TileSink sk{tile, lane};
+    switch (tmpl) {
+    case 0: features_zero_cols<0>(sk); break;
+    case 1: features_zero_cols<1>(sk); break;
+    default: features_zero_cols<2>(sk); break;
+    }
+}
+
+__device__ __forceinline__ void decode_any(const WlDev &W, uint32_t local, uint32_t *ch)
+{
+    switch (W.tmpl) {
+    case 0: decode_knobs<0>(W, local, ch); break;
+    case 1: decode_knobs<1>(W, local, ch); break;
+    default: decode_knobs<2>(W, local, ch); break;
+    }
+#pragma unroll
+    for (int j = 0; j < MAXKNOBS; ++j)
+        if (j >= W.n_knobs) ch[j] = 0;
+}
+
+struct SaParams {
+    const SpaceDev *S;
+    const uint16_t *fact;
+    const uint2 *nodes;
+    const float *leaf;
+    int T, D;
+    float base;
+    int n_chains, n_steps, init;
+    uint64_t seed;
+    uint32_t round, chain_base;
+    const float *temps;
+    const uint16_t *chain_w;
+    uint64_t *chain_idx;
+    float *chain_E;
+    uint32_t *accept_bits;
+    float *vis_E;
+    uint64_t *vis_idx;
+    uint64_t *keys;   // [n_chains][n_steps+1]
+};
+
+__global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P)
+{
+    extern __shared__ float sm[];
+    float *tile = sm;                  // [468][32]
+    float *part = sm + NFEAT * 32;     // [32][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + lane;
+    const bool live = c < P.n_chains;
+    const int64_t per = (int64_t)P.n_steps + 1;
+
+    // warp-0 state (registers)
+    uint32_t ch[MAXKNOBS];
+    uint64_t idx = 0, idx2 = 0;
+    float E = 0.f;
+    int w = 0;
+    uint32_t g = P.chain_base + (uint32_t)c;
+    uint32_t accw = 0;
+    int pj = -1;
+    uint32_t pv = 0;
+
+    if (warp == 0) {
+        if (live && P.chain_w) w = P.chain_w[c];
+        const WlDev &W = P.S->w[w];
+        if (live) {
+            if (P.init) {
+                const U4 r = philox(P.seed, g, 0, P.round, TAG_SA_INIT);
+                idx = W.offset + mulhi64((uint64_t)r.x | ((uint64_t)r.y << 32), (uint64_t)W.size);
+            } else {
+                idx = P.chain_idx[c];
+            }
+        } else {
+            idx = W.offset;
+        }
+        decode_any(W, (uint32_t)(idx - W.offset), ch);
+        zero_cols_any(W.tmpl, tile, lane);
+        feats_any(W, P.fact, ch, tile, lane);
+    }
+    __syncthreads();
+    gbt_walk_partials<SA_NW>(P.nodes, P.leaf, P.T, P.D, tile, lane, warp, part, nullptr, 0, 0, false);
+    __syncthreads();
+    if (warp == 0) {
+        E = gbt_combine(part, lane, P.base);
+        if (live) {
+            P.keys[(int64_t)c * per] = ((uint64_t)fkey(E) << 32) | (uint64_t)(idx - P.S->w[w].offset);
+            if (P.vis_E) { P.vis_E[(int64_t)c * per] = E; P.vis_idx[(int64_t)c * per] = idx; }
+        }
+    }
+
+    for (int s = 0; s < P.n_steps; ++s) {
+        U4 r;
+        if (warp == 0) {
+            const WlDev &W = P.S->w[w];
+            r = philox(P.seed, g, (uint32_t)s, P.round, TAG_SA_STEP);
+            idx2 = idx;
+            pj = -1;
+            if (W.n_ns > 0) {
+                const int j = W.ns_list[__umulhi(r.x, W.n_ns)];
+                uint32_t v = 0;
+#pragma unroll
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == j) v = ch[q];
+                uint32_t v2 = __umulhi(r.y, W.radix[j] - 1u);
+                if (v2 >= v) v2 += 1;
+                idx2 = idx - (uint64_t)v * W.place[j] + (uint64_t)v2 * W.place[j];
+                pj = j;
+                pv = v;
+#pragma unroll
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == j) ch[q] = v2;
+            }
+            feats_any(W, P.fact, ch, tile, lane);
+        }
+        __syncthreads();
+        gbt_walk_partials<SA_NW>(P.nodes, P.leaf, P.T, P.D, tile, lane, warp, part, nullptr, 0, 0, false);
+        __syncthreads();
+        if (warp == 0) {
+            const float E2 = gbt_combine(part, lane, P.base);
+            const float d = __fsub_rn(E2, E);
+            bool acc = d <= 0.0f;
+            if (!acc) {
+                const float T = __ldg(P.temps + s);
+                if (T > 0.0f) {
+                    const float u = __fmul_rn(__uint2float_rn(r.z >> 8), __int_as_float(0x33800000));
+                    acc = u < exp_det(-__fdiv_rn(d, T));
+                }
+            }
+            if (acc) {
+                idx = idx2;
+                E = E2;
+                accw |= 1u << (s & 31);
+            } else if (pj >= 0) {
+#pragma unroll
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == pj) ch[q] = pv;   // undo the move
+            }
+            if (live) {
+                const int64_t at = (int64_t)c * per + s + 1;
+                P.keys[at] = ((uint64_t)fkey(E2) << 32) | (uint64_t)(idx2 - P.S->w[w].offset);
+                if (P.vis_E) { P.vis_E[at] = E2; P.vis_idx[at] = idx2; }
+                if (P.accept_bits && ((s & 31) == 31 || s == P.n_steps - 1)) {
+                    P.accept_bits[(int64_t)c * ((P.n_steps + 31) / 32) + (s >> 5)] = accw;
+                }
+            }
+            if ((s & 31) == 31) accw = 0;
+        }
+    }
+    if (warp == 0 && live) {
+        P.chain_idx[c] = idx;
+        P.chain_E[c] = E;
+    }
+}
+
+}  // namespace at
+
+extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d_chain_energy,
+                          const uint16_t *d_chain_workload, const uint64_t *d_measured_sorted, int64_t n_measured,
+                          const at_sa_opts *o, uint64_t *d_out_idx, float *d_out_score, int32_t *d_out_n,
+                          void *stream)
+{
+    if (!sp || !g || !o) return at::fail(AT_EINVAL, "sa_explore: null handle");
+    if (!d_chain_idx || !d_chain_energy || !o->d_temps || !d_out_idx || !d_out_score || !d_out_n)
+        return at::fail(AT_EINVAL, "sa_explore: null buffer");
+    if (o->n_chains < 1 || o->n_steps < 0 || o->k_out < 1 || o->k_out > 1024 || n_measured < 0)
+        return at::fail(AT_EINVAL, "sa_explore: need n_chains >= 1, n_steps >= 0, 1 <= k_out <= 1024");
+    if (n_measured > 0 && !d_measured_sorted) return at::fail(AT_EINVAL, "sa_explore: null measured list");
+    if (g->n_features != at::NFEAT) return at::fail(AT_EMISMATCH, "sa_explore: model must take 468 features");
+    if ((uint64_t)o->chain_id_base + (uint64_t)o->n_chains > 0x100000000ull)
+        return at::fail(AT_ERANGE, "sa_explore: global chain ids exceed 2^32");
+    if ((o->d_visited_E == nullptr) != (o->d_visited_idx == nullptr))
+        return at::fail(AT_EINVAL, "sa_explore: d_visited_E and d_visited_idx go together");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t per = (int64_t)o->n_steps + 1;
+    const int64_t n_keys = (int64_t)o->n_chains * per;
+    const size_t key_bytes = ((size_t)n_keys * sizeof(uint64_t) + 255) / 256 * 256;
+    int rc = at::scratch_reserve(sp, key_bytes + at::topk_scratch_bytes(n_keys, o->k_out), s);
+    if (rc) return rc;
+    uint64_t *keys = (uint64_t *)sp->d_scratch;
+    uint64_t *tkbuf = (uint64_t *)((char *)sp->d_scratch + key_bytes);
+
+    at::SaParams P{};
+    P.S = sp->d_space;
+    P.fact = sp->d_fact;
+    P.nodes = g->d_nodes;
+    P.leaf = g->d_leaf;
+    P.T = g->n_trees;
+    P.D = g->depth;
+    P.base = g->base;
+    P.n_chains = o->n_chains;
+    P.n_steps = o->n_steps;
+    P.init = o->init;
+    P.seed = o->seed;
+    P.round = o->round;
+    P.chain_base = o->chain_id_base;
+    P.temps = o->d_temps;
+    P.chain_w = d_chain_workload;
+    P.chain_idx = d_chain_idx;
+    P.chain_E = d_chain_energy;
+    P.accept_bits = o->d_accept_bits;
+    P.vis_E = o->d_visited_E;
+    P.vis_idx = o->d_visited_idx;
+    P.keys = keys;
+    const size_t smem = (size_t)(at::NFEAT * 32 + 32 * 32) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        AT_CUDA_TRY(cudaFuncSetAttribute(at::sa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    {
+        at::ProfScope ps(AT_K_SA, s);
+        const unsigned blocks = (unsigned)((o->n_chains + 31) / 32);
+        at::sa_kernel<<<blocks, at::SA_NW * 32, smem, s>>>(P);
+        AT_LAUNCH_CHECK("sa_kernel");
+    }
+    for (int w = 0; w < sp->host.n_w; ++w) {
+        at::TkArgs a{};
+        a.mode = 0;
+        a.keys = keys;
+        a.n_src = n_keys;
+        a.per_chain = per;
+        a.chain_w = d_chain_workload;
+        a.w = w;
+        a.offset_w = sp->host.offset[w];
+        a.measured = d_measured_sorted;
+        a.n_measured = n_measured;
+        a.K = o->k_out;
+        a.out_idx = d_out_idx + (int64_t)w * o->k_out;
+        a.out_score = d_out_score + (int64_t)w * o->k_out;
+        a.out_n = d_out_n + w;
+        if (!d_chain_workload && w > 0) {
+            // no chain belongs to this workload: empty list
+            a.n_src = 0;
+        }
+        rc = at::topk_run(a, tkbuf, s);
+        if (rc) return rc;
+    }
+    return AT_OK;
+}

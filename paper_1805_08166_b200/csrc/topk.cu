@@ -1,0 +1,242 @@
+// topk.cu -- distinct top-K of collected candidates (a7; Alg. 1 P:152 "collect candidates",
+// reading Q23: unique by idx, measured excluded, ordered by (E asc, idx asc)).
+//
+// A candidate is the 64-bit key (order-preserving bits of E) << 32 | local idx, so the
+// (E, idx) order is plain u64 order and -- because E is a function of idx -- duplicates
+// of a configuration are equal keys.  Every block sorts a 4096-key tile in shared
+// memory (bitonic), drops repeats and keeps its K smallest distinct keys; the
+// per-block lists are reduced again by the same kernel until one list remains.  The
+// K smallest distinct keys of a union are always inside the union of the per-part
+// K smallest distinct keys, so the result is exact and independent of the tiling.
+#include "at_common.cuh"
+#include "topk.cuh"
+
+namespace at {
+
+constexpr int TK_TILE = 4096;
+constexpr int TK_THREADS = 1024;
+constexpr uint64_t KEY_NONE = ~0ull;
+
+__device__ __forceinline__ bool in_sorted(const uint64_t *__restrict__ a, int64_t n, uint64_t v)
+{
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < v) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && __ldg(a + lo) == v;
+}
+
+// mode 0: raw SA keys [n_chains][per_chain] filtered by chain workload == w and not measured
+// mode 1: lists [n_lists][n_w][k_in] of (idx, score) with counts, workload w, not measured
+// mode 2: partial key lists (already filtered), plain reduction
+struct TkSrc {
+    int mode;
+    const uint64_t *keys;
+    int64_t n;               // number of source keys (mode 0: n_chains*per_chain; 1: n_lists*k_in; 2: count)
+    int64_t per_chain;
+    const uint16_t *chain_w;
+    int w;
+    uint64_t offset_w;
+    const uint64_t *l_idx;
+    const float *l_score;
+    const int32_t *l_n;
+    int n_w, k_in;
+    const uint64_t *measured;
+    int64_t n_measured;
+};
+
+__device__ __forceinline__ uint64_t tk_load(const TkSrc &S, int64_t i)
+{
+    if (i >= S.n) return KEY_NONE;
+    if (S.mode == 2) return __ldg(S.keys + i);
+    uint64_t key, gidx;
+    if (S.mode == 0) {
+        const int64_t c = i / S.per_chain;
+        if (S.chain_w && (int)__ldg(S.chain_w + c) != S.w) return KEY_NONE;
+        key = __ldg(S.keys + i);
+        gidx = S.offset_w + (key & 0xFFFFFFFFull);
+    } else {
+        const int64_t l = i / S.k_in, j = i - l * S.k_in;
+        if (j >= __ldg(S.l_n + l * S.n_w + S.w)) return KEY_NONE;
+        const int64_t at = (l * S.n_w + S.w) * S.k_in + j;
+        gidx = __ldg(S.l_idx + at);
+        key = ((uint64_t)fkey(__ldg(S.l_score + at)) << 32) | (uint64_t)(gidx - S.offset_w);
+    }
+    if (S.n_measured && in_sorted(S.measured, S.n_measured, gidx)) return KEY_NONE;
+    return key;
+}
+
+__global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, uint64_t *__restrict__ out)
+{
+    __shared__ uint64_t s[TK_TILE];
+    __shared__ int wsum[TK_THREADS / 32];
+    const int tid = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * TK_TILE;
+    for (int i = tid; i < TK_TILE; i += TK_THREADS) s[i] = tk_load(S, base + i);
+    __syncthreads();
+    for (int k = 2; k <= TK_TILE; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < TK_TILE; i += TK_THREADS) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t a = s[i], b = s[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) { s[i] = b; s[ixj] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // distinct: keep keys that differ from their predecessor; compact the first K
+    constexpr int PER = TK_TILE / TK_THREADS;   // 4 consecutive keys per thread
+    uint64_t v[PER];
+    int flag[PER];
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int i = tid * PER + q;
+        v[q] = s[i];
+        flag[q] = (v[q] != KEY_NONE) && (i == 0 || s[i - 1] != v[q]);
+        cnt += flag[q];
+    }
+    // block exclusive scan of cnt
+    const int lane = tid & 31, warp = tid >> 5;
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int x = wsum[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+            if (lane >= off) x += y;
+        }
+        wsum[lane] = x;   // inclusive
+    }
+    __syncthreads();
+    int pos = incl - cnt + (warp > 0 ? wsum[warp - 1] : 0);
+    uint64_t *o = out + (int64_t)blockIdx.x * K;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        if (flag[q]) {
+            if (pos < K) o[pos] = v[q];
+            ++pos;
+        }
+    }
+    const int total = wsum[31];
+    for (int i = total + tid; i < K; i += TK_THREADS) o[i] = KEY_NONE;
+}
+
+__global__ void topk_finish_kernel(const uint64_t *__restrict__ keys, int K, uint64_t offset_w,
+                                   uint64_t *__restrict__ out_idx, float *__restrict__ out_score,
+                                   int32_t *__restrict__ out_n)
+{
+    // single block: keys are sorted and distinct with KEY_NONE padding
+    __shared__ int n_valid;
+    if (threadIdx.x == 0) n_valid = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+        const uint64_t k = keys[i];
+        if (k != KEY_NONE) {
+            out_idx[i] = offset_w + (k & 0xFFFFFFFFull);
+            out_score[i] = fkey_inv((uint32_t)(k >> 32));
+            atomicAdd(&n_valid, 1);
+        } else {
+            out_idx[i] = 0;
+            out_score[i] = 0.f;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *out_n = n_valid;
+}
+
+size_t topk_scratch_bytes(int64_t n_src, int K)
+{
+    const int64_t b1 = (n_src + TK_TILE - 1) / TK_TILE;
+    return (size_t)(2 * (b1 + 1) * (int64_t)K) * sizeof(uint64_t);
+}
+
+int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s)
+{
+    TkSrc S{};
+    S.mode = a.mode;
+    S.keys = a.keys;
+    S.n = a.n_src;
+    S.per_chain = a.per_chain;
+    S.chain_w = a.chain_w;
+    S.w = a.w;
+    S.offset_w = a.offset_w;
+    S.l_idx = a.l_idx;
+    S.l_score = a.l_score;
+    S.l_n = a.l_n;
+    S.n_w = a.n_w;
+    S.k_in = a.k_in;
+    S.measured = a.measured;
+    S.n_measured = a.n_measured;
+    const int K = a.K;
+    int64_t blocks = (a.n_src + TK_TILE - 1) / TK_TILE;
+    if (blocks < 1) blocks = 1;
+    uint64_t *bufA = scratch, *bufB = scratch + (blocks + 1) * K;
+    ProfScope ps(AT_K_TOPK, s);
+    topk_tile_kernel<<<(unsigned)blocks, TK_THREADS, 0, s>>>(S, K, bufA);
+    AT_LAUNCH_CHECK("topk_tile_kernel");
+    int64_t n = blocks * K;
+    while (blocks > 1) {
+        TkSrc R{};
+        R.mode = 2;
+        R.keys = bufA;
+        R.n = n;
+        blocks = (n + TK_TILE - 1) / TK_TILE;
+        topk_tile_kernel<<<(unsigned)blocks, TK_THREADS, 0, s>>>(R, K, bufB);
+        AT_LAUNCH_CHECK("topk_tile_kernel(reduce)");
+        n = blocks * K;
+        uint64_t *t = bufA; bufA = bufB; bufB = t;
+    }
+    topk_finish_kernel<<<1, 256, 0, s>>>(bufA, K, a.offset_w, a.out_idx, a.out_score, a.out_n);
+    AT_LAUNCH_CHECK("topk_finish_kernel");
+    return AT_OK;
+}
+
+}  // namespace at
+
+extern "C" int topk_merge(at_space sp, const uint64_t *d_in_idx, const float *d_in_score, const int32_t *d_in_n,
+                          int32_t n_lists, int32_t k_in, const uint64_t *d_measured_sorted, int64_t n_measured,
+                          int32_t k_out, uint64_t *d_out_idx, float *d_out_score, int32_t *d_out_n, void *stream)
+{
+    if (!sp || !d_in_idx || !d_in_score || !d_in_n || !d_out_idx || !d_out_score || !d_out_n)
+        return at::fail(AT_EINVAL, "topk_merge: null pointer");
+    if (n_lists < 1 || k_in < 1 || k_out < 1 || k_out > 1024 || n_measured < 0)
+        return at::fail(AT_EINVAL, "topk_merge: need n_lists, k_in >= 1 and 1 <= k_out <= 1024");
+    if (n_measured > 0 && !d_measured_sorted) return at::fail(AT_EINVAL, "topk_merge: null measured list");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n_src = (int64_t)n_lists * k_in;
+    int rc = at::scratch_reserve(sp, at::topk_scratch_bytes(n_src, k_out), s);
+    if (rc) return rc;
+    for (int w = 0; w < sp->host.n_w; ++w) {
+        at::TkArgs a{};
+        a.mode = 1;
+        a.n_src = n_src;
+        a.w = w;
+        a.offset_w = sp->host.offset[w];
+        a.l_idx = d_in_idx;
+        a.l_score = d_in_score;
+        a.l_n = d_in_n;
+        a.n_w = sp->host.n_w;
+        a.k_in = k_in;
+        a.measured = d_measured_sorted;
+        a.n_measured = n_measured;
+        a.K = k_out;
+        a.out_idx = d_out_idx + (int64_t)w * k_out;
+        a.out_score = d_out_score + (int64_t)w * k_out;
+        a.out_n = d_out_n + w;
+        rc = at::topk_run(a, (uint64_t *)sp->d_scratch, s);
+        if (rc) return rc;
+    }
+    return AT_OK;
+}

@@ -1,0 +1,30 @@
+// topk.cuh -- host interface of the distinct top-K reduction (topk.cu).
+#pragma once
+#include "at_common.cuh"
+
+namespace at {
+
+struct TkArgs {
+    int mode;                    // 0 SA keys, 1 (idx, score) lists
+    const uint64_t *keys;        // mode 0: [n_chains][per_chain] keys (fkey(E) << 32 | local idx)
+    int64_t n_src;
+    int64_t per_chain;
+    const uint16_t *chain_w;     // mode 0: workload of each chain (nullable)
+    int w;
+    uint64_t offset_w;
+    const uint64_t *l_idx;       // mode 1
+    const float *l_score;
+    const int32_t *l_n;
+    int n_w, k_in;
+    const uint64_t *measured;
+    int64_t n_measured;
+    int K;
+    uint64_t *out_idx;
+    float *out_score;
+    int32_t *out_n;
+};
+
+size_t topk_scratch_bytes(int64_t n_src, int K);
+int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s);
+
+}  // namespace at

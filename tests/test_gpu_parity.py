@@ -1,0 +1,407 @@
+"""GPU parity: the sm_100a library (through the C-ABI) against the CPU oracle.
+
+Every comparison is element by element on the same seeded inputs (paper_1805_08166_b200.synth):
+bit-exact for indices, features, leaf slots, accept bits, top-k, selections, histograms and
+fitted trees; scores within 1e-6 relative (north_star) -- and in practice bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1805_08166_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def at():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1805_08166_b200 import at as _at
+    from paper_1805_08166_b200 import build
+    build.build()
+    return _at
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def u64(a):
+    return dev(np.asarray(a, dtype=np.uint64).view(np.int64))
+
+
+def host_u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def gpu_features(at, space, idx):
+    X = space.features(u64(idx))
+    return X[:, :len(idx)].cpu().numpy().T.copy()
+
+
+def assert_bits_equal(a, b, what):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    bad = np.argwhere(a.view(np.uint32) != b.view(np.uint32)) if a.dtype == np.float32 else np.argwhere(a != b)
+    assert len(bad) == 0, f"{what}: {len(bad)} mismatches, first {bad[:5].tolist()} gpu={a[tuple(bad[0])]} oracle={b[tuple(bad[0])]}"
+
+
+# ------------------------------------------------------------------ space
+@pytest.mark.parametrize("wls", [[synth.MATMUL_512], [synth.CFG2A], [synth.CFG2B], synth.ALL_RESNET, synth.ALL_DW,
+                                 [synth.MATMUL_8, synth.CONV_TINY, synth.ALL_DW[8]]])
+def test_space_matches_oracle(at, wls):
+    g = at.Space(wls)
+    o = O.OracleSpace([O.workload(**w) for w in wls])
+    assert g.size_total == o.size()
+    assert g.offsets == [o.offset(w) for w in range(len(wls))] + [o.size()]
+    for w in range(len(wls)):
+        assert g.radices[w] == o.radices(w)
+
+
+# ------------------------------------------------------------------ features
+def test_features_all_of_config1_space(at):
+    """Config 1: every one of the 151,250 matmul-512 schedules, bit-exact."""
+    sp = at.Space([synth.MATMUL_512])
+    osp = O.OracleSpace([O.workload(**synth.MATMUL_512)])
+    idx = np.arange(osp.size(), dtype=np.uint64)
+    assert_bits_equal(gpu_features(at, sp, idx), osp.features(idx), "features cfg1")
+
+
+@pytest.mark.parametrize("name,wls,n", [
+    ("cfg2a", [synth.CFG2A], 3001), ("cfg2b", [synth.CFG2B], 2999), ("C1", [synth.resnet("C1")], 1500),
+    ("resnet-union", synth.ALL_RESNET, 6007), ("dw-union", synth.ALL_DW, 4099),
+    ("mixed", [synth.MATMUL_8, synth.CONV_TINY, synth.ALL_DW[3]], 1777)])
+def test_features_random_candidates(at, name, wls, n):
+    sp = at.Space(wls)
+    osp = O.OracleSpace([O.workload(**w) for w in wls])
+    idx = synth.uniform_indices(osp.size(), n, seed=hash(name) % 1000)
+    idx[:3] = [0, osp.size() - 1, osp.offset(len(wls) - 1)]
+    assert_bits_equal(gpu_features(at, sp, idx), osp.features(idx), f"features {name}")
+
+
+def test_features_edge_cases(at):
+    sp = at.Space([synth.CFG2A])
+    out = torch.full((468, 128), 7.0, device="cuda")
+    sp.features(u64(np.zeros(0, np.uint64)), out=out, ld=128)          # n = 0 is a no-op
+    assert torch.all(out == 7.0)
+    one = gpu_features(at, sp, np.array([12345], np.uint64))
+    osp = O.OracleSpace([O.workload(**synth.CFG2A)])
+    assert_bits_equal(one, osp.features(np.array([12345], np.uint64)), "n=1")
+    with pytest.raises(at.ATError):
+        sp.features(u64(np.zeros(10, np.uint64)), out=torch.empty((468, 8), device="cuda"), ld=8)
+
+
+# ------------------------------------------------------------------ GBT
+def test_hand_ensemble(at):
+    e = synth.hand_ensemble()
+    g = at.Gbt(e["feat"], e["thresh"], e["leaf"], n_features=2)
+    X = dev(np.array([[1, 2.5, 3], [0, 1.5, 0.7]], np.float32))
+    s, sl = g.predict(X, slots=True)
+    assert s.cpu().tolist() == [1.25, 3.5, 3.25]
+    assert sl.cpu().numpy().T.tolist() == [[0, 0], [3, 2], [2, 0]]
+    ex = g.export()
+    for k in ("feat", "thresh", "leaf"):
+        assert np.array_equal(ex[k], e[k])
+
+
+@pytest.mark.parametrize("T,D,n", [(100, 6, 2048), (37, 3, 1000), (500, 6, 777), (1000, 8, 300), (33, 1, 65)])
+def test_gbt_predict_scores_and_slots(at, T, D, n):
+    ens = synth.ensemble(T, D, seed=T * 10 + D)
+    osp = O.OracleSpace([O.workload(**w) for w in synth.ALL_RESNET])
+    idx = synth.uniform_indices(osp.size(), n, seed=T)
+    Xo = osp.features(idx)
+    sp = at.Space(synth.ALL_RESNET)
+    Xg = sp.features(u64(idx))
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"], base=0.125)
+    s, sl = g.predict(Xg, n=n, slots=True)
+    es, esl = O.OracleGbt(ens["feat"], ens["thresh"], ens["leaf"], base=0.125).predict(Xo, slots=True)
+    assert_bits_equal(sl.cpu().numpy(), esl, "leaf slots")
+    s = s.cpu().numpy()
+    assert np.all(np.abs(s - es) <= 1e-6 * np.maximum(np.abs(es), 1e-30) + 0.0)
+    assert_bits_equal(s, es, "scores (canonical order => bit-exact)")
+
+
+def test_scores_config1_exhaustive_top8(at):
+    """Config 1 pin: exhaustive scoring of all 151,250 configs; GPU top-8 == oracle top-8."""
+    ens = synth.ensemble(100, 6, seed=1805)
+    osp = O.OracleSpace([O.workload(**synth.MATMUL_512)])
+    idx = np.arange(osp.size(), dtype=np.uint64)
+    Xo = osp.features(idx)
+    es = O.OracleGbt(**ens).predict(Xo)
+    sp = at.Space([synth.MATMUL_512])
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    s = g.predict(sp.features(u64(idx)), n=len(idx)).cpu().numpy()
+    assert_bits_equal(s, es, "cfg1 scores")
+    o8 = np.lexsort((idx, es))[:8]
+    g8 = np.lexsort((idx, s))[:8]
+    assert np.array_equal(idx[o8], idx[g8])
+
+
+# ------------------------------------------------------------------ SA + top-k
+def run_both(at, wls, ens, n_chains, n_steps, seed, round_, temps, K, chain_workload=None, chain_idx=None,
+             measured=(), chain_id_base=0):
+    osp = O.OracleSpace([O.workload(**w) for w in wls])
+    oe = O.OracleGbt(**ens)
+    r = osp.sa_explore(oe, n_chains, n_steps, seed, round_, temps, chain_id_base=chain_id_base,
+                       chain_workload=chain_workload, chain_idx=chain_idx)
+    otop = osp.topk(r["visited_E"], r["visited_idx"], K, measured=measured)
+    sp = at.Space(wls)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"], base=ens["base"])
+    init = chain_idx is None
+    cidx = u64(np.zeros(n_chains, np.uint64) if init else chain_idx)
+    cw = None if chain_workload is None else dev(np.asarray(chain_workload, np.uint16).view(np.int16))
+    meas = u64(np.sort(np.asarray(measured, np.uint64))) if len(measured) else None
+    res = at.sa_explore(sp, g, cidx, dev(temps), seed=seed, round_=round_, k_out=K, chain_workload=cw,
+                        measured=meas, init=init, chain_id_base=chain_id_base, accept_bits=True, visited=True)
+    torch.cuda.synchronize()
+    return r, otop, res
+
+
+def compare_sa(r, otop, res):
+    assert_bits_equal(host_u64(res["visited_idx"]), r["visited_idx"], "visited idx")
+    assert_bits_equal(res["visited_E"].cpu().numpy(), r["visited_E"], "visited E")
+    assert_bits_equal(res["accept_bits"].cpu().numpy().view(np.uint32), r["accept_bits"], "accept bits")
+    assert_bits_equal(host_u64(res["chain_idx"]), r["chain_idx"], "final states")
+    assert_bits_equal(res["chain_energy"].cpu().numpy(), r["chain_energy"], "final energies")
+    on = res["out_n"].cpu().numpy()
+    for w, (oi, oE) in enumerate(otop):
+        assert on[w] == len(oi)
+        assert_bits_equal(host_u64(res["out_idx"][w, :on[w]]), oi, f"top-k idx w{w}")
+        assert_bits_equal(res["out_score"][w, :on[w]].cpu().numpy(), oE, f"top-k E w{w}")
+
+
+def test_sa_tiny_space_exhaustive(at):
+    """Chains started at every config of the matmul-8^3 space: top-k == exhaustive ranking."""
+    ens = synth.ensemble(40, 6, seed=4)
+    N = 2000
+    temps = synth.temperatures(5, 0.3)
+    r, otop, res = run_both(at, [synth.MATMUL_8], ens, N, 5, 5, 0, temps, 64, chain_idx=np.arange(N, dtype=np.uint64))
+    compare_sa(r, otop, res)
+
+
+@pytest.mark.parametrize("T,D,steps,chains", [(500, 6, 40, 70), (100, 6, 33, 96), (60, 8, 20, 33)])
+def test_sa_conv_parity(at, T, D, steps, chains):
+    ens = synth.ensemble(T, D, seed=T + D)
+    temps = synth.temperatures(steps, synth.energy_scale(T))
+    r, otop, res = run_both(at, [synth.CFG2A], ens, chains, steps, 1805, 3, temps, 128)
+    compare_sa(r, otop, res)
+
+
+def test_sa_union_with_measured_and_persistence(at):
+    ens = synth.ensemble(120, 6, seed=77)
+    n_chains, steps = 48, 24
+    cw = (np.arange(n_chains) % 12).astype(np.uint16)
+    temps = synth.temperatures(steps, synth.energy_scale(120))
+    r, otop, res = run_both(at, synth.ALL_RESNET, ens, n_chains, steps, 9, 0, temps, 16, chain_workload=cw)
+    compare_sa(r, otop, res)
+    # round 1 from the persisted states, excluding some measured configs
+    meas = np.concatenate([otop[w][0][:3] for w in range(12)])
+    r2, otop2, res2 = run_both(at, synth.ALL_RESNET, ens, n_chains, steps, 9, 1, temps, 16, chain_workload=cw,
+                               chain_idx=r["chain_idx"], measured=meas)
+    compare_sa(r2, otop2, res2)
+
+
+def test_sa_edge_temperatures_and_zero_steps(at):
+    ens = synth.ensemble(50, 5, seed=3)
+    for temps in (np.full(20, np.inf, np.float32), np.zeros(20, np.float32), np.zeros(0, np.float32)):
+        r, otop, res = run_both(at, [synth.CFG2B], ens, 40, len(temps), 2, 0, temps, 32)
+        compare_sa(r, otop, res)
+
+
+def test_sa_full_config2_sampled_chains(at):
+    """Config 2 at its benchmark size (4096 chains x 500 steps, 500 trees): chains sampled one by one."""
+    ens = synth.ensemble(500, 6, seed=1805)
+    steps = 500
+    temps = synth.temperatures(steps, synth.energy_scale(500))
+    sp = at.Space([synth.CFG2A])
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    res = at.sa_explore(sp, g, u64(np.zeros(4096, np.uint64)), dev(temps), seed=1805, round_=0, k_out=128,
+                        init=True, accept_bits=True, visited=True)
+    torch.cuda.synchronize()
+    osp = O.OracleSpace([O.workload(**synth.CFG2A)])
+    oe = O.OracleGbt(**ens)
+    for c in (0, 1, 2047, 4095):
+        r = osp.sa_explore(oe, 1, steps, 1805, 0, temps, chain_id_base=c)
+        assert_bits_equal(res["accept_bits"][c:c + 1].cpu().numpy().view(np.uint32), r["accept_bits"], f"chain {c}")
+        assert_bits_equal(host_u64(res["visited_idx"][c:c + 1]), r["visited_idx"], f"chain {c} idx")
+    # the returned top-k is the distinct top-k of the visited set (checked with numpy on the GPU's visited set,
+    # whose entries are themselves oracle-checked above on samples)
+    vE = res["visited_E"].cpu().numpy().ravel()
+    vI = host_u64(res["visited_idx"]).ravel()
+    o = np.lexsort((vI, vE))
+    _, first = np.unique(vI[o], return_index=True)
+    keep = o[np.sort(first)][:128]
+    assert np.array_equal(host_u64(res["out_idx"][0]), vI[keep])
+
+
+def test_topk_merge_matches_oracle(at):
+    wls = [synth.CFG2A, synth.CFG2B]
+    osp = O.OracleSpace([O.workload(**w) for w in wls])
+    rng = np.random.default_rng(0)
+    L, K = 5, 40
+    idx = np.zeros((L, 2, K), np.uint64)
+    sc = np.zeros((L, 2, K), np.float32)
+    cnt = rng.integers(0, K + 1, size=(L, 2)).astype(np.int32)
+    pool = {w: synth.uniform_indices(osp.size(w), 90, seed=w) + np.uint64(osp.offset(w)) for w in range(2)}
+    score_of = {int(i): np.float32(rng.integers(0, 20) / 8) for w in range(2) for i in pool[w]}   # many ties
+    for l in range(L):
+        for w in range(2):
+            pick = rng.choice(pool[w], size=K, replace=False)
+            idx[l, w] = pick
+            sc[l, w] = [score_of[int(i)] for i in pick]
+    meas = np.sort(pool[0][:7])
+    allE, allI = [], []
+    for l in range(L):
+        for w in range(2):
+            allE += list(sc[l, w, :cnt[l, w]])
+            allI += list(idx[l, w, :cnt[l, w]])
+    otop = osp.topk(np.array(allE, np.float32), np.array(allI, np.uint64), 30, measured=meas)
+    sp = at.Space(wls)
+    gi, gs, gn = at.topk_merge(sp, u64(idx), dev(sc), dev(cnt), 30, measured=u64(meas))
+    for w in range(2):
+        n = int(gn[w])
+        assert n == len(otop[w][0])
+        assert_bits_equal(host_u64(gi[w, :n]), otop[w][0], "merge idx")
+        assert_bits_equal(gs[w, :n].cpu().numpy(), otop[w][1], "merge E")
+
+
+# ------------------------------------------------------------------ select
+@pytest.mark.parametrize("b,eps,alpha,n_pool", [(64, 0.05, 0.1, 128), (64, 0.0, 0.0, 128), (8, 0.0, 0.0, 8),
+                                                (64, 0.05, 1.0, 40), (16, 0.5, 0.3, 100), (64, 0.05, 0.1, 1000)])
+def test_select_matches_oracle(at, b, eps, alpha, n_pool):
+    wls = synth.ALL_RESNET
+    osp = O.OracleSpace([O.workload(**w) for w in wls])
+    w = 6
+    pool = synth.uniform_indices(osp.size(w), n_pool, seed=n_pool) + np.uint64(osp.offset(w))
+    E = (np.random.default_rng(b).integers(0, 50, n_pool) / 16).astype(np.float32)   # ties on purpose
+    o = np.lexsort((pool, E))
+    pool, E = pool[o], E[o]
+    meas = np.sort(np.concatenate([synth.uniform_indices(osp.size(w), 30, seed=5) + np.uint64(osp.offset(w)),
+                                   np.array([1, 2, 3], np.uint64)]))
+    ref = osp.select(w, pool, E, b, eps, alpha, seed=11, round_=2, measured=meas)
+    sp = at.Space(wls)
+    out, n = at.select_topk(sp, w, u64(pool), dev(E), b=b, eps=eps, alpha=alpha, seed=11, round_=2,
+                            measured=u64(meas))
+    assert int(n) == len(ref)
+    assert_bits_equal(host_u64(out[:int(n)]), ref, "selection")
+
+
+def test_select_exhausted_space(at):
+    wl = dict(kind=0, n=1, m=1, k=2)
+    osp = O.OracleSpace([O.workload(**wl)])
+    meas = np.array([0, 1, 2, 3], np.uint64)
+    pool = np.array([4, 5], np.uint64)
+    E = np.array([0.1, 0.2], np.float32)
+    ref = osp.select(0, pool, E, 20, 0.5, 0.0, 1, 0, measured=meas)
+    sp = at.Space([wl])
+    out, n = at.select_topk(sp, 0, u64(pool), dev(E), b=20, eps=0.5, alpha=0.0, seed=1, round_=0, measured=u64(meas))
+    assert_bits_equal(host_u64(out[:int(n)]), ref, "exhausted")
+
+
+# ------------------------------------------------------------------ refit
+def fit_inputs(n, wls, seed):
+    osp = O.OracleSpace([O.workload(**w) for w in wls])
+    key = synth.group_keys(n, len(wls), seed=seed)
+    idx = np.array([osp.offset(int(k)) + int(v) for k, v in
+                    zip(key, synth.uniform_indices(1 << 62, n, seed=seed) % np.array([osp.size(int(k)) for k in key],
+                                                                                     dtype=np.uint64))], np.uint64)
+    X = osp.features(idx)
+    return osp, idx, X, synth.labels(X, seed=seed), key
+
+
+@pytest.mark.parametrize("n,wls,trees,depth", [(1500, [synth.CFG2A, synth.CFG2B], 6, 4),
+                                               (700, synth.ALL_DW[:3], 4, 6),
+                                               (3000, [synth.MATMUL_512], 3, 5)])
+def test_fit_matches_oracle(at, n, wls, trees, depth):
+    osp, idx, X, c, key = fit_inputs(n, wls, seed=n)
+    ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth, want_hist0=True)
+    sp = at.Space(wls)
+    Xg = sp.features(u64(idx))
+    pred = torch.empty(n, dtype=torch.float32, device="cuda")
+    h0 = torch.empty((468, 256, 2), dtype=torch.int64, device="cuda")
+    g = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), n_trees=trees, depth=depth, pred_out=pred,
+                        hist0_out=h0)
+    ex = g.export()
+    assert_bits_equal(h0.cpu().numpy(), ref["hist0"], "root histogram of tree 0")
+    assert_bits_equal(ex["feat"], ref["feat"], "split features")
+    assert_bits_equal(ex["thresh"], ref["thresh"], "thresholds")
+    assert_bits_equal(ex["leaf"], ref["leaf"], "leaves")
+    assert_bits_equal(pred.cpu().numpy(), ref["pred"], "fit predictions")
+
+
+def test_fit_many_unique_values_uses_quantile_cuts(at):
+    n = 2000
+    rng = np.random.default_rng(3)
+    X = np.zeros((n, 468), np.float32)
+    X[:, :40] = rng.random((n, 40)).astype(np.float32) * 1000        # > 256 unique values
+    X[:, 40:80] = rng.integers(0, 5, (n, 40)).astype(np.float32)
+    c = (X[:, 0] + 3 * X[:, 41] + rng.random(n)).astype(np.float32)
+    key = np.zeros(n, np.uint16)
+    ref = O.fit_hist(X, c, key, n_trees=3, depth=4)
+    Xg = dev(np.ascontiguousarray(np.pad(X, ((0, 48), (0, 0))).T))
+    g = __import__("paper_1805_08166_b200").at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), n_trees=3, depth=4)
+    ex = g.export()
+    for k in ("feat", "thresh", "leaf"):
+        assert_bits_equal(ex[k], ref[k], k)
+
+
+def test_fit_rank_invariance_two_emulated_ranks(at):
+    """Histogram slices + all-reduce: 2 ranks emulated with 2 host threads and 2 streams on one GPU
+    (host-side barrier, no kernel waits on another) give the bit-identical ensemble."""
+    import threading
+    n = 1200
+    osp, idx, X, c, key = fit_inputs(n, [synth.CFG2A], seed=9)
+    sp = at.Space([synth.CFG2A])
+    Xg = sp.features(u64(idx))
+    cg, kg = dev(c), dev(key.view(np.int16))
+    single = at.gbt_fit_hist(Xg, n, cg, kg, n_trees=4, depth=5).export()
+    torch.cuda.synchronize()
+    bar = threading.Barrier(2)
+    bufs = [None, None]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    out = [None, None]
+
+    def make_ar(r):
+        def ar(t):
+            streams[r].synchronize()
+            bufs[r] = t
+            bar.wait()
+            if r == 0:
+                s = bufs[0] + bufs[1]
+                bufs[0].copy_(s)
+                bufs[1].copy_(s)
+                torch.cuda.synchronize()
+            bar.wait()
+        return ar
+
+    def run(r):
+        with torch.cuda.stream(streams[r]):
+            rng = (0, n // 2) if r == 0 else (n // 2, n)
+            out[r] = at.gbt_fit_hist(Xg, n, cg, kg, n_trees=4, depth=5, hist_range=rng, allreduce=make_ar(r),
+                                     stream=streams[r])
+            streams[r].synchronize()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    for r in range(2):
+        ex = out[r].export()
+        for k in ("feat", "thresh", "leaf"):
+            assert_bits_equal(ex[k], single[k], f"rank {r} {k}")
+
+
+def test_fit_errors(at):
+    with pytest.raises(at.ATError) as e:
+        at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 0, torch.zeros(4, device="cuda"),
+                        torch.zeros(4, dtype=torch.int16, device="cuda"))
+    assert e.value.code == -7
+    with pytest.raises(at.ATError):
+        c = torch.tensor([1.0, float("nan"), 2.0, 3.0], device="cuda")
+        at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 4, c, torch.zeros(4, dtype=torch.int16, device="cuda"))
