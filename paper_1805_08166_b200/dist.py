@@ -1,0 +1,80 @@
+"""Multi-GPU plumbing for the hot path (one process per GPU, torch.distributed).
+
+The path shards three ways:
+  * SA chains: rank r owns global chain ids [r * n_per_rank, (r + 1) * n_per_rank); chain
+    randomness is keyed by the global id, so trajectories do not depend on the rank count;
+  * per-rank distinct top-k lists are all-gathered once (the exchange step of Alg. 1
+    P:152 "collect candidates") and merged by topk_merge;
+  * refit samples: every rank holds all samples, builds histograms over its contiguous
+    slice, and the per-level int64 histograms are summed with one all-reduce.
+Integer histograms and global-id RNG make every output bit-identical at any rank count.
+Only host logic lives here; all arithmetic runs in the library kernels.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def world():
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def chain_slice(n_per_rank: int, rank: int):
+    """Global chain-id base and count of this rank (weak scaling: n_per_rank chains per GPU)."""
+    return rank * n_per_rank, n_per_rank
+
+
+def sample_slice(n: int, rank: int, world_size: int):
+    """Contiguous histogram slice [begin, end) of n samples for this rank."""
+    q, r = divmod(n, world_size)
+    begin = rank * q + min(rank, r)
+    return begin, begin + q + (1 if rank < r else 0)
+
+
+def chain_workloads(base: int, count: int, n_workloads: int, device) -> torch.Tensor:
+    """Workload of each local chain: global chain c belongs to workload c mod n_workloads (config 3)."""
+    c = torch.arange(base, base + count, device=device, dtype=torch.int64)
+    return (c % n_workloads).to(torch.int16)
+
+
+def gather_lists(out_idx: torch.Tensor, out_score: torch.Tensor, out_n: torch.Tensor, group=None):
+    """All-gather every rank's [n_w][k] top-k lists -> [world][n_w][k] (one collective per tensor)."""
+    rank, ws = world()
+    if ws == 1:
+        return out_idx[None], out_score[None], out_n[None]
+    gi = [torch.empty_like(out_idx) for _ in range(ws)]
+    gs = [torch.empty_like(out_score) for _ in range(ws)]
+    gn = [torch.empty_like(out_n) for _ in range(ws)]
+    dist.all_gather(gi, out_idx.contiguous(), group=group)
+    dist.all_gather(gs, out_score.contiguous(), group=group)
+    dist.all_gather(gn, out_n.contiguous(), group=group)
+    return torch.stack(gi), torch.stack(gs), torch.stack(gn)
+
+
+def make_allreduce(group=None):
+    """Sum an int64 tensor in place across ranks (the refit's histogram exchange)."""
+    def _ar(t: torch.Tensor):
+        assert t.dtype == torch.int64
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return _ar
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    rank, ws = world()
+    if ws == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, device=None) -> float:
+    rank, ws = world()
+    if ws == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
