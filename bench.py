@@ -215,10 +215,10 @@ def run_ours(args):
                 "avg_launch_ms": round(sa_avg, 4), "step_share": shares}
 
     # ---- scoring sweep: features_extract + gbt_predict on 2^20 candidates (HBM roofline of the feature stream)
-    sweep = scoring_sweep(space, model, dev, stream, peaks)
+    sweep = None if args.quick else scoring_sweep(space, model, dev, stream, peaks)
 
     # ---- e2e: same step through the public API with host buffers (pinned) and copies in the timed region
-    e2e = run_e2e(args, step, chain_idx, measured, cost, d_idx, dev, stream, world)
+    e2e = None if args.quick else run_e2e(args, step, chain_idx, measured, cost, d_idx, dev, stream, world)
 
     clocks = clk.summary()
     out = {
@@ -230,7 +230,7 @@ def run_ours(args):
         "roofline": roofline, "scoring_sweep": sweep, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
         "kernel_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):
         out["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -398,6 +398,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="timed steps only (no sweep / e2e / cpu baseline): for ncu")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

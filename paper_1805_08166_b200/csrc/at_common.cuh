@@ -174,9 +174,10 @@ struct at_space_s {
 
 struct at_gbt_s {
     int32_t n_trees, depth, n_features;
+    int32_t t_pad;                // allocation padded to a multiple of 16 trees (zero-filled), for bulk copies
     float base;
-    uint2 *d_nodes;               // [T][2^D-1] {feature, threshold bits}
-    float *d_leaf;                // [T][2^D]
+    uint2 *d_nodes;               // [t_pad][2^D-1] {feature, threshold bits}
+    float *d_leaf;                // [t_pad][2^D]
 };
 
 namespace at {

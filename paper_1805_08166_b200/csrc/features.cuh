@@ -55,11 +55,21 @@ __device__ __forceinline__ void decode_knobs(const WlDev &W, uint32_t local, uin
     }
 }
 
-// Compute all 468 features of the loop nest given by knob choices `ch`.
-// Sink: put(int f, float v) for every column (static f after unrolling except relation).
+// Compute the 468 features of the loop nest given by knob choices `ch`.
+// Sink: put(int f, float v) / put_rel(int f, float v).
+// Work split (part, nparts): nparts == 1 computes everything; otherwise part b < 3 owns the
+// relation features (and footprint) of buffer b, and the loop rows are dealt round-robin to
+// parts 3 .. nparts-1 (to parts 0 .. nparts-1 when nparts < 4).  The cheap running products
+// are recomputed by every part; the expensive per-row work and the stores are not.
+__host__ __device__ __forceinline__ int row_owner(int k, int nparts)
+{
+    return nparts >= 4 ? 3 + k % (nparts - 3) : k % nparts;
+}
+
 template <int TMPL, class Sink>
 __device__ __forceinline__ void features_one(const WlDev &W, const uint16_t *__restrict__ fact,
-                                             const uint32_t *ch, Sink &sk)
+                                             const uint32_t *ch, Sink &sk, int part = 0, int nparts = 1,
+                                             bool rows_only = false)
 {
     constexpr int NL = Tmpl<TMPL>::NL;
     constexpr int NA = Tmpl<TMPL>::NA;
@@ -156,6 +166,11 @@ __device__ __forceinline__ void features_one(const WlDev &W, const uint16_t *__r
 #pragma unroll
         for (int q = 0; q < NA; ++q) if (a == q) A[q] *= ext[k];
         bu *= ext[k];
+        const bool own_row = nparts == 1 || part == (rows_only ? k % nparts : row_owner(k, nparts));
+        bool own_rel[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) own_rel[b] = !rows_only && (nparts == 1 || part == b % nparts);
+        if (!own_row && !own_rel[0] && !own_rel[1] && !own_rel[2]) continue;
         uint32_t T[3];
         uint32_t st[3];
         if (TMPL == 0) {
@@ -199,6 +214,7 @@ __device__ __forceinline__ void features_one(const WlDev &W, const uint16_t *__r
         // relation emission (before loop k joins the qualifying suffix)
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
+            if (!own_rel[b]) continue;
             while (tnext[b] <= 20 && (T[b] >> tnext[b]) != 0u) {
                 sk.put_rel(342 + 40 * b + tnext[b] - 1, has[b] ? smax_r[b] : 0.f);
                 sk.put_rel(362 + 40 * b + tnext[b] - 1, has[b] ? smax_t[b] : 0.f);
@@ -208,6 +224,7 @@ __device__ __forceinline__ void features_one(const WlDev &W, const uint16_t *__r
             smax_t[b] = has[b] ? fmaxf(smax_t[b], ftd) : ftd;
             has[b] = true;
         }
+        if (!own_row) continue;
         // the 19 context columns of row k
         const int base = 19 * k;
         sk.put(base + 0, __uint2float_rn(ext[k]));
@@ -230,12 +247,37 @@ __device__ __forceinline__ void features_one(const WlDev &W, const uint16_t *__r
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
+        if (rows_only || !(nparts == 1 || part == b % nparts)) continue;
         while (tnext[b] <= 20) {
             sk.put_rel(342 + 40 * b + tnext[b] - 1, smax_r[b]);
             sk.put_rel(362 + 40 * b + tnext[b] - 1, smax_t[b]);
             ++tnext[b];
         }
     }
+}
+
+// Relation features of buffer b, pair p (0: reuse, 1: top-down) from context rows already in a
+// smem tile [f][32] (rows_only pass).  The integer touch count is read back as its fp32
+// conversion: for thresholds 2^t <= 2^20 < 2^24 the comparison is exact (RN is monotone and
+// 2^t is representable), so this equals the integer test of the one-pass version.
+__device__ __forceinline__ void relation_from_tile(float *tile, int lane, int NL, int b, int p)
+{
+    const int colT = 10 + 3 * b, colZ = p == 0 ? 11 + 3 * b : 8;
+    const int out = 342 + 40 * b + 20 * p - 1;
+    float smax = 0.0f;
+    bool has = false;
+    int tnext = 1;
+    for (int k = NL - 1; k >= 0; --k) {
+        const float T = tile[(19 * k + colT) * 32 + lane];
+        const float z = tile[(19 * k + colZ) * 32 + lane];
+        while (tnext <= 20 && T >= __int_as_float((127 + tnext) << 23)) {
+            tile[(out + tnext) * 32 + lane] = has ? smax : 0.0f;
+            ++tnext;
+        }
+        smax = has ? fmaxf(smax, z) : z;
+        has = true;
+    }
+    for (; tnext <= 20; ++tnext) tile[(out + tnext) * 32 + lane] = has ? smax : 0.0f;
 }
 
 // columns that are zero for every candidate of a template (absent loop rows + padding)

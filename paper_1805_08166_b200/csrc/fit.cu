@@ -14,6 +14,7 @@
 //      (shared-memory atomics, one block per feature), all-reduce, fp64 split search
 //      (one block per node), partition of every sample; leaves -eta G / (H + lambda);
 //      fp32 prediction update in tree order.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -223,7 +224,7 @@ __global__ void positions_kernel(const uint16_t *__restrict__ key, const int32_t
     member[woff[k] + y] = (int32_t)i;
 }
 
-__global__ void __launch_bounds__(256) grads_kernel(const int32_t *__restrict__ member,
+__global__ void __launch_bounds__(128) grads_kernel(const int32_t *__restrict__ member,
                                                     const int32_t *__restrict__ counts,
                                                     const int32_t *__restrict__ woff,
                                                     const int32_t *__restrict__ gprefix, int group_size,
@@ -231,99 +232,159 @@ __global__ void __launch_bounds__(256) grads_kernel(const int32_t *__restrict__ 
                                                     int64_t *__restrict__ g, int64_t *__restrict__ h)
 {
     extern __shared__ unsigned char smraw[];
-    int64_t *sg = (int64_t *)smraw;
-    int64_t *sh = sg + group_size;
-    float *sc = (float *)(sh + group_size);
+    float *sc = (float *)smraw;
     float *sp = sc + group_size;
-    int32_t *si = (int32_t *)(sp + group_size);
     __shared__ int s_w;
     const int b = blockIdx.x;
-    if (b >= gprefix[FIT_MAXKEYS]) return;
     if (threadIdx.x == 0) {
         int lo = 0, hi = FIT_MAXKEYS;   // largest w with gprefix[w] <= b
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if (gprefix[mid] <= b) lo = mid; else hi = mid;
         }
-        while (lo + 1 <= FIT_MAXKEYS && gprefix[lo + 1] <= b) ++lo;
         s_w = lo;
     }
     __syncthreads();
     const int w = s_w;
-    const int gi = b - gprefix[w];
-    const int start = gi * group_size;
+    const int start = (b - gprefix[w]) * group_size;
     int m = counts[w] - start;
     if (m > group_size) m = group_size;
+    const int32_t *mem = member + woff[w] + start;
     for (int a = threadIdx.x; a < m; a += blockDim.x) {
-        const int i = member[woff[w] + start + a];
-        si[a] = i;
+        const int i = mem[a];
         sc[a] = cost[i];
         sp[a] = pred[i];
-        sg[a] = 0;
-        sh[a] = 0;
     }
     __syncthreads();
-    const int npairs = m * (m - 1) / 2;
-    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-        // unordered pair (a, c), a < c, from the linear pair index
-        int a = 0, rem = p;
-        while (rem >= m - 1 - a) { rem -= m - 1 - a; ++a; }
-        int c = a + 1 + rem;
-        if (sc[a] == sc[c]) continue;                 // sign(c_i - c_j) = 0
-        if (sc[a] < sc[c]) { const int t = a; a = c; c = t; }   // now cost[a] > cost[c]
-        const float d = __fsub_rn(sp[c], sp[a]);
-        const float e = exp_det(-d);
-        const float rho = __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
-        const float hh = __fmul_rn(rho, __fsub_rn(1.0f, rho));
-        const long long q = __double2ll_rn((double)rho * 4294967296.0);
-        const long long qh = __double2ll_rn((double)hh * 4294967296.0);
-        atomicAdd((unsigned long long *)&sg[a], (unsigned long long)(-2 * q));
-        atomicAdd((unsigned long long *)&sg[c], (unsigned long long)(2 * q));
-        atomicAdd((unsigned long long *)&sh[a], (unsigned long long)(2 * qh));
-        atomicAdd((unsigned long long *)&sh[c], (unsigned long long)(2 * qh));
-    }
-    __syncthreads();
+    // thread a accumulates member a's share of every pair it is in (no atomics; each pair's
+    // rho is computed identically by both of its members)
     for (int a = threadIdx.x; a < m; a += blockDim.x) {
-        g[si[a]] = sg[a];
-        h[si[a]] = sh[a];
+        long long ga = 0, ha = 0;
+        const float ca = sc[a], fa = sp[a];
+        for (int c = 0; c < m; ++c) {
+            const float cc = sc[c];
+            if (c == a || cc == ca) continue;   // sign(c_i - c_j) = 0 contributes nothing
+            const bool hi = ca > cc;            // a is the slower (i) of the pair
+            const float fi = hi ? fa : sp[c], fj = hi ? sp[c] : fa;
+            const float d = __fsub_rn(fj, fi);
+            const float e = exp_det(-d);
+            const float rho = __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
+            const float hh = __fmul_rn(rho, __fsub_rn(1.0f, rho));
+            const long long q = __double2ll_rn((double)rho * 4294967296.0);
+            const long long qh = __double2ll_rn((double)hh * 4294967296.0);
+            ga += hi ? -2 * q : 2 * q;          // both orders of Eq. 2 carry the same term
+            ha += 2 * qh;
+        }
+        g[mem[a]] = ga;
+        h[mem[a]] = ha;
     }
 }
 
 // ------------------------------------------------------------------ 3. levels
-template <bool SMEM>
-__global__ void __launch_bounds__(512) hist_kernel(const uint8_t *__restrict__ bins, const int32_t *__restrict__ node,
+// Histograms use a compact bin layout: feature f owns nb_f = ncuts_f + 1 cells starting at
+// boff[f]; a level's buffer is hist[node][TB][2] int64 (TB = sum_f nb_f).
+__global__ void bin_layout_kernel(const int32_t *__restrict__ ncuts, int F, int32_t *__restrict__ boff,
+                                  int32_t *__restrict__ info /* [0] TB, [1] max nb */)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int32_t o = 0, mx = 0;
+    for (int f = 0; f < F; ++f) {
+        boff[f] = o;
+        const int32_t nb = ncuts[f] + 1;
+        o += nb;
+        mx = nb > mx ? nb : mx;
+    }
+    boff[F] = o;
+    info[0] = o;
+    info[1] = mx;
+}
+
+// Warp-aggregated exact int64 histogram update.  64-bit shared-memory atomics are CAS loops on
+// sm_100a, so lanes hitting the same cell are first combined: peers = match_any(key); every
+// lane sums its group's int64 values by walking the group's lanes with full-warp shuffles
+// (trip count = the largest group, warp-uniform); the group's lowest lane does one atomic.
+__device__ __forceinline__ void agg_add(unsigned long long *cells, int key, long long gv, long long hv)
+{
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+    const int lane = threadIdx.x & 31;
+    const int maxg = (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)__popc(peers));
+    long long sg = 0, sh = 0;
+    unsigned m = peers;
+    for (int k = 0; k < maxg; ++k) {
+        const int src = m ? __ffs(m) - 1 : lane;
+        const long long vg = __shfl_sync(0xFFFFFFFFu, gv, src);
+        const long long vh = __shfl_sync(0xFFFFFFFFu, hv, src);
+        if (m) {
+            sg += vg;
+            sh += vh;
+            m &= m - 1;
+        }
+    }
+    if (key >= 0 && lane == __ffs(peers) - 1) {
+        atomicAdd(&cells[2 * key], (unsigned long long)sg);
+        atomicAdd(&cells[2 * key + 1], (unsigned long long)sh);
+    }
+}
+
+// grid (F, n_chunks): block (f, c) accumulates its sample chunk of the rank's slice for all nodes of
+// the level in shared memory, then stores (1 chunk) or atomically adds (several chunks) into hist.
+__global__ void __launch_bounds__(256) hist_kernel(const uint8_t *__restrict__ bins, const int32_t *__restrict__ node,
                                                    const int64_t *__restrict__ g, const int64_t *__restrict__ h,
-                                                   int64_t hb, int64_t he, int64_t n, int F, int B, int first, int nn,
-                                                   int64_t *__restrict__ hist)
+                                                   int64_t hb, int64_t he, int64_t n, int64_t chunk,
+                                                   const int32_t *__restrict__ boff, int TB, int first, int nn,
+                                                   int use_smem, int64_t *__restrict__ hist)
 {
     extern __shared__ unsigned long long shist[];
     const int f = blockIdx.x;
-    const int64_t cells = (int64_t)nn * B * 2;
-    if (SMEM) {
+    const int nb = boff[f + 1] - boff[f];
+    const int64_t cells = (int64_t)nn * nb * 2;
+    const int64_t i0 = hb + (int64_t)blockIdx.y * chunk;
+    int64_t i1 = i0 + chunk;
+    if (i1 > he) i1 = he;
+    const bool single = gridDim.y == 1;
+    if (use_smem) {
         for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) shist[q] = 0ull;
         __syncthreads();
     }
     const uint8_t *bf = bins + (int64_t)f * n;
-    for (int64_t i = hb + threadIdx.x; i < he; i += blockDim.x) {
-        const int nd = node[i] - first;
-        const int b = bf[i];
-        const unsigned long long gv = (unsigned long long)g[i], hv = (unsigned long long)h[i];
-        if (SMEM) {
-            atomicAdd(&shist[((int64_t)nd * B + b) * 2], gv);
-            atomicAdd(&shist[((int64_t)nd * B + b) * 2 + 1], hv);
+    for (int64_t i0w = i0; i0w < i1; i0w += blockDim.x) {
+        const int64_t i = i0w + threadIdx.x;
+        const bool ok = i < i1;
+        const int key = ok ? (node[i] - first) * nb + bf[i] : -1;
+        const long long gv = ok ? g[i] : 0, hv = ok ? h[i] : 0;
+        if (use_smem) {
+            agg_add(shist, key, gv, hv);
         } else {
-            int64_t *cell = hist + (((int64_t)nd * F + f) * B + b) * 2;
-            atomicAdd((unsigned long long *)cell, gv);
-            atomicAdd((unsigned long long *)cell + 1, hv);
+            // global cells of this feature: [node][TB] with stride TB, offset boff[f]
+            const int nd = ok ? node[i] - first : 0;
+            if (ok) {
+                unsigned long long *cell = (unsigned long long *)(hist + ((int64_t)nd * TB + boff[f] + bf[i]) * 2);
+                atomicAdd(cell, (unsigned long long)gv);
+                atomicAdd(cell + 1, (unsigned long long)hv);
+            }
         }
     }
-    if (SMEM) {
+    if (use_smem) {
         __syncthreads();
         for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) {
-            const int64_t nd = q / (2 * B), rem = q - nd * 2 * B;
-            hist[(nd * F + f) * B * 2 + rem] = (int64_t)shist[q];
+            const int64_t nd = q / (2 * nb), rem = q - nd * 2 * nb;
+            int64_t *dst = hist + (nd * TB + boff[f]) * 2 + rem;
+            if (single) *dst = (int64_t)shist[q];
+            else if (shist[q]) atomicAdd((unsigned long long *)dst, shist[q]);
         }
     }
+}
+
+// tree 0 root histogram back to the dense [F][B][2] layout (parity hook)
+__global__ void hist0_expand_kernel(const int64_t *__restrict__ hist, const int32_t *__restrict__ boff, int F, int B,
+                                    int64_t *__restrict__ out)
+{
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (int64_t)F * B) return;
+    const int f = (int)(q / B), b = (int)(q - (int64_t)f * B);
+    const int nb = boff[f + 1] - boff[f];
+    out[2 * q] = b < nb ? hist[(int64_t)(boff[f] + b) * 2] : 0;
+    out[2 * q + 1] = b < nb ? hist[(int64_t)(boff[f] + b) * 2 + 1] : 0;
 }
 
 struct SplitBest {
@@ -331,65 +392,18 @@ struct SplitBest {
     int f, s;
 };
 
+// a before b in (gain desc, f asc, s asc); f < 0 = no split
 __device__ __forceinline__ bool split_better(const SplitBest &a, const SplitBest &b)
 {
     if (a.f < 0) return false;
     if (b.f < 0) return true;
     if (a.gain != b.gain) return a.gain > b.gain;
-    return a.f < b.f;
+    if (a.f != b.f) return a.f < b.f;
+    return a.s < b.s;
 }
 
-__global__ void __launch_bounds__(256) split_kernel(const int64_t *__restrict__ hist, int F, int B, int first,
-                                                    const float *__restrict__ cuts, const int32_t *__restrict__ ncuts,
-                                                    double lam, double mcw, uint8_t *__restrict__ dead,
-                                                    int32_t *__restrict__ split_f, int32_t *__restrict__ split_s,
-                                                    uint16_t *__restrict__ tree_feat, float *__restrict__ tree_thr)
+__device__ __forceinline__ SplitBest warp_best(SplitBest best)
 {
-    __shared__ long long s_sum[2][8];
-    __shared__ SplitBest s_best[8];
-    const int q = blockIdx.x, nd = first + q;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (dead[nd]) {
-        if (tid == 0) {
-            tree_feat[nd] = 0;
-            tree_thr[nd] = __int_as_float(0x7f800000);
-            split_f[nd] = -1;
-            dead[2 * nd + 1] = 1;
-            dead[2 * nd + 2] = 1;
-        }
-        return;
-    }
-    const int64_t *hn = hist + (int64_t)q * F * B * 2;
-    // node totals from feature 0 (every sample sits in exactly one of its bins)
-    long long G0 = 0, H0 = 0;
-    for (int b = tid; b < B; b += 256) { G0 += hn[2 * b]; H0 += hn[2 * b + 1]; }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-        G0 += __shfl_xor_sync(0xFFFFFFFFu, G0, off);
-        H0 += __shfl_xor_sync(0xFFFFFFFFu, H0, off);
-    }
-    if (lane == 0) { s_sum[0][warp] = G0; s_sum[1][warp] = H0; }
-    __syncthreads();
-    long long Gi = 0, Hi = 0;
-    for (int w = 0; w < 8; ++w) { Gi += s_sum[0][w]; Hi += s_sum[1][w]; }
-    const double G = (double)Gi * FX, H = (double)Hi * FX;
-    const double parent = G * G / (H + lam);
-    SplitBest best{0.0, -1, 0};
-    for (int f = tid; f < F; f += 256) {
-        const int64_t *hf = hn + (int64_t)f * B * 2;
-        const int nc = ncuts[f];
-        long long GLi = 0, HLi = 0;
-        for (int s = 1; s <= nc; ++s) {
-            GLi += hf[2 * (s - 1)];
-            HLi += hf[2 * (s - 1) + 1];
-            const double GL = (double)GLi * FX, HL = (double)HLi * FX;
-            const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
-            if (HL < mcw || HR < mcw) continue;
-            const double gain = (GL * GL / (HL + lam) + GR * GR / (HR + lam)) - parent;
-            if (!(gain > 0.0)) continue;
-            if (best.f < 0 || gain > best.gain) { best.gain = gain; best.f = f; best.s = s; }
-        }
-    }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
         SplitBest o;
@@ -398,6 +412,176 @@ __global__ void __launch_bounds__(256) split_kernel(const int64_t *__restrict__ 
         o.s = __shfl_xor_sync(0xFFFFFFFFu, best.s, off);
         if (split_better(o, best)) best = o;
     }
+    return best;
+}
+
+// single-rank fast path: block f builds the level's histograms of feature f in shared memory
+// and immediately scans its splits for every node (warp per node), so the level's histograms
+// never touch HBM.  Same arithmetic as hist_kernel + split_feature_kernel.
+__global__ void __launch_bounds__(256) hist_split_kernel(const uint8_t *__restrict__ bins,
+                                                         const int32_t *__restrict__ node,
+                                                         const int64_t *__restrict__ g, const int64_t *__restrict__ h,
+                                                         int64_t n, const int32_t *__restrict__ boff, int F, int first,
+                                                         int nn, double lam, double mcw,
+                                                         const uint8_t *__restrict__ dead,
+                                                         double *__restrict__ best_gain, int32_t *__restrict__ best_s,
+                                                         int64_t *__restrict__ hist0)
+{
+    extern __shared__ unsigned long long shist[];
+    const int f = blockIdx.x;
+    const int nb = boff[f + 1] - boff[f];
+    const int64_t cells = (int64_t)nn * nb * 2;
+    for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) shist[q] = 0ull;
+    __syncthreads();
+    const uint8_t *bf = bins + (int64_t)f * n;
+    for (int64_t i0w = 0; i0w < n; i0w += blockDim.x) {
+        const int64_t i = i0w + threadIdx.x;
+        const bool ok = i < n;
+        const int key = ok ? (node[i] - first) * nb + bf[i] : -1;
+        agg_add(shist, key, ok ? g[i] : 0, ok ? h[i] : 0);
+    }
+    __syncthreads();
+    if (hist0)
+        for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) hist0[(int64_t)boff[f] * 2 + q] = (int64_t)shist[q];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nc = nb - 1;
+    for (int q = warp; q < nn; q += blockDim.x >> 5) {
+        const int nd = first + q;
+        if (dead[nd]) {
+            if (lane == 0) best_s[(int64_t)q * F + f] = 0;
+            continue;
+        }
+        const unsigned long long *hf = shist + (int64_t)q * nb * 2;
+        // node totals: every feature's bins partition the node's samples
+        long long Gi = 0, Hi = 0;
+        for (int b = lane; b < nb; b += 32) { Gi += (long long)hf[2 * b]; Hi += (long long)hf[2 * b + 1]; }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            Gi += __shfl_xor_sync(0xFFFFFFFFu, Gi, off);
+            Hi += __shfl_xor_sync(0xFFFFFFFFu, Hi, off);
+        }
+        const double G = (double)Gi * FX, H = (double)Hi * FX;
+        const double parent = G * G / (H + lam);
+        SplitBest best{0.0, -1, 0};
+        long long carryG = 0, carryH = 0;
+        for (int c0 = 0; c0 < nc; c0 += 32) {
+            const int b = c0 + lane;
+            long long vg = b < nc ? (long long)hf[2 * b] : 0, vh = b < nc ? (long long)hf[2 * b + 1] : 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const long long yg = __shfl_up_sync(0xFFFFFFFFu, vg, off);
+                const long long yh = __shfl_up_sync(0xFFFFFFFFu, vh, off);
+                if (lane >= off) { vg += yg; vh += yh; }
+            }
+            const long long GLi = carryG + vg, HLi = carryH + vh;
+            carryG += __shfl_sync(0xFFFFFFFFu, vg, 31);
+            carryH += __shfl_sync(0xFFFFFFFFu, vh, 31);
+            if (b < nc) {
+                const double GL = (double)GLi * FX, HL = (double)HLi * FX;
+                const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
+                if (!(HL < mcw || HR < mcw)) {
+                    const double gain = (GL * GL / (HL + lam) + GR * GR / (HR + lam)) - parent;
+                    if (gain > 0.0) {
+                        SplitBest cnd{gain, f, b + 1};
+                        if (split_better(cnd, best)) best = cnd;
+                    }
+                }
+            }
+        }
+        best = warp_best(best);
+        if (lane == 0) {
+            best_gain[(int64_t)q * F + f] = best.gain;
+            best_s[(int64_t)q * F + f] = best.f < 0 ? 0 : best.s;
+        }
+    }
+}
+
+// one warp per (node, feature): prefix sums over the feature's bins by warp scans (exact int64),
+// every split s = 1..ncuts_f evaluated in fp64 in the oracle's operation order.
+__global__ void __launch_bounds__(256) split_feature_kernel(const int64_t *__restrict__ hist,
+                                                            const int32_t *__restrict__ boff, int TB, int F, int first,
+                                                            int nn, double lam, double mcw,
+                                                            const uint8_t *__restrict__ dead,
+                                                            double *__restrict__ best_gain, int32_t *__restrict__ best_s)
+{
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (gw >= nn * F) return;
+    const int q = gw / F, f = gw - q * F;
+    const int nd = first + q;
+    if (dead[nd]) {
+        if (lane == 0) best_s[(int64_t)q * F + f] = 0;
+        return;
+    }
+    const int64_t *hn = hist + (int64_t)q * TB * 2;
+    // node totals from feature 0 (every sample is in exactly one of its bins)
+    long long Gi = 0, Hi = 0;
+    const int nb0 = boff[1] - boff[0];
+    for (int b = lane; b < nb0; b += 32) { Gi += hn[2 * b]; Hi += hn[2 * b + 1]; }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        Gi += __shfl_xor_sync(0xFFFFFFFFu, Gi, off);
+        Hi += __shfl_xor_sync(0xFFFFFFFFu, Hi, off);
+    }
+    const double G = (double)Gi * FX, H = (double)Hi * FX;
+    const double parent = G * G / (H + lam);
+    const int64_t *hf = hn + (int64_t)boff[f] * 2;
+    const int nc = boff[f + 1] - boff[f] - 1;   // ncuts_f
+    SplitBest best{0.0, -1, 0};
+    long long carryG = 0, carryH = 0;
+    for (int c0 = 0; c0 < nc; c0 += 32) {
+        const int b = c0 + lane;                 // split s = b + 1 puts bins <= b on the left
+        long long vg = b < nc ? hf[2 * b] : 0, vh = b < nc ? hf[2 * b + 1] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long yg = __shfl_up_sync(0xFFFFFFFFu, vg, off);
+            const long long yh = __shfl_up_sync(0xFFFFFFFFu, vh, off);
+            if (lane >= off) { vg += yg; vh += yh; }
+        }
+        const long long GLi = carryG + vg, HLi = carryH + vh;
+        carryG += __shfl_sync(0xFFFFFFFFu, vg, 31);
+        carryH += __shfl_sync(0xFFFFFFFFu, vh, 31);
+        if (b < nc) {
+            const double GL = (double)GLi * FX, HL = (double)HLi * FX;
+            const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
+            if (!(HL < mcw || HR < mcw)) {
+                const double gain = (GL * GL / (HL + lam) + GR * GR / (HR + lam)) - parent;
+                if (gain > 0.0) {
+                    SplitBest c{gain, f, b + 1};
+                    if (split_better(c, best)) best = c;
+                }
+            }
+        }
+    }
+    best = warp_best(best);
+    if (lane == 0) {
+        best_gain[(int64_t)q * F + f] = best.gain;
+        best_s[(int64_t)q * F + f] = best.f < 0 ? 0 : best.s;
+    }
+}
+
+// one block per node: best over features (gain desc, feature asc), write the tree node
+__global__ void __launch_bounds__(256) split_node_kernel(const double *__restrict__ best_gain,
+                                                         const int32_t *__restrict__ best_s, int F, int first,
+                                                         const float *__restrict__ cuts, int B,
+                                                         uint8_t *__restrict__ dead, int32_t *__restrict__ split_f,
+                                                         int32_t *__restrict__ split_s,
+                                                         uint16_t *__restrict__ tree_feat, float *__restrict__ tree_thr)
+{
+    __shared__ SplitBest s_best[8];
+    const int q = blockIdx.x, nd = first + q;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    SplitBest best{0.0, -1, 0};
+    if (!dead[nd]) {
+        for (int f = tid; f < F; f += 256) {
+            const int s = best_s[(int64_t)q * F + f];
+            if (s > 0) {
+                SplitBest c{best_gain[(int64_t)q * F + f], f, s};
+                if (split_better(c, best)) best = c;
+            }
+        }
+    }
+    best = warp_best(best);
     if (lane == 0) s_best[warp] = best;
     __syncthreads();
     if (tid == 0) {
@@ -405,6 +589,7 @@ __global__ void __launch_bounds__(256) split_kernel(const int64_t *__restrict__ 
         for (int w = 1; w < 8; ++w)
             if (split_better(s_best[w], b)) b = s_best[w];
         if (b.f < 0) {
+            // no valid split (or a dead node): pass-through, every sample goes left
             tree_feat[nd] = 0;
             tree_thr[nd] = __int_as_float(0x7f800000);
             split_f[nd] = -1;
@@ -467,13 +652,13 @@ __global__ void pack_nodes_kernel(const uint16_t *__restrict__ feat, const float
     nodes[i] = make_uint2(feat[i], __float_as_uint(thr[i]));
 }
 
-__global__ void finite_check_kernel(const float *__restrict__ c, int64_t n, int *__restrict__ bad)
+__global__ void finite_check_kernel(const float *__restrict__ c, int64_t n, int32_t *__restrict__ bad)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n && !isfinite(c[i])) *bad = 1;
 }
 
-__global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int *__restrict__ bad)
+__global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int32_t *__restrict__ bad)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n && k[i] >= FIT_MAXKEYS) *bad = 2;
@@ -530,11 +715,12 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
 
     Ws ws;
     ws.s = s;
-    int *d_bad = ws.get<int>(1);
+    int32_t *d_info = ws.get<int32_t>(8);
     uint32_t *sortA = ws.get<uint32_t>((size_t)F * n);
     uint32_t *sortB = ws.get<uint32_t>((size_t)F * n);
     float *cuts = ws.get<float>((size_t)F * (B - 1));
     int32_t *ncuts = ws.get<int32_t>(F);
+    int32_t *boff = ws.get<int32_t>(F + 1);
     uint8_t *bins = ws.get<uint8_t>((size_t)F * n);
     int32_t *rank = ws.get<int32_t>(n);
     int32_t *counts = ws.get<int32_t>(FIT_MAXKEYS);
@@ -546,46 +732,58 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     float *pred = ws.get<float>(n);
     int32_t *node = ws.get<int32_t>(n);
     const int max_nn = 1 << (D - 1);
-    int64_t *hist = ws.get<int64_t>((size_t)max_nn * F * B * 2);
     int64_t *lsum = ws.get<int64_t>((size_t)n_leaf * 2);
     uint8_t *dead = ws.get<uint8_t>(n_int + n_leaf);
     int32_t *split_f = ws.get<int32_t>(n_int);
     int32_t *split_s = ws.get<int32_t>(n_int);
+    double *best_gain = ws.get<double>((size_t)max_nn * F);
+    int32_t *best_s = ws.get<int32_t>((size_t)max_nn * F);
     uint16_t *t_feat = ws.get<uint16_t>((size_t)o->n_trees * n_int);
     float *t_thr = ws.get<float>((size_t)o->n_trees * n_int);
     float *t_leaf = ws.get<float>((size_t)o->n_trees * n_leaf);
     if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
 
-    // input checks (one sync): finite costs, group keys < 1024
-    {
-        int bad = 0;
-        AT_CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-        finite_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, n, d_bad);
-        key_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, n, d_bad);
-        AT_LAUNCH_CHECK("fit input checks");
-        AT_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        AT_CUDA_TRY(cudaStreamSynchronize(s));
-        if (bad == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
-        if (bad == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
-    }
+    // input checks + cuts + groups; one host sync reads back the sizes the launches need
+    int info[8] = {0};
     {
         ProfScope ps(AT_K_FIT_PREP, s);
+        AT_CUDA_TRY(cudaMemsetAsync(d_info, 0, 8 * sizeof(int32_t), s));
+        finite_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, n, d_info + 2);
+        key_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, n, d_info + 2);
         sort_feature_kernel<<<F, 1024, 0, s>>>(d_feat, ld, n, sortA, sortB);
         cuts_kernel<<<F, 1024, 0, s>>>(sortA, n, B, cuts, ncuts);
+        bin_layout_kernel<<<1, 32, 0, s>>>(ncuts, F, boff, d_info);
         bins_kernel<<<dim3(nblk(n, 256), F), 256, 0, s>>>(d_feat, ld, n, F, B, cuts, ncuts, bins);
         ranks_kernel<<<1, 1024, 0, s>>>(d_group_key, n, rank, counts, woff, gpre, GS);
+        AT_CUDA_TRY(cudaMemcpyAsync(d_info + 3, gpre + FIT_MAXKEYS, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         AT_CUDA_TRY(cudaMemsetAsync(pred, 0, sizeof(float) * n, s));
         AT_LAUNCH_CHECK("fit prep");
+        AT_CUDA_TRY(cudaMemcpyAsync(info, d_info, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        AT_CUDA_TRY(cudaStreamSynchronize(s));
     }
-    const size_t grad_smem = (size_t)GS * (2 * sizeof(int64_t) + 2 * sizeof(float) + sizeof(int32_t));
-    const unsigned grad_blocks = nblk(n, GS) + FIT_MAXKEYS;
+    if (info[2] == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
+    if (info[2] == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
+    const int TB = info[0], max_nb = info[1], n_groups = info[3];
+    int64_t *hist = ws.get<int64_t>((size_t)max_nn * TB * 2);
+    if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: histogram allocation failed");
+
+    const size_t grad_smem = (size_t)GS * 2 * sizeof(float);
+    const int64_t ns = he - hb;
+    const int64_t n_chunks = ns <= 4096 ? 1 : std::min<int64_t>((ns + 4095) / 4096, 64);
+    const int64_t chunk = n_chunks ? (ns + n_chunks - 1) / n_chunks : 0;
     static size_t hist_attr = 0;
+    if (hist_attr == 0) {
+        AT_CUDA_TRY(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        AT_CUDA_TRY(cudaFuncSetAttribute(hist_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        hist_attr = 160 * 1024;
+    }
     for (int t = 0; t < o->n_trees; ++t) {
         {
             ProfScope ps(AT_K_FIT_GRAD, s);
             positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, (uint32_t)t,
                                                           member);
-            grads_kernel<<<grad_blocks, 256, grad_smem, s>>>(member, counts, woff, gpre, GS, d_cost, pred, g, h);
+            if (n_groups > 0)
+                grads_kernel<<<n_groups, 128, grad_smem, s>>>(member, counts, woff, gpre, GS, d_cost, pred, g, h);
             AT_LAUNCH_CHECK("fit gradients");
         }
         AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
@@ -594,33 +792,40 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         float *tt = t_thr + (size_t)t * n_int;
         for (int d = 0; d < D; ++d) {
             const int first = (1 << d) - 1, nn = 1 << d;
-            const size_t cells = (size_t)nn * B * 2;
-            const size_t smem = cells * sizeof(int64_t);
-            {
+            const size_t cells = (size_t)nn * TB * 2;
+            const size_t smem = (size_t)nn * max_nb * 2 * sizeof(int64_t);
+            const int use_smem = smem <= 160 * 1024;
+            const bool want_h0 = t == 0 && d == 0 && o->d_hist0_out;
+            if (!o->allreduce && use_smem) {
+                // single rank: histograms stay in shared memory, split scan fused
                 ProfScope ps(AT_K_FIT_HIST, s);
-                if (smem <= 160 * 1024) {
-                    if (smem > hist_attr) {
-                        AT_CUDA_TRY(cudaFuncSetAttribute(hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         160 * 1024));
-                        hist_attr = 160 * 1024;
-                    }
-                    hist_kernel<true><<<F, 512, smem, s>>>(bins, node, g, h, hb, he, n, F, B, first, nn, hist);
-                } else {
-                    AT_CUDA_TRY(cudaMemsetAsync(hist, 0, cells * F * sizeof(int64_t), s));
-                    hist_kernel<false><<<F, 512, 0, s>>>(bins, node, g, h, hb, he, n, F, B, first, nn, hist);
+                hist_split_kernel<<<F, 256, smem, s>>>(bins, node, g, h, n, boff, F, first, nn, lam, mcw,
+                                                       dead, best_gain, best_s, want_h0 ? hist : nullptr);
+                AT_LAUNCH_CHECK("hist_split_kernel");
+            } else {
+                {
+                    ProfScope ps(AT_K_FIT_HIST, s);
+                    if (n_chunks != 1 || !use_smem || ns == 0)
+                        AT_CUDA_TRY(cudaMemsetAsync(hist, 0, cells * sizeof(int64_t), s));
+                    if (ns > 0)
+                        hist_kernel<<<dim3(F, (unsigned)n_chunks), 256, use_smem ? smem : 0, s>>>(
+                            bins, node, g, h, hb, he, n, chunk, boff, TB, first, nn, use_smem, hist);
+                    AT_LAUNCH_CHECK("hist_kernel");
                 }
-                AT_LAUNCH_CHECK("hist_kernel");
+                if (o->allreduce) {
+                    const int rc = o->allreduce(hist, (int64_t)cells, o->ctx, stream);
+                    if (rc) return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
+                }
+                ProfScope ps(AT_K_FIT_SPLIT, s);
+                split_feature_kernel<<<nblk((int64_t)nn * F, 8), 256, 0, s>>>(hist, boff, TB, F, first, nn, lam, mcw,
+                                                                              dead, best_gain, best_s);
+                AT_LAUNCH_CHECK("split_feature_kernel");
             }
-            if (o->allreduce) {
-                const int rc = o->allreduce(hist, (int64_t)(cells * F), o->ctx, stream);
-                if (rc) return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
-            }
-            if (t == 0 && d == 0 && o->d_hist0_out)
-                AT_CUDA_TRY(cudaMemcpyAsync(o->d_hist0_out, hist, (size_t)F * B * 2 * sizeof(int64_t),
-                                            cudaMemcpyDeviceToDevice, s));
+            if (want_h0)
+                hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hist, boff, F, B, o->d_hist0_out);
             {
                 ProfScope ps(AT_K_FIT_SPLIT, s);
-                split_kernel<<<nn, 256, 0, s>>>(hist, F, B, first, cuts, ncuts, lam, mcw, dead, split_f, split_s, tf, tt);
+                split_node_kernel<<<nn, 256, 0, s>>>(best_gain, best_s, F, first, cuts, B, dead, split_f, split_s, tf, tt);
                 partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
                 AT_LAUNCH_CHECK("split/partition");
             }
@@ -648,14 +853,19 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     gm->n_trees = o->n_trees;
     gm->depth = D;
     gm->n_features = F;
+    gm->t_pad = (o->n_trees + 15) / 16 * 16;
     gm->base = 0.0f;
-    if (cudaMalloc(&gm->d_nodes, sizeof(uint2) * (size_t)o->n_trees * n_int) != cudaSuccess ||
-        cudaMalloc(&gm->d_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf) != cudaSuccess) {
+    gm->d_nodes = nullptr;
+    gm->d_leaf = nullptr;
+    if (cudaMalloc(&gm->d_nodes, sizeof(uint2) * (size_t)gm->t_pad * n_int) != cudaSuccess ||
+        cudaMalloc(&gm->d_leaf, sizeof(float) * (size_t)gm->t_pad * n_leaf) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(gm->d_nodes);
         delete gm;
         return fail(AT_ENOMEM, "gbt_fit_hist: model allocation failed");
     }
+    AT_CUDA_TRY(cudaMemsetAsync(gm->d_nodes, 0, sizeof(uint2) * (size_t)gm->t_pad * n_int, s));
+    AT_CUDA_TRY(cudaMemsetAsync(gm->d_leaf, 0, sizeof(float) * (size_t)gm->t_pad * n_leaf, s));
     pack_nodes_kernel<<<nblk((int64_t)o->n_trees * n_int, 256), 256, 0, s>>>(t_feat, t_thr, (int64_t)o->n_trees * n_int,
                                                                              gm->d_nodes);
     AT_CUDA_TRY(cudaMemcpyAsync(gm->d_leaf, t_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf,

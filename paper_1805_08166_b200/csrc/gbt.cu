@@ -9,25 +9,53 @@ namespace at {
 
 constexpr int PRED_NW = 8;   // warps per block (tree slices); 32 candidates per block
 
-__global__ void __launch_bounds__(PRED_NW * 32) predict_kernel(const uint2 *__restrict__ nodes,
-                                                              const float *__restrict__ leaf, int T, int D,
-                                                              float base, int F, const float *__restrict__ X,
-                                                              int64_t n, int64_t ld, float *__restrict__ score,
-                                                              uint8_t *__restrict__ slots)
+TreeGeo make_geo(const at_gbt_s *g)
 {
-    extern __shared__ float sm[];
-    float *tile = sm;             // [F][32]
-    float *part = sm + F * 32;    // [32][32]
+    TreeGeo G{};
+    G.nodes = g->d_nodes;
+    G.leaf = g->d_leaf;
+    G.T = g->n_trees;
+    G.T_pad = g->t_pad;
+    G.D = g->depth;
+    G.ni = (1 << g->depth) - 1;
+    G.nl = 1 << g->depth;
+    const uint32_t per_tree = (uint32_t)G.ni * 8u + (uint32_t)G.nl * 4u;
+    int ch = (int)(TREE_BUF_BYTES / per_tree) / 16 * 16;
+    if (ch < 16) ch = 16;
+    if (ch > G.T_pad) ch = G.T_pad;
+    G.CH = ch;
+    G.NC = (G.T + ch - 1) / ch;
+    G.chunk_bytes = (uint32_t)ch * per_tree;
+    G.resident = G.NC <= 2;
+    return G;
+}
+
+__global__ void __launch_bounds__(PRED_NW * 32) predict_kernel(TreeGeo G, float base, int F,
+                                                              const float *__restrict__ X, int64_t n, int64_t ld,
+                                                              float *__restrict__ score, uint8_t *__restrict__ slots)
+{
+    extern __shared__ __align__(128) unsigned char smraw[];
+    float *tile = (float *)smraw;                                   // [F][32]
+    float *part = tile + F * 32;                                    // [32][32]
+    uint64_t *bar = (uint64_t *)(part + 32 * 32);                   // [2]
+    uint8_t *bufs = (uint8_t *)(bar + 2) + 112;                     // 128-B aligned
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t c0 = (int64_t)blockIdx.x * 32;
-    const int64_t cand = c0 + lane;
+    const int64_t cand = (int64_t)blockIdx.x * 32 + lane;
     const bool ok = cand < n;
+    ts_start(G, bufs, bar);
     // stage the candidate tile: warp w loads rows w, w + NW, ... (one 128-B line per row)
     for (int f = warp; f < F; f += PRED_NW) tile[f * 32 + lane] = ok ? __ldcs(X + (int64_t)f * ld + cand) : 0.0f;
     __syncthreads();
-    gbt_walk_partials<PRED_NW>(nodes, leaf, T, D, tile, lane, warp, part, slots, n, cand, ok);
-    __syncthreads();
+    ts_wait_resident(G, bar);
+    uint32_t ph[2] = {0u, 0u};
+    uint64_t c = 0;
+    walk_pass<PRED_NW>(G, bufs, bar, ph, c, (uint64_t)G.NC, tile, lane, warp, part, slots, n, cand, ok);
     if (warp == 0 && ok) score[cand] = gbt_combine(part, lane, base);
+}
+
+size_t tree_smem_bytes(const TreeGeo &G)
+{
+    return (size_t)2 * G.chunk_bytes + 128;
 }
 
 }  // namespace at
@@ -53,11 +81,14 @@ int gbt_create(int32_t n_trees, int32_t depth, int32_t n_features, const uint16_
     g->n_trees = n_trees;
     g->depth = depth;
     g->n_features = n_features;
+    g->t_pad = (n_trees + 15) / 16 * 16;
     g->base = base;
     g->d_nodes = nullptr;
     g->d_leaf = nullptr;
-    if (cudaMalloc(&g->d_nodes, nodes.size() * sizeof(uint2)) != cudaSuccess ||
-        cudaMalloc(&g->d_leaf, (size_t)n_trees * nl * sizeof(float)) != cudaSuccess) {
+    if (cudaMalloc(&g->d_nodes, (size_t)g->t_pad * ni * sizeof(uint2)) != cudaSuccess ||
+        cudaMalloc(&g->d_leaf, (size_t)g->t_pad * nl * sizeof(float)) != cudaSuccess ||
+        cudaMemset(g->d_nodes, 0, (size_t)g->t_pad * ni * sizeof(uint2)) != cudaSuccess ||
+        cudaMemset(g->d_leaf, 0, (size_t)g->t_pad * nl * sizeof(float)) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(g->d_nodes);
         delete g;
@@ -119,7 +150,8 @@ int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_s
     if (!d_feat || !d_score) return at::fail(AT_EINVAL, "gbt_predict: null buffer");
     if (ld < n) return at::fail(AT_EMISMATCH, "gbt_predict: ld < n");
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t smem = ((size_t)g->n_features * 32 + 32 * 32) * sizeof(float);
+    const at::TreeGeo G = at::make_geo(g);
+    const size_t smem = ((size_t)g->n_features * 32 + 32 * 32) * sizeof(float) + 16 + at::tree_smem_bytes(G);
     if (smem > 227 * 1024) return at::fail(AT_EUNSUPPORTED, "gbt_predict: too many features for the smem tile");
     static size_t attr = 0;
     if (smem > attr) {
@@ -128,8 +160,7 @@ int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_s
     }
     const int64_t blocks = (n + 31) / 32;
     at::ProfScope ps(AT_K_PREDICT, s);
-    at::predict_kernel<<<(unsigned)blocks, at::PRED_NW * 32, smem, s>>>(g->d_nodes, g->d_leaf, g->n_trees, g->depth,
-                                                                       g->base, g->n_features, d_feat, n, ld,
+    at::predict_kernel<<<(unsigned)blocks, at::PRED_NW * 32, smem, s>>>(G, g->base, g->n_features, d_feat, n, ld,
                                                                        d_score, d_leaf_slot);
     AT_LAUNCH_CHECK("predict_kernel");
     return AT_OK;

@@ -1,61 +1,144 @@
-// gbt.cuh -- device-side GBT walk + canonical reduction (reading Q19), shared by
-// gbt_predict and sa_explore.
+// gbt.cuh -- device-side GBT walk + canonical reduction (reading Q19), shared by gbt_predict
+// and sa_explore.
 //
-// Layout: a block owns a tile of 32 candidates (lane = candidate) whose features sit
-// in shared memory as tile[f * 32 + lane] (bank = lane for every f: conflict-free
-// gathers whatever node each lane is at).  The block's NW warps split the trees by
-// residue class: warp w owns q = w, w + NW, ... (q = t mod 32), walks those NQ = 32/NW
-// trees of every 32-tree round together (NQ independent walks = ILP) and keeps the
-// partial sums p[q] in registers, adding leaves in ascending t exactly as the
-// canonical order prescribes.  The 32 partials of a candidate are then combined by
-// the xor butterfly (off = 16 ... 1) and base is added.
+// Trees reach shared memory by TMA bulk copies (cp.async.bulk, completion on an mbarrier)
+// in chunks of CH trees (nodes [CH][2^D-1] uint2 {feature, threshold bits}, then leaves
+// [CH][2^D] f32), double-buffered: while the block walks chunk c, chunk c+1 is in flight
+// and chunk c+2 is issued as soon as every warp has left c's buffer.  An ensemble that
+// fits in the two buffers is loaded once and stays resident.
+//
+// A block owns 32 candidates (lane = candidate) whose features sit in shared memory as
+// tile[f * 32 + lane] (bank = lane for every f: conflict-free gathers whatever node each
+// lane is at).  Its NW warps split the trees by residue class: warp w walks the trees
+// t = w (mod NW); the NQ = 32/NW partial sums p[q], q = t mod 32, stay in registers and
+// receive leaves in ascending t, exactly the canonical order.  Walks of the NQ trees of a
+// 32-tree round advance level by level together (NQ independent dependency chains).
 #pragma once
 #include "at_common.cuh"
+#include "tma.cuh"
 
 namespace at {
 
+struct TreeGeo {
+    const uint2 *nodes;     // [T_pad][ni]
+    const float *leaf;      // [T_pad][nl]
+    int T, T_pad, D, ni, nl;
+    int CH;                 // trees per chunk (multiple of 16)
+    int NC;                 // chunks per pass
+    uint32_t chunk_bytes;   // CH * (ni * 8 + nl * 4)
+    int resident;           // NC <= 2: loaded once, never re-streamed
+};
+
+TreeGeo make_geo(const at_gbt_s *g);
+constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // per buffer (two buffers)
+
+__device__ __forceinline__ void ts_issue(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint64_t c)
+{
+    const int k = (int)(c % (uint64_t)G.NC);
+    const int b = (int)(c & 1);
+    const int t0 = k * G.CH;
+    const int nt = min(G.CH, G.T_pad - t0);
+    const uint32_t nb = (uint32_t)nt * G.ni * 8u, lb = (uint32_t)nt * G.nl * 4u;
+    uint8_t *dst = bufs + (size_t)b * G.chunk_bytes;
+    mbar_arrive_expect_tx(&bar[b], nb + lb);
+    bulk_g2s(dst, G.nodes + (int64_t)t0 * G.ni, nb, &bar[b]);
+    bulk_g2s(dst + (size_t)G.CH * G.ni * 8, G.leaf + (int64_t)t0 * G.nl, lb, &bar[b]);
+}
+
+// thread 0: initialise both barriers and start the first two chunks of the stream
+__device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64_t *bar)
+{
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_proxy_async();
+        ts_issue(G, bufs, bar, 0);
+        if (G.NC > 1) ts_issue(G, bufs, bar, 1);
+    }
+}
+
 template <int NW>
-__device__ __forceinline__ void gbt_walk_partials(const uint2 *__restrict__ nodes, const float *__restrict__ leaf,
-                                                  int T, int D, const float *tile, int lane, int warp,
-                                                  float *part /* [32][32] smem */, uint8_t *__restrict__ slots,
-                                                  int64_t slot_ld, int64_t cand, bool cand_ok)
+__device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const float *tile, int lane,
+                                           int warp, float *p, uint8_t *__restrict__ slots, int64_t slot_ld,
+                                           int64_t cand, bool cand_ok)
 {
     constexpr int NQ = 32 / NW;
-    const int ni = (1 << D) - 1;
-    float p[NQ];
-#pragma unroll
-    for (int j = 0; j < NQ; ++j) p[j] = 0.0f;
-    for (int t0 = 0; t0 < T; t0 += 32) {
-        int node[NQ];
-        const uint2 *tn[NQ];
-        bool ok[NQ];
+    const float *leaves = (const float *)(buf + (size_t)G.CH * G.ni * 8);
+    const uint8_t *tile_lane = (const uint8_t *)(tile + lane);   // feature f of this lane at + f * 128
+    const int c0 = k * G.CH;
+    const int c1 = min(c0 + G.CH, G.T);
+    const int D = G.D, ni = G.ni, nl = G.nl;
+    const uint32_t tree_bytes = (uint32_t)ni * 8u;
+    for (int b32 = c0 & ~31; b32 < c1; b32 += 32) {
+        const uint8_t *tb[NQ];
+        uint32_t off[NQ];   // byte offset of the current node: node i at 8 i, children at 2 off + 8 / + 16
 #pragma unroll
         for (int j = 0; j < NQ; ++j) {
-            const int t = t0 + warp + j * NW;
-            ok[j] = t < T;
-            tn[j] = nodes + (int64_t)(ok[j] ? t : 0) * ni;
-            node[j] = 0;
+            const int t = b32 + warp + j * NW;
+            const int lt = (t >= c0 && t < c1) ? t - c0 : 0;
+            tb[j] = buf + (uint32_t)lt * tree_bytes;
+            off[j] = 0;
         }
         for (int d = 0; d < D; ++d) {
 #pragma unroll
             for (int j = 0; j < NQ; ++j) {
-                const uint2 nd = __ldg(tn[j] + node[j]);
-                const float x = tile[nd.x * 32 + lane];
-                node[j] = 2 * node[j] + 2 - (x < __uint_as_float(nd.y) ? 1 : 0);
+                const uint2 nd = *(const uint2 *)(tb[j] + off[j]);
+                const float x = *(const float *)(tile_lane + (nd.x << 7));
+                off[j] = 2u * off[j] + (x < __uint_as_float(nd.y) ? 8u : 16u);
             }
         }
 #pragma unroll
         for (int j = 0; j < NQ; ++j) {
-            if (ok[j]) {
-                const int t = t0 + warp + j * NW;
-                const int slot = node[j] - ni;
-                p[j] = __fadd_rn(p[j], __ldg(leaf + (int64_t)t * (ni + 1) + slot));
+            const int t = b32 + warp + j * NW;
+            if (t >= c0 && t < c1) {
+                const int slot = (int)(off[j] >> 3) - ni;
+                p[j] = __fadd_rn(p[j], leaves[(t - c0) * nl + slot]);
                 if (slots && cand_ok) slots[(int64_t)t * slot_ld + cand] = (uint8_t)slot;
+            }
+        }
+    }
+}
+
+// One full pass over the ensemble.  `c` is the block-wide stream counter (identical in every
+// thread); `c_limit` the total number of chunks the kernel will consume.  Ends with the
+// partials in part[q * 32 + lane] and a __syncthreads.
+template <int NW>
+__device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph, uint64_t &c,
+                                          uint64_t c_limit, const float *tile, int lane, int warp, float *part,
+                                          uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand, bool cand_ok)
+{
+    constexpr int NQ = 32 / NW;
+    float p[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) p[j] = 0.0f;
+    if (G.resident) {
+        for (int k = 0; k < G.NC; ++k)
+            walk_chunk<NW>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, lane, warp, p, slots, slot_ld, cand, cand_ok);
+    } else {
+        for (int k = 0; k < G.NC; ++k, ++c) {
+            const int b = (int)(c & 1);
+            mbar_wait(&bar[b], ph[b]);
+            ph[b] ^= 1u;
+            walk_chunk<NW>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, lane, warp, p, slots, slot_ld, cand, cand_ok);
+            __syncthreads();   // every warp is done with buffer b
+            if (threadIdx.x == 0 && c + 2 < c_limit) {
+                fence_proxy_async();
+                ts_issue(G, bufs, bar, c + 2);
             }
         }
     }
 #pragma unroll
     for (int j = 0; j < NQ; ++j) part[(warp + j * NW) * 32 + lane] = p[j];
+    __syncthreads();
+}
+
+// resident ensembles: wait once for the initial load
+__device__ __forceinline__ void ts_wait_resident(const TreeGeo &G, uint64_t *bar)
+{
+    if (G.resident) {
+        mbar_wait(&bar[0], 0);
+        if (G.NC > 1) mbar_wait(&bar[1], 0);
+    }
 }
 
 // canonical combination of the 32 partials of candidate `lane` (call from one warp)

@@ -16,7 +16,7 @@
 
 namespace at {
 
-constexpr int SA_NW = 8;
+constexpr int SA_NW = 16;
 
 struct TileSink {
     float *tile;
@@ -25,23 +25,18 @@ struct TileSink {
     __device__ __forceinline__ void put_rel(int f, float v) { tile[f * 32 + lane] = v; }
 };
 
-template <int TMPL>
-__device__ __forceinline__ void feats_into_tile(const WlDev &W, const uint16_t *fact, const uint32_t *ch, float *tile,
-                                                int lane)
+__device__ __forceinline__ void feats_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, float *tile,
+                                          int lane, int part, int nparts)
 {
     TileSink sk{tile, lane};
-    features_one<TMPL>(W, fact, ch, sk);
-}
-
-__device__ __forceinline__ void feats_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, float *tile,
-                                          int lane)
-{
     switch (W.tmpl) {
-    case 0: feats_into_tile<0>(W, fact, ch, tile, lane); break;
-    case 1: feats_into_tile<1>(W, fact, ch, tile, lane); break;
-    default: feats_into_tile<2>(W, fact, ch, tile, lane); break;
+    case 0: features_one<0>(W, fact, ch, sk, part, nparts, true); break;
+    case 1: features_one<1>(W, fact, ch, sk, part, nparts, true); break;
+    default: features_one<2>(W, fact, ch, sk, part, nparts, true); break;
     }
 }
+
+__device__ __forceinline__ int n_loops(int tmpl) { return tmpl == 0 ? 8 : tmpl == 1 ? 18 : 16; }
 
 __device__ __forceinline__ void zero_cols_any(int tmpl, float *tile, int lane)
 {
@@ -68,9 +63,6 @@ __device__ __forceinline__ void decode_any(const WlDev &W, uint32_t local, uint3
 struct SaParams {
     const SpaceDev *S;
     const uint16_t *fact;
-    const uint2 *nodes;
-    const float *leaf;
-    int T, D;
     float base;
     int n_chains, n_steps, init;
     uint64_t seed;
@@ -85,26 +77,36 @@ struct SaParams {
     uint64_t *keys;   // [n_chains][n_steps+1]
 };
 
-__global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P)
+// shared-memory layout of sa_kernel
+struct SaSmem {
+    float tile[NFEAT * 32];
+    float part[32 * 32];
+    uint32_t ch[MAXKNOBS][32];
+    int32_t w[32];
+    uint64_t bar[2];
+};
+
+__global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P, TreeGeo G)
 {
-    extern __shared__ float sm[];
-    float *tile = sm;                  // [468][32]
-    float *part = sm + NFEAT * 32;     // [32][32]
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SaSmem &sm = *(SaSmem *)smraw;
+    uint8_t *bufs = smraw + ((sizeof(SaSmem) + 127) / 128) * 128;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c = blockIdx.x * 32 + lane;
     const bool live = c < P.n_chains;
     const int64_t per = (int64_t)P.n_steps + 1;
+    const uint64_t c_limit = (uint64_t)G.NC * (uint64_t)per;
 
-    // warp-0 state (registers)
+    ts_start(G, bufs, sm.bar);
+    // warp-0 state (registers): knob vector, index and energy of the chain of this lane
     uint32_t ch[MAXKNOBS];
     uint64_t idx = 0, idx2 = 0;
     float E = 0.f;
     int w = 0;
-    uint32_t g = P.chain_base + (uint32_t)c;
+    const uint32_t g = P.chain_base + (uint32_t)c;
     uint32_t accw = 0;
     int pj = -1;
     uint32_t pv = 0;
-
     if (warp == 0) {
         if (live && P.chain_w) w = P.chain_w[c];
         const WlDev &W = P.S->w[w];
@@ -119,14 +121,30 @@ __global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P)
             idx = W.offset;
         }
         decode_any(W, (uint32_t)(idx - W.offset), ch);
-        zero_cols_any(W.tmpl, tile, lane);
-        feats_any(W, P.fact, ch, tile, lane);
+#pragma unroll
+        for (int j = 0; j < MAXKNOBS; ++j) sm.ch[j][lane] = ch[j];
+        sm.w[lane] = w;
+        zero_cols_any(W.tmpl, sm.tile, lane);
     }
     __syncthreads();
-    gbt_walk_partials<SA_NW>(P.nodes, P.leaf, P.T, P.D, tile, lane, warp, part, nullptr, 0, 0, false);
-    __syncthreads();
+    uint32_t ph[2] = {0u, 0u};
+    uint64_t cs = 0;
+    // every warp computes its share of the features of all 32 chains of the block
+    auto features_phase = [&]() {
+        uint32_t chl[MAXKNOBS];
+#pragma unroll
+        for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[j][lane];
+        const WlDev &Wl = P.S->w[sm.w[lane]];
+        feats_any(Wl, P.fact, chl, sm.tile, lane, warp, SA_NW);   // context rows, dealt over all warps
+        __syncthreads();
+        if (warp < 6) relation_from_tile(sm.tile, lane, n_loops(Wl.tmpl), warp >> 1, warp & 1);
+        __syncthreads();
+    };
+    features_phase();
+    ts_wait_resident(G, sm.bar);
+    walk_pass<SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, lane, warp, sm.part, nullptr, 0, 0, false);
     if (warp == 0) {
-        E = gbt_combine(part, lane, P.base);
+        E = gbt_combine(sm.part, lane, P.base);
         if (live) {
             P.keys[(int64_t)c * per] = ((uint64_t)fkey(E) << 32) | (uint64_t)(idx - P.S->w[w].offset);
             if (P.vis_E) { P.vis_E[(int64_t)c * per] = E; P.vis_idx[(int64_t)c * per] = idx; }
@@ -152,14 +170,15 @@ __global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P)
                 pv = v;
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == j) ch[q] = v2;
+#pragma unroll
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == j) sm.ch[q][lane] = v2;
             }
-            feats_any(W, P.fact, ch, tile, lane);
         }
         __syncthreads();
-        gbt_walk_partials<SA_NW>(P.nodes, P.leaf, P.T, P.D, tile, lane, warp, part, nullptr, 0, 0, false);
-        __syncthreads();
+        features_phase();
+        walk_pass<SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, lane, warp, sm.part, nullptr, 0, 0, false);
         if (warp == 0) {
-            const float E2 = gbt_combine(part, lane, P.base);
+            const float E2 = gbt_combine(sm.part, lane, P.base);
             const float d = __fsub_rn(E2, E);
             bool acc = d <= 0.0f;
             if (!acc) {
@@ -176,6 +195,8 @@ __global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P)
             } else if (pj >= 0) {
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == pj) ch[q] = pv;   // undo the move
+#pragma unroll
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == pj) sm.ch[q][lane] = pv;
             }
             if (live) {
                 const int64_t at = (int64_t)c * per + s + 1;
@@ -192,6 +213,11 @@ __global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P)
         P.chain_idx[c] = idx;
         P.chain_E[c] = E;
     }
+}
+
+size_t sa_smem_bytes(const TreeGeo &G)
+{
+    return ((sizeof(SaSmem) + 127) / 128) * 128 + 2 * (size_t)G.chunk_bytes;
 }
 
 }  // namespace at
@@ -224,10 +250,6 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     at::SaParams P{};
     P.S = sp->d_space;
     P.fact = sp->d_fact;
-    P.nodes = g->d_nodes;
-    P.leaf = g->d_leaf;
-    P.T = g->n_trees;
-    P.D = g->depth;
     P.base = g->base;
     P.n_chains = o->n_chains;
     P.n_steps = o->n_steps;
@@ -243,16 +265,18 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     P.vis_E = o->d_visited_E;
     P.vis_idx = o->d_visited_idx;
     P.keys = keys;
-    const size_t smem = (size_t)(at::NFEAT * 32 + 32 * 32) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
+    const at::TreeGeo G = at::make_geo(g);
+    const size_t smem = at::sa_smem_bytes(G);
+    if (smem > 227 * 1024) return at::fail(AT_EUNSUPPORTED, "sa_explore: shared memory budget exceeded");
+    static size_t attr = 0;
+    if (smem > attr) {
         AT_CUDA_TRY(cudaFuncSetAttribute(at::sa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr = smem;
     }
     {
         at::ProfScope ps(AT_K_SA, s);
         const unsigned blocks = (unsigned)((o->n_chains + 31) / 32);
-        at::sa_kernel<<<blocks, at::SA_NW * 32, smem, s>>>(P);
+        at::sa_kernel<<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
         AT_LAUNCH_CHECK("sa_kernel");
     }
     for (int w = 0; w < sp->host.n_w; ++w) {
