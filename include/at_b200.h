@@ -229,7 +229,8 @@ AT_API int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t n_fe
 enum {
     AT_K_FEATURES = 0, AT_K_PREDICT = 1, AT_K_SA = 2, AT_K_TOPK = 3, AT_K_SELECT = 4,
     AT_K_FIT_PREP = 5, AT_K_FIT_GRAD = 6, AT_K_FIT_HIST = 7, AT_K_FIT_SPLIT = 8, AT_K_FIT_UPDATE = 9,
-    AT_K_NCLASSES = 10
+    AT_K_FIT_GRAPH = 10,   /* a single-rank fit's trees, launched as one CUDA graph */
+    AT_K_NCLASSES = 11
 };
 AT_API int64_t at_launch_count(void);
 AT_API int at_prof_enable(int on);

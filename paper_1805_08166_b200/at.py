@@ -17,7 +17,7 @@ LIB_PATH = PKG / "libautotvm_b200.so"
 NFEAT = 468
 
 AT_K = dict(features=0, predict=1, sa=2, topk=3, select=4, fit_prep=5, fit_grad=6, fit_hist=7, fit_split=8,
-            fit_update=9)
+            fit_update=9, fit_graph=10)
 
 
 class ATError(RuntimeError):

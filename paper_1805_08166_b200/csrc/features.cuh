@@ -256,28 +256,176 @@ __device__ __forceinline__ void features_one(const WlDev &W, const uint16_t *__r
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Block-cooperative variant used by sa_kernel (32 chains per block, lane = chain): the work of
+// one candidate is spread over the block's warps in three phases separated by barriers:
+//   L) loop extents: warp w lowers loops k = w, w + NW, ... for all 32 chains (one factor load
+//      each) into shared arrays ext[k][lane], axis[k][lane];
+//   R) context rows: warp w owns rows k = w (mod NW) and rebuilds that row's active products
+//      from the shared extents (inner loops' extents, top-down prefix) -- the same integer
+//      formulas as features_one;
+//   T) relation features from the finished rows (relation_from_tile).
+struct SaLowering {
+    uint32_t ext[MAXLOOPS][32];
+    uint8_t axis[MAXLOOPS][32];
+    uint32_t unroll_max[32];
+    uint8_t vec[32];
+};
+
+// (axis, level) of loop k of template TMPL with reorder knob p (DESIGN Q3 nest orders)
+template <int TMPL>
+__device__ __forceinline__ void loop_axis_level(int k, uint32_t p, int &axis, int &level)
+{
+    if (TMPL == 0) {
+        axis = k % 3;                         // i0 j0 k0 i1 j1 k1 i2 j2
+        level = k / 3;
+    } else if (k < 9) {
+        axis = k % 3;                         // spatial levels 0..2
+        level = k / 3;
+    } else if (TMPL == 1) {
+        if (k < 12) { axis = 3 + (int)perm3(p, k - 9); level = 0; }   // perm(rc0 ry0 rx0)
+        else if (k < 15) { axis = 3 + (k - 12); level = 1; }          // rc1 ry1 rx1
+        else { axis = k - 15; level = 3; }                            // f3 y3 x3
+    } else {
+        if (k < 13) { axis = 3 + ((k - 9) & 1); level = (k - 9) >> 1; }   // ry0 rx0 ry1 rx1
+        else { axis = (int)perm3(p, k - 13); level = 3; }                  // perm(c3 y3 x3)
+    }
+}
+
+template <int TMPL>
+__device__ __forceinline__ void sa_lower_loop(const WlDev &W, const uint16_t *__restrict__ fact, const uint32_t *ch,
+                                              int k, int lane, SaLowering &L)
+{
+    constexpr int NL = Tmpl<TMPL>::NL;
+    if (k >= NL) return;
+    const uint32_t p = TMPL == 1 ? ch[6] : TMPL == 2 ? ch[5] : 0u;
+    int axis, level;
+    loop_axis_level<TMPL>(k, p, axis, level);
+    const int Lv = TMPL == 0 ? (axis == 2 ? 2 : 3) : (axis < 3 ? 4 : 2);
+    uint32_t cha = 0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) if (q == axis) cha = ch[q];
+    L.ext[k][lane] = __ldg(fact + W.fact_off[axis] + cha * (uint32_t)Lv + level);
+    L.axis[k][lane] = (uint8_t)axis;
+    if (k == 0) {
+        L.unroll_max[lane] = W.unroll_vals[TMPL == 0 ? ch[3] : TMPL == 1 ? ch[7] : ch[6]];
+        L.vec[lane] = (uint8_t)(TMPL == 0 ? 0u : TMPL == 1 ? ch[8] : ch[7]);
+    }
+}
+
+template <int TMPL, class Sink>
+__device__ __forceinline__ void sa_row(const WlDev &W, const SaLowering &L, int k, int lane, uint32_t p, Sink &sk)
+{
+    constexpr int NL = Tmpl<TMPL>::NL;
+    constexpr int NA = Tmpl<TMPL>::NA;
+    if (k >= NL) return;
+    // all extents of this chain at once (independent loads), then predicated products:
+    // A_a and bottom-up over the loops inside k, top-down over the loops outside k
+    uint32_t ev[NL];
+    int av[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) { ev[l] = L.ext[l][lane]; av[l] = L.axis[l][lane]; }
+    uint32_t A[NA];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) A[q] = 1;
+    uint32_t bu = 1, td = 1;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        const bool inner = l > k;
+#pragma unroll
+        for (int q = 0; q < NA; ++q) A[q] = (inner && av[l] == q) ? A[q] * ev[l] : A[q];
+        bu = inner ? bu * ev[l] : bu;
+        td = l < k ? td * ev[l] : td;
+    }
+    uint32_t ek = 0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) if (l == k) ek = ev[l];
+    int a, level;
+    loop_axis_level<TMPL>(k, p, a, level);
+    uint32_t coef = 1;
+#pragma unroll
+    for (int q = 0; q < NA; ++q) if (a == q) coef = A[q];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) if (a == q) A[q] *= ek;
+    bu *= ek;
+    const uint32_t S = W.S;
+    uint32_t T[3], st[3];
+    if (TMPL == 0) {
+        T[0] = A[0] * A[1];
+        T[1] = A[2] * A[0];
+        T[2] = A[2] * A[1];
+        st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : 0u;
+        st[1] = (a == 2) ? coef * W.str_in[0] : (a == 0) ? coef * W.str_in[1] : 0u;
+        st[2] = (a == 2) ? coef * W.str_ker[0] : (a == 1) ? coef * W.str_ker[1] : 0u;
+    } else if (TMPL == 1) {
+        T[0] = A[0] * A[1] * A[2];
+        T[1] = A[3] * comp_touch(A[1], A[4], S) * comp_touch(A[2], A[5], S);
+        T[2] = A[0] * A[3] * A[4] * A[5];
+        st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : (a == 2) ? coef * W.str_out[2] : 0u;
+        st[1] = (a == 3) ? coef * W.str_in[0] : (a == 1) ? coef * S * W.str_in[1] : (a == 4) ? coef * W.str_in[1]
+              : (a == 2) ? coef * S * W.str_in[2] : (a == 5) ? coef * W.str_in[2] : 0u;
+        st[2] = (a == 0) ? coef * W.str_ker[0] : (a == 3) ? coef * W.str_ker[1] : (a == 4) ? coef * W.str_ker[2]
+              : (a == 5) ? coef * W.str_ker[3] : 0u;
+    } else {
+        T[0] = A[0] * A[1] * A[2];
+        T[1] = A[0] * comp_touch(A[1], A[3], S) * comp_touch(A[2], A[4], S);
+        T[2] = A[0] * A[3] * A[4];
+        st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : (a == 2) ? coef * W.str_out[2] : 0u;
+        st[1] = (a == 0) ? coef * W.str_in[0] : (a == 1) ? coef * S * W.str_in[1] : (a == 3) ? coef * W.str_in[1]
+              : (a == 2) ? coef * S * W.str_in[2] : (a == 4) ? coef * W.str_in[2] : 0u;
+        st[2] = (a == 0) ? coef * W.str_ker[0] : (a == 3) ? coef * W.str_ker[1] : (a == 4) ? coef * W.str_ker[2] : 0u;
+    }
+    int ann;
+    if (TMPL != 0 && k < 9) {
+        ann = 4 + level;
+    } else {
+        ann = (bu <= L.unroll_max[lane]) ? 1 : 0;
+        if (k == NL - 1 && L.vec[lane]) ann = 2;
+    }
+    const float fbu = __uint2float_rn(bu);
+    const int base = 19 * k;
+    sk.put(base + 0, __uint2float_rn(ek));
+#pragma unroll
+    for (int q = 0; q < 7; ++q) sk.put(base + 1 + q, ann == q ? 1.0f : 0.0f);
+    sk.put(base + 8, __uint2float_rn(td));
+    sk.put(base + 9, fbu);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        sk.put(base + 10 + 3 * b, __uint2float_rn(T[b]));
+        sk.put(base + 11 + 3 * b, __fdiv_rn(fbu, __uint2float_rn(T[b])));
+        sk.put(base + 12 + 3 * b, __uint2float_rn(st[b]));
+    }
+    if (k == 0) {
+        sk.put(462, fbu);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) sk.put(463 + b, __uint2float_rn(T[b]));
+    }
+}
+
 // Relation features of buffer b, pair p (0: reuse, 1: top-down) from context rows already in a
 // smem tile [f][32] (rows_only pass).  The integer touch count is read back as its fp32
 // conversion: for thresholds 2^t <= 2^20 < 2^24 the comparison is exact (RN is monotone and
-// 2^t is representable), so this equals the integer test of the one-pass version.
-__device__ __forceinline__ void relation_from_tile(float *tile, int lane, int NL, int b, int p)
+// 2^t is representable), so this equals the integer test of the one-pass version.  Every
+// Z value here is > 0 (reuse > 0, top-down >= 1), so "max over an empty set = 0" is simply a
+// max seeded with 0: R_t = max(0, max_{k : T_k < 2^t} Z_k), branch-free over a static t loop.
+// (half h computes thresholds t = 10 h + 1 .. 10 h + 10)
+__device__ __forceinline__ void relation_from_tile(float *tile, int lane, int NL, int b, int p, int h)
 {
     const int colT = 10 + 3 * b, colZ = p == 0 ? 11 + 3 * b : 8;
-    const int out = 342 + 40 * b + 20 * p - 1;
-    float smax = 0.0f;
-    bool has = false;
-    int tnext = 1;
-    for (int k = NL - 1; k >= 0; --k) {
-        const float T = tile[(19 * k + colT) * 32 + lane];
+    float R[10];
+#pragma unroll
+    for (int t = 0; t < 10; ++t) R[t] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < MAXLOOPS; ++k) {
+        // absent rows (k >= NL) are all-zero and must not qualify: read them as T = +inf
+        const float T = k < NL ? tile[(19 * k + colT) * 32 + lane] : __int_as_float(0x7f800000);
         const float z = tile[(19 * k + colZ) * 32 + lane];
-        while (tnext <= 20 && T >= __int_as_float((127 + tnext) << 23)) {
-            tile[(out + tnext) * 32 + lane] = has ? smax : 0.0f;
-            ++tnext;
-        }
-        smax = has ? fmaxf(smax, z) : z;
-        has = true;
+#pragma unroll
+        for (int t = 0; t < 10; ++t) R[t] = fmaxf(R[t], T < __int_as_float((128 + 10 * h + t) << 23) ? z : 0.0f);
     }
-    for (; tnext <= 20; ++tnext) tile[(out + tnext) * 32 + lane] = has ? smax : 0.0f;
+    const int out = 342 + 40 * b + 20 * p + 10 * h;
+#pragma unroll
+    for (int t = 0; t < 10; ++t) tile[(out + t) * 32 + lane] = R[t];
 }
 
 // columns that are zero for every candidate of a template (absent loop rows + padding)

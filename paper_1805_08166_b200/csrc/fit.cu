@@ -224,7 +224,7 @@ __global__ void positions_kernel(const uint16_t *__restrict__ key, const int32_t
     member[woff[k] + y] = (int32_t)i;
 }
 
-__global__ void __launch_bounds__(128) grads_kernel(const int32_t *__restrict__ member,
+__global__ void __launch_bounds__(256) grads_kernel(const int32_t *__restrict__ member,
                                                     const int32_t *__restrict__ counts,
                                                     const int32_t *__restrict__ woff,
                                                     const int32_t *__restrict__ gprefix, int group_size,
@@ -256,27 +256,40 @@ __global__ void __launch_bounds__(128) grads_kernel(const int32_t *__restrict__ 
         sp[a] = pred[i];
     }
     __syncthreads();
-    // thread a accumulates member a's share of every pair it is in (no atomics; each pair's
-    // rho is computed identically by both of its members)
-    for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    // SUB threads per member: thread (a, r) accumulates member a's share of its pairs with members
+    // c = r (mod SUB) (no atomics; each pair's rho is computed identically by both members), the SUB
+    // partial int64 sums are then added with xor shuffles (exact, order-free)
+    constexpr int SUB = 4;
+    for (int base = 0; base < m * SUB; base += blockDim.x) {
+        const int tix = base + (int)threadIdx.x;
+        const int a = tix / SUB, r = tix % SUB;
         long long ga = 0, ha = 0;
-        const float ca = sc[a], fa = sp[a];
-        for (int c = 0; c < m; ++c) {
-            const float cc = sc[c];
-            if (c == a || cc == ca) continue;   // sign(c_i - c_j) = 0 contributes nothing
-            const bool hi = ca > cc;            // a is the slower (i) of the pair
-            const float fi = hi ? fa : sp[c], fj = hi ? sp[c] : fa;
-            const float d = __fsub_rn(fj, fi);
-            const float e = exp_det(-d);
-            const float rho = __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
-            const float hh = __fmul_rn(rho, __fsub_rn(1.0f, rho));
-            const long long q = __double2ll_rn((double)rho * 4294967296.0);
-            const long long qh = __double2ll_rn((double)hh * 4294967296.0);
-            ga += hi ? -2 * q : 2 * q;          // both orders of Eq. 2 carry the same term
-            ha += 2 * qh;
+        if (a < m) {
+            const float ca = sc[a], fa = sp[a];
+            for (int c = r; c < m; c += SUB) {
+                const float cc = sc[c];
+                if (c == a || cc == ca) continue;   // sign(c_i - c_j) = 0 contributes nothing
+                const bool hi = ca > cc;            // a is the slower (i) of the pair
+                const float fi = hi ? fa : sp[c], fj = hi ? sp[c] : fa;
+                const float d = __fsub_rn(fj, fi);
+                const float e = exp_det(-d);
+                const float rho = __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
+                const float hh = __fmul_rn(rho, __fsub_rn(1.0f, rho));
+                const long long q = __double2ll_rn((double)rho * 4294967296.0);
+                const long long qh = __double2ll_rn((double)hh * 4294967296.0);
+                ga += hi ? -2 * q : 2 * q;          // both orders of Eq. 2 carry the same term
+                ha += 2 * qh;
+            }
         }
-        g[mem[a]] = ga;
-        h[mem[a]] = ha;
+#pragma unroll
+        for (int off = 1; off < SUB; off <<= 1) {
+            ga += __shfl_xor_sync(0xFFFFFFFFu, ga, off);
+            ha += __shfl_xor_sync(0xFFFFFFFFu, ha, off);
+        }
+        if (a < m && r == 0) {
+            g[mem[a]] = ga;
+            h[mem[a]] = ha;
+        }
     }
 }
 
@@ -415,15 +428,55 @@ __device__ __forceinline__ SplitBest warp_best(SplitBest best)
     return best;
 }
 
-// single-rank fast path: block f builds the level's histograms of feature f in shared memory
-// and immediately scans its splits for every node (warp per node), so the level's histograms
-// never touch HBM.  Same arithmetic as hist_kernel + split_feature_kernel.
-__global__ void __launch_bounds__(256) hist_split_kernel(const uint8_t *__restrict__ bins,
+// Best split of one (node, feature) histogram by one warp (exact int64 prefix sums by warp scans
+// over 32-bin chunks, fp64 gain in the oracle's operation order).  Splits right after an empty bin repeat the previous split's (G_L, H_L) -- and its gain -- so the
+// lower s wins the tie anyway; they are skipped.
+template <class Cell>
+__device__ __forceinline__ SplitBest scan_splits(const Cell *hf, int nb, long long Gi, long long Hi, double lam,
+                                                 double mcw, int f, int lane)
+{
+    const int nc = nb - 1;
+    const double G = (double)Gi * FX, H = (double)Hi * FX;
+    const double parent = G * G / (H + lam);
+    SplitBest best{0.0, -1, 0};
+    long long carryG = 0, carryH = 0;
+    for (int c0 = 0; c0 < nc; c0 += 32) {
+        const int b = c0 + lane;   // split s = b + 1 puts bins <= b on the left
+        long long vg = b < nc ? (long long)hf[2 * b] : 0, vh = b < nc ? (long long)hf[2 * b + 1] : 0;
+        const long long own_g = vg, own_h = vh;
+        if (__ballot_sync(0xFFFFFFFFu, vg != 0 || vh != 0) == 0) continue;   // empty chunk: carry unchanged
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long yg = __shfl_up_sync(0xFFFFFFFFu, vg, off);
+            const long long yh = __shfl_up_sync(0xFFFFFFFFu, vh, off);
+            if (lane >= off) { vg += yg; vh += yh; }
+        }
+        const long long GLi = carryG + vg, HLi = carryH + vh;
+        carryG += __shfl_sync(0xFFFFFFFFu, vg, 31);
+        carryH += __shfl_sync(0xFFFFFFFFu, vh, 31);
+        if (b < nc && (own_g != 0 || own_h != 0)) {
+            const double GL = (double)GLi * FX, HL = (double)HLi * FX;
+            const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
+            if (!(HL < mcw || HR < mcw)) {
+                const double gain = (GL * GL / (HL + lam) + GR * GR / (HR + lam)) - parent;
+                if (gain > 0.0) {
+                    SplitBest cnd{gain, f, b + 1};
+                    if (split_better(cnd, best)) best = cnd;
+                }
+            }
+        }
+    }
+    return warp_best(best);
+}
+
+// single-rank fast path: block f builds the level's histograms of feature f in shared memory and
+// scans its splits for every node (warp per node), so the level's histograms never touch HBM.
+__global__ void __launch_bounds__(256, 4) hist_split_kernel(const uint8_t *__restrict__ bins,
                                                          const int32_t *__restrict__ node,
                                                          const int64_t *__restrict__ g, const int64_t *__restrict__ h,
                                                          int64_t n, const int32_t *__restrict__ boff, int F, int first,
                                                          int nn, double lam, double mcw,
-                                                         const uint8_t *__restrict__ dead,
+                                                         uint8_t *__restrict__ dead,
                                                          double *__restrict__ best_gain, int32_t *__restrict__ best_s,
                                                          int64_t *__restrict__ hist0)
 {
@@ -444,10 +497,8 @@ __global__ void __launch_bounds__(256) hist_split_kernel(const uint8_t *__restri
     if (hist0)
         for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) hist0[(int64_t)boff[f] * 2 + q] = (int64_t)shist[q];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nc = nb - 1;
     for (int q = warp; q < nn; q += blockDim.x >> 5) {
-        const int nd = first + q;
-        if (dead[nd]) {
+        if (dead[first + q]) {
             if (lane == 0) best_s[(int64_t)q * F + f] = 0;
             continue;
         }
@@ -460,35 +511,7 @@ __global__ void __launch_bounds__(256) hist_split_kernel(const uint8_t *__restri
             Gi += __shfl_xor_sync(0xFFFFFFFFu, Gi, off);
             Hi += __shfl_xor_sync(0xFFFFFFFFu, Hi, off);
         }
-        const double G = (double)Gi * FX, H = (double)Hi * FX;
-        const double parent = G * G / (H + lam);
-        SplitBest best{0.0, -1, 0};
-        long long carryG = 0, carryH = 0;
-        for (int c0 = 0; c0 < nc; c0 += 32) {
-            const int b = c0 + lane;
-            long long vg = b < nc ? (long long)hf[2 * b] : 0, vh = b < nc ? (long long)hf[2 * b + 1] : 0;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const long long yg = __shfl_up_sync(0xFFFFFFFFu, vg, off);
-                const long long yh = __shfl_up_sync(0xFFFFFFFFu, vh, off);
-                if (lane >= off) { vg += yg; vh += yh; }
-            }
-            const long long GLi = carryG + vg, HLi = carryH + vh;
-            carryG += __shfl_sync(0xFFFFFFFFu, vg, 31);
-            carryH += __shfl_sync(0xFFFFFFFFu, vh, 31);
-            if (b < nc) {
-                const double GL = (double)GLi * FX, HL = (double)HLi * FX;
-                const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
-                if (!(HL < mcw || HR < mcw)) {
-                    const double gain = (GL * GL / (HL + lam) + GR * GR / (HR + lam)) - parent;
-                    if (gain > 0.0) {
-                        SplitBest cnd{gain, f, b + 1};
-                        if (split_better(cnd, best)) best = cnd;
-                    }
-                }
-            }
-        }
-        best = warp_best(best);
+        const SplitBest best = scan_splits(hf, nb, Gi, Hi, lam, mcw, f, lane);
         if (lane == 0) {
             best_gain[(int64_t)q * F + f] = best.gain;
             best_s[(int64_t)q * F + f] = best.f < 0 ? 0 : best.s;
@@ -523,37 +546,7 @@ __global__ void __launch_bounds__(256) split_feature_kernel(const int64_t *__res
         Gi += __shfl_xor_sync(0xFFFFFFFFu, Gi, off);
         Hi += __shfl_xor_sync(0xFFFFFFFFu, Hi, off);
     }
-    const double G = (double)Gi * FX, H = (double)Hi * FX;
-    const double parent = G * G / (H + lam);
-    const int64_t *hf = hn + (int64_t)boff[f] * 2;
-    const int nc = boff[f + 1] - boff[f] - 1;   // ncuts_f
-    SplitBest best{0.0, -1, 0};
-    long long carryG = 0, carryH = 0;
-    for (int c0 = 0; c0 < nc; c0 += 32) {
-        const int b = c0 + lane;                 // split s = b + 1 puts bins <= b on the left
-        long long vg = b < nc ? hf[2 * b] : 0, vh = b < nc ? hf[2 * b + 1] : 0;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const long long yg = __shfl_up_sync(0xFFFFFFFFu, vg, off);
-            const long long yh = __shfl_up_sync(0xFFFFFFFFu, vh, off);
-            if (lane >= off) { vg += yg; vh += yh; }
-        }
-        const long long GLi = carryG + vg, HLi = carryH + vh;
-        carryG += __shfl_sync(0xFFFFFFFFu, vg, 31);
-        carryH += __shfl_sync(0xFFFFFFFFu, vh, 31);
-        if (b < nc) {
-            const double GL = (double)GLi * FX, HL = (double)HLi * FX;
-            const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
-            if (!(HL < mcw || HR < mcw)) {
-                const double gain = (GL * GL / (HL + lam) + GR * GR / (HR + lam)) - parent;
-                if (gain > 0.0) {
-                    SplitBest c{gain, f, b + 1};
-                    if (split_better(c, best)) best = c;
-                }
-            }
-        }
-    }
-    best = warp_best(best);
+    const SplitBest best = scan_splits(hn + (int64_t)boff[f] * 2, boff[f + 1] - boff[f], Gi, Hi, lam, mcw, f, lane);
     if (lane == 0) {
         best_gain[(int64_t)q * F + f] = best.gain;
         best_s[(int64_t)q * F + f] = best.f < 0 ? 0 : best.s;
@@ -562,7 +555,7 @@ __global__ void __launch_bounds__(256) split_feature_kernel(const int64_t *__res
 
 // one block per node: best over features (gain desc, feature asc), write the tree node
 __global__ void __launch_bounds__(256) split_node_kernel(const double *__restrict__ best_gain,
-                                                         const int32_t *__restrict__ best_s, int F, int first,
+                                                         const int32_t *__restrict__ best_s, int F, int first, int nn,
                                                          const float *__restrict__ cuts, int B,
                                                          uint8_t *__restrict__ dead, int32_t *__restrict__ split_f,
                                                          int32_t *__restrict__ split_s,
@@ -777,32 +770,47 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         AT_CUDA_TRY(cudaFuncSetAttribute(hist_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         hist_attr = 160 * 1024;
     }
-    for (int t = 0; t < o->n_trees; ++t) {
-        {
-            ProfScope ps(AT_K_FIT_GRAD, s);
-            positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, (uint32_t)t,
-                                                          member);
-            if (n_groups > 0)
-                grads_kernel<<<n_groups, 128, grad_smem, s>>>(member, counts, woff, gpre, GS, d_cost, pred, g, h);
-            AT_LAUNCH_CHECK("fit gradients");
-        }
-        AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
-        AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
-        uint16_t *tf = t_feat + (size_t)t * n_int;
-        float *tt = t_thr + (size_t)t * n_int;
-        for (int d = 0; d < D; ++d) {
-            const int first = (1 << d) - 1, nn = 1 << d;
-            const size_t cells = (size_t)nn * TB * 2;
-            const size_t smem = (size_t)nn * max_nb * 2 * sizeof(int64_t);
-            const int use_smem = smem <= 160 * 1024;
-            const bool want_h0 = t == 0 && d == 0 && o->d_hist0_out;
-            if (!o->allreduce && use_smem) {
-                // single rank: histograms stay in shared memory, split scan fused
-                ProfScope ps(AT_K_FIT_HIST, s);
-                hist_split_kernel<<<F, 256, smem, s>>>(bins, node, g, h, n, boff, F, first, nn, lam, mcw,
-                                                       dead, best_gain, best_s, want_h0 ? hist : nullptr);
-                AT_LAUNCH_CHECK("hist_split_kernel");
-            } else {
+    // all trees are enqueued by one function; a single-rank fit (no host callback between levels) is
+    // captured once into a CUDA graph and launched as one unit, so ~15 launches per tree cost no host
+    // round trips.
+    auto enqueue_trees = [&](cudaStream_t s) -> int {
+        for (int t = 0; t < o->n_trees; ++t) {
+            {
+                ProfScope ps(AT_K_FIT_GRAD, s);
+                positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, (uint32_t)t,
+                                                              member);
+                if (n_groups > 0)
+                    grads_kernel<<<n_groups, 256, grad_smem, s>>>(member, counts, woff, gpre, GS, d_cost, pred, g, h);
+                AT_LAUNCH_CHECK("fit gradients");
+            }
+            AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
+            AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
+            uint16_t *tf = t_feat + (size_t)t * n_int;
+            float *tt = t_thr + (size_t)t * n_int;
+            for (int d = 0; d < D; ++d) {
+                const int first = (1 << d) - 1, nn = 1 << d;
+                const size_t cells = (size_t)nn * TB * 2;
+                const size_t smem = (size_t)nn * max_nb * 2 * sizeof(int64_t);
+                const int use_smem = smem <= 160 * 1024;
+                const bool want_h0 = t == 0 && d == 0 && o->d_hist0_out;
+                if (!o->allreduce && use_smem) {
+                    // single rank: histograms stay in shared memory, split scan fused
+                    {
+                        ProfScope ps(AT_K_FIT_HIST, s);
+                        hist_split_kernel<<<F, 256, smem, s>>>(bins, node, g, h, n, boff, F, first, nn, lam, mcw, dead,
+                                                               best_gain, best_s, want_h0 ? hist : nullptr);
+                        AT_LAUNCH_CHECK("hist_split_kernel");
+                    }
+                    if (want_h0)
+                        hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hist, boff, F, B,
+                                                                                     o->d_hist0_out);
+                    ProfScope ps(AT_K_FIT_SPLIT, s);
+                    split_node_kernel<<<nn, 256, 0, s>>>(best_gain, best_s, F, first, nn, cuts, B, dead,
+                                                                  split_f, split_s, tf, tt);
+                    partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
+                    AT_LAUNCH_CHECK("split/partition");
+                    continue;
+                }
                 {
                     ProfScope ps(AT_K_FIT_HIST, s);
                     if (n_chunks != 1 || !use_smem || ns == 0)
@@ -816,37 +824,63 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                     const int rc = o->allreduce(hist, (int64_t)cells, o->ctx, stream);
                     if (rc) return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
                 }
-                ProfScope ps(AT_K_FIT_SPLIT, s);
-                split_feature_kernel<<<nblk((int64_t)nn * F, 8), 256, 0, s>>>(hist, boff, TB, F, first, nn, lam, mcw,
-                                                                              dead, best_gain, best_s);
-                AT_LAUNCH_CHECK("split_feature_kernel");
+                if (want_h0)
+                    hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hist, boff, F, B, o->d_hist0_out);
+                {
+                    ProfScope ps(AT_K_FIT_SPLIT, s);
+                    split_feature_kernel<<<nblk((int64_t)nn * F, 8), 256, 0, s>>>(hist, boff, TB, F, first, nn, lam,
+                                                                                  mcw, dead, best_gain, best_s);
+                    split_node_kernel<<<nn, 256, 0, s>>>(best_gain, best_s, F, first, nn, cuts, B, dead, split_f, split_s,
+                                                         tf, tt);
+                    partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
+                    AT_LAUNCH_CHECK("split/partition");
+                }
             }
-            if (want_h0)
-                hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hist, boff, F, B, o->d_hist0_out);
             {
-                ProfScope ps(AT_K_FIT_SPLIT, s);
-                split_node_kernel<<<nn, 256, 0, s>>>(best_gain, best_s, F, first, cuts, B, dead, split_f, split_s, tf, tt);
-                partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
-                AT_LAUNCH_CHECK("split/partition");
+                ProfScope ps(AT_K_FIT_UPDATE, s);
+                AT_CUDA_TRY(cudaMemsetAsync(lsum, 0, sizeof(int64_t) * 2 * n_leaf, s));
+                if (he > hb) leafsum_kernel<<<nblk(he - hb, 256), 256, 0, s>>>(node, g, h, hb, he, n_int, lsum);
+                AT_LAUNCH_CHECK("leafsum");
+            }
+            if (o->allreduce) {
+                const int rc = o->allreduce(lsum, (int64_t)2 * n_leaf, o->ctx, stream);
+                if (rc) return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
+            }
+            {
+                ProfScope ps(AT_K_FIT_UPDATE, s);
+                float *tl = t_leaf + (size_t)t * n_leaf;
+                leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(lsum, n_leaf, eta, lam, tl);
+                pred_update_kernel<<<nblk(n, 256), 256, 0, s>>>(node, n, n_int, tl, pred);
+                AT_LAUNCH_CHECK("leaf/pred update");
             }
         }
+        return AT_OK;
+    };
+    if (o->allreduce) {
+        const int rc = enqueue_trees(s);
+        if (rc) return rc;
+    } else {
+        static thread_local cudaStream_t cs = nullptr;
+        if (!cs) AT_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        prof_suspend(true);
+        cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) { prof_suspend(false); return cuda_fail(e, "gbt_fit_hist: begin capture"); }
+        const int rc = enqueue_trees(cs);
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamEndCapture(cs, &graph);
+        prof_suspend(false);
+        if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: end capture");
+        cudaGraphExec_t exec = nullptr;
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph instantiate");
         {
-            ProfScope ps(AT_K_FIT_UPDATE, s);
-            AT_CUDA_TRY(cudaMemsetAsync(lsum, 0, sizeof(int64_t) * 2 * n_leaf, s));
-            if (he > hb) leafsum_kernel<<<nblk(he - hb, 256), 256, 0, s>>>(node, g, h, hb, he, n_int, lsum);
-            AT_LAUNCH_CHECK("leafsum");
+            ProfScope ps(AT_K_FIT_GRAPH, s);
+            e = cudaGraphLaunch(exec, s);
         }
-        if (o->allreduce) {
-            const int rc = o->allreduce(lsum, (int64_t)2 * n_leaf, o->ctx, stream);
-            if (rc) return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
-        }
-        {
-            ProfScope ps(AT_K_FIT_UPDATE, s);
-            float *tl = t_leaf + (size_t)t * n_leaf;
-            leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(lsum, n_leaf, eta, lam, tl);
-            pred_update_kernel<<<nblk(n, 256), 256, 0, s>>>(node, n, n_int, tl, pred);
-            AT_LAUNCH_CHECK("leaf/pred update");
-        }
+        cudaGraphExecDestroy(exec);
+        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph launch");
     }
     // the fitted ensemble handle
     at_gbt gm = new at_gbt_s();

@@ -63,36 +63,39 @@ __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf,
                                            int64_t cand, bool cand_ok)
 {
     constexpr int NQ = 32 / NW;
+    constexpr int R = 2;                 // 32-tree rounds walked together: R * NQ independent walks
+    constexpr int NJ = R * NQ;
     const float *leaves = (const float *)(buf + (size_t)G.CH * G.ni * 8);
     const uint8_t *tile_lane = (const uint8_t *)(tile + lane);   // feature f of this lane at + f * 128
     const int c0 = k * G.CH;
     const int c1 = min(c0 + G.CH, G.T);
     const int D = G.D, ni = G.ni, nl = G.nl;
     const uint32_t tree_bytes = (uint32_t)ni * 8u;
-    for (int b32 = c0 & ~31; b32 < c1; b32 += 32) {
-        const uint8_t *tb[NQ];
-        uint32_t off[NQ];   // byte offset of the current node: node i at 8 i, children at 2 off + 8 / + 16
+    for (int b64 = c0 & ~31; b64 < c1; b64 += 32 * R) {
+        const uint8_t *tb[NJ];
+        uint32_t off[NJ];   // byte offset of the current node: node i at 8 i, children at 2 off + 8 / + 16
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) {
-            const int t = b32 + warp + j * NW;
+        for (int jj = 0; jj < NJ; ++jj) {
+            const int t = b64 + 32 * (jj / NQ) + warp + (jj % NQ) * NW;
             const int lt = (t >= c0 && t < c1) ? t - c0 : 0;
-            tb[j] = buf + (uint32_t)lt * tree_bytes;
-            off[j] = 0;
+            tb[jj] = buf + (uint32_t)lt * tree_bytes;
+            off[jj] = 0;
         }
         for (int d = 0; d < D; ++d) {
 #pragma unroll
-            for (int j = 0; j < NQ; ++j) {
-                const uint2 nd = *(const uint2 *)(tb[j] + off[j]);
+            for (int jj = 0; jj < NJ; ++jj) {
+                const uint2 nd = *(const uint2 *)(tb[jj] + off[jj]);
                 const float x = *(const float *)(tile_lane + (nd.x << 7));
-                off[j] = 2u * off[j] + (x < __uint_as_float(nd.y) ? 8u : 16u);
+                off[jj] = 2u * off[jj] + (x < __uint_as_float(nd.y) ? 8u : 16u);
             }
         }
+        // leaves in ascending t within each residue class (round 0 before round 1)
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) {
-            const int t = b32 + warp + j * NW;
+        for (int jj = 0; jj < NJ; ++jj) {
+            const int t = b64 + 32 * (jj / NQ) + warp + (jj % NQ) * NW;
             if (t >= c0 && t < c1) {
-                const int slot = (int)(off[j] >> 3) - ni;
-                p[j] = __fadd_rn(p[j], leaves[(t - c0) * nl + slot]);
+                const int slot = (int)(off[jj] >> 3) - ni;
+                p[jj % NQ] = __fadd_rn(p[jj % NQ], leaves[(t - c0) * nl + slot]);
                 if (slots && cand_ok) slots[(int64_t)t * slot_ld + cand] = (uint8_t)slot;
             }
         }

@@ -25,6 +25,9 @@ int cuda_fail(cudaError_t e, const char *where)
 
 // ---------------------------------------------------------------- profiling
 static std::atomic<int64_t> g_launches{0};
+static thread_local bool g_suspend = false;
+
+void prof_suspend(bool on) { g_suspend = on; }
 static std::atomic<int> g_prof_on{0};
 static std::mutex g_prof_mu;
 struct EvPair { cudaEvent_t a, b; };
@@ -42,7 +45,7 @@ static cudaEvent_t take_event()
 void prof_begin(int cls, cudaStream_t s)
 {
     g_launches.fetch_add(1);
-    if (!g_prof_on.load()) return;
+    if (!g_prof_on.load() || g_suspend) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t e;
     if (!g_pool.empty()) { e = g_pool.back().a; g_pool.pop_back(); } else e = take_event();
@@ -52,7 +55,7 @@ void prof_begin(int cls, cudaStream_t s)
 
 void prof_end(int cls, cudaStream_t s)
 {
-    if (!g_prof_on.load()) return;
+    if (!g_prof_on.load() || g_suspend) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t e;
     if (!g_pool.empty()) { e = g_pool.back().a; g_pool.pop_back(); } else e = take_event();

@@ -83,10 +83,32 @@ struct SaSmem {
     float part[32 * 32];
     uint32_t ch[MAXKNOBS][32];
     int32_t w[32];
+    SaLowering low;
     uint64_t bar[2];
 };
 
-__global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P, TreeGeo G)
+__device__ __forceinline__ void sa_lower_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, int k, int lane,
+                                             SaLowering &L)
+{
+    switch (W.tmpl) {
+    case 0: sa_lower_loop<0>(W, fact, ch, k, lane, L); break;
+    case 1: sa_lower_loop<1>(W, fact, ch, k, lane, L); break;
+    default: sa_lower_loop<2>(W, fact, ch, k, lane, L); break;
+    }
+}
+
+__device__ __forceinline__ void sa_row_any(const WlDev &W, const SaLowering &L, const uint32_t *ch, int k, int lane,
+                                           float *tile)
+{
+    TileSink sk{tile, lane};
+    switch (W.tmpl) {
+    case 0: sa_row<0>(W, L, k, lane, 0u, sk); break;
+    case 1: sa_row<1>(W, L, k, lane, ch[6], sk); break;
+    default: sa_row<2>(W, L, k, lane, ch[5], sk); break;
+    }
+}
+
+__global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G)
 {
     extern __shared__ __align__(128) unsigned char smraw[];
     SaSmem &sm = *(SaSmem *)smraw;
@@ -129,15 +151,26 @@ __global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P, TreeGeo G)
     __syncthreads();
     uint32_t ph[2] = {0u, 0u};
     uint64_t cs = 0;
+#ifdef AT_SA_PHASE_TIMING
+    long long t_prop = 0, t_feat = 0, t_walk = 0, t_rows = 0, t0 = clock64();
+#endif
     // every warp computes its share of the features of all 32 chains of the block
     auto features_phase = [&]() {
         uint32_t chl[MAXKNOBS];
 #pragma unroll
         for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[j][lane];
         const WlDev &Wl = P.S->w[sm.w[lane]];
-        feats_any(Wl, P.fact, chl, sm.tile, lane, warp, SA_NW);   // context rows, dealt over all warps
+        // L) loop extents, dealt over the warps
+        for (int k = warp; k < MAXLOOPS; k += SA_NW) sa_lower_any(Wl, P.fact, chl, k, lane, sm.low);
         __syncthreads();
-        if (warp < 6) relation_from_tile(sm.tile, lane, n_loops(Wl.tmpl), warp >> 1, warp & 1);
+        // R) context rows
+        for (int k = warp; k < MAXLOOPS; k += SA_NW) sa_row_any(Wl, sm.low, chl, k, lane, sm.tile);
+        __syncthreads();
+#ifdef AT_SA_PHASE_TIMING
+        t_rows += clock64() - t0;
+#endif
+        // T) relation features: warps (buffer, pair, threshold half)
+        if (warp < 12) relation_from_tile(sm.tile, lane, n_loops(Wl.tmpl), warp >> 2, (warp >> 1) & 1, warp & 1);
         __syncthreads();
     };
     features_phase();
@@ -151,6 +184,10 @@ __global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P, TreeGeo G)
         }
     }
 
+#ifdef AT_SA_PHASE_TIMING
+    t_prop = t_feat = t_walk = t_rows = 0;
+    t0 = clock64();
+#endif
     for (int s = 0; s < P.n_steps; ++s) {
         U4 r;
         if (warp == 0) {
@@ -175,8 +212,17 @@ __global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P, TreeGeo G)
             }
         }
         __syncthreads();
+#ifdef AT_SA_PHASE_TIMING
+        { long long t = clock64(); t_prop += t - t0; t0 = t; }
+#endif
         features_phase();
+#ifdef AT_SA_PHASE_TIMING
+        { long long t = clock64(); t_feat += t - t0; t0 = t; }
+#endif
         walk_pass<SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, lane, warp, sm.part, nullptr, 0, 0, false);
+#ifdef AT_SA_PHASE_TIMING
+        { long long t = clock64(); t_walk += t - t0; t0 = t; }
+#endif
         if (warp == 0) {
             const float E2 = gbt_combine(sm.part, lane, P.base);
             const float d = __fsub_rn(E2, E);
@@ -213,6 +259,12 @@ __global__ void __launch_bounds__(SA_NW * 32) sa_kernel(SaParams P, TreeGeo G)
         P.chain_idx[c] = idx;
         P.chain_E[c] = E;
     }
+#ifdef AT_SA_PHASE_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("sa phases (cycles/step, block 0, T=%d NC=%d): proposal+accept %lld features %lld (rows %lld) walk %lld\n",
+               G.T, G.NC, t_prop / max(P.n_steps, 1), t_feat / max(P.n_steps, 1), t_rows / max(P.n_steps, 1),
+               t_walk / max(P.n_steps, 1));
+#endif
 }
 
 size_t sa_smem_bytes(const TreeGeo &G)
