@@ -405,3 +405,81 @@ def test_fit_errors(at):
     with pytest.raises(at.ATError):
         c = torch.tensor([1.0, float("nan"), 2.0, 3.0], device="cuda")
         at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 4, c, torch.zeros(4, dtype=torch.int16, device="cuda"))
+
+
+# ------------------------------------------------------------------ full-size configurations, sampled
+def test_config3_full_chain_count_sampled(at):
+    """Config 3 launch shape: 65,536 chains over the 12 ResNet spaces, 1000-tree depth-8 energy
+    (fewer steps to keep the test short); chains sampled and replayed one by one by the oracle."""
+    ens = synth.ensemble(1000, 8, seed=1805)
+    steps, n = 6, 65536
+    temps = synth.temperatures(steps, synth.energy_scale(1000))
+    cw = (np.arange(n) % 12).astype(np.uint16)
+    sp = at.Space(synth.ALL_RESNET)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    res = at.sa_explore(sp, g, u64(np.zeros(n, np.uint64)), dev(temps), seed=1805, round_=0, k_out=128,
+                        chain_workload=dev(cw.view(np.int16)), init=True, accept_bits=True, visited=True)
+    torch.cuda.synchronize()
+    osp = O.OracleSpace([O.workload(**w) for w in synth.ALL_RESNET])
+    oe = O.OracleGbt(**ens)
+    for c in (0, 11, 12345, 40000, 65535):
+        r = osp.sa_explore(oe, 1, steps, 1805, 0, temps, chain_id_base=c, chain_workload=cw[c:c + 1])
+        assert_bits_equal(host_u64(res["visited_idx"][c:c + 1]), r["visited_idx"], f"chain {c} idx")
+        assert_bits_equal(res["visited_E"][c:c + 1].cpu().numpy(), r["visited_E"], f"chain {c} E")
+        assert_bits_equal(res["accept_bits"][c:c + 1].cpu().numpy().view(np.uint32), r["accept_bits"], f"chain {c}")
+    # per-workload top-k == distinct top-k of the (sample-verified) visited set
+    vE = res["visited_E"].cpu().numpy()
+    vI = host_u64(res["visited_idx"])
+    on = res["out_n"].cpu().numpy()
+    for w in (0, 5, 11):
+        E, I = vE[cw == w].ravel(), vI[cw == w].ravel()
+        o = np.lexsort((I, E))
+        _, first = np.unique(I[o], return_index=True)
+        keep = o[np.sort(first)][:128]
+        assert on[w] == 128
+        assert np.array_equal(host_u64(res["out_idx"][w]), I[keep])
+
+
+def test_config4_refit_full_sample_count(at):
+    """Config 4: 10^5 synthetic measured samples over the 9 MobileNet depthwise spaces (first trees
+    only -- the oracle is O(n F) per level); trees, leaves and the root histogram bit-exact."""
+    n = 100000
+    osp = O.OracleSpace([O.workload(**w) for w in synth.ALL_DW])
+    key = synth.group_keys(n, 9, seed=4)
+    sizes = np.array([osp.size(w) for w in range(9)], dtype=np.uint64)
+    loc = synth.uniform_indices(1 << 62, n, seed=5) % sizes[key]
+    idx = loc + np.array([osp.offset(w) for w in range(9)], dtype=np.uint64)[key]
+    Xo = osp.features(idx)
+    c = synth.labels(Xo, seed=6)
+    ref = O.fit_hist(Xo, c, key, n_trees=2, depth=6, want_hist0=True)
+    sp = at.Space(synth.ALL_DW)
+    Xg = sp.features(u64(idx))
+    assert_bits_equal(Xg[:, :n].cpu().numpy().T, Xo, "features")
+    h0 = torch.empty((468, 256, 2), dtype=torch.int64, device="cuda")
+    pred = torch.empty(n, dtype=torch.float32, device="cuda")
+    gm = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), n_trees=2, depth=6, hist0_out=h0, pred_out=pred)
+    ex = gm.export()
+    assert_bits_equal(h0.cpu().numpy(), ref["hist0"], "root histogram")
+    for k in ("feat", "thresh", "leaf"):
+        assert_bits_equal(ex[k], ref[k], k)
+    assert_bits_equal(pred.cpu().numpy(), ref["pred"], "fit predictions")
+
+
+def test_config5_sweep_sampled(at):
+    """Config 5: the (a n + c) mod |S| sweep over the 12 ResNet spaces with a 2000-tree depth-8
+    ensemble; scores and leaf slots of sampled candidates against the oracle."""
+    ens = synth.ensemble(2000, 8, seed=1805)
+    sp = at.Space(synth.ALL_RESNET)
+    n = 1 << 14
+    idx = synth.sweep_indices(sp.size(), 10 ** 7, n)
+    assert len(np.unique(idx)) == n
+    X = sp.features(u64(idx))
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    s, sl = g.predict(X, n=n, slots=True)
+    osp = O.OracleSpace([O.workload(**w) for w in synth.ALL_RESNET])
+    pick = np.random.default_rng(0).choice(n, 48, replace=False)
+    Xo = osp.features(idx[pick])
+    es, esl = O.OracleGbt(**ens).predict(Xo, slots=True)
+    assert_bits_equal(X[:, pick].cpu().numpy().T, Xo, "sampled features")
+    assert_bits_equal(s.cpu().numpy()[pick], es, "sampled scores")
+    assert_bits_equal(sl.cpu().numpy()[:, pick], esl, "sampled leaf slots")
