@@ -1,13 +1,17 @@
 // gbt.cu -- gbt_create / gbt_export / gbt_destroy / gbt_predict.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "gbt.cuh"
 
 namespace at {
 
-constexpr int PRED_NW = 8;   // warps per block (tree slices); 32 candidates per block
+constexpr int PRED_NW = 16;  // warps per block (tree slices); 32 candidates per tile
 
 TreeGeo make_geo(const at_gbt_s *g)
 {
@@ -30,27 +34,94 @@ TreeGeo make_geo(const at_gbt_s *g)
     return G;
 }
 
-__global__ void __launch_bounds__(PRED_NW * 32) predict_kernel(TreeGeo G, float base, int F,
-                                                              const float *__restrict__ X, int64_t n, int64_t ld,
-                                                              float *__restrict__ score, uint8_t *__restrict__ slots)
+// Persistent scorer: one block per SM loops over 32-candidate tiles.  The ensemble streams (or
+// stays resident) through the TMA tree pipeline of gbt.cuh; the candidate tiles are fetched by
+// 1-D bulk copies (one 128-B row segment per feature, issued by warp 0's lanes) into two tile
+// buffers, so the next tile's HBM read overlaps the current tile's tree walk.
+struct PredSmemHdr {
+    uint64_t tree_bar[2];
+    uint64_t tile_bar[2];
+};
+
+// candidate tile = n_box 2-D TMA boxes of {32 candidates, box_rows features} of X[F][ld]
+struct TileMap {
+    CUtensorMap map;
+    int n_box, box_rows;
+};
+
+// one tile = GRP groups of 32 candidates; group g of tile `tile` starts at candidate (tile GRP + g) 32
+template <int GRP>
+__device__ __forceinline__ void tile_issue(const TileMap &tm, int64_t tile, float *dst, int tile_rows, uint64_t *bar)
 {
+    mbar_arrive_expect_tx(bar, (uint32_t)(GRP * tm.n_box * tm.box_rows * 32 * 4));
+    for (int g = 0; g < GRP; ++g)
+        for (int b = 0; b < tm.n_box; ++b)
+            tma_load_2d(dst + g * tile_rows * 32 + b * tm.box_rows * 32, &tm.map, (int)((tile * GRP + g) * 32),
+                        b * tm.box_rows, bar);
+}
+
+// Persistent scorer: one block per SM loops over tiles of 32 GRP candidates.  The ensemble
+// streams (or stays resident) through the TMA tree pipeline of gbt.cuh; candidate tiles arrive by
+// 2-D TMA (tensor map over X[F][ld]).  GRP = 1: two tile buffers, the next tile's HBM read overlaps
+// the current walk (small, resident ensembles: HBM-bound).  GRP = 2: one buffer of 64 candidates,
+// so every streamed tree byte serves twice the candidates (large ensembles: L2-bound).
+template <int GRP>
+__global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, float base, int F, int tile_rows,
+                                                                 const float *__restrict__ X, int64_t n, int64_t ld,
+                                                                 float *__restrict__ score, uint8_t *__restrict__ slots,
+                                                                 int use_bulk, const __grid_constant__ TileMap tm)
+{
+    constexpr int NBUF = GRP == 1 ? 2 : 1;
     extern __shared__ __align__(128) unsigned char smraw[];
-    float *tile = (float *)smraw;                                   // [F][32]
-    float *part = tile + F * 32;                                    // [32][32]
-    uint64_t *bar = (uint64_t *)(part + 32 * 32);                   // [2]
-    uint8_t *bufs = (uint8_t *)(bar + 2) + 112;                     // 128-B aligned
+    PredSmemHdr &hd = *(PredSmemHdr *)smraw;
+    float *part = (float *)(smraw + 128);                      // [GRP][32][32]
+    float *tiles = part + GRP * 32 * 32;                       // [NBUF][GRP][tile_rows][32], tile_rows >= F
+    uint8_t *bufs = (uint8_t *)(tiles + NBUF * GRP * tile_rows * 32);   // tree buffers (rows are 128 B)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t cand = (int64_t)blockIdx.x * 32 + lane;
-    const bool ok = cand < n;
-    ts_start(G, bufs, bar);
-    // stage the candidate tile: warp w loads rows w, w + NW, ... (one 128-B line per row)
-    for (int f = warp; f < F; f += PRED_NW) tile[f * 32 + lane] = ok ? __ldcs(X + (int64_t)f * ld + cand) : 0.0f;
+    const int64_t n_tiles = (n + 32 * GRP - 1) / (32 * GRP);
+    const int64_t my_tiles = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int tstride = GRP * tile_rows * 32;
+    if (threadIdx.x == 0) {
+        mbar_init(&hd.tile_bar[0], 1);
+        mbar_init(&hd.tile_bar[1], 1);
+    }
+    ts_start(G, bufs, hd.tree_bar);   // also fences the barrier initialisation
     __syncthreads();
-    ts_wait_resident(G, bar);
+    if (threadIdx.x == 0 && use_bulk) {
+        for (int i = 0; i < NBUF && i < my_tiles; ++i)
+            tile_issue<GRP>(tm, blockIdx.x + i * gridDim.x, tiles + i * tstride, tile_rows, &hd.tile_bar[i]);
+    }
+    ts_wait_resident(G, hd.tree_bar);
     uint32_t ph[2] = {0u, 0u};
     uint64_t c = 0;
-    walk_pass<PRED_NW>(G, bufs, bar, ph, c, (uint64_t)G.NC, tile, lane, warp, part, slots, n, cand, ok);
-    if (warp == 0 && ok) score[cand] = gbt_combine(part, lane, base);
+    const uint64_t c_limit = (uint64_t)G.NC * (uint64_t)my_tiles;
+    for (int64_t i = 0; i < my_tiles; ++i) {
+        const int64_t tile = blockIdx.x + i * gridDim.x;
+        const int tb = (int)(i % NBUF);
+        float *tl = tiles + tb * tstride;
+        const int64_t cand0 = tile * 32 * GRP + lane;
+        bool ok[GRP];
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) ok[g] = cand0 + 32 * g < n;
+        if (use_bulk) {
+            mbar_wait(&hd.tile_bar[tb], (uint32_t)((i / NBUF) & 1));
+        } else {
+            for (int g = 0; g < GRP; ++g)
+                for (int f = warp; f < F; f += PRED_NW)
+                    tl[g * tile_rows * 32 + f * 32 + lane] = ok[g] ? X[(int64_t)f * ld + cand0 + 32 * g] : 0.0f;
+            __syncthreads();
+        }
+        walk_pass<PRED_NW, GRP>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part, slots, n,
+                                cand0, ok);
+        if (warp < GRP) {
+            if (ok[warp]) score[cand0 + 32 * warp] = gbt_combine(part + warp * 1024, lane, base);
+        }
+        __syncthreads();   // part[] and the tile buffer are free again
+        if (use_bulk && threadIdx.x == 0 && i + NBUF < my_tiles) {
+            fence_proxy_async();
+            tile_issue<GRP>(tm, tile + NBUF * gridDim.x, tl, tile_rows, &hd.tile_bar[tb]);
+        }
+    }
 }
 
 size_t tree_smem_bytes(const TreeGeo &G)
@@ -151,17 +222,65 @@ int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_s
     if (ld < n) return at::fail(AT_EMISMATCH, "gbt_predict: ld < n");
     cudaStream_t s = (cudaStream_t)stream;
     const at::TreeGeo G = at::make_geo(g);
-    const size_t smem = ((size_t)g->n_features * 32 + 32 * 32) * sizeof(float) + 16 + at::tree_smem_bytes(G);
-    if (smem > 227 * 1024) return at::fail(AT_EUNSUPPORTED, "gbt_predict: too many features for the smem tile");
-    static size_t attr = 0;
-    if (smem > attr) {
-        AT_CUDA_TRY(cudaFuncSetAttribute(at::predict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
+    const int F = g->n_features;
+    const int n_box = (F + 255) / 256, box_rows = (F + n_box - 1) / n_box, tile_rows = n_box * box_rows;
+    // GRP = 2 (64 candidates per tile, one buffer) when the ensemble streams and it fits
+    auto smem_for = [&](int grp) {
+        const int nbuf = grp == 1 ? 2 : 1;
+        return 128 + (size_t)grp * 32 * 32 * sizeof(float) + (size_t)nbuf * grp * tile_rows * 32 * sizeof(float) +
+               at::tree_smem_bytes(G);
+    };
+    constexpr size_t SMEM_MAX = 227 * 1024;
+    const int grp = (!G.resident && smem_for(2) <= SMEM_MAX) ? 2 : 1;
+    const size_t smem = smem_for(grp);
+    if (smem > SMEM_MAX) return at::fail(AT_EUNSUPPORTED, "gbt_predict: too many features for the smem tiles");
+    static size_t attr1 = 0, attr2 = 0;
+    if (grp == 1 && smem > attr1) {
+        AT_CUDA_TRY(cudaFuncSetAttribute(at::predict_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr1 = smem;
     }
-    const int64_t blocks = (n + 31) / 32;
+    if (grp == 2 && smem > attr2) {
+        AT_CUDA_TRY(cudaFuncSetAttribute(at::predict_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr2 = smem;
+    }
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        AT_CUDA_TRY(cudaGetDevice(&dev));
+        AT_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    // TMA tensor map over X[F][ld] (needs 16-B aligned rows); otherwise plain loads
+    at::TileMap tm{};
+    tm.n_box = n_box;
+    tm.box_rows = box_rows;
+    int use_bulk = (ld % 4 == 0) && ((uintptr_t)d_feat % 16 == 0);
+    if (use_bulk) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+        }
+        const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)F};
+        const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+        const cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+        const cuuint32_t estr[2] = {1u, 1u};
+        if (!encode || encode(&tm.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)d_feat, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            use_bulk = 0;
+    }
+    const int64_t tiles = (n + 32 * grp - 1) / (32 * grp);
+    const unsigned blocks = (unsigned)std::min<int64_t>(tiles, n_sm);
     at::ProfScope ps(AT_K_PREDICT, s);
-    at::predict_kernel<<<(unsigned)blocks, at::PRED_NW * 32, smem, s>>>(G, g->base, g->n_features, d_feat, n, ld,
-                                                                       d_score, d_leaf_slot);
+    if (grp == 1)
+        at::predict_kernel<1><<<blocks, at::PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+                                                                     d_leaf_slot, use_bulk, tm);
+    else
+        at::predict_kernel<2><<<blocks, at::PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+                                                                     d_leaf_slot, use_bulk, tm);
     AT_LAUNCH_CHECK("predict_kernel");
     return AT_OK;
 }

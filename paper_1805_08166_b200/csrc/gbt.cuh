@@ -57,36 +57,42 @@ __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64
     }
 }
 
-template <int NW>
-__device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const float *tile, int lane,
-                                           int warp, float *p, uint8_t *__restrict__ slots, int64_t slot_ld,
-                                           int64_t cand, bool cand_ok)
+// GRP candidate groups of 32 (group g's tile at tile + g * gstride floats) walk the same trees:
+// every tree byte staged in shared memory serves 32 * GRP candidates.
+template <int NW, int GRP>
+__device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const float *tile, int gstride,
+                                           int lane, int warp, float (&p)[GRP][32 / NW], uint8_t *__restrict__ slots,
+                                           int64_t slot_ld, int64_t cand0, const bool (&cand_ok)[GRP])
 {
     constexpr int NQ = 32 / NW;
-    constexpr int R = 2;                 // 32-tree rounds walked together: R * NQ independent walks
+    constexpr int R = GRP == 1 ? 2 : 1;  // 32-tree rounds walked together: R * NQ * GRP independent walks
     constexpr int NJ = R * NQ;
     const float *leaves = (const float *)(buf + (size_t)G.CH * G.ni * 8);
-    const uint8_t *tile_lane = (const uint8_t *)(tile + lane);   // feature f of this lane at + f * 128
     const int c0 = k * G.CH;
     const int c1 = min(c0 + G.CH, G.T);
     const int D = G.D, ni = G.ni, nl = G.nl;
     const uint32_t tree_bytes = (uint32_t)ni * 8u;
     for (int b64 = c0 & ~31; b64 < c1; b64 += 32 * R) {
         const uint8_t *tb[NJ];
-        uint32_t off[NJ];   // byte offset of the current node: node i at 8 i, children at 2 off + 8 / + 16
+        uint32_t off[GRP][NJ];   // byte offset of the current node: node i at 8 i, children at 2 off + 8 / + 16
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj) {
             const int t = b64 + 32 * (jj / NQ) + warp + (jj % NQ) * NW;
-            const int lt = (t >= c0 && t < c1) ? t - c0 : 0;
+            const int lt = (t >= c0 && t < c1) ? t - c0 : 0;   // absent trees walk tree 0, result unused
             tb[jj] = buf + (uint32_t)lt * tree_bytes;
-            off[jj] = 0;
+#pragma unroll
+            for (int g = 0; g < GRP; ++g) off[g][jj] = 0;
         }
         for (int d = 0; d < D; ++d) {
 #pragma unroll
-            for (int jj = 0; jj < NJ; ++jj) {
-                const uint2 nd = *(const uint2 *)(tb[jj] + off[jj]);
-                const float x = *(const float *)(tile_lane + (nd.x << 7));
-                off[jj] = 2u * off[jj] + (x < __uint_as_float(nd.y) ? 8u : 16u);
+            for (int g = 0; g < GRP; ++g) {
+                const uint8_t *tile_lane = (const uint8_t *)(tile + g * gstride + lane);   // feature f at + f * 128
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj) {
+                    const uint2 nd = *(const uint2 *)(tb[jj] + off[g][jj]);
+                    const float x = *(const float *)(tile_lane + (nd.x << 7));
+                    off[g][jj] = 2u * off[g][jj] + (x < __uint_as_float(nd.y) ? 8u : 16u);
+                }
             }
         }
         // leaves in ascending t within each residue class (round 0 before round 1)
@@ -94,35 +100,43 @@ __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf,
         for (int jj = 0; jj < NJ; ++jj) {
             const int t = b64 + 32 * (jj / NQ) + warp + (jj % NQ) * NW;
             if (t >= c0 && t < c1) {
-                const int slot = (int)(off[jj] >> 3) - ni;
-                p[jj % NQ] = __fadd_rn(p[jj % NQ], leaves[(t - c0) * nl + slot]);
-                if (slots && cand_ok) slots[(int64_t)t * slot_ld + cand] = (uint8_t)slot;
+#pragma unroll
+                for (int g = 0; g < GRP; ++g) {
+                    const int slot = (int)(off[g][jj] >> 3) - ni;
+                    p[g][jj % NQ] = __fadd_rn(p[g][jj % NQ], leaves[(t - c0) * nl + slot]);
+                    if (slots && cand_ok[g]) slots[(int64_t)t * slot_ld + cand0 + 32 * g] = (uint8_t)slot;
+                }
             }
         }
     }
 }
 
 // One full pass over the ensemble.  `c` is the block-wide stream counter (identical in every
-// thread); `c_limit` the total number of chunks the kernel will consume.  Ends with the
-// partials in part[q * 32 + lane] and a __syncthreads.
-template <int NW>
+// thread); `c_limit` the total number of chunks the kernel will consume.  Ends with group g's
+// partials in part[g * 1024 + q * 32 + lane] and a __syncthreads.
+template <int NW, int GRP>
 __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph, uint64_t &c,
-                                          uint64_t c_limit, const float *tile, int lane, int warp, float *part,
-                                          uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand, bool cand_ok)
+                                          uint64_t c_limit, const float *tile, int gstride, int lane, int warp,
+                                          float *part, uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand0,
+                                          const bool (&cand_ok)[GRP])
 {
     constexpr int NQ = 32 / NW;
-    float p[NQ];
+    float p[GRP][NQ];
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) p[j] = 0.0f;
+    for (int g = 0; g < GRP; ++g)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) p[g][j] = 0.0f;
     if (G.resident) {
         for (int k = 0; k < G.NC; ++k)
-            walk_chunk<NW>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, lane, warp, p, slots, slot_ld, cand, cand_ok);
+            walk_chunk<NW, GRP>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
+                                cand0, cand_ok);
     } else {
         for (int k = 0; k < G.NC; ++k, ++c) {
             const int b = (int)(c & 1);
             mbar_wait(&bar[b], ph[b]);
             ph[b] ^= 1u;
-            walk_chunk<NW>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, lane, warp, p, slots, slot_ld, cand, cand_ok);
+            walk_chunk<NW, GRP>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
+                                cand0, cand_ok);
             __syncthreads();   // every warp is done with buffer b
             if (threadIdx.x == 0 && c + 2 < c_limit) {
                 fence_proxy_async();
@@ -131,7 +145,9 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
         }
     }
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) part[(warp + j * NW) * 32 + lane] = p[j];
+    for (int g = 0; g < GRP; ++g)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) part[g * 1024 + (warp + j * NW) * 32 + lane] = p[g][j];
     __syncthreads();
 }
 

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     __syncthreads();
     uint32_t ph[2] = {0u, 0u};
     uint64_t cs = 0;
+    const bool kNoCand[1] = {false};
 #ifdef AT_SA_PHASE_TIMING
     long long t_prop = 0, t_feat = 0, t_walk = 0, t_rows = 0, t0 = clock64();
 #endif
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     };
     features_phase();
     ts_wait_resident(G, sm.bar);
-    walk_pass<SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, lane, warp, sm.part, nullptr, 0, 0, false);
+    walk_pass<SA_NW, 1>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, 0, lane, warp, sm.part, nullptr, 0, 0, kNoCand);
     if (warp == 0) {
         E = gbt_combine(sm.part, lane, P.base);
         if (live) {
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
 #endif
-        walk_pass<SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, lane, warp, sm.part, nullptr, 0, 0, false);
+        walk_pass<SA_NW, 1>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, 0, lane, warp, sm.part, nullptr, 0, 0, kNoCand);
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_walk += t - t0; t0 = t; }
 #endif
