@@ -312,6 +312,20 @@ __global__ void bin_layout_kernel(const int32_t *__restrict__ ncuts, int F, int3
     info[1] = mx;
 }
 
+// Exact 64-bit add into shared memory with two native 32-bit atomics (sm_100a has no native 64-bit
+// shared atomic add: the 64-bit form compiles to a CAS loop).  The low word's returned old value
+// tells whether this add wrapped; that carry goes into the high word with the value's high part,
+// so the pair always holds the exact modular 64-bit sum, whatever the interleaving.
+__device__ __forceinline__ void smem_add_u64(unsigned long long *cell, unsigned long long v)
+{
+    unsigned *w = (unsigned *)cell;   // little endian: w[0] low word, w[1] high word
+    const unsigned lo = (unsigned)v;
+    unsigned hi = (unsigned)(v >> 32);
+    const unsigned old = atomicAdd(&w[0], lo);
+    hi += (old + lo < old) ? 1u : 0u;
+    if (hi) atomicAdd(&w[1], hi);
+}
+
 // Warp-aggregated exact int64 histogram update.  64-bit shared-memory atomics are CAS loops on
 // sm_100a, so lanes hitting the same cell are first combined: peers = match_any(key); every
 // lane sums its group's int64 values by walking the group's lanes with full-warp shuffles
@@ -334,8 +348,8 @@ __device__ __forceinline__ void agg_add(unsigned long long *cells, int key, long
         }
     }
     if (key >= 0 && lane == __ffs(peers) - 1) {
-        atomicAdd(&cells[2 * key], (unsigned long long)sg);
-        atomicAdd(&cells[2 * key + 1], (unsigned long long)sh);
+        smem_add_u64(&cells[2 * key], (unsigned long long)sg);
+        smem_add_u64(&cells[2 * key + 1], (unsigned long long)sh);
     }
 }
 
@@ -366,7 +380,7 @@ __global__ void __launch_bounds__(256) hist_kernel(const uint8_t *__restrict__ b
         const int key = ok ? (node[i] - first) * nb + bf[i] : -1;
         const long long gv = ok ? g[i] : 0, hv = ok ? h[i] : 0;
         if (use_smem) {
-            agg_add(shist, key, gv, hv);
+            agg_add(shist, key, gv, hv);   // exact: 2 x 32-bit atomics per distinct cell
         } else {
             // global cells of this feature: [node][TB] with stride TB, offset boff[f]
             const int nd = ok ? node[i] - first : 0;
@@ -487,11 +501,20 @@ __global__ void __launch_bounds__(256, 4) hist_split_kernel(const uint8_t *__res
     for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) shist[q] = 0ull;
     __syncthreads();
     const uint8_t *bf = bins + (int64_t)f * n;
-    for (int64_t i0w = 0; i0w < n; i0w += blockDim.x) {
-        const int64_t i = i0w + threadIdx.x;
-        const bool ok = i < n;
-        const int key = ok ? (node[i] - first) * nb + bf[i] : -1;
-        agg_add(shist, key, ok ? g[i] : 0, ok ? h[i] : 0);
+    // samples in batches of 4 per thread: all loads of a batch are issued before any aggregation
+    for (int64_t i0w = 0; i0w < n; i0w += 4 * (int64_t)blockDim.x) {
+        int key[4];
+        long long gv[4], hv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0w + u * (int64_t)blockDim.x + threadIdx.x;
+            const bool ok = i < n;
+            key[u] = ok ? (node[i] - first) * nb + bf[i] : -1;
+            gv[u] = ok ? g[i] : 0;
+            hv[u] = ok ? h[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) agg_add(shist, key[u], gv[u], hv[u]);
     }
     __syncthreads();
     if (hist0)

@@ -1,0 +1,18 @@
+"""Per-launch summary of an ncu --set full report: duration, DRAM bytes, throughput, occupancy, IPC."""
+import csv, subprocess, sys
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
+rows = list(csv.reader(out))
+h, units = rows[0], rows[1]
+want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size"]
+idx = {w: h.index(w) for w in want if w in h}
+for r in rows[2:]:
+    print("---")
+    for w, i in idx.items():
+        v = r[i][:90] if w == "Kernel Name" else r[i]
+        print(f"  {w:60s} {v} {units[i] if w != 'Kernel Name' else ''}")
