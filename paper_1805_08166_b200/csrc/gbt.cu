@@ -13,7 +13,7 @@ namespace at {
 
 constexpr int PRED_NW = 16;  // warps per block (tree slices); 32 candidates per tile
 
-TreeGeo make_geo(const at_gbt_s *g)
+TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes)
 {
     TreeGeo G{};
     G.nodes = g->d_nodes;
@@ -24,8 +24,8 @@ TreeGeo make_geo(const at_gbt_s *g)
     G.ni = (1 << g->depth) - 1;
     G.nl = 1 << g->depth;
     const uint32_t per_tree = (uint32_t)G.ni * 8u + (uint32_t)G.nl * 4u;
-    int ch = (int)(TREE_BUF_BYTES / per_tree) / 16 * 16;
-    if (ch < 16) ch = 16;
+    int ch = (int)(buf_bytes / per_tree) / 2 * 2;   // even: chunk offsets and sizes stay 16-B aligned
+    if (ch < 2) ch = 2;
     if (ch > G.T_pad) ch = G.T_pad;
     G.CH = ch;
     G.NC = (G.T + ch - 1) / ch;

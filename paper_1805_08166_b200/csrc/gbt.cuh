@@ -23,14 +23,14 @@ struct TreeGeo {
     const uint2 *nodes;     // [T_pad][ni]
     const float *leaf;      // [T_pad][nl]
     int T, T_pad, D, ni, nl;
-    int CH;                 // trees per chunk (multiple of 16)
+    int CH;                 // trees per chunk (even: 16-B aligned bulk copies)
     int NC;                 // chunks per pass
     uint32_t chunk_bytes;   // CH * (ni * 8 + nl * 4)
     int resident;           // NC <= 2: loaded once, never re-streamed
 };
 
-TreeGeo make_geo(const at_gbt_s *g);
-constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // per buffer (two buffers)
+constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // default per buffer (two buffers)
+TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes = TREE_BUF_BYTES);
 
 __device__ __forceinline__ void ts_issue(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint64_t c)
 {

@@ -2,14 +2,15 @@
 // (Alg. 1 P:152-153 "run parallel simulated annealing ... using energy function f-hat";
 // P:187 "a batch of parallel Markov chains", persistent states; readings Q20-Q23, Q28).
 //
-// Block = 32 chains (lane = chain) x SA_NW warps.  Per step, warp 0 draws the
-// Philox proposal of each chain, applies the single-knob move to the chain's knob
-// vector (kept in registers: no decode after the start state) and writes the
-// proposal's 468 features into the block's shared tile [468][32]; then all SA_NW
-// warps walk the ensemble (each a residue class of trees, gbt.cuh) and warp 0 folds
-// the partials in the canonical order, takes the Metropolis decision and records the
-// proposal's key for the distinct top-K.  Chain state never leaves the SM between
-// steps; only 8 bytes per chain-step (the visited key) go to HBM.
+// Block = GRP groups of 32 chains (lane = chain) x SA_NW warps.  Per step, the owner warp of
+// each group draws the Philox proposal of its chains and applies the single-knob move to the
+// chain's knob vector (kept in registers: no decode after the start state); all warps then
+// compute the proposals' 468 features into shared tiles [468][32] (loop extents, context rows,
+// relation features: three barrier-separated phases dealt over the warps), walk the ensemble
+// (each warp a residue class of trees, gbt.cuh; trees stream in by TMA bulk copies), and the
+// owner warps fold the partials in the canonical order, take the Metropolis decisions and record
+// the proposals' keys for the distinct top-K.  Chain state never leaves the SM between steps;
+// only 8 bytes per chain-step (the visited key) go to HBM.
 #include "features.cuh"
 #include "gbt.cuh"
 #include "topk.cuh"
@@ -77,13 +78,14 @@ struct SaParams {
     uint64_t *keys;   // [n_chains][n_steps+1]
 };
 
-// shared-memory layout of sa_kernel
+// shared-memory layout of sa_kernel: GRP groups of 32 chains
+template <int GRP>
 struct SaSmem {
-    float tile[NFEAT * 32];
-    float part[32 * 32];
-    uint32_t ch[MAXKNOBS][32];
-    int32_t w[32];
-    SaLowering low;
+    float tile[GRP][NFEAT * 32];
+    float part[GRP][32 * 32];
+    uint32_t ch[GRP][MAXKNOBS][32];
+    int32_t w[GRP][32];
+    SaLowering low[GRP];
     uint64_t bar[2];
 };
 
@@ -108,33 +110,39 @@ __device__ __forceinline__ void sa_row_any(const WlDev &W, const SaLowering &L, 
     }
 }
 
+// Block = GRP groups of 32 chains (lane = chain) x SA_NW warps.  Warp g owns group g's chain
+// state; every warp takes part in every group's feature phases and tree walk, so each tree byte
+// staged in shared memory serves 32 GRP chains.
+template <int GRP>
 __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G)
 {
     extern __shared__ __align__(128) unsigned char smraw[];
-    SaSmem &sm = *(SaSmem *)smraw;
-    uint8_t *bufs = smraw + ((sizeof(SaSmem) + 127) / 128) * 128;
+    SaSmem<GRP> &sm = *(SaSmem<GRP> *)smraw;
+    uint8_t *bufs = smraw + ((sizeof(SaSmem<GRP>) + 127) / 128) * 128;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int c = blockIdx.x * 32 + lane;
-    const bool live = c < P.n_chains;
+    const int og = warp < GRP ? warp : 0;                  // the group whose state this warp owns
+    const bool owner = warp < GRP;
+    const int c = blockIdx.x * 32 * GRP + og * 32 + lane;  // the owner's chain
+    const bool live = owner && c < P.n_chains;
     const int64_t per = (int64_t)P.n_steps + 1;
     const uint64_t c_limit = (uint64_t)G.NC * (uint64_t)per;
 
     ts_start(G, bufs, sm.bar);
-    // warp-0 state (registers): knob vector, index and energy of the chain of this lane
+    // owner-warp state (registers): knob vector, index and energy of the lane's chain
     uint32_t ch[MAXKNOBS];
     uint64_t idx = 0, idx2 = 0;
     float E = 0.f;
     int w = 0;
-    const uint32_t g = P.chain_base + (uint32_t)c;
+    const uint32_t gid = P.chain_base + (uint32_t)c;
     uint32_t accw = 0;
     int pj = -1;
     uint32_t pv = 0;
-    if (warp == 0) {
+    if (owner) {
         if (live && P.chain_w) w = P.chain_w[c];
         const WlDev &W = P.S->w[w];
         if (live) {
             if (P.init) {
-                const U4 r = philox(P.seed, g, 0, P.round, TAG_SA_INIT);
+                const U4 r = philox(P.seed, gid, 0, P.round, TAG_SA_INIT);
                 idx = W.offset + mulhi64((uint64_t)r.x | ((uint64_t)r.y << 32), (uint64_t)W.size);
             } else {
                 idx = P.chain_idx[c];
@@ -144,41 +152,55 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         }
         decode_any(W, (uint32_t)(idx - W.offset), ch);
 #pragma unroll
-        for (int j = 0; j < MAXKNOBS; ++j) sm.ch[j][lane] = ch[j];
-        sm.w[lane] = w;
-        zero_cols_any(W.tmpl, sm.tile, lane);
+        for (int j = 0; j < MAXKNOBS; ++j) sm.ch[og][j][lane] = ch[j];
+        sm.w[og][lane] = w;
+        zero_cols_any(W.tmpl, sm.tile[og], lane);
     }
     __syncthreads();
     uint32_t ph[2] = {0u, 0u};
     uint64_t cs = 0;
-    const bool kNoCand[1] = {false};
+    bool no_slots[GRP];
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) no_slots[g] = false;
 #ifdef AT_SA_PHASE_TIMING
     long long t_prop = 0, t_feat = 0, t_walk = 0, t_rows = 0, t0 = clock64();
 #endif
-    // every warp computes its share of the features of all 32 chains of the block
+    // every warp computes its share of the features of all chains of the block
     auto features_phase = [&]() {
-        uint32_t chl[MAXKNOBS];
+        // L) loop extents: items (group, loop)
+        for (int it = warp; it < GRP * MAXLOOPS; it += SA_NW) {
+            const int g = it / MAXLOOPS, k = it - g * MAXLOOPS;
+            uint32_t chl[MAXKNOBS];
 #pragma unroll
-        for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[j][lane];
-        const WlDev &Wl = P.S->w[sm.w[lane]];
-        // L) loop extents, dealt over the warps
-        for (int k = warp; k < MAXLOOPS; k += SA_NW) sa_lower_any(Wl, P.fact, chl, k, lane, sm.low);
+            for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[g][j][lane];
+            sa_lower_any(P.S->w[sm.w[g][lane]], P.fact, chl, k, lane, sm.low[g]);
+        }
         __syncthreads();
-        // R) context rows
-        for (int k = warp; k < MAXLOOPS; k += SA_NW) sa_row_any(Wl, sm.low, chl, k, lane, sm.tile);
+        // R) context rows: items (group, row)
+        for (int it = warp; it < GRP * MAXLOOPS; it += SA_NW) {
+            const int g = it / MAXLOOPS, k = it - g * MAXLOOPS;
+            uint32_t chl[MAXKNOBS];
+#pragma unroll
+            for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[g][j][lane];
+            sa_row_any(P.S->w[sm.w[g][lane]], sm.low[g], chl, k, lane, sm.tile[g]);
+        }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
         t_rows += clock64() - t0;
 #endif
-        // T) relation features: warps (buffer, pair, threshold half)
-        if (warp < 12) relation_from_tile(sm.tile, lane, n_loops(Wl.tmpl), warp >> 2, (warp >> 1) & 1, warp & 1);
+        // T) relation features: items (group, buffer, pair, threshold half)
+        for (int it = warp; it < GRP * 12; it += SA_NW) {
+            const int g = it / 12, r = it - g * 12;
+            relation_from_tile(sm.tile[g], lane, n_loops(P.S->w[sm.w[g][lane]].tmpl), r >> 2, (r >> 1) & 1, r & 1);
+        }
         __syncthreads();
     };
     features_phase();
     ts_wait_resident(G, sm.bar);
-    walk_pass<SA_NW, 1>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, 0, lane, warp, sm.part, nullptr, 0, 0, kNoCand);
-    if (warp == 0) {
-        E = gbt_combine(sm.part, lane, P.base);
+    walk_pass<SA_NW, GRP>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp, &sm.part[0][0],
+                          nullptr, 0, 0, no_slots);
+    if (owner) {
+        E = gbt_combine(sm.part[og], lane, P.base);
         if (live) {
             P.keys[(int64_t)c * per] = ((uint64_t)fkey(E) << 32) | (uint64_t)(idx - P.S->w[w].offset);
             if (P.vis_E) { P.vis_E[(int64_t)c * per] = E; P.vis_idx[(int64_t)c * per] = idx; }
@@ -191,9 +213,9 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #endif
     for (int s = 0; s < P.n_steps; ++s) {
         U4 r;
-        if (warp == 0) {
+        if (owner) {
             const WlDev &W = P.S->w[w];
-            r = philox(P.seed, g, (uint32_t)s, P.round, TAG_SA_STEP);
+            r = philox(P.seed, gid, (uint32_t)s, P.round, TAG_SA_STEP);
             idx2 = idx;
             pj = -1;
             if (W.n_ns > 0) {
@@ -209,7 +231,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == j) ch[q] = v2;
 #pragma unroll
-                for (int q = 0; q < MAXKNOBS; ++q) if (q == j) sm.ch[q][lane] = v2;
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == j) sm.ch[og][q][lane] = v2;
             }
         }
         __syncthreads();
@@ -220,12 +242,13 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
 #endif
-        walk_pass<SA_NW, 1>(G, bufs, sm.bar, ph, cs, c_limit, sm.tile, 0, lane, warp, sm.part, nullptr, 0, 0, kNoCand);
+        walk_pass<SA_NW, GRP>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+                              &sm.part[0][0], nullptr, 0, 0, no_slots);
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_walk += t - t0; t0 = t; }
 #endif
-        if (warp == 0) {
-            const float E2 = gbt_combine(sm.part, lane, P.base);
+        if (owner) {
+            const float E2 = gbt_combine(sm.part[og], lane, P.base);
             const float d = __fsub_rn(E2, E);
             bool acc = d <= 0.0f;
             if (!acc) {
@@ -243,7 +266,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == pj) ch[q] = pv;   // undo the move
 #pragma unroll
-                for (int q = 0; q < MAXKNOBS; ++q) if (q == pj) sm.ch[q][lane] = pv;
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == pj) sm.ch[og][q][lane] = pv;
             }
             if (live) {
                 const int64_t at = (int64_t)c * per + s + 1;
@@ -256,21 +279,22 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
             if ((s & 31) == 31) accw = 0;
         }
     }
-    if (warp == 0 && live) {
+    if (live) {
         P.chain_idx[c] = idx;
         P.chain_E[c] = E;
     }
 #ifdef AT_SA_PHASE_TIMING
     if (blockIdx.x == 0 && threadIdx.x == 0)
-        printf("sa phases (cycles/step, block 0, T=%d NC=%d): proposal+accept %lld features %lld (rows %lld) walk %lld\n",
-               G.T, G.NC, t_prop / max(P.n_steps, 1), t_feat / max(P.n_steps, 1), t_rows / max(P.n_steps, 1),
-               t_walk / max(P.n_steps, 1));
+        printf("sa phases (cycles/step, block 0, GRP=%d T=%d NC=%d CH=%d): proposal+accept %lld features %lld (rows %lld) "
+               "walk %lld\n", GRP, G.T, G.NC, G.CH, t_prop / max(P.n_steps, 1), t_feat / max(P.n_steps, 1),
+               t_rows / max(P.n_steps, 1), t_walk / max(P.n_steps, 1));
 #endif
 }
 
+template <int GRP>
 size_t sa_smem_bytes(const TreeGeo &G)
 {
-    return ((sizeof(SaSmem) + 127) / 128) * 128 + 2 * (size_t)G.chunk_bytes;
+    return ((sizeof(SaSmem<GRP>) + 127) / 128) * 128 + 2 * (size_t)G.chunk_bytes;
 }
 
 }  // namespace at
@@ -318,18 +342,37 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     P.vis_E = o->d_visited_E;
     P.vis_idx = o->d_visited_idx;
     P.keys = keys;
-    const at::TreeGeo G = at::make_geo(g);
-    const size_t smem = at::sa_smem_bytes(G);
-    if (smem > 227 * 1024) return at::fail(AT_EUNSUPPORTED, "sa_explore: shared memory budget exceeded");
-    static size_t attr = 0;
-    if (smem > attr) {
-        AT_CUDA_TRY(cudaFuncSetAttribute(at::sa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
+    // two 32-chain groups per block when there are enough chains to fill the SMs twice over and the
+    // ensemble streams (each streamed tree byte then serves 64 chains); otherwise one group
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        AT_CUDA_TRY(cudaGetDevice(&dev));
+        AT_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    constexpr size_t SMEM_MAX = 227 * 1024;
+    const at::TreeGeo G1 = at::make_geo(g);
+    const size_t hdr2 = ((sizeof(at::SaSmem<2>) + 127) / 128) * 128;
+    const at::TreeGeo G2 = at::make_geo(g, (uint32_t)((SMEM_MAX - hdr2) / 2));
+    const bool use2 = !G1.resident && o->n_chains >= 2 * 64 * n_sm && at::sa_smem_bytes<2>(G2) <= SMEM_MAX;
+    const at::TreeGeo G = use2 ? G2 : G1;
+    const size_t smem = use2 ? at::sa_smem_bytes<2>(G) : at::sa_smem_bytes<1>(G);
+    if (smem > SMEM_MAX) return at::fail(AT_EUNSUPPORTED, "sa_explore: shared memory budget exceeded");
+    static size_t attr1 = 0, attr2 = 0;
+    if (!use2 && smem > attr1) {
+        AT_CUDA_TRY(cudaFuncSetAttribute(at::sa_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr1 = smem;
+    }
+    if (use2 && smem > attr2) {
+        AT_CUDA_TRY(cudaFuncSetAttribute(at::sa_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr2 = smem;
     }
     {
         at::ProfScope ps(AT_K_SA, s);
-        const unsigned blocks = (unsigned)((o->n_chains + 31) / 32);
-        at::sa_kernel<<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
+        const int cpb = use2 ? 64 : 32;
+        const unsigned blocks = (unsigned)((o->n_chains + cpb - 1) / cpb);
+        if (use2) at::sa_kernel<2><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
+        else at::sa_kernel<1><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
         AT_LAUNCH_CHECK("sa_kernel");
     }
     for (int w = 0; w < sp->host.n_w; ++w) {
