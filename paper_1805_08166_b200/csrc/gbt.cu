@@ -25,6 +25,7 @@ TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes)
     G.nl = 1 << g->depth;
     const uint32_t per_tree = (uint32_t)G.ni * 8u + (uint32_t)G.nl * 4u;
     int ch = (int)(buf_bytes / per_tree) / 2 * 2;   // even: chunk offsets and sizes stay 16-B aligned
+    if (ch >= 32) ch = ch / 32 * 32;                 // whole 32-tree rounds: no idle walk slots
     if (ch < 2) ch = 2;
     if (ch > G.T_pad) ch = G.T_pad;
     G.CH = ch;
