@@ -208,9 +208,15 @@ def run_ours(args):
     sa_avg = sa_ms / max(sa_n, 1)
     achieved = node_steps / (sa_avg / 1e3) / 1e9
     shares = {k: round(v[1] / max(sum(step_ms), 1e-9), 4) for k, v in prof.items() if v[0]}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath)).get("sa_kernel", {})
+        if t:
+            traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
     roofline = {"kernel": "sa_kernel", "bound": "alu", "achieved": round(achieved, 2), "peak": round(lds_peak, 1),
                 "unit": "Gnode-steps/s", "frac": round(achieved / lds_peak, 4),
-                "traffic": None, "peak_source": "148 SMs x 16 node-steps/clk (two 128-B L1/shared wavefronts per "
+                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)", "peak_source": "148 SMs x 16 node-steps/clk (two 128-B L1/shared wavefronts per "
                                                  "warp node-step) x sm_max_mhz of MEASURED_PEAKS.json",
                 "avg_launch_ms": round(sa_avg, 4), "step_share": shares}
 
