@@ -620,6 +620,75 @@ __global__ void __launch_bounds__(256) split_node_kernel(const double *__restric
     }
 }
 
+// Split decision + partition in one launch (single rank, moderate n): every block decides all nn
+// nodes of the level (warp per node; the per-feature bests are read 8 at a time so the loads are
+// in flight together), block 0 stores the tree nodes and the dead flags, and each block then moves
+// its samples to their children.  Saves a launch and a dependent round trip per level.
+__global__ void __launch_bounds__(256) decide_partition_kernel(const double *__restrict__ best_gain,
+                                                               const int32_t *__restrict__ best_s, int F, int first,
+                                                               int nn, const float *__restrict__ cuts, int B,
+                                                               uint8_t *__restrict__ dead, int32_t *__restrict__ split_f,
+                                                               int32_t *__restrict__ split_s,
+                                                               uint16_t *__restrict__ tree_feat,
+                                                               float *__restrict__ tree_thr,
+                                                               const uint8_t *__restrict__ bins, int64_t n,
+                                                               int32_t *__restrict__ node)
+{
+    __shared__ int s_f[64], s_s[64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int q = warp; q < nn; q += blockDim.x >> 5) {
+        const int nd = first + q;
+        SplitBest best{0.0, -1, 0};
+        if (!dead[nd]) {
+            const double *bgq = best_gain + (int64_t)q * F;
+            const int32_t *bsq = best_s + (int64_t)q * F;
+            for (int f0 = 0; f0 < F; f0 += 32 * 8) {
+                double gv[8];
+                int sv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int f = f0 + 32 * u + lane;
+                    sv[u] = f < F ? bsq[f] : 0;
+                    gv[u] = f < F ? bgq[f] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (sv[u] > 0) {
+                        SplitBest c{gv[u], f0 + 32 * u + lane, sv[u]};
+                        if (split_better(c, best)) best = c;
+                    }
+                }
+            }
+        }
+        best = warp_best(best);
+        if (lane == 0) {
+            s_f[q] = best.f;
+            s_s[q] = best.s;
+            if (blockIdx.x == 0) {
+                if (best.f < 0) {
+                    tree_feat[nd] = 0;
+                    tree_thr[nd] = __int_as_float(0x7f800000);
+                    split_f[nd] = -1;
+                    dead[2 * nd + 1] = 1;
+                    dead[2 * nd + 2] = 1;
+                } else {
+                    tree_feat[nd] = (uint16_t)best.f;
+                    tree_thr[nd] = cuts[(int64_t)best.f * (B - 1) + best.s - 1];
+                    split_f[nd] = best.f;
+                    split_s[nd] = best.s;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nd = node[i];
+    const int q = nd - first;
+    const int sf = s_f[q];
+    node[i] = (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= s_s[q]) ? 2 * nd + 2 : 2 * nd + 1;
+}
+
 __global__ void partition_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ split_f,
                                  const int32_t *__restrict__ split_s, int32_t *__restrict__ node)
 {
@@ -828,9 +897,15 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                         hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hist, boff, F, B,
                                                                                      o->d_hist0_out);
                     ProfScope ps(AT_K_FIT_SPLIT, s);
-                    split_node_kernel<<<nn, 256, 0, s>>>(best_gain, best_s, F, first, nn, cuts, B, dead,
-                                                                  split_f, split_s, tf, tt);
-                    partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
+                    if (n <= 65536 && nn <= 64) {
+                        decide_partition_kernel<<<nblk(n, 256), 256, 0, s>>>(best_gain, best_s, F, first, nn, cuts, B,
+                                                                            dead, split_f, split_s, tf, tt, bins, n,
+                                                                            node);
+                    } else {
+                        split_node_kernel<<<nn, 256, 0, s>>>(best_gain, best_s, F, first, nn, cuts, B, dead,
+                                                             split_f, split_s, tf, tt);
+                        partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
+                    }
                     AT_LAUNCH_CHECK("split/partition");
                     continue;
                 }
