@@ -483,3 +483,42 @@ def test_config5_sweep_sampled(at):
     assert_bits_equal(X[:, pick].cpu().numpy().T, Xo, "sampled features")
     assert_bits_equal(s.cpu().numpy()[pick], es, "sampled scores")
     assert_bits_equal(sl.cpu().numpy()[:, pick], esl, "sampled leaf slots")
+
+
+# ------------------------------------------------------------------ Algorithm 1 end to end
+def test_algorithm1_rounds_match_oracle(at):
+    """Three rounds of Algorithm 1 (SA -> select -> measure -> refit, persistent chains) through the
+    C-ABI and through the oracle: identical selections, costs and final models every round."""
+    from paper_1805_08166_b200.tune import TuneConfig, Tuner
+    wl = dict(kind=0, n=64, m=128, k=32)
+    cfg = TuneConfig(n_chains=40, n_steps=25, b=16, lam=2, eps=0.125, alpha=0.1, n_trees=6, depth=4, seed=77)
+    osp = O.OracleSpace([O.workload(**wl)])
+
+    def measure(idx):   # stand-in for hardware run time (P:63): a fixed function of the schedule
+        return synth.labels(osp.features(np.asarray(idx, dtype=np.uint64)), seed=99)
+
+    ens0 = synth.ensemble(30, 5, seed=3)
+    tuner = Tuner(wl, at.Gbt(ens0["feat"], ens0["thresh"], ens0["leaf"]), measure, cfg)
+    # oracle replay of the same loop
+    model = O.OracleGbt(**ens0)
+    chains, measured, costs = None, [], []
+    for r in range(3):
+        sel_gpu = tuner.step()
+        temps = synth.temperatures(cfg.n_steps, synth.energy_scale(model.n_trees), cfg.t_ratio)
+        res = osp.sa_explore(model, cfg.n_chains, cfg.n_steps, cfg.seed, r, temps, chain_idx=chains)
+        chains = res["chain_idx"]
+        (pi, pe), = osp.topk(res["visited_E"], res["visited_idx"], cfg.lam * cfg.b, measured=measured)
+        sel = osp.select(0, pi, pe, cfg.b, cfg.eps, cfg.alpha, cfg.seed, r, measured=measured)
+        assert np.array_equal(sel_gpu, sel), f"round {r}"
+        measured += sel.tolist()
+        costs += measure(sel).tolist()
+        X = osp.features(np.array(measured, dtype=np.uint64))
+        fit = O.fit_hist(X, np.array(costs, np.float32), np.zeros(len(measured), np.uint16), n_trees=cfg.n_trees,
+                         depth=cfg.depth, seed=cfg.seed + r)
+        model = O.OracleGbt(fit["feat"], fit["thresh"], fit["leaf"])
+        ex = tuner.model.export()
+        for k in ("feat", "thresh", "leaf"):
+            assert_bits_equal(ex[k], fit[k], f"round {r} model {k}")
+        assert np.array_equal(host_u64(tuner.state.chain_idx), chains), f"round {r} chains"
+    assert len(set(tuner.state.measured)) == len(tuner.state.measured) == 3 * cfg.b      # never re-measured
+    assert tuner.state.best_cost == min(costs)
