@@ -57,58 +57,77 @@ __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64
     }
 }
 
-// GRP candidate groups of 32 (group g's tile at tile + g * gstride floats) walk the same trees:
-// every tree byte staged in shared memory serves 32 * GRP candidates.
+// A batch of NB trees t = t0, t0 + NW, ... (all owned by this warp: t = warp mod NW) walked for
+// GRP candidate groups at once: NB * GRP independent dependency chains.
+template <int NW, int GRP, int NB>
+__device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf, int c0, int t0, const float *tile,
+                                           int gstride, int lane, float (&p)[GRP][32 / NW],
+                                           uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand0,
+                                           const bool (&cand_ok)[GRP])
+{
+    constexpr int NQ = 32 / NW;
+    const float *leaves = (const float *)(buf + (size_t)G.CH * G.ni * 8);
+    const int D = G.D, ni = G.ni, nl = G.nl;
+    const uint32_t tree_bytes = (uint32_t)ni * 8u;
+    const uint8_t *tb[NB];
+    uint32_t off[GRP][NB];   // byte offset of the current node: node i at 8 i, children at 2 off + 8 / + 16
+#pragma unroll
+    for (int jj = 0; jj < NB; ++jj) {
+        tb[jj] = buf + (uint32_t)(t0 + jj * NW - c0) * tree_bytes;
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) off[g][jj] = 0;
+    }
+    for (int d = 0; d < D; ++d) {
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) {
+            const uint8_t *tile_lane = (const uint8_t *)(tile + g * gstride + lane);   // feature f at + f * 128
+#pragma unroll
+            for (int jj = 0; jj < NB; ++jj) {
+                const uint2 nd = *(const uint2 *)(tb[jj] + off[g][jj]);
+                const float x = *(const float *)(tile_lane + (nd.x << 7));
+                off[g][jj] = 2u * off[g][jj] + (x < __uint_as_float(nd.y) ? 8u : 16u);
+            }
+        }
+    }
+    // leaves in ascending t: tree t adds to its residue class q = t mod 32, slot (q - warp) / NW = q / NW
+#pragma unroll
+    for (int jj = 0; jj < NB; ++jj) {
+        const int t = t0 + jj * NW;
+        const int j = (t & 31) / NW;
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) {
+            const int slot = (int)(off[g][jj] >> 3) - ni;
+            const float lv = leaves[(t - c0) * nl + slot];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                if (q == j) p[g][q] = __fadd_rn(p[g][q], lv);
+            if (slots && cand_ok[g]) slots[(int64_t)t * slot_ld + cand0 + 32 * g] = (uint8_t)slot;
+        }
+    }
+}
+
+// Walk one staged chunk [c0, c1): every warp takes the trees of its residue classes (t = warp mod NW)
+// in ascending order, in batches of up to 4 / GRP trees; no walk slot is spent on an absent tree,
+// whatever the chunk size.  GRP candidate groups of 32 (group g's tile at tile + g * gstride floats)
+// share every staged tree byte.
 template <int NW, int GRP>
 __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const float *tile, int gstride,
                                            int lane, int warp, float (&p)[GRP][32 / NW], uint8_t *__restrict__ slots,
                                            int64_t slot_ld, int64_t cand0, const bool (&cand_ok)[GRP])
 {
-    constexpr int NQ = 32 / NW;
-    constexpr int R = GRP == 1 ? 2 : 1;  // 32-tree rounds walked together: R * NQ * GRP independent walks
-    constexpr int NJ = R * NQ;
-    const float *leaves = (const float *)(buf + (size_t)G.CH * G.ni * 8);
+    constexpr int NBMAX = GRP == 1 ? 4 : 2;
     const int c0 = k * G.CH;
     const int c1 = min(c0 + G.CH, G.T);
-    const int D = G.D, ni = G.ni, nl = G.nl;
-    const uint32_t tree_bytes = (uint32_t)ni * 8u;
-    for (int b64 = c0 & ~31; b64 < c1; b64 += 32 * R) {
-        const uint8_t *tb[NJ];
-        uint32_t off[GRP][NJ];   // byte offset of the current node: node i at 8 i, children at 2 off + 8 / + 16
-#pragma unroll
-        for (int jj = 0; jj < NJ; ++jj) {
-            const int t = b64 + 32 * (jj / NQ) + warp + (jj % NQ) * NW;
-            const int lt = (t >= c0 && t < c1) ? t - c0 : 0;   // absent trees walk tree 0, result unused
-            tb[jj] = buf + (uint32_t)lt * tree_bytes;
-#pragma unroll
-            for (int g = 0; g < GRP; ++g) off[g][jj] = 0;
-        }
-        for (int d = 0; d < D; ++d) {
-#pragma unroll
-            for (int g = 0; g < GRP; ++g) {
-                const uint8_t *tile_lane = (const uint8_t *)(tile + g * gstride + lane);   // feature f at + f * 128
-#pragma unroll
-                for (int jj = 0; jj < NJ; ++jj) {
-                    const uint2 nd = *(const uint2 *)(tb[jj] + off[g][jj]);
-                    const float x = *(const float *)(tile_lane + (nd.x << 7));
-                    off[g][jj] = 2u * off[g][jj] + (x < __uint_as_float(nd.y) ? 8u : 16u);
-                }
-            }
-        }
-        // leaves in ascending t within each residue class (round 0 before round 1)
-#pragma unroll
-        for (int jj = 0; jj < NJ; ++jj) {
-            const int t = b64 + 32 * (jj / NQ) + warp + (jj % NQ) * NW;
-            if (t >= c0 && t < c1) {
-#pragma unroll
-                for (int g = 0; g < GRP; ++g) {
-                    const int slot = (int)(off[g][jj] >> 3) - ni;
-                    p[g][jj % NQ] = __fadd_rn(p[g][jj % NQ], leaves[(t - c0) * nl + slot]);
-                    if (slots && cand_ok[g]) slots[(int64_t)t * slot_ld + cand0 + 32 * g] = (uint8_t)slot;
-                }
-            }
-        }
-    }
+    int t0 = c0 + ((warp - c0) % NW + NW) % NW;
+    for (; t0 + (NBMAX - 1) * NW < c1; t0 += NBMAX * NW)
+        walk_batch<NW, GRP, NBMAX>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+    const int rest = t0 < c1 ? (c1 - 1 - t0) / NW + 1 : 0;   // warp-uniform
+    if (NBMAX == 4 && rest == 3)
+        walk_batch<NW, GRP, 3>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+    else if (rest >= 2)
+        walk_batch<NW, GRP, 2>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+    else if (rest == 1)
+        walk_batch<NW, GRP, 1>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
 }
 
 // One full pass over the ensemble.  `c` is the block-wide stream counter (identical in every
