@@ -321,20 +321,32 @@ __device__ __forceinline__ void sa_row(const WlDev &W, const SaLowering &L, int 
     if (k >= NL) return;
     // all extents of this chain at once (independent loads), then predicated products:
     // A_a and bottom-up over the loops inside k, top-down over the loops outside k
+    // The axis of loop l is a compile-time constant except for the three reordered loops
+    // (T_CONV 9..11 over {3,4,5}, T_DW 13..15 over {0,1,2}), whose axis perm3 of knob p picks.
     uint32_t ev[NL];
-    int av[NL];
 #pragma unroll
-    for (int l = 0; l < NL; ++l) { ev[l] = L.ext[l][lane]; av[l] = L.axis[l][lane]; }
+    for (int l = 0; l < NL; ++l) ev[l] = L.ext[l][lane];
     uint32_t A[NA];
 #pragma unroll
     for (int q = 0; q < NA; ++q) A[q] = 1;
     uint32_t bu = 1, td = 1;
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
-        const bool inner = l > k;
+        const uint32_t m = l > k ? ev[l] : 1u;
+        if (TMPL == 1 && l >= 9 && l < 12) {
+            const uint32_t al = perm3(p, l - 9);
 #pragma unroll
-        for (int q = 0; q < NA; ++q) A[q] = (inner && av[l] == q) ? A[q] * ev[l] : A[q];
-        bu = inner ? bu * ev[l] : bu;
+            for (int q = 0; q < 3; ++q) A[3 + q] = al == (uint32_t)q ? A[3 + q] * m : A[3 + q];
+        } else if (TMPL == 2 && l >= 13 && l < 16) {
+            const uint32_t al = perm3(p, l - 13);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) A[q] = al == (uint32_t)q ? A[q] * m : A[q];
+        } else {
+            int al, lv;
+            loop_axis_level<TMPL>(l, p, al, lv);
+            A[al] *= m;
+        }
+        bu *= m;
         td = l < k ? td * ev[l] : td;
     }
     uint32_t ek = 0;
@@ -403,29 +415,33 @@ __device__ __forceinline__ void sa_row(const WlDev &W, const SaLowering &L, int 
 }
 
 // Relation features of buffer b, pair p (0: reuse, 1: top-down) from context rows already in a
-// smem tile [f][32] (rows_only pass).  The integer touch count is read back as its fp32
-// conversion: for thresholds 2^t <= 2^20 < 2^24 the comparison is exact (RN is monotone and
-// 2^t is representable), so this equals the integer test of the one-pass version.  Every
-// Z value here is > 0 (reuse > 0, top-down >= 1), so "max over an empty set = 0" is simply a
-// max seeded with 0: R_t = max(0, max_{k : T_k < 2^t} Z_k), branch-free over a static t loop.
-// (half h computes thresholds t = 10 h + 1 .. 10 h + 10)
-__device__ __forceinline__ void relation_from_tile(float *tile, int lane, int NL, int b, int p, int h)
+// smem tile [f][32] (rows-only pass).  Row k qualifies for threshold 2^t iff T_k < 2^t, i.e. iff
+// t >= bitlen(T_k) (T_k >= 1), so R_t = max(0, max_{k : bitlen(T_k) <= t} Z_k): each row deposits
+// its Z at slot max(1, bitlen(T_k)) (a per-lane max in the output rows themselves), then a prefix
+// max over t finishes.  bitlen is read from the exponent of the fp32 touch value: exact for
+// T < 2^24, and any larger T has bitlen > 20 either way.  Every Z is > 0 (reuse > 0, top-down
+// >= 1), so the empty-set value 0 is the max's identity.
+__device__ __forceinline__ void relation_from_tile(float *tile, int lane, int NL, int b, int p)
 {
     const int colT = 10 + 3 * b, colZ = p == 0 ? 11 + 3 * b : 8;
-    float R[10];
+    float *R = tile + (342 + 40 * b + 20 * p) * 32 + lane;   // R[(t - 1) * 32], t = 1..20
 #pragma unroll
-    for (int t = 0; t < 10; ++t) R[t] = 0.0f;
-#pragma unroll
-    for (int k = 0; k < MAXLOOPS; ++k) {
-        // absent rows (k >= NL) are all-zero and must not qualify: read them as T = +inf
-        const float T = k < NL ? tile[(19 * k + colT) * 32 + lane] : __int_as_float(0x7f800000);
+    for (int t = 0; t < 20; ++t) R[t * 32] = 0.0f;
+    for (int k = 0; k < NL; ++k) {
+        const float T = tile[(19 * k + colT) * 32 + lane];
         const float z = tile[(19 * k + colZ) * 32 + lane];
-#pragma unroll
-        for (int t = 0; t < 10; ++t) R[t] = fmaxf(R[t], T < __int_as_float((128 + 10 * h + t) << 23) ? z : 0.0f);
+        const int e = (int)((__float_as_uint(T) >> 23) & 0xFF) - 126;   // bitlen(T) for T >= 1
+        if (e <= 20) {
+            float *slot = R + (e < 1 ? 0 : e - 1) * 32;
+            *slot = fmaxf(*slot, z);
+        }
     }
-    const int out = 342 + 40 * b + 20 * p + 10 * h;
+    float m = 0.0f;
 #pragma unroll
-    for (int t = 0; t < 10; ++t) tile[(out + t) * 32 + lane] = R[t];
+    for (int t = 0; t < 20; ++t) {
+        m = fmaxf(m, R[t * 32]);
+        R[t * 32] = m;
+    }
 }
 
 // columns that are zero for every candidate of a template (absent loop rows + padding)

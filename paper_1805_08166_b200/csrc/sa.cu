@@ -188,10 +188,10 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #ifdef AT_SA_PHASE_TIMING
         t_rows += clock64() - t0;
 #endif
-        // T) relation features: items (group, buffer, pair, threshold half)
-        for (int it = warp; it < GRP * 12; it += SA_NW) {
-            const int g = it / 12, r = it - g * 12;
-            relation_from_tile(sm.tile[g], lane, n_loops(P.S->w[sm.w[g][lane]].tmpl), r >> 2, (r >> 1) & 1, r & 1);
+        // T) relation features: items (group, buffer, pair)
+        for (int it = warp; it < GRP * 6; it += SA_NW) {
+            const int g = it / 6, r = it - g * 6;
+            relation_from_tile(sm.tile[g], lane, n_loops(P.S->w[sm.w[g][lane]].tmpl), r >> 1, r & 1);
         }
         __syncthreads();
     };
