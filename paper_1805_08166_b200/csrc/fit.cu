@@ -224,6 +224,53 @@ __global__ void positions_kernel(const uint16_t *__restrict__ key, const int32_t
     member[woff[k] + y] = (int32_t)i;
 }
 
+// One pair's Eq. 2 contribution to member a (cost ca, prediction fa) from partner (cc, fc), both
+// orders of the pair, quantised to 2^-32 fixed point.
+__device__ __forceinline__ void pair_term(float ca, float fa, float cc, float fc, long long &ga, long long &ha)
+{
+    if (cc == ca) return;                   // sign(c_i - c_j) = 0 contributes nothing
+    const bool hi = ca > cc;                // a is the slower (i) of the pair
+    const float fi = hi ? fa : fc, fj = hi ? fc : fa;
+    const float d = __fsub_rn(fj, fi);
+    const float e = exp_det(-d);
+    const float rho = __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
+    const float hh = __fmul_rn(rho, __fsub_rn(1.0f, rho));
+    const long long q = __double2ll_rn((double)rho * 4294967296.0);
+    const long long qh = __double2ll_rn((double)hh * 4294967296.0);
+    ga += hi ? -2 * q : 2 * q;              // both orders of Eq. 2 carry the same term
+    ha += 2 * qh;
+}
+
+// Eq. 2 gradients of one group (members mem[0..m), costs sc[], predictions sp[] in shared memory),
+// written to g[mem[a]], h[mem[a]].  SUB threads per member: thread (a, r) accumulates member a's
+// share of its pairs with members c = r (mod SUB) (no atomics; each pair's rho is computed
+// identically by both members), the SUB partial int64 sums are then added with xor shuffles
+// (exact, order-free).
+__device__ __forceinline__ void group_pair_grads(const int32_t *mem, int m, const float *sc, const float *sp,
+                                                 int64_t *__restrict__ g, int64_t *__restrict__ h)
+{
+    constexpr int SUB = 4;
+    for (int base = 0; base < m * SUB; base += blockDim.x) {
+        const int tix = base + (int)threadIdx.x;
+        const int a = tix / SUB, r = tix % SUB;
+        long long ga = 0, ha = 0;
+        if (a < m) {
+            const float ca = sc[a], fa = sp[a];
+            for (int c = r; c < m; c += SUB)
+                if (c != a) pair_term(ca, fa, sc[c], sp[c], ga, ha);
+        }
+#pragma unroll
+        for (int off = 1; off < SUB; off <<= 1) {
+            ga += __shfl_xor_sync(0xFFFFFFFFu, ga, off);
+            ha += __shfl_xor_sync(0xFFFFFFFFu, ha, off);
+        }
+        if (a < m && r == 0) {
+            g[mem[a]] = ga;
+            h[mem[a]] = ha;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) grads_kernel(const int32_t *__restrict__ member,
                                                     const int32_t *__restrict__ counts,
                                                     const int32_t *__restrict__ woff,
@@ -256,41 +303,7 @@ __global__ void __launch_bounds__(256) grads_kernel(const int32_t *__restrict__ 
         sp[a] = pred[i];
     }
     __syncthreads();
-    // SUB threads per member: thread (a, r) accumulates member a's share of its pairs with members
-    // c = r (mod SUB) (no atomics; each pair's rho is computed identically by both members), the SUB
-    // partial int64 sums are then added with xor shuffles (exact, order-free)
-    constexpr int SUB = 4;
-    for (int base = 0; base < m * SUB; base += blockDim.x) {
-        const int tix = base + (int)threadIdx.x;
-        const int a = tix / SUB, r = tix % SUB;
-        long long ga = 0, ha = 0;
-        if (a < m) {
-            const float ca = sc[a], fa = sp[a];
-            for (int c = r; c < m; c += SUB) {
-                const float cc = sc[c];
-                if (c == a || cc == ca) continue;   // sign(c_i - c_j) = 0 contributes nothing
-                const bool hi = ca > cc;            // a is the slower (i) of the pair
-                const float fi = hi ? fa : sp[c], fj = hi ? sp[c] : fa;
-                const float d = __fsub_rn(fj, fi);
-                const float e = exp_det(-d);
-                const float rho = __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
-                const float hh = __fmul_rn(rho, __fsub_rn(1.0f, rho));
-                const long long q = __double2ll_rn((double)rho * 4294967296.0);
-                const long long qh = __double2ll_rn((double)hh * 4294967296.0);
-                ga += hi ? -2 * q : 2 * q;          // both orders of Eq. 2 carry the same term
-                ha += 2 * qh;
-            }
-        }
-#pragma unroll
-        for (int off = 1; off < SUB; off <<= 1) {
-            ga += __shfl_xor_sync(0xFFFFFFFFu, ga, off);
-            ha += __shfl_xor_sync(0xFFFFFFFFu, ha, off);
-        }
-        if (a < m && r == 0) {
-            g[mem[a]] = ga;
-            h[mem[a]] = ha;
-        }
-    }
+    group_pair_grads(mem, m, sc, sp, g, h);
 }
 
 // ------------------------------------------------------------------ 3. levels
@@ -749,6 +762,564 @@ __global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int3
     if (i < n && k[i] >= FIT_MAXKEYS) *bad = 2;
 }
 
+
+// ------------------------------------------------------------------ 4. fused forest (single rank, small n)
+// One cooperative launch fits the whole forest when the training set is small (Algorithm 1's D:
+// hundreds to a few thousand measured configurations).  Block b owns features b, b + G, ...; each
+// keeps, per feature, the samples in an order that is sorted by bin inside every node's segment
+// (a stable partition per level keeps it so), so a node's split candidates are the ends of its
+// bin runs and (G_L, H_L) are exact int64 prefix sums -- the same numbers as the histogram path
+// (cells with no samples are skipped there; cells whose sums are zero tie with the previous split
+// and lose to its smaller s), with O(n) work per feature and level instead of O(nodes x bins).
+// The best (gain, f, s) of every node is a 128-bit atomic max on a key ordered like split_better;
+// one grid barrier per level publishes it.  Per tree: gradients per group (members found by the
+// inverse of the Feistel cycle walk, so no member table), barrier, D levels, then every block
+// derives the leaves redundantly; the prediction update of tree t is applied by the owner of each
+// sample's group in tree t + 1 (and once more after the last tree).
+constexpr int FUSED_NMAX = 2048;
+constexpr int FUSED_NT = 256;
+constexpr int FUSED_NSUB = 8;   // sub-slots per node (block b uses b mod 8): bounds CAS contention
+constexpr int FUSED_NREP = 16;  // replicas of the release flag / decisions (block b reads b mod 16)
+
+struct FusedArgs {
+    const uint8_t *bins;
+    const int32_t *ncuts;
+    const float *cuts;
+    int B, n, F, D, n_trees, GS, n_groups;
+    const int32_t *counts, *woff, *gpre, *klist;
+    const float *cost;
+    float *pred[2];             // ping-pong: tree t reads pred[(t - 1) & 1], its chunk owners write pred[t & 1]
+    int64_t *g, *h;
+    uint16_t *gord, *gord0;
+    uint8_t *gnode;
+    unsigned long long *slot;   // [n_int][FUSED_NSUB] x (lo, hi), zero between levels
+    unsigned long long *dec;    // [FUSED_NREP][128] epoch << 32 | level decision (f << 8 | s, ~0u: none)
+    uint16_t *t_feat;
+    float *t_thr, *t_leaf;
+    uint64_t seed;
+    double lam, mcw, eta;
+    unsigned *bar;
+};
+
+__host__ __device__ inline size_t fused_smem_bytes(int N, int GS)
+{
+    int EP = 1;                                      // positions per thread (power of two)
+    while (EP * FUSED_NT < N) EP <<= 1;
+    const int PP = EP * FUSED_NT > 512 ? EP * FUSED_NT : 512;   // Pg also holds leaf sums / sort counters
+    size_t b = 8 * (2 * (size_t)N + 2 * (size_t)PP); // sg sh (int64, by sample) Ph Pg (int64, by position)
+    b += 12 * (size_t)GS;                            // mem sc sp
+    b += 6 * (size_t)N;                              // ord ord2 ord0 (u16)
+    b += 5 * (size_t)N;                              // nat nat2 sbin posbin leafof (u8)
+    b = (b + 15) & ~(size_t)15;
+    b += 2 * 257 * 4 + 2 * 128 * 4 + 8 * 16 + 512 + 256 * 4 + 128 * 32 + 128 * 4;   // segP segC decf decs scan dead lval kq/nst decw
+    return b;
+}
+
+__device__ __forceinline__ uint32_t feistel_inv(uint32_t y, int h, uint64_t seed, uint32_t tree, uint32_t wkey)
+{
+    // forward round r: (L, R) -> (R, L ^ F_r(R)); inverse: (L', R') -> (R' ^ F_r(L'), L')
+    const uint32_t mask = (1u << h) - 1u;
+    uint32_t L = y >> h, R = y & mask;
+#pragma unroll
+    for (int r = 3; r >= 0; --r) {
+        const U4 o = philox(seed, L, tree, (wkey << 2) | (uint32_t)r, TAG_GROUP_PERM);
+        const uint32_t pL = R ^ (o.x & mask), pR = L;
+        L = pL;
+        R = pR;
+    }
+    return (L << h) | R;
+}
+
+// 128-bit atomic max of (hi, lo) (unsigned lexicographic) at p[0] = lo, p[1] = hi
+__device__ __forceinline__ void slot_max(unsigned long long *p, unsigned long long klo, unsigned long long khi)
+{
+    unsigned long long lo = 0, hi = 0;
+    for (;;) {
+        if (khi < hi || (khi == hi && klo <= lo)) return;
+        unsigned long long olo, ohi;
+        asm volatile("{\n.reg .b128 c, s, d;\nmov.b128 c, {%2, %3};\nmov.b128 s, {%4, %5};\n"
+                     "atom.global.cas.b128 d, [%6], c, s;\nmov.b128 {%0, %1}, d;\n}"
+                     : "=l"(olo), "=l"(ohi)
+                     : "l"(lo), "l"(hi), "l"(klo), "l"(khi), "l"(p)
+                     : "memory");
+        if (olo == lo && ohi == hi) return;
+        lo = olo;
+        hi = ohi;
+    }
+}
+
+#ifdef AT_FIT_TIMING
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define FT_MARK(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long _t = gtimer(); ft[k] += _t - ft_last; ft_last = _t; } } while (0)
+#else
+#define FT_MARK(k) do {} while (0)
+#endif
+
+__global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
+{
+#ifdef AT_FIT_TIMING
+    unsigned long long ft[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer();
+#endif
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const int N = A.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = FUSED_NT / 32;
+    // Position-indexed int64 arrays (Pg, Ph, rex) are stored transposed: logical position
+    // j = t * EP + k (thread t's k-th contiguous position) lives at k * 256 + t, so the scans'
+    // per-thread runs are bank-conflict free.
+    int EP = 1, LE = 0;
+    while (EP * FUSED_NT < N) { EP <<= 1; ++LE; }
+    const int PP = EP * FUSED_NT > 512 ? EP * FUSED_NT : 512;
+    auto PH = [&](int j) { return ((j & (EP - 1)) << 8) + (j >> LE); };
+    int64_t *sg = (int64_t *)fsm, *sh = sg + N, *Ph = sh + N, *Pg = Ph + PP;
+    int32_t *mem = (int32_t *)(Pg + PP);
+    float *sc = (float *)(mem + A.GS), *sp = sc + A.GS;
+    uint16_t *ordA = (uint16_t *)(sp + A.GS), *ordB = ordA + N, *ord0 = ordB + N;
+    uint8_t *natA = (uint8_t *)(ord0 + N), *natB = natA + N, *sbin = natB + N, *posbin = sbin + N, *leafof = posbin + N;
+    unsigned char *tail = fsm + ((((size_t)(leafof + N - fsm)) + 15) & ~(size_t)15);
+    int32_t *segP = (int32_t *)tail, *segC = segP + 257, *decf = segC + 257, *decs = decf + 128;
+    long long *wsc = (long long *)(decs + 128);   // 16 long long: scan scratch
+    uint8_t *dead = (uint8_t *)(wsc + 16);
+    float *lval = (float *)(dead + 512);
+    unsigned long long *kq = (unsigned long long *)(lval + 256);   // [128] x (lo, hi) per-node keys / node stats
+    unsigned *decw = (unsigned *)(kq + 512);                         // [128] published decisions
+    int32_t *rex = (int32_t *)Pg;                  // partition scan (aliases Pg: disjoint in time)
+    unsigned *cnt = (unsigned *)Pg;                // counting sort scratch (init only)
+
+    const int G = gridDim.x, F = A.F, D = A.D;
+    const int n_int = (1 << D) - 1, n_leaf = 1 << D;
+    const bool resident = F <= G;
+    unsigned epoch = 0;
+    // gradient work items: (group, chunk of CM members); every item rebuilds its group's member
+    // list (inverse Feistel walk) and computes its chunk's members, one warp per member
+    const int CM = A.GS / 8 > 8 ? A.GS / 8 : 8;
+    const int chunks = (A.GS + CM - 1) / CM;
+    // Grid-wide sync.  Every block arrives on one counter (fire-and-forget add after a fence);
+    // block 0 alone polls it, reduces the level's sub-slots into the decisions (nn > 0), writes the
+    // tree nodes, re-zeroes the sub-slots (node ids are unique within a tree; later fences order
+    // the zeroing before the next tree's atomics) and publishes FUSED_NREP replicas of
+    // (epoch << 32 | decision) -- every block polls its own replica, so no L2 line is polled or
+    // read by all blocks, and the decisions arrive with the release.  decw[q] gets the decisions.
+    auto sync_all = [&](int t, int nn, int first) {
+        __syncthreads();
+        ++epoch;
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(A.bar, 1u);
+        }
+        const int nq = nn > 0 ? nn : 1;
+        if (blockIdx.x == 0) {
+            if (tid == 0) {
+                while (*(volatile unsigned *)A.bar < epoch * (unsigned)G) __nanosleep(20);
+                __threadfence();
+            }
+            __syncthreads();
+            for (int q = tid; q < nq; q += FUSED_NT) {
+                unsigned word = 0xFFFFFFFFu;
+                if (nn > 0) {
+                    const int nd = first + q;
+                    unsigned long long lo = 0, hi = 0;
+#pragma unroll
+                    for (int k = 0; k < FUSED_NSUB; ++k) {
+                        ulonglong2 *sp2 = (ulonglong2 *)(A.slot + 2 * (nd * FUSED_NSUB + k));
+                        const ulonglong2 v = __ldcg(sp2);
+                        __stcg(sp2, make_ulonglong2(0ull, 0ull));
+                        if (v.y > hi || (v.y == hi && v.x > lo)) { lo = v.x; hi = v.y; }
+                    }
+                    if (hi == 0) {
+                        A.t_feat[(size_t)t * n_int + nd] = 0;
+                        A.t_thr[(size_t)t * n_int + nd] = __int_as_float(0x7f800000);
+                    } else {
+                        const unsigned bf = 0xFFFFu - (unsigned)((lo >> 16) & 0xFFFFu);
+                        const unsigned bs = 0xFFFFu - (unsigned)(lo & 0xFFFFu);
+                        word = (bf << 8) | bs;
+                        A.t_feat[(size_t)t * n_int + nd] = (uint16_t)bf;
+                        A.t_thr[(size_t)t * n_int + nd] = A.cuts[(int64_t)bf * (A.B - 1) + bs - 1];
+                    }
+                }
+                const unsigned long long pub = ((unsigned long long)epoch << 32) | word;
+#pragma unroll
+                for (int r = 0; r < FUSED_NREP; ++r) __stcg(A.dec + r * 128 + q, pub);
+            }
+        }
+        for (int q = tid; q < nq; q += FUSED_NT) {
+            const volatile unsigned long long *src = A.dec + (blockIdx.x % FUSED_NREP) * 128 + q;
+            unsigned long long v = *src;
+            while ((unsigned)(v >> 32) != epoch) {
+                __nanosleep(20);
+                v = *src;
+            }
+            decw[q] = (unsigned)v;
+        }
+        __syncthreads();
+    };
+
+    // block-wide inclusive scan of Pg/Ph over all EP * 256 positions (padding holds zeros)
+    auto scan_pair = [&]() {
+        long long ag = 0, ah = 0;
+        for (int k = 0; k < EP; ++k) {
+            const int p = (k << 8) + tid;
+            ag += Pg[p]; ah += Ph[p]; Pg[p] = ag; Ph[p] = ah;
+        }
+        long long xg = ag, xh = ah;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long yg = __shfl_up_sync(0xFFFFFFFFu, xg, off), yh = __shfl_up_sync(0xFFFFFFFFu, xh, off);
+            if (lane >= off) { xg += yg; xh += yh; }
+        }
+        if (lane == 31) { wsc[2 * warp] = xg; wsc[2 * warp + 1] = xh; }
+        __syncthreads();
+        long long og = xg - ag, oh = xh - ah;
+        for (int w = 0; w < warp; ++w) { og += wsc[2 * w]; oh += wsc[2 * w + 1]; }
+        for (int k = 0; k < EP; ++k) { const int p = (k << 8) + tid; Pg[p] += og; Ph[p] += oh; }
+        __syncthreads();
+    };
+    // block-wide exclusive scan of the 0/1 flags rex (transposed, padding zero); wsc[8] = total
+    auto scan_flags = [&]() {
+        int a = 0;
+        for (int k = 0; k < EP; ++k) { const int p = (k << 8) + tid; const int v = rex[p]; rex[p] = a; a += v; }
+        int x = a;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+            if (lane >= off) x += y;
+        }
+        if (lane == 31) wsc[warp] = x;
+        __syncthreads();
+        int o = x - a;
+        for (int w = 0; w < warp; ++w) o += (int)wsc[w];
+        for (int k = 0; k < EP; ++k) rex[(k << 8) + tid] += o;
+        if (tid == FUSED_NT - 1) wsc[8] = o + a;
+        __syncthreads();
+    };
+
+    // ---- init: bin-sorted order of every owned feature (counting sort; order inside a bin is free)
+    for (int f = blockIdx.x; f < F; f += G) {
+        for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
+        for (int b = tid; b < 512; b += FUSED_NT) cnt[b] = 0;
+        __syncthreads();
+        for (int i = tid; i < N; i += FUSED_NT) atomicAdd(&cnt[sbin[i]], 1u);
+        __syncthreads();
+        if (warp == 0) {
+            unsigned v[8], a = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { v[k] = cnt[lane * 8 + k]; a += v[k]; }
+            unsigned x = a;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+                if (lane >= off) x += y;
+            }
+            unsigned o = x - a;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { cnt[256 + lane * 8 + k] = o; o += v[k]; }
+        }
+        __syncthreads();
+        for (int i = tid; i < N; i += FUSED_NT) ord0[atomicAdd(&cnt[256 + sbin[i]], 1u)] = (uint16_t)i;
+        __syncthreads();
+        if (!resident)
+            for (int j = tid; j < N; j += FUSED_NT) A.gord0[(int64_t)f * N + j] = ord0[j];
+        __syncthreads();
+    }
+
+    uint16_t *ord = ordA, *ord2 = ordB;
+    uint8_t *nat = natA, *nat2 = natB;
+    for (int t = 0; t < A.n_trees; ++t) {
+        unsigned long long *slot = A.slot;
+        // ---- gradients (and the previous tree's prediction update) per group
+        for (int item = blockIdx.x; item < A.n_groups * chunks; item += G) {
+            const int grp = item / chunks, a0 = (item - grp * chunks) * CM;
+            if (tid == 0) {
+                int lo = 0, hi = FIT_MAXKEYS;   // largest w with gpre[w] <= grp
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (A.gpre[mid] <= grp) lo = mid; else hi = mid;
+                }
+                decf[0] = lo;
+            }
+            __syncthreads();
+            const int w = decf[0];
+            __syncthreads();   // decf[0] is rewritten by the next item
+            const int nw = A.counts[w];
+            const int start = (grp - A.gpre[w]) * A.GS;
+            const int m = min(A.GS, nw - start);
+            const int a1 = min(m, a0 + CM);
+            if (a0 >= m) continue;   // block-uniform
+            int bits = 0;
+            while ((1ull << bits) < (unsigned long long)nw) ++bits;
+            int hb = (bits + 1) / 2;
+            if (hb < 1) hb = 1;
+            for (int a = tid; a < m; a += FUSED_NT) {
+                uint32_t r = feistel_inv((uint32_t)(start + a), hb, A.seed, (uint32_t)t, (uint32_t)w);
+                while (r >= (uint32_t)nw) r = feistel_inv(r, hb, A.seed, (uint32_t)t, (uint32_t)w);
+                const int i = A.klist[A.woff[w] + (int)r];
+                mem[a] = i;
+                float pv = 0.0f;
+                if (t > 0) {
+                    pv = __fadd_rn(__ldcg(A.pred[(t - 1) & 1] + i), lval[leafof[i]]);
+                    if (a >= a0 && a < a1) A.pred[t & 1][i] = pv;   // the chunk owning the member writes it
+                }
+                sp[a] = pv;
+                sc[a] = A.cost[i];
+            }
+            __syncthreads();
+            // warp per member of the chunk, lanes over its partners
+            for (int a = a0 + warp; a < a1; a += NW) {
+                long long ga = 0, ha = 0;
+                const float ca = sc[a], fa = sp[a];
+                for (int c = lane; c < m; c += 32)
+                    if (c != a) pair_term(ca, fa, sc[c], sp[c], ga, ha);
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    ga += __shfl_xor_sync(0xFFFFFFFFu, ga, off);
+                    ha += __shfl_xor_sync(0xFFFFFFFFu, ha, off);
+                }
+                if (lane == 0) {
+                    A.g[mem[a]] = ga;
+                    A.h[mem[a]] = ha;
+                }
+            }
+            __syncthreads();
+        }
+        FT_MARK(0);
+        sync_all(t, 0, 0);
+        FT_MARK(1);
+
+        for (int i = tid; i < N; i += FUSED_NT) { sg[i] = __ldcg(A.g + i); sh[i] = __ldcg(A.h + i); }
+        for (int q = tid; q < 512; q += FUSED_NT) dead[q] = 0;
+        if (tid == 0) { segP[0] = 0; segP[1] = N; }
+        __syncthreads();
+
+        for (int d = 0; d < D; ++d) {
+            const int nn = 1 << d, first = nn - 1, nnP = nn >> 1;
+            for (int f = blockIdx.x; f < F; f += G) {
+                const int nc = A.ncuts[f];
+                if (!resident) {
+                    for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
+                    if (d > 0)
+                        for (int j = tid; j < N; j += FUSED_NT) {
+                            ord[j] = A.gord[(int64_t)f * N + j];
+                            nat[j] = A.gnode[(int64_t)f * N + j];
+                        }
+                } else if (t == 0 && d == 0) {
+                    for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
+                }
+                FT_MARK(7);
+                if (d == 0) {
+                    for (int j = tid; j < N; j += FUSED_NT) {
+                        ord[j] = resident ? ord0[j] : A.gord0[(int64_t)f * N + j];
+                        nat[j] = 0;
+                    }
+                    if (tid == 0) { segC[0] = 0; segC[1] = N; }
+                    __syncthreads();
+                } else {
+                    // stable partition of every parent segment by the parent's decision
+                    __syncthreads();
+                    for (int kb = 0; kb < EP; kb += 4) {
+                        int bv[4], th[4];   // all gathers of the batch in flight together
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = tid * EP + kb + u;
+                            bv[u] = 0;
+                            th[u] = 1 << 30;
+                            if (kb + u < EP && j < N) {
+                                const int i = ord[j], q = nat[j], sf = decf[q];
+                                if (sf >= 0) {
+                                    th[u] = decs[q];
+                                    bv[u] = sf == f ? (int)sbin[i] : (int)__ldg(A.bins + (int64_t)sf * N + i);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (kb + u < EP) rex[((kb + u) << 8) + tid] = bv[u] >= th[u] ? 1 : 0;
+                    }
+                    __syncthreads();
+                    scan_flags();
+                    const int rtot = (int)wsc[8];
+                    auto rx = [&](int x) { return x < N ? rex[PH(x)] : rtot; };
+                    for (int j = tid; j < N; j += FUSED_NT) {
+                        const int q = nat[j], s0 = segP[q], s1 = segP[q + 1];
+                        const int r0 = rx(s0), nR = rx(s1) - r0, nL = (s1 - s0) - nR;
+                        const int rj = rx(j), right = rx(j + 1) - rj, rb = rj - r0;
+                        const int np = right ? s0 + nL + rb : s0 + (j - s0) - rb;
+                        ord2[np] = ord[j];
+                        nat2[np] = (uint8_t)(2 * q + right);
+                    }
+                    for (int q = tid; q < nnP; q += FUSED_NT) {
+                        const int s0 = segP[q], s1 = segP[q + 1];
+                        const int nR = rx(s1) - rx(s0);
+                        segC[2 * q] = s0;
+                        segC[2 * q + 1] = s1 - nR;
+                    }
+                    if (tid == 0) segC[2 * nnP] = N;
+                    __syncthreads();
+                    { uint16_t *tq = ord; ord = ord2; ord2 = tq; }
+                    { uint8_t *tq = nat; nat = nat2; nat2 = tq; }
+                }
+                FT_MARK(2);
+                // prefix sums of (g, h) in this order, then every node's run ends
+                for (int k = 0; k < EP; ++k) {
+                    const int j = tid * EP + k, p = (k << 8) + tid;
+                    long long vg = 0, vh = 0;
+                    if (j < N) {
+                        const int i = ord[j];
+                        posbin[j] = sbin[i];
+                        vg = sg[i];
+                        vh = sh[i];
+                    }
+                    Pg[p] = vg;
+                    Ph[p] = vh;
+                }
+                __syncthreads();
+                scan_pair();
+                FT_MARK(3);
+                // node statistics, one thread per node (Hi = -1: no candidates)
+                long long *nst = (long long *)kq;   // [128][4] bg bh Gi Hi (aliases kq: disjoint in time)
+                for (int q = tid; q < nn; q += FUSED_NT) {
+                    const int s0 = segC[q], s1 = segC[q + 1];
+                    if (dead[first + q] || s1 == s0) { nst[4 * q + 3] = -1; continue; }
+                    const long long bg = s0 ? Pg[PH(s0 - 1)] : 0, bh = s0 ? Ph[PH(s0 - 1)] : 0;
+                    nst[4 * q] = bg;
+                    nst[4 * q + 1] = bh;
+                    nst[4 * q + 2] = Pg[PH(s1 - 1)] - bg;
+                    nst[4 * q + 3] = Ph[PH(s1 - 1)] - bh;
+                }
+                __syncthreads();
+                // every run end of every node at once (thread-contiguous positions, independent
+                // fp64 chains); the candidate's key (f fixed: gain, then lower s) replaces (Pg, Ph)
+                for (int k = 0; k < EP; ++k) {
+                    const int j = tid * EP + k, p = (k << 8) + tid;
+                    if (j >= N) break;
+                    const int q = nat[j], b = posbin[j];
+                    const long long Hi = nst[4 * q + 3];
+                    unsigned long long klo = 0, khi = 0;
+                    if (Hi >= 0 && b < nc && (j + 1 == segC[q + 1] || posbin[j + 1] != b)) {
+                        const long long bg = nst[4 * q], bh = nst[4 * q + 1], Gi = nst[4 * q + 2];
+                        const double Gd = (double)Gi * FX, Hd = (double)Hi * FX;
+                        const double parent = Gd * Gd / (Hd + A.lam);
+                        const long long GLi = Pg[p] - bg, HLi = Ph[p] - bh;
+                        const double GL = (double)GLi * FX, HL = (double)HLi * FX;
+                        const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
+                        if (!(HL < A.mcw || HR < A.mcw)) {
+                            const double gain = (GL * GL / (HL + A.lam) + GR * GR / (HR + A.lam)) - parent;
+                            if (gain > 0.0) {
+                                klo = ((unsigned long long)(0xFFFFu - (unsigned)f) << 16) |
+                                      (unsigned long long)(0xFFFFu - (unsigned)(b + 1));
+                                khi = (unsigned long long)__double_as_longlong(gain);
+                            }
+                        }
+                    }
+                    Pg[p] = (long long)klo;
+                    Ph[p] = (long long)khi;
+                }
+                __syncthreads();
+                // per-node max of the keys (warp per node)
+                for (int q = warp; q < nn; q += NW) {
+                    const int s0 = segC[q], s1 = segC[q + 1];
+                    unsigned long long lo = 0, hi = 0;
+                    for (int j = s0 + lane; j < s1; j += 32) {
+                        const unsigned long long vl = (unsigned long long)Pg[PH(j)], vh = (unsigned long long)Ph[PH(j)];
+                        if (vh > hi || (vh == hi && vl > lo)) { lo = vl; hi = vh; }
+                    }
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) {
+                        const unsigned long long ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
+                        const unsigned long long oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+                        if (oh > hi || (oh == hi && ol > lo)) { lo = ol; hi = oh; }
+                    }
+                    if (lane == 0) { kq[2 * q] = lo; kq[2 * q + 1] = hi; }
+                }
+                __syncthreads();
+                FT_MARK(8);
+                // one thread per node: all of the block's atomics in flight together
+                for (int q = tid; q < nn; q += FUSED_NT) {
+                    const unsigned long long khi = kq[2 * q + 1];
+                    if (khi) slot_max(slot + 2 * ((first + q) * FUSED_NSUB + (blockIdx.x & (FUSED_NSUB - 1))), kq[2 * q], khi);
+                }
+                if (!resident) {
+                    __syncthreads();
+                    for (int j = tid; j < N; j += FUSED_NT) {
+                        A.gord[(int64_t)f * N + j] = ord[j];
+                        A.gnode[(int64_t)f * N + j] = nat[j];
+                    }
+                }
+                __syncthreads();
+                FT_MARK(4);
+            }
+            sync_all(t, nn, first);
+            FT_MARK(5);
+            // the level's decisions (identical in every block; a dead node never has a split)
+            for (int q = tid; q < nn; q += FUSED_NT) {
+                const int nd = first + q;
+                const unsigned word = decw[q];
+                if (word == 0xFFFFFFFFu) {
+                    decf[q] = -1;
+                    decs[q] = 0;
+                    dead[2 * nd + 1] = 1;
+                    dead[2 * nd + 2] = 1;
+                } else {
+                    decf[q] = (int)(word >> 8);
+                    decs[q] = (int)(word & 0xFFu);
+                }
+            }
+            for (int q = tid; q <= nn; q += FUSED_NT) segP[q] = segC[q];
+            __syncthreads();
+        }
+        // ---- leaves (every block, from its first feature's final order)
+        {
+            const int f = blockIdx.x;
+            if (!resident)
+                for (int j = tid; j < N; j += FUSED_NT) {
+                    ord[j] = A.gord[(int64_t)f * N + j];
+                    nat[j] = A.gnode[(int64_t)f * N + j];
+                }
+            unsigned long long *lsum = (unsigned long long *)Pg;
+            for (int l = tid; l < 2 * n_leaf; l += FUSED_NT) lsum[l] = 0ull;
+            __syncthreads();
+            for (int j = tid; j < N; j += FUSED_NT) {
+                const int i = ord[j], q = nat[j], sf = decf[q];
+                const int right = (sf >= 0 && (int)A.bins[(int64_t)sf * N + i] >= decs[q]) ? 1 : 0;
+                const int l = 2 * q + right;
+                leafof[i] = (uint8_t)l;
+                smem_add_u64(&lsum[2 * l], (unsigned long long)sg[i]);
+                smem_add_u64(&lsum[2 * l + 1], (unsigned long long)sh[i]);
+            }
+            __syncthreads();
+            for (int l = tid; l < n_leaf; l += FUSED_NT) {
+                const double Gd = (double)(long long)lsum[2 * l] * FX, Hd = (double)(long long)lsum[2 * l + 1] * FX;
+                const float v = (float)(-(A.eta * (Gd / (Hd + A.lam))));
+                lval[l] = v;
+                if (blockIdx.x == 0) A.t_leaf[(size_t)t * n_leaf + l] = v;
+            }
+            __syncthreads();
+        }
+        FT_MARK(6);
+    }
+    // the last tree's prediction update
+    const int T = A.n_trees;
+    for (int i = blockIdx.x * FUSED_NT + tid; i < N; i += G * FUSED_NT)
+        A.pred[T & 1][i] = __fadd_rn(__ldcg(A.pred[(T - 1) & 1] + i), lval[leafof[i]]);
+#ifdef AT_FIT_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("fused forest (block 0, ns per tree, G=%d resident=%d): grads %llu barrier0 %llu | per-tree sums over levels: "
+               "load %llu partition %llu scan %llu cand %llu (cas %llu) barrier %llu decide+leaves %llu\n", G, (int)resident,
+               ft[0] / A.n_trees, ft[1] / A.n_trees, ft[7] / A.n_trees, ft[2] / A.n_trees, ft[3] / A.n_trees,
+               ft[8] / A.n_trees, ft[4] / A.n_trees, ft[5] / A.n_trees, ft[6] / A.n_trees);
+#endif
+}
+
+__global__ void klist_kernel(const uint16_t *__restrict__ key, const int32_t *__restrict__ rank,
+                             const int32_t *__restrict__ woff, int64_t n, int32_t *__restrict__ klist)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) klist[woff[key[i]] + rank[i]] = (int32_t)i;
+}
+
 }  // namespace at
 
 namespace {
@@ -849,6 +1420,90 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     if (info[2] == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
     if (info[2] == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
     const int TB = info[0], max_nb = info[1], n_groups = info[3];
+    // the fitted ensemble handle (both paths)
+    auto finish = [&]() -> int {
+        // the fitted ensemble handle
+        at_gbt gm = new at_gbt_s();
+        gm->n_trees = o->n_trees;
+        gm->depth = D;
+        gm->n_features = F;
+        gm->t_pad = (o->n_trees + 15) / 16 * 16;
+        gm->base = 0.0f;
+        gm->d_nodes = nullptr;
+        gm->d_leaf = nullptr;
+        if (cudaMalloc(&gm->d_nodes, sizeof(uint2) * (size_t)gm->t_pad * n_int) != cudaSuccess ||
+            cudaMalloc(&gm->d_leaf, sizeof(float) * (size_t)gm->t_pad * n_leaf) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(gm->d_nodes);
+            delete gm;
+            return fail(AT_ENOMEM, "gbt_fit_hist: model allocation failed");
+        }
+        AT_CUDA_TRY(cudaMemsetAsync(gm->d_nodes, 0, sizeof(uint2) * (size_t)gm->t_pad * n_int, s));
+        AT_CUDA_TRY(cudaMemsetAsync(gm->d_leaf, 0, sizeof(float) * (size_t)gm->t_pad * n_leaf, s));
+        pack_nodes_kernel<<<nblk((int64_t)o->n_trees * n_int, 256), 256, 0, s>>>(t_feat, t_thr, (int64_t)o->n_trees * n_int,
+                                                                                 gm->d_nodes);
+        AT_CUDA_TRY(cudaMemcpyAsync(gm->d_leaf, t_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf,
+                                    cudaMemcpyDeviceToDevice, s));
+        if (o->d_pred_out) AT_CUDA_TRY(cudaMemcpyAsync(o->d_pred_out, pred, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+        AT_LAUNCH_CHECK("fit finish");
+        *out = gm;
+        return AT_OK;
+    };
+
+    // small single-rank fits: the whole forest in one cooperative launch (fused_forest_kernel)
+    const char *fused_e = getenv("AT_FIT_FUSED");   // "0" forces the level-by-level path
+    const int fused_env = fused_e ? atoi(fused_e) : 1;
+    if (fused_env && !o->allreduce && !o->d_hist0_out && n <= FUSED_NMAX) {
+        const size_t fsm = fused_smem_bytes((int)n, GS);
+        int dev = 0, nsm = 0, coop = 0, per = 0;
+        AT_CUDA_TRY(cudaGetDevice(&dev));
+        AT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        AT_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        static size_t fused_attr = 0;
+        if (fused_attr < fsm) {
+            AT_CUDA_TRY(cudaFuncSetAttribute(fused_forest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+            fused_attr = fsm;
+        }
+        AT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fused_forest_kernel, FUSED_NT, fsm));
+        if (coop && per > 0) {
+            const int G = (int)std::min<int64_t>(F, (int64_t)per * nsm);
+            const bool resident = F <= G;
+            int32_t *klist = ws.get<int32_t>(n);
+            unsigned long long *slot = ws.get<unsigned long long>((size_t)2 * FUSED_NSUB * n_int);
+            unsigned *bar = ws.get<unsigned>(32);
+            unsigned long long *decp = ws.get<unsigned long long>((size_t)FUSED_NREP * 128);
+            uint16_t *gord = resident ? nullptr : ws.get<uint16_t>((size_t)F * n);
+            uint16_t *gord0 = resident ? nullptr : ws.get<uint16_t>((size_t)F * n);
+            uint8_t *gnode = resident ? nullptr : ws.get<uint8_t>((size_t)F * n);
+            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+            AT_CUDA_TRY(cudaMemsetAsync(bar, 0, 32 * sizeof(unsigned), s));
+            AT_CUDA_TRY(cudaMemsetAsync(decp, 0, FUSED_NREP * 128 * sizeof(unsigned long long), s));
+            AT_CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(unsigned long long) * 2 * FUSED_NSUB * n_int, s));
+            klist_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, woff, n, klist);
+            AT_LAUNCH_CHECK("klist");
+            FusedArgs fa;
+            fa.bins = bins; fa.ncuts = ncuts; fa.cuts = cuts; fa.B = B;
+            fa.n = (int)n; fa.F = F; fa.D = D; fa.n_trees = o->n_trees; fa.GS = GS; fa.n_groups = n_groups;
+            fa.counts = counts; fa.woff = woff; fa.gpre = gpre; fa.klist = klist;
+            float *pred2 = ws.get<float>(n);
+            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+            fa.cost = d_cost; fa.g = g; fa.h = h;
+            fa.pred[0] = (o->n_trees & 1) ? pred2 : pred;   // the final predictions land in pred
+            fa.pred[1] = (o->n_trees & 1) ? pred : pred2;
+            fa.gord = gord; fa.gord0 = gord0; fa.gnode = gnode; fa.slot = slot;
+            fa.t_feat = t_feat; fa.t_thr = t_thr; fa.t_leaf = t_leaf;
+            fa.seed = o->seed; fa.lam = lam; fa.mcw = mcw; fa.eta = eta; fa.bar = bar;
+            fa.dec = decp;
+            void *args[] = {&fa};
+            {
+                ProfScope ps(AT_K_FIT_GRAPH, s);
+                AT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)fused_forest_kernel, dim3(G), dim3(FUSED_NT), args,
+                                                        fsm, s));
+            }
+            return finish();
+        }
+    }
+
     int64_t *hist = ws.get<int64_t>((size_t)max_nn * TB * 2);
     if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: histogram allocation failed");
 
@@ -980,30 +1635,5 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         cudaGraphExecDestroy(exec);
         if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph launch");
     }
-    // the fitted ensemble handle
-    at_gbt gm = new at_gbt_s();
-    gm->n_trees = o->n_trees;
-    gm->depth = D;
-    gm->n_features = F;
-    gm->t_pad = (o->n_trees + 15) / 16 * 16;
-    gm->base = 0.0f;
-    gm->d_nodes = nullptr;
-    gm->d_leaf = nullptr;
-    if (cudaMalloc(&gm->d_nodes, sizeof(uint2) * (size_t)gm->t_pad * n_int) != cudaSuccess ||
-        cudaMalloc(&gm->d_leaf, sizeof(float) * (size_t)gm->t_pad * n_leaf) != cudaSuccess) {
-        cudaGetLastError();
-        cudaFree(gm->d_nodes);
-        delete gm;
-        return fail(AT_ENOMEM, "gbt_fit_hist: model allocation failed");
-    }
-    AT_CUDA_TRY(cudaMemsetAsync(gm->d_nodes, 0, sizeof(uint2) * (size_t)gm->t_pad * n_int, s));
-    AT_CUDA_TRY(cudaMemsetAsync(gm->d_leaf, 0, sizeof(float) * (size_t)gm->t_pad * n_leaf, s));
-    pack_nodes_kernel<<<nblk((int64_t)o->n_trees * n_int, 256), 256, 0, s>>>(t_feat, t_thr, (int64_t)o->n_trees * n_int,
-                                                                             gm->d_nodes);
-    AT_CUDA_TRY(cudaMemcpyAsync(gm->d_leaf, t_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf,
-                                cudaMemcpyDeviceToDevice, s));
-    if (o->d_pred_out) AT_CUDA_TRY(cudaMemcpyAsync(o->d_pred_out, pred, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
-    AT_LAUNCH_CHECK("fit finish");
-    *out = gm;
-    return AT_OK;
+    return finish();
 }

@@ -4,6 +4,8 @@ Every comparison is element by element on the same seeded inputs (paper_1805_081
 bit-exact for indices, features, leaf slots, accept bits, top-k, selections, histograms and
 fitted trees; scores within 1e-6 relative (north_star) -- and in practice bit-exact.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -395,6 +397,59 @@ def test_fit_rank_invariance_two_emulated_ranks(at):
         ex = out[r].export()
         for k in ("feat", "thresh", "leaf"):
             assert_bits_equal(ex[k], single[k], f"rank {r} {k}")
+
+
+def _fit_both_paths(at, Xg, n, c, key, **kw):
+    """The fit with the fused single-launch forest (default for n <= 2048) and with the
+    level-by-level path (AT_FIT_FUSED=0), predictions included."""
+    out = []
+    for env in ("1", "0"):
+        os.environ["AT_FIT_FUSED"] = env
+        try:
+            pred = torch.empty(n, dtype=torch.float32, device="cuda")
+            ex = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), pred_out=pred, **kw).export()
+            ex["pred"] = pred.cpu().numpy()
+            out.append(ex)
+        finally:
+            os.environ.pop("AT_FIT_FUSED", None)
+    return out
+
+
+@pytest.mark.parametrize("n,wls,trees,depth,gs", [(1024, [synth.CFG2A], 5, 6, 64),     # bench's |D|
+                                                  (2048, synth.ALL_RESNET[:4], 3, 8, 64),
+                                                  (333, synth.ALL_DW[:5], 4, 3, 2),
+                                                  (1000, [synth.MATMUL_512], 3, 5, 1024),
+                                                  (1, [synth.CFG2A], 2, 4, 64),
+                                                  (37, [synth.CFG2A, synth.CFG2B], 3, 1, 8)])
+def test_fit_fused_forest_matches_oracle(at, n, wls, trees, depth, gs):
+    osp, idx, X, c, key = fit_inputs(n, wls, seed=n + depth)
+    ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth, group_size=gs)
+    sp = at.Space(wls)
+    Xg = sp.features(u64(idx))
+    fused, lvl = _fit_both_paths(at, Xg, n, c, key, n_trees=trees, depth=depth, group_size=gs)
+    for k in ("feat", "thresh", "leaf", "pred"):
+        assert_bits_equal(fused[k], ref[k], f"fused {k}")
+        assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
+
+
+def test_fit_fused_forest_many_features_and_ties(at):
+    """F = 1500 random features (more than one cooperative block per feature, so per-feature order
+    state round-trips through global memory), duplicated columns (exact gain ties broken by the lower
+    feature), constant columns, equal costs inside groups."""
+    n, F = 900, 1500
+    rng = np.random.default_rng(21)
+    X = rng.integers(0, 40, (n, F)).astype(np.float32)
+    X[:, 700:800] = X[:, 100:200]                   # duplicates of earlier features
+    X[:, 800:850] = 3.0                             # constant
+    X[:, 850:900] = rng.random((n, 50)).astype(np.float32) * 1e4
+    c = np.round(X[:, 100] + 2 * X[:, 150] + rng.integers(0, 3, n), 0).astype(np.float32)
+    key = (np.arange(n) % 7).astype(np.uint16)
+    ref = O.fit_hist(X, c, key, n_trees=3, depth=5)
+    Xg = dev(np.ascontiguousarray(X.T))
+    fused, lvl = _fit_both_paths(at, Xg, n, c, key, n_trees=3, depth=5)
+    for k in ("feat", "thresh", "leaf", "pred"):
+        assert_bits_equal(fused[k], ref[k], f"fused {k}")
+        assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
 
 
 def test_fit_errors(at):
