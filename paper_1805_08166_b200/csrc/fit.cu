@@ -808,10 +808,11 @@ __host__ __device__ inline size_t fused_smem_bytes(int N, int GS)
     const int PP = EP * FUSED_NT > 512 ? EP * FUSED_NT : 512;   // Pg also holds leaf sums / sort counters
     size_t b = 8 * (2 * (size_t)N + 2 * (size_t)PP); // sg sh (int64, by sample) Ph Pg (int64, by position)
     b += 12 * (size_t)GS;                            // mem sc sp
-    b += 6 * (size_t)N;                              // ord ord2 ord0 (u16)
+    b += 4 * (size_t)N;                              // ord ord2 (u16)
+    b += 2 * (size_t)EP * FUSED_NT;                  // rex (u16, by position, transposed)
     b += 5 * (size_t)N;                              // nat nat2 sbin posbin leafof (u8)
     b = (b + 15) & ~(size_t)15;
-    b += 2 * 257 * 4 + 2 * 128 * 4 + 8 * 16 + 512 + 256 * 4 + 128 * 32 + 128 * 4;   // segP segC decf decs scan dead lval kq/nst decw
+    b += 2 * 257 * 4 + 2 * 128 * 4 + 8 * 16 + 512 + 256 * 4 + 128 * 32 + 128 * 4 + 128 * 8;   // segP segC decf decs scan dead lval kq/nst decw npar
     return b;
 }
 
@@ -855,7 +856,9 @@ __device__ __forceinline__ unsigned long long gtimer()
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define FT_MARK(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long _t = gtimer(); ft[k] += _t - ft_last; ft_last = _t; } } while (0)
+#define FT_MARK(k) do { if (threadIdx.x == 0) { unsigned long long _t = gtimer(); ft[k] += _t - ft_last; ft_last = _t; } } while (0)
+__device__ unsigned long long g_ft_work_min = ~0ull, g_ft_work_max = 0ull;
+__device__ unsigned g_ft_smid[1024];
 #else
 #define FT_MARK(k) do {} while (0)
 #endif
@@ -878,8 +881,9 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
     int64_t *sg = (int64_t *)fsm, *sh = sg + N, *Ph = sh + N, *Pg = Ph + PP;
     int32_t *mem = (int32_t *)(Pg + PP);
     float *sc = (float *)(mem + A.GS), *sp = sc + A.GS;
-    uint16_t *ordA = (uint16_t *)(sp + A.GS), *ordB = ordA + N, *ord0 = ordB + N;
-    uint8_t *natA = (uint8_t *)(ord0 + N), *natB = natA + N, *sbin = natB + N, *posbin = sbin + N, *leafof = posbin + N;
+    uint16_t *ordA = (uint16_t *)(sp + A.GS), *ordB = ordA + N, *rex = ordB + N;   // rex: EP * 256
+    uint8_t *natA = (uint8_t *)(rex + EP * FUSED_NT), *natB = natA + N, *sbin = natB + N, *posbin = sbin + N,
+            *leafof = posbin + N;
     unsigned char *tail = fsm + ((((size_t)(leafof + N - fsm)) + 15) & ~(size_t)15);
     int32_t *segP = (int32_t *)tail, *segC = segP + 257, *decf = segC + 257, *decs = decf + 128;
     long long *wsc = (long long *)(decs + 128);   // 16 long long: scan scratch
@@ -887,7 +891,7 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
     float *lval = (float *)(dead + 512);
     unsigned long long *kq = (unsigned long long *)(lval + 256);   // [128] x (lo, hi) per-node keys / node stats
     unsigned *decw = (unsigned *)(kq + 512);                         // [128] published decisions
-    int32_t *rex = (int32_t *)Pg;                  // partition scan (aliases Pg: disjoint in time)
+    double *npar = (double *)(decw + 128);                           // [128] node parent scores
     unsigned *cnt = (unsigned *)Pg;                // counting sort scratch (init only)
 
     const int G = gridDim.x, F = A.F, D = A.D;
@@ -946,13 +950,20 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
                 for (int r = 0; r < FUSED_NREP; ++r) __stcg(A.dec + r * 128 + q, pub);
             }
         }
-        for (int q = tid; q < nq; q += FUSED_NT) {
-            const volatile unsigned long long *src = A.dec + (blockIdx.x % FUSED_NREP) * 128 + q;
-            unsigned long long v = *src;
+        // one thread polls entry 0 of the block's replica; the others then read theirs (each entry
+        // carries its epoch, so a rare not-yet-visible one is re-read)
+        const volatile unsigned long long *rep = A.dec + (blockIdx.x % FUSED_NREP) * 128;
+        if (tid == 0) {
+            unsigned long long v = rep[0];
             while ((unsigned)(v >> 32) != epoch) {
-                __nanosleep(20);
-                v = *src;
+                __nanosleep(64);
+                v = rep[0];
             }
+        }
+        __syncthreads();
+        for (int q = tid; q < nq; q += FUSED_NT) {
+            unsigned long long v = rep[q];
+            while ((unsigned)(v >> 32) != epoch) v = rep[q];
             decw[q] = (unsigned)v;
         }
         __syncthreads();
@@ -981,7 +992,7 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
     // block-wide exclusive scan of the 0/1 flags rex (transposed, padding zero); wsc[8] = total
     auto scan_flags = [&]() {
         int a = 0;
-        for (int k = 0; k < EP; ++k) { const int p = (k << 8) + tid; const int v = rex[p]; rex[p] = a; a += v; }
+        for (int k = 0; k < EP; ++k) { const int p = (k << 8) + tid; const int v = rex[p]; rex[p] = (uint16_t)a; a += v; }
         int x = a;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -992,7 +1003,7 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
         __syncthreads();
         int o = x - a;
         for (int w = 0; w < warp; ++w) o += (int)wsc[w];
-        for (int k = 0; k < EP; ++k) rex[(k << 8) + tid] += o;
+        for (int k = 0; k < EP; ++k) rex[(k << 8) + tid] = (uint16_t)(rex[(k << 8) + tid] + o);
         if (tid == FUSED_NT - 1) wsc[8] = o + a;
         __syncthreads();
     };
@@ -1019,10 +1030,9 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
             for (int k = 0; k < 8; ++k) { cnt[256 + lane * 8 + k] = o; o += v[k]; }
         }
         __syncthreads();
-        for (int i = tid; i < N; i += FUSED_NT) ord0[atomicAdd(&cnt[256 + sbin[i]], 1u)] = (uint16_t)i;
+        for (int i = tid; i < N; i += FUSED_NT) ordA[atomicAdd(&cnt[256 + sbin[i]], 1u)] = (uint16_t)i;
         __syncthreads();
-        if (!resident)
-            for (int j = tid; j < N; j += FUSED_NT) A.gord0[(int64_t)f * N + j] = ord0[j];
+        for (int j = tid; j < N; j += FUSED_NT) A.gord0[(int64_t)f * N + j] = ordA[j];
         __syncthreads();
     }
 
@@ -1110,9 +1120,20 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
                 }
                 FT_MARK(7);
                 if (d == 0) {
-                    for (int j = tid; j < N; j += FUSED_NT) {
-                        ord[j] = resident ? ord0[j] : A.gord0[(int64_t)f * N + j];
-                        nat[j] = 0;
+                    // the bin-sorted order, with the (g, h) and bins of every position
+                    for (int k = 0; k < EP; ++k) {
+                        const int j = tid * EP + k, p = (k << 8) + tid;
+                        long long vg = 0, vh = 0;
+                        if (j < N) {
+                            const int i = __ldcg(A.gord0 + (int64_t)f * N + j);
+                            ord[j] = (uint16_t)i;
+                            nat[j] = 0;
+                            posbin[j] = sbin[i];
+                            vg = sg[i];
+                            vh = sh[i];
+                        }
+                        Pg[p] = vg;
+                        Ph[p] = vh;
                     }
                     if (tid == 0) { segC[0] = 0; segC[1] = N; }
                     __syncthreads();
@@ -1160,22 +1181,22 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
                     __syncthreads();
                     { uint16_t *tq = ord; ord = ord2; ord2 = tq; }
                     { uint8_t *tq = nat; nat = nat2; nat2 = tq; }
+                    for (int k = 0; k < EP; ++k) {   // the positions' bins and (g, h)
+                        const int j = tid * EP + k, p = (k << 8) + tid;
+                        long long vg = 0, vh = 0;
+                        if (j < N) {
+                            const int i = ord[j];
+                            posbin[j] = sbin[i];
+                            vg = sg[i];
+                            vh = sh[i];
+                        }
+                        Pg[p] = vg;
+                        Ph[p] = vh;
+                    }
+                    __syncthreads();
                 }
                 FT_MARK(2);
                 // prefix sums of (g, h) in this order, then every node's run ends
-                for (int k = 0; k < EP; ++k) {
-                    const int j = tid * EP + k, p = (k << 8) + tid;
-                    long long vg = 0, vh = 0;
-                    if (j < N) {
-                        const int i = ord[j];
-                        posbin[j] = sbin[i];
-                        vg = sg[i];
-                        vh = sh[i];
-                    }
-                    Pg[p] = vg;
-                    Ph[p] = vh;
-                }
-                __syncthreads();
                 scan_pair();
                 FT_MARK(3);
                 // node statistics, one thread per node (Hi = -1: no candidates)
@@ -1186,8 +1207,11 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
                     const long long bg = s0 ? Pg[PH(s0 - 1)] : 0, bh = s0 ? Ph[PH(s0 - 1)] : 0;
                     nst[4 * q] = bg;
                     nst[4 * q + 1] = bh;
-                    nst[4 * q + 2] = Pg[PH(s1 - 1)] - bg;
-                    nst[4 * q + 3] = Ph[PH(s1 - 1)] - bh;
+                    const long long Gi = Pg[PH(s1 - 1)] - bg, Hi = Ph[PH(s1 - 1)] - bh;
+                    nst[4 * q + 2] = Gi;
+                    nst[4 * q + 3] = Hi;
+                    const double Gd = (double)Gi * FX, Hd = (double)Hi * FX;
+                    npar[q] = Gd * Gd / (Hd + A.lam);
                 }
                 __syncthreads();
                 // every run end of every node at once (thread-contiguous positions, independent
@@ -1200,8 +1224,7 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
                     unsigned long long klo = 0, khi = 0;
                     if (Hi >= 0 && b < nc && (j + 1 == segC[q + 1] || posbin[j + 1] != b)) {
                         const long long bg = nst[4 * q], bh = nst[4 * q + 1], Gi = nst[4 * q + 2];
-                        const double Gd = (double)Gi * FX, Hd = (double)Hi * FX;
-                        const double parent = Gd * Gd / (Hd + A.lam);
+                        const double parent = npar[q];
                         const long long GLi = Pg[p] - bg, HLi = Ph[p] - bh;
                         const double GL = (double)GLi * FX, HL = (double)HLi * FX;
                         const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
@@ -1305,6 +1328,17 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
     for (int i = blockIdx.x * FUSED_NT + tid; i < N; i += G * FUSED_NT)
         A.pred[T & 1][i] = __fadd_rn(__ldcg(A.pred[(T - 1) & 1] + i), lval[leafof[i]]);
 #ifdef AT_FIT_TIMING
+    if (threadIdx.x == 0) {
+        const unsigned long long wk = ft[7] + ft[2] + ft[3] + ft[8] + ft[4];
+        atomicMin(&g_ft_work_min, wk);
+        atomicMax(&g_ft_work_max, wk);
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (blockIdx.x < 1024) g_ft_smid[blockIdx.x] = smid;
+        __threadfence();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("per-block level work per tree: min %llu max %llu ns\n", g_ft_work_min / A.n_trees, g_ft_work_max / A.n_trees);
     if (blockIdx.x == 0 && threadIdx.x == 0)
         printf("fused forest (block 0, ns per tree, G=%d resident=%d): grads %llu barrier0 %llu | per-tree sums over levels: "
                "load %llu partition %llu scan %llu cand %llu (cas %llu) barrier %llu decide+leaves %llu\n", G, (int)resident,
@@ -1473,7 +1507,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             unsigned *bar = ws.get<unsigned>(32);
             unsigned long long *decp = ws.get<unsigned long long>((size_t)FUSED_NREP * 128);
             uint16_t *gord = resident ? nullptr : ws.get<uint16_t>((size_t)F * n);
-            uint16_t *gord0 = resident ? nullptr : ws.get<uint16_t>((size_t)F * n);
+            uint16_t *gord0 = ws.get<uint16_t>((size_t)F * n);   // initial bin-sorted orders
             uint8_t *gnode = resident ? nullptr : ws.get<uint8_t>((size_t)F * n);
             if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
             AT_CUDA_TRY(cudaMemsetAsync(bar, 0, 32 * sizeof(unsigned), s));
