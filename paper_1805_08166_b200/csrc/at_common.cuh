@@ -30,6 +30,7 @@ int cuda_fail(cudaError_t e, const char *where);
 // launch accounting + optional per-class CUDA-event timing (at_prof_*)
 void prof_begin(int cls, cudaStream_t s);
 void prof_end(int cls, cudaStream_t s);
+void note_launch();            // one library kernel launched (at_launch_count)
 void prof_suspend(bool on);   // while capturing a graph: count launches, record no events
 
 struct ProfScope {

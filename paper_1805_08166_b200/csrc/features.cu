@@ -78,7 +78,7 @@ extern "C" int features_extract(at_space sp, const uint64_t *d_idx, int64_t n, f
     const int64_t blocks = (n + at::FEAT_BLOCK - 1) / at::FEAT_BLOCK;
     if (blocks > 0x7FFFFFFF) return at::fail(AT_EUNSUPPORTED, "features_extract: n too large for one launch");
     at::ProfScope ps(AT_K_FEATURES, s);
-    at::features_kernel<<<(unsigned)blocks, at::FEAT_BLOCK, smem, s>>>(sp->d_space, sp->d_fact, d_idx, n, d_feat, ld);
+    at::features_kernel<<<(unsigned)blocks, at::FEAT_BLOCK, smem, s>>>(sp->d_space, sp->d_fact, d_idx, n, d_feat, ld); at::note_launch();
     AT_LAUNCH_CHECK("features_kernel");
     return AT_OK;
 }

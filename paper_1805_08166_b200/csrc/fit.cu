@@ -1438,13 +1438,13 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     {
         ProfScope ps(AT_K_FIT_PREP, s);
         AT_CUDA_TRY(cudaMemsetAsync(d_info, 0, 8 * sizeof(int32_t), s));
-        finite_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, n, d_info + 2);
-        key_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, n, d_info + 2);
-        sort_feature_kernel<<<F, 1024, 0, s>>>(d_feat, ld, n, sortA, sortB);
-        cuts_kernel<<<F, 1024, 0, s>>>(sortA, n, B, cuts, ncuts);
-        bin_layout_kernel<<<1, 32, 0, s>>>(ncuts, F, boff, d_info);
-        bins_kernel<<<dim3(nblk(n, 256), F), 256, 0, s>>>(d_feat, ld, n, F, B, cuts, ncuts, bins);
-        ranks_kernel<<<1, 1024, 0, s>>>(d_group_key, n, rank, counts, woff, gpre, GS);
+        finite_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, n, d_info + 2); note_launch();
+        key_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, n, d_info + 2); note_launch();
+        sort_feature_kernel<<<F, 1024, 0, s>>>(d_feat, ld, n, sortA, sortB); note_launch();
+        cuts_kernel<<<F, 1024, 0, s>>>(sortA, n, B, cuts, ncuts); note_launch();
+        bin_layout_kernel<<<1, 32, 0, s>>>(ncuts, F, boff, d_info); note_launch();
+        bins_kernel<<<dim3(nblk(n, 256), F), 256, 0, s>>>(d_feat, ld, n, F, B, cuts, ncuts, bins); note_launch();
+        ranks_kernel<<<1, 1024, 0, s>>>(d_group_key, n, rank, counts, woff, gpre, GS); note_launch();
         AT_CUDA_TRY(cudaMemcpyAsync(d_info + 3, gpre + FIT_MAXKEYS, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         AT_CUDA_TRY(cudaMemsetAsync(pred, 0, sizeof(float) * n, s));
         AT_LAUNCH_CHECK("fit prep");
@@ -1475,7 +1475,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         AT_CUDA_TRY(cudaMemsetAsync(gm->d_nodes, 0, sizeof(uint2) * (size_t)gm->t_pad * n_int, s));
         AT_CUDA_TRY(cudaMemsetAsync(gm->d_leaf, 0, sizeof(float) * (size_t)gm->t_pad * n_leaf, s));
         pack_nodes_kernel<<<nblk((int64_t)o->n_trees * n_int, 256), 256, 0, s>>>(t_feat, t_thr, (int64_t)o->n_trees * n_int,
-                                                                                 gm->d_nodes);
+                                                                                 gm->d_nodes); note_launch();
         AT_CUDA_TRY(cudaMemcpyAsync(gm->d_leaf, t_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf,
                                     cudaMemcpyDeviceToDevice, s));
         if (o->d_pred_out) AT_CUDA_TRY(cudaMemcpyAsync(o->d_pred_out, pred, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
@@ -1513,7 +1513,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             AT_CUDA_TRY(cudaMemsetAsync(bar, 0, 32 * sizeof(unsigned), s));
             AT_CUDA_TRY(cudaMemsetAsync(decp, 0, FUSED_NREP * 128 * sizeof(unsigned long long), s));
             AT_CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(unsigned long long) * 2 * FUSED_NSUB * n_int, s));
-            klist_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, woff, n, klist);
+            klist_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, woff, n, klist); note_launch();
             AT_LAUNCH_CHECK("klist");
             FusedArgs fa;
             fa.bins = bins; fa.ncuts = ncuts; fa.cuts = cuts; fa.B = B;
@@ -1533,6 +1533,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                 ProfScope ps(AT_K_FIT_GRAPH, s);
                 AT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)fused_forest_kernel, dim3(G), dim3(FUSED_NT), args,
                                                         fsm, s));
+                note_launch();
             }
             return finish();
         }
@@ -1559,9 +1560,11 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             {
                 ProfScope ps(AT_K_FIT_GRAD, s);
                 positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, (uint32_t)t,
-                                                              member);
-                if (n_groups > 0)
+                                                              member); note_launch();
+                if (n_groups > 0) {
                     grads_kernel<<<n_groups, 256, grad_smem, s>>>(member, counts, woff, gpre, GS, d_cost, pred, g, h);
+                    note_launch();
+                }
                 AT_LAUNCH_CHECK("fit gradients");
             }
             AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
@@ -1579,21 +1582,23 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                     {
                         ProfScope ps(AT_K_FIT_HIST, s);
                         hist_split_kernel<<<F, 256, smem, s>>>(bins, node, g, h, n, boff, F, first, nn, lam, mcw, dead,
-                                                               best_gain, best_s, want_h0 ? hist : nullptr);
+                                                               best_gain, best_s, want_h0 ? hist : nullptr); note_launch();
                         AT_LAUNCH_CHECK("hist_split_kernel");
                     }
-                    if (want_h0)
+                    if (want_h0) {
                         hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hist, boff, F, B,
                                                                                      o->d_hist0_out);
+                        note_launch();
+                    }
                     ProfScope ps(AT_K_FIT_SPLIT, s);
                     if (n <= 65536 && nn <= 64) {
                         decide_partition_kernel<<<nblk(n, 256), 256, 0, s>>>(best_gain, best_s, F, first, nn, cuts, B,
                                                                             dead, split_f, split_s, tf, tt, bins, n,
-                                                                            node);
+                                                                            node); note_launch();
                     } else {
                         split_node_kernel<<<nn, 256, 0, s>>>(best_gain, best_s, F, first, nn, cuts, B, dead,
-                                                             split_f, split_s, tf, tt);
-                        partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
+                                                             split_f, split_s, tf, tt); note_launch();
+                        partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node); note_launch();
                     }
                     AT_LAUNCH_CHECK("split/partition");
                     continue;
@@ -1602,31 +1607,35 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                     ProfScope ps(AT_K_FIT_HIST, s);
                     if (n_chunks != 1 || !use_smem || ns == 0)
                         AT_CUDA_TRY(cudaMemsetAsync(hist, 0, cells * sizeof(int64_t), s));
-                    if (ns > 0)
+                    if (ns > 0) {
                         hist_kernel<<<dim3(F, (unsigned)n_chunks), 256, use_smem ? smem : 0, s>>>(
                             bins, node, g, h, hb, he, n, chunk, boff, TB, first, nn, use_smem, hist);
+                        note_launch();
+                    }
                     AT_LAUNCH_CHECK("hist_kernel");
                 }
                 if (o->allreduce) {
                     const int rc = o->allreduce(hist, (int64_t)cells, o->ctx, stream);
                     if (rc) return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
                 }
-                if (want_h0)
+                if (want_h0) {
                     hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hist, boff, F, B, o->d_hist0_out);
+                    note_launch();
+                }
                 {
                     ProfScope ps(AT_K_FIT_SPLIT, s);
                     split_feature_kernel<<<nblk((int64_t)nn * F, 8), 256, 0, s>>>(hist, boff, TB, F, first, nn, lam,
-                                                                                  mcw, dead, best_gain, best_s);
+                                                                                  mcw, dead, best_gain, best_s); note_launch();
                     split_node_kernel<<<nn, 256, 0, s>>>(best_gain, best_s, F, first, nn, cuts, B, dead, split_f, split_s,
-                                                         tf, tt);
-                    partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node);
+                                                         tf, tt); note_launch();
+                    partition_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, node); note_launch();
                     AT_LAUNCH_CHECK("split/partition");
                 }
             }
             {
                 ProfScope ps(AT_K_FIT_UPDATE, s);
                 AT_CUDA_TRY(cudaMemsetAsync(lsum, 0, sizeof(int64_t) * 2 * n_leaf, s));
-                if (he > hb) leafsum_kernel<<<nblk(he - hb, 256), 256, 0, s>>>(node, g, h, hb, he, n_int, lsum);
+                if (he > hb) { leafsum_kernel<<<nblk(he - hb, 256), 256, 0, s>>>(node, g, h, hb, he, n_int, lsum); note_launch(); }
                 AT_LAUNCH_CHECK("leafsum");
             }
             if (o->allreduce) {
@@ -1636,8 +1645,8 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             {
                 ProfScope ps(AT_K_FIT_UPDATE, s);
                 float *tl = t_leaf + (size_t)t * n_leaf;
-                leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(lsum, n_leaf, eta, lam, tl);
-                pred_update_kernel<<<nblk(n, 256), 256, 0, s>>>(node, n, n_int, tl, pred);
+                leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(lsum, n_leaf, eta, lam, tl); note_launch();
+                pred_update_kernel<<<nblk(n, 256), 256, 0, s>>>(node, n, n_int, tl, pred); note_launch();
                 AT_LAUNCH_CHECK("leaf/pred update");
             }
         }

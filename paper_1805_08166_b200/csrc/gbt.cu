@@ -282,6 +282,7 @@ int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_s
     else
         at::predict_kernel<2><<<blocks, at::PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                      d_leaf_slot, use_bulk, tm);
+    at::note_launch();
     AT_LAUNCH_CHECK("predict_kernel");
     return AT_OK;
 }

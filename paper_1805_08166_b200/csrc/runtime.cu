@@ -28,6 +28,7 @@ static std::atomic<int64_t> g_launches{0};
 static thread_local bool g_suspend = false;
 
 void prof_suspend(bool on) { g_suspend = on; }
+void note_launch() { g_launches.fetch_add(1); }
 static std::atomic<int> g_prof_on{0};
 static std::mutex g_prof_mu;
 struct EvPair { cudaEvent_t a, b; };
@@ -44,7 +45,6 @@ static cudaEvent_t take_event()
 
 void prof_begin(int cls, cudaStream_t s)
 {
-    g_launches.fetch_add(1);
     if (!g_prof_on.load() || g_suspend) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t e;

@@ -373,6 +373,7 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         const unsigned blocks = (unsigned)((o->n_chains + cpb - 1) / cpb);
         if (use2) at::sa_kernel<2><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
         else at::sa_kernel<1><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
+        at::note_launch();
         AT_LAUNCH_CHECK("sa_kernel");
     }
     for (int w = 0; w < sp->host.n_w; ++w) {

@@ -193,7 +193,7 @@ extern "C" int select_topk(at_space sp, int32_t workload, const uint64_t *d_pool
     at::ProfScope ps(AT_K_SELECT, s);
     at::select_kernel<<<1, at::SEL_THREADS, 0, s>>>(sp->d_space, workload, d_pool_idx, d_pool_score, (int)n_pool,
                                                     d_measured_sorted, n_measured, o->b, o->eps, o->alpha, o->seed,
-                                                    o->round, d_out_idx, d_out_n);
+                                                    o->round, d_out_idx, d_out_n); at::note_launch();
     AT_LAUNCH_CHECK("select_kernel");
     return AT_OK;
 }

@@ -184,7 +184,7 @@ int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s)
     if (blocks < 1) blocks = 1;
     uint64_t *bufA = scratch, *bufB = scratch + (blocks + 1) * K;
     ProfScope ps(AT_K_TOPK, s);
-    topk_tile_kernel<<<(unsigned)blocks, TK_THREADS, 0, s>>>(S, K, bufA);
+    topk_tile_kernel<<<(unsigned)blocks, TK_THREADS, 0, s>>>(S, K, bufA); at::note_launch();
     AT_LAUNCH_CHECK("topk_tile_kernel");
     int64_t n = blocks * K;
     while (blocks > 1) {
@@ -193,12 +193,12 @@ int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s)
         R.keys = bufA;
         R.n = n;
         blocks = (n + TK_TILE - 1) / TK_TILE;
-        topk_tile_kernel<<<(unsigned)blocks, TK_THREADS, 0, s>>>(R, K, bufB);
+        topk_tile_kernel<<<(unsigned)blocks, TK_THREADS, 0, s>>>(R, K, bufB); at::note_launch();
         AT_LAUNCH_CHECK("topk_tile_kernel(reduce)");
         n = blocks * K;
         uint64_t *t = bufA; bufA = bufB; bufB = t;
     }
-    topk_finish_kernel<<<1, 256, 0, s>>>(bufA, K, a.offset_w, a.out_idx, a.out_score, a.out_n);
+    topk_finish_kernel<<<1, 256, 0, s>>>(bufA, K, a.offset_w, a.out_idx, a.out_score, a.out_n); at::note_launch();
     AT_LAUNCH_CHECK("topk_finish_kernel");
     return AT_OK;
 }
