@@ -69,23 +69,29 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
     const float *leaves = (const float *)(buf + (size_t)G.CH * G.ni * 8);
     const int D = G.D, ni = G.ni, nl = G.nl;
     const uint32_t tree_bytes = (uint32_t)ni * 8u;
-    const uint8_t *tb[NB];
-    uint32_t off[GRP][NB];   // byte offset of the current node: node i at 8 i, children at 2 off + 8 / + 16
+    // a = shared address of the current node = tb + 8 h (h: 1-based heap index, tb = tree base - 8);
+    // the left child 2h sits at 2a - tb, the right one 2h + 1 at 2a - tb + 8, so one select of a
+    // precomputed addend and one 3-input add advance a walk: LDS.64, IMAD, LDS, FSETP, SEL, IADD3
+    uint32_t add_l[NB], add_r[NB], a[GRP][NB];
 #pragma unroll
     for (int jj = 0; jj < NB; ++jj) {
-        tb[jj] = buf + (uint32_t)(t0 + jj * NW - c0) * tree_bytes;
+        const uint32_t tb = (uint32_t)__cvta_generic_to_shared(buf) + (uint32_t)(t0 + jj * NW - c0) * tree_bytes - 8u;
+        add_l[jj] = 0u - tb;
+        add_r[jj] = 8u - tb;
 #pragma unroll
-        for (int g = 0; g < GRP; ++g) off[g][jj] = 0;
+        for (int g = 0; g < GRP; ++g) a[g][jj] = tb + 8u;
     }
     for (int d = 0; d < D; ++d) {
 #pragma unroll
         for (int g = 0; g < GRP; ++g) {
-            const uint8_t *tile_lane = (const uint8_t *)(tile + g * gstride + lane);   // feature f at + f * 128
+            const uint32_t tile_lane = (uint32_t)__cvta_generic_to_shared(tile + g * gstride + lane);   // feature f at + f * 128
 #pragma unroll
             for (int jj = 0; jj < NB; ++jj) {
-                const uint2 nd = *(const uint2 *)(tb[jj] + off[g][jj]);
-                const float x = *(const float *)(tile_lane + (nd.x << 7));
-                off[g][jj] = 2u * off[g][jj] + (x < __uint_as_float(nd.y) ? 8u : 16u);
+                uint32_t nf, nt;
+                float x;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g][jj]));
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile_lane + (nf << 7)));
+                a[g][jj] = 2u * a[g][jj] + (x < __uint_as_float(nt) ? add_l[jj] : add_r[jj]);
             }
         }
     }
@@ -96,7 +102,7 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
         const int j = (t & 31) / NW;
 #pragma unroll
         for (int g = 0; g < GRP; ++g) {
-            const int slot = (int)(off[g][jj] >> 3) - ni;
+            const int slot = (int)((a[g][jj] + add_l[jj]) >> 3) - nl;   // h = (a - tb) / 8 in [2^D, 2^(D+1))
             const float lv = leaves[(t - c0) * nl + slot];
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
