@@ -801,19 +801,36 @@ struct FusedArgs {
     unsigned *bar;
 };
 
-__host__ __device__ inline size_t fused_smem_bytes(int N, int GS)
+__host__ __device__ inline int fused_ep(int N)
 {
     int EP = 1;                                      // positions per thread (power of two)
     while (EP * FUSED_NT < N) EP <<= 1;
-    const int PP = EP * FUSED_NT > 512 ? EP * FUSED_NT : 512;   // Pg also holds leaf sums / sort counters
-    size_t b = 8 * (2 * (size_t)N + 2 * (size_t)PP); // sg sh (int64, by sample) Ph Pg (int64, by position)
+    return EP;
+}
+
+// per-block node tables and scan scratch (nodes of one level <= 128, children <= 256)
+struct FusedTail {
+    int32_t segP[260], segC[260];                   // parent / child segment bounds (positions)
+    int32_t decf[128], decs[128];                   // level decisions (f, s); decf < 0: no split
+    int32_t Rst[128], Ren[128];                     // right-going count before a segment / through its end
+    long long baseG[128], baseH[128], endG[128], endH[128];   // prefix sums before / at the end of a node
+    unsigned nbh[128], nbl[128], nms[128];          // per-node best gain (hi, lo words) and its lowest s
+    unsigned decw[128];                             // published decision words
+    float lval[256];                                // leaf values of the current tree
+    int32_t wsi[2][FUSED_NT / 32];                  // scan scratch
+    long long wsl[2][2 * (FUSED_NT / 32)];
+    uint8_t dead[512];
+};
+
+__host__ __device__ inline size_t fused_smem_bytes(int N, int GS)
+{
+    size_t b = 16 * (size_t)N;                       // sg sh (int64, by sample)
+    b += 8 * 512;                                    // leaf sums (u64 [2^D][2]) / counting-sort counters
     b += 12 * (size_t)GS;                            // mem sc sp
-    b += 4 * (size_t)N;                              // ord ord2 (u16)
-    b += 2 * (size_t)EP * FUSED_NT;                  // rex (u16, by position, transposed)
-    b += 5 * (size_t)N;                              // nat nat2 sbin posbin leafof (u8)
+    b += 4 * (size_t)N;                              // ordA ordB (u16)
+    b += 5 * (size_t)N + 16;                         // natA natB sbin posbin leafof (u8)
     b = (b + 15) & ~(size_t)15;
-    b += 2 * 257 * 4 + 2 * 128 * 4 + 8 * 16 + 512 + 256 * 4 + 128 * 32 + 128 * 4 + 128 * 8;   // segP segC decf decs scan dead lval kq/nst decw npar
-    return b;
+    return b + sizeof(FusedTail);
 }
 
 __device__ __forceinline__ uint32_t feistel_inv(uint32_t y, int h, uint64_t seed, uint32_t tree, uint32_t wkey)
@@ -849,65 +866,87 @@ __device__ __forceinline__ void slot_max(unsigned long long *p, unsigned long lo
     }
 }
 
-#ifdef AT_FIT_TIMING
-__device__ __forceinline__ unsigned long long gtimer()
+// block-wide exclusive scan of one int per thread (thread order); `ws` must not be reused before
+// the next __syncthreads after this call
+__device__ __forceinline__ int blk_excl_int(int v, int lane, int warp, int32_t *ws, int &total)
 {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    int o = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < FUSED_NT / 32; ++w) {
+        const int u = ws[w];
+        o += w < warp ? u : 0;
+        tot += u;
+    }
+    total = tot;
+    return o + x - v;
 }
-#define FT_MARK(k) do { if (threadIdx.x == 0) { unsigned long long _t = gtimer(); ft[k] += _t - ft_last; ft_last = _t; } } while (0)
-__device__ unsigned long long g_ft_work_min = ~0ull, g_ft_work_max = 0ull;
-__device__ unsigned g_ft_smid[1024];
-#else
-#define FT_MARK(k) do {} while (0)
-#endif
 
-__global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
+// the same for a pair of int64 (exact, order-free)
+__device__ __forceinline__ void blk_excl_i64x2(long long a, long long b, int lane, int warp, long long *ws,
+                                               long long &oa, long long &ob)
 {
-#ifdef AT_FIT_TIMING
-    unsigned long long ft[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer();
-#endif
+    long long x = a, y = b;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long u = __shfl_up_sync(0xFFFFFFFFu, x, off), v = __shfl_up_sync(0xFFFFFFFFu, y, off);
+        if (lane >= off) { x += u; y += v; }
+    }
+    if (lane == 31) { ws[2 * warp] = x; ws[2 * warp + 1] = y; }
+    __syncthreads();
+    long long pa = x - a, pb = y - b;
+#pragma unroll
+    for (int w = 0; w < FUSED_NT / 32; ++w)
+        if (w < warp) { pa += ws[2 * w]; pb += ws[2 * w + 1]; }
+    oa = pa;
+    ob = pb;
+}
+
+// One cooperative launch fits the whole forest.  Block b owns feature b (and b + G, ... when F > G).
+// Thread t owns the EP consecutive positions t EP .. t EP + EP - 1 of the block's feature order, so
+// every per-position quantity of a level (sample, node, go-right flag, prefix sums, split key) stays
+// in registers between the block scans:
+//   partition: flags -> block scan -> right counts at segment bounds -> scatter of (sample, child);
+//   prefix sums of (g, h) in the new order -> node bases / totals -> every run end's fp64 gain;
+//   per-node max by native 32-bit shared atomics (gain high word, low word, then the lowest s among
+//   equal gains), one 128-bit global atomic max per node on (gain, 0xFFFF - f, 0xFFFF - s).
+template <int EP>
+__global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel(FusedArgs A)
+{
     extern __shared__ __align__(16) unsigned char fsm[];
     const int N = A.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = FUSED_NT / 32;
-    // Position-indexed int64 arrays (Pg, Ph, rex) are stored transposed: logical position
-    // j = t * EP + k (thread t's k-th contiguous position) lives at k * 256 + t, so the scans'
-    // per-thread runs are bank-conflict free.
-    int EP = 1, LE = 0;
-    while (EP * FUSED_NT < N) { EP <<= 1; ++LE; }
-    const int PP = EP * FUSED_NT > 512 ? EP * FUSED_NT : 512;
-    auto PH = [&](int j) { return ((j & (EP - 1)) << 8) + (j >> LE); };
-    int64_t *sg = (int64_t *)fsm, *sh = sg + N, *Ph = sh + N, *Pg = Ph + PP;
-    int32_t *mem = (int32_t *)(Pg + PP);
+    int64_t *sg = (int64_t *)fsm, *sh = sg + N;
+    unsigned long long *lsum = (unsigned long long *)(sh + N);   // [512]
+    unsigned *cnt = (unsigned *)lsum;                            // counting sort scratch (init only)
+    int32_t *mem = (int32_t *)(lsum + 512);
     float *sc = (float *)(mem + A.GS), *sp = sc + A.GS;
-    uint16_t *ordA = (uint16_t *)(sp + A.GS), *ordB = ordA + N, *rex = ordB + N;   // rex: EP * 256
-    uint8_t *natA = (uint8_t *)(rex + EP * FUSED_NT), *natB = natA + N, *sbin = natB + N, *posbin = sbin + N,
-            *leafof = posbin + N;
-    unsigned char *tail = fsm + ((((size_t)(leafof + N - fsm)) + 15) & ~(size_t)15);
-    int32_t *segP = (int32_t *)tail, *segC = segP + 257, *decf = segC + 257, *decs = decf + 128;
-    long long *wsc = (long long *)(decs + 128);   // 16 long long: scan scratch
-    uint8_t *dead = (uint8_t *)(wsc + 16);
-    float *lval = (float *)(dead + 512);
-    unsigned long long *kq = (unsigned long long *)(lval + 256);   // [128] x (lo, hi) per-node keys / node stats
-    unsigned *decw = (unsigned *)(kq + 512);                         // [128] published decisions
-    double *npar = (double *)(decw + 128);                           // [128] node parent scores
-    unsigned *cnt = (unsigned *)Pg;                // counting sort scratch (init only)
+    uint16_t *ordA = (uint16_t *)(sp + A.GS), *ordB = ordA + N;
+    uint8_t *natA = (uint8_t *)(ordB + N), *natB = natA + N, *sbin = natB + N, *posbin = sbin + N,
+            *leafof = posbin + N + 16;
+    FusedTail &T = *(FusedTail *)(fsm + ((((size_t)(leafof + N - fsm)) + 15) & ~(size_t)15));
 
     const int G = gridDim.x, F = A.F, D = A.D;
     const int n_int = (1 << D) - 1, n_leaf = 1 << D;
     const bool resident = F <= G;
     unsigned epoch = 0;
-    // gradient work items: (group, chunk of CM members); every item rebuilds its group's member
-    // list (inverse Feistel walk) and computes its chunk's members, one warp per member
     const int CM = A.GS / 8 > 8 ? A.GS / 8 : 8;
     const int chunks = (A.GS + CM - 1) / CM;
+    for (int q = tid; q < 128; q += FUSED_NT) { T.nbh[q] = 0; T.nbl[q] = 0; T.nms[q] = 0xFFFFFFFFu; }
+
     // Grid-wide sync.  Every block arrives on one counter (fire-and-forget add after a fence);
     // block 0 alone polls it, reduces the level's sub-slots into the decisions (nn > 0), writes the
     // tree nodes, re-zeroes the sub-slots (node ids are unique within a tree; later fences order
     // the zeroing before the next tree's atomics) and publishes FUSED_NREP replicas of
     // (epoch << 32 | decision) -- every block polls its own replica, so no L2 line is polled or
-    // read by all blocks, and the decisions arrive with the release.  decw[q] gets the decisions.
+    // read by all blocks, and the decisions arrive with the release.  T.decw[q] gets the decisions.
     auto sync_all = [&](int t, int nn, int first) {
         __syncthreads();
         ++epoch;
@@ -964,47 +1003,8 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
         for (int q = tid; q < nq; q += FUSED_NT) {
             unsigned long long v = rep[q];
             while ((unsigned)(v >> 32) != epoch) v = rep[q];
-            decw[q] = (unsigned)v;
+            T.decw[q] = (unsigned)v;
         }
-        __syncthreads();
-    };
-
-    // block-wide inclusive scan of Pg/Ph over all EP * 256 positions (padding holds zeros)
-    auto scan_pair = [&]() {
-        long long ag = 0, ah = 0;
-        for (int k = 0; k < EP; ++k) {
-            const int p = (k << 8) + tid;
-            ag += Pg[p]; ah += Ph[p]; Pg[p] = ag; Ph[p] = ah;
-        }
-        long long xg = ag, xh = ah;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const long long yg = __shfl_up_sync(0xFFFFFFFFu, xg, off), yh = __shfl_up_sync(0xFFFFFFFFu, xh, off);
-            if (lane >= off) { xg += yg; xh += yh; }
-        }
-        if (lane == 31) { wsc[2 * warp] = xg; wsc[2 * warp + 1] = xh; }
-        __syncthreads();
-        long long og = xg - ag, oh = xh - ah;
-        for (int w = 0; w < warp; ++w) { og += wsc[2 * w]; oh += wsc[2 * w + 1]; }
-        for (int k = 0; k < EP; ++k) { const int p = (k << 8) + tid; Pg[p] += og; Ph[p] += oh; }
-        __syncthreads();
-    };
-    // block-wide exclusive scan of the 0/1 flags rex (transposed, padding zero); wsc[8] = total
-    auto scan_flags = [&]() {
-        int a = 0;
-        for (int k = 0; k < EP; ++k) { const int p = (k << 8) + tid; const int v = rex[p]; rex[p] = (uint16_t)a; a += v; }
-        int x = a;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
-            if (lane >= off) x += y;
-        }
-        if (lane == 31) wsc[warp] = x;
-        __syncthreads();
-        int o = x - a;
-        for (int w = 0; w < warp; ++w) o += (int)wsc[w];
-        for (int k = 0; k < EP; ++k) rex[(k << 8) + tid] = (uint16_t)(rex[(k << 8) + tid] + o);
-        if (tid == FUSED_NT - 1) wsc[8] = o + a;
         __syncthreads();
     };
 
@@ -1049,11 +1049,11 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
                     const int mid = (lo + hi) >> 1;
                     if (A.gpre[mid] <= grp) lo = mid; else hi = mid;
                 }
-                decf[0] = lo;
+                T.wsi[0][0] = lo;
             }
             __syncthreads();
-            const int w = decf[0];
-            __syncthreads();   // decf[0] is rewritten by the next item
+            const int w = T.wsi[0][0];
+            __syncthreads();   // rewritten by the next item
             const int nw = A.counts[w];
             const int start = (grp - A.gpre[w]) * A.GS;
             const int m = min(A.GS, nw - start);
@@ -1070,7 +1070,7 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
                 mem[a] = i;
                 float pv = 0.0f;
                 if (t > 0) {
-                    pv = __fadd_rn(__ldcg(A.pred[(t - 1) & 1] + i), lval[leafof[i]]);
+                    pv = __fadd_rn(__ldcg(A.pred[(t - 1) & 1] + i), T.lval[leafof[i]]);
                     if (a >= a0 && a < a1) A.pred[t & 1][i] = pv;   // the chunk owning the member writes it
                 }
                 sp[a] = pv;
@@ -1095,13 +1095,11 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
             }
             __syncthreads();
         }
-        FT_MARK(0);
         sync_all(t, 0, 0);
-        FT_MARK(1);
 
         for (int i = tid; i < N; i += FUSED_NT) { sg[i] = __ldcg(A.g + i); sh[i] = __ldcg(A.h + i); }
-        for (int q = tid; q < 512; q += FUSED_NT) dead[q] = 0;
-        if (tid == 0) { segP[0] = 0; segP[1] = N; }
+        for (int q = tid; q < 512; q += FUSED_NT) T.dead[q] = 0;
+        if (tid == 0) { T.segP[0] = 0; T.segP[1] = N; }
         __syncthreads();
 
         for (int d = 0; d < D; ++d) {
@@ -1115,198 +1113,228 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
                             ord[j] = A.gord[(int64_t)f * N + j];
                             nat[j] = A.gnode[(int64_t)f * N + j];
                         }
+                    __syncthreads();
                 } else if (t == 0 && d == 0) {
                     for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
-                }
-                FT_MARK(7);
-                if (d == 0) {
-                    // the bin-sorted order, with the (g, h) and bins of every position
-                    for (int k = 0; k < EP; ++k) {
-                        const int j = tid * EP + k, p = (k << 8) + tid;
-                        long long vg = 0, vh = 0;
-                        if (j < N) {
-                            const int i = __ldcg(A.gord0 + (int64_t)f * N + j);
-                            ord[j] = (uint16_t)i;
-                            nat[j] = 0;
-                            posbin[j] = sbin[i];
-                            vg = sg[i];
-                            vh = sh[i];
-                        }
-                        Pg[p] = vg;
-                        Ph[p] = vh;
-                    }
-                    if (tid == 0) { segC[0] = 0; segC[1] = N; }
                     __syncthreads();
+                }
+                int iv[EP], qv[EP];   // sample and node of each owned position (in the level's order)
+                if (d == 0) {
+#pragma unroll
+                    for (int k = 0; k < EP; ++k) {
+                        const int j = tid * EP + k;
+                        iv[k] = 0;
+                        qv[k] = 0;
+                        if (j < N) {
+                            iv[k] = (int)__ldcg(A.gord0 + (int64_t)f * N + j);
+                            ord[j] = (uint16_t)iv[k];
+                            nat[j] = 0;
+                        }
+                    }
+                    if (tid == 0) { T.segC[0] = 0; T.segC[1] = N; }
                 } else {
                     // stable partition of every parent segment by the parent's decision
-                    __syncthreads();
-                    for (int kb = 0; kb < EP; kb += 4) {
-                        int bv[4], th[4];   // all gathers of the batch in flight together
+                    int fl[EP], c = 0;
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int j = tid * EP + kb + u;
-                            bv[u] = 0;
-                            th[u] = 1 << 30;
-                            if (kb + u < EP && j < N) {
-                                const int i = ord[j], q = nat[j], sf = decf[q];
-                                if (sf >= 0) {
-                                    th[u] = decs[q];
-                                    bv[u] = sf == f ? (int)sbin[i] : (int)__ldg(A.bins + (int64_t)sf * N + i);
-                                }
+                    for (int k = 0; k < EP; ++k) {   // all gathers of the thread in flight together
+                        const int j = tid * EP + k;
+                        fl[k] = 0;
+                        iv[k] = 0;
+                        qv[k] = 0;
+                        int bv = 0, th = 1 << 30;
+                        if (j < N) {
+                            const int i = ord[j], q = nat[j], sf = T.decf[q];
+                            iv[k] = i;
+                            qv[k] = q;
+                            if (sf >= 0) {
+                                th = T.decs[q];
+                                bv = sf == f ? (int)sbin[i] : (int)__ldg(A.bins + (int64_t)sf * N + i);
                             }
                         }
+                        fl[k] = bv >= th ? 1 : 0;
+                        c += fl[k];
+                    }
+                    int rtot;
+                    const int ex0 = blk_excl_int(c, lane, warp, T.wsi[0], rtot);
+                    int ex = ex0;
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (kb + u < EP) rex[((kb + u) << 8) + tid] = bv[u] >= th[u] ? 1 : 0;
+                    for (int k = 0; k < EP; ++k) {
+                        const int j = tid * EP + k;
+                        if (j < N) {
+                            const int q = qv[k];
+                            if (j == T.segP[q]) T.Rst[q] = ex;
+                            if (j + 1 == T.segP[q + 1]) T.Ren[q] = ex + fl[k];
+                        }
+                        ex += fl[k];
                     }
                     __syncthreads();
-                    scan_flags();
-                    const int rtot = (int)wsc[8];
-                    auto rx = [&](int x) { return x < N ? rex[PH(x)] : rtot; };
-                    for (int j = tid; j < N; j += FUSED_NT) {
-                        const int q = nat[j], s0 = segP[q], s1 = segP[q + 1];
-                        const int r0 = rx(s0), nR = rx(s1) - r0, nL = (s1 - s0) - nR;
-                        const int rj = rx(j), right = rx(j + 1) - rj, rb = rj - r0;
-                        const int np = right ? s0 + nL + rb : s0 + (j - s0) - rb;
-                        ord2[np] = ord[j];
-                        nat2[np] = (uint8_t)(2 * q + right);
+                    ex = ex0;
+#pragma unroll
+                    for (int k = 0; k < EP; ++k) {
+                        const int j = tid * EP + k;
+                        if (j < N) {
+                            const int q = qv[k], s0 = T.segP[q], s1 = T.segP[q + 1];
+                            const int r0 = T.Rst[q], nR = T.Ren[q] - r0, nL = (s1 - s0) - nR, rb = ex - r0;
+                            const int np = fl[k] ? s0 + nL + rb : j - rb;
+                            ord2[np] = (uint16_t)iv[k];
+                            nat2[np] = (uint8_t)(2 * q + fl[k]);
+                        }
+                        ex += fl[k];
                     }
                     for (int q = tid; q < nnP; q += FUSED_NT) {
-                        const int s0 = segP[q], s1 = segP[q + 1];
-                        const int nR = rx(s1) - rx(s0);
-                        segC[2 * q] = s0;
-                        segC[2 * q + 1] = s1 - nR;
+                        const int s0 = T.segP[q], s1 = T.segP[q + 1];
+                        const int nR = s1 > s0 ? T.Ren[q] - T.Rst[q] : 0;
+                        T.segC[2 * q] = s0;
+                        T.segC[2 * q + 1] = s1 - nR;
                     }
-                    if (tid == 0) segC[2 * nnP] = N;
+                    if (tid == 0) T.segC[nn] = N;
                     __syncthreads();
                     { uint16_t *tq = ord; ord = ord2; ord2 = tq; }
                     { uint8_t *tq = nat; nat = nat2; nat2 = tq; }
-                    for (int k = 0; k < EP; ++k) {   // the positions' bins and (g, h)
-                        const int j = tid * EP + k, p = (k << 8) + tid;
-                        long long vg = 0, vh = 0;
-                        if (j < N) {
-                            const int i = ord[j];
-                            posbin[j] = sbin[i];
-                            vg = sg[i];
-                            vh = sh[i];
-                        }
-                        Pg[p] = vg;
-                        Ph[p] = vh;
+#pragma unroll
+                    for (int k = 0; k < EP; ++k) {
+                        const int j = tid * EP + k;
+                        if (j < N) { iv[k] = ord[j]; qv[k] = nat[j]; }
                     }
-                    __syncthreads();
                 }
-                FT_MARK(2);
-                // prefix sums of (g, h) in this order, then every node's run ends
-                scan_pair();
-                FT_MARK(3);
-                // node statistics, one thread per node (Hi = -1: no candidates)
-                long long *nst = (long long *)kq;   // [128][4] bg bh Gi Hi (aliases kq: disjoint in time)
-                for (int q = tid; q < nn; q += FUSED_NT) {
-                    const int s0 = segC[q], s1 = segC[q + 1];
-                    if (dead[first + q] || s1 == s0) { nst[4 * q + 3] = -1; continue; }
-                    const long long bg = s0 ? Pg[PH(s0 - 1)] : 0, bh = s0 ? Ph[PH(s0 - 1)] : 0;
-                    nst[4 * q] = bg;
-                    nst[4 * q + 1] = bh;
-                    const long long Gi = Pg[PH(s1 - 1)] - bg, Hi = Ph[PH(s1 - 1)] - bh;
-                    nst[4 * q + 2] = Gi;
-                    nst[4 * q + 3] = Hi;
-                    const double Gd = (double)Gi * FX, Hd = (double)Hi * FX;
-                    npar[q] = Gd * Gd / (Hd + A.lam);
+                // prefix sums of (g, h) in this order; node bases and totals
+                long long pg[EP], ph[EP];
+                int qb[EP];   // node << 8 | bin of each owned position
+                long long ag = 0, ah = 0;
+#pragma unroll
+                for (int k = 0; k < EP; ++k) {
+                    const int j = tid * EP + k;
+                    long long g = 0, h = 0;
+                    qb[k] = 0;
+                    if (j < N) {
+                        const int i = iv[k], b = sbin[i];
+                        g = sg[i];
+                        h = sh[i];
+                        qb[k] = (qv[k] << 8) | b;
+                        posbin[j] = (uint8_t)b;
+                    }
+                    ag += g;
+                    ah += h;
+                    pg[k] = ag;
+                    ph[k] = ah;
+                }
+                long long og, oh;
+                blk_excl_i64x2(ag, ah, lane, warp, T.wsl[0], og, oh);
+                {
+                    long long prg = og, prh = oh;
+#pragma unroll
+                    for (int k = 0; k < EP; ++k) {
+                        const int j = tid * EP + k;
+                        pg[k] += og;
+                        ph[k] += oh;
+                        if (j < N) {
+                            const int q = qb[k] >> 8;
+                            if (j == T.segC[q]) { T.baseG[q] = prg; T.baseH[q] = prh; }
+                            if (j + 1 == T.segC[q + 1]) { T.endG[q] = pg[k]; T.endH[q] = ph[k]; }
+                        }
+                        prg = pg[k];
+                        prh = ph[k];
+                    }
                 }
                 __syncthreads();
-                // every run end of every node at once (thread-contiguous positions, independent
-                // fp64 chains); the candidate's key (f fixed: gain, then lower s) replaces (Pg, Ph)
-                for (int k = 0; k < EP; ++k) {
-                    const int j = tid * EP + k, p = (k << 8) + tid;
-                    if (j >= N) break;
-                    const int q = nat[j], b = posbin[j];
-                    const long long Hi = nst[4 * q + 3];
-                    unsigned long long klo = 0, khi = 0;
-                    if (Hi >= 0 && b < nc && (j + 1 == segC[q + 1] || posbin[j + 1] != b)) {
-                        const long long bg = nst[4 * q], bh = nst[4 * q + 1], Gi = nst[4 * q + 2];
-                        const double parent = npar[q];
-                        const long long GLi = Pg[p] - bg, HLi = Ph[p] - bh;
+                // every run end of every node: the split s = b + 1 (left = bins <= b), fp64 gain in
+                // the oracle's operation order
+                unsigned long long gk[EP];
+                {
+                    int lastq = -1;
+                    long long bG = 0, bH = 0, Gi = 0, Hi = 0;
+                    double parent = 0.0;
+#pragma unroll
+                    for (int k = 0; k < EP; ++k) {
+                        const int j = tid * EP + k;
+                        gk[k] = 0ull;
+                        if (j >= N) continue;
+                        const int q = qb[k] >> 8, b = qb[k] & 0xFF;
+                        if (T.dead[first + q] || b >= nc) continue;
+                        const int s1 = T.segC[q + 1];
+                        const int nb = j + 1 >= s1 ? -1 : (k + 1 < EP ? (qb[k + 1] & 0xFF) : (int)posbin[j + 1]);
+                        if (nb == b) continue;
+                        if (q != lastq) {
+                            lastq = q;
+                            bG = T.baseG[q];
+                            bH = T.baseH[q];
+                            Gi = T.endG[q] - bG;
+                            Hi = T.endH[q] - bH;
+                            const double Gd = (double)Gi * FX, Hd = (double)Hi * FX;
+                            parent = Gd * Gd / (Hd + A.lam);
+                        }
+                        const long long GLi = pg[k] - bG, HLi = ph[k] - bH;
                         const double GL = (double)GLi * FX, HL = (double)HLi * FX;
                         const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
-                        if (!(HL < A.mcw || HR < A.mcw)) {
-                            const double gain = (GL * GL / (HL + A.lam) + GR * GR / (HR + A.lam)) - parent;
-                            if (gain > 0.0) {
-                                klo = ((unsigned long long)(0xFFFFu - (unsigned)f) << 16) |
-                                      (unsigned long long)(0xFFFFu - (unsigned)(b + 1));
-                                khi = (unsigned long long)__double_as_longlong(gain);
-                            }
-                        }
+                        if (HL < A.mcw || HR < A.mcw) continue;
+                        const double gain = (GL * GL / (HL + A.lam) + GR * GR / (HR + A.lam)) - parent;
+                        if (gain > 0.0) gk[k] = (unsigned long long)__double_as_longlong(gain);
                     }
-                    Pg[p] = (long long)klo;
-                    Ph[p] = (long long)khi;
                 }
-                __syncthreads();
-                // per-node max of the keys (warp per node)
-                for (int q = warp; q < nn; q += NW) {
-                    const int s0 = segC[q], s1 = segC[q + 1];
-                    unsigned long long lo = 0, hi = 0;
-                    for (int j = s0 + lane; j < s1; j += 32) {
-                        const unsigned long long vl = (unsigned long long)Pg[PH(j)], vh = (unsigned long long)Ph[PH(j)];
-                        if (vh > hi || (vh == hi && vl > lo)) { lo = vl; hi = vh; }
-                    }
+                // per-node max: gain high word, low word, then the lowest s among equal gains
 #pragma unroll
-                    for (int off = 16; off >= 1; off >>= 1) {
-                        const unsigned long long ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
-                        const unsigned long long oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
-                        if (oh > hi || (oh == hi && ol > lo)) { lo = ol; hi = oh; }
-                    }
-                    if (lane == 0) { kq[2 * q] = lo; kq[2 * q + 1] = hi; }
-                }
+                for (int k = 0; k < EP; ++k)
+                    if (gk[k]) atomicMax(&T.nbh[(qb[k] >> 8)], (unsigned)(gk[k] >> 32));
                 __syncthreads();
-                FT_MARK(8);
-                // one thread per node: all of the block's atomics in flight together
+#pragma unroll
+                for (int k = 0; k < EP; ++k)
+                    if (gk[k] && (unsigned)(gk[k] >> 32) == T.nbh[(qb[k] >> 8)]) atomicMax(&T.nbl[(qb[k] >> 8)], (unsigned)gk[k]);
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < EP; ++k)
+                    if (gk[k] && gk[k] == (((unsigned long long)T.nbh[(qb[k] >> 8)] << 32) | T.nbl[(qb[k] >> 8)]))
+                        atomicMin(&T.nms[(qb[k] >> 8)], (unsigned)((qb[k] & 0xFF) + 1));
+                __syncthreads();
                 for (int q = tid; q < nn; q += FUSED_NT) {
-                    const unsigned long long khi = kq[2 * q + 1];
-                    if (khi) slot_max(slot + 2 * ((first + q) * FUSED_NSUB + (blockIdx.x & (FUSED_NSUB - 1))), kq[2 * q], khi);
+                    const unsigned long long gb = ((unsigned long long)T.nbh[q] << 32) | T.nbl[q];
+                    if (gb)
+                        slot_max(slot + 2 * ((first + q) * FUSED_NSUB + (blockIdx.x & (FUSED_NSUB - 1))),
+                                 ((unsigned long long)(0xFFFFu - (unsigned)f) << 16) |
+                                     (unsigned long long)(0xFFFFu - T.nms[q]),
+                                 gb);
+                    T.nbh[q] = 0;
+                    T.nbl[q] = 0;
+                    T.nms[q] = 0xFFFFFFFFu;
                 }
-                if (!resident) {
-                    __syncthreads();
+                if (!resident)
                     for (int j = tid; j < N; j += FUSED_NT) {
                         A.gord[(int64_t)f * N + j] = ord[j];
                         A.gnode[(int64_t)f * N + j] = nat[j];
                     }
-                }
                 __syncthreads();
-                FT_MARK(4);
             }
             sync_all(t, nn, first);
-            FT_MARK(5);
             // the level's decisions (identical in every block; a dead node never has a split)
             for (int q = tid; q < nn; q += FUSED_NT) {
                 const int nd = first + q;
-                const unsigned word = decw[q];
+                const unsigned word = T.decw[q];
                 if (word == 0xFFFFFFFFu) {
-                    decf[q] = -1;
-                    decs[q] = 0;
-                    dead[2 * nd + 1] = 1;
-                    dead[2 * nd + 2] = 1;
+                    T.decf[q] = -1;
+                    T.decs[q] = 0;
+                    T.dead[2 * nd + 1] = 1;
+                    T.dead[2 * nd + 2] = 1;
                 } else {
-                    decf[q] = (int)(word >> 8);
-                    decs[q] = (int)(word & 0xFFu);
+                    T.decf[q] = (int)(word >> 8);
+                    T.decs[q] = (int)(word & 0xFFu);
                 }
             }
-            for (int q = tid; q <= nn; q += FUSED_NT) segP[q] = segC[q];
+            for (int q = tid; q <= nn; q += FUSED_NT) T.segP[q] = T.segC[q];
             __syncthreads();
         }
         // ---- leaves (every block, from its first feature's final order)
         {
             const int f = blockIdx.x;
-            if (!resident)
+            if (!resident) {
                 for (int j = tid; j < N; j += FUSED_NT) {
                     ord[j] = A.gord[(int64_t)f * N + j];
                     nat[j] = A.gnode[(int64_t)f * N + j];
                 }
-            unsigned long long *lsum = (unsigned long long *)Pg;
+            }
             for (int l = tid; l < 2 * n_leaf; l += FUSED_NT) lsum[l] = 0ull;
             __syncthreads();
             for (int j = tid; j < N; j += FUSED_NT) {
-                const int i = ord[j], q = nat[j], sf = decf[q];
-                const int right = (sf >= 0 && (int)A.bins[(int64_t)sf * N + i] >= decs[q]) ? 1 : 0;
+                const int i = ord[j], q = nat[j], sf = T.decf[q];
+                const int right = (sf >= 0 && (int)A.bins[(int64_t)sf * N + i] >= T.decs[q]) ? 1 : 0;
                 const int l = 2 * q + right;
                 leafof[i] = (uint8_t)l;
                 smem_add_u64(&lsum[2 * l], (unsigned long long)sg[i]);
@@ -1316,35 +1344,16 @@ __global__ void __launch_bounds__(FUSED_NT, 4) fused_forest_kernel(FusedArgs A)
             for (int l = tid; l < n_leaf; l += FUSED_NT) {
                 const double Gd = (double)(long long)lsum[2 * l] * FX, Hd = (double)(long long)lsum[2 * l + 1] * FX;
                 const float v = (float)(-(A.eta * (Gd / (Hd + A.lam))));
-                lval[l] = v;
+                T.lval[l] = v;
                 if (blockIdx.x == 0) A.t_leaf[(size_t)t * n_leaf + l] = v;
             }
             __syncthreads();
         }
-        FT_MARK(6);
     }
     // the last tree's prediction update
-    const int T = A.n_trees;
+    const int TT = A.n_trees;
     for (int i = blockIdx.x * FUSED_NT + tid; i < N; i += G * FUSED_NT)
-        A.pred[T & 1][i] = __fadd_rn(__ldcg(A.pred[(T - 1) & 1] + i), lval[leafof[i]]);
-#ifdef AT_FIT_TIMING
-    if (threadIdx.x == 0) {
-        const unsigned long long wk = ft[7] + ft[2] + ft[3] + ft[8] + ft[4];
-        atomicMin(&g_ft_work_min, wk);
-        atomicMax(&g_ft_work_max, wk);
-        unsigned smid;
-        asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        if (blockIdx.x < 1024) g_ft_smid[blockIdx.x] = smid;
-        __threadfence();
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0)
-        printf("per-block level work per tree: min %llu max %llu ns\n", g_ft_work_min / A.n_trees, g_ft_work_max / A.n_trees);
-    if (blockIdx.x == 0 && threadIdx.x == 0)
-        printf("fused forest (block 0, ns per tree, G=%d resident=%d): grads %llu barrier0 %llu | per-tree sums over levels: "
-               "load %llu partition %llu scan %llu cand %llu (cas %llu) barrier %llu decide+leaves %llu\n", G, (int)resident,
-               ft[0] / A.n_trees, ft[1] / A.n_trees, ft[7] / A.n_trees, ft[2] / A.n_trees, ft[3] / A.n_trees,
-               ft[8] / A.n_trees, ft[4] / A.n_trees, ft[5] / A.n_trees, ft[6] / A.n_trees);
-#endif
+        A.pred[TT & 1][i] = __fadd_rn(__ldcg(A.pred[(TT - 1) & 1] + i), T.lval[leafof[i]]);
 }
 
 __global__ void klist_kernel(const uint16_t *__restrict__ key, const int32_t *__restrict__ rank,
@@ -1489,16 +1498,22 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     const int fused_env = fused_e ? atoi(fused_e) : 1;
     if (fused_env && !o->allreduce && !o->d_hist0_out && n <= FUSED_NMAX) {
         const size_t fsm = fused_smem_bytes((int)n, GS);
+        const int fep = fused_ep((int)n);
+        const void *fk = fep == 1   ? (const void *)fused_forest_kernel<1>
+                         : fep == 2 ? (const void *)fused_forest_kernel<2>
+                         : fep == 4 ? (const void *)fused_forest_kernel<4>
+                                    : (const void *)fused_forest_kernel<8>;
         int dev = 0, nsm = 0, coop = 0, per = 0;
         AT_CUDA_TRY(cudaGetDevice(&dev));
         AT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         AT_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-        static size_t fused_attr = 0;
-        if (fused_attr < fsm) {
-            AT_CUDA_TRY(cudaFuncSetAttribute(fused_forest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-            fused_attr = fsm;
+        static size_t fused_attr[4] = {0, 0, 0, 0};
+        const int fslot = fep == 1 ? 0 : fep == 2 ? 1 : fep == 4 ? 2 : 3;
+        if (fused_attr[fslot] < fsm) {
+            AT_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+            fused_attr[fslot] = fsm;
         }
-        AT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fused_forest_kernel, FUSED_NT, fsm));
+        AT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fk, FUSED_NT, fsm));
         if (coop && per > 0) {
             const int G = (int)std::min<int64_t>(F, (int64_t)per * nsm);
             const bool resident = F <= G;
@@ -1531,7 +1546,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             void *args[] = {&fa};
             {
                 ProfScope ps(AT_K_FIT_GRAPH, s);
-                AT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)fused_forest_kernel, dim3(G), dim3(FUSED_NT), args,
+                AT_CUDA_TRY(cudaLaunchCooperativeKernel(fk, dim3(G), dim3(FUSED_NT), args,
                                                         fsm, s));
                 note_launch();
             }
