@@ -818,6 +818,7 @@ struct FusedTail {
     unsigned decw[128];                             // published decision words
     float lval[256];                                // leaf values of the current tree
     int32_t wsi[2][FUSED_NT / 32];                  // scan scratch
+    int32_t gpre[FIT_MAXKEYS + 1];                  // group prefix per workload (copy)
     long long wsl[2][2 * (FUSED_NT / 32)];
     uint8_t dead[512];
 };
@@ -917,9 +918,25 @@ __device__ __forceinline__ void blk_excl_i64x2(long long a, long long b, int lan
 //   prefix sums of (g, h) in the new order -> node bases / totals -> every run end's fp64 gain;
 //   per-node max by native 32-bit shared atomics (gain high word, low word, then the lowest s among
 //   equal gains), one 128-bit global atomic max per node on (gain, 0xFFFF - f, 0xFFFF - s).
+#ifdef AT_FIT_TIMING
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ unsigned long long g_ft_work_max = 0ull, g_ft_grad_max = 0ull;
+#define FT_MARK(k) do { if (threadIdx.x == 0) { unsigned long long _t = gtimer(); ft[k] += _t - ft_last; ft_last = _t; } } while (0)
+#else
+#define FT_MARK(k) do {} while (0)
+#endif
+
 template <int EP>
 __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel(FusedArgs A)
 {
+#ifdef AT_FIT_TIMING
+    unsigned long long ft[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer();
+#endif
     extern __shared__ __align__(16) unsigned char fsm[];
     const int N = A.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = FUSED_NT / 32;
@@ -940,32 +957,32 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
     const int CM = A.GS / 8 > 8 ? A.GS / 8 : 8;
     const int chunks = (A.GS + CM - 1) / CM;
     for (int q = tid; q < 128; q += FUSED_NT) { T.nbh[q] = 0; T.nbl[q] = 0; T.nms[q] = 0xFFFFFFFFu; }
+    for (int q = tid; q <= FIT_MAXKEYS; q += FUSED_NT) T.gpre[q] = A.gpre[q];
 
-    // Grid-wide sync.  Every block arrives on one counter (fire-and-forget add after a fence);
-    // block 0 alone polls it, reduces the level's sub-slots into the decisions (nn > 0), writes the
-    // tree nodes, re-zeroes the sub-slots (node ids are unique within a tree; later fences order
-    // the zeroing before the next tree's atomics) and publishes FUSED_NREP replicas of
-    // (epoch << 32 | decision) -- every block polls its own replica, so no L2 line is polled or
-    // read by all blocks, and the decisions arrive with the release.  T.decw[q] gets the decisions.
+    // Grid-wide sync.  Every block arrives on one counter (fence, then an atomic add that returns
+    // the count); the LAST block to arrive reduces the level's sub-slots into the decisions (nn > 0),
+    // re-zeroes them (node ids are unique within a tree; later fences order the zeroing before the
+    // next tree's atomics) and publishes FUSED_NREP replicas of (epoch << 32 | decision); the tree
+    // nodes (feature, threshold) are written after the release.  In every block, thread q polls
+    // entry q of the block's replica (each entry carries its epoch), so the decisions arrive with
+    // the release and no L2 line is polled by all blocks.  T.decw[q] gets the decisions.
     auto sync_all = [&](int t, int nn, int first) {
         __syncthreads();
         ++epoch;
         if (tid == 0) {
             __threadfence();
-            atomicAdd(A.bar, 1u);
+            const unsigned old = atomicAdd(A.bar, 1u);
+            T.wsi[1][0] = old == epoch * (unsigned)G - 1u ? 1 : 0;
         }
+        __syncthreads();
         const int nq = nn > 0 ? nn : 1;
-        if (blockIdx.x == 0) {
-            if (tid == 0) {
-                while (*(volatile unsigned *)A.bar < epoch * (unsigned)G) __nanosleep(20);
-                __threadfence();
-            }
-            __syncthreads();
+        if (T.wsi[1][0]) {   // block-uniform: the last arriver
+            __threadfence();
             for (int q = tid; q < nq; q += FUSED_NT) {
                 unsigned word = 0xFFFFFFFFu;
+                unsigned long long lo = 0, hi = 0;
                 if (nn > 0) {
                     const int nd = first + q;
-                    unsigned long long lo = 0, hi = 0;
 #pragma unroll
                     for (int k = 0; k < FUSED_NSUB; ++k) {
                         ulonglong2 *sp2 = (ulonglong2 *)(A.slot + 2 * (nd * FUSED_NSUB + k));
@@ -973,36 +990,28 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
                         __stcg(sp2, make_ulonglong2(0ull, 0ull));
                         if (v.y > hi || (v.y == hi && v.x > lo)) { lo = v.x; hi = v.y; }
                     }
-                    if (hi == 0) {
-                        A.t_feat[(size_t)t * n_int + nd] = 0;
-                        A.t_thr[(size_t)t * n_int + nd] = __int_as_float(0x7f800000);
-                    } else {
-                        const unsigned bf = 0xFFFFu - (unsigned)((lo >> 16) & 0xFFFFu);
-                        const unsigned bs = 0xFFFFu - (unsigned)(lo & 0xFFFFu);
-                        word = (bf << 8) | bs;
-                        A.t_feat[(size_t)t * n_int + nd] = (uint16_t)bf;
-                        A.t_thr[(size_t)t * n_int + nd] = A.cuts[(int64_t)bf * (A.B - 1) + bs - 1];
-                    }
+                    if (hi != 0)
+                        word = ((0xFFFFu - (unsigned)((lo >> 16) & 0xFFFFu)) << 8) | (0xFFFFu - (unsigned)(lo & 0xFFFFu));
                 }
                 const unsigned long long pub = ((unsigned long long)epoch << 32) | word;
 #pragma unroll
                 for (int r = 0; r < FUSED_NREP; ++r) __stcg(A.dec + r * 128 + q, pub);
+                if (nn > 0) {   // the tree's nodes, off the release path
+                    const int nd = first + q;
+                    const unsigned bf = word >> 8, bs = word & 0xFFu;
+                    A.t_feat[(size_t)t * n_int + nd] = word == 0xFFFFFFFFu ? (uint16_t)0 : (uint16_t)bf;
+                    A.t_thr[(size_t)t * n_int + nd] = word == 0xFFFFFFFFu ? __int_as_float(0x7f800000)
+                                                                           : A.cuts[(int64_t)bf * (A.B - 1) + bs - 1];
+                }
             }
         }
-        // one thread polls entry 0 of the block's replica; the others then read theirs (each entry
-        // carries its epoch, so a rare not-yet-visible one is re-read)
         const volatile unsigned long long *rep = A.dec + (blockIdx.x % FUSED_NREP) * 128;
-        if (tid == 0) {
-            unsigned long long v = rep[0];
-            while ((unsigned)(v >> 32) != epoch) {
-                __nanosleep(64);
-                v = rep[0];
-            }
-        }
-        __syncthreads();
         for (int q = tid; q < nq; q += FUSED_NT) {
             unsigned long long v = rep[q];
-            while ((unsigned)(v >> 32) != epoch) v = rep[q];
+            while ((unsigned)(v >> 32) != epoch) {
+                __nanosleep(32);
+                v = rep[q];
+            }
             T.decw[q] = (unsigned)v;
         }
         __syncthreads();
@@ -1047,7 +1056,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
                 int lo = 0, hi = FIT_MAXKEYS;   // largest w with gpre[w] <= grp
                 while (hi - lo > 1) {
                     const int mid = (lo + hi) >> 1;
-                    if (A.gpre[mid] <= grp) lo = mid; else hi = mid;
+                    if (T.gpre[mid] <= grp) lo = mid; else hi = mid;
                 }
                 T.wsi[0][0] = lo;
             }
@@ -1055,7 +1064,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
             const int w = T.wsi[0][0];
             __syncthreads();   // rewritten by the next item
             const int nw = A.counts[w];
-            const int start = (grp - A.gpre[w]) * A.GS;
+            const int start = (grp - T.gpre[w]) * A.GS;
             const int m = min(A.GS, nw - start);
             const int a1 = min(m, a0 + CM);
             if (a0 >= m) continue;   // block-uniform
@@ -1095,7 +1104,9 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
             }
             __syncthreads();
         }
+        FT_MARK(0);
         sync_all(t, 0, 0);
+        FT_MARK(1);
 
         for (int i = tid; i < N; i += FUSED_NT) { sg[i] = __ldcg(A.g + i); sh[i] = __ldcg(A.h + i); }
         for (int q = tid; q < 512; q += FUSED_NT) T.dead[q] = 0;
@@ -1303,7 +1314,9 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
                     }
                 __syncthreads();
             }
+            FT_MARK(2);
             sync_all(t, nn, first);
+            FT_MARK(3);
             // the level's decisions (identical in every block; a dead node never has a split)
             for (int q = tid; q < nn; q += FUSED_NT) {
                 const int nd = first + q;
@@ -1350,6 +1363,19 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
             __syncthreads();
         }
     }
+#ifdef AT_FIT_TIMING
+    FT_MARK(4);
+    if (threadIdx.x == 0) {
+        atomicMax(&g_ft_work_max, ft[2]);
+        atomicMax(&g_ft_grad_max, ft[0]);
+        __threadfence();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("fused forest ns/tree (block 0, G=%d): grads %llu gsync %llu | levels: work %llu sync %llu | "
+               "decide+leaves %llu | max over blocks: grads %llu work %llu (from earlier-finishing blocks)\n", G,
+               ft[0] / A.n_trees, ft[1] / A.n_trees, ft[2] / A.n_trees, ft[3] / A.n_trees, ft[4] / A.n_trees,
+               g_ft_grad_max / A.n_trees, g_ft_work_max / A.n_trees);
+#endif
     // the last tree's prediction update
     const int TT = A.n_trees;
     for (int i = blockIdx.x * FUSED_NT + tid; i < N; i += G * FUSED_NT)
