@@ -414,6 +414,141 @@ __device__ __forceinline__ void sa_row(const WlDev &W, const SaLowering &L, int 
     }
 }
 
+// sa_kernel's fused row item: the extents of every loop straight from the knob vector (one
+// factor-table load per loop, no shared lowering phase), then row k exactly as sa_row, and the
+// row's relation contributions deposited at once: row k qualifies for threshold 2^t iff
+// T_k < 2^t, i.e. iff t >= bitlen(T_k), so it raises slot max(1, bitlen(T_k)) of R[b][p] to its
+// Z (shared atomic max on the fp32 bits: every Z is > 0, and the slots start at +0); a prefix
+// max over t (relation_prefix) then gives R_t = max_{k : T_k < 2^t} Z_k, 0 for an empty set.
+template <int TMPL>
+__device__ __forceinline__ void sa_row_rel(const WlDev &W, const uint16_t *__restrict__ fact, const uint32_t *ch,
+                                           int k, int lane, float *tile)
+{
+    constexpr int NL = Tmpl<TMPL>::NL;
+    constexpr int NA = Tmpl<TMPL>::NA;
+    if (k >= NL) return;
+    const uint32_t p = TMPL == 1 ? ch[6] : TMPL == 2 ? ch[5] : 0u;
+    uint32_t ev[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        int axis, level;
+        loop_axis_level<TMPL>(l, p, axis, level);
+        const int Lv = TMPL == 0 ? (axis == 2 ? 2 : 3) : (axis < 3 ? 4 : 2);
+        uint32_t cha = 0;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) if (q == axis) cha = ch[q];
+        ev[l] = __ldg(fact + W.fact_off[axis] + cha * (uint32_t)Lv + level);
+    }
+    const uint32_t unroll_max = W.unroll_vals[TMPL == 0 ? ch[3] : TMPL == 1 ? ch[7] : ch[6]];
+    const uint32_t vec = TMPL == 0 ? 0u : TMPL == 1 ? ch[8] : ch[7];
+    uint32_t A[NA];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) A[q] = 1;
+    uint32_t bu = 1, td = 1;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        const uint32_t m = l > k ? ev[l] : 1u;
+        if (TMPL == 1 && l >= 9 && l < 12) {
+            const uint32_t al = perm3(p, l - 9);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) A[3 + q] = al == (uint32_t)q ? A[3 + q] * m : A[3 + q];
+        } else if (TMPL == 2 && l >= 13 && l < 16) {
+            const uint32_t al = perm3(p, l - 13);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) A[q] = al == (uint32_t)q ? A[q] * m : A[q];
+        } else {
+            int al, lv;
+            loop_axis_level<TMPL>(l, p, al, lv);
+            A[al] *= m;
+        }
+        bu *= m;
+        td = l < k ? td * ev[l] : td;
+    }
+    uint32_t ek = 0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) if (l == k) ek = ev[l];
+    int a, level;
+    loop_axis_level<TMPL>(k, p, a, level);
+    uint32_t coef = 1;
+#pragma unroll
+    for (int q = 0; q < NA; ++q) if (a == q) coef = A[q];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) if (a == q) A[q] *= ek;
+    bu *= ek;
+    const uint32_t S = W.S;
+    uint32_t T[3], st[3];
+    if (TMPL == 0) {
+        T[0] = A[0] * A[1];
+        T[1] = A[2] * A[0];
+        T[2] = A[2] * A[1];
+        st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : 0u;
+        st[1] = (a == 2) ? coef * W.str_in[0] : (a == 0) ? coef * W.str_in[1] : 0u;
+        st[2] = (a == 2) ? coef * W.str_ker[0] : (a == 1) ? coef * W.str_ker[1] : 0u;
+    } else if (TMPL == 1) {
+        T[0] = A[0] * A[1] * A[2];
+        T[1] = A[3] * comp_touch(A[1], A[4], S) * comp_touch(A[2], A[5], S);
+        T[2] = A[0] * A[3] * A[4] * A[5];
+        st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : (a == 2) ? coef * W.str_out[2] : 0u;
+        st[1] = (a == 3) ? coef * W.str_in[0] : (a == 1) ? coef * S * W.str_in[1] : (a == 4) ? coef * W.str_in[1]
+              : (a == 2) ? coef * S * W.str_in[2] : (a == 5) ? coef * W.str_in[2] : 0u;
+        st[2] = (a == 0) ? coef * W.str_ker[0] : (a == 3) ? coef * W.str_ker[1] : (a == 4) ? coef * W.str_ker[2]
+              : (a == 5) ? coef * W.str_ker[3] : 0u;
+    } else {
+        T[0] = A[0] * A[1] * A[2];
+        T[1] = A[0] * comp_touch(A[1], A[3], S) * comp_touch(A[2], A[4], S);
+        T[2] = A[0] * A[3] * A[4];
+        st[0] = (a == 0) ? coef * W.str_out[0] : (a == 1) ? coef * W.str_out[1] : (a == 2) ? coef * W.str_out[2] : 0u;
+        st[1] = (a == 0) ? coef * W.str_in[0] : (a == 1) ? coef * S * W.str_in[1] : (a == 3) ? coef * W.str_in[1]
+              : (a == 2) ? coef * S * W.str_in[2] : (a == 4) ? coef * W.str_in[2] : 0u;
+        st[2] = (a == 0) ? coef * W.str_ker[0] : (a == 3) ? coef * W.str_ker[1] : (a == 4) ? coef * W.str_ker[2] : 0u;
+    }
+    int ann;
+    if (TMPL != 0 && k < 9) {
+        ann = 4 + level;
+    } else {
+        ann = (bu <= unroll_max) ? 1 : 0;
+        if (k == NL - 1 && vec) ann = 2;
+    }
+    float *col = tile + lane;   // feature f at col[f * 32]
+    const float fbu = __uint2float_rn(bu), ftd = __uint2float_rn(td);
+    const int base = 19 * k;
+    col[(base + 0) * 32] = __uint2float_rn(ek);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) col[(base + 1 + q) * 32] = ann == q ? 1.0f : 0.0f;
+    col[(base + 8) * 32] = ftd;
+    col[(base + 9) * 32] = fbu;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        const float reuse = __fdiv_rn(fbu, __uint2float_rn(T[b]));
+        col[(base + 10 + 3 * b) * 32] = __uint2float_rn(T[b]);
+        col[(base + 11 + 3 * b) * 32] = reuse;
+        col[(base + 12 + 3 * b) * 32] = __uint2float_rn(st[b]);
+        const int e = 32 - __clz((int)T[b]);   // bitlen(T) >= 1
+        if (e <= 20) {
+            unsigned *R = (unsigned *)(col + (342 + 40 * b + (e - 1)) * 32);
+            atomicMax(R, __float_as_uint(reuse));
+            atomicMax(R + 20 * 32, __float_as_uint(ftd));
+        }
+    }
+    if (k == 0) {
+        col[462 * 32] = fbu;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) col[(463 + b) * 32] = __uint2float_rn(T[b]);
+    }
+}
+
+// prefix max over t of the deposited relation slots R[b][p][t] (sa_row_rel)
+__device__ __forceinline__ void relation_prefix(float *tile, int lane, int b, int p)
+{
+    float *R = tile + (342 + 40 * b + 20 * p) * 32 + lane;
+    float m = 0.0f;
+#pragma unroll
+    for (int t = 0; t < 20; ++t) {
+        m = fmaxf(m, R[t * 32]);
+        R[t * 32] = m;
+    }
+}
+
 // Relation features of buffer b, pair p (0: reuse, 1: top-down) from context rows already in a
 // smem tile [f][32] (rows-only pass).  Row k qualifies for threshold 2^t iff T_k < 2^t, i.e. iff
 // t >= bitlen(T_k) (T_k >= 1), so R_t = max(0, max_{k : bitlen(T_k) <= t} Z_k): each row deposits

@@ -85,29 +85,25 @@ struct SaSmem {
     float part[GRP][32 * 32];
     uint32_t ch[GRP][MAXKNOBS][32];
     int32_t w[GRP][32];
-    SaLowering low[GRP];
     uint64_t bar[2];
 };
 
-__device__ __forceinline__ void sa_lower_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, int k, int lane,
-                                             SaLowering &L)
+__device__ __forceinline__ void sa_row_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, int k, int lane,
+                                           float *tile)
 {
     switch (W.tmpl) {
-    case 0: sa_lower_loop<0>(W, fact, ch, k, lane, L); break;
-    case 1: sa_lower_loop<1>(W, fact, ch, k, lane, L); break;
-    default: sa_lower_loop<2>(W, fact, ch, k, lane, L); break;
+    case 0: sa_row_rel<0>(W, fact, ch, k, lane, tile); break;
+    case 1: sa_row_rel<1>(W, fact, ch, k, lane, tile); break;
+    default: sa_row_rel<2>(W, fact, ch, k, lane, tile); break;
     }
 }
 
-__device__ __forceinline__ void sa_row_any(const WlDev &W, const SaLowering &L, const uint32_t *ch, int k, int lane,
-                                           float *tile)
+// relation slots of every group back to +0 (before the next rows deposit into them); warps
+// g >= GRP only, which are idle while the owner warps propose / decide
+template <int GRP>
+__device__ __forceinline__ void zero_relation(float (*tile)[NFEAT * 32], int lane, int warp)
 {
-    TileSink sk{tile, lane};
-    switch (W.tmpl) {
-    case 0: sa_row<0>(W, L, k, lane, 0u, sk); break;
-    case 1: sa_row<1>(W, L, k, lane, ch[6], sk); break;
-    default: sa_row<2>(W, L, k, lane, ch[5], sk); break;
-    }
+    for (int r = warp - GRP; r < GRP * 120; r += SA_NW - GRP) tile[r / 120][(342 + r % 120) * 32 + lane] = 0.0f;
 }
 
 // Block = GRP groups of 32 chains (lane = chain) x SA_NW warps.  Warp g owns group g's chain
@@ -155,6 +151,8 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         for (int j = 0; j < MAXKNOBS; ++j) sm.ch[og][j][lane] = ch[j];
         sm.w[og][lane] = w;
         zero_cols_any(W.tmpl, sm.tile[og], lane);
+    } else {
+        zero_relation<GRP>(sm.tile, lane, warp);
     }
     __syncthreads();
     uint32_t ph[2] = {0u, 0u};
@@ -167,31 +165,22 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #endif
     // every warp computes its share of the features of all chains of the block
     auto features_phase = [&]() {
-        // L) loop extents: items (group, loop)
+        // R) context rows and their relation deposits: items (group, row)
         for (int it = warp; it < GRP * MAXLOOPS; it += SA_NW) {
             const int g = it / MAXLOOPS, k = it - g * MAXLOOPS;
             uint32_t chl[MAXKNOBS];
 #pragma unroll
             for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[g][j][lane];
-            sa_lower_any(P.S->w[sm.w[g][lane]], P.fact, chl, k, lane, sm.low[g]);
-        }
-        __syncthreads();
-        // R) context rows: items (group, row)
-        for (int it = warp; it < GRP * MAXLOOPS; it += SA_NW) {
-            const int g = it / MAXLOOPS, k = it - g * MAXLOOPS;
-            uint32_t chl[MAXKNOBS];
-#pragma unroll
-            for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[g][j][lane];
-            sa_row_any(P.S->w[sm.w[g][lane]], sm.low[g], chl, k, lane, sm.tile[g]);
+            sa_row_any(P.S->w[sm.w[g][lane]], P.fact, chl, k, lane, sm.tile[g]);
         }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
         t_rows += clock64() - t0;
 #endif
-        // T) relation features: items (group, buffer, pair)
+        // T) prefix max of the relation slots: items (group, buffer, pair)
         for (int it = warp; it < GRP * 6; it += SA_NW) {
             const int g = it / 6, r = it - g * 6;
-            relation_from_tile(sm.tile[g], lane, n_loops(P.S->w[sm.w[g][lane]].tmpl), r >> 1, r & 1);
+            relation_prefix(sm.tile[g], lane, r >> 1, r & 1);
         }
         __syncthreads();
     };
@@ -199,6 +188,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     ts_wait_resident(G, sm.bar);
     walk_pass<SA_NW, GRP>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp, &sm.part[0][0],
                           nullptr, 0, 0, no_slots);
+    if (!owner) zero_relation<GRP>(sm.tile, lane, warp);
     if (owner) {
         E = gbt_combine(sm.part[og], lane, P.base);
         if (live) {
@@ -247,6 +237,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_walk += t - t0; t0 = t; }
 #endif
+        if (!owner) zero_relation<GRP>(sm.tile, lane, warp);
         if (owner) {
             const float E2 = gbt_combine(sm.part[og], lane, P.base);
             const float d = __fsub_rn(E2, E);
