@@ -214,11 +214,27 @@ typedef struct {
     void *ctx;
     float *d_pred_out;
     int64_t *d_hist0_out;
+    int32_t objective;            /* AT_OBJ_RANK (Eq. 2) or AT_OBJ_REG: sum_i (f_i - c_i)^2,
+                                     g_i = 2 (f_i - c_i), h_i = 2 in 2^-32 fixed point; valid while
+                                     sum_i |f_i - c_i| < 2^30 */
+    const float *d_base_margin;   /* nullable [n]: initial predictions f_i (else 0); transfer
+                                     learning fits f_local on top of f_global (Eq. 4) */
 } at_fit_opts;
+enum { AT_OBJ_RANK = 0, AT_OBJ_REG = 1 };
 
 AT_API int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t n_features,
                  const float *d_cost, const uint16_t *d_group_key,
                  int64_t hist_begin, int64_t hist_end, const at_fit_opts *o, at_gbt *out, void *stream);
+
+/* gbt_concat -- transfer learning, Eq. 4: f(x) = f_global(x) + f_local(x) as ONE
+ * ensemble (a's trees, then b's), so gbt_predict / sa_explore score it unchanged.  A tree
+ * shallower than max(depth) is padded with pass-through nodes (feature 0, threshold +inf:
+ * always left), its leaves moved to the leftmost descendant slots (slot s -> s << (D - d)),
+ * which leaves every tree's value unchanged; base = a.base + b.base (fp32).  The sum is taken
+ * in the canonical order of the combined ensemble (Q19), i.e. equal to f_a(x) + f_b(x) up to
+ * fp32 rounding.  Host-side construction like gbt_create; *out is a new handle.  Errors:
+ * AT_EMISMATCH (different n_features). */
+AT_API int gbt_concat(at_gbt a, at_gbt b, at_gbt *out);
 
 /* ------------------------------------------------------------------ instrumentation
  * at_launch_count: kernels this library launched since load (bench "gpu_launches").

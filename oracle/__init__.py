@@ -72,7 +72,8 @@ class Gbt(C.Structure):
 class FitOpts(C.Structure):
     _fields_ = [("n_trees", C.c_int32), ("depth", C.c_int32), ("max_bins", C.c_int32),
                 ("group_size", C.c_int32), ("eta", C.c_float), ("lambda_", C.c_float),
-                ("min_child_weight", C.c_float), ("seed", C.c_uint64)]
+                ("min_child_weight", C.c_float), ("seed", C.c_uint64), ("objective", C.c_int32),
+                ("base_margin", C.POINTER(C.c_float))]
 
 
 _lib = None
@@ -260,6 +261,30 @@ class OracleGbt:
         return (score, sl) if slots else score
 
 
+def gbt_concat(a, b):
+    """Eq. 4: the global model's trees then the local model's, as one OracleGbt."""
+    D = max(a.depth, b.depth)
+    T = a.n_trees + b.n_trees
+    feat = np.zeros((T, (1 << D) - 1), np.uint16)
+    thr = np.zeros((T, (1 << D) - 1), np.float32)
+    leaf = np.zeros((T, 1 << D), np.float32)
+    base = C.c_float()
+    ga, gb = a.c(), b.c()
+    lib().or_gbt_concat(C.byref(ga), C.byref(gb), _p(feat, C.c_uint16), _p(thr, C.c_float), _p(leaf, C.c_float),
+                        C.byref(base))
+    return OracleGbt(feat, thr, leaf, base.value)
+
+
+def reg_gradients(cost, pred):
+    cost = np.ascontiguousarray(cost, dtype=np.float32)
+    pred = np.ascontiguousarray(pred, dtype=np.float32)
+    n = cost.shape[0]
+    g = np.zeros(n, np.int64)
+    h = np.zeros(n, np.int64)
+    lib().or_reg_gradients(_p(cost, C.c_float), _p(pred, C.c_float), C.c_int64(n), _p(g, C.c_int64), _p(h, C.c_int64))
+    return g, h
+
+
 def philox(ctr, key):
     c = (C.c_uint32 * 4)(*ctr)
     k = (C.c_uint32 * 2)(*key)
@@ -322,12 +347,16 @@ def rank_loss(cost, pred):
 
 
 def fit_hist(X, cost, gkey, n_trees=100, depth=6, max_bins=256, group_size=64, eta=0.1, lam=1.0,
-             min_child_weight=1.0, seed=1805, want_hist0=False):
+             min_child_weight=1.0, seed=1805, want_hist0=False, objective="rank", base_margin=None):
+    """objective "rank" (Eq. 2, P:176-179) or "reg" (sum (f - c)^2, P:175); base_margin [n]:
+    initial predictions (transfer learning, Eq. 4)."""
     X = np.ascontiguousarray(X, dtype=np.float32)
     n, F = X.shape
     cost = np.ascontiguousarray(cost, dtype=np.float32)
     gk = np.ascontiguousarray(gkey, dtype=np.uint16)
-    o = FitOpts(n_trees, depth, max_bins, group_size, eta, lam, min_child_weight, seed)
+    bm = None if base_margin is None else np.ascontiguousarray(base_margin, dtype=np.float32)
+    o = FitOpts(n_trees, depth, max_bins, group_size, eta, lam, min_child_weight, seed,
+                {"rank": 0, "reg": 1}[objective], None if bm is None else _p(bm, C.c_float))
     ni, nl = (1 << depth) - 1, 1 << depth
     feat = np.zeros((n_trees, ni), np.uint16)
     thr = np.zeros((n_trees, ni), np.float32)

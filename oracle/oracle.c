@@ -872,6 +872,18 @@ int or_pair_gradients(const float *cost, const float *pred, const uint16_t *gkey
     return 0;
 }
 
+/* Regression loss of P:175, sum_i (f_i - c_i)^2 taken literally: dl/df_i = 2 (f_i - c_i),
+ * d2l/df_i^2 = 2, in the same 2^-32 fixed point as the rank-loss terms. */
+int or_reg_gradients(const float *cost, const float *pred, int64_t n, int64_t *g, int64_t *h)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        double r = (double)pred[i] - (double)cost[i];
+        g[i] = llrint(2.0 * r * 4294967296.0);
+        h[i] = 2 * (int64_t)4294967296LL;
+    }
+    return 0;
+}
+
 double or_rank_loss(const float *cost, const float *pred, int64_t n)
 {
     double L = 0.0;
@@ -901,7 +913,9 @@ int or_fit_hist(const float *X, int64_t n, int F, const float *cost, const uint1
         for (int f = 0; f < F; ++f)
             bins[(size_t)i * F + f] = bin_of(cuts + (size_t)f * (B - 1), ncuts[f], X[(size_t)i * F + f]);
     float *pred = (float *)malloc(sizeof(float) * (size_t)n);
-    for (int64_t i = 0; i < n; ++i) pred[i] = 0.0f;   /* base score 0 (Q35) */
+    /* base score 0 (Q35), or the caller's margin: f = f_global + f_local fits f_local on top of
+     * f_global's predictions (Eq. 4) */
+    for (int64_t i = 0; i < n; ++i) pred[i] = o->base_margin ? o->base_margin[i] : 0.0f;
     int64_t *g = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
     int64_t *h = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
     int64_t *node = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
@@ -915,7 +929,8 @@ int or_fit_hist(const float *X, int64_t n, int F, const float *cost, const uint1
     char *dead = (char *)malloc((size_t)(n_int + n_leaf));
 
     for (int t = 0; t < o->n_trees; ++t) {
-        or_pair_gradients(cost, pred, gkey, n, o->seed, t, o->group_size, g, h);
+        if (o->objective == 1) or_reg_gradients(cost, pred, n, g, h);
+        else or_pair_gradients(cost, pred, gkey, n, o->seed, t, o->group_size, g, h);
         for (int64_t i = 0; i < n; ++i) node[i] = 0;
         memset(dead, 0, (size_t)(n_int + n_leaf));
         uint16_t *tf = feat + (size_t)t * n_int;
@@ -986,5 +1001,36 @@ int or_fit_hist(const float *X, int64_t n, int F, const float *cost, const uint1
     if (pred_out) memcpy(pred_out, pred, sizeof(float) * (size_t)n);
     free(cuts); free(ncuts); free(bins); free(pred); free(g); free(h); free(node);
     free(hg); free(hh); free(dead); free(Gn); free(Hn); free(bf); free(bs); free(bg);
+    return 0;
+}
+
+/* ======================================================================
+ * Transfer learning, Eq. 4: one ensemble holding the global model's trees, then
+ * the local model's; a shallower tree is padded to the common depth with pass-through nodes.
+ * ==================================================================== */
+static void copy_padded(const or_gbt *m, int t, int D, uint16_t *feat, float *thresh, float *leaf)
+{
+    const int64_t ni = ((int64_t)1 << m->depth) - 1, nl = (int64_t)1 << m->depth;
+    const int64_t NI = ((int64_t)1 << D) - 1, NL = (int64_t)1 << D;
+    for (int64_t k = 0; k < NI; ++k) { feat[k] = 0; thresh[k] = INFINITY; }
+    for (int64_t l = 0; l < NL; ++l) leaf[l] = 0.0f;
+    /* heap node k of depth d keeps index k: the top levels coincide */
+    for (int64_t k = 0; k < ni; ++k) { feat[k] = m->feat[(size_t)t * ni + k]; thresh[k] = m->thresh[(size_t)t * ni + k]; }
+    /* old leaf slot s is heap node ni + s; below it every node goes left, so it ends at the
+     * leftmost descendant (ni + s + 1) * 2^(D - d) - 1, i.e. slot s << (D - d) */
+    for (int64_t s = 0; s < nl; ++s) leaf[s << (D - m->depth)] = m->leaf[(size_t)t * nl + s];
+}
+
+int or_gbt_concat(const or_gbt *a, const or_gbt *b, uint16_t *feat, float *thresh, float *leaf, float *base)
+{
+    const int D = a->depth > b->depth ? a->depth : b->depth;
+    const int64_t NI = ((int64_t)1 << D) - 1, NL = (int64_t)1 << D;
+    for (int t = 0; t < a->n_trees; ++t)
+        copy_padded(a, t, D, feat + (size_t)t * NI, thresh + (size_t)t * NI, leaf + (size_t)t * NL);
+    for (int t = 0; t < b->n_trees; ++t) {
+        const size_t u = (size_t)(a->n_trees + t);
+        copy_padded(b, t, D, feat + u * NI, thresh + u * NI, leaf + u * NL);
+    }
+    *base = a->base + b->base;
     return 0;
 }

@@ -142,6 +142,8 @@ typedef struct {
     int32_t n_trees, depth, max_bins, group_size;
     float eta, lambda, min_child_weight;
     uint64_t seed;
+    int32_t objective;          /* 0: rank loss, Eq. 2; 1: regression loss sum (f - c)^2 */
+    const float *base_margin;   /* [n] initial predictions (transfer learning, Eq. 4); NULL -> 0 */
 } or_fit_opts;
 
 int or_fit_cuts(const float *X /* [n][F] */, int64_t n, int F, int max_bins,
@@ -155,6 +157,15 @@ int or_fit_hist(const float *X /* [n][F] */, int64_t n, int F, const float *cost
                 float *pred_out /* [n] final fit predictions, nullable */,
                 int64_t *hist0_out /* tree-0 root histogram [F][max_bins][2], nullable */);
 double or_rank_loss(const float *cost, const float *pred, int64_t n);   /* Eq. 2 over all ordered pairs */
+/* regression loss sum_i (f_i - c_i)^2: g_i = 2 (f_i - c_i), h_i = 2, quantised to 2^-32 */
+int or_reg_gradients(const float *cost, const float *pred, int64_t n, int64_t *g, int64_t *h);
+
+/* ---- transfer learning, Eq. 4: f(x) = f_global(x) + f_local(x) as ONE ensemble:
+ * the trees of a then those of b (a tree shallower than max(depth) padded with pass-through
+ * nodes (f 0, theta +inf: always left), its leaf copied to the leftmost descendant slot),
+ * base = a.base + b.base (fp32).  Arrays sized for (a.n_trees + b.n_trees) trees of depth
+ * max(a.depth, b.depth). */
+int or_gbt_concat(const or_gbt *a, const or_gbt *b, uint16_t *feat, float *thresh, float *leaf, float *base);
 
 #ifdef __cplusplus
 }

@@ -50,7 +50,9 @@ class FitOpts(C.Structure):
     _fields_ = [("n_trees", C.c_int32), ("depth", C.c_int32), ("max_bins", C.c_int32), ("group_size", C.c_int32),
                 ("eta", C.c_float), ("lambda_", C.c_float), ("min_child_weight", C.c_float), ("seed", C.c_uint64),
                 ("allreduce", ALLREDUCE_FN), ("ctx", C.c_void_p), ("d_pred_out", C.c_void_p),
-                ("d_hist0_out", C.c_void_p)]
+                ("d_hist0_out", C.c_void_p), ("objective", C.c_int32), ("d_base_margin", C.c_void_p)]
+
+OBJECTIVES = {"rank": 0, "reg": 1}   # Eq. 2 / sum (f - c)^2
 
 
 _lib = None
@@ -75,6 +77,7 @@ def lib() -> C.CDLL:
         L.gbt_info.argtypes = [vp, vp, vp, vp]
         L.gbt_export.argtypes = [vp, vp, vp, vp, vp]
         L.gbt_destroy.argtypes = [vp]
+        L.gbt_concat.argtypes = [vp, vp, C.POINTER(vp)]
         L.gbt_predict.argtypes = [vp, vp, i64, i64, vp, vp, vp]
         L.sa_explore.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.POINTER(SaOpts), vp, vp, vp, vp]
         L.topk_merge.argtypes = [vp, vp, vp, vp, i32, i32, vp, i64, i32, vp, vp, vp, vp]
@@ -198,6 +201,12 @@ class Gbt:
         except Exception:
             pass
 
+    def concat(self, other: "Gbt") -> "Gbt":
+        """Eq. 4: self's trees then other's as one ensemble (gbt_concat)."""
+        h = C.c_void_p()
+        _check(lib().gbt_concat(self.h, other.h, C.byref(h)))
+        return Gbt(handle=h)
+
     def export(self):
         T, D = self.n_trees, self.depth
         feat = np.zeros((T, (1 << D) - 1), np.uint16)
@@ -287,8 +296,10 @@ def select_topk(space: Space, workload_id, pool_idx, pool_score, *, b, eps, alph
 
 def gbt_fit_hist(X, n, cost, group_key, *, n_trees=100, depth=6, max_bins=256, group_size=64, eta=0.1, lam=1.0,
                  min_child_weight=1.0, seed=1805, hist_range=None, allreduce=None, pred_out=None, hist0_out=None,
-                 stream=None) -> Gbt:
-    """Histogram GBT refit under the rank loss.  X: SoA [F][ld] CUDA tensor of all n samples.
+                 objective="rank", base_margin=None, stream=None) -> Gbt:
+    """Histogram GBT refit under the rank loss (objective "rank") or the regression loss ("reg").
+    X: SoA [F][ld] CUDA tensor of all n samples; base_margin: optional [n] CUDA float tensor of
+    initial predictions (transfer learning: f_global(x_i), Eq. 4).
 
     allreduce: optional python callable(tensor_view_int64) summing in place across ranks;
     it receives a torch view of the library's device buffer.
@@ -312,7 +323,8 @@ def gbt_fit_hist(X, n, cost, group_key, *, n_trees=100, depth=6, max_bins=256, g
         cb = ALLREDUCE_FN()
     o = FitOpts(n_trees, depth, max_bins, group_size, eta, lam, min_child_weight, seed, cb, None,
                 pred_out.data_ptr() if pred_out is not None else None,
-                hist0_out.data_ptr() if hist0_out is not None else None)
+                hist0_out.data_ptr() if hist0_out is not None else None, OBJECTIVES[objective],
+                base_margin.data_ptr() if base_margin is not None else None)
     h = C.c_void_p()
     _check(lib().gbt_fit_hist(_ptr(X), n, ld, F, _ptr(cost), _ptr(group_key), hb, he, C.byref(o), C.byref(h),
                               _stream(stream)))

@@ -306,6 +306,21 @@ __global__ void __launch_bounds__(256) grads_kernel(const int32_t *__restrict__ 
     group_pair_grads(mem, m, sc, sp, g, h);
 }
 
+// Regression loss of P:175, sum_i (f_i - c_i)^2: g_i = 2 (f_i - c_i), h_i = 2 in 2^-32 fixed point
+// (the difference in fp64 from the two fp32 values, one RN multiply by 2^33, round to nearest).
+__device__ __forceinline__ void reg_grad(float f, float c, int64_t &g, int64_t &h)
+{
+    g = __double2ll_rn(2.0 * ((double)f - (double)c) * 4294967296.0);
+    h = 2ll * 4294967296ll;
+}
+
+__global__ void reg_grads_kernel(const float *__restrict__ cost, const float *__restrict__ pred, int64_t n,
+                                 int64_t *__restrict__ g, int64_t *__restrict__ h)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) reg_grad(pred[i], cost[i], g[i], h[i]);
+}
+
 // ------------------------------------------------------------------ 3. levels
 // Histograms use a compact bin layout: feature f owns nb_f = ncuts_f + 1 cells starting at
 // boff[f]; a level's buffer is hist[node][TB][2] int64 (TB = sum_f nb_f).
@@ -799,6 +814,7 @@ struct FusedArgs {
     uint64_t seed;
     double lam, mcw, eta;
     unsigned *bar;
+    int objective;              // AT_OBJ_RANK / AT_OBJ_REG
 };
 
 __host__ __device__ inline int fused_ep(int N)
@@ -1049,8 +1065,21 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
     uint8_t *nat = natA, *nat2 = natB;
     for (int t = 0; t < A.n_trees; ++t) {
         unsigned long long *slot = A.slot;
-        // ---- gradients (and the previous tree's prediction update) per group
-        for (int item = blockIdx.x; item < A.n_groups * chunks; item += G) {
+        // ---- gradients (and the previous tree's prediction update)
+        if (A.objective == AT_OBJ_REG) {   // per sample: grid-stride over the samples
+            for (int i = blockIdx.x * FUSED_NT + tid; i < N; i += G * FUSED_NT) {
+                float pv = __ldcg(A.pred[0] + i);   // tree 0: the initial predictions
+                if (t > 0) {
+                    pv = __fadd_rn(__ldcg(A.pred[(t - 1) & 1] + i), T.lval[leafof[i]]);
+                    A.pred[t & 1][i] = pv;
+                }
+                int64_t gi, hi;
+                reg_grad(pv, A.cost[i], gi, hi);
+                A.g[i] = gi;
+                A.h[i] = hi;
+            }
+        }
+        for (int item = blockIdx.x; A.objective == AT_OBJ_RANK && item < A.n_groups * chunks; item += G) {
             const int grp = item / chunks, a0 = (item - grp * chunks) * CM;
             if (tid == 0) {
                 int lo = 0, hi = FIT_MAXKEYS;   // largest w with gpre[w] <= grp
@@ -1077,7 +1106,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
                 while (r >= (uint32_t)nw) r = feistel_inv(r, hb, A.seed, (uint32_t)t, (uint32_t)w);
                 const int i = A.klist[A.woff[w] + (int)r];
                 mem[a] = i;
-                float pv = 0.0f;
+                float pv = __ldcg(A.pred[0] + i);   // tree 0: the initial predictions
                 if (t > 0) {
                     pv = __fadd_rn(__ldcg(A.pred[(t - 1) & 1] + i), T.lval[leafof[i]]);
                     if (a >= a0 && a < a1) A.pred[t & 1][i] = pv;   // the chunk owning the member writes it
@@ -1431,6 +1460,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     if (o->depth < 1 || o->depth > 8) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: depth must be in [1, 8]");
     if (o->max_bins < 2 || o->max_bins > 256) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: max_bins must be in [2, 256]");
     if (o->n_trees < 1 || o->group_size < 2 || o->group_size > 1024) return fail(AT_EINVAL, "gbt_fit_hist: bad n_trees / group_size");
+    if (o->objective != AT_OBJ_RANK && o->objective != AT_OBJ_REG) return fail(AT_EINVAL, "gbt_fit_hist: bad objective");
     if (hb < 0 || he < hb || he > n) return fail(AT_EINVAL, "gbt_fit_hist: bad histogram slice");
     if (!o->allreduce && (hb != 0 || he != n)) return fail(AT_EINVAL, "gbt_fit_hist: a slice needs an allreduce");
     cudaStream_t s = (cudaStream_t)stream;
@@ -1481,7 +1511,10 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         bins_kernel<<<dim3(nblk(n, 256), F), 256, 0, s>>>(d_feat, ld, n, F, B, cuts, ncuts, bins); note_launch();
         ranks_kernel<<<1, 1024, 0, s>>>(d_group_key, n, rank, counts, woff, gpre, GS); note_launch();
         AT_CUDA_TRY(cudaMemcpyAsync(d_info + 3, gpre + FIT_MAXKEYS, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        AT_CUDA_TRY(cudaMemsetAsync(pred, 0, sizeof(float) * n, s));
+        if (o->d_base_margin)   // initial predictions: f_global(x_i) for a transfer-learning fit (Eq. 4)
+            AT_CUDA_TRY(cudaMemcpyAsync(pred, o->d_base_margin, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+        else
+            AT_CUDA_TRY(cudaMemsetAsync(pred, 0, sizeof(float) * n, s));
         AT_LAUNCH_CHECK("fit prep");
         AT_CUDA_TRY(cudaMemcpyAsync(info, d_info, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         AT_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1565,6 +1598,9 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             fa.cost = d_cost; fa.g = g; fa.h = h;
             fa.pred[0] = (o->n_trees & 1) ? pred2 : pred;   // the final predictions land in pred
             fa.pred[1] = (o->n_trees & 1) ? pred : pred2;
+            if (fa.pred[0] != pred)   // pred[0] holds the initial predictions (tree 0 reads them)
+                AT_CUDA_TRY(cudaMemcpyAsync(fa.pred[0], pred, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+            fa.objective = o->objective;
             fa.gord = gord; fa.gord0 = gord0; fa.gnode = gnode; fa.slot = slot;
             fa.t_feat = t_feat; fa.t_thr = t_thr; fa.t_leaf = t_leaf;
             fa.seed = o->seed; fa.lam = lam; fa.mcw = mcw; fa.eta = eta; fa.bar = bar;
@@ -1600,11 +1636,16 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         for (int t = 0; t < o->n_trees; ++t) {
             {
                 ProfScope ps(AT_K_FIT_GRAD, s);
-                positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, (uint32_t)t,
-                                                              member); note_launch();
-                if (n_groups > 0) {
-                    grads_kernel<<<n_groups, 256, grad_smem, s>>>(member, counts, woff, gpre, GS, d_cost, pred, g, h);
-                    note_launch();
+                if (o->objective == AT_OBJ_REG) {
+                    reg_grads_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, pred, n, g, h); note_launch();
+                } else {
+                    positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed,
+                                                                  (uint32_t)t, member); note_launch();
+                    if (n_groups > 0) {
+                        grads_kernel<<<n_groups, 256, grad_smem, s>>>(member, counts, woff, gpre, GS, d_cost, pred, g,
+                                                                      h);
+                        note_launch();
+                    }
                 }
                 AT_LAUNCH_CHECK("fit gradients");
             }

@@ -204,6 +204,37 @@ int gbt_export(at_gbt g, uint16_t *feat, float *thresh, float *leaf, float *base
     return AT_OK;
 }
 
+// Eq. 4: f_global + f_local as one ensemble.  A depth-d tree inside a depth-D
+// ensemble keeps heap nodes 0 .. 2^d - 2; its former leaf nodes and everything below them are
+// pass-through (feature 0, threshold +inf), so former slot s always ends at slot s * 2^(D - d).
+int gbt_concat(at_gbt a, at_gbt b, at_gbt *out)
+{
+    if (!a || !b || !out) return at::fail(AT_EINVAL, "gbt_concat: null handle");
+    if (a->n_features != b->n_features) return at::fail(AT_EMISMATCH, "gbt_concat: different n_features");
+    const int D = std::max(a->depth, b->depth);
+    const int64_t NI = (1 << D) - 1, NL = 1 << D;
+    const int T = a->n_trees + b->n_trees;
+    std::vector<uint16_t> feat((size_t)T * NI, 0);
+    std::vector<float> thr((size_t)T * NI, INFINITY), leaf((size_t)T * NL, 0.0f);
+    int t0 = 0;
+    for (at_gbt m : {a, b}) {
+        const int64_t ni = (1 << m->depth) - 1, nl = 1 << m->depth;
+        std::vector<uint16_t> f((size_t)m->n_trees * ni);
+        std::vector<float> th((size_t)m->n_trees * ni), lv((size_t)m->n_trees * nl);
+        const int rc = gbt_export(m, f.data(), th.data(), lv.data(), nullptr);
+        if (rc) return rc;
+        const int sh = D - m->depth;
+        for (int t = 0; t < m->n_trees; ++t) {
+            const size_t u = (size_t)(t0 + t);
+            std::copy(f.begin() + (size_t)t * ni, f.begin() + (size_t)(t + 1) * ni, feat.begin() + u * NI);
+            std::copy(th.begin() + (size_t)t * ni, th.begin() + (size_t)(t + 1) * ni, thr.begin() + u * NI);
+            for (int64_t q = 0; q < nl; ++q) leaf[u * NL + ((size_t)q << sh)] = lv[(size_t)t * nl + q];
+        }
+        t0 += m->n_trees;
+    }
+    return gbt_create(T, D, a->n_features, feat.data(), thr.data(), leaf.data(), a->base + b->base, out);   // host fp32 add (SSE, RN)
+}
+
 int gbt_destroy(at_gbt g)
 {
     if (!g) return AT_OK;

@@ -452,6 +452,87 @@ def test_fit_fused_forest_many_features_and_ties(at):
         assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
 
 
+# ------------------------------------------------------------------ §8(f): regression objective, transfer (Eq. 4)
+@pytest.mark.parametrize("n,wls,trees,depth,margin", [(1024, [synth.CFG2A], 4, 6, False),
+                                                      (333, synth.ALL_DW[:5], 3, 4, True),
+                                                      (2048, synth.ALL_RESNET[:4], 2, 8, False),
+                                                      (37, [synth.CFG2B], 3, 2, True)])
+def test_fit_regression_matches_oracle(at, n, wls, trees, depth, margin):
+    """P:175 regression objective (g = 2 (f - c), h = 2), optionally on top of a base margin, in both
+    the fused single-launch forest and the level-by-level path."""
+    osp, idx, X, c, key = fit_inputs(n, wls, seed=3 * n + depth)
+    m = np.random.default_rng(n).normal(0, 0.5, n).astype(np.float32) if margin else None
+    ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth, objective="reg", base_margin=m)
+    Xg = at.Space(wls).features(u64(idx))
+    kw = dict(n_trees=trees, depth=depth, objective="reg")
+    if margin:
+        kw["base_margin"] = dev(m)
+    fused, lvl = _fit_both_paths(at, Xg, n, c, key, **kw)
+    for k in ("feat", "thresh", "leaf", "pred"):
+        assert_bits_equal(fused[k], ref[k], f"fused {k}")
+        assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
+
+
+@pytest.mark.parametrize("n,trees,depth", [(1024, 5, 6), (3000, 3, 5)])
+def test_fit_rank_with_base_margin_matches_oracle(at, n, trees, depth):
+    """Rank loss (Eq. 2) fitted on top of per-sample initial predictions (both paths)."""
+    osp, idx, X, c, key = fit_inputs(n, [synth.CFG2A, synth.CFG2B], seed=n + 7)
+    m = np.random.default_rng(n + 1).normal(0, 1.0, n).astype(np.float32)
+    ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth, base_margin=m)
+    Xg = at.Space([synth.CFG2A, synth.CFG2B]).features(u64(idx))
+    fused, lvl = _fit_both_paths(at, Xg, n, c, key, n_trees=trees, depth=depth, base_margin=dev(m))
+    for k in ("feat", "thresh", "leaf", "pred"):
+        assert_bits_equal(fused[k], ref[k], f"fused {k}")
+        assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
+
+
+def test_gbt_concat_matches_oracle(at):
+    """gbt_concat (Eq. 4): a depth-8 and a depth-5 ensemble become one depth-8 ensemble whose
+    arrays and scores equal the oracle's concatenation bit for bit."""
+    a, b = synth.ensemble(70, 8, seed=11), synth.ensemble(45, 5, seed=12)
+    ga, gb = at.Gbt(a["feat"], a["thresh"], a["leaf"], base=0.25), at.Gbt(b["feat"], b["thresh"], b["leaf"], base=-1.5)
+    cat = ga.concat(gb).export()
+    ref = O.gbt_concat(O.OracleGbt(a["feat"], a["thresh"], a["leaf"], base=0.25),
+                       O.OracleGbt(b["feat"], b["thresh"], b["leaf"], base=-1.5))
+    for k in ("feat", "thresh", "leaf"):
+        assert_bits_equal(cat[k], getattr(ref, k), k)
+    assert np.float32(cat["base"]) == np.float32(ref.base)
+    sp = at.Space([synth.CFG2A])
+    idx = synth.uniform_indices(sp.size(), 3000, seed=13)
+    X = sp.features(u64(idx))
+    got = at.Gbt(cat["feat"], cat["thresh"], cat["leaf"], base=cat["base"]).predict(X, 3000)
+    assert_bits_equal(got.cpu().numpy(), ref.predict(X[:, :3000].cpu().numpy().T.copy()), "concat scores")
+
+
+def test_transfer_learning_pipeline_matches_oracle(at):
+    """Eq. 4 end to end: a global model on history of C1-C6, its scores on the target's samples as
+    the margin of the local fit, then f_global + f_local as one ensemble scoring new candidates."""
+    hist_wls, tgt = synth.ALL_RESNET[:6], synth.CFG2B
+    _, hidx, HX, hc, hkey = fit_inputs(1500, hist_wls, seed=41)
+    gref = O.fit_hist(HX, hc, hkey, n_trees=8, depth=6)
+    gg = at.gbt_fit_hist(at.Space(hist_wls).features(u64(hidx)), 1500, dev(hc), dev(hkey.view(np.int16)),
+                         n_trees=8, depth=6)
+    ge = gg.export()
+    for k in ("feat", "thresh", "leaf"):
+        assert_bits_equal(ge[k], gref[k], f"global {k}")
+    osp, tidx, TX, tc, tkey = fit_inputs(400, [tgt], seed=42)
+    tsp = at.Space([tgt])
+    TXg = tsp.features(u64(tidx))
+    margin_g = gg.predict(TXg, 400)
+    og = O.OracleGbt(gref["feat"], gref["thresh"], gref["leaf"])
+    margin_o = og.predict(TX)
+    assert_bits_equal(margin_g.cpu().numpy(), margin_o, "global scores on the target samples")
+    lref = O.fit_hist(TX, tc, tkey, n_trees=6, depth=4, base_margin=margin_o)
+    lg = at.gbt_fit_hist(TXg, 400, dev(tc), dev(tkey.view(np.int16)), n_trees=6, depth=4, base_margin=margin_g)
+    le = lg.export()
+    for k in ("feat", "thresh", "leaf"):
+        assert_bits_equal(le[k], lref[k], f"local {k}")
+    cat_o = O.gbt_concat(og, O.OracleGbt(lref["feat"], lref["thresh"], lref["leaf"]))
+    cidx = synth.uniform_indices(osp.size(), 2000, seed=43)
+    got = gg.concat(lg).predict(tsp.features(u64(cidx)), 2000)
+    assert_bits_equal(got.cpu().numpy(), cat_o.predict(osp.features(cidx)), "transfer model scores")
+
+
 def test_fit_errors(at):
     with pytest.raises(at.ATError) as e:
         at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 0, torch.zeros(4, device="cuda"),

@@ -549,3 +549,108 @@ def test_fit_cuts_rule():
     q = [s[((b + 1) * 1000) // 256] for b in range(255)]
     uq = [v for i, v in enumerate(q) if v != s[0] and (i == 0 or v != q[i - 1])]
     assert list(cuts[1, :nc[1]]) == uq
+
+
+# ---------------------------------------------------------------- §8(f): regression objective
+def test_reg_gradients_closed_form():
+    """P:175 loss sum_i (f_i - c_i)^2: dl/df_i = 2 (f_i - c_i), d2l/df_i^2 = 2, in 2^-32 units;
+    the gradient is checked against a central finite difference of the loss itself."""
+    c = np.array([1.0, 2.5, -3.0, 7.25], np.float32)
+    f = np.array([0.0, 3.0, -3.0, 1.0], np.float32)
+    g, h = O.reg_gradients(c, f)
+    assert g.tolist() == [-2 * 2**32, 2**32, 0, -int(12.5 * 2**32)]
+    assert h.tolist() == [2**33] * 4
+    loss = lambda ff: float(np.sum((ff.astype(np.float64) - c.astype(np.float64)) ** 2))
+    for i in range(4):
+        e = np.zeros(4)
+        e[i] = 1e-3
+        fd = (loss(f + e) - loss(f - e)) / 2e-3
+        assert abs(fd - g[i] / 2**32) < 1e-6
+
+
+def test_fit_regression_newton_step_is_the_group_mean():
+    """With eta = 1, lambda = 0 a squared-loss leaf is -G/H = the mean residual of its samples, so
+    one depth-1 tree on a single 2-valued feature predicts each value's mean cost exactly; the next
+    tree sees zero gradients, finds no split (gain 0 is not > 0) and changes nothing."""
+    X = np.array([[0.0], [0.0], [1.0], [1.0], [1.0]], np.float32)
+    c = np.array([1.0, 3.0, 2.0, 4.0, 6.0], np.float32)
+    key = np.zeros(5, np.uint16)
+    r = O.fit_hist(X, c, key, n_trees=2, depth=1, eta=1.0, lam=0.0, min_child_weight=0.0, objective="reg")
+    assert r["feat"][0, 0] == 0 and r["thresh"][0, 0] == 1.0
+    assert r["leaf"][0].tolist() == [2.0, 4.0]
+    assert r["pred"].tolist() == [2.0, 2.0, 4.0, 4.0, 4.0]
+    assert r["thresh"][1, 0] == np.inf and r["leaf"][1, 0] == 0.0   # slot 1 is unreachable (0/0 at lambda 0)
+
+
+def test_fit_regression_margin_equals_shifted_labels():
+    """Transfer margin (Eq. 4): fitting c on top of margin m is fitting c - m from zero (exact here:
+    small integers); the trees are identical and the predictions differ by exactly m."""
+    rng = np.random.default_rng(5)
+    n = 300
+    X = rng.integers(0, 6, (n, 8)).astype(np.float32)
+    m = rng.integers(-4, 5, n).astype(np.float32)
+    c = (X[:, 0] * 2 + X[:, 3] + rng.integers(0, 3, n)).astype(np.float32)
+    key = np.zeros(n, np.uint16)
+    a = O.fit_hist(X, c, key, n_trees=1, depth=3, objective="reg", base_margin=m)
+    b = O.fit_hist(X, (c - m).astype(np.float32), key, n_trees=1, depth=3, objective="reg")
+    for k in ("feat", "thresh", "leaf"):
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(a["pred"], (b["pred"] + m).astype(np.float32))
+
+
+def test_fit_rank_margin_constant_shift_invariance():
+    """Eq. 2 sees only differences f_j - f_i: a constant margin leaves the first tree unchanged, and
+    the training predictions are shifted by the margin."""
+    osp = space(synth.CFG2B)
+    n = 400
+    idx = synth.uniform_indices(osp.size(), n, seed=2)
+    X = osp.features(idx)
+    c = synth.labels(X, seed=2)
+    key = np.zeros(n, np.uint16)
+    a = O.fit_hist(X, c, key, n_trees=1, depth=4)
+    b = O.fit_hist(X, c, key, n_trees=1, depth=4, base_margin=np.full(n, 0.5, np.float32))
+    for k in ("feat", "thresh", "leaf"):
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(b["pred"], (a["pred"] + np.float32(0.5)).astype(np.float32))
+
+
+# ---------------------------------------------------------------- §8(f): transfer learning, Eq. 4
+def _rand_ens(T, D, F, seed):
+    rng = np.random.default_rng(seed)
+    ni, nl = (1 << D) - 1, 1 << D
+    return O.OracleGbt(rng.integers(0, F, (T, ni)).astype(np.uint16),
+                       rng.integers(0, 8, (T, ni)).astype(np.float32) + 0.5,
+                       rng.uniform(-1, 1, (T, nl)).astype(np.float32), base=float(rng.uniform(-1, 1)))
+
+
+def test_padded_tree_keeps_every_value():
+    """A depth-2 tree inside a depth-5 ensemble (pass-through nodes below, leaves at the leftmost
+    descendants) returns the same leaf for every input: brute force over all 8^3 feature vectors."""
+    small = O.OracleGbt(np.array([[0, 1, 2]], np.uint16), np.array([[3.5, 2.5, 5.5]], np.float32),
+                        np.array([[1.0, 2.0, 3.0, 4.0]], np.float32), base=0.75)
+    zero = O.OracleGbt(np.zeros((1, 31), np.uint16), np.full((1, 31), np.inf, np.float32),
+                       np.zeros((1, 32), np.float32))
+    cat = O.gbt_concat(small, zero)
+    assert cat.depth == 5 and cat.n_trees == 2
+    X = np.array(list(itertools.product(range(8), repeat=3)), np.float32)
+    ref = O.OracleGbt(small.feat, small.thresh, small.leaf).predict(X)   # base 0: the leaf itself
+    got = O.OracleGbt(cat.feat[:1], cat.thresh[:1], cat.leaf[:1]).predict(X)
+    assert len(np.unique(ref)) == 4   # every leaf is reached
+    assert np.array_equal(got, ref)
+
+
+def test_concat_is_sum_of_models_within_fp32_rounding():
+    """Eq. 4: f(x) = f_global(x) + f_local(x); the concatenated ensemble's canonical fp32 sum agrees
+    with the fp64 sum of the two models' exact tree sums within (T + 2) ulp-scaled error."""
+    a, b = _rand_ens(37, 6, 20, seed=3), _rand_ens(21, 4, 20, seed=4)
+    cat = O.gbt_concat(a, b)
+    assert cat.n_trees == 58 and cat.depth == 6
+    assert cat.base == np.float32(np.float32(a.base) + np.float32(b.base))
+    X = np.random.default_rng(6).integers(0, 8, (500, 20)).astype(np.float32)
+    got = cat.predict(X).astype(np.float64)
+    _, sa = a.predict(X, slots=True)
+    _, sb = b.predict(X, slots=True)
+    exact = (a.leaf.astype(np.float64)[np.arange(37)[:, None], sa].sum(0)
+             + b.leaf.astype(np.float64)[np.arange(21)[:, None], sb].sum(0) + np.float64(cat.base))
+    bound = (58 + 2) * 2.0 ** -24 * (np.abs(a.leaf).max() * 37 + np.abs(b.leaf).max() * 21 + 2)
+    assert np.max(np.abs(got - exact)) <= bound
