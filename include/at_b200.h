@@ -226,6 +226,37 @@ AT_API int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t n_fe
                  const float *d_cost, const uint16_t *d_group_key,
                  int64_t hist_begin, int64_t hist_end, const at_fit_opts *o, at_gbt *out, void *stream);
 
+/* ------------------------------------------------------------------ uncertainty
+ * "We can use bootstrapping to get the model's uncertainty estimate" with EI / UCB acquisition
+ * (readings Q40-Q43).
+ * bootstrap_resample -- model `model`'s training multiset: output row r is input sample
+ * (u * n) >> 32, u = word 0 of Philox(r, model, round, TAG_BOOT = 6) (n draws with replacement);
+ * copies the features (SoA [n_features][ld] -> [n_features][ld_out]), costs and group keys, and
+ * the drawn indices to d_idx_out (nullable).  Fit each model on its multiset with gbt_fit_hist,
+ * then gbt_concat the K models (equal tree counts) for gbt_predict_acq.
+ * gbt_predict_acq -- K = n_models equal-size models concatenated in g (model k = trees
+ * [k T/K, (k+1) T/K)): each model's score in the canonical order (Q19) plus model_base[k] -- bit
+ * for bit gbt_predict of that model alone -- then in fp64 over the K scores the mean mu and the
+ * population std sigma (model order), and the energy to minimise: AT_ACQ_MEAN mu, AT_ACQ_UCB
+ * mu - kappa sigma (the confidence bound of a minimised cost), AT_ACQ_EI -EI(mu, sigma; best)
+ * with EI = d Phi(d / sigma) + sigma phi(d / sigma), d = best - mu (fp32, exp_det, A&S 7.1.26).
+ * Writes d_score [n] and, when non-NULL, d_mean / d_std [n] (fp32). */
+enum { AT_ACQ_MEAN = 0, AT_ACQ_UCB = 1, AT_ACQ_EI = 2 };
+typedef struct {
+    int32_t n_models;             /* 1..8, divides the ensemble's tree count */
+    int32_t kind;                 /* AT_ACQ_* */
+    float kappa;                  /* UCB exploration weight */
+    float best;                   /* EI incumbent (model scale), e.g. min mu over the measured set */
+    float model_base[8];          /* base score of each model (gbt_concat sums the bases) */
+} at_acq_opts;
+
+AT_API int bootstrap_resample(const float *d_feat, int64_t n, int64_t ld, int32_t n_features, const float *d_cost,
+                              const uint16_t *d_group_key, int32_t model, uint64_t seed, uint32_t round,
+                              float *d_feat_out, int64_t ld_out, float *d_cost_out, uint16_t *d_key_out,
+                              int64_t *d_idx_out, void *stream);
+AT_API int gbt_predict_acq(at_gbt g, const float *d_feat, int64_t n, int64_t ld, const at_acq_opts *o, float *d_score,
+                           float *d_mean, float *d_std, void *stream);
+
 /* gbt_concat -- transfer learning, Eq. 4: f(x) = f_global(x) + f_local(x) as ONE
  * ensemble (a's trees, then b's), so gbt_predict / sa_explore score it unchanged.  A tree
  * shallower than max(depth) is padded with pass-through nodes (feature 0, threshold +inf:

@@ -94,6 +94,9 @@ def lib():
         _lib.or_touch_bruteforce.restype = C.c_uint64
         _lib.or_encode.restype = C.c_uint64
         _lib.or_gbt_score.restype = C.c_float
+        _lib.or_expected_improvement.restype = C.c_float
+        _lib.or_expected_improvement.argtypes = [C.c_float, C.c_float, C.c_float]
+        _lib.or_acquisition.restype = C.c_float
         _lib.or_rank_loss.restype = C.c_double
     return _lib
 
@@ -273,6 +276,42 @@ def gbt_concat(a, b):
     lib().or_gbt_concat(C.byref(ga), C.byref(gb), _p(feat, C.c_uint16), _p(thr, C.c_float), _p(leaf, C.c_float),
                         C.byref(base))
     return OracleGbt(feat, thr, leaf, base.value)
+
+
+ACQ = {"mean": 0, "ucb": 1, "ei": 2}
+
+
+def bootstrap_indices(n, model, seed=1805, round_=0):
+    """Q40: model `model`'s bootstrap multiset (n draws with replacement, Philox tag BOOT)."""
+    idx = np.zeros(n, np.int64)
+    lib().or_bootstrap_indices(C.c_int64(n), C.c_int32(model), C.c_uint64(seed), C.c_uint32(round_), _p(idx, C.c_int64))
+    return idx
+
+
+def expected_improvement(mu, sd, best):
+    return float(np.float32(lib().or_expected_improvement(C.c_float(mu), C.c_float(sd), C.c_float(best))))
+
+
+def acquisition(kind, f, kappa=1.0, best=0.0):
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    m, s = C.c_float(), C.c_float()
+    v = lib().or_acquisition(C.c_int(ACQ[kind]), C.c_int(len(f)), _p(f, C.c_float), C.c_float(kappa), C.c_float(best),
+                             C.byref(m), C.byref(s))
+    return float(np.float32(v)), float(np.float32(m.value)), float(np.float32(s.value))
+
+
+def predict_acq(models, X, kind="ucb", kappa=1.0, best=0.0):
+    """Acquisition over K models: (score, mean, std) per row of X [n][F]."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n, F = X.shape
+    arr = (Gbt * len(models))(*[m.c() for m in models])
+    score, mean, std = np.zeros(n, np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32)
+    rc = lib().or_gbt_predict_acq(arr, C.c_int(len(models)), _p(X, C.c_float), C.c_int64(n), C.c_int(F),
+                                  C.c_int(ACQ[kind]), C.c_float(kappa), C.c_float(best), _p(score, C.c_float),
+                                  _p(mean, C.c_float), _p(std, C.c_float))
+    if rc != 0:
+        raise ValueError(f"oracle predict_acq rc={rc}")
+    return score, mean, std
 
 
 def reg_gradients(cost, pred):

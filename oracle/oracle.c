@@ -12,7 +12,7 @@
 #include <stdlib.h>
 #include <string.h>
 
-enum { TAG_SA_INIT = 0, TAG_SA_STEP = 1, TAG_EPS = 2, TAG_GROUP_PERM = 3 };
+enum { TAG_SA_INIT = 0, TAG_SA_STEP = 1, TAG_EPS = 2, TAG_GROUP_PERM = 3, TAG_BOOT = 6 };
 
 static float f_from_bits(uint32_t b) { float f; memcpy(&f, &b, 4); return f; }
 
@@ -1032,5 +1032,74 @@ int or_gbt_concat(const or_gbt *a, const or_gbt *b, uint16_t *feat, float *thres
         copy_padded(b, t, D, feat + u * NI, thresh + u * NI, leaf + u * NL);
     }
     *base = a->base + b->base;
+    return 0;
+}
+
+/* ======================================================================
+ * Uncertainty estimate by bootstrapping, EI / UCB acquisition (readings Q40-Q43)
+ * ==================================================================== */
+/* Q40: model k's training multiset: draw r = 0..n-1 picks sample (u * n) >> 32 with
+ * u = word 0 of Philox(r, k, round, TAG_BOOT) (uniform, with replacement). */
+int or_bootstrap_indices(int64_t n, int32_t model, uint64_t seed, uint32_t round, int64_t *idx)
+{
+    for (int64_t r = 0; r < n; ++r) {
+        uint32_t o[4];
+        philox(seed, (uint32_t)r, (uint32_t)model, round, TAG_BOOT, o);
+        idx[r] = (int64_t)(((uint64_t)o[0] * (uint64_t)n) >> 32);
+    }
+    return 0;
+}
+
+/* Q43: expected improvement below the incumbent `best` for a minimised cost, in fp32 with one
+ * RN operation per step: EI = d Phi(z) + sigma phi(z), d = best - mu, z = d / sigma; sigma = 0
+ * gives max(d, 0).  Phi(z) = 1 - erfc(z / sqrt 2) / 2 (z >= 0), erfc(x / sqrt 2)/2 (z < 0), with
+ * Abramowitz-Stegun 7.1.26 for erfc(x) = t (a1 + t (a2 + t (a3 + t (a4 + t a5)))) exp(-x^2),
+ * t = 1 / (1 + p x) (|error| <= 1.5e-7), phi(z) = exp(-z^2 / 2) / sqrt(2 pi); exp = exp_det. */
+float or_expected_improvement(float mu, float sd, float best)
+{
+    float d = best - mu;
+    if (!(sd > 0.0f)) return d > 0.0f ? d : 0.0f;
+    float z = d / sd;
+    float x = fabsf(z) * 0.70710677f;                     /* |z| / sqrt 2 */
+    float t = 1.0f / (1.0f + 0.3275911f * x);
+    float poly = 1.061405429f;
+    poly = poly * t + -1.453152027f;
+    poly = poly * t + 1.421413741f;
+    poly = poly * t + -0.284496736f;
+    poly = poly * t + 0.254829592f;
+    poly = poly * t;
+    float ec = poly * or_exp_det(-(x * x));               /* erfc(x) */
+    float Phi = z >= 0.0f ? 1.0f - 0.5f * ec : 0.5f * ec;
+    float phi = 0.3989423f * or_exp_det((-0.5f * z) * z);
+    return d * Phi + sd * phi;
+}
+
+/* Q41/Q42: over the K models' scores f[k]: mean and population standard deviation in fp64
+ * (sequential sums in model order), then the energy SA minimises:
+ * kind 0 mean, kind 1 lower confidence bound mu - kappa sigma (UCB for a minimised cost,
+ * fp64, rounded once), kind 2 -EI(mu, sigma, best) in fp32. */
+float or_acquisition(int kind, int K, const float *f, float kappa, float best, float *mean_out, float *std_out)
+{
+    double mu = 0.0, v = 0.0;
+    for (int k = 0; k < K; ++k) mu += (double)f[k];
+    mu = mu / (double)K;
+    for (int k = 0; k < K; ++k) { double e = (double)f[k] - mu; v += e * e; }
+    double sd = sqrt(v / (double)K);
+    if (mean_out) *mean_out = (float)mu;
+    if (std_out) *std_out = (float)sd;
+    if (kind == 1) return (float)(mu - (double)kappa * sd);
+    if (kind == 2) return -or_expected_improvement((float)mu, (float)sd, best);
+    return (float)mu;
+}
+
+int or_gbt_predict_acq(const or_gbt *models, int K, const float *X, int64_t n, int F, int kind, float kappa,
+                       float best, float *score, float *mean, float *std)
+{
+    float f[64];
+    if (K < 1 || K > 64) return -1;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int k = 0; k < K; ++k) f[k] = or_gbt_score(&models[k], X + (size_t)i * F, NULL);
+        score[i] = or_acquisition(kind, K, f, kappa, best, mean ? &mean[i] : NULL, std ? &std[i] : NULL);
+    }
     return 0;
 }

@@ -167,6 +167,14 @@ int or_reg_gradients(const float *cost, const float *pred, int64_t n, int64_t *g
  * max(a.depth, b.depth). */
 int or_gbt_concat(const or_gbt *a, const or_gbt *b, uint16_t *feat, float *thresh, float *leaf, float *base);
 
+/* ---- bootstrap uncertainty, EI / UCB acquisition (Q40-Q43) ---- */
+int or_bootstrap_indices(int64_t n, int32_t model, uint64_t seed, uint32_t round, int64_t *idx);
+float or_expected_improvement(float mu, float sd, float best);
+float or_acquisition(int kind /* 0 mean, 1 UCB (mu - kappa sigma), 2 -EI */, int K, const float *f, float kappa,
+                     float best, float *mean_out, float *std_out);
+int or_gbt_predict_acq(const or_gbt *models /* [K] */, int K, const float *X /* [n][F] */, int64_t n, int F,
+                       int kind, float kappa, float best, float *score, float *mean, float *std);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,7 +52,13 @@ class FitOpts(C.Structure):
                 ("allreduce", ALLREDUCE_FN), ("ctx", C.c_void_p), ("d_pred_out", C.c_void_p),
                 ("d_hist0_out", C.c_void_p), ("objective", C.c_int32), ("d_base_margin", C.c_void_p)]
 
-OBJECTIVES = {"rank": 0, "reg": 1}   # Eq. 2 / sum (f - c)^2
+OBJECTIVES = {"rank": 0, "reg": 1}
+ACQ = {"mean": 0, "ucb": 1, "ei": 2}   # P:208-215 acquisition over bootstrap models
+
+
+class AcqOpts(C.Structure):
+    _fields_ = [("n_models", C.c_int32), ("kind", C.c_int32), ("kappa", C.c_float), ("best", C.c_float),
+                ("model_base", C.c_float * 8)]   # Eq. 2 / sum (f - c)^2
 
 
 _lib = None
@@ -78,6 +84,8 @@ def lib() -> C.CDLL:
         L.gbt_export.argtypes = [vp, vp, vp, vp, vp]
         L.gbt_destroy.argtypes = [vp]
         L.gbt_concat.argtypes = [vp, vp, C.POINTER(vp)]
+        L.gbt_predict_acq.argtypes = [vp, vp, i64, i64, C.POINTER(AcqOpts), vp, vp, vp, vp]
+        L.bootstrap_resample.argtypes = [vp, i64, i64, i32, vp, vp, i32, C.c_uint64, C.c_uint32, vp, i64, vp, vp, vp, vp]
         L.gbt_predict.argtypes = [vp, vp, i64, i64, vp, vp, vp]
         L.sa_explore.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.POINTER(SaOpts), vp, vp, vp, vp]
         L.topk_merge.argtypes = [vp, vp, vp, vp, i32, i32, vp, i64, i32, vp, vp, vp, vp]
@@ -200,6 +208,17 @@ class Gbt:
             self.close()
         except Exception:
             pass
+
+    def predict_acq(self, X, n, n_models, kind="ucb", kappa=1.0, best=0.0, model_base=None, stream=None):
+        """K = n_models equal concatenated models: (energy, mean, std) per candidate."""
+        import torch
+        ld = X.shape[1]
+        out = [torch.empty(n, dtype=torch.float32, device=X.device) for _ in range(3)]
+        mb = (C.c_float * 8)(*([0.0] * 8 if model_base is None else list(model_base) + [0.0] * (8 - len(model_base))))
+        o = AcqOpts(n_models, ACQ[kind], kappa, best, mb)
+        _check(lib().gbt_predict_acq(self.h, _ptr(X), n, ld, C.byref(o), _ptr(out[0]), _ptr(out[1]), _ptr(out[2]),
+                                     _stream(stream)))
+        return tuple(out)
 
     def concat(self, other: "Gbt") -> "Gbt":
         """Eq. 4: self's trees then other's as one ensemble (gbt_concat)."""
@@ -329,6 +348,20 @@ def gbt_fit_hist(X, n, cost, group_key, *, n_trees=100, depth=6, max_bins=256, g
     _check(lib().gbt_fit_hist(_ptr(X), n, ld, F, _ptr(cost), _ptr(group_key), hb, he, C.byref(o), C.byref(h),
                               _stream(stream)))
     return Gbt(handle=h)
+
+
+def bootstrap_resample(X, n, cost, group_key, model, *, seed=1805, round_=0, stream=None):
+    """Q40: model `model`'s bootstrap multiset of the n samples -> (X_out [F][n'], cost, keys, idx)."""
+    import torch
+    F, ld = X.shape
+    ldo = (n + 3) // 4 * 4
+    Xo = torch.zeros((F, ldo), dtype=torch.float32, device=X.device)
+    co = torch.empty(n, dtype=torch.float32, device=X.device)
+    ko = torch.empty(n, dtype=torch.int16, device=X.device)
+    io = torch.empty(n, dtype=torch.int64, device=X.device)
+    _check(lib().bootstrap_resample(_ptr(X), n, ld, F, _ptr(cost), _ptr(group_key), model, seed, round_, _ptr(Xo), ldo,
+                                    _ptr(co), _ptr(ko), _ptr(io), _stream(stream)))
+    return Xo, co, ko, io
 
 
 class _CudaArray:

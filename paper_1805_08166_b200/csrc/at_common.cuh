@@ -46,7 +46,7 @@ constexpr int MAXLOOPS = 18;
 constexpr int MAXKNOBS = 9;
 constexpr int MAXW = 16;
 
-enum Tag : uint32_t { TAG_SA_INIT = 0, TAG_SA_STEP = 1, TAG_EPS = 2, TAG_GROUP_PERM = 3 };
+enum Tag : uint32_t { TAG_SA_INIT = 0, TAG_SA_STEP = 1, TAG_EPS = 2, TAG_GROUP_PERM = 3, TAG_BOOT = 6 };
 
 // ---------------------------------------------------------------- Philox4x32-10
 // Counter-based RNG (Salmon et al., SC'11), counter (id, step, round, tag), key (seed lo, hi).

@@ -1447,6 +1447,46 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
 
+namespace at {
+// Q40: bootstrap multiset of model `model`: row r <- sample (u * n) >> 32, u = Philox(r, model, round, TAG_BOOT).x
+__global__ void bootstrap_kernel(const float *__restrict__ X, int64_t n, int64_t ld, int F, const float *__restrict__ c,
+                                 const uint16_t *__restrict__ key, uint32_t model, uint64_t seed, uint32_t round,
+                                 float *__restrict__ Xo, int64_t ldo, float *__restrict__ co, uint16_t *__restrict__ ko,
+                                 int64_t *__restrict__ io)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const U4 u = philox(seed, (uint32_t)r, model, round, TAG_BOOT);
+    const int64_t i = (int64_t)(((uint64_t)u.x * (uint64_t)n) >> 32);
+    for (int f = blockIdx.y; f < F; f += gridDim.y) Xo[(int64_t)f * ldo + r] = X[(int64_t)f * ld + i];
+    if (blockIdx.y == 0) {
+        co[r] = c[i];
+        ko[r] = key[i];
+        if (io) io[r] = i;
+    }
+}
+}  // namespace at
+
+extern "C" int bootstrap_resample(const float *d_feat, int64_t n, int64_t ld, int32_t F, const float *d_cost,
+                                  const uint16_t *d_key, int32_t model, uint64_t seed, uint32_t round,
+                                  float *d_feat_out, int64_t ld_out, float *d_cost_out, uint16_t *d_key_out,
+                                  int64_t *d_idx_out, void *stream)
+{
+    using namespace at;
+    if (n < 0 || n > 0xFFFFFFFFll || F < 1) return fail(AT_EINVAL, "bootstrap_resample: bad n / n_features");
+    if (n == 0) return AT_OK;
+    if (!d_feat || !d_cost || !d_key || !d_feat_out || !d_cost_out || !d_key_out)
+        return fail(AT_EINVAL, "bootstrap_resample: null buffer");
+    if (ld < n || ld_out < n) return fail(AT_EMISMATCH, "bootstrap_resample: ld < n");
+    cudaStream_t s = (cudaStream_t)stream;
+    const dim3 grid(nblk(n, 256), (unsigned)std::min(F, 64));
+    bootstrap_kernel<<<grid, 256, 0, s>>>(d_feat, n, ld, F, d_cost, d_key, (uint32_t)model, seed, round, d_feat_out,
+                                          ld_out, d_cost_out, d_key_out, d_idx_out);
+    note_launch();
+    AT_LAUNCH_CHECK("bootstrap_kernel");
+    return AT_OK;
+}
+
 extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t F, const float *d_cost,
                             const uint16_t *d_group_key, int64_t hb, int64_t he, const at_fit_opts *o, at_gbt *out,
                             void *stream)

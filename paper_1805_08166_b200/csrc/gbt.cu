@@ -32,6 +32,7 @@ TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes)
     G.NC = (G.T + ch - 1) / ch;
     G.chunk_bytes = (uint32_t)ch * per_tree;
     G.resident = G.NC <= 2;
+    G.Tm = G.T;
     return G;
 }
 
@@ -66,17 +67,65 @@ __device__ __forceinline__ void tile_issue(const TileMap &tm, int64_t tile, floa
 // 2-D TMA (tensor map over X[F][ld]).  GRP = 1: two tile buffers, the next tile's HBM read overlaps
 // the current walk (small, resident ensembles: HBM-bound).  GRP = 2: one buffer of 64 candidates,
 // so every streamed tree byte serves twice the candidates (large ensembles: L2-bound).
-template <int GRP>
+// K bootstrap models scored at once (gbt_predict_acq): per-model canonical sums, then the acquisition
+struct AcqArgs {
+    int K, kind;
+    float kappa, best;
+    float base[8];
+    float *mean, *std;
+};
+
+// Q43, the oracle's sequence of fp32 RN operations (exp = exp_det): EI below `best` of a minimised cost
+__device__ __forceinline__ float expected_improvement(float mu, float sd, float best)
+{
+    const float d = __fsub_rn(best, mu);
+    if (!(sd > 0.0f)) return d > 0.0f ? d : 0.0f;
+    const float z = __fdiv_rn(d, sd);
+    const float x = __fmul_rn(fabsf(z), 0.70710677f);
+    const float t = __fdiv_rn(1.0f, __fadd_rn(1.0f, __fmul_rn(0.3275911f, x)));
+    float poly = 1.061405429f;
+    poly = __fadd_rn(__fmul_rn(poly, t), -1.453152027f);
+    poly = __fadd_rn(__fmul_rn(poly, t), 1.421413741f);
+    poly = __fadd_rn(__fmul_rn(poly, t), -0.284496736f);
+    poly = __fadd_rn(__fmul_rn(poly, t), 0.254829592f);
+    poly = __fmul_rn(poly, t);
+    const float ec = __fmul_rn(poly, exp_det(-__fmul_rn(x, x)));
+    const float Phi = z >= 0.0f ? __fsub_rn(1.0f, __fmul_rn(0.5f, ec)) : __fmul_rn(0.5f, ec);
+    const float phi = __fmul_rn(0.3989423f, exp_det(__fmul_rn(__fmul_rn(-0.5f, z), z)));
+    return __fadd_rn(__fmul_rn(d, Phi), __fmul_rn(sd, phi));
+}
+
+// Q41/Q42: fp64 mean / population std in model order; mean, UCB (mu - kappa sigma) or -EI
+__device__ __forceinline__ float acquisition(const AcqArgs &Q, const float *f, int stride, float &mean, float &sd)
+{
+    double mu = 0.0, v = 0.0;
+    for (int k = 0; k < Q.K; ++k) mu = __dadd_rn(mu, (double)f[k * stride]);
+    mu = __ddiv_rn(mu, (double)Q.K);
+    for (int k = 0; k < Q.K; ++k) {
+        const double e = __dsub_rn((double)f[k * stride], mu);
+        v = __dadd_rn(v, __dmul_rn(e, e));
+    }
+    const double s = __dsqrt_rn(__ddiv_rn(v, (double)Q.K));
+    mean = (float)mu;
+    sd = (float)s;
+    if (Q.kind == 1) return (float)__dsub_rn(mu, __dmul_rn((double)Q.kappa, s));
+    if (Q.kind == 2) return -expected_improvement(mean, sd, Q.best);
+    return mean;
+}
+
+template <int GRP, int KM>
 __global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, float base, int F, int tile_rows,
                                                                  const float *__restrict__ X, int64_t n, int64_t ld,
                                                                  float *__restrict__ score, uint8_t *__restrict__ slots,
-                                                                 int use_bulk, const __grid_constant__ TileMap tm)
+                                                                 int use_bulk, const __grid_constant__ TileMap tm,
+                                                                 const __grid_constant__ AcqArgs Q)
 {
     constexpr int NBUF = GRP == 1 ? 2 : 1;
     extern __shared__ __align__(128) unsigned char smraw[];
     PredSmemHdr &hd = *(PredSmemHdr *)smraw;
-    float *part = (float *)(smraw + 128);                      // [GRP][32][32]
-    float *tiles = part + GRP * 32 * 32;                       // [NBUF][GRP][tile_rows][32], tile_rows >= F
+    float *part = (float *)(smraw + 128);                      // [GRP][KM][32][32]
+    float *fk = part + GRP * KM * 32 * 32;                     // [GRP][KM][32] per-model scores (KM > 1)
+    float *tiles = fk + (KM > 1 ? GRP * KM * 32 : 0);          // [NBUF][GRP][tile_rows][32], tile_rows >= F
     uint8_t *bufs = (uint8_t *)(tiles + NBUF * GRP * tile_rows * 32);   // tree buffers (rows are 128 B)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_tiles = (n + 32 * GRP - 1) / (32 * GRP);
@@ -112,10 +161,26 @@ __global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, flo
                     tl[g * tile_rows * 32 + f * 32 + lane] = ok[g] ? X[(int64_t)f * ld + cand0 + 32 * g] : 0.0f;
             __syncthreads();
         }
-        walk_pass<PRED_NW, GRP>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part, slots, n,
-                                cand0, ok);
-        if (warp < GRP) {
-            if (ok[warp]) score[cand0 + 32 * warp] = gbt_combine(part + warp * 1024, lane, base);
+        walk_pass<PRED_NW, GRP, KM>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part, slots,
+                                    n, cand0, ok);
+        if (KM == 1) {
+            if (warp < GRP) {
+                if (ok[warp]) score[cand0 + 32 * warp] = gbt_combine(part + warp * 1024, lane, base);
+            }
+        } else {
+            // warp (g, m) folds model m's partials in the canonical order; then warp g takes the acquisition
+            if (warp < GRP * Q.K) {
+                const int g = warp / Q.K, m = warp - g * Q.K;
+                fk[(g * KM + m) * 32 + lane] = gbt_combine(part + (g * KM + m) * 1024, lane, Q.base[m]);
+            }
+            __syncthreads();
+            if (warp < GRP && ok[warp]) {
+                float mu, sd;
+                const int64_t i = cand0 + 32 * warp;
+                score[i] = acquisition(Q, fk + warp * KM * 32 + lane, 32, mu, sd);
+                if (Q.mean) Q.mean[i] = mu;
+                if (Q.std) Q.std[i] = sd;
+            }
         }
         __syncthreads();   // part[] and the tile buffer are free again
         if (use_bulk && threadIdx.x == 0 && i + NBUF < my_tiles) {
@@ -244,36 +309,38 @@ int gbt_destroy(at_gbt g)
     return AT_OK;
 }
 
-int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_score, uint8_t *d_leaf_slot,
-                void *stream)
+}  // extern "C"
+
+namespace at {
+
+// gbt_predict / gbt_predict_acq: one persistent scorer launch (KM = 1: one model; KM = 8: up to 8
+// concatenated models of equal tree count with their acquisition)
+static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_score, uint8_t *d_leaf_slot,
+                          const AcqArgs *acq, void *stream)
 {
-    if (!g) return at::fail(AT_EINVAL, "gbt_predict: null model");
-    if (n < 0) return at::fail(AT_EINVAL, "gbt_predict: n < 0");
-    if (n == 0) return AT_OK;
-    if (!d_feat || !d_score) return at::fail(AT_EINVAL, "gbt_predict: null buffer");
-    if (ld < n) return at::fail(AT_EMISMATCH, "gbt_predict: ld < n");
     cudaStream_t s = (cudaStream_t)stream;
-    const at::TreeGeo G = at::make_geo(g);
+    const int KM = acq ? 8 : 1;
+    TreeGeo G = make_geo(g, acq ? 32 * 1024 : TREE_BUF_BYTES);
+    if (acq) G.Tm = g->n_trees / acq->K;
     const int F = g->n_features;
     const int n_box = (F + 255) / 256, box_rows = (F + n_box - 1) / n_box, tile_rows = n_box * box_rows;
     // GRP = 2 (64 candidates per tile, one buffer) when the ensemble streams and it fits
     auto smem_for = [&](int grp) {
         const int nbuf = grp == 1 ? 2 : 1;
-        return 128 + (size_t)grp * 32 * 32 * sizeof(float) + (size_t)nbuf * grp * tile_rows * 32 * sizeof(float) +
-               at::tree_smem_bytes(G);
+        return 128 + (size_t)grp * KM * 32 * 32 * sizeof(float) + (KM > 1 ? (size_t)grp * KM * 32 * sizeof(float) : 0) +
+               (size_t)nbuf * grp * tile_rows * 32 * sizeof(float) + tree_smem_bytes(G);
     };
     constexpr size_t SMEM_MAX = 227 * 1024;
-    const int grp = (!G.resident && smem_for(2) <= SMEM_MAX) ? 2 : 1;
+    const int grp = (!acq && !G.resident && smem_for(2) <= SMEM_MAX) ? 2 : 1;
     const size_t smem = smem_for(grp);
-    if (smem > SMEM_MAX) return at::fail(AT_EUNSUPPORTED, "gbt_predict: too many features for the smem tiles");
-    static size_t attr1 = 0, attr2 = 0;
-    if (grp == 1 && smem > attr1) {
-        AT_CUDA_TRY(cudaFuncSetAttribute(at::predict_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr1 = smem;
-    }
-    if (grp == 2 && smem > attr2) {
-        AT_CUDA_TRY(cudaFuncSetAttribute(at::predict_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr2 = smem;
+    if (smem > SMEM_MAX) return fail(AT_EUNSUPPORTED, "gbt_predict: too many features for the smem tiles");
+    const void *kern = acq ? (const void *)predict_kernel<1, 8>
+                     : grp == 1 ? (const void *)predict_kernel<1, 1> : (const void *)predict_kernel<2, 1>;
+    static size_t attr[3] = {0, 0, 0};
+    const int ai = acq ? 2 : grp - 1;
+    if (smem > attr[ai]) {
+        AT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[ai] = smem;
     }
     static int n_sm = 0;
     if (!n_sm) {
@@ -282,7 +349,7 @@ int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_s
         AT_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
     // TMA tensor map over X[F][ld] (needs 16-B aligned rows); otherwise plain loads
-    at::TileMap tm{};
+    TileMap tm{};
     tm.n_box = n_box;
     tm.box_rows = box_rows;
     int use_bulk = (ld % 4 == 0) && ((uintptr_t)d_feat % 16 == 0);
@@ -306,16 +373,58 @@ int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_s
     }
     const int64_t tiles = (n + 32 * grp - 1) / (32 * grp);
     const unsigned blocks = (unsigned)std::min<int64_t>(tiles, n_sm);
-    at::ProfScope ps(AT_K_PREDICT, s);
-    if (grp == 1)
-        at::predict_kernel<1><<<blocks, at::PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
-                                                                     d_leaf_slot, use_bulk, tm);
+    AcqArgs Q{};
+    if (acq) Q = *acq;
+    ProfScope ps(AT_K_PREDICT, s);
+    if (acq)
+        predict_kernel<1, 8><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+                                                                d_leaf_slot, use_bulk, tm, Q);
+    else if (grp == 1)
+        predict_kernel<1, 1><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+                                                                d_leaf_slot, use_bulk, tm, Q);
     else
-        at::predict_kernel<2><<<blocks, at::PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
-                                                                     d_leaf_slot, use_bulk, tm);
-    at::note_launch();
+        predict_kernel<2, 1><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+                                                                d_leaf_slot, use_bulk, tm, Q);
+    note_launch();
     AT_LAUNCH_CHECK("predict_kernel");
     return AT_OK;
+}
+
+}  // namespace at
+
+extern "C" {
+
+int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_score, uint8_t *d_leaf_slot,
+                void *stream)
+{
+    if (!g) return at::fail(AT_EINVAL, "gbt_predict: null model");
+    if (n < 0) return at::fail(AT_EINVAL, "gbt_predict: n < 0");
+    if (n == 0) return AT_OK;
+    if (!d_feat || !d_score) return at::fail(AT_EINVAL, "gbt_predict: null buffer");
+    if (ld < n) return at::fail(AT_EMISMATCH, "gbt_predict: ld < n");
+    return at::predict_launch(g, d_feat, n, ld, d_score, d_leaf_slot, nullptr, stream);
+}
+
+int gbt_predict_acq(at_gbt g, const float *d_feat, int64_t n, int64_t ld, const at_acq_opts *o, float *d_score,
+                    float *d_mean, float *d_std, void *stream)
+{
+    if (!g || !o) return at::fail(AT_EINVAL, "gbt_predict_acq: null model / options");
+    if (o->n_models < 1 || o->n_models > 8 || g->n_trees % o->n_models != 0)
+        return at::fail(AT_EINVAL, "gbt_predict_acq: need 1 <= n_models <= 8 dividing n_trees");
+    if (o->kind < AT_ACQ_MEAN || o->kind > AT_ACQ_EI) return at::fail(AT_EINVAL, "gbt_predict_acq: bad kind");
+    if (n < 0) return at::fail(AT_EINVAL, "gbt_predict_acq: n < 0");
+    if (n == 0) return AT_OK;
+    if (!d_feat || !d_score) return at::fail(AT_EINVAL, "gbt_predict_acq: null buffer");
+    if (ld < n) return at::fail(AT_EMISMATCH, "gbt_predict_acq: ld < n");
+    at::AcqArgs Q{};
+    Q.K = o->n_models;
+    Q.kind = o->kind;
+    Q.kappa = o->kappa;
+    Q.best = o->best;
+    for (int k = 0; k < 8; ++k) Q.base[k] = k < Q.K ? o->model_base[k] : 0.0f;
+    Q.mean = d_mean;
+    Q.std = d_std;
+    return at::predict_launch(g, d_feat, n, ld, d_score, nullptr, &Q, stream);
 }
 
 }  // extern "C"

@@ -27,6 +27,7 @@ struct TreeGeo {
     int NC;                 // chunks per pass
     uint32_t chunk_bytes;   // CH * (ni * 8 + nl * 4)
     int resident;           // NC <= 2: loaded once, never re-streamed
+    int Tm;                 // trees per model (KM > 1: K equal models concatenated, gbt_predict_acq)
 };
 
 constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // default per buffer (two buffers)
@@ -59,9 +60,9 @@ __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64
 
 // A batch of NB trees t = t0, t0 + NW, ... (all owned by this warp: t = warp mod NW) walked for
 // GRP candidate groups at once: NB * GRP independent dependency chains.
-template <int NW, int GRP, int NB>
+template <int NW, int GRP, int NB, int KM>
 __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf, int c0, int t0, const float *tile,
-                                           int gstride, int lane, float (&p)[GRP][32 / NW],
+                                           int gstride, int lane, float (&p)[GRP][KM][32 / NW],
                                            uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand0,
                                            const bool (&cand_ok)[GRP])
 {
@@ -95,18 +96,24 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
             }
         }
     }
-    // leaves in ascending t: tree t adds to its residue class q = t mod 32, slot (q - warp) / NW = q / NW
+    // leaves in ascending t: tree t adds to its residue class q = t mod 32, slot (q - warp) / NW = q / NW;
+    // with KM models of Tm trees, tree t = km Tm + u adds to model km's class u mod 32 (all trees of
+    // one (model, class) pair share t mod NW, so one warp owns it and sums it in ascending u)
 #pragma unroll
     for (int jj = 0; jj < NB; ++jj) {
         const int t = t0 + jj * NW;
-        const int j = (t & 31) / NW;
+        int km = 0, u = t;
+        if (KM > 1) { km = t / G.Tm; u = t - km * G.Tm; }
+        const int j = (u & 31) / NW;
 #pragma unroll
         for (int g = 0; g < GRP; ++g) {
             const int slot = (int)((a[g][jj] + add_l[jj]) >> 3) - nl;   // h = (a - tb) / 8 in [2^D, 2^(D+1))
             const float lv = leaves[(t - c0) * nl + slot];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q)
-                if (q == j) p[g][q] = __fadd_rn(p[g][q], lv);
+            for (int m = 0; m < KM; ++m)
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    if (m == km && q == j) p[g][m][q] = __fadd_rn(p[g][m][q], lv);
             if (slots && cand_ok[g]) slots[(int64_t)t * slot_ld + cand0 + 32 * g] = (uint8_t)slot;
         }
     }
@@ -116,9 +123,9 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
 // in ascending order, in batches of up to 4 / GRP trees; no walk slot is spent on an absent tree,
 // whatever the chunk size.  GRP candidate groups of 32 (group g's tile at tile + g * gstride floats)
 // share every staged tree byte.
-template <int NW, int GRP>
+template <int NW, int GRP, int KM>
 __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const float *tile, int gstride,
-                                           int lane, int warp, float (&p)[GRP][32 / NW], uint8_t *__restrict__ slots,
+                                           int lane, int warp, float (&p)[GRP][KM][32 / NW], uint8_t *__restrict__ slots,
                                            int64_t slot_ld, int64_t cand0, const bool (&cand_ok)[GRP])
 {
     constexpr int NBMAX = GRP == 1 ? 4 : 2;
@@ -126,41 +133,44 @@ __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf,
     const int c1 = min(c0 + G.CH, G.T);
     int t0 = c0 + ((warp - c0) % NW + NW) % NW;
     for (; t0 + (NBMAX - 1) * NW < c1; t0 += NBMAX * NW)
-        walk_batch<NW, GRP, NBMAX>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, NBMAX, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
     const int rest = t0 < c1 ? (c1 - 1 - t0) / NW + 1 : 0;   // warp-uniform
     if (NBMAX == 4 && rest == 3)
-        walk_batch<NW, GRP, 3>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 3, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
     else if (rest >= 2)
-        walk_batch<NW, GRP, 2>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 2, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
     else if (rest == 1)
-        walk_batch<NW, GRP, 1>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 1, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
 }
 
 // One full pass over the ensemble.  `c` is the block-wide stream counter (identical in every
 // thread); `c_limit` the total number of chunks the kernel will consume.  Ends with group g's
-// partials in part[g * 1024 + q * 32 + lane] and a __syncthreads.
-template <int NW, int GRP>
+// partials in part[g * 1024 + q * 32 + lane] (KM models: part[((g KM + m) 32 + q) 32 + lane])
+// and a __syncthreads.
+template <int NW, int GRP, int KM = 1>
 __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph, uint64_t &c,
                                           uint64_t c_limit, const float *tile, int gstride, int lane, int warp,
                                           float *part, uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand0,
                                           const bool (&cand_ok)[GRP])
 {
     constexpr int NQ = 32 / NW;
-    float p[GRP][NQ];
+    float p[GRP][KM][NQ];
 #pragma unroll
     for (int g = 0; g < GRP; ++g)
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) p[g][j] = 0.0f;
+        for (int m = 0; m < KM; ++m)
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) p[g][m][j] = 0.0f;
     if (G.resident) {
         for (int k = 0; k < G.NC; ++k)
-            walk_chunk<NW, GRP>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
+            walk_chunk<NW, GRP, KM>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
                                 cand0, cand_ok);
     } else {
         for (int k = 0; k < G.NC; ++k, ++c) {
             const int b = (int)(c & 1);
             mbar_wait(&bar[b], ph[b]);
             ph[b] ^= 1u;
-            walk_chunk<NW, GRP>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
+            walk_chunk<NW, GRP, KM>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
                                 cand0, cand_ok);
             __syncthreads();   // every warp is done with buffer b
             if (threadIdx.x == 0 && c + 2 < c_limit) {
@@ -172,7 +182,12 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
 #pragma unroll
     for (int g = 0; g < GRP; ++g)
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) part[g * 1024 + (warp + j * NW) * 32 + lane] = p[g][j];
+        for (int m = 0; m < KM; ++m) {
+            // the warp's classes of model m: q = j NW + r, r = (warp - m Tm) mod NW
+            const int r = KM == 1 ? warp : ((warp - (m * G.Tm) % NW) % NW + NW) % NW;
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) part[((g * KM + m) * 32 + (r + j * NW)) * 32 + lane] = p[g][m][j];
+        }
     __syncthreads();
 }
 

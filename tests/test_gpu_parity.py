@@ -533,6 +533,70 @@ def test_transfer_learning_pipeline_matches_oracle(at):
     assert_bits_equal(got.cpu().numpy(), cat_o.predict(osp.features(cidx)), "transfer model scores")
 
 
+# ------------------------------------------------------------------ §8(f): bootstrap uncertainty, EI / UCB
+def test_bootstrap_resample_matches_oracle(at):
+    """Q40 multisets: the drawn indices and the gathered features / costs / keys."""
+    osp, idx, X, c, key = fit_inputs(777, [synth.CFG2A, synth.CFG2B], seed=5)
+    Xg = at.Space([synth.CFG2A, synth.CFG2B]).features(u64(idx))
+    for k in range(3):
+        Xo, co, ko, io = at.bootstrap_resample(Xg, 777, dev(c), dev(key.view(np.int16)), k, seed=31, round_=2)
+        ref = O.bootstrap_indices(777, k, seed=31, round_=2)
+        assert_bits_equal(io.cpu().numpy(), ref, f"model {k} indices")
+        assert_bits_equal(Xo[:, :777].cpu().numpy().T.copy(), X[ref], "gathered features")
+        assert_bits_equal(co.cpu().numpy(), c[ref], "gathered costs")
+        assert_bits_equal(ko.cpu().numpy().view(np.uint16), key[ref], "gathered keys")
+
+
+@pytest.mark.parametrize("kind", ["mean", "ucb", "ei"])
+def test_predict_acq_matches_oracle(at, kind):
+    """K = 5 models of 37 trees (not a multiple of 32) and mixed depths, concatenated: every model's
+    canonical score, then mean / std / acquisition, bit for bit against the oracle."""
+    depths = [6, 4, 6, 5, 6]
+    ens = [synth.ensemble(37, d, seed=60 + k) for k, d in enumerate(depths)]
+    bases = [0.0, 0.5, -0.25, 1.0, 0.0]
+    gs = [at.Gbt(e["feat"], e["thresh"], e["leaf"], base=b) for e, b in zip(ens, bases)]
+    cat = gs[0]
+    for g in gs[1:]:
+        cat = cat.concat(g)
+    sp = at.Space([synth.CFG2A])
+    idx = synth.uniform_indices(sp.size(), 2500, seed=61)
+    Xg = sp.features(u64(idx))
+    sc, mu, sd = cat.predict_acq(Xg, 2500, 5, kind=kind, kappa=1.5, best=-0.3, model_base=bases)
+    om = [O.OracleGbt(e["feat"], e["thresh"], e["leaf"], base=b) for e, b in zip(ens, bases)]
+    X = Xg[:, :2500].cpu().numpy().T.copy()
+    rs, rm, rsd = O.predict_acq(om, X, kind=kind, kappa=1.5, best=-0.3)
+    assert_bits_equal(mu.cpu().numpy(), rm, "mean")
+    assert_bits_equal(sd.cpu().numpy(), rsd, "std")
+    assert_bits_equal(sc.cpu().numpy(), rs, kind)
+    assert np.all(rsd > 0)
+
+
+def test_bootstrap_ensemble_pipeline_matches_oracle(at):
+    """P:211 end to end: 5 bootstrap multisets of D, one rank-loss model per multiset, the models
+    concatenated, UCB over them on new candidates -- each stage against the oracle."""
+    osp, idx, X, c, key = fit_inputs(600, [synth.CFG2B], seed=71)
+    Xg = osp_g = at.Space([synth.CFG2B]).features(u64(idx))
+    models, oms = [], []
+    for k in range(5):
+        Xo, co, ko, io = at.bootstrap_resample(Xg, 600, dev(c), dev(key.view(np.int16)), k, seed=72)
+        r = O.bootstrap_indices(600, k, seed=72)
+        ref = O.fit_hist(X[r], c[r], key[r], n_trees=6, depth=5)
+        g = at.gbt_fit_hist(Xo, 600, co, ko, n_trees=6, depth=5)
+        ex = g.export()
+        for f in ("feat", "thresh", "leaf"):
+            assert_bits_equal(ex[f], ref[f], f"model {k} {f}")
+        models.append(g)
+        oms.append(O.OracleGbt(ref["feat"], ref["thresh"], ref["leaf"]))
+    cat = models[0]
+    for g in models[1:]:
+        cat = cat.concat(g)
+    cidx = synth.uniform_indices(osp.size(), 1500, seed=73)
+    sc, mu, sd = cat.predict_acq(at.Space([synth.CFG2B]).features(u64(cidx)), 1500, 5, kind="ucb", kappa=1.0)
+    rs, rm, rsd = O.predict_acq(oms, osp.features(cidx), kind="ucb", kappa=1.0)
+    assert_bits_equal(sc.cpu().numpy(), rs, "ucb")
+    assert_bits_equal(sd.cpu().numpy(), rsd, "std")
+
+
 def test_fit_errors(at):
     with pytest.raises(at.ATError) as e:
         at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 0, torch.zeros(4, device="cuda"),

@@ -654,3 +654,62 @@ def test_concat_is_sum_of_models_within_fp32_rounding():
              + b.leaf.astype(np.float64)[np.arange(21)[:, None], sb].sum(0) + np.float64(cat.base))
     bound = (58 + 2) * 2.0 ** -24 * (np.abs(a.leaf).max() * 37 + np.abs(b.leaf).max() * 21 + 2)
     assert np.max(np.abs(got - exact)) <= bound
+
+
+# ---------------------------------------------------------------- §8(f): bootstrap uncertainty, EI / UCB
+def test_bootstrap_indices_are_uniform_with_replacement():
+    """Q40: n draws with replacement: every index in range, the unique fraction of a bootstrap
+    sample tends to 1 - 1/e, and over many models every sample is drawn ~uniformly (chi-square)."""
+    n, K = 2000, 40
+    cnt = np.zeros(n)
+    fr = []
+    for k in range(K):
+        idx = O.bootstrap_indices(n, k, seed=9)
+        assert idx.min() >= 0 and idx.max() < n
+        assert np.array_equal(idx, O.bootstrap_indices(n, k, seed=9))
+        fr.append(len(np.unique(idx)) / n)
+        np.add.at(cnt, idx, 1)
+    assert abs(np.mean(fr) - (1 - math.exp(-1))) < 0.01
+    chi2 = np.sum((cnt - K) ** 2 / K)
+    assert chi2 < n + 6 * math.sqrt(2 * n)          # n - 1 dof: mean n - 1, sd sqrt(2 (n - 1))
+    assert not np.array_equal(O.bootstrap_indices(n, 0, seed=9), O.bootstrap_indices(n, 1, seed=9))
+
+
+def test_acquisition_mean_std_ucb_against_numpy():
+    """Q41/Q42: mean and population std of the K scores (numpy fp64 as the reference routine);
+    UCB = mu - kappa sigma; kappa = 0 or K = 1 reduce to the mean."""
+    rng = np.random.default_rng(4)
+    for K in (1, 2, 5, 8):
+        for _ in range(200):
+            f = rng.normal(0, 2, K).astype(np.float32)
+            v, m, s = O.acquisition("ucb", f, kappa=1.5)
+            f64 = f.astype(np.float64)
+            assert abs(m - np.mean(f64)) <= 1e-6 * max(1.0, abs(np.mean(f64)))
+            assert abs(s - np.std(f64)) <= 1e-6 * max(1.0, np.std(f64))
+            assert abs(v - (np.mean(f64) - 1.5 * np.std(f64))) <= 2e-6 * max(1.0, abs(v))
+            assert O.acquisition("ucb", f, kappa=0.0)[0] == O.acquisition("mean", f)[0] == np.float32(m)
+            if K == 1:
+                assert s == 0.0 and v == f[0]
+
+
+def test_expected_improvement_closed_forms_and_bound():
+    """Q43: EI(mu = best) = sigma phi(0) = sigma / sqrt(2 pi); sigma = 0 gives max(best - mu, 0);
+    on a grid EI matches the exact fp64 formula (math.erfc, math.exp) within the A&S 7.1.26 error
+    bound plus fp32 rounding, is >= max(best - mu, 0) and decreases as mu grows."""
+    for sd in (0.1, 1.0, 7.5):
+        assert abs(O.expected_improvement(2.0, sd, 2.0) - sd / math.sqrt(2 * math.pi)) <= 3e-7 * sd
+    assert O.expected_improvement(1.0, 0.0, 3.0) == 2.0 and O.expected_improvement(4.0, 0.0, 3.0) == 0.0
+    prev = None
+    for mu in np.linspace(-6, 6, 241):
+        sd, best = 1.3, 0.4
+        got = O.expected_improvement(float(mu), sd, best)
+        d = best - float(np.float32(mu))
+        z = d / sd
+        Phi = 0.5 * math.erfc(-z / math.sqrt(2))
+        ref = d * Phi + sd * math.exp(-z * z / 2) / math.sqrt(2 * math.pi)
+        assert abs(got - ref) <= 2e-7 * (abs(d) + sd) + 1e-6 * abs(ref)
+        assert got >= max(d, 0.0) - 1e-6
+        if prev is not None:
+            assert got <= prev + 1e-7
+        prev = got
+    assert O.acquisition("ei", np.array([1.0, 3.0], np.float32), best=2.5)[0] == -O.expected_improvement(2.0, 1.0, 2.5)
