@@ -153,6 +153,8 @@ typedef struct {
     uint32_t *d_accept_bits;      /* nullable: [n_chains][(n_steps+31)/32], bit s = step s accepted */
     float *d_visited_E;           /* nullable: [n_chains][n_steps+1] energies of start + proposals */
     uint64_t *d_visited_idx;      /* nullable: [n_chains][n_steps+1] their global indices */
+    const struct at_acq_opts_s *acq;   /* nullable: the energy is the acquisition over acq->n_models
+                                          concatenated models (gbt_predict_acq) */
 } at_sa_opts;
 
 AT_API int sa_explore(at_space sp, at_gbt g,
@@ -242,7 +244,7 @@ AT_API int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t n_fe
  * with EI = d Phi(d / sigma) + sigma phi(d / sigma), d = best - mu (fp32, exp_det, A&S 7.1.26).
  * Writes d_score [n] and, when non-NULL, d_mean / d_std [n] (fp32). */
 enum { AT_ACQ_MEAN = 0, AT_ACQ_UCB = 1, AT_ACQ_EI = 2 };
-typedef struct {
+typedef struct at_acq_opts_s {
     int32_t n_models;             /* 1..8, divides the ensemble's tree count */
     int32_t kind;                 /* AT_ACQ_* */
     float kappa;                  /* UCB exploration weight */

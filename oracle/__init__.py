@@ -186,8 +186,14 @@ class OracleSpace:
 
     # -- SA / top-k / select -------------------------------------------------
     def sa_explore(self, ens, n_chains, n_steps, seed, round_, temps, chain_id_base=0,
-                   chain_workload=None, chain_idx=None):
-        g = ens.c()
+                   chain_workload=None, chain_idx=None, acq=None):
+        """acq: optional (kind, kappa, best) -- `ens` is then a list of K models and the energy is
+        their acquisition."""
+        if acq is not None:
+            arr = (Gbt * len(ens))(*[m.c() for m in ens])
+            g = arr
+        else:
+            g = ens.c()
         init = chain_idx is None
         cidx = np.zeros(n_chains, np.uint64) if init else np.array(chain_idx, dtype=np.uint64)
         cE = np.zeros(n_chains, np.float32)
@@ -197,8 +203,11 @@ class OracleSpace:
         vI = np.zeros((n_chains, n_steps + 1), np.uint64)
         temps = np.ascontiguousarray(temps, dtype=np.float32)
         cw = None if chain_workload is None else np.ascontiguousarray(chain_workload, dtype=np.uint16)
-        rc = lib().or_sa_explore(
-            C.byref(self.s), C.byref(g), C.c_int32(n_chains), C.c_int32(n_steps), C.c_uint64(seed),
+        head = (C.byref(self.s), C.byref(g)) if acq is None else \
+            (C.byref(self.s), g, C.c_int(len(ens)), C.c_int(ACQ[acq[0]]), C.c_float(acq[1]), C.c_float(acq[2]))
+        fn = lib().or_sa_explore if acq is None else lib().or_sa_explore_acq
+        rc = fn(
+            *head, C.c_int32(n_chains), C.c_int32(n_steps), C.c_uint64(seed),
             C.c_uint32(round_), C.c_uint32(chain_id_base), _p(temps, C.c_float),
             None if cw is None else _p(cw, C.c_uint16), C.c_int(1 if init else 0),
             _p(cidx, C.c_uint64), _p(cE, C.c_float), _p(acc, C.c_uint32), _p(vE, C.c_float), _p(vI, C.c_uint64))

@@ -531,21 +531,58 @@ int or_gbt_predict(const or_gbt *m, const float *X, int64_t n, int F, float *sco
     return 0;
 }
 
-static float score_idx(const or_space_set *s, const or_gbt *m, uint64_t gidx)
+/* SA energy of configuration gidx: f-hat(g(e, s)); with K bootstrap models, the acquisition of
+ * their scores (K = 1 with kind 0 is exactly f-hat) */
+typedef struct { const or_gbt *models; int K, kind; float kappa, best; } or_energy;
+
+float or_acquisition(int kind, int K, const float *f, float kappa, float best, float *mean_out, float *std_out);
+
+static float energy_idx(const or_space_set *s, const or_energy *en, uint64_t gidx)
 {
-    float x[OR_NFEAT];
+    float x[OR_NFEAT], f[64];
     or_features(s, &gidx, 1, x);
-    return or_gbt_score(m, x, NULL);
+    if (en->K == 1 && en->kind == 0) return or_gbt_score(&en->models[0], x, NULL);
+    for (int k = 0; k < en->K; ++k) f[k] = or_gbt_score(&en->models[k], x, NULL);
+    return or_acquisition(en->kind, en->K, f, en->kappa, en->best, NULL, NULL);
 }
 
 /* ======================================================================
  * Parallel simulated annealing (Alg. 1; O9, Q20-Q23)
  * ==================================================================== */
+static int sa_explore_energy(const or_space_set *s, const or_energy *en,
+                             int32_t n_chains, int32_t n_steps, uint64_t seed, uint32_t round,
+                             uint32_t chain_id_base, const float *temps, const uint16_t *chain_workload,
+                             int init, uint64_t *chain_idx, float *chain_energy,
+                             uint32_t *accept_bits, float *visited_E, uint64_t *visited_idx);
+
 int or_sa_explore(const or_space_set *s, const or_gbt *m,
                   int32_t n_chains, int32_t n_steps, uint64_t seed, uint32_t round,
                   uint32_t chain_id_base, const float *temps, const uint16_t *chain_workload,
                   int init, uint64_t *chain_idx, float *chain_energy,
                   uint32_t *accept_bits, float *visited_E, uint64_t *visited_idx)
+{
+    or_energy en = {m, 1, 0, 0.0f, 0.0f};
+    return sa_explore_energy(s, &en, n_chains, n_steps, seed, round, chain_id_base, temps, chain_workload, init,
+                             chain_idx, chain_energy, accept_bits, visited_E, visited_idx);
+}
+
+int or_sa_explore_acq(const or_space_set *s, const or_gbt *models, int K, int kind, float kappa, float best,
+                      int32_t n_chains, int32_t n_steps, uint64_t seed, uint32_t round,
+                      uint32_t chain_id_base, const float *temps, const uint16_t *chain_workload,
+                      int init, uint64_t *chain_idx, float *chain_energy,
+                      uint32_t *accept_bits, float *visited_E, uint64_t *visited_idx)
+{
+    if (K < 1 || K > 64) return -3;
+    or_energy en = {models, K, kind, kappa, best};
+    return sa_explore_energy(s, &en, n_chains, n_steps, seed, round, chain_id_base, temps, chain_workload, init,
+                             chain_idx, chain_energy, accept_bits, visited_E, visited_idx);
+}
+
+static int sa_explore_energy(const or_space_set *s, const or_energy *en,
+                             int32_t n_chains, int32_t n_steps, uint64_t seed, uint32_t round,
+                             uint32_t chain_id_base, const float *temps, const uint16_t *chain_workload,
+                             int init, uint64_t *chain_idx, float *chain_energy,
+                             uint32_t *accept_bits, float *visited_E, uint64_t *visited_idx)
 {
     int n_words = (n_steps + 31) / 32;
     for (int32_t c = 0; c < n_chains; ++c) {
@@ -563,7 +600,7 @@ int or_sa_explore(const or_space_set *s, const or_gbt *m,
             idx = chain_idx[c];
             if (idx < s->offset[w] || idx >= s->offset[w + 1]) return -2;
         }
-        float E = score_idx(s, m, idx);   /* energies recomputed under the current f-hat */
+        float E = energy_idx(s, en, idx);   /* energies recomputed under the current f-hat */
         visited_E[(size_t)c * (n_steps + 1)] = E;
         visited_idx[(size_t)c * (n_steps + 1)] = idx;
         if (accept_bits) for (int q = 0; q < n_words; ++q) accept_bits[(size_t)c * n_words + q] = 0;
@@ -583,7 +620,7 @@ int or_sa_explore(const or_space_set *s, const or_gbt *m,
                 choices[j] = v2;
                 idx2 = s->offset[w] + or_encode(sp, choices);
             }
-            float E2 = score_idx(s, m, idx2);
+            float E2 = energy_idx(s, en, idx2);
             float d = E2 - E;
             int accept = 0;
             if (d <= 0.0f) {

@@ -172,6 +172,12 @@ int or_bootstrap_indices(int64_t n, int32_t model, uint64_t seed, uint32_t round
 float or_expected_improvement(float mu, float sd, float best);
 float or_acquisition(int kind /* 0 mean, 1 UCB (mu - kappa sigma), 2 -EI */, int K, const float *f, float kappa,
                      float best, float *mean_out, float *std_out);
+/* SA whose energy is the acquisition over K models (kind 0 / K 1: plain f-hat, = or_sa_explore) */
+int or_sa_explore_acq(const or_space_set *s, const or_gbt *models, int K, int kind, float kappa, float best,
+                      int32_t n_chains, int32_t n_steps, uint64_t seed, uint32_t round,
+                      uint32_t chain_id_base, const float *temps, const uint16_t *chain_workload,
+                      int init, uint64_t *chain_idx, float *chain_energy,
+                      uint32_t *accept_bits, float *visited_E, uint64_t *visited_idx);
 int or_gbt_predict_acq(const or_gbt *models /* [K] */, int K, const float *X /* [n][F] */, int64_t n, int F,
                        int kind, float kappa, float best, float *score, float *mean, float *std);
 

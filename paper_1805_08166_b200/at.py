@@ -35,7 +35,7 @@ class SaOpts(C.Structure):
     _fields_ = [("n_chains", C.c_int32), ("n_steps", C.c_int32), ("k_out", C.c_int32), ("init", C.c_int32),
                 ("seed", C.c_uint64), ("round", C.c_uint32), ("chain_id_base", C.c_uint32),
                 ("d_temps", C.c_void_p), ("d_accept_bits", C.c_void_p), ("d_visited_E", C.c_void_p),
-                ("d_visited_idx", C.c_void_p)]
+                ("d_visited_idx", C.c_void_p), ("acq", C.c_void_p)]
 
 
 class SelectOpts(C.Structure):
@@ -249,8 +249,10 @@ class Gbt:
 
 
 def sa_explore(space: Space, gbt: Gbt, chain_idx, temps, *, seed, round_, k_out, chain_workload=None,
-               measured=None, init=False, chain_id_base=0, accept_bits=None, visited=False, stream=None):
-    """Run the SA kernel; returns dict(out_idx [nw][k], out_score, out_n [nw], chain_energy, ...)."""
+               measured=None, init=False, chain_id_base=0, accept_bits=None, visited=False, acq=None, stream=None):
+    """Run the SA kernel; returns dict(out_idx [nw][k], out_score, out_n [nw], chain_energy, ...).
+    acq: optional dict(n_models, kind, kappa, best, model_base): the energy is then the acquisition
+    over the n_models models concatenated in `gbt`."""
     import torch
     dev = chain_idx.device
     n_chains = chain_idx.numel()
@@ -259,6 +261,11 @@ def sa_explore(space: Space, gbt: Gbt, chain_idx, temps, *, seed, round_, k_out,
     o.n_chains, o.n_steps, o.k_out, o.init = n_chains, n_steps, k_out, 1 if init else 0
     o.seed, o.round, o.chain_id_base = seed, round_, chain_id_base
     o.d_temps = temps.data_ptr()
+    if acq is not None:
+        mb = list(acq.get("model_base", [])) + [0.0] * 8
+        ao = AcqOpts(acq["n_models"], ACQ[acq.get("kind", "ucb")], acq.get("kappa", 1.0), acq.get("best", 0.0),
+                     (C.c_float * 8)(*mb[:8]))
+        o.acq = C.cast(C.pointer(ao), C.c_void_p)
     res = {}
     if accept_bits is True:
         accept_bits = torch.zeros((n_chains, (n_steps + 31) // 32), dtype=torch.int32, device=dev)

@@ -200,6 +200,52 @@ __device__ __forceinline__ void ts_wait_resident(const TreeGeo &G, uint64_t *bar
     }
 }
 
+// K bootstrap models scored at once (gbt_predict_acq): per-model canonical sums, then the acquisition
+struct AcqArgs {
+    int K, kind;
+    float kappa, best;
+    float base[8];
+    float *mean, *std;
+};
+
+// Q43, the oracle's sequence of fp32 RN operations (exp = exp_det): EI below `best` of a minimised cost
+__device__ __forceinline__ float expected_improvement(float mu, float sd, float best)
+{
+    const float d = __fsub_rn(best, mu);
+    if (!(sd > 0.0f)) return d > 0.0f ? d : 0.0f;
+    const float z = __fdiv_rn(d, sd);
+    const float x = __fmul_rn(fabsf(z), 0.70710677f);
+    const float t = __fdiv_rn(1.0f, __fadd_rn(1.0f, __fmul_rn(0.3275911f, x)));
+    float poly = 1.061405429f;
+    poly = __fadd_rn(__fmul_rn(poly, t), -1.453152027f);
+    poly = __fadd_rn(__fmul_rn(poly, t), 1.421413741f);
+    poly = __fadd_rn(__fmul_rn(poly, t), -0.284496736f);
+    poly = __fadd_rn(__fmul_rn(poly, t), 0.254829592f);
+    poly = __fmul_rn(poly, t);
+    const float ec = __fmul_rn(poly, exp_det(-__fmul_rn(x, x)));
+    const float Phi = z >= 0.0f ? __fsub_rn(1.0f, __fmul_rn(0.5f, ec)) : __fmul_rn(0.5f, ec);
+    const float phi = __fmul_rn(0.3989423f, exp_det(__fmul_rn(__fmul_rn(-0.5f, z), z)));
+    return __fadd_rn(__fmul_rn(d, Phi), __fmul_rn(sd, phi));
+}
+
+// Q41/Q42: fp64 mean / population std in model order; mean, UCB (mu - kappa sigma) or -EI
+__device__ __forceinline__ float acquisition(const AcqArgs &Q, const float *f, int stride, float &mean, float &sd)
+{
+    double mu = 0.0, v = 0.0;
+    for (int k = 0; k < Q.K; ++k) mu = __dadd_rn(mu, (double)f[k * stride]);
+    mu = __ddiv_rn(mu, (double)Q.K);
+    for (int k = 0; k < Q.K; ++k) {
+        const double e = __dsub_rn((double)f[k * stride], mu);
+        v = __dadd_rn(v, __dmul_rn(e, e));
+    }
+    const double s = __dsqrt_rn(__ddiv_rn(v, (double)Q.K));
+    mean = (float)mu;
+    sd = (float)s;
+    if (Q.kind == 1) return (float)__dsub_rn(mu, __dmul_rn((double)Q.kappa, s));
+    if (Q.kind == 2) return -expected_improvement(mean, sd, Q.best);
+    return mean;
+}
+
 // canonical combination of the 32 partials of candidate `lane` (call from one warp)
 __device__ __forceinline__ float gbt_combine(const float *part, int lane, float base)
 {

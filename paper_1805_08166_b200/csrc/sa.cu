@@ -76,13 +76,15 @@ struct SaParams {
     float *vis_E;
     uint64_t *vis_idx;
     uint64_t *keys;   // [n_chains][n_steps+1]
+    AcqArgs Q;        // KM > 1: energy = acquisition over Q.K concatenated models
 };
 
 // shared-memory layout of sa_kernel: GRP groups of 32 chains
-template <int GRP>
+template <int GRP, int KM = 1>
 struct SaSmem {
     float tile[GRP][NFEAT * 32];
-    float part[GRP][32 * 32];
+    float part[GRP][KM * 32 * 32];
+    float fk[GRP][KM > 1 ? KM * 32 : 1];   // per-model energies (KM > 1)
     uint32_t ch[GRP][MAXKNOBS][32];
     int32_t w[GRP][32];
     uint64_t bar[2];
@@ -109,12 +111,27 @@ __device__ __forceinline__ void zero_relation(float (*tile)[NFEAT * 32], int lan
 // Block = GRP groups of 32 chains (lane = chain) x SA_NW warps.  Warp g owns group g's chain
 // state; every warp takes part in every group's feature phases and tree walk, so each tree byte
 // staged in shared memory serves 32 GRP chains.
-template <int GRP>
+template <int GRP, int KM>
 __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G)
 {
     extern __shared__ __align__(128) unsigned char smraw[];
-    SaSmem<GRP> &sm = *(SaSmem<GRP> *)smraw;
-    uint8_t *bufs = smraw + ((sizeof(SaSmem<GRP>) + 127) / 128) * 128;
+    SaSmem<GRP, KM> &sm = *(SaSmem<GRP, KM> *)smraw;
+    uint8_t *bufs = smraw + ((sizeof(SaSmem<GRP, KM>) + 127) / 128) * 128;
+    // the energy of group og's chains after a walk: f-hat, or the acquisition over the K models
+    auto energy = [&](int og, int lane) -> float {
+        if (KM == 1) return gbt_combine(sm.part[og], lane, P.base);
+        float mu, sd;
+        return acquisition(P.Q, &sm.fk[og][lane], 32, mu, sd);
+    };
+    auto fold_models = [&](int warp, int lane) {   // KM > 1: every warp (g, m) folds model m's partials
+        if (KM > 1) {
+            if (warp < GRP * P.Q.K) {
+                const int g = warp / P.Q.K, m = warp - g * P.Q.K;
+                sm.fk[g][m * 32 + lane] = gbt_combine(&sm.part[g][m * 1024], lane, P.Q.base[m]);
+            }
+            __syncthreads();
+        }
+    };
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int og = warp < GRP ? warp : 0;                  // the group whose state this warp owns
     const bool owner = warp < GRP;
@@ -186,11 +203,12 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     };
     features_phase();
     ts_wait_resident(G, sm.bar);
-    walk_pass<SA_NW, GRP>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp, &sm.part[0][0],
+    walk_pass<SA_NW, GRP, KM>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp, &sm.part[0][0],
                           nullptr, 0, 0, no_slots);
+    fold_models(warp, lane);
     if (!owner) zero_relation<GRP>(sm.tile, lane, warp);
     if (owner) {
-        E = gbt_combine(sm.part[og], lane, P.base);
+        E = energy(og, lane);
         if (live) {
             P.keys[(int64_t)c * per] = ((uint64_t)fkey(E) << 32) | (uint64_t)(idx - P.S->w[w].offset);
             if (P.vis_E) { P.vis_E[(int64_t)c * per] = E; P.vis_idx[(int64_t)c * per] = idx; }
@@ -232,14 +250,15 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
 #endif
-        walk_pass<SA_NW, GRP>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+        walk_pass<SA_NW, GRP, KM>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
                               &sm.part[0][0], nullptr, 0, 0, no_slots);
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_walk += t - t0; t0 = t; }
 #endif
+        fold_models(warp, lane);
         if (!owner) zero_relation<GRP>(sm.tile, lane, warp);
         if (owner) {
-            const float E2 = gbt_combine(sm.part[og], lane, P.base);
+            const float E2 = energy(og, lane);
             const float d = __fsub_rn(E2, E);
             bool acc = d <= 0.0f;
             if (!acc) {
@@ -282,10 +301,10 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #endif
 }
 
-template <int GRP>
+template <int GRP, int KM = 1>
 size_t sa_smem_bytes(const TreeGeo &G)
 {
-    return ((sizeof(SaSmem<GRP>) + 127) / 128) * 128 + 2 * (size_t)G.chunk_bytes;
+    return ((sizeof(SaSmem<GRP, KM>) + 127) / 128) * 128 + 2 * (size_t)G.chunk_bytes;
 }
 
 }  // namespace at
@@ -333,6 +352,17 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     P.vis_E = o->d_visited_E;
     P.vis_idx = o->d_visited_idx;
     P.keys = keys;
+    const at_acq_opts *acq = o->acq;
+    if (acq) {
+        if (acq->n_models < 1 || acq->n_models > 8 || g->n_trees % acq->n_models != 0)
+            return at::fail(AT_EINVAL, "sa_explore: acq needs 1 <= n_models <= 8 dividing n_trees");
+        if (acq->kind < AT_ACQ_MEAN || acq->kind > AT_ACQ_EI) return at::fail(AT_EINVAL, "sa_explore: bad acq kind");
+        P.Q.K = acq->n_models;
+        P.Q.kind = acq->kind;
+        P.Q.kappa = acq->kappa;
+        P.Q.best = acq->best;
+        for (int k = 0; k < 8; ++k) P.Q.base[k] = k < acq->n_models ? acq->model_base[k] : 0.0f;
+    }
     // two 32-chain groups per block when there are enough chains to fill the SMs twice over and the
     // ensemble streams (each streamed tree byte then serves 64 chains); otherwise one group
     static int n_sm = 0;
@@ -342,28 +372,32 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         AT_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
     constexpr size_t SMEM_MAX = 227 * 1024;
-    const at::TreeGeo G1 = at::make_geo(g);
+    at::TreeGeo G1 = at::make_geo(g);
     const size_t hdr2 = ((sizeof(at::SaSmem<2>) + 127) / 128) * 128;
     const at::TreeGeo G2 = at::make_geo(g, (uint32_t)((SMEM_MAX - hdr2) / 2));
-    const bool use2 = !G1.resident && o->n_chains >= 2 * 64 * n_sm && at::sa_smem_bytes<2>(G2) <= SMEM_MAX;
-    const at::TreeGeo G = use2 ? G2 : G1;
-    const size_t smem = use2 ? at::sa_smem_bytes<2>(G) : at::sa_smem_bytes<1>(G);
-    if (smem > SMEM_MAX) return at::fail(AT_EUNSUPPORTED, "sa_explore: shared memory budget exceeded");
-    static size_t attr1 = 0, attr2 = 0;
-    if (!use2 && smem > attr1) {
-        AT_CUDA_TRY(cudaFuncSetAttribute(at::sa_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr1 = smem;
+    const bool use2 = !acq && !G1.resident && o->n_chains >= 2 * 64 * n_sm && at::sa_smem_bytes<2>(G2) <= SMEM_MAX;
+    if (acq) {   // K models: 32 KB tree buffers leave room for the per-model partials
+        G1 = at::make_geo(g, 32 * 1024);
+        G1.Tm = g->n_trees / acq->n_models;
     }
-    if (use2 && smem > attr2) {
-        AT_CUDA_TRY(cudaFuncSetAttribute(at::sa_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr2 = smem;
+    const at::TreeGeo G = use2 ? G2 : G1;
+    const size_t smem = acq ? at::sa_smem_bytes<1, 8>(G) : use2 ? at::sa_smem_bytes<2>(G) : at::sa_smem_bytes<1>(G);
+    if (smem > SMEM_MAX) return at::fail(AT_EUNSUPPORTED, "sa_explore: shared memory budget exceeded");
+    const void *kern = acq ? (const void *)at::sa_kernel<1, 8>
+                     : use2 ? (const void *)at::sa_kernel<2, 1> : (const void *)at::sa_kernel<1, 1>;
+    static size_t attr[3] = {0, 0, 0};
+    const int ai = acq ? 2 : use2 ? 1 : 0;
+    if (smem > attr[ai]) {
+        AT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[ai] = smem;
     }
     {
         at::ProfScope ps(AT_K_SA, s);
         const int cpb = use2 ? 64 : 32;
         const unsigned blocks = (unsigned)((o->n_chains + cpb - 1) / cpb);
-        if (use2) at::sa_kernel<2><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
-        else at::sa_kernel<1><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
+        if (acq) at::sa_kernel<1, 8><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
+        else if (use2) at::sa_kernel<2, 1><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
+        else at::sa_kernel<1, 1><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
         at::note_launch();
         AT_LAUNCH_CHECK("sa_kernel");
     }

@@ -597,6 +597,29 @@ def test_bootstrap_ensemble_pipeline_matches_oracle(at):
     assert_bits_equal(sd.cpu().numpy(), rsd, "std")
 
 
+@pytest.mark.parametrize("kind,K,T,D", [("ucb", 3, 40, 6), ("ei", 5, 33, 5), ("mean", 2, 64, 8)])
+def test_sa_acquisition_energy_matches_oracle(at, kind, K, T, D):
+    """SA whose energy is the acquisition over K bootstrap-style models: proposals,
+    energies, accept bits, final states and top-k bit for bit against the oracle."""
+    ens = [synth.ensemble(T, D, seed=90 + k) for k in range(K)]
+    bases = [0.1 * k for k in range(K)]
+    steps, chains = 25, 70
+    temps = synth.temperatures(steps, synth.energy_scale(T))
+    osp = O.OracleSpace([O.workload(**synth.CFG2B)])
+    om = [O.OracleGbt(e["feat"], e["thresh"], e["leaf"], base=b) for e, b in zip(ens, bases)]
+    r = osp.sa_explore(om, chains, steps, 1805, 4, temps, acq=(kind, 0.7, -0.2))
+    otop = osp.topk(r["visited_E"], r["visited_idx"], 64)
+    gs = [at.Gbt(e["feat"], e["thresh"], e["leaf"], base=b) for e, b in zip(ens, bases)]
+    cat = gs[0]
+    for g in gs[1:]:
+        cat = cat.concat(g)
+    res = at.sa_explore(at.Space([synth.CFG2B]), cat, u64(np.zeros(chains, np.uint64)), dev(temps), seed=1805,
+                        round_=4, k_out=64, init=True, accept_bits=True, visited=True,
+                        acq=dict(n_models=K, kind=kind, kappa=0.7, best=-0.2, model_base=bases))
+    torch.cuda.synchronize()
+    compare_sa(r, otop, res)
+
+
 def test_fit_errors(at):
     with pytest.raises(at.ATError) as e:
         at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 0, torch.zeros(4, device="cuda"),

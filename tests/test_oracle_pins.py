@@ -713,3 +713,16 @@ def test_expected_improvement_closed_forms_and_bound():
             assert got <= prev + 1e-7
         prev = got
     assert O.acquisition("ei", np.array([1.0, 3.0], np.float32), best=2.5)[0] == -O.expected_improvement(2.0, 1.0, 2.5)
+
+
+def test_sa_acquisition_over_identical_models_is_plain_sa():
+    """K copies of one model have sigma = 0 and an fp64 mean equal to the model's fp32 score, so SA
+    with the UCB energy over them replays plain SA exactly (P:208-215 reduces to f-hat)."""
+    osp = space(synth.CFG2B)
+    e = synth.ensemble(30, 5, seed=8)
+    m = O.OracleGbt(e["feat"], e["thresh"], e["leaf"], base=0.3)
+    temps = synth.temperatures(15, 0.2)
+    a = osp.sa_explore(m, 20, 15, 1805, 1, temps)
+    b = osp.sa_explore([m, m, m], 20, 15, 1805, 1, temps, acq=("ucb", 2.0, 0.0))
+    for k in ("visited_idx", "visited_E", "accept_bits", "chain_idx"):
+        assert np.array_equal(a[k], b[k]), k
