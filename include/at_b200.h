@@ -109,6 +109,15 @@ AT_API int space_destroy(at_space sp);
 AT_API int features_extract(at_space sp, const uint64_t *d_idx, int64_t n, float *d_feat, int64_t ld,
                      void *stream);
 
+/* features_knobs -- the configuration representation "directly use configuration s as the
+ * model's input" (reading Q44), the baseline the loop-context features are compared
+ * with: per knob in knob order a split knob's ordered factor tuple (outer factor first), the
+ * reorder knob's permutation index, the unroll knob's max-step value, the vectorize flag, as fp32
+ * columns of d_feat SoA [AT_KNOB_FEATURES][ld] (zero padded).  Models over it are created with
+ * n_features = AT_KNOB_FEATURES and scored by gbt_predict. */
+#define AT_KNOB_FEATURES 32
+AT_API int features_knobs(at_space sp, const uint64_t *d_idx, int64_t n, float *d_feat, int64_t ld, void *stream);
+
 /* ------------------------------------------------------------------ GBT model
  * Complete binary trees of depth D in heap layout (children 2i+1, 2i+2); node i of
  * tree t: feature feat[t][i], threshold thresh[t][i]; go left iff x[feat] < thresh

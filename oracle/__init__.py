@@ -185,6 +185,15 @@ class OracleSpace:
         return out
 
     # -- SA / top-k / select -------------------------------------------------
+    def features_knobs(self, idx):
+        """Configuration features (Q44): [n][32] fp32."""
+        idx = np.ascontiguousarray(idx, dtype=np.uint64)
+        out = np.zeros((len(idx), 32), np.float32)
+        rc = lib().or_features_knobs(C.byref(self.s), _p(idx, C.c_uint64), C.c_int64(len(idx)), _p(out, C.c_float))
+        if rc != 0:
+            raise ValueError(f"oracle features_knobs rc={rc}")
+        return out
+
     def sa_explore(self, ens, n_chains, n_steps, seed, round_, temps, chain_id_base=0,
                    chain_workload=None, chain_idx=None, acq=None):
         """acq: optional (kind, kappa, best) -- `ens` is then a list of K models and the energy is

@@ -1140,3 +1140,34 @@ int or_gbt_predict_acq(const or_gbt *models, int K, const float *X, int64_t n, i
     }
     return 0;
 }
+
+/* ======================================================================
+ * Configuration features ("directly use configuration s as the model's input";
+ * reading Q44): per knob in knob order, a split knob's ordered factor tuple (outer first), the
+ * reorder knob's permutation index, the unroll knob's max-step value, the vectorize flag; as
+ * fp32 columns, zero padded to OR_NKNOBF.
+ * ==================================================================== */
+int or_features_knobs(const or_space_set *s, const uint64_t *idx, int64_t n, float *out /* [n][OR_NKNOBF] */)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        int w = or_space_set_find(s, idx[i]);
+        if (w < 0) return -2;
+        const or_space *sp = &s->sp[w];
+        int choices[OR_MAXKNOBS];
+        or_decode(sp, idx[i] - s->offset[w], choices);
+        float *x = out + (size_t)i * OR_NKNOBF;
+        for (int c = 0; c < OR_NKNOBF; ++c) x[c] = 0.0f;
+        int c = 0;
+        for (int j = 0; j < sp->n_knobs; ++j) {
+            if (sp->knob_kind[j] == 0) {
+                int L = sp->axis_levels[sp->knob_axis[j]];
+                for (int l = 0; l < L; ++l) x[c++] = (float)sp->fact[j][(size_t)choices[j] * L + l];
+            } else if (sp->knob_kind[j] == 2) {
+                x[c++] = (float)sp->unroll_vals[choices[j]];
+            } else {
+                x[c++] = (float)choices[j];
+            }
+        }
+    }
+    return 0;
+}

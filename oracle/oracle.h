@@ -27,6 +27,7 @@ extern "C" {
 #define OR_MAXLOOPS 18     /* T_CONV nest depth (Q3) */
 #define OR_MAXKNOBS 9
 #define OR_MAXW 16         /* workloads in one union space */
+#define OR_NKNOBF 32       /* configuration-feature columns (Q44) */
 
 /* workload e (P:45 matmul, Table 1 P:276-296 conv2d, MobileNet depthwise Q30) */
 typedef struct {
@@ -166,6 +167,9 @@ int or_reg_gradients(const float *cost, const float *pred, int64_t n, int64_t *g
  * base = a.base + b.base (fp32).  Arrays sized for (a.n_trees + b.n_trees) trees of depth
  * max(a.depth, b.depth). */
 int or_gbt_concat(const or_gbt *a, const or_gbt *b, uint16_t *feat, float *thresh, float *leaf, float *base);
+
+/* ---- configuration features, the knob representation of P:229-232 (Q44) ---- */
+int or_features_knobs(const or_space_set *s, const uint64_t *idx, int64_t n, float *out /* [n][OR_NKNOBF] */);
 
 /* ---- bootstrap uncertainty, EI / UCB acquisition (Q40-Q43) ---- */
 int or_bootstrap_indices(int64_t n, int32_t model, uint64_t seed, uint32_t round, int64_t *idx);

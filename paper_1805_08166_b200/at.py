@@ -53,6 +53,7 @@ class FitOpts(C.Structure):
                 ("d_hist0_out", C.c_void_p), ("objective", C.c_int32), ("d_base_margin", C.c_void_p)]
 
 OBJECTIVES = {"rank": 0, "reg": 1}
+KNOB_FEATURES = 32   # AT_KNOB_FEATURES
 ACQ = {"mean": 0, "ucb": 1, "ei": 2}   # P:208-215 acquisition over bootstrap models
 
 
@@ -79,6 +80,7 @@ def lib() -> C.CDLL:
         L.space_info.argtypes = [vp, vp, vp, vp, vp, vp]
         L.space_destroy.argtypes = [vp]
         L.features_extract.argtypes = [vp, vp, i64, vp, i64, vp]
+        L.features_knobs.argtypes = [vp, vp, i64, vp, i64, vp]
         L.gbt_create.argtypes = [i32, i32, i32, vp, vp, vp, C.c_float, C.POINTER(vp)]
         L.gbt_info.argtypes = [vp, vp, vp, vp]
         L.gbt_export.argtypes = [vp, vp, vp, vp, vp]
@@ -174,6 +176,17 @@ class Space:
         if out is None:
             out = torch.empty((NFEAT, ld), dtype=torch.float32, device=idx.device)
         _check(lib().features_extract(self.h, _u64(idx), n, _ptr(out), ld, _stream(stream)))
+        return out
+
+    def knob_features(self, idx, out=None, ld=None, stream=None):
+        """Configuration features: idx int64 CUDA tensor -> SoA [32][ld] float32."""
+        import torch
+        n = idx.numel()
+        if ld is None:
+            ld = max(4, (n + 127) // 128 * 128)
+        if out is None:
+            out = torch.empty((KNOB_FEATURES, ld), dtype=torch.float32, device=idx.device)
+        _check(lib().features_knobs(self.h, _u64(idx), n, _ptr(out), ld, _stream(stream)))
         return out
 
 

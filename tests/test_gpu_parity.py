@@ -620,6 +620,28 @@ def test_sa_acquisition_energy_matches_oracle(at, kind, K, T, D):
     compare_sa(r, otop, res)
 
 
+@pytest.mark.parametrize("wls", [[synth.MATMUL_512], synth.ALL_RESNET, synth.ALL_DW,
+                                 [synth.MATMUL_8, synth.CONV_TINY, synth.ALL_DW[8]]])
+def test_knob_features_match_oracle(at, wls):
+    """Configuration features (Q44) bit for bit, and a model over them (fitted on the
+    knob representation, n_features = 32) scores identically on both sides."""
+    osp = O.OracleSpace([O.workload(**w) for w in wls])
+    idx = synth.uniform_indices(osp.size(), 3001, seed=17)
+    sp = at.Space(wls)
+    Xg = sp.knob_features(u64(idx))
+    ref = osp.features_knobs(idx)
+    assert_bits_equal(Xg[:, :3001].cpu().numpy().T.copy(), ref, "knob features")
+    c = synth.labels(osp.features(idx), seed=5)   # costs from the loop-context view, model on the knob view
+    key = np.zeros(3001, np.uint16)
+    fref = O.fit_hist(ref, c, key, n_trees=4, depth=5)
+    g = at.gbt_fit_hist(Xg, 3001, dev(c), dev(key.view(np.int16)), n_trees=4, depth=5)
+    ex = g.export()
+    for k in ("feat", "thresh", "leaf"):
+        assert_bits_equal(ex[k], fref[k], f"knob-feature model {k}")
+    s = g.predict(Xg, 3001).cpu().numpy()
+    assert_bits_equal(s, O.OracleGbt(fref["feat"], fref["thresh"], fref["leaf"]).predict(ref), "scores")
+
+
 def test_fit_errors(at):
     with pytest.raises(at.ATError) as e:
         at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 0, torch.zeros(4, device="cuda"),

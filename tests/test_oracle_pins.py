@@ -726,3 +726,39 @@ def test_sa_acquisition_over_identical_models_is_plain_sa():
     b = osp.sa_explore([m, m, m], 20, 15, 1805, 1, temps, acq=("ucb", 2.0, 0.0))
     for k in ("visited_idx", "visited_E", "accept_bits", "chain_idx"):
         assert np.array_equal(a[k], b[k]), k
+
+
+# ---------------------------------------------------------------- §8(f): configuration features (Q44)
+def test_knob_features_factor_products_and_ends():
+    """Q44: each split knob's columns are an ordered factorization of its axis extent (product =
+    extent); index 0 is the first lexicographic tuple (1, ..., 1, extent) with the other knobs at
+    their first value; index |S| - 1 is (extent, 1, ..., 1) with every other knob at its last."""
+    cases = [(synth.MATMUL_512, [3, 3, 2], [512, 512, 512], [("u", [1, 2, 4, 8, 16])]),
+             (synth.CFG2A, [4, 4, 4, 2, 2, 2], [128, 28, 28, 128, 3, 3], [("p", 5), ("u", [0, 512, 1500]), ("v", 1)]),
+             (synth.ALL_DW[3], [4, 4, 4, 2, 2], [128, 28, 28, 3, 3], [("p", 5), ("u", [0, 512, 1500]), ("v", 1)])]
+    for wl, levels, ext, rest in cases:
+        osp = space(wl)
+        n_split = sum(levels)
+        X = osp.features_knobs(synth.uniform_indices(osp.size(), 500, seed=3))
+        c = 0
+        for L, e in zip(levels, ext):
+            assert np.all(np.prod(X[:, c:c + L].astype(np.int64), axis=1) == e)
+            c += L
+        assert np.all(X[:, n_split + len(rest):] == 0)
+        first, last = osp.features_knobs([0, osp.size() - 1])
+        c = 0
+        for L, e in zip(levels, ext):
+            assert first[c:c + L].tolist() == [1] * (L - 1) + [e]
+            assert last[c:c + L].tolist() == [e] + [1] * (L - 1)
+            c += L
+        for k, (kind, v) in enumerate(rest):
+            assert first[c + k] == (v[0] if kind == "u" else 0)
+            assert last[c + k] == (v[-1] if kind == "u" else v)
+
+
+def test_knob_features_identify_the_configuration():
+    """The configuration representation is one-to-one: all 151,250 configurations of the config-1
+    space have distinct knob-feature rows (brute force)."""
+    osp = space(synth.MATMUL_512)
+    X = osp.features_knobs(np.arange(osp.size(), dtype=np.uint64))
+    assert len(np.unique(X, axis=0)) == osp.size() == 151250
