@@ -128,14 +128,19 @@ __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf,
                                            int lane, int warp, float (&p)[GRP][KM][32 / NW], uint8_t *__restrict__ slots,
                                            int64_t slot_ld, int64_t cand0, const bool (&cand_ok)[GRP])
 {
-    constexpr int NBMAX = GRP == 1 ? 4 : 2;
+    constexpr int NBMAX = GRP == 1 ? (KM == 1 ? 6 : 4) : 2;
     const int c0 = k * G.CH;
     const int c1 = min(c0 + G.CH, G.T);
     int t0 = c0 + ((warp - c0) % NW + NW) % NW;
     for (; t0 + (NBMAX - 1) * NW < c1; t0 += NBMAX * NW)
         walk_batch<NW, GRP, NBMAX, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
-    const int rest = t0 < c1 ? (c1 - 1 - t0) / NW + 1 : 0;   // warp-uniform
-    if (NBMAX == 4 && rest == 3)
+    int rest = t0 < c1 ? (c1 - 1 - t0) / NW + 1 : 0;   // warp-uniform, < NBMAX
+    if (NBMAX > 4 && rest >= 4) {
+        walk_batch<NW, GRP, 4, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        t0 += 4 * NW;
+        rest -= 4;
+    }
+    if (NBMAX >= 4 && rest == 3)
         walk_batch<NW, GRP, 3, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
     else if (rest >= 2)
         walk_batch<NW, GRP, 2, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);

@@ -372,7 +372,10 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         AT_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
     constexpr size_t SMEM_MAX = 227 * 1024;
-    at::TreeGeo G1 = at::make_geo(g);
+    // one group: the tree buffers take all the shared memory the group's state leaves (bigger chunks:
+    // more trees per warp per chunk, more independent walks in flight, fewer chunk barriers)
+    const size_t hdr1 = ((sizeof(at::SaSmem<1>) + 127) / 128) * 128;
+    at::TreeGeo G1 = at::make_geo(g, (uint32_t)((SMEM_MAX - hdr1) / 2));
     const size_t hdr2 = ((sizeof(at::SaSmem<2>) + 127) / 128) * 128;
     const at::TreeGeo G2 = at::make_geo(g, (uint32_t)((SMEM_MAX - hdr2) / 2));
     const bool use2 = !acq && !G1.resident && o->n_chains >= 2 * 64 * n_sm && at::sa_smem_bytes<2>(G2) <= SMEM_MAX;
