@@ -180,6 +180,8 @@ struct at_gbt_s {
     float base;
     uint2 *d_nodes;               // [t_pad][2^D-1] {feature, threshold bits}
     float *d_leaf;                // [t_pad][2^D]
+    cudaStream_t last;            // stream of the last enqueued use: gbt_destroy frees stream-ordered
+                                  // there (no device-wide sync from cudaFree inside a tuning loop)
 };
 
 namespace at {

@@ -1573,10 +1573,11 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         gm->base = 0.0f;
         gm->d_nodes = nullptr;
         gm->d_leaf = nullptr;
-        if (cudaMalloc(&gm->d_nodes, sizeof(uint2) * (size_t)gm->t_pad * n_int) != cudaSuccess ||
-            cudaMalloc(&gm->d_leaf, sizeof(float) * (size_t)gm->t_pad * n_leaf) != cudaSuccess) {
+        gm->last = s;
+        if (cudaMallocAsync((void **)&gm->d_nodes, sizeof(uint2) * (size_t)gm->t_pad * n_int, s) != cudaSuccess ||
+            cudaMallocAsync((void **)&gm->d_leaf, sizeof(float) * (size_t)gm->t_pad * n_leaf, s) != cudaSuccess) {
             cudaGetLastError();
-            cudaFree(gm->d_nodes);
+            cudaFreeAsync(gm->d_nodes, s);
             delete gm;
             return fail(AT_ENOMEM, "gbt_fit_hist: model allocation failed");
         }

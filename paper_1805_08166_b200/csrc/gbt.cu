@@ -176,20 +176,21 @@ int gbt_create(int32_t n_trees, int32_t depth, int32_t n_features, const uint16_
     g->base = base;
     g->d_nodes = nullptr;
     g->d_leaf = nullptr;
-    if (cudaMalloc(&g->d_nodes, (size_t)g->t_pad * ni * sizeof(uint2)) != cudaSuccess ||
-        cudaMalloc(&g->d_leaf, (size_t)g->t_pad * nl * sizeof(float)) != cudaSuccess ||
-        cudaMemset(g->d_nodes, 0, (size_t)g->t_pad * ni * sizeof(uint2)) != cudaSuccess ||
-        cudaMemset(g->d_leaf, 0, (size_t)g->t_pad * nl * sizeof(float)) != cudaSuccess) {
+    g->last = 0;
+    if (cudaMallocAsync((void **)&g->d_nodes, (size_t)g->t_pad * ni * sizeof(uint2), 0) != cudaSuccess ||
+        cudaMallocAsync((void **)&g->d_leaf, (size_t)g->t_pad * nl * sizeof(float), 0) != cudaSuccess ||
+        cudaMemsetAsync(g->d_nodes, 0, (size_t)g->t_pad * ni * sizeof(uint2), 0) != cudaSuccess ||
+        cudaMemsetAsync(g->d_leaf, 0, (size_t)g->t_pad * nl * sizeof(float), 0) != cudaSuccess) {
         cudaGetLastError();
-        cudaFree(g->d_nodes);
+        cudaFreeAsync(g->d_nodes, 0);
         delete g;
         return at::fail(AT_ENOMEM, "gbt_create: device allocation failed");
     }
     cudaError_t e1 = cudaMemcpy(g->d_nodes, nodes.data(), nodes.size() * sizeof(uint2), cudaMemcpyHostToDevice);
     cudaError_t e2 = cudaMemcpy(g->d_leaf, leaf, (size_t)n_trees * nl * sizeof(float), cudaMemcpyHostToDevice);
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
-        cudaFree(g->d_nodes);
-        cudaFree(g->d_leaf);
+        cudaFreeAsync(g->d_nodes, 0);
+        cudaFreeAsync(g->d_leaf, 0);
         delete g;
         return at::cuda_fail(e1 != cudaSuccess ? e1 : e2, "gbt_create upload");
     }
@@ -209,6 +210,7 @@ int gbt_info(at_gbt g, int32_t *n_trees, int32_t *depth, int32_t *n_features)
 int gbt_export(at_gbt g, uint16_t *feat, float *thresh, float *leaf, float *base)
 {
     if (!g) return at::fail(AT_EINVAL, "gbt_export: null model");
+    AT_CUDA_TRY(cudaStreamSynchronize(g->last));   // the fit that wrote it may run on a non-blocking stream
     const int64_t ni = (1 << g->depth) - 1, nl = 1 << g->depth;
     if (feat || thresh) {
         std::vector<uint2> nodes((size_t)g->n_trees * ni);
@@ -257,8 +259,9 @@ int gbt_concat(at_gbt a, at_gbt b, at_gbt *out)
 int gbt_destroy(at_gbt g)
 {
     if (!g) return AT_OK;
-    cudaFree(g->d_nodes);
-    cudaFree(g->d_leaf);
+    // stream-ordered after the model's last enqueued use (predict / SA / fit output)
+    cudaFreeAsync(g->d_nodes, g->last);
+    cudaFreeAsync(g->d_leaf, g->last);
     delete g;
     return AT_OK;
 }
@@ -273,6 +276,7 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
                           const AcqArgs *acq, void *stream)
 {
     cudaStream_t s = (cudaStream_t)stream;
+    g->last = s;
     const int KM = acq ? 8 : 1;
     TreeGeo G = make_geo(g, acq ? 32 * 1024 : TREE_BUF_BYTES);
     if (acq) G.Tm = g->n_trees / acq->K;

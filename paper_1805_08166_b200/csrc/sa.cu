@@ -326,6 +326,7 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     if ((o->d_visited_E == nullptr) != (o->d_visited_idx == nullptr))
         return at::fail(AT_EINVAL, "sa_explore: d_visited_E and d_visited_idx go together");
     cudaStream_t s = (cudaStream_t)stream;
+    g->last = s;
     const int64_t per = (int64_t)o->n_steps + 1;
     const int64_t n_keys = (int64_t)o->n_chains * per;
     const size_t key_bytes = ((size_t)n_keys * sizeof(uint64_t) + 255) / 256 * 256;
