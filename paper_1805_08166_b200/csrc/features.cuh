@@ -414,19 +414,18 @@ __device__ __forceinline__ void sa_row(const WlDev &W, const SaLowering &L, int 
     }
 }
 
-// sa_kernel's fused row item: the extents of every loop straight from the knob vector (one
-// factor-table load per loop, no shared lowering phase), then row k exactly as sa_row, and the
+// sa_kernel's fused row item: the extents of every loop (kept in shared memory by the owner warp,
+// sa_extents, after each move), then row k exactly as sa_row, and the
 // row's relation contributions deposited at once: row k qualifies for threshold 2^t iff
 // T_k < 2^t, i.e. iff t >= bitlen(T_k), so it raises slot max(1, bitlen(T_k)) of R[b][p] to its
 // Z (shared atomic max on the fp32 bits: every Z is > 0, and the slots start at +0); a prefix
 // max over t (relation_prefix) then gives R_t = max_{k : T_k < 2^t} Z_k, 0 for an empty set.
+// the extents of every loop of template TMPL for knob vector ch (one factor-table load per loop)
 template <int TMPL>
-__device__ __forceinline__ void sa_row_rel(const WlDev &W, const uint16_t *__restrict__ fact, const uint32_t *ch,
-                                           int k, int lane, float *tile)
+__device__ __forceinline__ void sa_extents(const WlDev &W, const uint16_t *__restrict__ fact, const uint32_t *ch,
+                                           uint32_t *ext /* [MAXLOOPS][32] at the lane */)
 {
     constexpr int NL = Tmpl<TMPL>::NL;
-    constexpr int NA = Tmpl<TMPL>::NA;
-    if (k >= NL) return;
     const uint32_t p = TMPL == 1 ? ch[6] : TMPL == 2 ? ch[5] : 0u;
     uint32_t ev[NL];
 #pragma unroll
@@ -439,6 +438,21 @@ __device__ __forceinline__ void sa_row_rel(const WlDev &W, const uint16_t *__res
         for (int q = 0; q < 6; ++q) if (q == axis) cha = ch[q];
         ev[l] = __ldg(fact + W.fact_off[axis] + cha * (uint32_t)Lv + level);
     }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) ext[l * 32] = ev[l];
+}
+
+template <int TMPL>
+__device__ __forceinline__ void sa_row_rel(const WlDev &W, const uint32_t *ext /* [l * 32] at the lane */,
+                                           const uint32_t *ch, int k, int lane, float *tile)
+{
+    constexpr int NL = Tmpl<TMPL>::NL;
+    constexpr int NA = Tmpl<TMPL>::NA;
+    if (k >= NL) return;
+    const uint32_t p = TMPL == 1 ? ch[6] : TMPL == 2 ? ch[5] : 0u;
+    uint32_t ev[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) ev[l] = ext[l * 32];
     const uint32_t unroll_max = W.unroll_vals[TMPL == 0 ? ch[3] : TMPL == 1 ? ch[7] : ch[6]];
     const uint32_t vec = TMPL == 0 ? 0u : TMPL == 1 ? ch[8] : ch[7];
     uint32_t A[NA];

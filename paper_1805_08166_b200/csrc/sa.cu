@@ -86,17 +86,27 @@ struct SaSmem {
     float part[GRP][KM * 32 * 32];
     float fk[GRP][KM > 1 ? KM * 32 : 1];   // per-model energies (KM > 1)
     uint32_t ch[GRP][MAXKNOBS][32];
+    uint32_t ext[GRP][MAXLOOPS][32];      // loop extents of each chain's current proposal (owner-written)
     int32_t w[GRP][32];
     uint64_t bar[2];
 };
 
-__device__ __forceinline__ void sa_row_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, int k, int lane,
+__device__ __forceinline__ void sa_row_any(const WlDev &W, const uint32_t *ext, const uint32_t *ch, int k, int lane,
                                            float *tile)
 {
     switch (W.tmpl) {
-    case 0: sa_row_rel<0>(W, fact, ch, k, lane, tile); break;
-    case 1: sa_row_rel<1>(W, fact, ch, k, lane, tile); break;
-    default: sa_row_rel<2>(W, fact, ch, k, lane, tile); break;
+    case 0: sa_row_rel<0>(W, ext, ch, k, lane, tile); break;
+    case 1: sa_row_rel<1>(W, ext, ch, k, lane, tile); break;
+    default: sa_row_rel<2>(W, ext, ch, k, lane, tile); break;
+    }
+}
+
+__device__ __forceinline__ void sa_extents_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, uint32_t *ext)
+{
+    switch (W.tmpl) {
+    case 0: sa_extents<0>(W, fact, ch, ext); break;
+    case 1: sa_extents<1>(W, fact, ch, ext); break;
+    default: sa_extents<2>(W, fact, ch, ext); break;
     }
 }
 
@@ -166,6 +176,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         decode_any(W, (uint32_t)(idx - W.offset), ch);
 #pragma unroll
         for (int j = 0; j < MAXKNOBS; ++j) sm.ch[og][j][lane] = ch[j];
+        sa_extents_any(W, P.fact, ch, &sm.ext[og][0][lane]);
         sm.w[og][lane] = w;
         zero_cols_any(W.tmpl, sm.tile[og], lane);
     } else {
@@ -188,7 +199,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
             uint32_t chl[MAXKNOBS];
 #pragma unroll
             for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[g][j][lane];
-            sa_row_any(P.S->w[sm.w[g][lane]], P.fact, chl, k, lane, sm.tile[g]);
+            sa_row_any(P.S->w[sm.w[g][lane]], &sm.ext[g][0][lane], chl, k, lane, sm.tile[g]);
         }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
@@ -241,6 +252,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == j) sm.ch[og][q][lane] = v2;
             }
+            sa_extents_any(W, P.fact, ch, &sm.ext[og][0][lane]);   // the proposal's loop extents
         }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
