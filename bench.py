@@ -74,6 +74,11 @@ class Clocks:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                        "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
+            # nvidia-smi needs ~0.1-0.5 s before its first sample: wait for it, so the (short) timed
+            # region that follows is actually sampled
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
+                time.sleep(0.01)
         except Exception:
             self.p = None
         return self

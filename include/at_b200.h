@@ -14,6 +14,14 @@
  *                     (1-eps)b-subset" + "randomly sample eps b" ...... Alg. 1, Eq. 3
  *   gbt_fit_hist      "update f-hat using D" with the rank loss ....... Alg. 1, Eq. 2
  *
+ * and the SURVEY §8(f) widenings, on the same kernels:
+ *   gbt_fit_hist objective / d_base_margin   regression loss; f_local fitted on top of
+ *                                            f_global (transfer learning, Eq. 4)
+ *   gbt_concat        f_global + f_local as one ensemble ......... Eq. 4
+ *   bootstrap_resample, gbt_predict_acq, at_sa_opts.acq
+ *                     bootstrap uncertainty, EI / UCB acquisition .. P:208-215
+ *   features_knobs    the configuration representation s .......... P:229-232
+ *
  * Conventions
  *  - Every pointer named d_* is DEVICE memory owned by the caller; every other
  *    pointer is host memory owned by the caller.  The library never retains a

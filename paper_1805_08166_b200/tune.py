@@ -9,7 +9,12 @@
     s* <- history best
 
 Chains persist across rounds.  Before the first refit f-hat is the caller's initial model
-(e.g. a transferred / synthetic ensemble).  The measurement f is a callable on global indices that
+(e.g. a transferred / synthetic ensemble).  Options:
+  objective="reg"        the regression loss sum (f - c)^2 instead of Eq. 2 (P:175);
+  global_model=g         transfer learning, Eq. 4: f-hat = f_global + f_local, the local
+                         fit on top of f_global's scores (base margin), scored as one ensemble;
+  n_bootstrap=K, acq     K models on bootstrap multisets of D and an EI / UCB acquisition as the
+                         SA energy.  The measurement f is a callable on global indices that
 returns costs (the hardware run of P:63); features of the measured configurations come from
 features_extract.  Everything numeric runs in the library's kernels; this module only sequences
 the calls and keeps the database.  Single GPU (the multi-GPU pieces are in dist.py / bench.py).
@@ -33,6 +38,10 @@ class TuneConfig:
     depth: int = 6
     t_ratio: float = 0.05        # geometric temperature schedule T0 -> t_ratio T0 (reading Q21)
     seed: int = 1805
+    objective: str = "rank"      # "rank" (Eq. 2) or "reg"
+    n_bootstrap: int = 0         # K >= 2: bootstrap ensemble with an acquisition energy
+    acq: str = "ucb"             # "ucb" | "ei" | "mean"
+    kappa: float = 1.0
 
 
 @dataclass
@@ -46,7 +55,7 @@ class TuneState:
 
 
 class Tuner:
-    def __init__(self, workload: dict, model, measure, cfg: TuneConfig = TuneConfig()):
+    def __init__(self, workload: dict, model, measure, cfg: TuneConfig = TuneConfig(), global_model=None):
         import torch
 
         from . import at
@@ -54,6 +63,8 @@ class Tuner:
         self.torch = torch
         self.space = at.Space([workload])
         self.model = model
+        self.global_model = global_model   # f_global of Eq. 4 (or None)
+        self.acq = None                    # acquisition options of the current energy (bootstrap)
         self.measure = measure
         self.cfg = cfg
         self.state = TuneState(chain_idx=torch.zeros(cfg.n_chains, dtype=torch.int64, device="cuda"))
@@ -62,7 +73,8 @@ class Tuner:
     def _temps(self):
         import torch
         from .synth import energy_scale, temperatures
-        t0 = energy_scale(self.model.n_trees)
+        n_trees = self.model.n_trees // (self.acq["n_models"] if self.acq else 1)
+        t0 = energy_scale(n_trees)
         return torch.from_numpy(temperatures(self.cfg.n_steps, t0, self.cfg.t_ratio)).cuda()
 
     def step(self):
@@ -72,7 +84,7 @@ class Tuner:
         if st.measured:
             meas = torch.from_numpy(np.sort(np.array(st.measured, dtype=np.uint64)).view(np.int64)).cuda()
         res = at.sa_explore(self.space, self.model, st.chain_idx, self._temps(), seed=cfg.seed, round_=self.round,
-                            k_out=cfg.lam * cfg.b, measured=meas, init=self.round == 0)
+                            k_out=cfg.lam * cfg.b, measured=meas, init=self.round == 0, acq=self.acq)
         n_pool = int(res["out_n"][0])
         sel, n_sel = at.select_topk(self.space, 0, res["out_idx"][0, :n_pool].contiguous(),
                                     res["out_score"][0, :n_pool].contiguous(), b=cfg.b, eps=cfg.eps,
@@ -85,15 +97,41 @@ class Tuner:
         i = int(np.argmin(costs)) if len(costs) else -1
         if i >= 0 and costs[i] < st.best_cost:
             st.best_cost, st.best_idx = float(costs[i]), int(selected[i])
-        # update f-hat using D (rank loss, from scratch)
+        # update f-hat using D (from scratch)
+        self.model, self.acq = self.refit()
+        self.round += 1
+        return selected
+
+    def _fit(self, X, n, c, key):
+        """One model on (X, c): f_local on top of f_global's scores when transferring (Eq. 4)."""
+        at, cfg = self.at, self.cfg
+        margin = self.global_model.predict(X, n) if self.global_model is not None else None
+        local = at.gbt_fit_hist(X, n, c, key, n_trees=cfg.n_trees, depth=cfg.depth, seed=cfg.seed + self.round,
+                                objective=cfg.objective, base_margin=margin)
+        return self.global_model.concat(local) if self.global_model is not None else local
+
+    def refit(self):
+        """update f-hat using D: one model, or K bootstrap models concatenated for the acquisition."""
+        at, torch, cfg, st = self.at, self.torch, self.cfg, self.state
+        n = len(st.measured)
         idx = torch.from_numpy(np.array(st.measured, dtype=np.uint64).view(np.int64)).cuda()
         X = self.space.features(idx)
         c = torch.from_numpy(np.array(st.costs, dtype=np.float32)).cuda()
-        key = torch.zeros(len(st.measured), dtype=torch.int16, device="cuda")
-        self.model = at.gbt_fit_hist(X, len(st.measured), c, key, n_trees=cfg.n_trees, depth=cfg.depth,
-                                     seed=cfg.seed + self.round)
-        self.round += 1
-        return selected
+        key = torch.zeros(n, dtype=torch.int16, device="cuda")
+        if cfg.n_bootstrap < 2:
+            return self._fit(X, n, c, key), None
+        model = None
+        for k in range(cfg.n_bootstrap):
+            Xk, ck, kk, _ = at.bootstrap_resample(X, n, c, key, k, seed=cfg.seed, round_=self.round)
+            mk = self._fit(Xk, n, ck, kk)
+            model = mk if model is None else model.concat(mk)
+        base = float(self.global_model.export()["base"]) if self.global_model is not None else 0.0
+        acq = dict(n_models=cfg.n_bootstrap, kind=cfg.acq, kappa=cfg.kappa, best=0.0,
+                   model_base=[base] * cfg.n_bootstrap)
+        if cfg.acq == "ei":   # incumbent: the lowest mean score over the measured configurations
+            _, mu, _ = model.predict_acq(X, n, cfg.n_bootstrap, kind="mean", model_base=acq["model_base"])
+            acq["best"] = float(mu.min())
+        return model, acq
 
     def run(self, max_trials: int):
         while len(self.state.measured) < max_trials:

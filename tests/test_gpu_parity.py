@@ -767,3 +767,56 @@ def test_algorithm1_rounds_match_oracle(at):
         assert np.array_equal(host_u64(tuner.state.chain_idx), chains), f"round {r} chains"
     assert len(set(tuner.state.measured)) == len(tuner.state.measured) == 3 * cfg.b      # never re-measured
     assert tuner.state.best_cost == min(costs)
+
+
+@pytest.mark.parametrize("objective,K,acq", [("reg", 3, "ei"), ("rank", 2, "ucb")])
+def test_algorithm1_with_transfer_and_bootstrap_matches_oracle(at, objective, K, acq):
+    """Algorithm 1 with the §8(f) options together: a global model (Eq. 4) under every local fit,
+    K bootstrap models (P:211) and an EI / UCB SA energy (P:208-215), regression or rank loss;
+    two rounds replayed by the oracle: identical selections and models."""
+    from paper_1805_08166_b200.tune import TuneConfig, Tuner
+    wl = dict(kind=0, n=64, m=128, k=32)
+    cfg = TuneConfig(n_chains=36, n_steps=20, b=12, lam=2, eps=0.125, alpha=0.1, n_trees=5, depth=4, seed=55,
+                     objective=objective, n_bootstrap=K, acq=acq, kappa=0.8)
+    osp = O.OracleSpace([O.workload(**wl)])
+
+    def measure(idx):
+        return synth.labels(osp.features(np.asarray(idx, dtype=np.uint64)), seed=98)
+
+    eg = synth.ensemble(20, 5, seed=6)
+    gglob = at.Gbt(eg["feat"], eg["thresh"], eg["leaf"], base=0.125)
+    oglob = O.OracleGbt(eg["feat"], eg["thresh"], eg["leaf"], base=0.125)
+    tuner = Tuner(wl, gglob, measure, cfg, global_model=gglob)
+    model, oacq, chains, measured, costs = oglob, None, None, [], []
+    for r in range(2):
+        sel_gpu = tuner.step()
+        T = (model[0] if isinstance(model, list) else model).n_trees
+        temps = synth.temperatures(cfg.n_steps, synth.energy_scale(T), cfg.t_ratio)
+        res = osp.sa_explore(model, cfg.n_chains, cfg.n_steps, cfg.seed, r, temps, chain_idx=chains, acq=oacq)
+        chains = res["chain_idx"]
+        (pi, pe), = osp.topk(res["visited_E"], res["visited_idx"], cfg.lam * cfg.b, measured=measured)
+        sel = osp.select(0, pi, pe, cfg.b, cfg.eps, cfg.alpha, cfg.seed, r, measured=measured)
+        assert np.array_equal(sel_gpu, sel), f"round {r}"
+        measured += sel.tolist()
+        costs += measure(sel).tolist()
+        X = osp.features(np.array(measured, dtype=np.uint64))
+        c = np.array(costs, np.float32)
+        models = []
+        for k in range(K):
+            ri = O.bootstrap_indices(len(measured), k, seed=cfg.seed, round_=r)
+            Xk = X[ri]
+            fit = O.fit_hist(Xk, c[ri], np.zeros(len(ri), np.uint16), n_trees=cfg.n_trees, depth=cfg.depth,
+                             seed=cfg.seed + r, objective=objective, base_margin=oglob.predict(Xk))
+            models.append(O.gbt_concat(oglob, O.OracleGbt(fit["feat"], fit["thresh"], fit["leaf"])))
+        best = 0.0
+        if acq == "ei":
+            best = float(O.predict_acq(models, X, kind="mean")[1].min())
+        model, oacq = models, (acq, cfg.kappa, best)
+        ex = tuner.model.export()
+        cat = models[0]
+        for m in models[1:]:
+            cat = O.gbt_concat(cat, m)
+        for f in ("feat", "thresh", "leaf"):
+            assert_bits_equal(ex[f], getattr(cat, f), f"round {r} models {f}")
+        assert np.float32(tuner.acq["best"]) == np.float32(best)
+    assert tuner.state.best_cost == min(costs)
