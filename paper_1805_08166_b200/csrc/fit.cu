@@ -986,14 +986,16 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
         __syncthreads();
         ++epoch;
         if (tid == 0) {
-            __threadfence();
-            const unsigned old = atomicAdd(A.bar, 1u);
+            // one acq_rel arrival: releases this block's writes (ordered before it by the
+            // __syncthreads, PTX fences being cumulative) and, for the last arriver, acquires all
+            // the other blocks' -- no separate __threadfence on either side
+            unsigned old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(A.bar) : "memory");
             T.wsi[1][0] = old == epoch * (unsigned)G - 1u ? 1 : 0;
         }
         __syncthreads();
         const int nq = nn > 0 ? nn : 1;
         if (T.wsi[1][0]) {   // block-uniform: the last arriver
-            __threadfence();
             for (int q = tid; q < nq; q += FUSED_NT) {
                 unsigned word = 0xFFFFFFFFu;
                 unsigned long long lo = 0, hi = 0;
@@ -1021,12 +1023,15 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
                 }
             }
         }
-        const volatile unsigned long long *rep = A.dec + (blockIdx.x % FUSED_NREP) * 128;
+        const unsigned long long *rep = A.dec + (blockIdx.x % FUSED_NREP) * 128;
         for (int q = tid; q < nq; q += FUSED_NT) {
-            unsigned long long v = rep[q];
+            // acquire loads: everything the reducer saw (hence every block's pre-barrier writes:
+            // gradients, slot keys) is visible to this block's later reads
+            unsigned long long v;
+            asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(rep + q) : "memory");
             while ((unsigned)(v >> 32) != epoch) {
                 __nanosleep(32);
-                v = rep[q];
+                asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(rep + q) : "memory");
             }
             T.decw[q] = (unsigned)v;
         }
