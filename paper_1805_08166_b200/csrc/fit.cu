@@ -830,6 +830,7 @@ struct FusedTail {
     int32_t decf[128], decs[128];                   // level decisions (f, s); decf < 0: no split
     int32_t Rst[128], Ren[128];                     // right-going count before a segment / through its end
     long long baseG[128], baseH[128], endG[128], endH[128];   // prefix sums before / at the end of a node
+    long long rbG[128], rbH[128], reG[128], reH[128];         // leaves: flagged prefix before / through a node
     unsigned nbh[128], nbl[128], nms[128];          // per-node best gain (hi, lo words) and its lowest s
     unsigned decw[128];                             // published decision words
     float lval[256];                                // leaf values of the current tree
@@ -1368,7 +1369,10 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
             for (int q = tid; q <= nn; q += FUSED_NT) T.segP[q] = T.segC[q];
             __syncthreads();
         }
-        // ---- leaves (every block, from its first feature's final order)
+        // ---- leaves (every block, from its first feature's final order): the last level's decisions
+        // as go-right flags per owned position, one block scan of the flagged (g, h), so each node's
+        // right-child sums are two prefix values at its segment bounds and the left child is the node
+        // total (the last level's bases / ends) minus them -- exact int64, no atomics
         {
             const int f = blockIdx.x;
             if (!resident) {
@@ -1376,20 +1380,52 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
                     ord[j] = A.gord[(int64_t)f * N + j];
                     nat[j] = A.gnode[(int64_t)f * N + j];
                 }
+                __syncthreads();
             }
-            for (int l = tid; l < 2 * n_leaf; l += FUSED_NT) lsum[l] = 0ull;
-            __syncthreads();
-            for (int j = tid; j < N; j += FUSED_NT) {
-                const int i = ord[j], q = nat[j], sf = T.decf[q];
-                const int right = (sf >= 0 && (int)A.bins[(int64_t)sf * N + i] >= T.decs[q]) ? 1 : 0;
-                const int l = 2 * q + right;
-                leafof[i] = (uint8_t)l;
-                smem_add_u64(&lsum[2 * l], (unsigned long long)sg[i]);
-                smem_add_u64(&lsum[2 * l + 1], (unsigned long long)sh[i]);
+            long long rg[EP], rh[EP];
+            int qv[EP];
+            long long ag = 0, ah = 0;
+#pragma unroll
+            for (int k = 0; k < EP; ++k) {   // all gathers of the thread in flight together
+                const int j = tid * EP + k;
+                int fl = 0, q = 0, i = 0;
+                if (j < N) {
+                    i = ord[j];
+                    q = nat[j];
+                    const int sf = T.decf[q];
+                    if (sf >= 0) fl = (int)__ldg(A.bins + (int64_t)sf * N + i) >= T.decs[q] ? 1 : 0;
+                    leafof[i] = (uint8_t)(2 * q + fl);
+                }
+                qv[k] = q;
+                if (fl) { ag += sg[i]; ah += sh[i]; }
+                rg[k] = ag;
+                rh[k] = ah;
+            }
+            long long og, oh;
+            blk_excl_i64x2(ag, ah, lane, warp, T.wsl[1], og, oh);
+            {
+                long long pg = og, ph = oh;
+#pragma unroll
+                for (int k = 0; k < EP; ++k) {
+                    const int j = tid * EP + k;
+                    const long long ig = og + rg[k], ih = oh + rh[k];
+                    if (j < N) {
+                        const int q = qv[k];
+                        if (j == T.segP[q]) { T.rbG[q] = pg; T.rbH[q] = ph; }
+                        if (j + 1 == T.segP[q + 1]) { T.reG[q] = ig; T.reH[q] = ih; }
+                    }
+                    pg = ig;
+                    ph = ih;
+                }
             }
             __syncthreads();
             for (int l = tid; l < n_leaf; l += FUSED_NT) {
-                const double Gd = (double)(long long)lsum[2 * l] * FX, Hd = (double)(long long)lsum[2 * l + 1] * FX;
+                const int q = l >> 1;
+                const bool any = T.segP[q + 1] > T.segP[q];
+                const long long RG = any ? T.reG[q] - T.rbG[q] : 0, RH = any ? T.reH[q] - T.rbH[q] : 0;
+                const long long NG = any ? T.endG[q] - T.baseG[q] : 0, NH = any ? T.endH[q] - T.baseH[q] : 0;
+                const long long LGi = (l & 1) ? RG : NG - RG, LHi = (l & 1) ? RH : NH - RH;
+                const double Gd = (double)LGi * FX, Hd = (double)LHi * FX;
                 const float v = (float)(-(A.eta * (Gd / (Hd + A.lam))));
                 T.lval[l] = v;
                 if (blockIdx.x == 0) A.t_leaf[(size_t)t * n_leaf + l] = v;
