@@ -325,19 +325,22 @@ __global__ void reg_grads_kernel(const float *__restrict__ cost, const float *__
 // Histograms use a compact bin layout: feature f owns nb_f = ncuts_f + 1 cells starting at
 // boff[f]; a level's buffer is hist[node][TB][2] int64 (TB = sum_f nb_f).
 __global__ void bin_layout_kernel(const int32_t *__restrict__ ncuts, int F, int32_t *__restrict__ boff,
-                                  int32_t *__restrict__ info /* [0] TB, [1] max nb */)
+                                  int32_t *__restrict__ info /* [0] TB, [1] max nb, [4] n splittable */,
+                                  int32_t *__restrict__ flist /* [F] splittable features, ascending */)
 {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    int32_t o = 0, mx = 0;
+    int32_t o = 0, mx = 0, nf = 0;
     for (int f = 0; f < F; ++f) {
         boff[f] = o;
         const int32_t nb = ncuts[f] + 1;
         o += nb;
         mx = nb > mx ? nb : mx;
+        if (nb > 1) flist[nf++] = f;   // a feature without cuts (constant on D) can never split
     }
     boff[F] = o;
     info[0] = o;
     info[1] = mx;
+    info[4] = nf;
 }
 
 // Exact 64-bit add into shared memory with two native 32-bit atomics (sm_100a has no native 64-bit
@@ -815,6 +818,8 @@ struct FusedArgs {
     double lam, mcw, eta;
     unsigned *bar;
     int objective;              // AT_OBJ_RANK / AT_OBJ_REG
+    const int32_t *flist;       // the features that can split (ncuts > 0), ascending; nF of them
+    int nF;
 };
 
 __host__ __device__ inline int fused_ep(int N)
@@ -967,7 +972,9 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
             *leafof = posbin + N + 16;
     FusedTail &T = *(FusedTail *)(fsm + ((((size_t)(leafof + N - fsm)) + 15) & ~(size_t)15));
 
-    const int G = gridDim.x, F = A.F, D = A.D;
+    // blocks own the features that can split (constant ones never can: no cut), block b feature
+    // flist[b] (and flist[b + G], ... when there are more than blocks)
+    const int G = gridDim.x, F = A.nF, D = A.D;
     const int n_int = (1 << D) - 1, n_leaf = 1 << D;
     const bool resident = F <= G;
     unsigned epoch = 0;
@@ -1040,7 +1047,8 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
     };
 
     // ---- init: bin-sorted order of every owned feature (counting sort; order inside a bin is free)
-    for (int f = blockIdx.x; f < F; f += G) {
+    for (int fi = blockIdx.x; fi < F; fi += G) {
+        const int f = __ldg(A.flist + fi);
         for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
         for (int b = tid; b < 512; b += FUSED_NT) cnt[b] = 0;
         __syncthreads();
@@ -1150,7 +1158,8 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
 
         for (int d = 0; d < D; ++d) {
             const int nn = 1 << d, first = nn - 1, nnP = nn >> 1;
-            for (int f = blockIdx.x; f < F; f += G) {
+            for (int fi = blockIdx.x; fi < F; fi += G) {
+                const int f = __ldg(A.flist + fi);
                 const int nc = A.ncuts[f];
                 if (!resident) {
                     for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
@@ -1374,7 +1383,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
         // right-child sums are two prefix values at its segment bounds and the left child is the node
         // total (the last level's bases / ends) minus them -- exact int64, no atomics
         {
-            const int f = blockIdx.x;
+            const int f = __ldg(A.flist + blockIdx.x);
             if (!resident) {
                 for (int j = tid; j < N; j += FUSED_NT) {
                     ord[j] = A.gord[(int64_t)f * N + j];
@@ -1557,6 +1566,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     float *cuts = ws.get<float>((size_t)F * (B - 1));
     int32_t *ncuts = ws.get<int32_t>(F);
     int32_t *boff = ws.get<int32_t>(F + 1);
+    int32_t *flist = ws.get<int32_t>(F);
     uint8_t *bins = ws.get<uint8_t>((size_t)F * n);
     int32_t *rank = ws.get<int32_t>(n);
     int32_t *counts = ws.get<int32_t>(FIT_MAXKEYS);
@@ -1588,7 +1598,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         key_check_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, n, d_info + 2); note_launch();
         sort_feature_kernel<<<F, 1024, 0, s>>>(d_feat, ld, n, sortA, sortB); note_launch();
         cuts_kernel<<<F, 1024, 0, s>>>(sortA, n, B, cuts, ncuts); note_launch();
-        bin_layout_kernel<<<1, 32, 0, s>>>(ncuts, F, boff, d_info); note_launch();
+        bin_layout_kernel<<<1, 32, 0, s>>>(ncuts, F, boff, d_info, flist); note_launch();
         bins_kernel<<<dim3(nblk(n, 256), F), 256, 0, s>>>(d_feat, ld, n, F, B, cuts, ncuts, bins); note_launch();
         ranks_kernel<<<1, 1024, 0, s>>>(d_group_key, n, rank, counts, woff, gpre, GS); note_launch();
         AT_CUDA_TRY(cudaMemcpyAsync(d_info + 3, gpre + FIT_MAXKEYS, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
@@ -1603,6 +1613,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     if (info[2] == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
     if (info[2] == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
     const int TB = info[0], max_nb = info[1], n_groups = info[3];
+    const int n_split = info[4];   // features with at least one cut
     // the fitted ensemble handle (both paths)
     auto finish = [&]() -> int {
         // the fitted ensemble handle
@@ -1656,8 +1667,12 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         }
         AT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fk, FUSED_NT, fsm));
         if (coop && per > 0) {
-            const int G = (int)std::min<int64_t>(F, (int64_t)per * nsm);
-            const bool resident = F <= G;
+            // blocks for the splittable features only (all constant: one block on feature 0, which has no
+            // cut, so every node stays a pass-through and the leaves are the node totals)
+            const int nF = std::max(n_split, 1);
+            if (n_split == 0) AT_CUDA_TRY(cudaMemsetAsync(flist, 0, sizeof(int32_t), s));
+            const int G = (int)std::min<int64_t>(nF, (int64_t)per * nsm);
+            const bool resident = nF <= G;
             int32_t *klist = ws.get<int32_t>(n);
             unsigned long long *slot = ws.get<unsigned long long>((size_t)2 * FUSED_NSUB * n_int);
             unsigned *bar = ws.get<unsigned>(32);
@@ -1673,6 +1688,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             AT_LAUNCH_CHECK("klist");
             FusedArgs fa;
             fa.bins = bins; fa.ncuts = ncuts; fa.cuts = cuts; fa.B = B;
+            fa.flist = flist; fa.nF = nF;
             fa.n = (int)n; fa.F = F; fa.D = D; fa.n_trees = o->n_trees; fa.GS = GS; fa.n_groups = n_groups;
             fa.counts = counts; fa.woff = woff; fa.gpre = gpre; fa.klist = klist;
             float *pred2 = ws.get<float>(n);
