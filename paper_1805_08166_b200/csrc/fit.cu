@@ -795,7 +795,7 @@ __global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int3
 // derives the leaves redundantly; the prediction update of tree t is applied by the owner of each
 // sample's group in tree t + 1 (and once more after the last tree).
 constexpr int FUSED_NMAX = 2048;
-constexpr int FUSED_NT = 256;
+constexpr int FUSED_NT = 512;
 constexpr int FUSED_NSUB = 8;   // sub-slots per node (block b uses b mod 8): bounds CAS contention
 constexpr int FUSED_NREP = 16;  // replicas of the release flag / decisions (block b reads b mod 16)
 
@@ -947,17 +947,17 @@ __device__ __forceinline__ unsigned long long gtimer()
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-__device__ unsigned long long g_ft_work_max = 0ull, g_ft_grad_max = 0ull;
+__device__ unsigned long long g_ft_work_max = 0ull, g_ft_grad_max = 0ull, g_ft_bar_ns = 0ull, g_ft_bar_n = 0ull;
 #define FT_MARK(k) do { if (threadIdx.x == 0) { unsigned long long _t = gtimer(); ft[k] += _t - ft_last; ft_last = _t; } } while (0)
 #else
 #define FT_MARK(k) do {} while (0)
 #endif
 
 template <int EP>
-__global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel(FusedArgs A)
+__global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel(FusedArgs A)
 {
 #ifdef AT_FIT_TIMING
-    unsigned long long ft[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer();
+    unsigned long long ft[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer(), t_arr = 0;
 #endif
     extern __shared__ __align__(16) unsigned char fsm[];
     const int N = A.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -998,6 +998,9 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
             // __syncthreads, PTX fences being cumulative) and, for the last arriver, acquires all
             // the other blocks' -- no separate __threadfence on either side
             unsigned old;
+#ifdef AT_FIT_TIMING
+            t_arr = gtimer();
+#endif
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(A.bar) : "memory");
             T.wsi[1][0] = old == epoch * (unsigned)G - 1u ? 1 : 0;
         }
@@ -1044,6 +1047,12 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
             T.decw[q] = (unsigned)v;
         }
         __syncthreads();
+#ifdef AT_FIT_TIMING
+        if (tid == 0 && T.wsi[1][0]) {   // the last arriver: its arrival -> its release = the barrier itself
+            atomicAdd(&g_ft_bar_ns, gtimer() - t_arr);
+            atomicAdd(&g_ft_bar_n, 1ull);
+        }
+#endif
     };
 
     // ---- init: bin-sorted order of every owned feature (counting sort; order inside a bin is free)
@@ -1454,6 +1463,9 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 8 ? 2 : 4) fused_forest_kernel
                "decide+leaves %llu | max over blocks: grads %llu work %llu (from earlier-finishing blocks)\n", G,
                ft[0] / A.n_trees, ft[1] / A.n_trees, ft[2] / A.n_trees, ft[3] / A.n_trees, ft[4] / A.n_trees,
                g_ft_grad_max / A.n_trees, g_ft_work_max / A.n_trees);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("barrier (last arriver: arrival -> release seen): %llu ns avg over %llu\n",
+               g_ft_bar_n ? g_ft_bar_ns / g_ft_bar_n : 0ull, g_ft_bar_n);
 #endif
     // the last tree's prediction update
     const int TT = A.n_trees;
