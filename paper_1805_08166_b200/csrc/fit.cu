@@ -795,7 +795,8 @@ __global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int3
 // derives the leaves redundantly; the prediction update of tree t is applied by the owner of each
 // sample's group in tree t + 1 (and once more after the last tree).
 constexpr int FUSED_NMAX = 2048;
-constexpr int FUSED_NT = 512;
+constexpr int FUSED_NT_MAX = 512;   // threads per block: 512 when every splittable feature gets a
+                                     // block at 2 blocks / SM, else 256 (4 / SM)
 constexpr int FUSED_NSUB = 8;   // sub-slots per node (block b uses b mod 8): bounds CAS contention
 constexpr int FUSED_NREP = 16;  // replicas of the release flag / decisions (block b reads b mod 16)
 
@@ -822,10 +823,10 @@ struct FusedArgs {
     int nF;
 };
 
-__host__ __device__ inline int fused_ep(int N)
+__host__ __device__ inline int fused_ep(int N, int NT)
 {
     int EP = 1;                                      // positions per thread (power of two)
-    while (EP * FUSED_NT < N) EP <<= 1;
+    while (EP * NT < N) EP <<= 1;
     return EP;
 }
 
@@ -839,9 +840,9 @@ struct FusedTail {
     unsigned nbh[128], nbl[128], nms[128];          // per-node best gain (hi, lo words) and its lowest s
     unsigned decw[128];                             // published decision words
     float lval[256];                                // leaf values of the current tree
-    int32_t wsi[2][FUSED_NT / 32];                  // scan scratch
+    int32_t wsi[2][FUSED_NT_MAX / 32];              // scan scratch
     int32_t gpre[FIT_MAXKEYS + 1];                  // group prefix per workload (copy)
-    long long wsl[2][2 * (FUSED_NT / 32)];
+    long long wsl[2][2 * (FUSED_NT_MAX / 32)];
     uint8_t dead[512];
 };
 
@@ -891,6 +892,7 @@ __device__ __forceinline__ void slot_max(unsigned long long *p, unsigned long lo
 
 // block-wide exclusive scan of one int per thread (thread order); `ws` must not be reused before
 // the next __syncthreads after this call
+template <int NW>
 __device__ __forceinline__ int blk_excl_int(int v, int lane, int warp, int32_t *ws, int &total)
 {
     int x = v;
@@ -903,7 +905,7 @@ __device__ __forceinline__ int blk_excl_int(int v, int lane, int warp, int32_t *
     __syncthreads();
     int o = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < FUSED_NT / 32; ++w) {
+    for (int w = 0; w < NW; ++w) {
         const int u = ws[w];
         o += w < warp ? u : 0;
         tot += u;
@@ -913,6 +915,7 @@ __device__ __forceinline__ int blk_excl_int(int v, int lane, int warp, int32_t *
 }
 
 // the same for a pair of int64 (exact, order-free)
+template <int NW>
 __device__ __forceinline__ void blk_excl_i64x2(long long a, long long b, int lane, int warp, long long *ws,
                                                long long &oa, long long &ob)
 {
@@ -926,7 +929,7 @@ __device__ __forceinline__ void blk_excl_i64x2(long long a, long long b, int lan
     __syncthreads();
     long long pa = x - a, pb = y - b;
 #pragma unroll
-    for (int w = 0; w < FUSED_NT / 32; ++w)
+    for (int w = 0; w < NW; ++w)
         if (w < warp) { pa += ws[2 * w]; pb += ws[2 * w + 1]; }
     oa = pa;
     ob = pb;
@@ -953,15 +956,15 @@ __device__ unsigned long long g_ft_work_max = 0ull, g_ft_grad_max = 0ull, g_ft_b
 #define FT_MARK(k) do {} while (0)
 #endif
 
-template <int EP>
-__global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel(FusedArgs A)
+template <int EP, int NT>
+__global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ? 2 : 4)) fused_forest_kernel(FusedArgs A)
 {
 #ifdef AT_FIT_TIMING
     unsigned long long ft[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer(), t_arr = 0;
 #endif
     extern __shared__ __align__(16) unsigned char fsm[];
     const int N = A.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = FUSED_NT / 32;
+    constexpr int NW = NT / 32;
     int64_t *sg = (int64_t *)fsm, *sh = sg + N;
     unsigned long long *lsum = (unsigned long long *)(sh + N);   // [512]
     unsigned *cnt = (unsigned *)lsum;                            // counting sort scratch (init only)
@@ -980,8 +983,8 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
     unsigned epoch = 0;
     const int CM = A.GS / 8 > 8 ? A.GS / 8 : 8;
     const int chunks = (A.GS + CM - 1) / CM;
-    for (int q = tid; q < 128; q += FUSED_NT) { T.nbh[q] = 0; T.nbl[q] = 0; T.nms[q] = 0xFFFFFFFFu; }
-    for (int q = tid; q <= FIT_MAXKEYS; q += FUSED_NT) T.gpre[q] = A.gpre[q];
+    for (int q = tid; q < 128; q += NT) { T.nbh[q] = 0; T.nbl[q] = 0; T.nms[q] = 0xFFFFFFFFu; }
+    for (int q = tid; q <= FIT_MAXKEYS; q += NT) T.gpre[q] = A.gpre[q];
 
     // Grid-wide sync.  Every block arrives on one counter (fence, then an atomic add that returns
     // the count); the LAST block to arrive reduces the level's sub-slots into the decisions (nn > 0),
@@ -1007,7 +1010,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
         __syncthreads();
         const int nq = nn > 0 ? nn : 1;
         if (T.wsi[1][0]) {   // block-uniform: the last arriver
-            for (int q = tid; q < nq; q += FUSED_NT) {
+            for (int q = tid; q < nq; q += NT) {
                 unsigned word = 0xFFFFFFFFu;
                 unsigned long long lo = 0, hi = 0;
                 if (nn > 0) {
@@ -1035,7 +1038,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
             }
         }
         const unsigned long long *rep = A.dec + (blockIdx.x % FUSED_NREP) * 128;
-        for (int q = tid; q < nq; q += FUSED_NT) {
+        for (int q = tid; q < nq; q += NT) {
             // acquire loads: everything the reducer saw (hence every block's pre-barrier writes:
             // gradients, slot keys) is visible to this block's later reads
             unsigned long long v;
@@ -1058,10 +1061,10 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
     // ---- init: bin-sorted order of every owned feature (counting sort; order inside a bin is free)
     for (int fi = blockIdx.x; fi < F; fi += G) {
         const int f = __ldg(A.flist + fi);
-        for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
-        for (int b = tid; b < 512; b += FUSED_NT) cnt[b] = 0;
+        for (int i = tid; i < N; i += NT) sbin[i] = A.bins[(int64_t)f * N + i];
+        for (int b = tid; b < 512; b += NT) cnt[b] = 0;
         __syncthreads();
-        for (int i = tid; i < N; i += FUSED_NT) atomicAdd(&cnt[sbin[i]], 1u);
+        for (int i = tid; i < N; i += NT) atomicAdd(&cnt[sbin[i]], 1u);
         __syncthreads();
         if (warp == 0) {
             unsigned v[8], a = 0;
@@ -1078,9 +1081,9 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
             for (int k = 0; k < 8; ++k) { cnt[256 + lane * 8 + k] = o; o += v[k]; }
         }
         __syncthreads();
-        for (int i = tid; i < N; i += FUSED_NT) ordA[atomicAdd(&cnt[256 + sbin[i]], 1u)] = (uint16_t)i;
+        for (int i = tid; i < N; i += NT) ordA[atomicAdd(&cnt[256 + sbin[i]], 1u)] = (uint16_t)i;
         __syncthreads();
-        for (int j = tid; j < N; j += FUSED_NT) A.gord0[(int64_t)f * N + j] = ordA[j];
+        for (int j = tid; j < N; j += NT) A.gord0[(int64_t)f * N + j] = ordA[j];
         __syncthreads();
     }
 
@@ -1090,7 +1093,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
         unsigned long long *slot = A.slot;
         // ---- gradients (and the previous tree's prediction update)
         if (A.objective == AT_OBJ_REG) {   // per sample: grid-stride over the samples
-            for (int i = blockIdx.x * FUSED_NT + tid; i < N; i += G * FUSED_NT) {
+            for (int i = blockIdx.x * NT + tid; i < N; i += G * NT) {
                 float pv = __ldcg(A.pred[0] + i);   // tree 0: the initial predictions
                 if (t > 0) {
                     pv = __fadd_rn(__ldcg(A.pred[(t - 1) & 1] + i), T.lval[leafof[i]]);
@@ -1124,7 +1127,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
             while ((1ull << bits) < (unsigned long long)nw) ++bits;
             int hb = (bits + 1) / 2;
             if (hb < 1) hb = 1;
-            for (int a = tid; a < m; a += FUSED_NT) {
+            for (int a = tid; a < m; a += NT) {
                 uint32_t r = feistel_inv((uint32_t)(start + a), hb, A.seed, (uint32_t)t, (uint32_t)w);
                 while (r >= (uint32_t)nw) r = feistel_inv(r, hb, A.seed, (uint32_t)t, (uint32_t)w);
                 const int i = A.klist[A.woff[w] + (int)r];
@@ -1160,8 +1163,8 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
         sync_all(t, 0, 0);
         FT_MARK(1);
 
-        for (int i = tid; i < N; i += FUSED_NT) { sg[i] = __ldcg(A.g + i); sh[i] = __ldcg(A.h + i); }
-        for (int q = tid; q < 512; q += FUSED_NT) T.dead[q] = 0;
+        for (int i = tid; i < N; i += NT) { sg[i] = __ldcg(A.g + i); sh[i] = __ldcg(A.h + i); }
+        for (int q = tid; q < 512; q += NT) T.dead[q] = 0;
         if (tid == 0) { T.segP[0] = 0; T.segP[1] = N; }
         __syncthreads();
 
@@ -1171,15 +1174,15 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                 const int f = __ldg(A.flist + fi);
                 const int nc = A.ncuts[f];
                 if (!resident) {
-                    for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
+                    for (int i = tid; i < N; i += NT) sbin[i] = A.bins[(int64_t)f * N + i];
                     if (d > 0)
-                        for (int j = tid; j < N; j += FUSED_NT) {
+                        for (int j = tid; j < N; j += NT) {
                             ord[j] = A.gord[(int64_t)f * N + j];
                             nat[j] = A.gnode[(int64_t)f * N + j];
                         }
                     __syncthreads();
                 } else if (t == 0 && d == 0) {
-                    for (int i = tid; i < N; i += FUSED_NT) sbin[i] = A.bins[(int64_t)f * N + i];
+                    for (int i = tid; i < N; i += NT) sbin[i] = A.bins[(int64_t)f * N + i];
                     __syncthreads();
                 }
                 int iv[EP], qv[EP];   // sample and node of each owned position (in the level's order)
@@ -1219,7 +1222,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                         c += fl[k];
                     }
                     int rtot;
-                    const int ex0 = blk_excl_int(c, lane, warp, T.wsi[0], rtot);
+                    const int ex0 = blk_excl_int<NW>(c, lane, warp, T.wsi[0], rtot);
                     int ex = ex0;
 #pragma unroll
                     for (int k = 0; k < EP; ++k) {
@@ -1245,7 +1248,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                         }
                         ex += fl[k];
                     }
-                    for (int q = tid; q < nnP; q += FUSED_NT) {
+                    for (int q = tid; q < nnP; q += NT) {
                         const int s0 = T.segP[q], s1 = T.segP[q + 1];
                         const int nR = s1 > s0 ? T.Ren[q] - T.Rst[q] : 0;
                         T.segC[2 * q] = s0;
@@ -1283,7 +1286,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                     ph[k] = ah;
                 }
                 long long og, oh;
-                blk_excl_i64x2(ag, ah, lane, warp, T.wsl[0], og, oh);
+                blk_excl_i64x2<NW>(ag, ah, lane, warp, T.wsl[0], og, oh);
                 {
                     long long prg = og, prh = oh;
 #pragma unroll
@@ -1349,7 +1352,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                     if (gk[k] && gk[k] == (((unsigned long long)T.nbh[(qb[k] >> 8)] << 32) | T.nbl[(qb[k] >> 8)]))
                         atomicMin(&T.nms[(qb[k] >> 8)], (unsigned)((qb[k] & 0xFF) + 1));
                 __syncthreads();
-                for (int q = tid; q < nn; q += FUSED_NT) {
+                for (int q = tid; q < nn; q += NT) {
                     const unsigned long long gb = ((unsigned long long)T.nbh[q] << 32) | T.nbl[q];
                     if (gb)
                         slot_max(slot + 2 * ((first + q) * FUSED_NSUB + (blockIdx.x & (FUSED_NSUB - 1))),
@@ -1361,7 +1364,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                     T.nms[q] = 0xFFFFFFFFu;
                 }
                 if (!resident)
-                    for (int j = tid; j < N; j += FUSED_NT) {
+                    for (int j = tid; j < N; j += NT) {
                         A.gord[(int64_t)f * N + j] = ord[j];
                         A.gnode[(int64_t)f * N + j] = nat[j];
                     }
@@ -1371,7 +1374,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
             sync_all(t, nn, first);
             FT_MARK(3);
             // the level's decisions (identical in every block; a dead node never has a split)
-            for (int q = tid; q < nn; q += FUSED_NT) {
+            for (int q = tid; q < nn; q += NT) {
                 const int nd = first + q;
                 const unsigned word = T.decw[q];
                 if (word == 0xFFFFFFFFu) {
@@ -1384,7 +1387,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                     T.decs[q] = (int)(word & 0xFFu);
                 }
             }
-            for (int q = tid; q <= nn; q += FUSED_NT) T.segP[q] = T.segC[q];
+            for (int q = tid; q <= nn; q += NT) T.segP[q] = T.segC[q];
             __syncthreads();
         }
         // ---- leaves (every block, from its first feature's final order): the last level's decisions
@@ -1394,7 +1397,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
         {
             const int f = __ldg(A.flist + blockIdx.x);
             if (!resident) {
-                for (int j = tid; j < N; j += FUSED_NT) {
+                for (int j = tid; j < N; j += NT) {
                     ord[j] = A.gord[(int64_t)f * N + j];
                     nat[j] = A.gnode[(int64_t)f * N + j];
                 }
@@ -1420,7 +1423,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                 rh[k] = ah;
             }
             long long og, oh;
-            blk_excl_i64x2(ag, ah, lane, warp, T.wsl[1], og, oh);
+            blk_excl_i64x2<NW>(ag, ah, lane, warp, T.wsl[1], og, oh);
             {
                 long long pg = og, ph = oh;
 #pragma unroll
@@ -1437,7 +1440,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
                 }
             }
             __syncthreads();
-            for (int l = tid; l < n_leaf; l += FUSED_NT) {
+            for (int l = tid; l < n_leaf; l += NT) {
                 const int q = l >> 1;
                 const bool any = T.segP[q + 1] > T.segP[q];
                 const long long RG = any ? T.reG[q] - T.rbG[q] : 0, RH = any ? T.reH[q] - T.rbH[q] : 0;
@@ -1469,7 +1472,7 @@ __global__ void __launch_bounds__(FUSED_NT, EP >= 4 ? 1 : 2) fused_forest_kernel
 #endif
     // the last tree's prediction update
     const int TT = A.n_trees;
-    for (int i = blockIdx.x * FUSED_NT + tid; i < N; i += G * FUSED_NT)
+    for (int i = blockIdx.x * NT + tid; i < N; i += G * NT)
         A.pred[TT & 1][i] = __fadd_rn(__ldcg(A.pred[(TT - 1) & 1] + i), T.lval[leafof[i]]);
 }
 
@@ -1661,27 +1664,38 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     const char *fused_e = getenv("AT_FIT_FUSED");   // "0" forces the level-by-level path
     const int fused_env = fused_e ? atoi(fused_e) : 1;
     if (fused_env && !o->allreduce && !o->d_hist0_out && n <= FUSED_NMAX) {
-        const size_t fsm = fused_smem_bytes((int)n, GS);
-        const int fep = fused_ep((int)n);
-        const void *fk = fep == 1   ? (const void *)fused_forest_kernel<1>
-                         : fep == 2 ? (const void *)fused_forest_kernel<2>
-                         : fep == 4 ? (const void *)fused_forest_kernel<4>
-                                    : (const void *)fused_forest_kernel<8>;
         int dev = 0, nsm = 0, coop = 0, per = 0;
         AT_CUDA_TRY(cudaGetDevice(&dev));
         AT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         AT_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-        static size_t fused_attr[4] = {0, 0, 0, 0};
-        const int fslot = fep == 1 ? 0 : fep == 2 ? 1 : fep == 4 ? 2 : 3;
-        if (fused_attr[fslot] < fsm) {
-            AT_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-            fused_attr[fslot] = fsm;
+        const int nF = std::max(n_split, 1);   // blocks own the splittable features
+        // the kernel variant: 512 threads per block when every splittable feature still gets its own
+        // resident block at 2 blocks / SM, else 256 threads (4 / SM)
+        const void *fk = nullptr;
+        int NT = 512, fep = 1;
+        size_t fsm = 0;
+        static size_t fused_attr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int pass = 0; pass < 2; ++pass) {
+            NT = pass == 0 ? 512 : 256;
+            fep = fused_ep((int)n, NT);
+            fsm = fused_smem_bytes((int)n, GS);
+            if (NT == 512)
+                fk = fep == 1 ? (const void *)fused_forest_kernel<1, 512> : fep == 2 ? (const void *)fused_forest_kernel<2, 512>
+                   : (const void *)fused_forest_kernel<4, 512>;
+            else
+                fk = fep == 1   ? (const void *)fused_forest_kernel<1, 256> : fep == 2 ? (const void *)fused_forest_kernel<2, 256>
+                   : fep == 4 ? (const void *)fused_forest_kernel<4, 256> : (const void *)fused_forest_kernel<8, 256>;
+            const int fslot = (pass == 0 ? 0 : 4) + (fep == 1 ? 0 : fep == 2 ? 1 : fep == 4 ? 2 : 3);
+            if (fused_attr[fslot] < fsm) {
+                AT_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+                fused_attr[fslot] = fsm;
+            }
+            AT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fk, NT, fsm));
+            if (pass == 0 && per > 0 && nF <= per * nsm) break;
         }
-        AT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fk, FUSED_NT, fsm));
         if (coop && per > 0) {
             // blocks for the splittable features only (all constant: one block on feature 0, which has no
             // cut, so every node stays a pass-through and the leaves are the node totals)
-            const int nF = std::max(n_split, 1);
             if (n_split == 0) AT_CUDA_TRY(cudaMemsetAsync(flist, 0, sizeof(int32_t), s));
             const int G = (int)std::min<int64_t>(nF, (int64_t)per * nsm);
             const bool resident = nF <= G;
@@ -1718,7 +1732,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             void *args[] = {&fa};
             {
                 ProfScope ps(AT_K_FIT_GRAPH, s);
-                AT_CUDA_TRY(cudaLaunchCooperativeKernel(fk, dim3(G), dim3(FUSED_NT), args,
+                AT_CUDA_TRY(cudaLaunchCooperativeKernel(fk, dim3(G), dim3(NT), args,
                                                         fsm, s));
                 note_launch();
             }
