@@ -422,8 +422,8 @@ __device__ __forceinline__ void sa_row(const WlDev &W, const SaLowering &L, int 
 // max over t (relation_prefix) then gives R_t = max_{k : T_k < 2^t} Z_k, 0 for an empty set.
 // the extents of every loop of template TMPL for knob vector ch (one factor-table load per loop)
 template <int TMPL>
-__device__ __forceinline__ void sa_extents(const WlDev &W, const uint16_t *__restrict__ fact, const uint32_t *ch,
-                                           uint32_t *ext /* [MAXLOOPS][32] at the lane */)
+__device__ __forceinline__ void sa_extents(const uint32_t (&foff)[6], const uint16_t *__restrict__ fact,
+                                           const uint32_t *ch, uint32_t *ext /* [MAXLOOPS][32] at the lane */)
 {
     constexpr int NL = Tmpl<TMPL>::NL;
     const uint32_t p = TMPL == 1 ? ch[6] : TMPL == 2 ? ch[5] : 0u;
@@ -436,7 +436,10 @@ __device__ __forceinline__ void sa_extents(const WlDev &W, const uint16_t *__res
         uint32_t cha = 0;
 #pragma unroll
         for (int q = 0; q < 6; ++q) if (q == axis) cha = ch[q];
-        ev[l] = __ldg(fact + W.fact_off[axis] + cha * (uint32_t)Lv + level);
+        uint32_t fo = 0;   // the split table of this axis (register copy: no dependent global load)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) if (q == axis) fo = foff[q];
+        ev[l] = __ldg(fact + fo + cha * (uint32_t)Lv + level);
     }
 #pragma unroll
     for (int l = 0; l < NL; ++l) ext[l * 32] = ev[l];

@@ -75,7 +75,7 @@ struct SaParams {
     uint32_t *accept_bits;
     float *vis_E;
     uint64_t *vis_idx;
-    uint64_t *keys;   // [n_chains][n_steps+1]
+    uint64_t *keys;   // [n_steps+1][n_chains] (step-major: a warp's 32 keys are one coalesced store)
     AcqArgs Q;        // KM > 1: energy = acquisition over Q.K concatenated models
 };
 
@@ -87,6 +87,7 @@ struct SaSmem {
     float fk[GRP][KM > 1 ? KM * 32 : 1];   // per-model energies (KM > 1)
     uint32_t ch[GRP][MAXKNOBS][32];
     uint32_t ext[GRP][MAXLOOPS][32];      // loop extents of each chain's current proposal (owner-written)
+    uint32_t rnd[GRP][4][32];             // the next step's Philox words, precomputed by a helper warp
     int32_t w[GRP][32];
     uint64_t bar[2];
 };
@@ -101,12 +102,13 @@ __device__ __forceinline__ void sa_row_any(const WlDev &W, const uint32_t *ext, 
     }
 }
 
-__device__ __forceinline__ void sa_extents_any(const WlDev &W, const uint16_t *fact, const uint32_t *ch, uint32_t *ext)
+__device__ __forceinline__ void sa_extents_any(int tmpl, const uint32_t (&foff)[6], const uint16_t *fact,
+                                               const uint32_t *ch, uint32_t *ext)
 {
-    switch (W.tmpl) {
-    case 0: sa_extents<0>(W, fact, ch, ext); break;
-    case 1: sa_extents<1>(W, fact, ch, ext); break;
-    default: sa_extents<2>(W, fact, ch, ext); break;
+    switch (tmpl) {
+    case 0: sa_extents<0>(foff, fact, ch, ext); break;
+    case 1: sa_extents<1>(foff, fact, ch, ext); break;
+    default: sa_extents<2>(foff, fact, ch, ext); break;
     }
 }
 
@@ -160,6 +162,8 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     uint32_t accw = 0;
     int pj = -1;
     uint32_t pv = 0;
+    uint32_t foff[6] = {0u, 0u, 0u, 0u, 0u, 0u};   // the chain's split-table offsets (fixed workload)
+    int tmpl = 0;
     if (owner) {
         if (live && P.chain_w) w = P.chain_w[c];
         const WlDev &W = P.S->w[w];
@@ -176,7 +180,10 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         decode_any(W, (uint32_t)(idx - W.offset), ch);
 #pragma unroll
         for (int j = 0; j < MAXKNOBS; ++j) sm.ch[og][j][lane] = ch[j];
-        sa_extents_any(W, P.fact, ch, &sm.ext[og][0][lane]);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) foff[q] = W.fact_off[q];
+        tmpl = W.tmpl;
+        sa_extents_any(tmpl, foff, P.fact, ch, &sm.ext[og][0][lane]);
         sm.w[og][lane] = w;
         zero_cols_any(W.tmpl, sm.tile[og], lane);
     } else {
@@ -212,7 +219,21 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         }
         __syncthreads();
     };
+    // helper warp GRP + g draws step s's Philox words of group g's chains (off the owner's serial
+    // proposal path); the walk's closing barrier publishes them before the owner reads them
+    auto draw_next = [&](int s) {
+        if (warp >= GRP && warp < 2 * GRP && s < P.n_steps) {
+            const int g = warp - GRP;
+            const uint32_t gc = P.chain_base + (uint32_t)(blockIdx.x * 32 * GRP + g * 32 + lane);
+            const U4 r = philox(P.seed, gc, (uint32_t)s, P.round, TAG_SA_STEP);
+            sm.rnd[g][0][lane] = r.x;
+            sm.rnd[g][1][lane] = r.y;
+            sm.rnd[g][2][lane] = r.z;
+            sm.rnd[g][3][lane] = r.w;
+        }
+    };
     features_phase();
+    draw_next(0);
     ts_wait_resident(G, sm.bar);
     walk_pass<SA_NW, GRP, KM>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp, &sm.part[0][0],
                           nullptr, 0, 0, no_slots);
@@ -221,7 +242,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     if (owner) {
         E = energy(og, lane);
         if (live) {
-            P.keys[(int64_t)c * per] = ((uint64_t)fkey(E) << 32) | (uint64_t)(idx - P.S->w[w].offset);
+            P.keys[c] = ((uint64_t)fkey(E) << 32) | (uint64_t)(idx - P.S->w[w].offset);   // step-major: coalesced
             if (P.vis_E) { P.vis_E[(int64_t)c * per] = E; P.vis_idx[(int64_t)c * per] = idx; }
         }
     }
@@ -234,7 +255,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         U4 r;
         if (owner) {
             const WlDev &W = P.S->w[w];
-            r = philox(P.seed, gid, (uint32_t)s, P.round, TAG_SA_STEP);
+            r = U4{sm.rnd[og][0][lane], sm.rnd[og][1][lane], sm.rnd[og][2][lane], sm.rnd[og][3][lane]};   // Philox(gid, s)
             idx2 = idx;
             pj = -1;
             if (W.n_ns > 0) {
@@ -252,13 +273,14 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == j) sm.ch[og][q][lane] = v2;
             }
-            sa_extents_any(W, P.fact, ch, &sm.ext[og][0][lane]);   // the proposal's loop extents
+            sa_extents_any(tmpl, foff, P.fact, ch, &sm.ext[og][0][lane]);   // the proposal's loop extents
         }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_prop += t - t0; t0 = t; }
 #endif
         features_phase();
+        draw_next(s + 1);
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
 #endif
@@ -292,7 +314,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
             }
             if (live) {
                 const int64_t at = (int64_t)c * per + s + 1;
-                P.keys[at] = ((uint64_t)fkey(E2) << 32) | (uint64_t)(idx2 - P.S->w[w].offset);
+                P.keys[(int64_t)(s + 1) * P.n_chains + c] = ((uint64_t)fkey(E2) << 32) | (uint64_t)(idx2 - P.S->w[w].offset);
                 if (P.vis_E) { P.vis_E[at] = E2; P.vis_idx[at] = idx2; }
                 if (P.accept_bits && ((s & 31) == 31 || s == P.n_steps - 1)) {
                     P.accept_bits[(int64_t)c * ((P.n_steps + 31) / 32) + (s >> 5)] = accw;
@@ -422,7 +444,7 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         a.mode = 0;
         a.keys = keys;
         a.n_src = n_keys;
-        a.per_chain = per;
+        a.n_chains = o->n_chains;
         a.chain_w = d_chain_workload;
         a.w = w;
         a.offset_w = sp->host.offset[w];

@@ -27,14 +27,14 @@ __device__ __forceinline__ bool in_sorted(const uint64_t *__restrict__ a, int64_
     return lo < n && __ldg(a + lo) == v;
 }
 
-// mode 0: raw SA keys [n_chains][per_chain] filtered by chain workload == w and not measured
+// mode 0: raw SA keys [steps + 1][n_chains] filtered by chain workload == w and not measured
 // mode 1: lists [n_lists][n_w][k_in] of (idx, score) with counts, workload w, not measured
 // mode 2: partial key lists (already filtered), plain reduction
 struct TkSrc {
     int mode;
     const uint64_t *keys;
-    int64_t n;               // number of source keys (mode 0: n_chains*per_chain; 1: n_lists*k_in; 2: count)
-    int64_t per_chain;
+    int64_t n;               // number of source keys (mode 0: (steps+1)*n_chains; 1: n_lists*k_in; 2: count)
+    int64_t n_chains;
     const uint16_t *chain_w;
     int w;
     uint64_t offset_w;
@@ -52,7 +52,7 @@ __device__ __forceinline__ uint64_t tk_load(const TkSrc &S, int64_t i)
     if (S.mode == 2) return __ldg(S.keys + i);
     uint64_t key, gidx;
     if (S.mode == 0) {
-        const int64_t c = i / S.per_chain;
+        const int64_t c = i % S.n_chains;
         if (S.chain_w && (int)__ldg(S.chain_w + c) != S.w) return KEY_NONE;
         key = __ldg(S.keys + i);
         gidx = S.offset_w + (key & 0xFFFFFFFFull);
@@ -168,7 +168,7 @@ int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s)
     S.mode = a.mode;
     S.keys = a.keys;
     S.n = a.n_src;
-    S.per_chain = a.per_chain;
+    S.n_chains = a.n_chains;
     S.chain_w = a.chain_w;
     S.w = a.w;
     S.offset_w = a.offset_w;

@@ -6,9 +6,9 @@ namespace at {
 
 struct TkArgs {
     int mode;                    // 0 SA keys, 1 (idx, score) lists
-    const uint64_t *keys;        // mode 0: [n_chains][per_chain] keys (fkey(E) << 32 | local idx)
+    const uint64_t *keys;        // mode 0: [steps + 1][n_chains] keys (fkey(E) << 32 | local idx)
     int64_t n_src;
-    int64_t per_chain;
+    int64_t n_chains;
     const uint16_t *chain_w;     // mode 0: workload of each chain (nullable)
     int w;
     uint64_t offset_w;
