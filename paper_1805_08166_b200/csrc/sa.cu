@@ -39,9 +39,13 @@ __device__ __forceinline__ void feats_any(const WlDev &W, const uint16_t *fact, 
 
 __device__ __forceinline__ int n_loops(int tmpl) { return tmpl == 0 ? 8 : tmpl == 1 ? 18 : 16; }
 
+// TM >= 0: every workload of the space uses template TM (compile-time: one code path, a smaller
+// hot loop); TM = -1: per-lane dispatch (mixed-template unions)
+template <int TM>
 __device__ __forceinline__ void zero_cols_any(int tmpl, float *tile, int lane)
 {
     TileSink sk{tile, lane};
+    if (TM >= 0) { features_zero_cols<TM < 0 ? 0 : TM>(sk); return; }
     switch (tmpl) {
     case 0: features_zero_cols<0>(sk); break;
     case 1: features_zero_cols<1>(sk); break;
@@ -49,12 +53,17 @@ __device__ __forceinline__ void zero_cols_any(int tmpl, float *tile, int lane)
     }
 }
 
+template <int TM>
 __device__ __forceinline__ void decode_any(const WlDev &W, uint32_t local, uint32_t *ch)
 {
-    switch (W.tmpl) {
-    case 0: decode_knobs<0>(W, local, ch); break;
-    case 1: decode_knobs<1>(W, local, ch); break;
-    default: decode_knobs<2>(W, local, ch); break;
+    if (TM >= 0) {
+        decode_knobs<TM < 0 ? 0 : TM>(W, local, ch);
+    } else {
+        switch (W.tmpl) {
+        case 0: decode_knobs<0>(W, local, ch); break;
+        case 1: decode_knobs<1>(W, local, ch); break;
+        default: decode_knobs<2>(W, local, ch); break;
+        }
     }
 #pragma unroll
     for (int j = 0; j < MAXKNOBS; ++j)
@@ -92,9 +101,11 @@ struct SaSmem {
     uint64_t bar[2];
 };
 
+template <int TM>
 __device__ __forceinline__ void sa_row_any(const WlDev &W, const uint32_t *ext, const uint32_t *ch, int k, int lane,
                                            float *tile)
 {
+    if (TM >= 0) { sa_row_rel<TM < 0 ? 0 : TM>(W, ext, ch, k, lane, tile); return; }
     switch (W.tmpl) {
     case 0: sa_row_rel<0>(W, ext, ch, k, lane, tile); break;
     case 1: sa_row_rel<1>(W, ext, ch, k, lane, tile); break;
@@ -102,9 +113,11 @@ __device__ __forceinline__ void sa_row_any(const WlDev &W, const uint32_t *ext, 
     }
 }
 
+template <int TM>
 __device__ __forceinline__ void sa_extents_any(int tmpl, const uint32_t (&foff)[6], const uint16_t *fact,
                                                const uint32_t *ch, uint32_t *ext)
 {
+    if (TM >= 0) { sa_extents<TM < 0 ? 0 : TM>(foff, fact, ch, ext); return; }
     switch (tmpl) {
     case 0: sa_extents<0>(foff, fact, ch, ext); break;
     case 1: sa_extents<1>(foff, fact, ch, ext); break;
@@ -123,7 +136,7 @@ __device__ __forceinline__ void zero_relation(float (*tile)[NFEAT * 32], int lan
 // Block = GRP groups of 32 chains (lane = chain) x SA_NW warps.  Warp g owns group g's chain
 // state; every warp takes part in every group's feature phases and tree walk, so each tree byte
 // staged in shared memory serves 32 GRP chains.
-template <int GRP, int KM>
+template <int GRP, int KM, int TM>
 __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G)
 {
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -177,15 +190,15 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         } else {
             idx = W.offset;
         }
-        decode_any(W, (uint32_t)(idx - W.offset), ch);
+        decode_any<TM>(W, (uint32_t)(idx - W.offset), ch);
 #pragma unroll
         for (int j = 0; j < MAXKNOBS; ++j) sm.ch[og][j][lane] = ch[j];
 #pragma unroll
         for (int q = 0; q < 6; ++q) foff[q] = W.fact_off[q];
         tmpl = W.tmpl;
-        sa_extents_any(tmpl, foff, P.fact, ch, &sm.ext[og][0][lane]);
+        sa_extents_any<TM>(tmpl, foff, P.fact, ch, &sm.ext[og][0][lane]);
         sm.w[og][lane] = w;
-        zero_cols_any(W.tmpl, sm.tile[og], lane);
+        zero_cols_any<TM>(W.tmpl, sm.tile[og], lane);
     } else {
         zero_relation<GRP>(sm.tile, lane, warp);
     }
@@ -206,7 +219,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
             uint32_t chl[MAXKNOBS];
 #pragma unroll
             for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[g][j][lane];
-            sa_row_any(P.S->w[sm.w[g][lane]], &sm.ext[g][0][lane], chl, k, lane, sm.tile[g]);
+            sa_row_any<TM>(P.S->w[sm.w[g][lane]], &sm.ext[g][0][lane], chl, k, lane, sm.tile[g]);
         }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
@@ -273,7 +286,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == j) sm.ch[og][q][lane] = v2;
             }
-            sa_extents_any(tmpl, foff, P.fact, ch, &sm.ext[og][0][lane]);   // the proposal's loop extents
+            sa_extents_any<TM>(tmpl, foff, P.fact, ch, &sm.ext[og][0][lane]);   // the proposal's loop extents
         }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
@@ -421,21 +434,26 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     const at::TreeGeo G = use2 ? G2 : G1;
     const size_t smem = acq ? at::sa_smem_bytes<1, 8>(G) : use2 ? at::sa_smem_bytes<2>(G) : at::sa_smem_bytes<1>(G);
     if (smem > SMEM_MAX) return at::fail(AT_EUNSUPPORTED, "sa_explore: shared memory budget exceeded");
-    const void *kern = acq ? (const void *)at::sa_kernel<1, 8>
-                     : use2 ? (const void *)at::sa_kernel<2, 1> : (const void *)at::sa_kernel<1, 1>;
-    static size_t attr[3] = {0, 0, 0};
-    const int ai = acq ? 2 : use2 ? 1 : 0;
+    // one template for every workload of the space: the compile-time specialised kernel
+    int tm = sp->host.w[0].tmpl;
+    for (int q = 1; q < sp->host.n_w; ++q)
+        if (sp->host.w[q].tmpl != tm) tm = -1;
+    if (acq) tm = -1;
+    using KF = void (*)(at::SaParams, at::TreeGeo);
+    const KF k1[4] = {at::sa_kernel<1, 1, -1>, at::sa_kernel<1, 1, 0>, at::sa_kernel<1, 1, 1>, at::sa_kernel<1, 1, 2>};
+    const KF k2[4] = {at::sa_kernel<2, 1, -1>, at::sa_kernel<2, 1, 0>, at::sa_kernel<2, 1, 1>, at::sa_kernel<2, 1, 2>};
+    const KF kern = acq ? at::sa_kernel<1, 8, -1> : use2 ? k2[tm + 1] : k1[tm + 1];
+    static size_t attr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const int ai = acq ? 8 : (use2 ? 4 : 0) + tm + 1;
     if (smem > attr[ai]) {
-        AT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AT_CUDA_TRY(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[ai] = smem;
     }
     {
         at::ProfScope ps(AT_K_SA, s);
         const int cpb = use2 ? 64 : 32;
         const unsigned blocks = (unsigned)((o->n_chains + cpb - 1) / cpb);
-        if (acq) at::sa_kernel<1, 8><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
-        else if (use2) at::sa_kernel<2, 1><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
-        else at::sa_kernel<1, 1><<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
+        kern<<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
         at::note_launch();
         AT_LAUNCH_CHECK("sa_kernel");
     }
