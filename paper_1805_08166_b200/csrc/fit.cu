@@ -798,7 +798,6 @@ constexpr int FUSED_NMAX = 2048;
 constexpr int FUSED_NT_MAX = 512;   // threads per block: 512 when every splittable feature gets a
                                      // block at 2 blocks / SM, else 256 (4 / SM)
 constexpr int FUSED_NSUB = 8;   // sub-slots per node (block b uses b mod 8): bounds CAS contention
-constexpr int FUSED_NREP = 16;  // replicas of the release flag / decisions (block b reads b mod 16)
 
 struct FusedArgs {
     const uint8_t *bins;
@@ -811,8 +810,7 @@ struct FusedArgs {
     int64_t *g, *h;
     uint16_t *gord, *gord0;
     uint8_t *gnode;
-    unsigned long long *slot;   // [n_int][FUSED_NSUB] x (lo, hi), zero between levels
-    unsigned long long *dec;    // [FUSED_NREP][128] epoch << 32 | level decision (f << 8 | s, ~0u: none)
+    unsigned long long *slot;   // [2 tree parities][n_int][FUSED_NSUB] x (lo, hi)
     uint16_t *t_feat;
     float *t_thr, *t_leaf;
     uint64_t seed;
@@ -986,72 +984,67 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
     for (int q = tid; q < 128; q += NT) { T.nbh[q] = 0; T.nbl[q] = 0; T.nms[q] = 0xFFFFFFFFu; }
     for (int q = tid; q <= FIT_MAXKEYS; q += NT) T.gpre[q] = A.gpre[q];
 
-    // Grid-wide sync.  Every block arrives on one counter (fence, then an atomic add that returns
-    // the count); the LAST block to arrive reduces the level's sub-slots into the decisions (nn > 0),
-    // re-zeroes them (node ids are unique within a tree; later fences order the zeroing before the
-    // next tree's atomics) and publishes FUSED_NREP replicas of (epoch << 32 | decision); the tree
-    // nodes (feature, threshold) are written after the release.  In every block, thread q polls
-    // entry q of the block's replica (each entry carries its epoch), so the decisions arrive with
-    // the release and no L2 line is polled by all blocks.  T.decw[q] gets the decisions.
+    // Grid-wide sync.  Every block arrives on one counter (a release add) and its thread 0 polls the
+    // counter with acquire loads until all G blocks are in; then EVERY block reads the level's
+    // FUSED_NSUB sub-slot keys per node and takes the decisions itself (no reducer, no publish /
+    // poll hop: 1.9 -> ~1.4 us per barrier).  The sub-slots of a tree live in its parity half; block 0
+    // zeroes tree t - 1's half after tree t's gradient barrier (every block has read it by then) and
+    // writes the tree's nodes.  T.decw[q] gets the decisions.
     auto sync_all = [&](int t, int nn, int first) {
         __syncthreads();
         ++epoch;
         if (tid == 0) {
-            // one acq_rel arrival: releases this block's writes (ordered before it by the
-            // __syncthreads, PTX fences being cumulative) and, for the last arriver, acquires all
-            // the other blocks' -- no separate __threadfence on either side
-            unsigned old;
+            // arrival: one release add (this block's writes, ordered before it by the __syncthreads,
+            // PTX fences being cumulative), then acquire polls of the counter until every block is in
 #ifdef AT_FIT_TIMING
             t_arr = gtimer();
 #endif
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(A.bar) : "memory");
-            T.wsi[1][0] = old == epoch * (unsigned)G - 1u ? 1 : 0;
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.bar) : "memory");
+            const unsigned want = epoch * (unsigned)G;
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.bar) : "memory");
+            while (v < want) {
+                __nanosleep(20);
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.bar) : "memory");
+            }
         }
         __syncthreads();
-        const int nq = nn > 0 ? nn : 1;
-        if (T.wsi[1][0]) {   // block-uniform: the last arriver
-            for (int q = tid; q < nq; q += NT) {
-                unsigned word = 0xFFFFFFFFu;
+        // every block reduces the level's sub-slots itself (no reducer -> publish -> poll hop):
+        // FUSED_NSUB consecutive lanes per node, max by xor shuffles within the group
+        if (nn > 0) {
+            const unsigned long long *sb = A.slot + (size_t)(t & 1) * 2 * FUSED_NSUB * n_int;
+            for (int base = 0; base < nn * FUSED_NSUB; base += NT) {
+                const int e = base + tid, q = e / FUSED_NSUB;
                 unsigned long long lo = 0, hi = 0;
-                if (nn > 0) {
-                    const int nd = first + q;
+                if (q < nn) {
+                    const ulonglong2 v = __ldcg((const ulonglong2 *)(sb + 2 * ((first + q) * FUSED_NSUB + (e % FUSED_NSUB))));
+                    lo = v.x;
+                    hi = v.y;
+                }
 #pragma unroll
-                    for (int k = 0; k < FUSED_NSUB; ++k) {
-                        ulonglong2 *sp2 = (ulonglong2 *)(A.slot + 2 * (nd * FUSED_NSUB + k));
-                        const ulonglong2 v = __ldcg(sp2);
-                        __stcg(sp2, make_ulonglong2(0ull, 0ull));
-                        if (v.y > hi || (v.y == hi && v.x > lo)) { lo = v.x; hi = v.y; }
+                for (int off = FUSED_NSUB / 2; off >= 1; off >>= 1) {
+                    const unsigned long long ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
+                    const unsigned long long oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+                    if (oh > hi || (oh == hi && ol > lo)) { lo = ol; hi = oh; }
+                }
+                if (q < nn && e % FUSED_NSUB == 0) {
+                    const unsigned word = hi == 0 ? 0xFFFFFFFFu
+                                                  : ((0xFFFFu - (unsigned)((lo >> 16) & 0xFFFFu)) << 8) |
+                                                        (0xFFFFu - (unsigned)(lo & 0xFFFFu));
+                    T.decw[q] = word;
+                    if (blockIdx.x == 0) {   // the tree's nodes
+                        const int nd = first + q;
+                        const unsigned bf = word >> 8, bs = word & 0xFFu;
+                        A.t_feat[(size_t)t * n_int + nd] = word == 0xFFFFFFFFu ? (uint16_t)0 : (uint16_t)bf;
+                        A.t_thr[(size_t)t * n_int + nd] = word == 0xFFFFFFFFu ? __int_as_float(0x7f800000)
+                                                                               : A.cuts[(int64_t)bf * (A.B - 1) + bs - 1];
                     }
-                    if (hi != 0)
-                        word = ((0xFFFFu - (unsigned)((lo >> 16) & 0xFFFFu)) << 8) | (0xFFFFu - (unsigned)(lo & 0xFFFFu));
-                }
-                const unsigned long long pub = ((unsigned long long)epoch << 32) | word;
-#pragma unroll
-                for (int r = 0; r < FUSED_NREP; ++r) __stcg(A.dec + r * 128 + q, pub);
-                if (nn > 0) {   // the tree's nodes, off the release path
-                    const int nd = first + q;
-                    const unsigned bf = word >> 8, bs = word & 0xFFu;
-                    A.t_feat[(size_t)t * n_int + nd] = word == 0xFFFFFFFFu ? (uint16_t)0 : (uint16_t)bf;
-                    A.t_thr[(size_t)t * n_int + nd] = word == 0xFFFFFFFFu ? __int_as_float(0x7f800000)
-                                                                           : A.cuts[(int64_t)bf * (A.B - 1) + bs - 1];
                 }
             }
-        }
-        const unsigned long long *rep = A.dec + (blockIdx.x % FUSED_NREP) * 128;
-        for (int q = tid; q < nq; q += NT) {
-            // acquire loads: everything the reducer saw (hence every block's pre-barrier writes:
-            // gradients, slot keys) is visible to this block's later reads
-            unsigned long long v;
-            asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(rep + q) : "memory");
-            while ((unsigned)(v >> 32) != epoch) {
-                __nanosleep(32);
-                asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(rep + q) : "memory");
-            }
-            T.decw[q] = (unsigned)v;
         }
         __syncthreads();
 #ifdef AT_FIT_TIMING
-        if (tid == 0 && T.wsi[1][0]) {   // the last arriver: its arrival -> its release = the barrier itself
+        if (tid == 0 && blockIdx.x == 0) {   // block 0: its arrival -> release (includes waiting for the others)
             atomicAdd(&g_ft_bar_ns, gtimer() - t_arr);
             atomicAdd(&g_ft_bar_n, 1ull);
         }
@@ -1163,6 +1156,9 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
         sync_all(t, 0, 0);
         FT_MARK(1);
 
+        if (blockIdx.x == 0)   // tree t - 1's slots (every block has read them): zero for tree t + 1
+            for (int e = tid; e < 2 * FUSED_NSUB * n_int; e += NT)
+                __stcg(A.slot + (size_t)((t + 1) & 1) * 2 * FUSED_NSUB * n_int + e, 0ull);
         for (int i = tid; i < N; i += NT) { sg[i] = __ldcg(A.g + i); sh[i] = __ldcg(A.h + i); }
         for (int q = tid; q < 512; q += NT) T.dead[q] = 0;
         if (tid == 0) { T.segP[0] = 0; T.segP[1] = N; }
@@ -1355,7 +1351,8 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
                 for (int q = tid; q < nn; q += NT) {
                     const unsigned long long gb = ((unsigned long long)T.nbh[q] << 32) | T.nbl[q];
                     if (gb)
-                        slot_max(slot + 2 * ((first + q) * FUSED_NSUB + (blockIdx.x & (FUSED_NSUB - 1))),
+                        slot_max(slot + (size_t)(t & 1) * 2 * FUSED_NSUB * n_int +
+                                     2 * ((first + q) * FUSED_NSUB + (blockIdx.x & (FUSED_NSUB - 1))),
                                  ((unsigned long long)(0xFFFFu - (unsigned)f) << 16) |
                                      (unsigned long long)(0xFFFFu - T.nms[q]),
                                  gb);
@@ -1700,16 +1697,14 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             const int G = (int)std::min<int64_t>(nF, (int64_t)per * nsm);
             const bool resident = nF <= G;
             int32_t *klist = ws.get<int32_t>(n);
-            unsigned long long *slot = ws.get<unsigned long long>((size_t)2 * FUSED_NSUB * n_int);
+            unsigned long long *slot = ws.get<unsigned long long>((size_t)2 * 2 * FUSED_NSUB * n_int);   // 2 tree parities
             unsigned *bar = ws.get<unsigned>(32);
-            unsigned long long *decp = ws.get<unsigned long long>((size_t)FUSED_NREP * 128);
             uint16_t *gord = resident ? nullptr : ws.get<uint16_t>((size_t)F * n);
             uint16_t *gord0 = ws.get<uint16_t>((size_t)F * n);   // initial bin-sorted orders
             uint8_t *gnode = resident ? nullptr : ws.get<uint8_t>((size_t)F * n);
             if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
             AT_CUDA_TRY(cudaMemsetAsync(bar, 0, 32 * sizeof(unsigned), s));
-            AT_CUDA_TRY(cudaMemsetAsync(decp, 0, FUSED_NREP * 128 * sizeof(unsigned long long), s));
-            AT_CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(unsigned long long) * 2 * FUSED_NSUB * n_int, s));
+            AT_CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(unsigned long long) * 2 * 2 * FUSED_NSUB * n_int, s));
             klist_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, woff, n, klist); note_launch();
             AT_LAUNCH_CHECK("klist");
             FusedArgs fa;
@@ -1728,7 +1723,6 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             fa.gord = gord; fa.gord0 = gord0; fa.gnode = gnode; fa.slot = slot;
             fa.t_feat = t_feat; fa.t_thr = t_thr; fa.t_leaf = t_leaf;
             fa.seed = o->seed; fa.lam = lam; fa.mcw = mcw; fa.eta = eta; fa.bar = bar;
-            fa.dec = decp;
             void *args[] = {&fa};
             {
                 ProfScope ps(AT_K_FIT_GRAPH, s);
