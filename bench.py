@@ -230,6 +230,13 @@ def run_ours(args):
                 "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)", "peak_source": "148 SMs x 16 node-steps/clk (two 128-B L1/shared wavefronts per "
                                                  "warp node-step) x sm_max_mhz of MEASURED_PEAKS.json",
                 "avg_launch_ms": round(sa_avg, 4), "step_share": shares}
+    # the walk's measured ceiling: tools/micro/walk_ceiling.cu (the same node-step instruction pattern,
+    # everything in shared memory, no barriers, up to 24 walks per warp) plateaus at this rate
+    wpath = os.path.join(ROOT, "profiles", "r01_walk_ceiling.json")
+    if os.path.exists(wpath):
+        wc = max(r.get("Gnode_steps_per_s", 0.0) for r in json.load(open(wpath))["results"] if "error" not in r)
+        roofline["walk_ceiling_measured"] = round(wc, 1)
+        roofline["frac_of_measured_ceiling"] = round(achieved / wc, 4)
 
     # ---- scoring sweep: features_extract + gbt_predict on 2^20 candidates (HBM roofline of the feature stream)
     sweep = None if args.quick else scoring_sweep(space, model, dev, stream, peaks)
