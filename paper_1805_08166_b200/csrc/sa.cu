@@ -94,8 +94,12 @@ struct SaSmem {
     float tile[GRP][NFEAT * 32];
     float part[GRP][KM * 32 * 32];
     float fk[GRP][KM > 1 ? KM * 32 : 1];   // per-model energies (KM > 1)
-    uint32_t ch[GRP][MAXKNOBS][32];
-    uint32_t ext[GRP][MAXLOOPS][32];      // loop extents of each chain's current proposal (owner-written)
+    uint32_t chb[2][GRP][MAXKNOBS][32];   // proposal knob vectors, by step parity (owner-written)
+    int32_t pjs[2][GRP][32];              // ... the move that made it (knob, -1: none) and the old value
+    uint32_t pvs[2][GRP][32];
+    uint32_t extc[2][GRP][MAXLOOPS][32];  // loop extents of the next proposal for both outcomes of the
+                                          // current step (0: accepted, 1: rejected), by helper warps
+    uint32_t esel[GRP][32];               // which one the owner's decision selected
     uint32_t rnd[GRP][4][32];             // the next step's Philox words, precomputed by a helper warp
     int32_t w[GRP][32];
     uint64_t bar[2];
@@ -191,12 +195,16 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
             idx = W.offset;
         }
         decode_any<TM>(W, (uint32_t)(idx - W.offset), ch);
+        // the start state is "step -1's proposal": parity 1, no move; its extents in candidate 0
 #pragma unroll
-        for (int j = 0; j < MAXKNOBS; ++j) sm.ch[og][j][lane] = ch[j];
+        for (int j = 0; j < MAXKNOBS; ++j) sm.chb[1][og][j][lane] = ch[j];
+        sm.pjs[1][og][lane] = -1;
+        sm.pvs[1][og][lane] = 0u;
+        sm.esel[og][lane] = 0u;
 #pragma unroll
         for (int q = 0; q < 6; ++q) foff[q] = W.fact_off[q];
         tmpl = W.tmpl;
-        sa_extents_any<TM>(tmpl, foff, P.fact, ch, &sm.ext[og][0][lane]);
+        sa_extents_any<TM>(tmpl, foff, P.fact, ch, &sm.extc[0][og][0][lane]);
         sm.w[og][lane] = w;
         zero_cols_any<TM>(W.tmpl, sm.tile[og], lane);
     } else {
@@ -212,14 +220,14 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     long long t_prop = 0, t_feat = 0, t_walk = 0, t_rows = 0, t0 = clock64();
 #endif
     // every warp computes its share of the features of all chains of the block
-    auto features_phase = [&]() {
+    auto features_phase = [&](int par) {
         // R) context rows and their relation deposits: items (group, row)
         for (int it = warp; it < GRP * MAXLOOPS; it += SA_NW) {
             const int g = it / MAXLOOPS, k = it - g * MAXLOOPS;
             uint32_t chl[MAXKNOBS];
 #pragma unroll
-            for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.ch[g][j][lane];
-            sa_row_any<TM>(P.S->w[sm.w[g][lane]], &sm.ext[g][0][lane], chl, k, lane, sm.tile[g]);
+            for (int j = 0; j < MAXKNOBS; ++j) chl[j] = sm.chb[par][g][j][lane];
+            sa_row_any<TM>(P.S->w[sm.w[g][lane]], &sm.extc[sm.esel[g][lane]][g][0][lane], chl, k, lane, sm.tile[g]);
         }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
@@ -245,13 +253,49 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
             sm.rnd[g][3][lane] = r.w;
         }
     };
-    features_phase();
+    // While the owner warps decide step s (serial, after the walk), helper warps GRP + 2g + b build
+    // the loop extents of step s + 1's proposal for group g under both outcomes -- b = 0: the move
+    // applied to step s's proposal (accepted), b = 1: to the state before it (rejected) -- so the
+    // owner's proposal needs no extents of its own; the proposal barrier publishes them.
+    auto precompute = [&](int s_next, int par) {   // par: parity of step s_next - 1's proposal
+        const int hw = warp - GRP;
+        if (hw >= 0 && hw < 2 * GRP && s_next < P.n_steps) {
+            const int g = hw >> 1, b = hw & 1;
+            const uint32_t gc = P.chain_base + (uint32_t)(blockIdx.x * 32 * GRP + g * 32 + lane);
+            const U4 r = philox(P.seed, gc, (uint32_t)s_next, P.round, TAG_SA_STEP);
+            const WlDev &W = P.S->w[sm.w[g][lane]];
+            uint32_t x[MAXKNOBS];
+#pragma unroll
+            for (int j = 0; j < MAXKNOBS; ++j) x[j] = sm.chb[par][g][j][lane];
+            const int pjx = sm.pjs[par][g][lane];
+            const uint32_t pvx = sm.pvs[par][g][lane];
+            if (b == 1)
+#pragma unroll
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == pjx) x[q] = pvx;
+            if (W.n_ns > 0) {   // the owner's move, replayed
+                const int j = W.ns_list[__umulhi(r.x, W.n_ns)];
+                uint32_t v = 0;
+#pragma unroll
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == j) v = x[q];
+                uint32_t v2 = __umulhi(r.y, W.radix[j] - 1u);
+                if (v2 >= v) v2 += 1;
+#pragma unroll
+                for (int q = 0; q < MAXKNOBS; ++q) if (q == j) x[q] = v2;
+            }
+            uint32_t fo[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) fo[q] = W.fact_off[q];
+            sa_extents_any<TM>(W.tmpl, fo, P.fact, x, &sm.extc[b][g][0][lane]);
+        }
+    };
+    features_phase(1);
     draw_next(0);
     ts_wait_resident(G, sm.bar);
     walk_pass<SA_NW, GRP, KM>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp, &sm.part[0][0],
                           nullptr, 0, 0, no_slots);
     fold_models(warp, lane);
     if (!owner) zero_relation<GRP>(sm.tile, lane, warp);
+    precompute(0, 1);
     if (owner) {
         E = energy(og, lane);
         if (live) {
@@ -264,8 +308,10 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     t_prop = t_feat = t_walk = t_rows = 0;
     t0 = clock64();
 #endif
+    bool rejected = false;   // the owner's last decision (selects the precomputed extents)
     for (int s = 0; s < P.n_steps; ++s) {
         U4 r;
+        const int par = s & 1;
         if (owner) {
             const WlDev &W = P.S->w[w];
             r = U4{sm.rnd[og][0][lane], sm.rnd[og][1][lane], sm.rnd[og][2][lane], sm.rnd[og][3][lane]};   // Philox(gid, s)
@@ -283,16 +329,18 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
                 pv = v;
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == j) ch[q] = v2;
-#pragma unroll
-                for (int q = 0; q < MAXKNOBS; ++q) if (q == j) sm.ch[og][q][lane] = v2;
             }
-            sa_extents_any<TM>(tmpl, foff, P.fact, ch, &sm.ext[og][0][lane]);   // the proposal's loop extents
+#pragma unroll
+            for (int q = 0; q < MAXKNOBS; ++q) sm.chb[par][og][q][lane] = ch[q];
+            sm.pjs[par][og][lane] = pj;
+            sm.pvs[par][og][lane] = pv;
+            sm.esel[og][lane] = rejected ? 1u : 0u;   // the helpers' extents of this proposal
         }
         __syncthreads();
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_prop += t - t0; t0 = t; }
 #endif
-        features_phase();
+        features_phase(par);
         draw_next(s + 1);
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
@@ -304,6 +352,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #endif
         fold_models(warp, lane);
         if (!owner) zero_relation<GRP>(sm.tile, lane, warp);
+        precompute(s + 1, par);
         if (owner) {
             const float E2 = energy(og, lane);
             const float d = __fsub_rn(E2, E);
@@ -322,9 +371,8 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
             } else if (pj >= 0) {
 #pragma unroll
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == pj) ch[q] = pv;   // undo the move
-#pragma unroll
-                for (int q = 0; q < MAXKNOBS; ++q) if (q == pj) sm.ch[og][q][lane] = pv;
             }
+            rejected = !acc;
             if (live) {
                 const int64_t at = (int64_t)c * per + s + 1;
                 P.keys[(int64_t)(s + 1) * P.n_chains + c] = ((uint64_t)fkey(E2) << 32) | (uint64_t)(idx2 - P.S->w[w].offset);
