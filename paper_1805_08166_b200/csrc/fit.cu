@@ -180,17 +180,34 @@ __global__ void __launch_bounds__(1024) ranks_kernel(const uint16_t *__restrict_
             __syncthreads();
         }
     }
-    if (tid == 0) {
-        int32_t o = 0, g = 0;
-        for (int k = 0; k < FIT_MAXKEYS; ++k) {
-            counts[k] = cnt[k];
-            woff[k] = o;
-            gprefix[k] = g;
-            o += cnt[k];
-            g += (cnt[k] + group_size - 1) / group_size;
-        }
-        gprefix[FIT_MAXKEYS] = g;
+    // exclusive prefix sums of the counts and of the group counts over the FIT_MAXKEYS keys: one key
+    // per thread (1024 threads), warp shuffles + one shared pass over the warp totals
+    __shared__ int32_t wo[32], wg[32];
+    const int k = tid;   // FIT_MAXKEYS == 1024 == blockDim.x
+    const int32_t c = cnt[k], gk = (c + group_size - 1) / group_size;
+    int32_t xo = c, xg = gk;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int32_t yo = __shfl_up_sync(0xFFFFFFFFu, xo, off), yg = __shfl_up_sync(0xFFFFFFFFu, xg, off);
+        if (lane >= off) { xo += yo; xg += yg; }
     }
+    if (lane == 31) { wo[warp] = xo; wg[warp] = xg; }
+    __syncthreads();
+    if (warp == 0) {
+        int32_t a = wo[lane], b = wg[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int32_t ya = __shfl_up_sync(0xFFFFFFFFu, a, off), yb = __shfl_up_sync(0xFFFFFFFFu, b, off);
+            if (lane >= off) { a += ya; b += yb; }
+        }
+        wo[lane] = a - wo[lane];
+        wg[lane] = b - wg[lane];
+    }
+    __syncthreads();
+    counts[k] = c;
+    woff[k] = wo[warp] + xo - c;
+    gprefix[k] = wg[warp] + xg - gk;
+    if (k == FIT_MAXKEYS - 1) gprefix[FIT_MAXKEYS] = wg[warp] + xg;
 }
 
 __device__ __forceinline__ uint32_t feistel(uint32_t x, int h, uint64_t seed, uint32_t tree, uint32_t wkey)

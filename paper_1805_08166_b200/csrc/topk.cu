@@ -63,7 +63,7 @@ __device__ __forceinline__ uint64_t tk_load(const TkSrc &S, int64_t i)
         gidx = __ldg(S.l_idx + at);
         key = ((uint64_t)fkey(__ldg(S.l_score + at)) << 32) | (uint64_t)(gidx - S.offset_w);
     }
-    if (S.n_measured && in_sorted(S.measured, S.n_measured, gidx)) return KEY_NONE;
+    (void)gidx;   // measured configurations are dropped after the tile's sort (see topk_tile_kernel)
     return key;
 }
 
@@ -88,39 +88,80 @@ __global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, u
             __syncthreads();
         }
     }
-    // distinct: keep keys that differ from their predecessor; compact the first K
+    // distinct: keep keys that differ from their predecessor
     constexpr int PER = TK_TILE / TK_THREADS;   // 4 consecutive keys per thread
+    const int lane = tid & 31, warp = tid >> 5;
     uint64_t v[PER];
     int flag[PER];
-    int cnt = 0;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         const int i = tid * PER + q;
         v[q] = s[i];
         flag[q] = (v[q] != KEY_NONE) && (i == 0 || s[i - 1] != v[q]);
-        cnt += flag[q];
     }
-    // block exclusive scan of cnt
-    const int lane = tid & 31, warp = tid >> 5;
-    int incl = cnt;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-        if (lane >= off) incl += y;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        int x = wsum[lane];
+    // block exclusive scan of per-thread counts; returns this thread's offset, total in *tot
+    auto scan = [&](int c, int *tot) {
+        int incl = c;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
-            if (lane >= off) x += y;
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+            if (lane >= off) incl += y;
         }
-        wsum[lane] = x;   // inclusive
+        __syncthreads();   // wsum reuse
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            int x = wsum[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+                if (lane >= off) x += y;
+            }
+            wsum[lane] = x;   // inclusive
+        }
+        __syncthreads();
+        *tot = wsum[31];
+        return incl - c + (warp > 0 ? wsum[warp - 1] : 0);
+    };
+    // measured configurations: checked only for the distinct keys that can reach the first K --
+    // ranks [0, K), then [K, K + m) for the m measured among those, ... (rarely more than one round)
+    if (S.n_measured && S.mode != 2) {
+        int c0 = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) c0 += flag[q];
+        int tot;
+        const int r0 = scan(c0, &tot);
+        __shared__ int s_m;
+        int lo = 0, hi = K;
+        while (lo < tot) {
+            if (tid == 0) s_m = 0;
+            __syncthreads();
+            int r = r0, m = 0;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                if (flag[q]) {
+                    if (r >= lo && r < hi && in_sorted(S.measured, S.n_measured, S.offset_w + (v[q] & 0xFFFFFFFFull))) {
+                        flag[q] = 2;   // measured: dropped below
+                        ++m;
+                    }
+                    ++r;
+                }
+            }
+            if (m) atomicAdd(&s_m, m);
+            __syncthreads();
+            const int mm = s_m;
+            if (mm == 0) break;
+            lo = hi;
+            hi += mm;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) flag[q] = flag[q] == 1 ? 1 : 0;
     }
-    __syncthreads();
-    int pos = incl - cnt + (warp > 0 ? wsum[warp - 1] : 0);
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) cnt += flag[q];
+    int total_valid;
+    int pos = scan(cnt, &total_valid);
     uint64_t *o = out + (int64_t)blockIdx.x * K;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -129,8 +170,7 @@ __global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, u
             ++pos;
         }
     }
-    const int total = wsum[31];
-    for (int i = total + tid; i < K; i += TK_THREADS) o[i] = KEY_NONE;
+    for (int i = total_valid + tid; i < K; i += TK_THREADS) o[i] = KEY_NONE;
 }
 
 __global__ void topk_finish_kernel(const uint64_t *__restrict__ keys, int K, uint64_t offset_w,
