@@ -798,6 +798,328 @@ __global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int3
 }
 
 
+// ------------------------------------------------------------------ 3b. subtraction path (single rank, large n)
+// Level-by-level like section 3, with the two standard GPU-histogram reductions of work:
+//  * a node's samples are contiguous in a position array (perm), rebuilt per level by a scatter
+//    (left children fill their parent's segment from the front, right children from the back; the
+//    order inside a segment is arbitrary -- every consumer is an order-free integer sum);
+//  * only the smaller child of every split node is histogrammed; the larger one is parent - smaller
+//    (exact in int64), so a tree costs <= n (1 + (D - 1) / 2) sample visits instead of n D.
+// A histogram block owns one node's sample chunk and a range of the splittable features whose cells
+// fit in shared memory; a warp takes one sample (bins read as a row-major u8 row, 4 features per
+// lane-load), lanes map to features, so one warp-wide atomic touches distinct cells.  64-bit cells
+// are two 32-bit words updated by native shared atomics with an explicit carry (smem_add_u64's
+// rule); blocks flush with native 64-bit global atomics.  Node totals travel down the tree
+// (left = the winning split's prefix sums, right = total - left), so the leaves need no extra pass.
+constexpr int SUB_NT = 512;
+constexpr int SUB_CELLS = 6144;   // cells per block: 4 x 4 B x 6144 = 96 KB of shared memory
+constexpr int SUB_MAXR = 64;
+
+struct SubRange {
+    int k_lo, k_hi, c_lo, c_cnt;   // compact features [k_lo, k_hi), cells [c_lo, c_lo + c_cnt)
+};
+
+// bins [F][n] (column-major) -> binsR [n][FsP] over the splittable features flist[0..Fs), zero padded
+__global__ void rowbins_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ flist, int Fs,
+                               int FsP, uint8_t *__restrict__ binsR)
+{
+    __shared__ uint8_t t[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int k0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int k = k0 + r;
+        const int64_t i = i0 + threadIdx.x;
+        t[r][threadIdx.x] = (k < Fs && i < n) ? bins[(int64_t)flist[k] * n + i] : (uint8_t)0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r;
+        const int k = k0 + threadIdx.x;
+        if (i < n && k < FsP) binsR[i * FsP + k] = t[threadIdx.x][r];
+    }
+}
+
+__device__ __forceinline__ void sub_add64(uint32_t *lo, uint32_t *hi, int c, uint32_t vlo, uint32_t vhi)
+{
+    const uint32_t old = atomicAdd(&lo[c], vlo);
+    const uint32_t add = vhi + ((old + vlo < old) ? 1u : 0u);   // exact modular 64-bit sum
+    if (add) atomicAdd(&hi[c], add);
+}
+
+// items[b] = {node slot, p0, p1, -}: block (b, r) adds positions [p0, p1) of perm (identity when
+// perm == nullptr) into the cells of feature range r of hist[slot].
+__global__ void __launch_bounds__(SUB_NT, 2) sub_hist_kernel(const uint8_t *__restrict__ binsR, int FsP,
+                                                             const int32_t *__restrict__ perm,
+                                                             const int64_t *__restrict__ g,
+                                                             const int64_t *__restrict__ h,
+                                                             const int4 *__restrict__ items,
+                                                             const int32_t *__restrict__ n_items,
+                                                             const SubRange *__restrict__ ranges,
+                                                             const int32_t *__restrict__ coffR, int TB,
+                                                             int64_t *__restrict__ hist)
+{
+    extern __shared__ uint32_t sm[];
+    if ((int)blockIdx.x >= *n_items) return;
+    const SubRange R = ranges[blockIdx.y];
+    const int4 it = items[blockIdx.x];
+    const int C = R.c_cnt;
+    uint32_t *glo = sm, *ghi = sm + C, *hlo = sm + 2 * C, *hhi = sm + 3 * C;
+    int32_t *coff = (int32_t *)(sm + 4 * C);   // coff[j * nq + q]: cell base of feature k_lo + 4 q + j
+    const int nf = R.k_hi - R.k_lo, nq = (nf + 3) >> 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int q = tid; q < 4 * C; q += SUB_NT) sm[q] = 0u;
+    for (int q = tid; q < 4 * nq; q += SUB_NT) {
+        const int j = q / nq, qq = q - j * nq, k = R.k_lo + 4 * qq + j;
+        coff[q] = k < R.k_hi ? coffR[k] - R.c_lo : -1;
+    }
+    __syncthreads();
+    for (int p = it.y + warp; p < it.z; p += SUB_NT / 32) {
+        const int i = perm ? perm[p] : p;
+        const unsigned long long gv = (unsigned long long)g[i], hv = (unsigned long long)h[i];
+        if ((gv | hv) == 0ull) continue;   // contributes nothing (warp-uniform)
+        const uint32_t gl = (uint32_t)gv, gh = (uint32_t)(gv >> 32), hl = (uint32_t)hv, hh = (uint32_t)(hv >> 32);
+        const uint32_t *row = (const uint32_t *)(binsR + (int64_t)i * FsP + R.k_lo);
+        for (int q = lane; q < nq; q += 32) {
+            const uint32_t w = row[q];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c0 = coff[j * nq + q];
+                if (c0 >= 0) {
+                    const int c = c0 + (int)((w >> (8 * j)) & 255u);
+                    sub_add64(glo, ghi, c, gl, gh);
+                    sub_add64(hlo, hhi, c, hl, hh);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    unsigned long long *hn = (unsigned long long *)(hist + ((int64_t)it.x * TB + R.c_lo) * 2);
+    for (int c = tid; c < C; c += SUB_NT) {
+        const unsigned long long G = (unsigned long long)glo[c] | ((unsigned long long)ghi[c] << 32);
+        const unsigned long long H = (unsigned long long)hlo[c] | ((unsigned long long)hhi[c] << 32);
+        if (G) atomicAdd(&hn[2 * c], G);
+        if (H) atomicAdd(&hn[2 * c + 1], H);
+    }
+}
+
+// root items: chunks of [0, n) for node slot 0
+__global__ void sub_root_items_kernel(int n, int target, int4 *__restrict__ items, int32_t *__restrict__ n_items)
+{
+    const int ch = max(64, (n + target - 1) / target);
+    const int m = (n + ch - 1) / ch;
+    for (int b = threadIdx.x; b < m; b += blockDim.x) items[b] = make_int4(0, b * ch, min(n, (b + 1) * ch), 0);
+    if (threadIdx.x == 0) *n_items = m;
+}
+
+// root totals from the cells of the first splittable feature (its bins partition the samples),
+// the root segment, and (parity hook) the single cell of every constant feature
+__global__ void sub_root_tot_kernel(int64_t *__restrict__ hist, const int32_t *__restrict__ boff,
+                                    const int32_t *__restrict__ flist, int F, int n, int fill_const,
+                                    int64_t *__restrict__ tot, int32_t *__restrict__ seg_start,
+                                    int32_t *__restrict__ seg_cnt)
+{
+    __shared__ long long s_t[2];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        const int f = flist[0];
+        long long G = 0, H = 0;
+        for (int b = boff[f] + lane; b < boff[f + 1]; b += 32) { G += hist[2 * b]; H += hist[2 * b + 1]; }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            G += __shfl_xor_sync(0xFFFFFFFFu, G, off);
+            H += __shfl_xor_sync(0xFFFFFFFFu, H, off);
+        }
+        if (lane == 0) {
+            tot[0] = G; tot[1] = H; s_t[0] = G; s_t[1] = H;
+            seg_start[0] = 0; seg_cnt[0] = n;
+        }
+    }
+    __syncthreads();
+    if (fill_const)
+        for (int f = threadIdx.x; f < F; f += blockDim.x)
+            if (boff[f + 1] - boff[f] == 1) { hist[2 * boff[f]] = s_t[0]; hist[2 * boff[f] + 1] = s_t[1]; }
+}
+
+// warp per (node, splittable feature): best split from the node histogram and the node totals
+__global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restrict__ hist,
+                                                        const int32_t *__restrict__ boff,
+                                                        const int32_t *__restrict__ flist, int Fs, int TB, int first,
+                                                        int nn, const int64_t *__restrict__ tot, double lam,
+                                                        double mcw, const uint8_t *__restrict__ dead,
+                                                        double *__restrict__ best_gain, int32_t *__restrict__ best_s)
+{
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (gw >= nn * Fs) return;
+    const int q = gw / Fs, k = gw - q * Fs;
+    const int nd = first + q, f = flist[k];
+    if (dead[nd]) {
+        if (lane == 0) best_s[(int64_t)q * Fs + k] = 0;
+        return;
+    }
+    const SplitBest best = scan_splits(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f], tot[2 * nd],
+                                       tot[2 * nd + 1], lam, mcw, f, lane);
+    if (lane == 0) {
+        best_gain[(int64_t)q * Fs + k] = best.gain;
+        best_s[(int64_t)q * Fs + k] = best.f < 0 ? 0 : best.s;
+    }
+}
+
+// warp per node: the winner over features, the tree node, and the children's totals
+__global__ void __launch_bounds__(256) sub_decide_kernel(const double *__restrict__ best_gain,
+                                                         const int32_t *__restrict__ best_s,
+                                                         const int32_t *__restrict__ flist, int Fs, int first, int nn,
+                                                         const float *__restrict__ cuts, int B,
+                                                         const int64_t *__restrict__ hist,
+                                                         const int32_t *__restrict__ boff, int TB,
+                                                         uint8_t *__restrict__ dead, int32_t *__restrict__ split_f,
+                                                         int32_t *__restrict__ split_s, uint16_t *__restrict__ tree_feat,
+                                                         float *__restrict__ tree_thr, int64_t *__restrict__ tot)
+{
+    const int lane = threadIdx.x & 31;
+    const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (q >= nn) return;
+    const int nd = first + q;
+    SplitBest best{0.0, -1, 0};
+    if (!dead[nd]) {
+        for (int k = lane; k < Fs; k += 32) {
+            const int s = best_s[(int64_t)q * Fs + k];
+            if (s > 0) {
+                SplitBest c{best_gain[(int64_t)q * Fs + k], flist[k], s};
+                if (split_better(c, best)) best = c;
+            }
+        }
+    }
+    best = warp_best(best);
+    const long long G = tot[2 * nd], H = tot[2 * nd + 1];
+    if (best.f < 0) {
+        if (lane == 0) {
+            tree_feat[nd] = 0;
+            tree_thr[nd] = __int_as_float(0x7f800000);
+            split_f[nd] = -1;
+            dead[2 * nd + 1] = 1;
+            dead[2 * nd + 2] = 1;
+            tot[2 * (2 * nd + 1)] = G; tot[2 * (2 * nd + 1) + 1] = H;
+            tot[2 * (2 * nd + 2)] = 0; tot[2 * (2 * nd + 2) + 1] = 0;
+        }
+        return;
+    }
+    const int64_t *hf = hist + ((int64_t)q * TB + boff[best.f]) * 2;
+    long long GL = 0, HL = 0;
+    for (int b = lane; b < best.s; b += 32) { GL += hf[2 * b]; HL += hf[2 * b + 1]; }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        GL += __shfl_xor_sync(0xFFFFFFFFu, GL, off);
+        HL += __shfl_xor_sync(0xFFFFFFFFu, HL, off);
+    }
+    if (lane == 0) {
+        tree_feat[nd] = (uint16_t)best.f;
+        tree_thr[nd] = cuts[(int64_t)best.f * (B - 1) + best.s - 1];
+        split_f[nd] = best.f;
+        split_s[nd] = best.s;
+        tot[2 * (2 * nd + 1)] = GL; tot[2 * (2 * nd + 1) + 1] = HL;
+        tot[2 * (2 * nd + 2)] = G - GL; tot[2 * (2 * nd + 2) + 1] = H - HL;
+    }
+}
+
+// samples of level-d nodes move to their children: node ids, and positions in the parent's segment
+// (left from the front, right from the back); cursor[2 q + right] counts them
+__global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restrict__ bins, int64_t n,
+                                                          const int32_t *__restrict__ split_f,
+                                                          const int32_t *__restrict__ split_s, int first, int nn,
+                                                          const int32_t *__restrict__ seg_start,
+                                                          const int32_t *__restrict__ seg_cnt,
+                                                          int32_t *__restrict__ cursor, int32_t *__restrict__ node,
+                                                          int32_t *__restrict__ perm)
+{
+    __shared__ int sc[256], sbase[256];
+    const int tid = threadIdx.x;
+    for (int q = tid; q < 2 * nn; q += blockDim.x) sc[q] = 0;
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
+    const bool ok = i < n;
+    int nd = 0, slot = 0, r = 0, right = 0;
+    if (ok) {
+        nd = node[i];
+        const int sf = split_f[nd];
+        right = (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= split_s[nd]) ? 1 : 0;
+        slot = (nd - first) * 2 + right;
+        r = atomicAdd(&sc[slot], 1);
+    }
+    __syncthreads();
+    for (int q = tid; q < 2 * nn; q += blockDim.x)
+        if (sc[q]) sbase[q] = atomicAdd(&cursor[q], sc[q]);
+    __syncthreads();
+    if (ok) {
+        node[i] = 2 * nd + 1 + right;
+        const int o = sbase[slot] + r;
+        perm[right ? seg_start[nd] + seg_cnt[nd] - 1 - o : seg_start[nd] + o] = (int32_t)i;
+    }
+}
+
+// one block: children's segments, the smaller child of every split node as histogram items (chunks
+// of <= ch positions), and the (parent, smaller, larger) slot triples for the subtraction
+__global__ void sub_worklist_kernel(int first, int nn, const int32_t *__restrict__ split_f,
+                                    const int32_t *__restrict__ cursor, int32_t *__restrict__ seg_start,
+                                    int32_t *__restrict__ seg_cnt, int target, int4 *__restrict__ items,
+                                    int32_t *__restrict__ n_items, int4 *__restrict__ subs, int32_t *__restrict__ n_subs)
+{
+    __shared__ int s_small[128], s_cs[128], s_alive[128];
+    const int q = threadIdx.x;
+    const int cfirst = 2 * first + 1;   // first node of level d + 1
+    if (q < nn) {
+        const int nd = first + q;
+        const int L = cursor[2 * q], Rc = cursor[2 * q + 1];
+        seg_start[2 * nd + 1] = seg_start[nd];
+        seg_cnt[2 * nd + 1] = L;
+        seg_start[2 * nd + 2] = seg_start[nd] + L;
+        seg_cnt[2 * nd + 2] = Rc;
+        s_alive[q] = split_f[nd] >= 0;
+        s_small[q] = L <= Rc ? 2 * nd + 1 : 2 * nd + 2;
+        s_cs[q] = L <= Rc ? L : Rc;
+    }
+    __syncthreads();
+    if (q == 0) {
+        long long total = 0;
+        for (int p = 0; p < nn; ++p) total += s_alive[p] ? s_cs[p] : 0;
+        const int ch = (int)max(64ll, (total + target - 1) / target);
+        int m = 0, ns = 0;
+        for (int p = 0; p < nn; ++p) {
+            if (!s_alive[p]) continue;
+            const int sm_nd = s_small[p], big = (sm_nd & 1) ? sm_nd + 1 : sm_nd - 1;
+            subs[ns++] = make_int4(p, sm_nd - cfirst, big - cfirst, 0);
+            const int st = seg_start[sm_nd], cnt = s_cs[p];
+            for (int o = 0; o < cnt; o += ch) items[m++] = make_int4(sm_nd - cfirst, st + o, st + min(cnt, o + ch), 0);
+        }
+        *n_items = m;
+        *n_subs = ns;
+    }
+}
+
+// larger child = parent - smaller child, every cell (exact int64)
+__global__ void sub_subtract_kernel(const int64_t *__restrict__ parent, int64_t *__restrict__ child, int TB,
+                                    const int4 *__restrict__ subs, const int32_t *__restrict__ n_subs)
+{
+    if ((int)blockIdx.y >= *n_subs) return;
+    const int4 s = subs[blockIdx.y];
+    const int64_t m = 2 * (int64_t)TB;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x)
+        child[s.z * m + c] = parent[s.x * m + c] - child[s.y * m + c];
+}
+
+// last level: every sample's leaf, prediction update in tree order
+__global__ void sub_final_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ node,
+                                 const int32_t *__restrict__ split_f, const int32_t *__restrict__ split_s, int n_int,
+                                 const float *__restrict__ leaf, float *__restrict__ pred)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nd = node[i];
+    const int sf = split_f[nd];
+    const int child = (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= split_s[nd]) ? 2 * nd + 2 : 2 * nd + 1;
+    pred[i] = __fadd_rn(pred[i], leaf[child - n_int]);
+}
+
 // ------------------------------------------------------------------ 4. fused forest (single rank, small n)
 // One cooperative launch fits the whole forest when the training set is small (Algorithm 1's D:
 // hundreds to a few thousand measured configurations).  Block b owns features b, b + G, ...; each
@@ -1620,6 +1942,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
 
     // input checks + cuts + groups; one host sync reads back the sizes the launches need
     int info[8] = {0};
+    std::vector<int32_t> ncuts_h(F);
     {
         ProfScope ps(AT_K_FIT_PREP, s);
         AT_CUDA_TRY(cudaMemsetAsync(d_info, 0, 8 * sizeof(int32_t), s));
@@ -1637,6 +1960,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             AT_CUDA_TRY(cudaMemsetAsync(pred, 0, sizeof(float) * n, s));
         AT_LAUNCH_CHECK("fit prep");
         AT_CUDA_TRY(cudaMemcpyAsync(info, d_info, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        AT_CUDA_TRY(cudaMemcpyAsync(ncuts_h.data(), ncuts, F * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         AT_CUDA_TRY(cudaStreamSynchronize(s));
     }
     if (info[2] == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
@@ -1747,6 +2071,181 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                                                         fsm, s));
                 note_launch();
             }
+            return finish();
+        }
+    }
+
+    // a single-rank fit has no host callback between levels: its launches are captured once into a
+    // CUDA graph and launched as one unit (no host round trips for ~10 launches per level)
+    auto run_captured = [&](auto &&enqueue) -> int {
+        static thread_local cudaStream_t cs = nullptr;
+        if (!cs) AT_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        prof_suspend(true);
+        cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) { prof_suspend(false); return cuda_fail(e, "gbt_fit_hist: begin capture"); }
+        const int rc = enqueue(cs);
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamEndCapture(cs, &graph);
+        prof_suspend(false);
+        if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: end capture");
+        cudaGraphExec_t exec = nullptr;
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph instantiate");
+        {
+            ProfScope ps(AT_K_FIT_GRAPH, s);
+            e = cudaGraphLaunch(exec, s);
+        }
+        cudaGraphExecDestroy(exec);
+        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph launch");
+        return AT_OK;
+    };
+
+    // single rank, larger n: histogram subtraction over node-contiguous positions (section 3b)
+    const char *sub_e = getenv("AT_FIT_SUB");   // "0" forces the plain level-by-level path
+    if ((!sub_e || atoi(sub_e) != 0) && !o->allreduce && n_split > 0) {
+        // compact splittable features, their cell bases, and feature ranges that fit a block's cells
+        std::vector<int32_t> boff_h(F + 1), flist_h, coff_h;
+        for (int f = 0; f < F; ++f) {
+            boff_h[f + 1] = boff_h[f] + ncuts_h[f] + 1;
+            if (ncuts_h[f] > 0) flist_h.push_back(f);
+        }
+        const int Fs = (int)flist_h.size(), FsP = (Fs + 15) / 16 * 16;
+        for (int k = 0; k < Fs; ++k) coff_h.push_back(boff_h[flist_h[k]]);
+        auto cell_end = [&](int k) { return boff_h[flist_h[k] + 1]; };   // one past the last cell of k
+        std::vector<SubRange> rng;
+        for (int k = 0; k < Fs;) {
+            const int lo = k;
+            int hi = std::min(Fs, k + 4);
+            while (hi < Fs && cell_end(std::min(Fs, hi + 4) - 1) - coff_h[lo] <= SUB_CELLS) hi = std::min(Fs, hi + 4);
+            rng.push_back(SubRange{lo, hi, coff_h[lo], cell_end(hi - 1) - coff_h[lo]});
+            k = hi;
+        }
+        const int NR = (int)rng.size();
+        int max_c = 0;
+        for (const SubRange &r : rng) max_c = std::max(max_c, r.c_cnt);
+        if (NR <= SUB_MAXR && max_c <= SUB_CELLS) {
+            int dev = 0, nsm = 0;
+            AT_CUDA_TRY(cudaGetDevice(&dev));
+            AT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            const int target = std::max(1, 2 * (2 * nsm) / NR);   // ~2 waves of 2 blocks / SM
+            const int max_items = target + max_nn + 1;
+            uint8_t *binsR = ws.get<uint8_t>((size_t)n * FsP);
+            int32_t *perm = ws.get<int32_t>(n);
+            int32_t *coffR = ws.get<int32_t>(Fs);
+            SubRange *d_rng = ws.get<SubRange>(NR);
+            int4 *items = ws.get<int4>(max_items);
+            int4 *subs = ws.get<int4>(max_nn + 1);
+            int32_t *cnts = ws.get<int32_t>(4);   // [0] n_items, [1] n_subs
+            int32_t *cursor = ws.get<int32_t>(2 * max_nn);
+            int32_t *seg_start = ws.get<int32_t>(n_int + n_leaf);
+            int32_t *seg_cnt = ws.get<int32_t>(n_int + n_leaf);
+            int64_t *tot = ws.get<int64_t>(2 * (size_t)(n_int + n_leaf));
+            int64_t *hA = ws.get<int64_t>((size_t)max_nn * TB * 2);
+            int64_t *hB = ws.get<int64_t>((size_t)max_nn * TB * 2);
+            double *bg = ws.get<double>((size_t)max_nn * Fs);
+            int32_t *bs = ws.get<int32_t>((size_t)max_nn * Fs);
+            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+            AT_CUDA_TRY(cudaMemcpyAsync(coffR, coff_h.data(), Fs * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            AT_CUDA_TRY(cudaMemcpyAsync(d_rng, rng.data(), NR * sizeof(SubRange), cudaMemcpyHostToDevice, s));
+            rowbins_kernel<<<dim3(nblk(n, 32), nblk(FsP, 32)), dim3(32, 8), 0, s>>>(bins, n, flist, Fs, FsP, binsR);
+            note_launch();
+            AT_LAUNCH_CHECK("rowbins");
+            const size_t hsm = (size_t)4 * max_c * sizeof(uint32_t) + (size_t)(4 * ((Fs + 3) / 4 + 1)) * sizeof(int32_t);
+            static size_t sub_attr = 0;
+            if (sub_attr < hsm) {
+                AT_CUDA_TRY(cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+                sub_attr = hsm;
+            }
+            auto enqueue_sub = [&](cudaStream_t s) -> int {
+                for (int t = 0; t < o->n_trees; ++t) {
+                    {
+                        ProfScope ps(AT_K_FIT_GRAD, s);
+                        if (o->objective == AT_OBJ_REG) {
+                            reg_grads_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, pred, n, g, h); note_launch();
+                        } else {
+                            positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed,
+                                                                          (uint32_t)t, member); note_launch();
+                            if (n_groups > 0) {
+                                grads_kernel<<<n_groups, 256, (size_t)GS * 2 * sizeof(float), s>>>(member, counts, woff, gpre, GS,
+                                                                                     d_cost, pred, g, h);
+                                note_launch();
+                            }
+                        }
+                        AT_LAUNCH_CHECK("fit gradients");
+                    }
+                    AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
+                    AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
+                    uint16_t *tf = t_feat + (size_t)t * n_int;
+                    float *tt = t_thr + (size_t)t * n_int;
+                    int64_t *hp = hA, *hc = hB;
+                    {
+                        ProfScope ps(AT_K_FIT_HIST, s);
+                        AT_CUDA_TRY(cudaMemsetAsync(hp, 0, sizeof(int64_t) * 2 * (size_t)TB, s));
+                        sub_root_items_kernel<<<1, 256, 0, s>>>((int)n, target, items, cnts); note_launch();
+                        sub_hist_kernel<<<dim3(max_items, NR), SUB_NT, hsm, s>>>(binsR, FsP, nullptr, g, h, items, cnts,
+                                                                                 d_rng, coffR, TB, hp); note_launch();
+                        const int want_h0 = t == 0 && o->d_hist0_out;
+                        sub_root_tot_kernel<<<1, 256, 0, s>>>(hp, boff, flist, F, (int)n, want_h0, tot, seg_start,
+                                                              seg_cnt); note_launch();
+                        if (want_h0) {
+                            hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hp, boff, F, B, o->d_hist0_out);
+                            note_launch();
+                        }
+                        AT_LAUNCH_CHECK("root histogram");
+                    }
+                    for (int d = 0; d < D; ++d) {
+                        const int first = (1 << d) - 1, nn = 1 << d;
+                        {
+                            ProfScope ps(AT_K_FIT_SPLIT, s);
+                            sub_split_kernel<<<nblk((int64_t)nn * Fs, 8), 256, 0, s>>>(hp, boff, flist, Fs, TB, first, nn,
+                                                                                      tot, lam, mcw, dead, bg, bs);
+                            note_launch();
+                            sub_decide_kernel<<<nblk(nn, 8), 256, 0, s>>>(bg, bs, flist, Fs, first, nn, cuts, B, hp, boff,
+                                                                          TB, dead, split_f, split_s, tf, tt, tot);
+                            note_launch();
+                            AT_LAUNCH_CHECK("split/decide");
+                        }
+                        if (d == D - 1) break;
+                        {
+                            ProfScope ps(AT_K_FIT_SPLIT, s);
+                            AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * nn, s));
+                            sub_scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, first, nn,
+                                                                            seg_start, seg_cnt, cursor, node, perm);
+                            note_launch();
+                            sub_worklist_kernel<<<1, 128, 0, s>>>(first, nn, split_f, cursor, seg_start, seg_cnt, target,
+                                                                  items, cnts, subs, cnts + 1);
+                            note_launch();
+                            AT_LAUNCH_CHECK("scatter");
+                        }
+                        {
+                            ProfScope ps(AT_K_FIT_HIST, s);
+                            AT_CUDA_TRY(cudaMemsetAsync(hc, 0, sizeof(int64_t) * 2 * (size_t)TB * 2 * nn, s));
+                            sub_hist_kernel<<<dim3(target + nn, NR), SUB_NT, hsm, s>>>(binsR, FsP, perm, g, h, items, cnts,
+                                                                                      d_rng, coffR, TB, hc);
+                            note_launch();
+                            sub_subtract_kernel<<<dim3(std::min<unsigned>(nblk(2 * (int64_t)TB, 256), 64), nn), 256, 0,
+                                                  s>>>(hp, hc, TB, subs, cnts + 1);
+                            note_launch();
+                            AT_LAUNCH_CHECK("histograms");
+                        }
+                        std::swap(hp, hc);
+                    }
+                    {
+                        ProfScope ps(AT_K_FIT_UPDATE, s);
+                        float *tl = t_leaf + (size_t)t * n_leaf;
+                        leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(tot + 2 * (size_t)n_int, n_leaf, eta, lam, tl);
+                        note_launch();
+                        sub_final_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, node, split_f, split_s, n_int, tl, pred);
+                        note_launch();
+                        AT_LAUNCH_CHECK("leaf/pred update");
+                    }
+                }
+                return AT_OK;
+            };
+            const int rc = run_captured(enqueue_sub);
+            if (rc) return rc;
             return finish();
         }
     }
@@ -1873,27 +2372,8 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         const int rc = enqueue_trees(s);
         if (rc) return rc;
     } else {
-        static thread_local cudaStream_t cs = nullptr;
-        if (!cs) AT_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        prof_suspend(true);
-        cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-        if (e != cudaSuccess) { prof_suspend(false); return cuda_fail(e, "gbt_fit_hist: begin capture"); }
-        const int rc = enqueue_trees(cs);
-        cudaGraph_t graph = nullptr;
-        e = cudaStreamEndCapture(cs, &graph);
-        prof_suspend(false);
-        if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
-        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: end capture");
-        cudaGraphExec_t exec = nullptr;
-        e = cudaGraphInstantiate(&exec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph instantiate");
-        {
-            ProfScope ps(AT_K_FIT_GRAPH, s);
-            e = cudaGraphLaunch(exec, s);
-        }
-        cudaGraphExecDestroy(exec);
-        if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph launch");
+        const int rc = run_captured(enqueue_trees);
+        if (rc) return rc;
     }
     return finish();
 }

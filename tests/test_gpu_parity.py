@@ -321,15 +321,22 @@ def fit_inputs(n, wls, seed):
 @pytest.mark.parametrize("n,wls,trees,depth", [(1500, [synth.CFG2A, synth.CFG2B], 6, 4),
                                                (700, synth.ALL_DW[:3], 4, 6),
                                                (3000, [synth.MATMUL_512], 3, 5)])
-def test_fit_matches_oracle(at, n, wls, trees, depth):
+@pytest.mark.parametrize("path", ["subtraction", "level-by-level"])
+def test_fit_matches_oracle(at, n, wls, trees, depth, path):
+    """hist0_out (the parity hook for tree 0's root histogram) routes around the fused forest."""
     osp, idx, X, c, key = fit_inputs(n, wls, seed=n)
     ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth, want_hist0=True)
     sp = at.Space(wls)
     Xg = sp.features(u64(idx))
     pred = torch.empty(n, dtype=torch.float32, device="cuda")
     h0 = torch.empty((468, 256, 2), dtype=torch.int64, device="cuda")
-    g = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), n_trees=trees, depth=depth, pred_out=pred,
-                        hist0_out=h0)
+    os.environ.update(FIT_PATHS[path])
+    try:
+        g = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), n_trees=trees, depth=depth, pred_out=pred,
+                            hist0_out=h0)
+    finally:
+        for k in FIT_PATHS[path]:
+            os.environ.pop(k, None)
     ex = g.export()
     assert_bits_equal(h0.cpu().numpy(), ref["hist0"], "root histogram of tree 0")
     assert_bits_equal(ex["feat"], ref["feat"], "split features")
@@ -399,20 +406,31 @@ def test_fit_rank_invariance_two_emulated_ranks(at):
             assert_bits_equal(ex[k], single[k], f"rank {r} {k}")
 
 
-def _fit_both_paths(at, Xg, n, c, key, **kw):
-    """The fit with the fused single-launch forest (default for n <= 2048) and with the
-    level-by-level path (AT_FIT_FUSED=0), predictions included."""
-    out = []
-    for env in ("1", "0"):
-        os.environ["AT_FIT_FUSED"] = env
+FIT_PATHS = {"fused": {"AT_FIT_FUSED": "1"},                          # single launch (n <= 2048)
+             "subtraction": {"AT_FIT_FUSED": "0"},                   # default above 2048
+             "level-by-level": {"AT_FIT_FUSED": "0", "AT_FIT_SUB": "0"}}
+
+
+def _fit_paths(at, Xg, n, c, key, paths=tuple(FIT_PATHS), **kw):
+    """The fit through each single-rank path (env-selected), predictions included."""
+    out = {}
+    for name in paths:
+        os.environ.update(FIT_PATHS[name])
         try:
             pred = torch.empty(n, dtype=torch.float32, device="cuda")
             ex = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), pred_out=pred, **kw).export()
             ex["pred"] = pred.cpu().numpy()
-            out.append(ex)
+            out[name] = ex
         finally:
-            os.environ.pop("AT_FIT_FUSED", None)
+            for k in FIT_PATHS[name]:
+                os.environ.pop(k, None)
     return out
+
+
+def _check_paths(outs, ref, keys=("feat", "thresh", "leaf", "pred")):
+    for name, ex in outs.items():
+        for k in keys:
+            assert_bits_equal(ex[k], ref[k], f"{name} {k}")
 
 
 @pytest.mark.parametrize("n,wls,trees,depth,gs", [(1024, [synth.CFG2A], 5, 6, 64),     # bench's |D|
@@ -426,10 +444,7 @@ def test_fit_fused_forest_matches_oracle(at, n, wls, trees, depth, gs):
     ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth, group_size=gs)
     sp = at.Space(wls)
     Xg = sp.features(u64(idx))
-    fused, lvl = _fit_both_paths(at, Xg, n, c, key, n_trees=trees, depth=depth, group_size=gs)
-    for k in ("feat", "thresh", "leaf", "pred"):
-        assert_bits_equal(fused[k], ref[k], f"fused {k}")
-        assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
+    _check_paths(_fit_paths(at, Xg, n, c, key, n_trees=trees, depth=depth, group_size=gs), ref)
 
 
 def test_fit_fused_forest_many_features_and_ties(at):
@@ -446,10 +461,37 @@ def test_fit_fused_forest_many_features_and_ties(at):
     key = (np.arange(n) % 7).astype(np.uint16)
     ref = O.fit_hist(X, c, key, n_trees=3, depth=5)
     Xg = dev(np.ascontiguousarray(X.T))
-    fused, lvl = _fit_both_paths(at, Xg, n, c, key, n_trees=3, depth=5)
-    for k in ("feat", "thresh", "leaf", "pred"):
-        assert_bits_equal(fused[k], ref[k], f"fused {k}")
-        assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
+    _check_paths(_fit_paths(at, Xg, n, c, key, n_trees=3, depth=5), ref)
+
+
+@pytest.mark.parametrize("n,wls,trees,depth", [(20000, synth.ALL_DW, 3, 6),
+                                               (9000, synth.ALL_RESNET[:4], 2, 8),
+                                               (2049, [synth.CFG2A], 3, 3)])
+def test_fit_subtraction_path_matches_oracle(at, n, wls, trees, depth):
+    """Histogram subtraction over node-contiguous positions (the single-rank path above 2048
+    samples) and the plain level-by-level path against the oracle."""
+    osp, idx, X, c, key = fit_inputs(n, wls, seed=n + 11)
+    ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth)
+    Xg = at.Space(wls).features(u64(idx))
+    _check_paths(_fit_paths(at, Xg, n, c, key, paths=("subtraction", "level-by-level"), n_trees=trees, depth=depth), ref)
+
+
+def test_fit_subtraction_many_feature_ranges(at):
+    """F = 1500 features with up to 256 bins each: the cells of the splittable features span many
+    shared-memory ranges (one histogram block per range); quantile cuts, duplicated and constant
+    columns, zero-gradient groups (equal costs)."""
+    n, F = 5000, 1500
+    rng = np.random.default_rng(33)
+    X = rng.integers(0, 200, (n, F)).astype(np.float32)
+    X[:, 1000:1100] = rng.random((n, 100)).astype(np.float32) * 1e4     # > 256 unique: quantile cuts
+    X[:, 1100:1200] = X[:, 200:300]                                      # duplicates
+    X[:, 1200:1250] = 7.0                                                # constant
+    c = np.round(X[:, 5] + 2 * X[:, 1010] / 100 + rng.integers(0, 3, n), 0).astype(np.float32)
+    c[:64] = 1.0                                                         # one group of equal costs
+    key = (np.arange(n) % 3).astype(np.uint16)
+    ref = O.fit_hist(X, c, key, n_trees=2, depth=6, want_hist0=False)
+    Xg = dev(np.ascontiguousarray(X.T))
+    _check_paths(_fit_paths(at, Xg, n, c, key, paths=("subtraction", "level-by-level"), n_trees=2, depth=6), ref)
 
 
 # ------------------------------------------------------------------ §8(f): regression objective, transfer (Eq. 4)
@@ -467,10 +509,7 @@ def test_fit_regression_matches_oracle(at, n, wls, trees, depth, margin):
     kw = dict(n_trees=trees, depth=depth, objective="reg")
     if margin:
         kw["base_margin"] = dev(m)
-    fused, lvl = _fit_both_paths(at, Xg, n, c, key, **kw)
-    for k in ("feat", "thresh", "leaf", "pred"):
-        assert_bits_equal(fused[k], ref[k], f"fused {k}")
-        assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
+    _check_paths(_fit_paths(at, Xg, n, c, key, **kw), ref)
 
 
 @pytest.mark.parametrize("n,trees,depth", [(1024, 5, 6), (3000, 3, 5)])
@@ -480,10 +519,7 @@ def test_fit_rank_with_base_margin_matches_oracle(at, n, trees, depth):
     m = np.random.default_rng(n + 1).normal(0, 1.0, n).astype(np.float32)
     ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth, base_margin=m)
     Xg = at.Space([synth.CFG2A, synth.CFG2B]).features(u64(idx))
-    fused, lvl = _fit_both_paths(at, Xg, n, c, key, n_trees=trees, depth=depth, base_margin=dev(m))
-    for k in ("feat", "thresh", "leaf", "pred"):
-        assert_bits_equal(fused[k], ref[k], f"fused {k}")
-        assert_bits_equal(lvl[k], ref[k], f"level-by-level {k}")
+    _check_paths(_fit_paths(at, Xg, n, c, key, n_trees=trees, depth=depth, base_margin=dev(m)), ref)
 
 
 def test_gbt_concat_matches_oracle(at):
@@ -702,12 +738,19 @@ def test_config4_refit_full_sample_count(at):
     assert_bits_equal(Xg[:, :n].cpu().numpy().T, Xo, "features")
     h0 = torch.empty((468, 256, 2), dtype=torch.int64, device="cuda")
     pred = torch.empty(n, dtype=torch.float32, device="cuda")
-    gm = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), n_trees=2, depth=6, hist0_out=h0, pred_out=pred)
-    ex = gm.export()
-    assert_bits_equal(h0.cpu().numpy(), ref["hist0"], "root histogram")
-    for k in ("feat", "thresh", "leaf"):
-        assert_bits_equal(ex[k], ref[k], k)
-    assert_bits_equal(pred.cpu().numpy(), ref["pred"], "fit predictions")
+    for path in ("subtraction", "level-by-level"):
+        os.environ.update(FIT_PATHS[path])
+        try:
+            gm = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), n_trees=2, depth=6, hist0_out=h0,
+                                 pred_out=pred)
+        finally:
+            for k in FIT_PATHS[path]:
+                os.environ.pop(k, None)
+        ex = gm.export()
+        assert_bits_equal(h0.cpu().numpy(), ref["hist0"], f"{path} root histogram")
+        for k in ("feat", "thresh", "leaf"):
+            assert_bits_equal(ex[k], ref[k], f"{path} {k}")
+        assert_bits_equal(pred.cpu().numpy(), ref["pred"], f"{path} fit predictions")
 
 
 def test_config5_sweep_sampled(at):
