@@ -811,31 +811,39 @@ __global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int3
 // are two 32-bit words updated by native shared atomics with an explicit carry (smem_add_u64's
 // rule); blocks flush with native 64-bit global atomics.  Node totals travel down the tree
 // (left = the winning split's prefix sums, right = total - left), so the leaves need no extra pass.
-constexpr int SUB_NT = 512;
-constexpr int SUB_CELLS = 6144;   // cells per block: 4 x 4 B x 6144 = 96 KB of shared memory
-constexpr int SUB_MAXR = 64;
+constexpr int SUB_NT = 1024;
+constexpr int SUB_ROWS = 400;   // rows of 32 cells: 4 planes x 4 B x 32 x 400 = 200 KB of shared memory
+constexpr int SUB_NQW = 4;      // row words per lane and sample: <= 512 features per range
+constexpr int SUB_MAXR = 256;
 
+// A feature range: compact features [k_lo, k_lo + nf).  Feature r (local index) lives in bank column
+// r mod 32 of the block's shared histogram, at rows rowbase[k_lo + r] .. + nb - 1, so the lane that
+// handles it (lane = r mod 32) owns that bank: one warp-wide atomic never conflicts.  Its bin byte
+// sits in the sample's row at byte_off + 128 (r / 128) + 4 (r mod 32) + (r mod 128) / 32, so one
+// 32-bit load per lane brings the bins of features 128u + 32j + lane, j = 0..3.
 struct SubRange {
-    int k_lo, k_hi, c_lo, c_cnt;   // compact features [k_lo, k_hi), cells [c_lo, c_lo + c_cnt)
+    int k_lo, nf, rows, byte_off;
 };
 
-// bins [F][n] (column-major) -> binsR [n][FsP] over the splittable features flist[0..Fs), zero padded
-__global__ void rowbins_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ flist, int Fs,
-                               int FsP, uint8_t *__restrict__ binsR)
+// bins [F][n] (column-major) -> binsR [n][FsP] in the ranges' byte order (inv[b] = compact feature
+// at row byte b, -1 = padding)
+__global__ void rowbins_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ flist,
+                               const int32_t *__restrict__ inv, int FsP, uint8_t *__restrict__ binsR)
 {
     __shared__ uint8_t t[32][33];
     const int64_t i0 = (int64_t)blockIdx.x * 32;
-    const int k0 = blockIdx.y * 32;
+    const int b0 = blockIdx.y * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int k = k0 + r;
+        const int b = b0 + r;
         const int64_t i = i0 + threadIdx.x;
-        t[r][threadIdx.x] = (k < Fs && i < n) ? bins[(int64_t)flist[k] * n + i] : (uint8_t)0;
+        const int k = b < FsP ? inv[b] : -1;
+        t[r][threadIdx.x] = (k >= 0 && i < n) ? bins[(int64_t)flist[k] * n + i] : (uint8_t)0;
     }
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int64_t i = i0 + r;
-        const int k = k0 + threadIdx.x;
-        if (i < n && k < FsP) binsR[i * FsP + k] = t[threadIdx.x][r];
+        const int b = b0 + threadIdx.x;
+        if (i < n && b < FsP) binsR[i * FsP + b] = t[threadIdx.x][r];
     }
 }
 
@@ -847,58 +855,105 @@ __device__ __forceinline__ void sub_add64(uint32_t *lo, uint32_t *hi, int c, uin
 }
 
 // items[b] = {node slot, p0, p1, -}: block (b, r) adds positions [p0, p1) of perm (identity when
-// perm == nullptr) into the cells of feature range r of hist[slot].
-__global__ void __launch_bounds__(SUB_NT, 2) sub_hist_kernel(const uint8_t *__restrict__ binsR, int FsP,
+// perm == nullptr) into the cells of feature range r of hist[slot].  Warp w takes positions
+// it.y + w + NW t (balanced to within one sample), 32 of them per batch (one coalesced load of their
+// sample ids and gradients), then walks them with the next sample's row words in flight while the
+// current one's atomics issue.
+__global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__restrict__ binsR, int FsP,
                                                              const int32_t *__restrict__ perm,
                                                              const int64_t *__restrict__ g,
                                                              const int64_t *__restrict__ h,
                                                              const int4 *__restrict__ items,
                                                              const int32_t *__restrict__ n_items,
                                                              const SubRange *__restrict__ ranges,
-                                                             const int32_t *__restrict__ coffR, int TB,
+                                                             const int32_t *__restrict__ rowbase,
+                                                             const int32_t *__restrict__ gbase,
+                                                             const int32_t *__restrict__ nbk, int TB,
                                                              int64_t *__restrict__ hist)
 {
     extern __shared__ uint32_t sm[];
     if ((int)blockIdx.x >= *n_items) return;
     const SubRange R = ranges[blockIdx.y];
     const int4 it = items[blockIdx.x];
-    const int C = R.c_cnt;
-    uint32_t *glo = sm, *ghi = sm + C, *hlo = sm + 2 * C, *hhi = sm + 3 * C;
-    int32_t *coff = (int32_t *)(sm + 4 * C);   // coff[j * nq + q]: cell base of feature k_lo + 4 q + j
-    const int nf = R.k_hi - R.k_lo, nq = (nf + 3) >> 2;
+    const int P = R.rows * 32;
+    uint32_t *glo = sm, *ghi = sm + P, *hlo = sm + 2 * P, *hhi = sm + 3 * P;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int q = tid; q < 4 * C; q += SUB_NT) sm[q] = 0u;
-    for (int q = tid; q < 4 * nq; q += SUB_NT) {
-        const int j = q / nq, qq = q - j * nq, k = R.k_lo + 4 * qq + j;
-        coff[q] = k < R.k_hi ? coffR[k] - R.c_lo : -1;
-    }
-    __syncthreads();
-    for (int p = it.y + warp; p < it.z; p += SUB_NT / 32) {
-        const int i = perm ? perm[p] : p;
-        const unsigned long long gv = (unsigned long long)g[i], hv = (unsigned long long)h[i];
-        if ((gv | hv) == 0ull) continue;   // contributes nothing (warp-uniform)
-        const uint32_t gl = (uint32_t)gv, gh = (uint32_t)(gv >> 32), hl = (uint32_t)hv, hh = (uint32_t)(hv >> 32);
-        const uint32_t *row = (const uint32_t *)(binsR + (int64_t)i * FsP + R.k_lo);
-        for (int q = lane; q < nq; q += 32) {
-            const uint32_t w = row[q];
+    constexpr int NW = SUB_NT / 32;
+    for (int q = tid; q < 4 * P; q += SUB_NT) sm[q] = 0u;
+    const int nqw = (R.nf + 127) >> 7;
+    int rb[SUB_NQW][4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int c0 = coff[j * nq + q];
-                if (c0 >= 0) {
-                    const int c = c0 + (int)((w >> (8 * j)) & 255u);
-                    sub_add64(glo, ghi, c, gl, gh);
-                    sub_add64(hlo, hhi, c, hl, hh);
-                }
+    for (int u = 0; u < SUB_NQW; ++u)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = 128 * u + 32 * j + lane;
+            rb[u][j] = r < R.nf ? rowbase[R.k_lo + r] * 32 + lane : -1;
+        }
+    __syncthreads();
+    const uint8_t *rows = binsR + R.byte_off + 4 * lane;
+    for (int t0 = 0; it.y + warp + NW * t0 < it.z; t0 += 32) {
+        const int pl = it.y + warp + NW * (t0 + lane);
+        const bool okl = pl < it.z;
+        const int il = okl ? (perm ? perm[pl] : pl) : 0;
+        const unsigned long long gvl = okl ? (unsigned long long)g[il] : 0ull;
+        const unsigned long long hvl = okl ? (unsigned long long)h[il] : 0ull;
+        const int cnt = (int)__popc(__ballot_sync(0xFFFFFFFFu, okl));
+        uint32_t w[SUB_NQW], wn[SUB_NQW];
+        {
+            const uint32_t *row = (const uint32_t *)(rows + (int64_t)__shfl_sync(0xFFFFFFFFu, il, 0) * FsP);
+#pragma unroll
+            for (int u = 0; u < SUB_NQW; ++u) w[u] = u < nqw ? row[32 * u] : 0u;
+        }
+        for (int sI = 0; sI < cnt; ++sI) {
+            const int inext = __shfl_sync(0xFFFFFFFFu, il, (sI + 1) & 31);
+            if (sI + 1 < cnt) {
+                const uint32_t *row = (const uint32_t *)(rows + (int64_t)inext * FsP);
+#pragma unroll
+                for (int u = 0; u < SUB_NQW; ++u) wn[u] = u < nqw ? row[32 * u] : 0u;
             }
+            const unsigned long long gv = __shfl_sync(0xFFFFFFFFu, gvl, sI);
+            const unsigned long long hv = __shfl_sync(0xFFFFFFFFu, hvl, sI);
+            if ((gv | hv) != 0ull) {   // warp-uniform: a zero-gradient sample contributes nothing
+                const uint32_t gl = (uint32_t)gv, gh = (uint32_t)(gv >> 32), hl = (uint32_t)hv, hh = (uint32_t)(hv >> 32);
+#pragma unroll
+                for (int u = 0; u < SUB_NQW; ++u)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (rb[u][j] >= 0) {
+                            const int c = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
+                            sub_add64(glo, ghi, c, gl, gh);
+                            sub_add64(hlo, hhi, c, hl, hh);
+                        }
+            }
+#pragma unroll
+            for (int u = 0; u < SUB_NQW; ++u) w[u] = wn[u];
         }
     }
     __syncthreads();
-    unsigned long long *hn = (unsigned long long *)(hist + ((int64_t)it.x * TB + R.c_lo) * 2);
-    for (int c = tid; c < C; c += SUB_NT) {
-        const unsigned long long G = (unsigned long long)glo[c] | ((unsigned long long)ghi[c] << 32);
-        const unsigned long long H = (unsigned long long)hlo[c] | ((unsigned long long)hhi[c] << 32);
-        if (G) atomicAdd(&hn[2 * c], G);
-        if (H) atomicAdd(&hn[2 * c + 1], H);
+    // flush: lane = bank column, a warp walks a band of rows; each lane tracks the feature of its
+    // column that holds the current row
+    const int band = (R.rows + NW - 1) / NW;
+    const int row0 = warp * band, row1 = min(R.rows, row0 + band);
+    if (row0 >= row1) return;
+    int r = lane;   // this column's features: lane, lane + 32, ...
+    while (r < R.nf && rowbase[R.k_lo + r] + nbk[R.k_lo + r] <= row0) r += 32;
+    int rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF, rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
+    int cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
+    unsigned long long *hn = (unsigned long long *)(hist + (int64_t)it.x * TB * 2);
+    for (int row = row0; row < row1; ++row) {
+        if (row >= rend) {
+            r += 32;
+            rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF;
+            rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
+            cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
+        }
+        if (row < rbase) continue;
+        const int a = row * 32 + lane;
+        const unsigned long long G = (unsigned long long)glo[a] | ((unsigned long long)ghi[a] << 32);
+        const unsigned long long H = (unsigned long long)hlo[a] | ((unsigned long long)hhi[a] << 32);
+        const int64_t cell = (int64_t)(cbase + row - rbase) * 2;
+        if (G) atomicAdd(&hn[cell], G);
+        if (H) atomicAdd(&hn[cell + 1], H);
     }
 }
 
@@ -982,12 +1037,24 @@ __global__ void __launch_bounds__(256) sub_decide_kernel(const double *__restric
     const int nd = first + q;
     SplitBest best{0.0, -1, 0};
     if (!dead[nd]) {
-        for (int k = lane; k < Fs; k += 32) {
-            const int s = best_s[(int64_t)q * Fs + k];
-            if (s > 0) {
-                SplitBest c{best_gain[(int64_t)q * Fs + k], flist[k], s};
-                if (split_better(c, best)) best = c;
+        const double *bgq = best_gain + (int64_t)q * Fs;
+        const int32_t *bsq = best_s + (int64_t)q * Fs;
+        for (int k0 = 0; k0 < Fs; k0 += 32 * 8) {   // 8 loads of each kind in flight per lane
+            double gv[8];
+            int sv[8], fv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = k0 + 32 * u + lane;
+                sv[u] = k < Fs ? bsq[k] : 0;
+                gv[u] = k < Fs ? bgq[k] : 0.0;
+                fv[u] = k < Fs ? flist[k] : 0;
             }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (sv[u] > 0) {
+                    SplitBest c{gv[u], fv[u], sv[u]};
+                    if (split_better(c, best)) best = c;
+                }
         }
     }
     best = warp_best(best);
@@ -1064,35 +1131,46 @@ __global__ void sub_worklist_kernel(int first, int nn, const int32_t *__restrict
                                     int32_t *__restrict__ seg_cnt, int target, int4 *__restrict__ items,
                                     int32_t *__restrict__ n_items, int4 *__restrict__ subs, int32_t *__restrict__ n_subs)
 {
-    __shared__ int s_small[128], s_cs[128], s_alive[128];
+    __shared__ int s_cs[128], s_m0[129], s_s0[129], s_ch;
     const int q = threadIdx.x;
     const int cfirst = 2 * first + 1;   // first node of level d + 1
+    int small = 0, st = 0, cs = 0, alive = 0;
     if (q < nn) {
         const int nd = first + q;
-        const int L = cursor[2 * q], Rc = cursor[2 * q + 1];
-        seg_start[2 * nd + 1] = seg_start[nd];
+        const int L = cursor[2 * q], Rc = cursor[2 * q + 1], s0 = seg_start[nd];
+        seg_start[2 * nd + 1] = s0;
         seg_cnt[2 * nd + 1] = L;
-        seg_start[2 * nd + 2] = seg_start[nd] + L;
+        seg_start[2 * nd + 2] = s0 + L;
         seg_cnt[2 * nd + 2] = Rc;
-        s_alive[q] = split_f[nd] >= 0;
-        s_small[q] = L <= Rc ? 2 * nd + 1 : 2 * nd + 2;
-        s_cs[q] = L <= Rc ? L : Rc;
+        alive = split_f[nd] >= 0;
+        small = L <= Rc ? 2 * nd + 1 : 2 * nd + 2;
+        st = L <= Rc ? s0 : s0 + L;
+        cs = L <= Rc ? L : Rc;
+        s_cs[q] = alive ? cs : 0;
     }
     __syncthreads();
     if (q == 0) {
         long long total = 0;
-        for (int p = 0; p < nn; ++p) total += s_alive[p] ? s_cs[p] : 0;
+        for (int p = 0; p < nn; ++p) total += s_cs[p];
         const int ch = (int)max(64ll, (total + target - 1) / target);
         int m = 0, ns = 0;
         for (int p = 0; p < nn; ++p) {
-            if (!s_alive[p]) continue;
-            const int sm_nd = s_small[p], big = (sm_nd & 1) ? sm_nd + 1 : sm_nd - 1;
-            subs[ns++] = make_int4(p, sm_nd - cfirst, big - cfirst, 0);
-            const int st = seg_start[sm_nd], cnt = s_cs[p];
-            for (int o = 0; o < cnt; o += ch) items[m++] = make_int4(sm_nd - cfirst, st + o, st + min(cnt, o + ch), 0);
+            s_m0[p] = m;
+            s_s0[p] = ns;
+            m += (s_cs[p] + ch - 1) / ch;
+            ns += split_f[first + p] >= 0 ? 1 : 0;
         }
+        s_ch = ch;
         *n_items = m;
         *n_subs = ns;
+    }
+    __syncthreads();
+    if (q < nn && alive) {
+        const int big = (small & 1) ? small + 1 : small - 1;
+        const int ch = s_ch;
+        int m = s_m0[q];
+        subs[s_s0[q]] = make_int4(q, small - cfirst, big - cfirst, 0);
+        for (int o = 0; o < cs; o += ch) items[m++] = make_int4(small - cfirst, st + o, st + min(cs, o + ch), 0);
     }
 }
 
@@ -2105,35 +2183,59 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     // single rank, larger n: histogram subtraction over node-contiguous positions (section 3b)
     const char *sub_e = getenv("AT_FIT_SUB");   // "0" forces the plain level-by-level path
     if ((!sub_e || atoi(sub_e) != 0) && !o->allreduce && n_split > 0) {
-        // compact splittable features, their cell bases, and feature ranges that fit a block's cells
-        std::vector<int32_t> boff_h(F + 1), flist_h, coff_h;
+        // compact splittable features and the feature ranges whose bank columns fit a block's rows
+        std::vector<int32_t> boff_h(F + 1), flist_h;
         for (int f = 0; f < F; ++f) {
             boff_h[f + 1] = boff_h[f] + ncuts_h[f] + 1;
             if (ncuts_h[f] > 0) flist_h.push_back(f);
         }
-        const int Fs = (int)flist_h.size(), FsP = (Fs + 15) / 16 * 16;
-        for (int k = 0; k < Fs; ++k) coff_h.push_back(boff_h[flist_h[k]]);
-        auto cell_end = [&](int k) { return boff_h[flist_h[k] + 1]; };   // one past the last cell of k
+        const int Fs = (int)flist_h.size();
+        std::vector<int32_t> rowbase_h(Fs), gbase_h(Fs), nbk_h(Fs);
+        for (int k = 0; k < Fs; ++k) {
+            gbase_h[k] = boff_h[flist_h[k]];
+            nbk_h[k] = ncuts_h[flist_h[k]] + 1;
+        }
         std::vector<SubRange> rng;
+        int FsP = 0;
         for (int k = 0; k < Fs;) {
-            const int lo = k;
-            int hi = std::min(Fs, k + 4);
-            while (hi < Fs && cell_end(std::min(Fs, hi + 4) - 1) - coff_h[lo] <= SUB_CELLS) hi = std::min(Fs, hi + 4);
-            rng.push_back(SubRange{lo, hi, coff_h[lo], cell_end(hi - 1) - coff_h[lo]});
-            k = hi;
+            // add stripes of 32 features (one per bank column) while every column fits
+            int col[32] = {0};
+            int nf = 0;
+            while (k + nf < Fs && nf < 128 * SUB_NQW) {
+                int trial[32];
+                std::copy(col, col + 32, trial);
+                const int m = std::min(32, Fs - (k + nf));
+                bool fits = true;
+                for (int l = 0; l < m; ++l) {
+                    trial[l] += nbk_h[k + nf + l];
+                    fits = fits && trial[l] <= SUB_ROWS;
+                }
+                if (!fits && nf > 0) break;
+                for (int l = 0; l < m; ++l) rowbase_h[k + nf + l] = col[l];
+                std::copy(trial, trial + 32, col);
+                nf += m;
+            }
+            const int rows = *std::max_element(col, col + 32);
+            rng.push_back(SubRange{k, nf, rows, FsP});
+            FsP += 128 * ((nf + 127) / 128);
+            k += nf;
         }
         const int NR = (int)rng.size();
-        int max_c = 0;
-        for (const SubRange &r : rng) max_c = std::max(max_c, r.c_cnt);
-        if (NR <= SUB_MAXR && max_c <= SUB_CELLS) {
+        int max_rows = 0;
+        for (const SubRange &r : rng) max_rows = std::max(max_rows, r.rows);
+        std::vector<int32_t> inv_h(FsP, -1);
+        for (const SubRange &R : rng)
+            for (int r = 0; r < R.nf; ++r)
+                inv_h[R.byte_off + 128 * (r / 128) + 4 * (r % 32) + (r % 128) / 32] = R.k_lo + r;
+        if (NR <= SUB_MAXR && max_rows <= SUB_ROWS) {
             int dev = 0, nsm = 0;
             AT_CUDA_TRY(cudaGetDevice(&dev));
             AT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-            const int target = std::max(1, 2 * (2 * nsm) / NR);   // ~2 waves of 2 blocks / SM
+            const int target = std::max(1, nsm / NR);   // one wave of 1 block / SM
             const int max_items = target + max_nn + 1;
             uint8_t *binsR = ws.get<uint8_t>((size_t)n * FsP);
             int32_t *perm = ws.get<int32_t>(n);
-            int32_t *coffR = ws.get<int32_t>(Fs);
+            int32_t *d_tab = ws.get<int32_t>(3 * (size_t)Fs + FsP);   // rowbase, gbase, nbk, inv
             SubRange *d_rng = ws.get<SubRange>(NR);
             int4 *items = ws.get<int4>(max_items);
             int4 *subs = ws.get<int4>(max_nn + 1);
@@ -2147,12 +2249,17 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             double *bg = ws.get<double>((size_t)max_nn * Fs);
             int32_t *bs = ws.get<int32_t>((size_t)max_nn * Fs);
             if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
-            AT_CUDA_TRY(cudaMemcpyAsync(coffR, coff_h.data(), Fs * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            std::vector<int32_t> tab(rowbase_h);
+            tab.insert(tab.end(), gbase_h.begin(), gbase_h.end());
+            tab.insert(tab.end(), nbk_h.begin(), nbk_h.end());
+            tab.insert(tab.end(), inv_h.begin(), inv_h.end());
+            AT_CUDA_TRY(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
             AT_CUDA_TRY(cudaMemcpyAsync(d_rng, rng.data(), NR * sizeof(SubRange), cudaMemcpyHostToDevice, s));
-            rowbins_kernel<<<dim3(nblk(n, 32), nblk(FsP, 32)), dim3(32, 8), 0, s>>>(bins, n, flist, Fs, FsP, binsR);
+            const int32_t *d_rowbase = d_tab, *d_gbase = d_tab + Fs, *d_nbk = d_tab + 2 * Fs, *d_inv = d_tab + 3 * Fs;
+            rowbins_kernel<<<dim3(nblk(n, 32), nblk(FsP, 32)), dim3(32, 8), 0, s>>>(bins, n, flist, d_inv, FsP, binsR);
             note_launch();
             AT_LAUNCH_CHECK("rowbins");
-            const size_t hsm = (size_t)4 * max_c * sizeof(uint32_t) + (size_t)(4 * ((Fs + 3) / 4 + 1)) * sizeof(int32_t);
+            const size_t hsm = (size_t)4 * 32 * max_rows * sizeof(uint32_t);
             static size_t sub_attr = 0;
             if (sub_attr < hsm) {
                 AT_CUDA_TRY(cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
@@ -2185,7 +2292,8 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                         AT_CUDA_TRY(cudaMemsetAsync(hp, 0, sizeof(int64_t) * 2 * (size_t)TB, s));
                         sub_root_items_kernel<<<1, 256, 0, s>>>((int)n, target, items, cnts); note_launch();
                         sub_hist_kernel<<<dim3(max_items, NR), SUB_NT, hsm, s>>>(binsR, FsP, nullptr, g, h, items, cnts,
-                                                                                 d_rng, coffR, TB, hp); note_launch();
+                                                                                 d_rng, d_rowbase, d_gbase, d_nbk, TB, hp);
+                        note_launch();
                         const int want_h0 = t == 0 && o->d_hist0_out;
                         sub_root_tot_kernel<<<1, 256, 0, s>>>(hp, boff, flist, F, (int)n, want_h0, tot, seg_start,
                                                               seg_cnt); note_launch();
@@ -2223,7 +2331,8 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                             ProfScope ps(AT_K_FIT_HIST, s);
                             AT_CUDA_TRY(cudaMemsetAsync(hc, 0, sizeof(int64_t) * 2 * (size_t)TB * 2 * nn, s));
                             sub_hist_kernel<<<dim3(target + nn, NR), SUB_NT, hsm, s>>>(binsR, FsP, perm, g, h, items, cnts,
-                                                                                      d_rng, coffR, TB, hc);
+                                                                                      d_rng, d_rowbase, d_gbase, d_nbk,
+                                                                                      TB, hc);
                             note_launch();
                             sub_subtract_kernel<<<dim3(std::min<unsigned>(nblk(2 * (int64_t)TB, 256), 64), nn), 256, 0,
                                                   s>>>(hp, hc, TB, subs, cnts + 1);
