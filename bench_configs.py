@@ -92,6 +92,57 @@ def score_case(at, synth, wls, T, D, n, sweep=False, peaks=None):
             "predict_Gnode_steps_per_s": round(n * T * D / (tp / 1e3) / 1e9, 2)}
 
 
+def sweep_case(at, synth, T, D, Ns, chunk=1 << 24, peaks=None):
+    """Config 5 as a sweep over N: candidates (a n + c) mod |S_union| scored in chunks of
+    <= 2^24 by features_extract -> gbt_predict (the features of 10^8 candidates would be 187 GB)."""
+    import numpy as np
+    import torch
+    sp = at.Space(synth.ALL_RESNET)
+    ens = synth.ensemble(T, D, seed=1805)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    cmax = min(chunk, max(Ns))
+    X = torch.empty((468, cmax), dtype=torch.float32, device="cuda")
+    rows = []
+    for n in Ns:
+        idx = torch.from_numpy(synth.sweep_indices(sp.size(), 0, n).view(np.int64)).cuda()
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+
+        def run():
+            for c0 in range(0, n, chunk):
+                c1 = min(n, c0 + chunk)
+                sp.features(idx[c0:c1], out=X, ld=cmax)
+                g.predict(X, n=c1 - c0, out=out[c0:c1])
+
+        ms = timed(run, reps=1 if n >= 10 ** 7 else 3, warm=1)
+        # fused: sa_explore with 0 steps scores its chain states (features in shared memory, never in
+        # HBM) and keeps the distinct top-64 per workload
+        offs = np.array(sp.offsets[:12], dtype=np.uint64)
+        cw = torch.from_numpy((np.searchsorted(offs, idx.cpu().numpy().view(np.uint64), "right") - 1)
+                              .astype(np.int16)).cuda()
+        temps = torch.empty(0, dtype=torch.float32, device="cuda")
+        fused = {}
+
+        def run_fused():
+            for c0 in range(0, n, chunk):
+                c1 = min(n, c0 + chunk)
+                fused["r"] = at.sa_explore(sp, g, idx[c0:c1], temps, seed=1805, round_=0, k_out=64,
+                                           chain_workload=cw[c0:c1], init=False)
+
+        msf = timed(run_fused, reps=1 if n >= 10 ** 7 else 3, warm=1)
+        last = (n - 1) // chunk * chunk   # the last chunk's scores, both ways
+        same = bool(torch.equal(fused["r"]["chain_energy"].view(torch.int32), out[last:].view(torch.int32)))
+        rows.append({"candidates": n, "ms": round(ms, 3), "cand_per_s": round(n / (ms / 1e3), 1),
+                     "Gnode_steps_per_s": round(n * T * D / (ms / 1e3) / 1e9, 2),
+                     "fused_ms": round(msf, 3), "fused_cand_per_s": round(n / (msf / 1e3), 1),
+                     "fused_scores_bit_identical": same})
+        del idx, out, cw
+        torch.cuda.empty_cache()
+    return {"trees": T, "depth": D, "chunk": chunk,
+            "path": "unfused: features_extract -> gbt_predict per chunk; fused: sa_explore with 0 steps per chunk "
+                    "(+ distinct top-64 per workload)",
+            "sweep": rows}
+
+
 def main():
     import numpy as np
     import torch
@@ -135,6 +186,7 @@ def main():
                        "ms_per_tree": round(ms / 100, 3)}
     if "cfg5" in only:
         res["cfg5"] = score_case(at, synth, synth.ALL_RESNET, 2000, 8, 1 << 16, sweep=True, peaks=peaks)
+        res["cfg5_sweep"] = sweep_case(at, synth, 2000, 8, [10 ** 4, 10 ** 5, 10 ** 6, 10 ** 7, 10 ** 8], peaks=peaks)
     print(json.dumps(res))
 
 

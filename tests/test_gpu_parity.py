@@ -863,3 +863,26 @@ def test_algorithm1_with_transfer_and_bootstrap_matches_oracle(at, objective, K,
             assert_bits_equal(ex[f], getattr(cat, f), f"round {r} models {f}")
         assert np.float32(tuner.acq["best"]) == np.float32(best)
     assert tuner.state.best_cost == min(costs)
+
+
+def test_fused_scoring_is_sa_with_zero_steps(at):
+    """The fused scorer of config 5 (sa_explore with 0 steps: features in shared memory, never in HBM)
+    gives the bit-identical scores of features_extract -> gbt_predict, and its distinct top-k is the
+    top of the sorted scores (the sweep indices are distinct)."""
+    ens = synth.ensemble(300, 8, seed=1805)
+    sp = at.Space(synth.ALL_RESNET)
+    n = 5000
+    idx = synth.sweep_indices(sp.size(), 12345, n)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    s = g.predict(sp.features(u64(idx)), n=n).cpu().numpy()
+    offs = np.array(sp.offsets[:12], dtype=np.uint64)
+    w = (np.searchsorted(offs, idx, "right") - 1).astype(np.uint16)
+    r = at.sa_explore(sp, g, u64(idx), torch.empty(0, dtype=torch.float32, device="cuda"), seed=1, round_=0,
+                      k_out=16, chain_workload=dev(w.view(np.int16)), init=False)
+    assert_bits_equal(r["chain_energy"].cpu().numpy(), s, "fused scores")
+    for wl in range(12):
+        m = w == wl
+        order = np.lexsort((idx[m], s[m]))[:16]
+        k = int(r["out_n"][wl])
+        assert_bits_equal(host_u64(r["out_idx"][wl][:k]), idx[m][order][:k], f"workload {wl} top-k")
+
