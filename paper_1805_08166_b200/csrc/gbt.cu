@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include <cuda.h>
@@ -13,17 +14,18 @@ namespace at {
 
 constexpr int PRED_NW = 16;  // warps per block (tree slices); 32 candidates per tile
 
-TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes)
+TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes, bool rank)
 {
     TreeGeo G{};
-    G.nodes = g->d_nodes;
+    G.nodes = rank ? (const uint8_t *)g->d_rk_nodes : (const uint8_t *)g->d_nodes;
+    G.nbytes = rank ? 4 : 8;
     G.leaf = g->d_leaf;
     G.T = g->n_trees;
     G.T_pad = g->t_pad;
     G.D = g->depth;
     G.ni = (1 << g->depth) - 1;
     G.nl = 1 << g->depth;
-    const uint32_t per_tree = (uint32_t)G.ni * 8u + (uint32_t)G.nl * 4u;
+    const uint32_t per_tree = (uint32_t)G.ni * (uint32_t)G.nbytes + (uint32_t)G.nl * 4u;
     int ch = (int)(buf_bytes / per_tree) / 2 * 2;   // even: chunk offsets and sizes stay 16-B aligned
     if (ch >= 32) ch = ch / 32 * 32;                 // whole 32-tree rounds: no idle walk slots
     if (ch < 2) ch = 2;
@@ -52,10 +54,10 @@ struct TileMap {
 };
 
 // one tile = GRP groups of 32 candidates; group g of tile `tile` starts at candidate (tile GRP + g) 32
-template <int GRP>
-__device__ __forceinline__ void tile_issue(const TileMap &tm, int64_t tile, float *dst, int tile_rows, uint64_t *bar)
+template <int GRP, class T>
+__device__ __forceinline__ void tile_issue(const TileMap &tm, int64_t tile, T *dst, int tile_rows, uint64_t *bar)
 {
-    mbar_arrive_expect_tx(bar, (uint32_t)(GRP * tm.n_box * tm.box_rows * 32 * 4));
+    mbar_arrive_expect_tx(bar, (uint32_t)(GRP * tm.n_box * tm.box_rows * 32 * sizeof(T)));
     for (int g = 0; g < GRP; ++g)
         for (int b = 0; b < tm.n_box; ++b)
             tma_load_2d(dst + g * tile_rows * 32 + b * tm.box_rows * 32, &tm.map, (int)((tile * GRP + g) * 32),
@@ -67,19 +69,21 @@ __device__ __forceinline__ void tile_issue(const TileMap &tm, int64_t tile, floa
 // 2-D TMA (tensor map over X[F][ld]).  GRP = 1: two tile buffers, the next tile's HBM read overlaps
 // the current walk (small, resident ensembles: HBM-bound).  GRP = 2: one buffer of 64 candidates,
 // so every streamed tree byte serves twice the candidates (large ensembles: L2-bound).
-template <int GRP, int KM>
+template <int GRP, int KM, bool RK>
 __global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, float base, int F, int tile_rows,
-                                                                 const float *__restrict__ X, int64_t n, int64_t ld,
+                                                                 const void *__restrict__ Xv, int64_t n, int64_t ld,
                                                                  float *__restrict__ score, uint8_t *__restrict__ slots,
                                                                  int use_bulk, const __grid_constant__ TileMap tm,
                                                                  const __grid_constant__ AcqArgs Q)
 {
+    using T = typename std::conditional<RK, uint32_t, float>::type;   // tile element: rank pair or feature value
     constexpr int NBUF = GRP == 1 ? 2 : 1;
+    const T *X = (const T *)Xv;
     extern __shared__ __align__(128) unsigned char smraw[];
     PredSmemHdr &hd = *(PredSmemHdr *)smraw;
     float *part = (float *)(smraw + 128);                      // [GRP][KM][32][32]
     float *fk = part + GRP * KM * 32 * 32;                     // [GRP][KM][32] per-model scores (KM > 1)
-    float *tiles = fk + (KM > 1 ? GRP * KM * 32 : 0);          // [NBUF][GRP][tile_rows][32], tile_rows >= F
+    T *tiles = (T *)(fk + (KM > 1 ? GRP * KM * 32 : 0));      // [NBUF][GRP][tile_rows][32], tile_rows >= F
     uint8_t *bufs = (uint8_t *)(tiles + NBUF * GRP * tile_rows * 32);   // tree buffers (rows are 128 B)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_tiles = (n + 32 * GRP - 1) / (32 * GRP);
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, flo
     for (int64_t i = 0; i < my_tiles; ++i) {
         const int64_t tile = blockIdx.x + i * gridDim.x;
         const int tb = (int)(i % NBUF);
-        float *tl = tiles + tb * tstride;
+        T *tl = tiles + tb * tstride;
         const int64_t cand0 = tile * 32 * GRP + lane;
         bool ok[GRP];
 #pragma unroll
@@ -112,10 +116,10 @@ __global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, flo
         } else {
             for (int g = 0; g < GRP; ++g)
                 for (int f = warp; f < F; f += PRED_NW)
-                    tl[g * tile_rows * 32 + f * 32 + lane] = ok[g] ? X[(int64_t)f * ld + cand0 + 32 * g] : 0.0f;
+                    tl[g * tile_rows * 32 + f * 32 + lane] = ok[g] ? X[(int64_t)f * ld + cand0 + 32 * g] : (T)0;
             __syncthreads();
         }
-        walk_pass<PRED_NW, GRP, KM>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part, slots,
+        walk_pass<PRED_NW, GRP, KM, RK>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part, slots,
                                     n, cand0, ok);
         if (KM == 1) {
             if (warp < GRP) {
@@ -262,6 +266,9 @@ int gbt_destroy(at_gbt g)
     // stream-ordered after the model's last enqueued use (predict / SA / fit output)
     cudaFreeAsync(g->d_nodes, g->last);
     cudaFreeAsync(g->d_leaf, g->last);
+    if (g->d_rk_nodes) cudaFreeAsync(g->d_rk_nodes, g->last);
+    if (g->d_thr_off) cudaFreeAsync(g->d_thr_off, g->last);
+    if (g->d_thr_val) cudaFreeAsync(g->d_thr_val, g->last);
     delete g;
     return AT_OK;
 }
@@ -269,6 +276,83 @@ int gbt_destroy(at_gbt g)
 }  // extern "C"
 
 namespace at {
+
+// ---------------------------------------------------------------- rank form (deep ensembles)
+// Depth >= 7 ensembles stream through shared memory once per candidate tile, and a block's walks in
+// flight are bounded by how many trees and candidates fit beside each other.  The rank form halves
+// both: a node is one word {feature | k << 16} (k = the 1-based index of its threshold among the
+// feature's sorted distinct thresholds) and a candidate feature is the u16 rank(x) = #{theta <= x},
+// computed by rank_encode_kernel.  For thresholds theta_1 < ... < theta_m, rank(x) < k <=> not
+// (theta_k <= x) <=> x < theta_k, so every branch -- and every score -- is bit-identical to the fp32
+// walk; a NaN feature ranks 0xFFFF (goes right everywhere, like x < theta = false).
+static int build_rank_form(at_gbt g)
+{
+    if (g->rk_state) return g->rk_state;
+    g->rk_state = -1;
+    if (g->n_features > 1022) return -1;   // tile byte offsets (F / 2) * 128 must fit 16 bits
+    const int64_t ni = (1 << g->depth) - 1;
+    std::vector<uint16_t> feat((size_t)g->n_trees * ni);
+    std::vector<float> thr((size_t)g->n_trees * ni);
+    if (gbt_export(g, feat.data(), thr.data(), nullptr, nullptr) != AT_OK) return -1;
+    const int F = g->n_features;
+    std::vector<std::vector<float>> vals(F);
+    for (size_t i = 0; i < feat.size(); ++i) vals[feat[i]].push_back(thr[i]);
+    std::vector<int32_t> off(F + 1, 0);
+    std::vector<float> tab;
+    for (int f = 0; f < F; ++f) {
+        std::vector<float> &v = vals[f];
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end(), [](float x, float y) { return x == y; }), v.end());   // -0 == +0
+        if (v.size() > 65534) return -1;
+        off[f] = (int32_t)tab.size();
+        tab.insert(tab.end(), v.begin(), v.end());
+    }
+    off[F] = (int32_t)tab.size();
+    std::vector<uint32_t> rk((size_t)g->t_pad * ni, 0u);   // padded trees: feature 0, k 0 (never walked)
+    for (size_t i = 0; i < feat.size(); ++i) {
+        const std::vector<float> &v = vals[feat[i]];
+        const size_t k = (size_t)(std::lower_bound(v.begin(), v.end(), thr[i]) - v.begin()) + 1;
+        const uint32_t off_f = ((uint32_t)feat[i] >> 1) * 128u + ((uint32_t)feat[i] & 1u) * 2u;   // byte in the tile
+        rk[i] = off_f | ((uint32_t)k << 16);
+    }
+    if (cudaMalloc((void **)&g->d_rk_nodes, rk.size() * 4) != cudaSuccess ||
+        cudaMalloc((void **)&g->d_thr_off, off.size() * 4) != cudaSuccess ||
+        cudaMalloc((void **)&g->d_thr_val, std::max<size_t>(tab.size(), 1) * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (cudaMemcpy(g->d_rk_nodes, rk.data(), rk.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(g->d_thr_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        (!tab.empty() && cudaMemcpy(g->d_thr_val, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess))
+        return -1;
+    g->rk_state = 1;
+    return 1;
+}
+
+// Xr[p][i] = rank(X[2p][i]) | rank(X[2p + 1][i]) << 16, rank = #{theta <= x} among the feature's
+// sorted distinct thresholds (binary search; NaN ranks 0xFFFF)
+__device__ __forceinline__ uint32_t rank_of(float x, const int32_t *__restrict__ off, const float *__restrict__ val, int f)
+{
+    const int b = __ldg(off + f), e = __ldg(off + f + 1);
+    int lo = b, hi = e;   // first theta > x
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(val + mid) <= x) lo = mid + 1; else hi = mid;
+    }
+    return x != x ? 0xFFFFu : (uint32_t)(lo - b);
+}
+
+__global__ void rank_encode_kernel(const float *__restrict__ X, int64_t n, int64_t ld, int F,
+                                   const int32_t *__restrict__ off, const float *__restrict__ val,
+                                   uint32_t *__restrict__ Xr, int64_t ldr)
+{
+    const int p = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t r0 = rank_of(X[(int64_t)(2 * p) * ld + i], off, val, 2 * p);
+    const uint32_t r1 = 2 * p + 1 < F ? rank_of(X[(int64_t)(2 * p + 1) * ld + i], off, val, 2 * p + 1) : 0u;
+    Xr[(int64_t)p * ldr + i] = r0 | (r1 << 16);
+}
 
 // gbt_predict / gbt_predict_acq: one persistent scorer launch (KM = 1: one model; KM = 8: up to 8
 // concatenated models of equal tree count with their acquisition)
@@ -278,33 +362,102 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
     cudaStream_t s = (cudaStream_t)stream;
     g->last = s;
     const int KM = acq ? 8 : 1;
-    TreeGeo G = make_geo(g, acq ? 32 * 1024 : TREE_BUF_BYTES);
-    if (acq) G.Tm = g->n_trees / acq->K;
     const int F = g->n_features;
     const int n_box = (F + 255) / 256, box_rows = (F + n_box - 1) / n_box, tile_rows = n_box * box_rows;
+    constexpr size_t SMEM_MAX = 227 * 1024;
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        AT_CUDA_TRY(cudaGetDevice(&dev));
+        AT_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    // rank form: deep ensembles that stream (4 candidate groups per tile, 16-tree chunks)
+    const char *rk_e = getenv("AT_PREDICT_RANK");   // "0" forces the fp32 walk
+    const bool want_rk = !acq && g->depth >= 7 && (!rk_e || atoi(rk_e) != 0) && n > 0;
+    constexpr int RGRP = 4;
+    if (want_rk && build_rank_form(g) == 1) {
+        const int P = (F + 1) / 2;   // u32 rank pairs per candidate
+        const int pn_box = (P + 255) / 256, pbox_rows = (P + pn_box - 1) / pn_box, ptile_rows = pn_box * pbox_rows;
+        TreeGeo G = make_geo(g, 16 * ((uint32_t)((1 << g->depth) - 1) * 4u + (uint32_t)(1 << g->depth) * 4u), true);
+        const size_t smem = 128 + (size_t)RGRP * 32 * 32 * sizeof(float) + (size_t)RGRP * ptile_rows * 32 * 4 +
+                            tree_smem_bytes(G);
+        if (!G.resident && smem <= SMEM_MAX) {
+            static size_t rk_attr = 0;
+            if (smem > rk_attr) {
+                AT_CUDA_TRY(cudaFuncSetAttribute(predict_kernel<RGRP, 1, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                rk_attr = smem;
+                // freed stream-ordered scratch (the rank tiles below) stays in the pool between calls
+                cudaMemPool_t pool;
+                int dev = 0;
+                uint64_t keep = ~0ull;
+                if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            const int64_t ldr = (n + 3) / 4 * 4;   // 16-B rows for the tensor map
+            uint32_t *Xr = nullptr;
+            AT_CUDA_TRY(cudaMallocAsync((void **)&Xr, (size_t)P * ldr * 4, s));
+            {
+                ProfScope ps(AT_K_FEATURES, s);
+                rank_encode_kernel<<<dim3((unsigned)((n + 255) / 256), P), 256, 0, s>>>(d_feat, n, ld, F, g->d_thr_off,
+                                                                                       g->d_thr_val, Xr, ldr);
+                note_launch();
+                AT_LAUNCH_CHECK("rank_encode_kernel");
+            }
+            TileMap tm{};
+            tm.n_box = pn_box;
+            tm.box_rows = pbox_rows;
+            int use_bulk = 0;
+            {
+                static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+                if (!encode) {
+                    void *fn = nullptr;
+                    cudaDriverEntryPointQueryResult q;
+                    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                        q == cudaDriverEntryPointSuccess)
+                        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+                }
+                const cuuint64_t dims[2] = {(cuuint64_t)ldr, (cuuint64_t)P};
+                const cuuint64_t strides[1] = {(cuuint64_t)ldr * 4};
+                const cuuint32_t box[2] = {32u, (cuuint32_t)pbox_rows};
+                const cuuint32_t estr[2] = {1u, 1u};
+                use_bulk = encode && encode(&tm.map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void *)Xr, dims, strides, box,
+                                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            }
+            const int64_t tiles = (n + 32 * RGRP - 1) / (32 * RGRP);
+            const unsigned blocks = (unsigned)std::min<int64_t>(tiles, n_sm);
+            AcqArgs Q{};
+            {
+                ProfScope ps(AT_K_PREDICT, s);
+                predict_kernel<RGRP, 1, true><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
+                                                                                 d_score, d_leaf_slot, use_bulk, tm, Q);
+                note_launch();
+                AT_LAUNCH_CHECK("predict_kernel (rank form)");
+            }
+            AT_CUDA_TRY(cudaFreeAsync(Xr, s));
+            return AT_OK;
+        }
+    }
+    TreeGeo G = make_geo(g, acq ? 32 * 1024 : TREE_BUF_BYTES);
+    if (acq) G.Tm = g->n_trees / acq->K;
     // GRP = 2 (64 candidates per tile, one buffer) when the ensemble streams and it fits
     auto smem_for = [&](int grp) {
         const int nbuf = grp == 1 ? 2 : 1;
         return 128 + (size_t)grp * KM * 32 * 32 * sizeof(float) + (KM > 1 ? (size_t)grp * KM * 32 * sizeof(float) : 0) +
                (size_t)nbuf * grp * tile_rows * 32 * sizeof(float) + tree_smem_bytes(G);
     };
-    constexpr size_t SMEM_MAX = 227 * 1024;
     const int grp = (!acq && !G.resident && smem_for(2) <= SMEM_MAX) ? 2 : 1;
     const size_t smem = smem_for(grp);
     if (smem > SMEM_MAX) return fail(AT_EUNSUPPORTED, "gbt_predict: too many features for the smem tiles");
-    const void *kern = acq ? (const void *)predict_kernel<1, 8>
-                     : grp == 1 ? (const void *)predict_kernel<1, 1> : (const void *)predict_kernel<2, 1>;
+    const void *kern = acq ? (const void *)predict_kernel<1, 8, false>
+                     : grp == 1 ? (const void *)predict_kernel<1, 1, false> : (const void *)predict_kernel<2, 1, false>;
     static size_t attr[3] = {0, 0, 0};
     const int ai = acq ? 2 : grp - 1;
     if (smem > attr[ai]) {
         AT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[ai] = smem;
-    }
-    static int n_sm = 0;
-    if (!n_sm) {
-        int dev = 0;
-        AT_CUDA_TRY(cudaGetDevice(&dev));
-        AT_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
     // TMA tensor map over X[F][ld] (needs 16-B aligned rows); otherwise plain loads
     TileMap tm{};
@@ -335,13 +488,13 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
     if (acq) Q = *acq;
     ProfScope ps(AT_K_PREDICT, s);
     if (acq)
-        predict_kernel<1, 8><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+        predict_kernel<1, 8, false><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                 d_leaf_slot, use_bulk, tm, Q);
     else if (grp == 1)
-        predict_kernel<1, 1><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+        predict_kernel<1, 1, false><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                 d_leaf_slot, use_bulk, tm, Q);
     else
-        predict_kernel<2, 1><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+        predict_kernel<2, 1, false><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                 d_leaf_slot, use_bulk, tm, Q);
     note_launch();
     AT_LAUNCH_CHECK("predict_kernel");

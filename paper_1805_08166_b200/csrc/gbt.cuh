@@ -20,18 +20,19 @@
 namespace at {
 
 struct TreeGeo {
-    const uint2 *nodes;     // [T_pad][ni]
+    const uint8_t *nodes;   // [T_pad][ni] uint2 {feature, threshold bits} (nbytes 8) or rank words (nbytes 4)
+    int nbytes;             // bytes per internal node
     const float *leaf;      // [T_pad][nl]
     int T, T_pad, D, ni, nl;
     int CH;                 // trees per chunk (even: 16-B aligned bulk copies)
     int NC;                 // chunks per pass
-    uint32_t chunk_bytes;   // CH * (ni * 8 + nl * 4)
+    uint32_t chunk_bytes;   // CH * (ni * nbytes + nl * 4)
     int resident;           // NC <= 2: loaded once, never re-streamed
     int Tm;                 // trees per model (KM > 1: K equal models concatenated, gbt_predict_acq)
 };
 
 constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // default per buffer (two buffers)
-TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes = TREE_BUF_BYTES);
+TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes = TREE_BUF_BYTES, bool rank = false);
 
 __device__ __forceinline__ void ts_issue(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint64_t c)
 {
@@ -39,11 +40,11 @@ __device__ __forceinline__ void ts_issue(const TreeGeo &G, uint8_t *bufs, uint64
     const int b = (int)(c & 1);
     const int t0 = k * G.CH;
     const int nt = min(G.CH, G.T_pad - t0);
-    const uint32_t nb = (uint32_t)nt * G.ni * 8u, lb = (uint32_t)nt * G.nl * 4u;
+    const uint32_t nb = (uint32_t)nt * G.ni * (uint32_t)G.nbytes, lb = (uint32_t)nt * G.nl * 4u;
     uint8_t *dst = bufs + (size_t)b * G.chunk_bytes;
     mbar_arrive_expect_tx(&bar[b], nb + lb);
-    bulk_g2s(dst, G.nodes + (int64_t)t0 * G.ni, nb, &bar[b]);
-    bulk_g2s(dst + (size_t)G.CH * G.ni * 8, G.leaf + (int64_t)t0 * G.nl, lb, &bar[b]);
+    bulk_g2s(dst, G.nodes + (int64_t)t0 * G.ni * G.nbytes, nb, &bar[b]);
+    bulk_g2s(dst + (size_t)G.CH * G.ni * G.nbytes, G.leaf + (int64_t)t0 * G.nl, lb, &bar[b]);
 }
 
 // thread 0: initialise both barriers and start the first two chunks of the stream
@@ -59,40 +60,58 @@ __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64
 }
 
 // A batch of NB trees t = t0, t0 + NW, ... (all owned by this warp: t = warp mod NW) walked for
-// GRP candidate groups at once: NB * GRP independent dependency chains.
-template <int NW, int GRP, int NB, int KM>
-__device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf, int c0, int t0, const float *tile,
+// GRP candidate groups at once: NB * GRP independent dependency chains.  RK: rank form -- 4-byte
+// nodes {tile byte offset of the feature | k << 16}, tiles of u16 feature ranks in pairs,
+// x < theta <=> rank < k.
+template <int NW, int GRP, int NB, int KM, bool RK = false>
+__device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf, int c0, int t0, const void *tile,
                                            int gstride, int lane, float (&p)[GRP][KM][32 / NW],
                                            uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand0,
                                            const bool (&cand_ok)[GRP])
 {
     constexpr int NQ = 32 / NW;
-    const float *leaves = (const float *)(buf + (size_t)G.CH * G.ni * 8);
+    constexpr uint32_t NBY = RK ? 4u : 8u;   // bytes per node
+    const float *leaves = (const float *)(buf + (size_t)G.CH * G.ni * NBY);
     const int D = G.D, ni = G.ni, nl = G.nl;
-    const uint32_t tree_bytes = (uint32_t)ni * 8u;
-    // a = shared address of the current node = tb + 8 h (h: 1-based heap index, tb = tree base - 8);
-    // the left child 2h sits at 2a - tb, the right one 2h + 1 at 2a - tb + 8, so one select of a
-    // precomputed addend and one 3-input add advance a walk: LDS.64, IMAD, LDS, FSETP, SEL, IADD3
+    const uint32_t tree_bytes = (uint32_t)ni * NBY;
+    // a = shared address of the current node = tb + NBY h (h: 1-based heap index, tb = tree base -
+    // NBY); the left child 2h sits at 2a - tb, the right one 2h + 1 at 2a - tb + NBY, so one select
+    // of a precomputed addend and one 3-input add advance a walk: LDS.64, IMAD, LDS, FSETP, SEL, IADD3
     uint32_t add_l[NB], add_r[NB], a[GRP][NB];
 #pragma unroll
     for (int jj = 0; jj < NB; ++jj) {
-        const uint32_t tb = (uint32_t)__cvta_generic_to_shared(buf) + (uint32_t)(t0 + jj * NW - c0) * tree_bytes - 8u;
+        const uint32_t tb = (uint32_t)__cvta_generic_to_shared(buf) + (uint32_t)(t0 + jj * NW - c0) * tree_bytes - NBY;
         add_l[jj] = 0u - tb;
-        add_r[jj] = 8u - tb;
+        add_r[jj] = NBY - tb;
 #pragma unroll
-        for (int g = 0; g < GRP; ++g) a[g][jj] = tb + 8u;
+        for (int g = 0; g < GRP; ++g) a[g][jj] = tb + NBY;
     }
     for (int d = 0; d < D; ++d) {
 #pragma unroll
         for (int g = 0; g < GRP; ++g) {
-            const uint32_t tile_lane = (uint32_t)__cvta_generic_to_shared(tile + g * gstride + lane);   // feature f at + f * 128
+            if (RK) {
+                // u32 tile of rank pairs: feature f of candidate `lane` at + (f / 2) * 128 + (f % 2) * 2
+                // (bank = lane whatever f); the node's low half is that byte offset
+                const uint32_t tile_lane =
+                    (uint32_t)__cvta_generic_to_shared((const uint32_t *)tile + g * gstride + lane);
 #pragma unroll
-            for (int jj = 0; jj < NB; ++jj) {
-                uint32_t nf, nt;
-                float x;
-                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g][jj]));
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile_lane + (nf << 7)));
-                a[g][jj] = 2u * a[g][jj] + (x < __uint_as_float(nt) ? add_l[jj] : add_r[jj]);
+                for (int jj = 0; jj < NB; ++jj) {
+                    uint32_t nd, x;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nd) : "r"(a[g][jj]));
+                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(tile_lane + (nd & 0xFFFFu)));
+                    a[g][jj] = 2u * a[g][jj] + (x < (nd >> 16) ? add_l[jj] : add_r[jj]);
+                }
+            } else {
+                const uint32_t tile_lane =
+                    (uint32_t)__cvta_generic_to_shared((const float *)tile + g * gstride + lane);   // f at + f * 128
+#pragma unroll
+                for (int jj = 0; jj < NB; ++jj) {
+                    uint32_t nf, nt;
+                    float x;
+                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g][jj]));
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile_lane + (nf << 7)));
+                    a[g][jj] = 2u * a[g][jj] + (x < __uint_as_float(nt) ? add_l[jj] : add_r[jj]);
+                }
             }
         }
     }
@@ -107,7 +126,7 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
         const int j = (u & 31) / NW;
 #pragma unroll
         for (int g = 0; g < GRP; ++g) {
-            const int slot = (int)((a[g][jj] + add_l[jj]) >> 3) - nl;   // h = (a - tb) / 8 in [2^D, 2^(D+1))
+            const int slot = (int)((a[g][jj] + add_l[jj]) >> (RK ? 2 : 3)) - nl;   // h = (a - tb) / NBY in [2^D, 2^(D+1))
             const float lv = leaves[(t - c0) * nl + slot];
 #pragma unroll
             for (int m = 0; m < KM; ++m)
@@ -123,8 +142,8 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
 // in ascending order, in batches of up to 4 / GRP trees; no walk slot is spent on an absent tree,
 // whatever the chunk size.  GRP candidate groups of 32 (group g's tile at tile + g * gstride floats)
 // share every staged tree byte.
-template <int NW, int GRP, int KM>
-__device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const float *tile, int gstride,
+template <int NW, int GRP, int KM, bool RK = false>
+__device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const void *tile, int gstride,
                                            int lane, int warp, float (&p)[GRP][KM][32 / NW], uint8_t *__restrict__ slots,
                                            int64_t slot_ld, int64_t cand0, const bool (&cand_ok)[GRP])
 {
@@ -133,28 +152,28 @@ __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf,
     const int c1 = min(c0 + G.CH, G.T);
     int t0 = c0 + ((warp - c0) % NW + NW) % NW;
     for (; t0 + (NBMAX - 1) * NW < c1; t0 += NBMAX * NW)
-        walk_batch<NW, GRP, NBMAX, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, NBMAX, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
     int rest = t0 < c1 ? (c1 - 1 - t0) / NW + 1 : 0;   // warp-uniform, < NBMAX
     if (NBMAX > 4 && rest >= 4) {
-        walk_batch<NW, GRP, 4, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 4, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
         t0 += 4 * NW;
         rest -= 4;
     }
     if (NBMAX >= 4 && rest == 3)
-        walk_batch<NW, GRP, 3, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 3, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
     else if (rest >= 2)
-        walk_batch<NW, GRP, 2, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 2, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
     else if (rest == 1)
-        walk_batch<NW, GRP, 1, KM>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 1, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
 }
 
 // One full pass over the ensemble.  `c` is the block-wide stream counter (identical in every
 // thread); `c_limit` the total number of chunks the kernel will consume.  Ends with group g's
 // partials in part[g * 1024 + q * 32 + lane] (KM models: part[((g KM + m) 32 + q) 32 + lane])
 // and a __syncthreads.
-template <int NW, int GRP, int KM = 1>
+template <int NW, int GRP, int KM = 1, bool RK = false>
 __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph, uint64_t &c,
-                                          uint64_t c_limit, const float *tile, int gstride, int lane, int warp,
+                                          uint64_t c_limit, const void *tile, int gstride, int lane, int warp,
                                           float *part, uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand0,
                                           const bool (&cand_ok)[GRP])
 {
@@ -168,14 +187,14 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
             for (int j = 0; j < NQ; ++j) p[g][m][j] = 0.0f;
     if (G.resident) {
         for (int k = 0; k < G.NC; ++k)
-            walk_chunk<NW, GRP, KM>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
+            walk_chunk<NW, GRP, KM, RK>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
                                 cand0, cand_ok);
     } else {
         for (int k = 0; k < G.NC; ++k, ++c) {
             const int b = (int)(c & 1);
             mbar_wait(&bar[b], ph[b]);
             ph[b] ^= 1u;
-            walk_chunk<NW, GRP, KM>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
+            walk_chunk<NW, GRP, KM, RK>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
                                 cand0, cand_ok);
             __syncthreads();   // every warp is done with buffer b
             if (threadIdx.x == 0 && c + 2 < c_limit) {

@@ -113,8 +113,10 @@ def test_hand_ensemble(at):
         assert np.array_equal(ex[k], e[k])
 
 
-@pytest.mark.parametrize("T,D,n", [(100, 6, 2048), (37, 3, 1000), (500, 6, 777), (1000, 8, 300), (33, 1, 65)])
+@pytest.mark.parametrize("T,D,n", [(100, 6, 2048), (37, 3, 1000), (500, 6, 777), (1000, 8, 300), (33, 1, 65),
+                                   (2000, 8, 4099), (150, 7, 1000)])
 def test_gbt_predict_scores_and_slots(at, T, D, n):
+    """Depth >= 7 ensembles that stream go through the rank form (u16 feature ranks, 4-B nodes)."""
     ens = synth.ensemble(T, D, seed=T * 10 + D)
     osp = O.OracleSpace([O.workload(**w) for w in synth.ALL_RESNET])
     idx = synth.uniform_indices(osp.size(), n, seed=T)
@@ -128,6 +130,42 @@ def test_gbt_predict_scores_and_slots(at, T, D, n):
     s = s.cpu().numpy()
     assert np.all(np.abs(s - es) <= 1e-6 * np.maximum(np.abs(es), 1e-30) + 0.0)
     assert_bits_equal(s, es, "scores (canonical order => bit-exact)")
+
+
+@pytest.mark.parametrize("T,D", [(400, 8), (300, 7)])
+def test_predict_rank_form_edge_values(at, T, D):
+    """Rank form vs the fp32 walk (AT_PREDICT_RANK=0) on feature values equal to thresholds, -0.0 /
+    +0.0, +-inf and NaN, with +inf pass-through and -inf / 0.0 thresholds: same scores, same slots."""
+    rng = np.random.default_rng(T)
+    ens = synth.ensemble(T, D, seed=T + D)
+    th = ens["thresh"]
+    th[:, 0] = np.float32(np.inf)                          # roots: pass-through
+    th[rng.random(th.shape) < 0.02] = np.float32(-np.inf)
+    th[rng.random(th.shape) < 0.02] = np.float32(0.0)
+    th[rng.random(th.shape) < 0.02] = np.float32(-0.0)
+    n = 3000
+    X = np.power(2.0, rng.integers(0, 42, size=(468, n)) / 2.0).astype(np.float32)   # many exact threshold values
+    m = rng.random(X.shape)
+    X[m < 0.01] = np.float32(-0.0)
+    X[(m >= 0.01) & (m < 0.02)] = np.float32(0.0)
+    X[(m >= 0.02) & (m < 0.025)] = np.float32(np.inf)
+    X[(m >= 0.025) & (m < 0.03)] = np.float32(-np.inf)
+    X[(m >= 0.03) & (m < 0.035)] = np.float32(np.nan)
+    Xg = dev(np.ascontiguousarray(X))
+    g = at.Gbt(ens["feat"], th, ens["leaf"], base=0.5)
+    outs = []
+    for env in ("1", "0"):
+        os.environ["AT_PREDICT_RANK"] = env
+        try:
+            s, sl = g.predict(Xg, n=n, slots=True)
+            outs.append((s.cpu().numpy(), sl.cpu().numpy()))
+        finally:
+            os.environ.pop("AT_PREDICT_RANK", None)
+    assert_bits_equal(outs[0][1], outs[1][1], "leaf slots")
+    assert_bits_equal(outs[0][0], outs[1][0], "scores")
+    fin = np.all(np.isfinite(X), axis=0)   # the oracle on the finite-feature candidates
+    es, esl = O.OracleGbt(ens["feat"], th, ens["leaf"], base=0.5).predict(np.ascontiguousarray(X[:, fin].T), slots=True)
+    assert_bits_equal(outs[0][0][fin], es, "scores vs oracle")
 
 
 def test_scores_config1_exhaustive_top8(at):
