@@ -182,8 +182,8 @@ struct at_gbt_s {
     float *d_leaf;                // [t_pad][2^D]
     cudaStream_t last;            // stream of the last enqueued use: gbt_destroy frees stream-ordered
                                   // there (no device-wide sync from cudaFree inside a tuning loop)
-    // rank form for deep ensembles (gbt.cu): node = feature | k << 16 with k the 1-based index of
-    // its threshold among feature f's sorted distinct thresholds thr_val[thr_off[f] ..]; x < theta_k
+    // rank form for deep ensembles (gbt.cu): node = k | (tile byte offset of f) << 16 with k the
+    // 1-based index of its threshold among feature f's sorted distinct thresholds thr_val[thr_off[f] ..]; x < theta_k
     // <=> rank(x) < k, rank(x) = #{theta <= x}.  rk_state: 0 not built, 1 built, -1 unavailable
     uint32_t *d_rk_nodes;
     int32_t *d_thr_off;

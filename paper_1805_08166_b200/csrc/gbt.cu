@@ -280,7 +280,7 @@ namespace at {
 // ---------------------------------------------------------------- rank form (deep ensembles)
 // Depth >= 7 ensembles stream through shared memory once per candidate tile, and a block's walks in
 // flight are bounded by how many trees and candidates fit beside each other.  The rank form halves
-// both: a node is one word {feature | k << 16} (k = the 1-based index of its threshold among the
+// both: a node is one word {k | tile offset << 16} (k = the 1-based index of its threshold among the
 // feature's sorted distinct thresholds) and a candidate feature is the u16 rank(x) = #{theta <= x},
 // computed by rank_encode_kernel.  For thresholds theta_1 < ... < theta_m, rank(x) < k <=> not
 // (theta_k <= x) <=> x < theta_k, so every branch -- and every score -- is bit-identical to the fp32
@@ -308,12 +308,12 @@ static int build_rank_form(at_gbt g)
         tab.insert(tab.end(), v.begin(), v.end());
     }
     off[F] = (int32_t)tab.size();
-    std::vector<uint32_t> rk((size_t)g->t_pad * ni, 0u);   // padded trees: feature 0, k 0 (never walked)
+    std::vector<uint32_t> rk((size_t)g->t_pad * ni, 0u);   // padded trees: offset 0, k 0 (never walked)
     for (size_t i = 0; i < feat.size(); ++i) {
         const std::vector<float> &v = vals[feat[i]];
         const size_t k = (size_t)(std::lower_bound(v.begin(), v.end(), thr[i]) - v.begin()) + 1;
         const uint32_t off_f = ((uint32_t)feat[i] >> 1) * 128u + ((uint32_t)feat[i] & 1u) * 2u;   // byte in the tile
-        rk[i] = off_f | ((uint32_t)k << 16);
+        rk[i] = (uint32_t)k | (off_f << 16);
     }
     if (cudaMalloc((void **)&g->d_rk_nodes, rk.size() * 4) != cudaSuccess ||
         cudaMalloc((void **)&g->d_thr_off, off.size() * 4) != cudaSuccess ||
@@ -374,19 +374,23 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
     // rank form: deep ensembles that stream (4 candidate groups per tile, 16-tree chunks)
     const char *rk_e = getenv("AT_PREDICT_RANK");   // "0" forces the fp32 walk
     const bool want_rk = !acq && g->depth >= 7 && (!rk_e || atoi(rk_e) != 0) && n > 0;
-    constexpr int RGRP = 4;
+    // AT_RK_GRP: candidate groups per tile (2: 32-tree chunks, default; 4: 16-tree chunks -- the same
+    // walks in flight per warp, half the tiles: equal at 10^7+ candidates, worse balanced below)
+    const char *rg_e = getenv("AT_RK_GRP");
+    const int RGRP = rg_e && atoi(rg_e) == 4 ? 4 : 2;
     if (want_rk && build_rank_form(g) == 1) {
         const int P = (F + 1) / 2;   // u32 rank pairs per candidate
         const int pn_box = (P + 255) / 256, pbox_rows = (P + pn_box - 1) / pn_box, ptile_rows = pn_box * pbox_rows;
-        TreeGeo G = make_geo(g, 16 * ((uint32_t)((1 << g->depth) - 1) * 4u + (uint32_t)(1 << g->depth) * 4u), true);
+        TreeGeo G = make_geo(g, (RGRP == 2 ? 32 : 16) * ((uint32_t)((1 << g->depth) - 1) * 4u + (uint32_t)(1 << g->depth) * 4u),
+                             true);
         const size_t smem = 128 + (size_t)RGRP * 32 * 32 * sizeof(float) + (size_t)RGRP * ptile_rows * 32 * 4 +
                             tree_smem_bytes(G);
         if (!G.resident && smem <= SMEM_MAX) {
-            static size_t rk_attr = 0;
-            if (smem > rk_attr) {
-                AT_CUDA_TRY(cudaFuncSetAttribute(predict_kernel<RGRP, 1, true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                rk_attr = smem;
+            const void *rk_kern = RGRP == 2 ? (const void *)predict_kernel<2, 1, true> : (const void *)predict_kernel<4, 1, true>;
+            static size_t rk_attr[2] = {0, 0};
+            if (smem > rk_attr[RGRP == 2]) {
+                AT_CUDA_TRY(cudaFuncSetAttribute(rk_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                rk_attr[RGRP == 2] = smem;
                 // freed stream-ordered scratch (the rank tiles below) stays in the pool between calls
                 cudaMemPool_t pool;
                 int dev = 0;
@@ -431,8 +435,12 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
             AcqArgs Q{};
             {
                 ProfScope ps(AT_K_PREDICT, s);
-                predict_kernel<RGRP, 1, true><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
-                                                                                 d_score, d_leaf_slot, use_bulk, tm, Q);
+                if (RGRP == 2)
+                    predict_kernel<2, 1, true><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
+                                                                                  d_score, d_leaf_slot, use_bulk, tm, Q);
+                else
+                    predict_kernel<4, 1, true><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
+                                                                                  d_score, d_leaf_slot, use_bulk, tm, Q);
                 note_launch();
                 AT_LAUNCH_CHECK("predict_kernel (rank form)");
             }

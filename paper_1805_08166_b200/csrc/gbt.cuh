@@ -61,7 +61,7 @@ __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64
 
 // A batch of NB trees t = t0, t0 + NW, ... (all owned by this warp: t = warp mod NW) walked for
 // GRP candidate groups at once: NB * GRP independent dependency chains.  RK: rank form -- 4-byte
-// nodes {tile byte offset of the feature | k << 16}, tiles of u16 feature ranks in pairs,
+// nodes {k | tile byte offset of the feature << 16}, tiles of u16 feature ranks in pairs,
 // x < theta <=> rank < k.
 template <int NW, int GRP, int NB, int KM, bool RK = false>
 __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf, int c0, int t0, const void *tile,
@@ -91,15 +91,15 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
         for (int g = 0; g < GRP; ++g) {
             if (RK) {
                 // u32 tile of rank pairs: feature f of candidate `lane` at + (f / 2) * 128 + (f % 2) * 2
-                // (bank = lane whatever f); the node's low half is that byte offset
+                // (bank = lane whatever f); the node's high half is that byte offset, the low half k
                 const uint32_t tile_lane =
                     (uint32_t)__cvta_generic_to_shared((const uint32_t *)tile + g * gstride + lane);
 #pragma unroll
                 for (int jj = 0; jj < NB; ++jj) {
                     uint32_t nd, x;
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nd) : "r"(a[g][jj]));
-                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(tile_lane + (nd & 0xFFFFu)));
-                    a[g][jj] = 2u * a[g][jj] + (x < (nd >> 16) ? add_l[jj] : add_r[jj]);
+                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(tile_lane + (nd >> 16)));
+                    a[g][jj] = 2u * a[g][jj] + (x < (nd & 0xFFFFu) ? add_l[jj] : add_r[jj]);
                 }
             } else {
                 const uint32_t tile_lane =
