@@ -226,10 +226,12 @@ __device__ __forceinline__ uint32_t feistel(uint32_t x, int h, uint64_t seed, ui
 
 __global__ void positions_kernel(const uint16_t *__restrict__ key, const int32_t *__restrict__ rank,
                                  const int32_t *__restrict__ counts, const int32_t *__restrict__ woff, int64_t n,
-                                 uint64_t seed, uint32_t tree, int32_t *__restrict__ member)
+                                 uint64_t seed, uint32_t tree, int32_t *__restrict__ member,
+                                 const int32_t *__restrict__ d_tree = nullptr)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (d_tree) tree = (uint32_t)*d_tree;   // per-tree graph: the tree index lives on the device
     const uint32_t k = key[i];
     const uint32_t nw = (uint32_t)counts[k];
     int bits = 0;
@@ -452,8 +454,9 @@ __global__ void __launch_bounds__(256) hist_kernel(const uint8_t *__restrict__ b
 
 // tree 0 root histogram back to the dense [F][B][2] layout (parity hook)
 __global__ void hist0_expand_kernel(const int64_t *__restrict__ hist, const int32_t *__restrict__ boff, int F, int B,
-                                    int64_t *__restrict__ out)
+                                    int64_t *__restrict__ out, const int32_t *__restrict__ d_tree = nullptr)
 {
+    if (d_tree && *d_tree != 0) return;   // tree 0 only
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (int64_t)F * B) return;
     const int f = (int)(q / B), b = (int)(q - (int64_t)f * B);
@@ -812,7 +815,7 @@ __global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int3
 // rule); blocks flush with native 64-bit global atomics.  Node totals travel down the tree
 // (left = the winning split's prefix sums, right = total - left), so the leaves need no extra pass.
 constexpr int SUB_NT = 1024;
-constexpr int SUB_ROWS = 400;   // rows of 32 cells: 4 planes x 4 B x 32 x 400 = 200 KB of shared memory
+constexpr int SUB_ROWS = 400;   // rows of 32 cells (+ 1 trash row): 4 planes x 4 B x 32 x 401 = 200 KB of shared memory
 constexpr int SUB_NQW = 4;      // row words per lane and sample: <= 512 features per range
 constexpr int SUB_MAXR = 256;
 
@@ -850,8 +853,8 @@ __global__ void rowbins_kernel(const uint8_t *__restrict__ bins, int64_t n, cons
 __device__ __forceinline__ void sub_add64(uint32_t *lo, uint32_t *hi, int c, uint32_t vlo, uint32_t vhi)
 {
     const uint32_t old = atomicAdd(&lo[c], vlo);
-    const uint32_t add = vhi + ((old + vlo < old) ? 1u : 0u);   // exact modular 64-bit sum
-    if (add) atomicAdd(&hi[c], add);
+    atomicAdd(&hi[c], vhi + ((old + vlo < old) ? 1u : 0u));   // exact modular 64-bit sum (unconditional:
+                                                               // no divergent branch in the warp)
 }
 
 // items[b] = {node slot, p0, p1, -}: block (b, r) adds positions [p0, p1) of perm (identity when
@@ -875,7 +878,7 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
     if ((int)blockIdx.x >= *n_items) return;
     const SubRange R = ranges[blockIdx.y];
     const int4 it = items[blockIdx.x];
-    const int P = R.rows * 32;
+    const int P = (R.rows + 1) * 32;   // + a trash row: empty slots (padding bytes are 0) add there
     uint32_t *glo = sm, *ghi = sm + P, *hlo = sm + 2 * P, *hhi = sm + 3 * P;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = SUB_NT / 32;
@@ -887,7 +890,7 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int r = 128 * u + 32 * j + lane;
-            rb[u][j] = r < R.nf ? rowbase[R.k_lo + r] * 32 + lane : -1;
+            rb[u][j] = (r < R.nf ? rowbase[R.k_lo + r] : R.rows) * 32 + lane;
         }
     __syncthreads();
     const uint8_t *rows = binsR + R.byte_off + 4 * lane;
@@ -916,14 +919,15 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
             if ((gv | hv) != 0ull) {   // warp-uniform: a zero-gradient sample contributes nothing
                 const uint32_t gl = (uint32_t)gv, gh = (uint32_t)(gv >> 32), hl = (uint32_t)hv, hh = (uint32_t)(hv >> 32);
 #pragma unroll
-                for (int u = 0; u < SUB_NQW; ++u)
+                for (int u = 0; u < SUB_NQW; ++u) {
+                    if (u >= nqw) break;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (rb[u][j] >= 0) {
-                            const int c = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
-                            sub_add64(glo, ghi, c, gl, gh);
-                            sub_add64(hlo, hhi, c, hl, hh);
-                        }
+                    for (int j = 0; j < 4; ++j) {
+                        const int c = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
+                        sub_add64(glo, ghi, c, gl, gh);
+                        sub_add64(hlo, hhi, c, hl, hh);
+                    }
+                }
             }
 #pragma unroll
             for (int u = 0; u < SUB_NQW; ++u) w[u] = wn[u];
@@ -971,8 +975,9 @@ __global__ void sub_root_items_kernel(int n, int target, int4 *__restrict__ item
 __global__ void sub_root_tot_kernel(int64_t *__restrict__ hist, const int32_t *__restrict__ boff,
                                     const int32_t *__restrict__ flist, int F, int n, int fill_const,
                                     int64_t *__restrict__ tot, int32_t *__restrict__ seg_start,
-                                    int32_t *__restrict__ seg_cnt)
+                                    int32_t *__restrict__ seg_cnt, const int32_t *__restrict__ d_tree)
 {
+    fill_const = fill_const && *d_tree == 0;   // the parity hook wants tree 0's root histogram
     __shared__ long long s_t[2];
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < 32) {
@@ -1029,8 +1034,11 @@ __global__ void __launch_bounds__(256) sub_decide_kernel(const double *__restric
                                                          const int32_t *__restrict__ boff, int TB,
                                                          uint8_t *__restrict__ dead, int32_t *__restrict__ split_f,
                                                          int32_t *__restrict__ split_s, uint16_t *__restrict__ tree_feat,
-                                                         float *__restrict__ tree_thr, int64_t *__restrict__ tot)
+                                                         float *__restrict__ tree_thr, int64_t *__restrict__ tot,
+                                                         int n_int, const int32_t *__restrict__ d_tree)
 {
+    tree_feat += (int64_t)*d_tree * n_int;   // this tree's nodes
+    tree_thr += (int64_t)*d_tree * n_int;
     const int lane = threadIdx.x & 31;
     const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (q >= nn) return;
@@ -1188,14 +1196,30 @@ __global__ void sub_subtract_kernel(const int64_t *__restrict__ parent, int64_t 
 // last level: every sample's leaf, prediction update in tree order
 __global__ void sub_final_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ node,
                                  const int32_t *__restrict__ split_f, const int32_t *__restrict__ split_s, int n_int,
-                                 const float *__restrict__ leaf, float *__restrict__ pred)
+                                 const float *__restrict__ leaf, float *__restrict__ pred, const int32_t *__restrict__ d_tree)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    leaf += (int64_t)*d_tree * (n_int + 1);
     const int nd = node[i];
     const int sf = split_f[nd];
     const int child = (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= split_s[nd]) ? 2 * nd + 2 : 2 * nd + 1;
     pred[i] = __fadd_rn(pred[i], leaf[child - n_int]);
+}
+
+// leaves of this tree from the level-D node totals: w = -eta G / (H + lambda)
+__global__ void sub_leaf_kernel(const int64_t *__restrict__ sums, int n_leaf, double eta, double lam,
+                                float *__restrict__ leaf, const int32_t *__restrict__ d_tree)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= n_leaf) return;
+    const double G = (double)sums[2 * l] * FX, H = (double)sums[2 * l + 1] * FX;
+    leaf[(int64_t)*d_tree * n_leaf + l] = (float)(-(eta * (G / (H + lam))));
+}
+
+__global__ void sub_tree_next_kernel(int32_t *d_tree)
+{
+    *d_tree += 1;
 }
 
 // ------------------------------------------------------------------ 4. fused forest (single rank, small n)
@@ -2155,7 +2179,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
 
     // a single-rank fit has no host callback between levels: its launches are captured once into a
     // CUDA graph and launched as one unit (no host round trips for ~10 launches per level)
-    auto run_captured = [&](auto &&enqueue) -> int {
+    auto run_captured = [&](auto &&enqueue, int reps) -> int {
         static thread_local cudaStream_t cs = nullptr;
         if (!cs) AT_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         prof_suspend(true);
@@ -2173,7 +2197,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph instantiate");
         {
             ProfScope ps(AT_K_FIT_GRAPH, s);
-            e = cudaGraphLaunch(exec, s);
+            for (int r = 0; r < reps && e == cudaSuccess; ++r) e = cudaGraphLaunch(exec, s);
         }
         cudaGraphExecDestroy(exec);
         if (e != cudaSuccess) return cuda_fail(e, "gbt_fit_hist: graph launch");
@@ -2259,101 +2283,109 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             rowbins_kernel<<<dim3(nblk(n, 32), nblk(FsP, 32)), dim3(32, 8), 0, s>>>(bins, n, flist, d_inv, FsP, binsR);
             note_launch();
             AT_LAUNCH_CHECK("rowbins");
-            const size_t hsm = (size_t)4 * 32 * max_rows * sizeof(uint32_t);
+            const size_t hsm = (size_t)4 * 32 * (max_rows + 1) * sizeof(uint32_t);
             static size_t sub_attr = 0;
             if (sub_attr < hsm) {
                 AT_CUDA_TRY(cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
                 sub_attr = hsm;
             }
+            // one tree is captured once and its graph launched n_trees times: the tree index lives on the
+            // device (d_tree, advanced by the graph's last node), so the host cost per fit is one capture
+            int32_t *d_tree = ws.get<int32_t>(1);
+            int4 *root_items = ws.get<int4>(max_items);
+            int32_t *root_n = ws.get<int32_t>(4);
+            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+            AT_CUDA_TRY(cudaMemsetAsync(d_tree, 0, sizeof(int32_t), s));
+            sub_root_items_kernel<<<1, 256, 0, s>>>((int)n, target, root_items, root_n);
+            note_launch();
             auto enqueue_sub = [&](cudaStream_t s) -> int {
-                for (int t = 0; t < o->n_trees; ++t) {
-                    {
-                        ProfScope ps(AT_K_FIT_GRAD, s);
-                        if (o->objective == AT_OBJ_REG) {
-                            reg_grads_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, pred, n, g, h); note_launch();
-                        } else {
-                            positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed,
-                                                                          (uint32_t)t, member); note_launch();
-                            if (n_groups > 0) {
-                                grads_kernel<<<n_groups, 256, (size_t)GS * 2 * sizeof(float), s>>>(member, counts, woff, gpre, GS,
-                                                                                     d_cost, pred, g, h);
-                                note_launch();
-                            }
+                {
+                    ProfScope ps(AT_K_FIT_GRAD, s);
+                    if (o->objective == AT_OBJ_REG) {
+                        reg_grads_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, pred, n, g, h); note_launch();
+                    } else {
+                        positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, 0u,
+                                                                      member, d_tree); note_launch();
+                        if (n_groups > 0) {
+                            grads_kernel<<<n_groups, 256, (size_t)GS * 2 * sizeof(float), s>>>(member, counts, woff, gpre,
+                                                                                                GS, d_cost, pred, g, h);
+                            note_launch();
                         }
-                        AT_LAUNCH_CHECK("fit gradients");
                     }
-                    AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
-                    AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
-                    uint16_t *tf = t_feat + (size_t)t * n_int;
-                    float *tt = t_thr + (size_t)t * n_int;
-                    int64_t *hp = hA, *hc = hB;
+                    AT_LAUNCH_CHECK("fit gradients");
+                }
+                AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
+                AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
+                int64_t *hp = hA, *hc = hB;
+                {
+                    ProfScope ps(AT_K_FIT_HIST, s);
+                    AT_CUDA_TRY(cudaMemsetAsync(hp, 0, sizeof(int64_t) * 2 * (size_t)TB, s));
+                    sub_hist_kernel<<<dim3(max_items, NR), SUB_NT, hsm, s>>>(binsR, FsP, nullptr, g, h, root_items, root_n,
+                                                                             d_rng, d_rowbase, d_gbase, d_nbk, TB, hp);
+                    note_launch();
+                    const int want_h0 = o->d_hist0_out != nullptr;
+                    sub_root_tot_kernel<<<1, 256, 0, s>>>(hp, boff, flist, F, (int)n, want_h0, tot, seg_start, seg_cnt,
+                                                          d_tree); note_launch();
+                    if (want_h0) {
+                        hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hp, boff, F, B, o->d_hist0_out,
+                                                                                     d_tree);
+                        note_launch();
+                    }
+                    AT_LAUNCH_CHECK("root histogram");
+                }
+                for (int d = 0; d < D; ++d) {
+                    const int first = (1 << d) - 1, nn = 1 << d;
+                    {
+                        ProfScope ps(AT_K_FIT_SPLIT, s);
+                        sub_split_kernel<<<nblk((int64_t)nn * Fs, 8), 256, 0, s>>>(hp, boff, flist, Fs, TB, first, nn, tot,
+                                                                                  lam, mcw, dead, bg, bs);
+                        note_launch();
+                        sub_decide_kernel<<<nblk(nn, 8), 256, 0, s>>>(bg, bs, flist, Fs, first, nn, cuts, B, hp, boff, TB,
+                                                                      dead, split_f, split_s, t_feat, t_thr, tot, n_int,
+                                                                      d_tree);
+                        note_launch();
+                        AT_LAUNCH_CHECK("split/decide");
+                    }
+                    if (d == D - 1) break;
+                    {
+                        ProfScope ps(AT_K_FIT_SPLIT, s);
+                        AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * nn, s));
+                        sub_scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, first, nn, seg_start,
+                                                                        seg_cnt, cursor, node, perm);
+                        note_launch();
+                        sub_worklist_kernel<<<1, 128, 0, s>>>(first, nn, split_f, cursor, seg_start, seg_cnt, target, items,
+                                                              cnts, subs, cnts + 1);
+                        note_launch();
+                        AT_LAUNCH_CHECK("scatter");
+                    }
                     {
                         ProfScope ps(AT_K_FIT_HIST, s);
-                        AT_CUDA_TRY(cudaMemsetAsync(hp, 0, sizeof(int64_t) * 2 * (size_t)TB, s));
-                        sub_root_items_kernel<<<1, 256, 0, s>>>((int)n, target, items, cnts); note_launch();
-                        sub_hist_kernel<<<dim3(max_items, NR), SUB_NT, hsm, s>>>(binsR, FsP, nullptr, g, h, items, cnts,
-                                                                                 d_rng, d_rowbase, d_gbase, d_nbk, TB, hp);
+                        AT_CUDA_TRY(cudaMemsetAsync(hc, 0, sizeof(int64_t) * 2 * (size_t)TB * 2 * nn, s));
+                        sub_hist_kernel<<<dim3(target + nn, NR), SUB_NT, hsm, s>>>(binsR, FsP, perm, g, h, items, cnts,
+                                                                                  d_rng, d_rowbase, d_gbase, d_nbk, TB, hc);
                         note_launch();
-                        const int want_h0 = t == 0 && o->d_hist0_out;
-                        sub_root_tot_kernel<<<1, 256, 0, s>>>(hp, boff, flist, F, (int)n, want_h0, tot, seg_start,
-                                                              seg_cnt); note_launch();
-                        if (want_h0) {
-                            hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hp, boff, F, B, o->d_hist0_out);
-                            note_launch();
-                        }
-                        AT_LAUNCH_CHECK("root histogram");
-                    }
-                    for (int d = 0; d < D; ++d) {
-                        const int first = (1 << d) - 1, nn = 1 << d;
-                        {
-                            ProfScope ps(AT_K_FIT_SPLIT, s);
-                            sub_split_kernel<<<nblk((int64_t)nn * Fs, 8), 256, 0, s>>>(hp, boff, flist, Fs, TB, first, nn,
-                                                                                      tot, lam, mcw, dead, bg, bs);
-                            note_launch();
-                            sub_decide_kernel<<<nblk(nn, 8), 256, 0, s>>>(bg, bs, flist, Fs, first, nn, cuts, B, hp, boff,
-                                                                          TB, dead, split_f, split_s, tf, tt, tot);
-                            note_launch();
-                            AT_LAUNCH_CHECK("split/decide");
-                        }
-                        if (d == D - 1) break;
-                        {
-                            ProfScope ps(AT_K_FIT_SPLIT, s);
-                            AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * nn, s));
-                            sub_scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, first, nn,
-                                                                            seg_start, seg_cnt, cursor, node, perm);
-                            note_launch();
-                            sub_worklist_kernel<<<1, 128, 0, s>>>(first, nn, split_f, cursor, seg_start, seg_cnt, target,
-                                                                  items, cnts, subs, cnts + 1);
-                            note_launch();
-                            AT_LAUNCH_CHECK("scatter");
-                        }
-                        {
-                            ProfScope ps(AT_K_FIT_HIST, s);
-                            AT_CUDA_TRY(cudaMemsetAsync(hc, 0, sizeof(int64_t) * 2 * (size_t)TB * 2 * nn, s));
-                            sub_hist_kernel<<<dim3(target + nn, NR), SUB_NT, hsm, s>>>(binsR, FsP, perm, g, h, items, cnts,
-                                                                                      d_rng, d_rowbase, d_gbase, d_nbk,
-                                                                                      TB, hc);
-                            note_launch();
-                            sub_subtract_kernel<<<dim3(std::min<unsigned>(nblk(2 * (int64_t)TB, 256), 64), nn), 256, 0,
-                                                  s>>>(hp, hc, TB, subs, cnts + 1);
-                            note_launch();
-                            AT_LAUNCH_CHECK("histograms");
-                        }
-                        std::swap(hp, hc);
-                    }
-                    {
-                        ProfScope ps(AT_K_FIT_UPDATE, s);
-                        float *tl = t_leaf + (size_t)t * n_leaf;
-                        leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(tot + 2 * (size_t)n_int, n_leaf, eta, lam, tl);
+                        sub_subtract_kernel<<<dim3(std::min<unsigned>(nblk(2 * (int64_t)TB, 256), 64), nn), 256, 0, s>>>(
+                            hp, hc, TB, subs, cnts + 1);
                         note_launch();
-                        sub_final_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, node, split_f, split_s, n_int, tl, pred);
-                        note_launch();
-                        AT_LAUNCH_CHECK("leaf/pred update");
+                        AT_LAUNCH_CHECK("histograms");
                     }
+                    std::swap(hp, hc);
+                }
+                {
+                    ProfScope ps(AT_K_FIT_UPDATE, s);
+                    sub_leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(tot + 2 * (size_t)n_int, n_leaf, eta, lam, t_leaf,
+                                                                      d_tree);
+                    note_launch();
+                    sub_final_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, node, split_f, split_s, n_int, t_leaf, pred,
+                                                                  d_tree);
+                    note_launch();
+                    sub_tree_next_kernel<<<1, 1, 0, s>>>(d_tree);
+                    note_launch();
+                    AT_LAUNCH_CHECK("leaf/pred update");
                 }
                 return AT_OK;
             };
-            const int rc = run_captured(enqueue_sub);
+            const int rc = run_captured(enqueue_sub, o->n_trees);
             if (rc) return rc;
             return finish();
         }
@@ -2481,7 +2513,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         const int rc = enqueue_trees(s);
         if (rc) return rc;
     } else {
-        const int rc = run_captured(enqueue_trees);
+        const int rc = run_captured(enqueue_trees, 1);
         if (rc) return rc;
     }
     return finish();
