@@ -13,3 +13,10 @@ ncu --set full --clock-control none --import-source on -k regex:fused_forest -c 
 ncu --set full --clock-control none --import-source on -k regex:"predict_kernel|features_kernel" -c 4 -o gpurun_out/scoring \
     python tools/prof_scoring.py > gpurun_out/ncu_scoring.log 2>&1
 ls -la gpurun_out
+ncu --set full --clock-control none --import-source on -k regex:sub_hist_kernel -c 2 -o gpurun_out/subhist \
+    python tools/prof_fit.py 1 > gpurun_out/ncu_subhist.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/fit_launches.csv \
+    python tools/prof_fit.py 5 > gpurun_out/ncu_fit.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:predict_kernel -s 1 -c 1 -o gpurun_out/pred5rk \
+    python tools/prof_cfg5.py > gpurun_out/ncu_pred5rk.log 2>&1
+ls -la gpurun_out
