@@ -1000,33 +1000,9 @@ __global__ void sub_root_tot_kernel(int64_t *__restrict__ hist, const int32_t *_
             if (boff[f + 1] - boff[f] == 1) { hist[2 * boff[f]] = s_t[0]; hist[2 * boff[f] + 1] = s_t[1]; }
 }
 
-// warp per (node, splittable feature): best split from the node histogram and the node totals
-__global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restrict__ hist,
-                                                        const int32_t *__restrict__ boff,
-                                                        const int32_t *__restrict__ flist, int Fs, int TB, int first,
-                                                        int nn, const int64_t *__restrict__ tot, double lam,
-                                                        double mcw, const uint8_t *__restrict__ dead,
-                                                        double *__restrict__ best_gain, int32_t *__restrict__ best_s)
-{
-    const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (gw >= nn * Fs) return;
-    const int q = gw / Fs, k = gw - q * Fs;
-    const int nd = first + q, f = flist[k];
-    if (dead[nd]) {
-        if (lane == 0) best_s[(int64_t)q * Fs + k] = 0;
-        return;
-    }
-    const SplitBest best = scan_splits(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f], tot[2 * nd],
-                                       tot[2 * nd + 1], lam, mcw, f, lane);
-    if (lane == 0) {
-        best_gain[(int64_t)q * Fs + k] = best.gain;
-        best_s[(int64_t)q * Fs + k] = best.f < 0 ? 0 : best.s;
-    }
-}
-
-// warp per node: the winner over features, the tree node, and the children's totals
-__global__ void __launch_bounds__(256) sub_decide_kernel(const double *__restrict__ best_gain,
+// one warp, node q of the level: the winner over features, the tree node, the children's totals
+// (run by the last block of sub_split_kernel; the per-feature bests come from other blocks: L2 loads)
+__device__ __forceinline__ void sub_decide_node(int q, const double *__restrict__ best_gain,
                                                          const int32_t *__restrict__ best_s,
                                                          const int32_t *__restrict__ flist, int Fs, int first, int nn,
                                                          const float *__restrict__ cuts, int B,
@@ -1040,8 +1016,6 @@ __global__ void __launch_bounds__(256) sub_decide_kernel(const double *__restric
     tree_feat += (int64_t)*d_tree * n_int;   // this tree's nodes
     tree_thr += (int64_t)*d_tree * n_int;
     const int lane = threadIdx.x & 31;
-    const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (q >= nn) return;
     const int nd = first + q;
     SplitBest best{0.0, -1, 0};
     if (!dead[nd]) {
@@ -1053,8 +1027,8 @@ __global__ void __launch_bounds__(256) sub_decide_kernel(const double *__restric
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int k = k0 + 32 * u + lane;
-                sv[u] = k < Fs ? bsq[k] : 0;
-                gv[u] = k < Fs ? bgq[k] : 0.0;
+                sv[u] = k < Fs ? __ldcg(bsq + k) : 0;
+                gv[u] = k < Fs ? __ldcg(bgq + k) : 0.0;
                 fv[u] = k < Fs ? flist[k] : 0;
             }
 #pragma unroll
@@ -1097,45 +1071,53 @@ __global__ void __launch_bounds__(256) sub_decide_kernel(const double *__restric
     }
 }
 
-// samples of level-d nodes move to their children: node ids, and positions in the parent's segment
-// (left from the front, right from the back); cursor[2 q + right] counts them
-__global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restrict__ bins, int64_t n,
-                                                          const int32_t *__restrict__ split_f,
-                                                          const int32_t *__restrict__ split_s, int first, int nn,
-                                                          const int32_t *__restrict__ seg_start,
-                                                          const int32_t *__restrict__ seg_cnt,
-                                                          int32_t *__restrict__ cursor, int32_t *__restrict__ node,
-                                                          int32_t *__restrict__ perm)
+// warp per (node, splittable feature): best split from the node histogram and the node totals; the
+// last block to finish (release-add on `done`) then decides every node of the level
+__global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restrict__ hist,
+                                                        const int32_t *__restrict__ boff,
+                                                        const int32_t *__restrict__ flist, int Fs, int TB, int first,
+                                                        int nn, int64_t *__restrict__ tot, double lam,
+                                                        double mcw, uint8_t *__restrict__ dead,
+                                                        double *__restrict__ best_gain, int32_t *__restrict__ best_s,
+                                                        const float *__restrict__ cuts, int B,
+                                                        int32_t *__restrict__ split_f, int32_t *__restrict__ split_s,
+                                                        uint16_t *__restrict__ tree_feat, float *__restrict__ tree_thr,
+                                                        int n_int, const int32_t *__restrict__ d_tree,
+                                                        unsigned *__restrict__ done)
 {
-    __shared__ int sc[256], sbase[256];
-    const int tid = threadIdx.x;
-    for (int q = tid; q < 2 * nn; q += blockDim.x) sc[q] = 0;
-    __syncthreads();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
-    const bool ok = i < n;
-    int nd = 0, slot = 0, r = 0, right = 0;
-    if (ok) {
-        nd = node[i];
-        const int sf = split_f[nd];
-        right = (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= split_s[nd]) ? 1 : 0;
-        slot = (nd - first) * 2 + right;
-        r = atomicAdd(&sc[slot], 1);
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (gw < nn * Fs) {
+        const int q = gw / Fs, k = gw - q * Fs;
+        const int nd = first + q, f = flist[k];
+        if (dead[nd]) {
+            if (lane == 0) best_s[(int64_t)q * Fs + k] = 0;
+        } else {
+            const SplitBest best = scan_splits(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f],
+                                               tot[2 * nd], tot[2 * nd + 1], lam, mcw, f, lane);
+            if (lane == 0) {
+                best_gain[(int64_t)q * Fs + k] = best.gain;
+                best_s[(int64_t)q * Fs + k] = best.f < 0 ? 0 : best.s;
+            }
+        }
     }
+    __shared__ int s_last;
+    __threadfence();
     __syncthreads();
-    for (int q = tid; q < 2 * nn; q += blockDim.x)
-        if (sc[q]) sbase[q] = atomicAdd(&cursor[q], sc[q]);
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
     __syncthreads();
-    if (ok) {
-        node[i] = 2 * nd + 1 + right;
-        const int o = sbase[slot] + r;
-        perm[right ? seg_start[nd] + seg_cnt[nd] - 1 - o : seg_start[nd] + o] = (int32_t)i;
-    }
+    if (!s_last) return;
+    __threadfence();
+    for (int q = threadIdx.x >> 5; q < nn; q += blockDim.x >> 5)
+        sub_decide_node(q, best_gain, best_s, flist, Fs, first, nn, cuts, B, hist, boff, TB, dead, split_f, split_s,
+                        tree_feat, tree_thr, tot, n_int, d_tree);
+    if (threadIdx.x == 0) *done = 0u;   // for the next level
 }
 
 // one block: children's segments, the smaller child of every split node as histogram items (chunks
 // of <= ch positions), and the (parent, smaller, larger) slot triples for the subtraction
-__global__ void sub_worklist_kernel(int first, int nn, const int32_t *__restrict__ split_f,
-                                    const int32_t *__restrict__ cursor, int32_t *__restrict__ seg_start,
+__device__ __forceinline__ void sub_worklist(int first, int nn, const int32_t *__restrict__ split_f,
+                                             int32_t *__restrict__ cursor, int32_t *__restrict__ seg_start,
                                     int32_t *__restrict__ seg_cnt, int target, int4 *__restrict__ items,
                                     int32_t *__restrict__ n_items, int4 *__restrict__ subs, int32_t *__restrict__ n_subs)
 {
@@ -1145,7 +1127,9 @@ __global__ void sub_worklist_kernel(int first, int nn, const int32_t *__restrict
     int small = 0, st = 0, cs = 0, alive = 0;
     if (q < nn) {
         const int nd = first + q;
-        const int L = cursor[2 * q], Rc = cursor[2 * q + 1], s0 = seg_start[nd];
+        const int L = __ldcg(cursor + 2 * q), Rc = __ldcg(cursor + 2 * q + 1), s0 = seg_start[nd];
+        cursor[2 * q] = 0;   // for the next level's scatter
+        cursor[2 * q + 1] = 0;
         seg_start[2 * nd + 1] = s0;
         seg_cnt[2 * nd + 1] = L;
         seg_start[2 * nd + 2] = s0 + L;
@@ -1182,6 +1166,54 @@ __global__ void sub_worklist_kernel(int first, int nn, const int32_t *__restrict
     }
 }
 
+// samples of level-d nodes move to their children: node ids, and positions in the parent's segment
+// (left from the front, right from the back); cursor[2 q + right] counts them; the last block to
+// finish builds the next level's work list
+__global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restrict__ bins, int64_t n,
+                                                          const int32_t *__restrict__ split_f,
+                                                          const int32_t *__restrict__ split_s, int first, int nn,
+                                                          int32_t *__restrict__ seg_start,
+                                                          int32_t *__restrict__ seg_cnt,
+                                                          int32_t *__restrict__ cursor, int32_t *__restrict__ node,
+                                                          int32_t *__restrict__ perm, int target, int4 *__restrict__ items,
+                                                          int32_t *__restrict__ n_items, int4 *__restrict__ subs,
+                                                          int32_t *__restrict__ n_subs, unsigned *__restrict__ done)
+{
+    __shared__ int sc[256], sbase[256];
+    const int tid = threadIdx.x;
+    for (int q = tid; q < 2 * nn; q += blockDim.x) sc[q] = 0;
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
+    const bool ok = i < n;
+    int nd = 0, slot = 0, r = 0, right = 0;
+    if (ok) {
+        nd = node[i];
+        const int sf = split_f[nd];
+        right = (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= split_s[nd]) ? 1 : 0;
+        slot = (nd - first) * 2 + right;
+        r = atomicAdd(&sc[slot], 1);
+    }
+    __syncthreads();
+    for (int q = tid; q < 2 * nn; q += blockDim.x)
+        if (sc[q]) sbase[q] = atomicAdd(&cursor[q], sc[q]);
+    __syncthreads();
+    if (ok) {
+        node[i] = 2 * nd + 1 + right;
+        const int o = sbase[slot] + r;
+        perm[right ? seg_start[nd] + seg_cnt[nd] - 1 - o : seg_start[nd] + o] = (int32_t)i;
+    }
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    sub_worklist(first, nn, split_f, cursor, seg_start, seg_cnt, target, items, n_items, subs,
+                 n_subs);
+    if (tid == 0) *done = 0u;
+}
+
 // larger child = parent - smaller child, every cell (exact int64)
 __global__ void sub_subtract_kernel(const int64_t *__restrict__ parent, int64_t *__restrict__ child, int TB,
                                     const int4 *__restrict__ subs, const int32_t *__restrict__ n_subs)
@@ -1194,7 +1226,7 @@ __global__ void sub_subtract_kernel(const int64_t *__restrict__ parent, int64_t 
 }
 
 // last level: every sample's leaf, prediction update in tree order
-__global__ void sub_final_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ node,
+__global__ void sub_final_kernel(const uint8_t *__restrict__ bins, int64_t n, int32_t *__restrict__ node,
                                  const int32_t *__restrict__ split_f, const int32_t *__restrict__ split_s, int n_int,
                                  const float *__restrict__ leaf, float *__restrict__ pred, const int32_t *__restrict__ d_tree)
 {
@@ -1202,6 +1234,7 @@ __global__ void sub_final_kernel(const uint8_t *__restrict__ bins, int64_t n, co
     if (i >= n) return;
     leaf += (int64_t)*d_tree * (n_int + 1);
     const int nd = node[i];
+    node[i] = 0;   // every sample starts the next tree at the root
     const int sf = split_f[nd];
     const int child = (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= split_s[nd]) ? 2 * nd + 2 : 2 * nd + 1;
     pred[i] = __fadd_rn(pred[i], leaf[child - n_int]);
@@ -1209,9 +1242,11 @@ __global__ void sub_final_kernel(const uint8_t *__restrict__ bins, int64_t n, co
 
 // leaves of this tree from the level-D node totals: w = -eta G / (H + lambda)
 __global__ void sub_leaf_kernel(const int64_t *__restrict__ sums, int n_leaf, double eta, double lam,
-                                float *__restrict__ leaf, const int32_t *__restrict__ d_tree)
+                                float *__restrict__ leaf, const int32_t *__restrict__ d_tree,
+                                uint8_t *__restrict__ dead, int n_dead)
 {
     const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int q = l; q < n_dead; q += gridDim.x * blockDim.x) dead[q] = 0;   // for the next tree
     if (l >= n_leaf) return;
     const double G = (double)sums[2 * l] * FX, H = (double)sums[2 * l + 1] * FX;
     leaf[(int64_t)*d_tree * n_leaf + l] = (float)(-(eta * (G / (H + lam))));
@@ -2295,7 +2330,13 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             int4 *root_items = ws.get<int4>(max_items);
             int32_t *root_n = ws.get<int32_t>(4);
             if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+            unsigned *done = ws.get<unsigned>(2);   // last-block counters of split and scatter
+            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
             AT_CUDA_TRY(cudaMemsetAsync(d_tree, 0, sizeof(int32_t), s));
+            AT_CUDA_TRY(cudaMemsetAsync(done, 0, 2 * sizeof(unsigned), s));
+            AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * max_nn, s));
+            AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
+            AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
             sub_root_items_kernel<<<1, 256, 0, s>>>((int)n, target, root_items, root_n);
             note_launch();
             auto enqueue_sub = [&](cudaStream_t s) -> int {
@@ -2314,9 +2355,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                     }
                     AT_LAUNCH_CHECK("fit gradients");
                 }
-                AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
-                AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
-                int64_t *hp = hA, *hc = hB;
+                int64_t *hp = hA, *hc = hB;   // node[] and dead[] were zeroed by the previous tree (or below)
                 {
                     ProfScope ps(AT_K_FIT_HIST, s);
                     AT_CUDA_TRY(cudaMemsetAsync(hp, 0, sizeof(int64_t) * 2 * (size_t)TB, s));
@@ -2337,24 +2376,18 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                     const int first = (1 << d) - 1, nn = 1 << d;
                     {
                         ProfScope ps(AT_K_FIT_SPLIT, s);
-                        sub_split_kernel<<<nblk((int64_t)nn * Fs, 8), 256, 0, s>>>(hp, boff, flist, Fs, TB, first, nn, tot,
-                                                                                  lam, mcw, dead, bg, bs);
-                        note_launch();
-                        sub_decide_kernel<<<nblk(nn, 8), 256, 0, s>>>(bg, bs, flist, Fs, first, nn, cuts, B, hp, boff, TB,
-                                                                      dead, split_f, split_s, t_feat, t_thr, tot, n_int,
-                                                                      d_tree);
+                        sub_split_kernel<<<nblk((int64_t)nn * Fs, 8), 256, 0, s>>>(
+                            hp, boff, flist, Fs, TB, first, nn, tot, lam, mcw, dead, bg, bs, cuts, B, split_f, split_s,
+                            t_feat, t_thr, n_int, d_tree, done);
                         note_launch();
                         AT_LAUNCH_CHECK("split/decide");
                     }
                     if (d == D - 1) break;
                     {
                         ProfScope ps(AT_K_FIT_SPLIT, s);
-                        AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * nn, s));
                         sub_scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, first, nn, seg_start,
-                                                                        seg_cnt, cursor, node, perm);
-                        note_launch();
-                        sub_worklist_kernel<<<1, 128, 0, s>>>(first, nn, split_f, cursor, seg_start, seg_cnt, target, items,
-                                                              cnts, subs, cnts + 1);
+                                                                        seg_cnt, cursor, node, perm, target, items, cnts,
+                                                                        subs, cnts + 1, done + 1);
                         note_launch();
                         AT_LAUNCH_CHECK("scatter");
                     }
@@ -2374,7 +2407,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                 {
                     ProfScope ps(AT_K_FIT_UPDATE, s);
                     sub_leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(tot + 2 * (size_t)n_int, n_leaf, eta, lam, t_leaf,
-                                                                      d_tree);
+                                                                      d_tree, dead, n_int + n_leaf);
                     note_launch();
                     sub_final_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, node, split_f, split_s, n_int, t_leaf, pred,
                                                                   d_tree);
