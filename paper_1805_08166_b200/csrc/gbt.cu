@@ -360,7 +360,6 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
                           const AcqArgs *acq, void *stream)
 {
     cudaStream_t s = (cudaStream_t)stream;
-    g->last = s;
     const int KM = acq ? 8 : 1;
     const int F = g->n_features;
     const int n_box = (F + 255) / 256, box_rows = (F + n_box - 1) / n_box, tile_rows = n_box * box_rows;
@@ -374,11 +373,14 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
     // rank form: deep ensembles that stream (4 candidate groups per tile, 16-tree chunks)
     const char *rk_e = getenv("AT_PREDICT_RANK");   // "0" forces the fp32 walk
     const bool want_rk = !acq && g->depth >= 7 && (!rk_e || atoi(rk_e) != 0) && n > 0;
+    // the rank tables are built (once) from the model as its last writer left it, then this stream owns it
+    const int rk_ok = want_rk ? build_rank_form(g) : 0;
+    g->last = s;
     // AT_RK_GRP: candidate groups per tile (2: 32-tree chunks, default; 4: 16-tree chunks -- the same
     // walks in flight per warp, half the tiles: equal at 10^7+ candidates, worse balanced below)
     const char *rg_e = getenv("AT_RK_GRP");
     const int RGRP = rg_e && atoi(rg_e) == 4 ? 4 : 2;
-    if (want_rk && build_rank_form(g) == 1) {
+    if (want_rk && rk_ok == 1) {
         const int P = (F + 1) / 2;   // u32 rank pairs per candidate
         const int pn_box = (P + 255) / 256, pbox_rows = (P + pn_box - 1) / pn_box, ptile_rows = pn_box * pbox_rows;
         TreeGeo G = make_geo(g, (RGRP == 2 ? 32 : 16) * ((uint32_t)((1 << g->depth) - 1) * 4u + (uint32_t)(1 << g->depth) * 4u),

@@ -168,6 +168,31 @@ def test_predict_rank_form_edge_values(at, T, D):
     assert_bits_equal(outs[0][0][fin], es, "scores vs oracle")
 
 
+def test_predict_rank_form_of_a_fitted_model(at):
+    """A device-only handle (gbt_fit_hist output, depth 8) gets its rank tables built lazily on the
+    first deep predict; scores and slots equal the fp32 walk's and the oracle's."""
+    n = 2500
+    osp, idx, X, c, key = fit_inputs(n, synth.ALL_RESNET[:3], seed=41)
+    sp = at.Space(synth.ALL_RESNET[:3])
+    Xg = sp.features(u64(idx))
+    gm = at.gbt_fit_hist(Xg, n, dev(c), dev(key.view(np.int16)), n_trees=120, depth=8)
+    ex = gm.export()
+    cand = synth.uniform_indices(osp.size(), 3000, seed=42)
+    Xc = sp.features(u64(cand))
+    outs = []
+    for env in ("1", "0"):
+        os.environ["AT_PREDICT_RANK"] = env
+        try:
+            s, sl = gm.predict(Xc, n=3000, slots=True)
+            outs.append((s.cpu().numpy(), sl.cpu().numpy()))
+        finally:
+            os.environ.pop("AT_PREDICT_RANK", None)
+    assert_bits_equal(outs[0][1], outs[1][1], "leaf slots")
+    assert_bits_equal(outs[0][0], outs[1][0], "scores")
+    es = O.OracleGbt(ex["feat"], ex["thresh"], ex["leaf"]).predict(osp.features(cand))
+    assert_bits_equal(outs[0][0], es, "scores vs oracle")
+
+
 def test_scores_config1_exhaustive_top8(at):
     """Config 1 pin: exhaustive scoring of all 151,250 configs; GPU top-8 == oracle top-8."""
     ens = synth.ensemble(100, 6, seed=1805)
