@@ -557,6 +557,18 @@ def test_fit_subtraction_many_feature_ranges(at):
     _check_paths(_fit_paths(at, Xg, n, c, key, paths=("subtraction", "level-by-level"), n_trees=2, depth=6), ref)
 
 
+def test_fit_subtraction_large_gradients(at):
+    """Regression on costs of order 10^4: |g| = 2 |f - c| 2^32 reaches 2^46, so the 64-bit histogram sums
+    need their carries (low word -> high word) at every level."""
+    n = 3000
+    osp, idx, X, c, key = fit_inputs(n, [synth.CFG2A, synth.CFG2B], seed=77)
+    c = (c / c.max() * 2.0e4 + 3000.0).astype(np.float32)
+    ref = O.fit_hist(X, c, key, n_trees=3, depth=5, objective="reg")
+    Xg = at.Space([synth.CFG2A, synth.CFG2B]).features(u64(idx))
+    _check_paths(_fit_paths(at, Xg, n, c, key, paths=("subtraction", "level-by-level"), n_trees=3, depth=5,
+                            objective="reg"), ref)
+
+
 # ------------------------------------------------------------------ §8(f): regression objective, transfer (Eq. 4)
 @pytest.mark.parametrize("n,wls,trees,depth,margin", [(1024, [synth.CFG2A], 4, 6, False),
                                                       (333, synth.ALL_DW[:5], 3, 4, True),
