@@ -330,28 +330,70 @@ static int build_rank_form(at_gbt g)
 }
 
 // Xr[p][i] = rank(X[2p][i]) | rank(X[2p + 1][i]) << 16, rank = #{theta <= x} among the feature's
-// sorted distinct thresholds (binary search; NaN ranks 0xFFFF)
-__device__ __forceinline__ uint32_t rank_of(float x, const int32_t *__restrict__ off, const float *__restrict__ val, int f)
+// sorted distinct thresholds (NaN ranks 0xFFFF).  Block = one feature pair x RE_CAND candidates: the
+// pair's two tables are staged in shared memory (when they fit) and every thread runs branch-free
+// binary searches (a fixed number of halvings per table) for 8 candidates at once.
+constexpr int RE_NT = 256, RE_PER = 8, RE_CAND = RE_NT * RE_PER, RE_SMEM = 8192;
+
+// global-table fallback (a feature with more thresholds than the staging buffer holds)
+__device__ __forceinline__ uint32_t rank_search_g(const float *__restrict__ tab, int len, float x)
 {
-    const int b = __ldg(off + f), e = __ldg(off + f + 1);
-    int lo = b, hi = e;   // first theta > x
+    int lo = 0, hi = len;   // first theta > x
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (__ldg(val + mid) <= x) lo = mid + 1; else hi = mid;
+        if (__ldg(tab + mid) <= x) lo = mid + 1; else hi = mid;
     }
-    return x != x ? 0xFFFFu : (uint32_t)(lo - b);
+    return x != x ? 0xFFFFu : (uint32_t)lo;
 }
 
-__global__ void rank_encode_kernel(const float *__restrict__ X, int64_t n, int64_t ld, int F,
-                                   const int32_t *__restrict__ off, const float *__restrict__ val,
-                                   uint32_t *__restrict__ Xr, int64_t ldr)
+// staged table padded with +inf to P - 1 entries (P a power of two > len): log2 P branch-free halvings
+__device__ __forceinline__ uint32_t rank_search_s(const float *tab, int len, int P, float x)
 {
+    int lo = 0;
+    for (int step = P >> 1; step > 0; step >>= 1) lo += tab[lo + step - 1] <= x ? step : 0;
+    return x != x ? 0xFFFFu : (uint32_t)min(lo, len);   // x = +inf also passes the padding
+}
+
+__global__ void __launch_bounds__(RE_NT) rank_encode_kernel(const float *__restrict__ X, int64_t n, int64_t ld, int F,
+                                                            const int32_t *__restrict__ off,
+                                                            const float *__restrict__ val, uint32_t *__restrict__ Xr,
+                                                            int64_t ldr)
+{
+    __shared__ float st[RE_SMEM];
     const int p = blockIdx.y;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t r0 = rank_of(X[(int64_t)(2 * p) * ld + i], off, val, 2 * p);
-    const uint32_t r1 = 2 * p + 1 < F ? rank_of(X[(int64_t)(2 * p + 1) * ld + i], off, val, 2 * p + 1) : 0u;
-    Xr[(int64_t)p * ldr + i] = r0 | (r1 << 16);
+    const int f0 = 2 * p, f1 = 2 * p + 1 < F ? 2 * p + 1 : -1;
+    const int b0 = off[f0], l0 = off[f0 + 1] - b0;
+    const int b1 = f1 >= 0 ? off[f1] : 0, l1 = f1 >= 0 ? off[f1 + 1] - b1 : 0;
+    int P0 = 1, P1 = 1;
+    while (P0 <= l0) P0 *= 2;
+    while (P1 <= l1) P1 *= 2;
+    const bool staged = P0 + P1 <= RE_SMEM;   // block-uniform
+    if (staged) {
+        for (int q = threadIdx.x; q < P0; q += RE_NT) st[q] = q < l0 ? val[b0 + q] : __int_as_float(0x7f800000);
+        for (int q = threadIdx.x; q < P1; q += RE_NT) st[P0 + q] = q < l1 ? val[b1 + q] : __int_as_float(0x7f800000);
+    }
+    __syncthreads();
+    const int64_t i0 = (int64_t)blockIdx.x * RE_CAND + threadIdx.x;
+    float x0[RE_PER], x1[RE_PER];
+#pragma unroll
+    for (int k = 0; k < RE_PER; ++k) {
+        const int64_t i = i0 + (int64_t)k * RE_NT;
+        x0[k] = i < n ? X[(int64_t)f0 * ld + i] : 0.0f;
+        x1[k] = (i < n && f1 >= 0) ? X[(int64_t)f1 * ld + i] : 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < RE_PER; ++k) {
+        const int64_t i = i0 + (int64_t)k * RE_NT;
+        uint32_t r0, r1;
+        if (staged) {
+            r0 = rank_search_s(st, l0, P0, x0[k]);
+            r1 = f1 >= 0 ? rank_search_s(st + P0, l1, P1, x1[k]) : 0u;
+        } else {
+            r0 = rank_search_g(val + b0, l0, x0[k]);
+            r1 = f1 >= 0 ? rank_search_g(val + b1, l1, x1[k]) : 0u;
+        }
+        if (i < n) Xr[(int64_t)p * ldr + i] = r0 | (r1 << 16);
+    }
 }
 
 // gbt_predict / gbt_predict_acq: one persistent scorer launch (KM = 1: one model; KM = 8: up to 8
@@ -405,8 +447,8 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
             AT_CUDA_TRY(cudaMallocAsync((void **)&Xr, (size_t)P * ldr * 4, s));
             {
                 ProfScope ps(AT_K_FEATURES, s);
-                rank_encode_kernel<<<dim3((unsigned)((n + 255) / 256), P), 256, 0, s>>>(d_feat, n, ld, F, g->d_thr_off,
-                                                                                       g->d_thr_val, Xr, ldr);
+                rank_encode_kernel<<<dim3((unsigned)((n + RE_CAND - 1) / RE_CAND), P), RE_NT, 0, s>>>(
+                    d_feat, n, ld, F, g->d_thr_off, g->d_thr_val, Xr, ldr);
                 note_launch();
                 AT_LAUNCH_CHECK("rank_encode_kernel");
             }
