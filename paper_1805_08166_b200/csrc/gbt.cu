@@ -333,7 +333,7 @@ static int build_rank_form(at_gbt g)
 // sorted distinct thresholds (NaN ranks 0xFFFF).  Block = one feature pair x RE_CAND candidates: the
 // pair's two tables are staged in shared memory (when they fit) and every thread runs branch-free
 // binary searches (a fixed number of halvings per table) for 8 candidates at once.
-constexpr int RE_NT = 256, RE_PER = 8, RE_CAND = RE_NT * RE_PER, RE_SMEM = 8192;
+constexpr int RE_NT = 256, RE_PER = 8, RE_CAND = RE_NT * RE_PER, RE_SMEM = 512;
 
 // global-table fallback (a feature with more thresholds than the staging buffer holds)
 __device__ __forceinline__ uint32_t rank_search_g(const float *__restrict__ tab, int len, float x)
@@ -346,11 +346,14 @@ __device__ __forceinline__ uint32_t rank_search_g(const float *__restrict__ tab,
     return x != x ? 0xFFFFu : (uint32_t)lo;
 }
 
-// staged table padded with +inf to P - 1 entries (P a power of two > len): log2 P branch-free halvings
+// staged table padded with +inf to P - 1 entries (P a power of two > len, P <= 256): log2 P branch-free
+// halvings, unrolled (the guards are block-uniform)
 __device__ __forceinline__ uint32_t rank_search_s(const float *tab, int len, int P, float x)
 {
     int lo = 0;
-    for (int step = P >> 1; step > 0; step >>= 1) lo += tab[lo + step - 1] <= x ? step : 0;
+#pragma unroll
+    for (int step = 128; step > 0; step >>= 1)
+        if (step < P) lo += tab[lo + step - 1] <= x ? step : 0;
     return x != x ? 0xFFFFu : (uint32_t)min(lo, len);   // x = +inf also passes the padding
 }
 
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(RE_NT) rank_encode_kernel(const float *__restr
     int P0 = 1, P1 = 1;
     while (P0 <= l0) P0 *= 2;
     while (P1 <= l1) P1 *= 2;
-    const bool staged = P0 + P1 <= RE_SMEM;   // block-uniform
+    const bool staged = P0 <= 256 && P1 <= 256;   // block-uniform (fitted models: <= 255 cuts per feature)
     if (staged) {
         for (int q = threadIdx.x; q < P0; q += RE_NT) st[q] = q < l0 ? val[b0 + q] : __int_as_float(0x7f800000);
         for (int q = threadIdx.x; q < P1; q += RE_NT) st[P0 + q] = q < l1 ? val[b1 + q] : __int_as_float(0x7f800000);
