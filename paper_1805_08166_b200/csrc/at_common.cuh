@@ -31,6 +31,7 @@ int cuda_fail(cudaError_t e, const char *where);
 void prof_begin(int cls, cudaStream_t s);
 void prof_end(int cls, cudaStream_t s);
 void note_launch();            // one library kernel launched (at_launch_count)
+void pool_keep();              // keep freed stream-ordered scratch in the default pool (once per device)
 void prof_suspend(bool on);   // while capturing a graph: count launches, record no events
 
 struct ProfScope {

@@ -2042,6 +2042,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     if (hb < 0 || he < hb || he > n) return fail(AT_EINVAL, "gbt_fit_hist: bad histogram slice");
     if (!o->allreduce && (hb != 0 || he != n)) return fail(AT_EINVAL, "gbt_fit_hist: a slice needs an allreduce");
     cudaStream_t s = (cudaStream_t)stream;
+    pool_keep();   // the workspace below is stream-ordered scratch
     const int D = o->depth, B = o->max_bins, GS = o->group_size;
     const int n_int = (1 << D) - 1, n_leaf = 1 << D;
     const double lam = (double)o->lambda, mcw = (double)o->min_child_weight, eta = (double)o->eta;

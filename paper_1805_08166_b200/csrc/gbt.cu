@@ -438,13 +438,8 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
             if (smem > rk_attr[RGRP == 2]) {
                 AT_CUDA_TRY(cudaFuncSetAttribute(rk_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 rk_attr[RGRP == 2] = smem;
-                // freed stream-ordered scratch (the rank tiles below) stays in the pool between calls
-                cudaMemPool_t pool;
-                int dev = 0;
-                uint64_t keep = ~0ull;
-                if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
-                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
             }
+            pool_keep();   // the rank tiles below are stream-ordered scratch
             const int64_t ldr = (n + 3) / 4 * 4;   // 16-B rows for the tensor map
             uint32_t *Xr = nullptr;
             AT_CUDA_TRY(cudaMallocAsync((void **)&Xr, (size_t)P * ldr * 4, s));

@@ -29,6 +29,22 @@ static thread_local bool g_suspend = false;
 
 void prof_suspend(bool on) { g_suspend = on; }
 void note_launch() { g_launches.fetch_add(1); }
+
+// Stream-ordered scratch (cudaMallocAsync / cudaFreeAsync: fit workspaces, rank tiles, model tables)
+// stays in the device's default pool between calls instead of going back to the driver at every
+// synchronisation (release threshold 0 by default), so a call inside a tuning loop does not pay
+// for re-mapping its workspace.  Once per device.
+void pool_keep()
+{
+    static int done_dev[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done_dev[dev]) return;
+    cudaMemPool_t pool;
+    uint64_t keep = ~0ull;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    done_dev[dev] = 1;
+}
 static std::atomic<int> g_prof_on{0};
 static std::mutex g_prof_mu;
 struct EvPair { cudaEvent_t a, b; };
