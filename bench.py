@@ -366,15 +366,43 @@ def oracle_step(n_chains, r, state):
 def cpu_baseline(sample_chains=256):
     """The oracle as it stands, one thread, on a bounded sample of the step: SA over `sample_chains`
     chains x 500 steps + top-k, then the full select + refit; the SA part is extrapolated linearly to
-    4096 chains (chains are independent) to express a full-step rate in the metric's unit."""
+    4096 chains (chains are independent) to express a full-step rate in the metric's unit.  Beside it
+    (SURVEY 8(d)): the same oracle with its SA chains split over every host core (one thread per
+    chain slice, the ctypes calls release the GIL), select + refit still single-threaded."""
     st = {}
     t_sa, t_rest = oracle_step(sample_chains, 0, st)
     est = t_sa * CHAINS / sample_chains + t_rest
-    return {"value": round(CHAINS * (SA_STEPS + 1) / est, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"SA {sample_chains} chains x {SA_STEPS} steps + top-k ({t_sa:.2f} s, extrapolated x"
-                      f"{CHAINS // sample_chains} to 4096 chains) + select + refit 100 trees on |D|=1024 "
-                      f"({t_rest:.2f} s); single-threaded C oracle",
-            "cpu": _cpu_model()}
+    out = {"value": round(CHAINS * (SA_STEPS + 1) / est, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"SA {sample_chains} chains x {SA_STEPS} steps + top-k ({t_sa:.2f} s, extrapolated x"
+                     f"{CHAINS // sample_chains} to 4096 chains) + select + refit 100 trees on |D|=1024 "
+                     f"({t_rest:.2f} s); single-threaded C oracle",
+           "cpu": _cpu_model()}
+    try:
+        out["threads"] = _cpu_baseline_threads(st, t_rest)
+    except Exception as e:   # a host without threads support still reports the 1-thread baseline
+        out["threads"] = {"error": str(e)[:200]}
+    return out
+
+
+def _cpu_baseline_threads(st, t_rest, per_thread=32):
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+    nproc = os.cpu_count() or 1
+    osp, ens, temps = st["osp"], st["ens"], st["temps"]
+    n = nproc * per_thread
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(nproc) as ex:
+        futs = [ex.submit(osp.sa_explore, ens, per_thread, SA_STEPS, SEED, 1, temps, chain_id_base=k * per_thread)
+                for k in range(nproc)]
+        res = [f.result() for f in futs]
+    osp.topk(np.concatenate([r["visited_E"] for r in res]), np.concatenate([r["visited_idx"] for r in res]), K_POOL,
+             measured=st["d_idx"])
+    t_sa = time.perf_counter() - t0
+    est = t_sa * CHAINS / n + t_rest
+    return {"value": round(CHAINS * (SA_STEPS + 1) / est, 1), "unit": UNIT, "cores": nproc,
+            "sample": f"SA {n} chains on {nproc} threads + top-k ({t_sa:.2f} s, extrapolated to 4096 chains) + "
+                      f"single-threaded select + refit ({t_rest:.2f} s)"}
 
 
 def _cpu_model():
