@@ -1072,7 +1072,7 @@ __device__ __forceinline__ void sub_decide_node(int q, const double *__restrict_
 }
 
 // warp per (node, splittable feature): best split from the node histogram and the node totals; the
-// last block to finish (release-add on `done`) then decides every node of the level
+// last warp to finish a node's features (count in done[q]) then decides that node
 __global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restrict__ hist,
                                                         const int32_t *__restrict__ boff,
                                                         const int32_t *__restrict__ flist, int Fs, int TB, int first,
@@ -1087,31 +1087,31 @@ __global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restric
 {
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (gw < nn * Fs) {
-        const int q = gw / Fs, k = gw - q * Fs;
-        const int nd = first + q, f = flist[k];
-        if (dead[nd]) {
-            if (lane == 0) best_s[(int64_t)q * Fs + k] = 0;
-        } else {
-            const SplitBest best = scan_splits(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f],
-                                               tot[2 * nd], tot[2 * nd + 1], lam, mcw, f, lane);
-            if (lane == 0) {
-                best_gain[(int64_t)q * Fs + k] = best.gain;
-                best_s[(int64_t)q * Fs + k] = best.f < 0 ? 0 : best.s;
-            }
+    if (gw >= nn * Fs) return;
+    const int q = gw / Fs, k = gw - q * Fs;
+    const int nd = first + q, f = flist[k];
+    if (dead[nd]) {
+        if (lane == 0) best_s[(int64_t)q * Fs + k] = 0;
+    } else {
+        const SplitBest best = scan_splits(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f], tot[2 * nd],
+                                           tot[2 * nd + 1], lam, mcw, f, lane);
+        if (lane == 0) {
+            best_gain[(int64_t)q * Fs + k] = best.gain;
+            best_s[(int64_t)q * Fs + k] = best.f < 0 ? 0 : best.s;
         }
     }
-    __shared__ int s_last;
+    // the last warp to finish a node's features decides that node (done[q] counts them)
+    unsigned last = 0;
+    if (lane == 0) {
+        __threadfence();
+        last = atomicAdd(&done[q], 1u) == (unsigned)(Fs - 1);
+    }
+    last = __shfl_sync(0xFFFFFFFFu, last, 0);
+    if (!last) return;
     __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int q = threadIdx.x >> 5; q < nn; q += blockDim.x >> 5)
-        sub_decide_node(q, best_gain, best_s, flist, Fs, first, nn, cuts, B, hist, boff, TB, dead, split_f, split_s,
-                        tree_feat, tree_thr, tot, n_int, d_tree);
-    if (threadIdx.x == 0) *done = 0u;   // for the next level
+    sub_decide_node(q, best_gain, best_s, flist, Fs, first, nn, cuts, B, hist, boff, TB, dead, split_f, split_s,
+                    tree_feat, tree_thr, tot, n_int, d_tree);
+    if (lane == 0) done[q] = 0u;   // for the next level
 }
 
 // one block: children's segments, the smaller child of every split node as histogram items (chunks
@@ -2331,10 +2331,10 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             int4 *root_items = ws.get<int4>(max_items);
             int32_t *root_n = ws.get<int32_t>(4);
             if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
-            unsigned *done = ws.get<unsigned>(2);   // last-block counters of split and scatter
+            unsigned *done = ws.get<unsigned>(2 + max_nn);   // last-block counter of the scatter, per-node split counters
             if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
             AT_CUDA_TRY(cudaMemsetAsync(d_tree, 0, sizeof(int32_t), s));
-            AT_CUDA_TRY(cudaMemsetAsync(done, 0, 2 * sizeof(unsigned), s));
+            AT_CUDA_TRY(cudaMemsetAsync(done, 0, (2 + max_nn) * sizeof(unsigned), s));
             AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * max_nn, s));
             AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
             AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
@@ -2379,7 +2379,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                         ProfScope ps(AT_K_FIT_SPLIT, s);
                         sub_split_kernel<<<nblk((int64_t)nn * Fs, 8), 256, 0, s>>>(
                             hp, boff, flist, Fs, TB, first, nn, tot, lam, mcw, dead, bg, bs, cuts, B, split_f, split_s,
-                            t_feat, t_thr, n_int, d_tree, done);
+                            t_feat, t_thr, n_int, d_tree, done + 2);
                         note_launch();
                         AT_LAUNCH_CHECK("split/decide");
                     }
