@@ -1071,11 +1071,54 @@ __device__ __forceinline__ void sub_decide_node(int q, const double *__restrict_
     }
 }
 
-// warp per (node, splittable feature): best split from the node histogram and the node totals; the
-// last warp to finish a node's features (count in done[q]) then decides that node
+// Best split over one 32-split chunk c of one feature: the carry (sums of the bins before the chunk)
+// by a warp reduction, then the chunk's exact int64 prefix scan and fp64 gains in the oracle's order
+// (scan_splits restricted to one chunk).
+__device__ __forceinline__ SplitBest scan_chunk(const int64_t *hf, int nb, int c, long long Gi, long long Hi,
+                                                double lam, double mcw, int f, int lane)
+{
+    const int nc = nb - 1;
+    const double G = (double)Gi * FX, H = (double)Hi * FX;
+    const double parent = G * G / (H + lam);
+    SplitBest best{0.0, -1, 0};
+    long long carryG = 0, carryH = 0;
+    for (int b = lane; b < 32 * c; b += 32) { carryG += hf[2 * b]; carryH += hf[2 * b + 1]; }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        carryG += __shfl_xor_sync(0xFFFFFFFFu, carryG, off);
+        carryH += __shfl_xor_sync(0xFFFFFFFFu, carryH, off);
+    }
+    const int b = 32 * c + lane;   // split s = b + 1 puts bins <= b on the left
+    long long vg = b < nc ? hf[2 * b] : 0, vh = b < nc ? hf[2 * b + 1] : 0;
+    const long long own_g = vg, own_h = vh;
+    if (__ballot_sync(0xFFFFFFFFu, vg != 0 || vh != 0) == 0) return best;   // empty chunk: no new split
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long yg = __shfl_up_sync(0xFFFFFFFFu, vg, off);
+        const long long yh = __shfl_up_sync(0xFFFFFFFFu, vh, off);
+        if (lane >= off) { vg += yg; vh += yh; }
+    }
+    const long long GLi = carryG + vg, HLi = carryH + vh;
+    if (b < nc && (own_g != 0 || own_h != 0)) {
+        const double GL = (double)GLi * FX, HL = (double)HLi * FX;
+        const double GR = (double)(Gi - GLi) * FX, HR = (double)(Hi - HLi) * FX;
+        if (!(HL < mcw || HR < mcw)) {
+            const double gain = (GL * GL / (HL + lam) + GR * GR / (HR + lam)) - parent;
+            if (gain > 0.0) {
+                SplitBest cnd{gain, f, b + 1};
+                if (split_better(cnd, best)) best = cnd;
+            }
+        }
+    }
+    return warp_best(best);
+}
+
+// warp per (node, feature, 32-split chunk) entry: best split of the chunk from the node histogram and
+// the node totals; the last warp to finish a node's entries (count in done[q]) decides that node
 __global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restrict__ hist,
                                                         const int32_t *__restrict__ boff,
-                                                        const int32_t *__restrict__ flist, int Fs, int TB, int first,
+                                                        const int32_t *__restrict__ ent_f,
+                                                        const int32_t *__restrict__ ent_c, int NE, int TB, int first,
                                                         int nn, int64_t *__restrict__ tot, double lam,
                                                         double mcw, uint8_t *__restrict__ dead,
                                                         double *__restrict__ best_gain, int32_t *__restrict__ best_s,
@@ -1087,29 +1130,29 @@ __global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restric
 {
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (gw >= nn * Fs) return;
-    const int q = gw / Fs, k = gw - q * Fs;
-    const int nd = first + q, f = flist[k];
+    if (gw >= nn * NE) return;
+    const int q = gw / NE, j = gw - q * NE;
+    const int nd = first + q, f = ent_f[j];
     if (dead[nd]) {
-        if (lane == 0) best_s[(int64_t)q * Fs + k] = 0;
+        if (lane == 0) best_s[(int64_t)q * NE + j] = 0;
     } else {
-        const SplitBest best = scan_splits(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f], tot[2 * nd],
-                                           tot[2 * nd + 1], lam, mcw, f, lane);
+        const SplitBest best = scan_chunk(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f], ent_c[j],
+                                          tot[2 * nd], tot[2 * nd + 1], lam, mcw, f, lane);
         if (lane == 0) {
-            best_gain[(int64_t)q * Fs + k] = best.gain;
-            best_s[(int64_t)q * Fs + k] = best.f < 0 ? 0 : best.s;
+            best_gain[(int64_t)q * NE + j] = best.gain;
+            best_s[(int64_t)q * NE + j] = best.f < 0 ? 0 : best.s;
         }
     }
-    // the last warp to finish a node's features decides that node (done[q] counts them)
     unsigned last = 0;
     if (lane == 0) {
         __threadfence();
-        last = atomicAdd(&done[q], 1u) == (unsigned)(Fs - 1);
+        last = atomicAdd(&done[q], 1u) == (unsigned)(NE - 1);
     }
     last = __shfl_sync(0xFFFFFFFFu, last, 0);
     if (!last) return;
     __threadfence();
-    sub_decide_node(q, best_gain, best_s, flist, Fs, first, nn, cuts, B, hist, boff, TB, dead, split_f, split_s,
+    // entries in feature order, chunks ascending: the (gain desc, f asc, s asc) rule picks as before
+    sub_decide_node(q, best_gain, best_s, ent_f, NE, first, nn, cuts, B, hist, boff, TB, dead, split_f, split_s,
                     tree_feat, tree_thr, tot, n_int, d_tree);
     if (lane == 0) done[q] = 0u;   // for the next level
 }
@@ -2306,8 +2349,20 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             int64_t *tot = ws.get<int64_t>(2 * (size_t)(n_int + n_leaf));
             int64_t *hA = ws.get<int64_t>((size_t)max_nn * TB * 2);
             int64_t *hB = ws.get<int64_t>((size_t)max_nn * TB * 2);
-            double *bg = ws.get<double>((size_t)max_nn * Fs);
-            int32_t *bs = ws.get<int32_t>((size_t)max_nn * Fs);
+            // split entries: (feature, 32-split chunk), features ascending, chunks ascending
+            std::vector<int32_t> ent_h;
+            for (int k = 0; k < Fs; ++k) {
+                const int nchk = std::max(1, (ncuts_h[flist_h[k]] + 31) / 32);
+                for (int c = 0; c < nchk; ++c) ent_h.push_back(flist_h[k]);
+            }
+            const int NE = (int)ent_h.size();
+            for (int k = 0, j = 0; k < Fs; ++k) {
+                const int nchk = std::max(1, (ncuts_h[flist_h[k]] + 31) / 32);
+                for (int c = 0; c < nchk; ++c, ++j) ent_h.push_back(c);
+            }
+            int32_t *d_ent = ws.get<int32_t>(2 * (size_t)NE);   // [feature of entry][chunk of entry]
+            double *bg = ws.get<double>((size_t)max_nn * NE);
+            int32_t *bs = ws.get<int32_t>((size_t)max_nn * NE);
             if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
             std::vector<int32_t> tab(rowbase_h);
             tab.insert(tab.end(), gbase_h.begin(), gbase_h.end());
@@ -2315,6 +2370,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             tab.insert(tab.end(), inv_h.begin(), inv_h.end());
             AT_CUDA_TRY(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
             AT_CUDA_TRY(cudaMemcpyAsync(d_rng, rng.data(), NR * sizeof(SubRange), cudaMemcpyHostToDevice, s));
+            AT_CUDA_TRY(cudaMemcpyAsync(d_ent, ent_h.data(), ent_h.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
             const int32_t *d_rowbase = d_tab, *d_gbase = d_tab + Fs, *d_nbk = d_tab + 2 * Fs, *d_inv = d_tab + 3 * Fs;
             rowbins_kernel<<<dim3(nblk(n, 32), nblk(FsP, 32)), dim3(32, 8), 0, s>>>(bins, n, flist, d_inv, FsP, binsR);
             note_launch();
@@ -2377,9 +2433,9 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                     const int first = (1 << d) - 1, nn = 1 << d;
                     {
                         ProfScope ps(AT_K_FIT_SPLIT, s);
-                        sub_split_kernel<<<nblk((int64_t)nn * Fs, 8), 256, 0, s>>>(
-                            hp, boff, flist, Fs, TB, first, nn, tot, lam, mcw, dead, bg, bs, cuts, B, split_f, split_s,
-                            t_feat, t_thr, n_int, d_tree, done + 2);
+                        sub_split_kernel<<<nblk((int64_t)nn * NE, 8), 256, 0, s>>>(
+                            hp, boff, d_ent, d_ent + NE, NE, TB, first, nn, tot, lam, mcw, dead, bg, bs, cuts, B, split_f,
+                            split_s, t_feat, t_thr, n_int, d_tree, done + 2);
                         note_launch();
                         AT_LAUNCH_CHECK("split/decide");
                     }
