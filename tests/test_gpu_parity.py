@@ -168,6 +168,31 @@ def test_predict_rank_form_edge_values(at, T, D):
     assert_bits_equal(outs[0][0][fin], es, "scores vs oracle")
 
 
+def test_predict_rank_form_odd_feature_count(at):
+    """F = 7 (the last rank pair has one feature), depth 8, 200 streamed trees; rank vs fp32 vs oracle."""
+    rng = np.random.default_rng(5)
+    T, D, F, n = 200, 8, 7, 1500
+    ni, nl = (1 << D) - 1, 1 << D
+    feat = rng.integers(0, F, size=(T, ni)).astype(np.uint16)
+    thr = rng.integers(0, 50, size=(T, ni)).astype(np.float32)
+    leaf = ((rng.random((T, nl)) - 0.5) * 0.2).astype(np.float32)
+    X = rng.integers(0, 50, size=(F, n)).astype(np.float32)
+    g = at.Gbt(feat, thr, leaf, n_features=F)
+    Xg = dev(np.ascontiguousarray(X))
+    outs = []
+    for env in ("1", "0"):
+        os.environ["AT_PREDICT_RANK"] = env
+        try:
+            s, sl = g.predict(Xg, n=n, slots=True)
+            outs.append((s.cpu().numpy(), sl.cpu().numpy()))
+        finally:
+            os.environ.pop("AT_PREDICT_RANK", None)
+    assert_bits_equal(outs[0][1], outs[1][1], "leaf slots")
+    assert_bits_equal(outs[0][0], outs[1][0], "scores")
+    es = O.OracleGbt(feat, thr, leaf).predict(np.ascontiguousarray(X.T))
+    assert_bits_equal(outs[0][0], es, "scores vs oracle")
+
+
 def test_predict_rank_form_of_a_fitted_model(at):
     """A device-only handle (gbt_fit_hist output, depth 8) gets its rank tables built lazily on the
     first deep predict; scores and slots equal the fp32 walk's and the oracle's."""
