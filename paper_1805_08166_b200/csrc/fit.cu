@@ -921,11 +921,20 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
 #pragma unroll
                 for (int u = 0; u < SUB_NQW; ++u) {
                     if (u >= nqw) break;
+                    // the 8 low-word atomics of the 4 slots first (their returns in flight together), then
+                    // the 8 high words with their carries
+                    int c[4];
+                    uint32_t og[4], oh[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const int c = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
-                        sub_add64(glo, ghi, c, gl, gh);
-                        sub_add64(hlo, hhi, c, hl, hh);
+                        c[j] = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
+                        og[j] = atomicAdd(&glo[c[j]], gl);
+                        oh[j] = atomicAdd(&hlo[c[j]], hl);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        atomicAdd(&ghi[c[j]], gh + ((og[j] + gl < og[j]) ? 1u : 0u));   // exact modular 64-bit sums
+                        atomicAdd(&hhi[c[j]], hh + ((oh[j] + hl < oh[j]) ? 1u : 0u));
                     }
                 }
             }
