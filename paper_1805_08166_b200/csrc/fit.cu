@@ -32,10 +32,12 @@ __global__ void __launch_bounds__(1024) sort_feature_kernel(const float *__restr
     __shared__ uint32_t wcount[32][257];
     __shared__ uint32_t base[256];
     __shared__ uint32_t tile_total[256];
+    __shared__ int s_skip;
     const int f = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t *src = bufA + (int64_t)f * n, *dst = bufB + (int64_t)f * n;
     for (int64_t i = tid; i < n; i += 1024) src[i] = fkey(X[(int64_t)f * ld + i]);
+    if (tid == 0) s_skip = 0;
     __syncthreads();
     for (int pass = 0; pass < 4; ++pass) {
         const int sh = 8 * pass;
@@ -43,6 +45,16 @@ __global__ void __launch_bounds__(1024) sort_feature_kernel(const float *__restr
         __syncthreads();
         for (int64_t i = tid; i < n; i += 1024) atomicAdd(&base[(src[i] >> sh) & 255u], 1u);
         __syncthreads();
+        // a digit shared by every key (small integers have all-zero low mantissa bytes): the pass
+        // would be the identity permutation, skip it
+        if (tid < 256 && base[tid] == (uint32_t)n) s_skip = 1;
+        __syncthreads();
+        if (s_skip) {
+            __syncthreads();
+            if (tid == 0) s_skip = 0;
+            __syncthreads();
+            continue;
+        }
         if (tid == 0) {
             uint32_t run = 0;
             for (int d = 0; d < 256; ++d) { const uint32_t c = base[d]; base[d] = run; run += c; }
@@ -73,6 +85,9 @@ __global__ void __launch_bounds__(1024) sort_feature_kernel(const float *__restr
         uint32_t *t = src; src = dst; dst = t;
         __syncthreads();
     }
+    // an odd number of performed passes leaves the sorted keys in bufB: the caller reads bufA
+    if (src != bufA + (int64_t)f * n)
+        for (int64_t i = tid; i < n; i += 1024) bufA[(int64_t)f * n + i] = src[i];
 }
 
 __global__ void __launch_bounds__(1024) cuts_kernel(const uint32_t *__restrict__ sorted, int64_t n, int B,
