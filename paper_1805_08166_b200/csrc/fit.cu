@@ -171,35 +171,50 @@ __global__ void bins_kernel(const float *__restrict__ X, int64_t ld, int64_t n, 
 }
 
 // ------------------------------------------------------------------ 2. groups
-__global__ void __launch_bounds__(1024) ranks_kernel(const uint16_t *__restrict__ key, int64_t n,
-                                                     int32_t *__restrict__ rank, int32_t *__restrict__ counts,
-                                                     int32_t *__restrict__ woff, int32_t *__restrict__ gprefix,
-                                                     int group_size)
+// rank[i] = #{j < i : key[j] = key[i]} (the sample's position among its workload's samples, index
+// order), counts, their exclusive prefix woff, and the group prefix gprefix.  Three passes so the
+// 10^5-sample case is not one block: (1) per 1024-sample block, block-local ranks (warps in order)
+// and the block's key counts bc[b][k]; (2) one thread per key turns bc into exclusive offsets over the
+// blocks and builds the prefixes; (3) rank += the block's offset for the key.
+__global__ void __launch_bounds__(1024) ranks_local_kernel(const uint16_t *__restrict__ key, int64_t n,
+                                                           int32_t *__restrict__ rank, int32_t *__restrict__ bc)
 {
     __shared__ int32_t cnt[FIT_MAXKEYS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int k = tid; k < FIT_MAXKEYS; k += 1024) cnt[k] = 0;
+    cnt[tid] = 0;   // FIT_MAXKEYS == blockDim.x
     __syncthreads();
-    for (int64_t t0 = 0; t0 < n; t0 += 1024) {
-        const int64_t i = t0 + tid;
-        const bool ok = i < n;
-        const uint32_t k = ok ? (uint32_t)key[i] : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, k);
-        const int r = __popc(peers & ((1u << lane) - 1u));
-        for (int w = 0; w < 32; ++w) {
-            if (warp == w && ok) {
-                rank[i] = cnt[k] + r;
-                __syncwarp(peers);
-                if (r == 0) cnt[k] += __popc(peers);
-            }
-            __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * 1024 + tid;
+    const bool ok = i < n && key[i] < FIT_MAXKEYS;   // a bad key is reported by key_check_kernel
+    const uint32_t k = ok ? (uint32_t)key[i] : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, k);
+    const int r = __popc(peers & ((1u << lane) - 1u));
+    for (int w = 0; w < 32; ++w) {
+        if (warp == w && ok) {
+            rank[i] = cnt[k] + r;
+            __syncwarp(peers);
+            if (r == 0) cnt[k] += __popc(peers);
         }
+        __syncthreads();
+    }
+    bc[(int64_t)blockIdx.x * FIT_MAXKEYS + tid] = cnt[tid];
+}
+
+__global__ void __launch_bounds__(1024) ranks_scan_kernel(int nb, int32_t *__restrict__ bc,
+                                                          int32_t *__restrict__ counts, int32_t *__restrict__ woff,
+                                                          int32_t *__restrict__ gprefix, int group_size)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = tid;   // FIT_MAXKEYS == 1024 == blockDim.x
+    int32_t c = 0;
+    for (int b = 0; b < nb; ++b) {   // exclusive offsets of key k over the blocks (coalesced over k)
+        const int32_t x = bc[(int64_t)b * FIT_MAXKEYS + k];
+        bc[(int64_t)b * FIT_MAXKEYS + k] = c;
+        c += x;
     }
     // exclusive prefix sums of the counts and of the group counts over the FIT_MAXKEYS keys: one key
-    // per thread (1024 threads), warp shuffles + one shared pass over the warp totals
+    // per thread, warp shuffles + one shared pass over the warp totals
     __shared__ int32_t wo[32], wg[32];
-    const int k = tid;   // FIT_MAXKEYS == 1024 == blockDim.x
-    const int32_t c = cnt[k], gk = (c + group_size - 1) / group_size;
+    const int32_t gk = (c + group_size - 1) / group_size;
     int32_t xo = c, xg = gk;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -223,6 +238,13 @@ __global__ void __launch_bounds__(1024) ranks_kernel(const uint16_t *__restrict_
     woff[k] = wo[warp] + xo - c;
     gprefix[k] = wg[warp] + xg - gk;
     if (k == FIT_MAXKEYS - 1) gprefix[FIT_MAXKEYS] = wg[warp] + xg;
+}
+
+__global__ void ranks_add_kernel(const uint16_t *__restrict__ key, int64_t n, const int32_t *__restrict__ bc,
+                                 int32_t *__restrict__ rank)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && key[i] < FIT_MAXKEYS) rank[i] += bc[(i >> 10) * FIT_MAXKEYS + key[i]];
 }
 
 __device__ __forceinline__ uint32_t feistel(uint32_t x, int h, uint64_t seed, uint32_t tree, uint32_t wkey)
@@ -2157,7 +2179,14 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         cuts_kernel<<<F, 1024, 0, s>>>(sortA, n, B, cuts, ncuts); note_launch();
         bin_layout_kernel<<<1, 32, 0, s>>>(ncuts, F, boff, d_info, flist); note_launch();
         bins_kernel<<<dim3(nblk(n, 256), F), 256, 0, s>>>(d_feat, ld, n, F, B, cuts, ncuts, bins); note_launch();
-        ranks_kernel<<<1, 1024, 0, s>>>(d_group_key, n, rank, counts, woff, gpre, GS); note_launch();
+        {
+            const int nbk = (int)((n + 1023) / 1024);
+            int32_t *bc = ws.get<int32_t>((size_t)nbk * FIT_MAXKEYS);
+            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+            ranks_local_kernel<<<nbk, 1024, 0, s>>>(d_group_key, n, rank, bc); note_launch();
+            ranks_scan_kernel<<<1, 1024, 0, s>>>(nbk, bc, counts, woff, gpre, GS); note_launch();
+            ranks_add_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, n, bc, rank); note_launch();
+        }
         AT_CUDA_TRY(cudaMemcpyAsync(d_info + 3, gpre + FIT_MAXKEYS, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         if (o->d_base_margin)   // initial predictions: f_global(x_i) for a transfer-learning fit (Eq. 4)
             AT_CUDA_TRY(cudaMemcpyAsync(pred, o->d_base_margin, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
