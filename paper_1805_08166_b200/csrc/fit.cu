@@ -847,10 +847,12 @@ __global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int3
 //    (exact in int64), so a tree costs <= n (1 + (D - 1) / 2) sample visits instead of n D.
 // A histogram block owns one node's sample chunk and a range of the splittable features whose cells
 // fit in shared memory; a warp takes one sample (bins read as a row-major u8 row, 4 features per
-// lane-load), lanes map to features, so one warp-wide atomic touches distinct cells.  64-bit cells
-// are two 32-bit words updated by native shared atomics with an explicit carry (smem_add_u64's
-// rule); blocks flush with native 64-bit global atomics.  Node totals travel down the tree
-// (left = the winning split's prefix sums, right = total - left), so the leaves need no extra pass.
+// lane-load), lanes map to features, and each feature's cells sit in its lane's bank column, so one
+// warp-wide atomic touches 32 distinct banks.  64-bit cells are two 32-bit words updated by native
+// shared atomics with an explicit carry (smem_add_u64's rule); blocks flush with native 64-bit
+// global atomics.  Node totals travel down the tree (left = the winning split's prefix sums, right =
+// total - left), so the leaves need no extra pass.  Per level: split search (+ decisions), scatter
+// (+ next work list), histograms of the smaller children, subtraction; one tree is one CUDA graph.
 constexpr int SUB_NT = 1024;
 constexpr int SUB_ROWS = 400;   // rows of 32 cells (+ 1 trash row): 4 planes x 4 B x 32 x 401 = 200 KB of shared memory
 constexpr int SUB_NQW = 4;      // row words per lane and sample: <= 512 features per range
@@ -887,12 +889,6 @@ __global__ void rowbins_kernel(const uint8_t *__restrict__ bins, int64_t n, cons
     }
 }
 
-__device__ __forceinline__ void sub_add64(uint32_t *lo, uint32_t *hi, int c, uint32_t vlo, uint32_t vhi)
-{
-    const uint32_t old = atomicAdd(&lo[c], vlo);
-    atomicAdd(&hi[c], vhi + ((old + vlo < old) ? 1u : 0u));   // exact modular 64-bit sum (unconditional:
-                                                               // no divergent branch in the warp)
-}
 
 // items[b] = {node slot, p0, p1, -}: block (b, r) adds positions [p0, p1) of perm (identity when
 // perm == nullptr) into the cells of feature range r of hist[slot].  Warp w takes positions
