@@ -425,10 +425,15 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     const int64_t per = (int64_t)o->n_steps + 1;
     const int64_t n_keys = (int64_t)o->n_chains * per;
     const size_t key_bytes = ((size_t)n_keys * sizeof(uint64_t) + 255) / 256 * 256;
-    int rc = at::scratch_reserve(sp, key_bytes + at::topk_scratch_bytes(n_keys, o->k_out), s);
+    // chain lists per workload (multi-workload spaces): the top-k then reads only a workload's own keys
+    const bool lists = d_chain_workload && sp->host.n_w > 1;
+    const size_t list_bytes = lists ? (((size_t)sp->host.n_w * o->n_chains + at::MAXW) * sizeof(int32_t) + 255) / 256 * 256 : 0;
+    int rc = at::scratch_reserve(sp, key_bytes + list_bytes + at::topk_scratch_bytes(n_keys, o->k_out), s);
     if (rc) return rc;
     uint64_t *keys = (uint64_t *)sp->d_scratch;
-    uint64_t *tkbuf = (uint64_t *)((char *)sp->d_scratch + key_bytes);
+    int32_t *chain_list = lists ? (int32_t *)((char *)sp->d_scratch + key_bytes) : nullptr;
+    int32_t *list_n = lists ? chain_list + (size_t)sp->host.n_w * o->n_chains : nullptr;
+    uint64_t *tkbuf = (uint64_t *)((char *)sp->d_scratch + key_bytes + list_bytes);
 
     at::SaParams P{};
     P.S = sp->d_space;
@@ -505,9 +510,16 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         at::note_launch();
         AT_LAUNCH_CHECK("sa_kernel");
     }
+    if (lists) {
+        AT_CUDA_TRY(cudaMemsetAsync(list_n, 0, at::MAXW * sizeof(int32_t), s));
+        at::topk_chain_lists(d_chain_workload, o->n_chains, sp->host.n_w, chain_list, list_n, s);
+        AT_LAUNCH_CHECK("chain lists");
+    }
     for (int w = 0; w < sp->host.n_w; ++w) {
         at::TkArgs a{};
         a.mode = 0;
+        a.chain_list = lists ? chain_list + (size_t)w * o->n_chains : nullptr;
+        a.list_n = list_n;
         a.keys = keys;
         a.n_src = n_keys;
         a.n_chains = o->n_chains;

@@ -36,6 +36,7 @@ struct TkSrc {
     int64_t n;               // number of source keys (mode 0: (steps+1)*n_chains; 1: n_lists*k_in; 2: count)
     int64_t n_chains;
     const uint16_t *chain_w;
+    const int32_t *chain_list, *list_n;
     int w;
     uint64_t offset_w;
     const uint64_t *l_idx;
@@ -51,7 +52,15 @@ __device__ __forceinline__ uint64_t tk_load(const TkSrc &S, int64_t i)
     if (i >= S.n) return KEY_NONE;
     if (S.mode == 2) return __ldg(S.keys + i);
     uint64_t key, gidx;
-    if (S.mode == 0) {
+    if (S.mode == 0 && S.chain_list) {
+        // the workload's own chains only: i = step * cnt + j
+        const int64_t cnt = __ldg(S.list_n + S.w);
+        if (cnt == 0) return KEY_NONE;
+        const int64_t st = i / cnt, j = i - st * cnt;
+        if (st * S.n_chains >= S.n) return KEY_NONE;
+        key = __ldg(S.keys + st * S.n_chains + __ldg(S.chain_list + j));
+        gidx = S.offset_w + (key & 0xFFFFFFFFull);
+    } else if (S.mode == 0) {
         const int64_t c = i % S.n_chains;
         if (S.chain_w && (int)__ldg(S.chain_w + c) != S.w) return KEY_NONE;
         key = __ldg(S.keys + i);
@@ -73,8 +82,15 @@ __global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, u
     __shared__ int wsum[TK_THREADS / 32];
     const int tid = threadIdx.x;
     const int64_t base = (int64_t)blockIdx.x * TK_TILE;
-    for (int i = tid; i < TK_TILE; i += TK_THREADS) s[i] = tk_load(S, base + i);
-    __syncthreads();
+    int anyv = 0;
+    for (int i = tid; i < TK_TILE; i += TK_THREADS) {
+        s[i] = tk_load(S, base + i);
+        anyv |= s[i] != KEY_NONE;
+    }
+    if (!__syncthreads_or(anyv)) {   // an empty tile (other workloads' chains, padding lists): empty list
+        for (int i = tid; i < K; i += TK_THREADS) out[(int64_t)blockIdx.x * K + i] = KEY_NONE;
+        return;
+    }
     for (int k = 2; k <= TK_TILE; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int i = tid; i < TK_TILE; i += TK_THREADS) {
@@ -196,6 +212,22 @@ __global__ void topk_finish_kernel(const uint64_t *__restrict__ keys, int K, uin
     if (threadIdx.x == 0) *out_n = n_valid;
 }
 
+__global__ void chain_lists_kernel(const uint16_t *__restrict__ chain_w, int64_t n_chains, int n_w,
+                                   int32_t *__restrict__ list, int32_t *__restrict__ cnt)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_chains) return;
+    const int w = chain_w[c];
+    if (w >= n_w) return;
+    list[(int64_t)w * n_chains + atomicAdd(&cnt[w], 1)] = (int32_t)c;   // order free: the top-K is tiling-invariant
+}
+
+void topk_chain_lists(const uint16_t *chain_w, int64_t n_chains, int n_w, int32_t *list, int32_t *cnt, cudaStream_t s)
+{
+    chain_lists_kernel<<<(unsigned)((n_chains + 255) / 256), 256, 0, s>>>(chain_w, n_chains, n_w, list, cnt);
+    at::note_launch();
+}
+
 size_t topk_scratch_bytes(int64_t n_src, int K)
 {
     const int64_t b1 = (n_src + TK_TILE - 1) / TK_TILE;
@@ -210,6 +242,8 @@ int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s)
     S.n = a.n_src;
     S.n_chains = a.n_chains;
     S.chain_w = a.chain_w;
+    S.chain_list = a.chain_list;
+    S.list_n = a.list_n;
     S.w = a.w;
     S.offset_w = a.offset_w;
     S.l_idx = a.l_idx;

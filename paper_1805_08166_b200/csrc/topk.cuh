@@ -10,6 +10,8 @@ struct TkArgs {
     int64_t n_src;
     int64_t n_chains;
     const uint16_t *chain_w;     // mode 0: workload of each chain (nullable)
+    const int32_t *chain_list;   // mode 0, optional: the chains of workload w (any order) ...
+    const int32_t *list_n;       // ... and their number (device): only those chains' keys are read
     int w;
     uint64_t offset_w;
     const uint64_t *l_idx;       // mode 1
@@ -25,6 +27,8 @@ struct TkArgs {
 };
 
 size_t topk_scratch_bytes(int64_t n_src, int K);
+// chain lists per workload: list[w * n_chains + j], j < cnt[w] (cnt zeroed by the caller)
+void topk_chain_lists(const uint16_t *chain_w, int64_t n_chains, int n_w, int32_t *list, int32_t *cnt, cudaStream_t s);
 int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s);
 
 }  // namespace at
