@@ -428,7 +428,8 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     // chain lists per workload (multi-workload spaces): the top-k then reads only a workload's own keys
     const bool lists = d_chain_workload && sp->host.n_w > 1;
     const size_t list_bytes = lists ? (((size_t)sp->host.n_w * o->n_chains + at::MAXW) * sizeof(int32_t) + 255) / 256 * 256 : 0;
-    int rc = at::scratch_reserve(sp, key_bytes + list_bytes + at::topk_scratch_bytes(n_keys, o->k_out), s);
+    int rc = at::scratch_reserve(sp, key_bytes + list_bytes + at::topk_scratch_bytes(n_keys, o->k_out, lists ? sp->host.n_w : 1),
+                                 s);
     if (rc) return rc;
     uint64_t *keys = (uint64_t *)sp->d_scratch;
     int32_t *chain_list = lists ? (int32_t *)((char *)sp->d_scratch + key_bytes) : nullptr;
@@ -515,10 +516,12 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         at::topk_chain_lists(d_chain_workload, o->n_chains, sp->host.n_w, chain_list, list_n, s);
         AT_LAUNCH_CHECK("chain lists");
     }
-    for (int w = 0; w < sp->host.n_w; ++w) {
+    // one batched top-k over all workloads (chain lists), or one pass per workload
+    const int nb = lists ? sp->host.n_w : 1;
+    for (int w = 0; w < sp->host.n_w; w += nb) {
         at::TkArgs a{};
         a.mode = 0;
-        a.chain_list = lists ? chain_list + (size_t)w * o->n_chains : nullptr;
+        a.chain_list = lists ? chain_list : nullptr;
         a.list_n = list_n;
         a.keys = keys;
         a.n_src = n_keys;
@@ -536,7 +539,9 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
             // no chain belongs to this workload: empty list
             a.n_src = 0;
         }
-        rc = at::topk_run(a, tkbuf, s);
+        uint64_t offs[at::MAXW];
+        for (int q = 0; q < at::MAXW; ++q) offs[q] = q < sp->host.n_w ? sp->host.offset[q] : 0;
+        rc = at::topk_run(a, tkbuf, s, nb, offs);
         if (rc) return rc;
     }
     return AT_OK;

@@ -45,46 +45,65 @@ struct TkSrc {
     int n_w, k_in;
     const uint64_t *measured;
     int64_t n_measured;
+    // batched over workloads (blockIdx.y = workload w + y): per-y strides of the mode-2 input keys and
+    // of the chain lists, and every workload's index offset
+    int64_t key_stride, list_stride;
+    uint64_t offsets[MAXW];
 };
 
-__device__ __forceinline__ uint64_t tk_load(const TkSrc &S, int64_t i)
+// the block's view of its workload (blockIdx.y)
+struct TkW {
+    int w;
+    uint64_t offset_w;
+    const uint64_t *keys;
+    const int32_t *chain_list;
+};
+
+__device__ __forceinline__ uint64_t tk_load(const TkSrc &S, const TkW &V, int64_t i)
 {
     if (i >= S.n) return KEY_NONE;
-    if (S.mode == 2) return __ldg(S.keys + i);
+    if (S.mode == 2) return __ldg(V.keys + i);
     uint64_t key, gidx;
-    if (S.mode == 0 && S.chain_list) {
+    if (S.mode == 0 && V.chain_list) {
         // the workload's own chains only: i = step * cnt + j
-        const int64_t cnt = __ldg(S.list_n + S.w);
+        const int64_t cnt = __ldg(S.list_n + V.w);
         if (cnt == 0) return KEY_NONE;
         const int64_t st = i / cnt, j = i - st * cnt;
         if (st * S.n_chains >= S.n) return KEY_NONE;
-        key = __ldg(S.keys + st * S.n_chains + __ldg(S.chain_list + j));
-        gidx = S.offset_w + (key & 0xFFFFFFFFull);
+        key = __ldg(S.keys + st * S.n_chains + __ldg(V.chain_list + j));
+        gidx = V.offset_w + (key & 0xFFFFFFFFull);
     } else if (S.mode == 0) {
         const int64_t c = i % S.n_chains;
-        if (S.chain_w && (int)__ldg(S.chain_w + c) != S.w) return KEY_NONE;
+        if (S.chain_w && (int)__ldg(S.chain_w + c) != V.w) return KEY_NONE;
         key = __ldg(S.keys + i);
-        gidx = S.offset_w + (key & 0xFFFFFFFFull);
+        gidx = V.offset_w + (key & 0xFFFFFFFFull);
     } else {
         const int64_t l = i / S.k_in, j = i - l * S.k_in;
-        if (j >= __ldg(S.l_n + l * S.n_w + S.w)) return KEY_NONE;
-        const int64_t at = (l * S.n_w + S.w) * S.k_in + j;
+        if (j >= __ldg(S.l_n + l * S.n_w + V.w)) return KEY_NONE;
+        const int64_t at = (l * S.n_w + V.w) * S.k_in + j;
         gidx = __ldg(S.l_idx + at);
-        key = ((uint64_t)fkey(__ldg(S.l_score + at)) << 32) | (uint64_t)(gidx - S.offset_w);
+        key = ((uint64_t)fkey(__ldg(S.l_score + at)) << 32) | (uint64_t)(gidx - V.offset_w);
     }
     (void)gidx;   // measured configurations are dropped after the tile's sort (see topk_tile_kernel)
     return key;
 }
 
-__global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, uint64_t *__restrict__ out)
+__global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, uint64_t *__restrict__ out,
+                                                               int64_t out_stride)
 {
+    TkW V;
+    V.w = S.w + (int)blockIdx.y;
+    V.offset_w = S.offsets[V.w];
+    V.keys = S.keys + (int64_t)blockIdx.y * S.key_stride;
+    V.chain_list = S.chain_list ? S.chain_list + (int64_t)blockIdx.y * S.list_stride : nullptr;
+    out += (int64_t)blockIdx.y * out_stride;
     __shared__ uint64_t s[TK_TILE];
     __shared__ int wsum[TK_THREADS / 32];
     const int tid = threadIdx.x;
     const int64_t base = (int64_t)blockIdx.x * TK_TILE;
     int anyv = 0;
     for (int i = tid; i < TK_TILE; i += TK_THREADS) {
-        s[i] = tk_load(S, base + i);
+        s[i] = tk_load(S, V, base + i);
         anyv |= s[i] != KEY_NONE;
     }
     if (!__syncthreads_or(anyv)) {   // an empty tile (other workloads' chains, padding lists): empty list
@@ -156,7 +175,7 @@ __global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, u
 #pragma unroll
             for (int q = 0; q < PER; ++q) {
                 if (flag[q]) {
-                    if (r >= lo && r < hi && in_sorted(S.measured, S.n_measured, S.offset_w + (v[q] & 0xFFFFFFFFull))) {
+                    if (r >= lo && r < hi && in_sorted(S.measured, S.n_measured, V.offset_w + (v[q] & 0xFFFFFFFFull))) {
                         flag[q] = 2;   // measured: dropped below
                         ++m;
                     }
@@ -189,10 +208,16 @@ __global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, u
     for (int i = total_valid + tid; i < K; i += TK_THREADS) o[i] = KEY_NONE;
 }
 
-__global__ void topk_finish_kernel(const uint64_t *__restrict__ keys, int K, uint64_t offset_w,
+__global__ void topk_finish_kernel(const uint64_t *__restrict__ keys, int64_t key_stride, int K, TkSrc S,
                                    uint64_t *__restrict__ out_idx, float *__restrict__ out_score,
                                    int32_t *__restrict__ out_n)
 {
+    // blockIdx.y = workload S.w + y: its list, its offset, its output rows
+    keys += (int64_t)blockIdx.y * key_stride;
+    const uint64_t offset_w = S.offsets[S.w + blockIdx.y];
+    out_idx += (int64_t)blockIdx.y * K;
+    out_score += (int64_t)blockIdx.y * K;
+    out_n += blockIdx.y;
     // single block: keys are sorted and distinct with KEY_NONE padding
     __shared__ int n_valid;
     if (threadIdx.x == 0) n_valid = 0;
@@ -228,13 +253,15 @@ void topk_chain_lists(const uint16_t *chain_w, int64_t n_chains, int n_w, int32_
     at::note_launch();
 }
 
-size_t topk_scratch_bytes(int64_t n_src, int K)
+size_t topk_scratch_bytes(int64_t n_src, int K, int n_batch)
 {
     const int64_t b1 = (n_src + TK_TILE - 1) / TK_TILE;
-    return (size_t)(2 * (b1 + 1) * (int64_t)K) * sizeof(uint64_t);
+    return (size_t)(2 * (b1 + 1) * (int64_t)K) * sizeof(uint64_t) * (size_t)n_batch;
 }
 
-int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s)
+// n_batch workloads a.w .. a.w + n_batch - 1 in one launch per pass (blockIdx.y); their outputs are
+// consecutive rows of a.out_* (K entries each) and a.out_n[y]
+int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s, int n_batch, const uint64_t *offsets)
 {
     TkSrc S{};
     S.mode = a.mode;
@@ -253,26 +280,34 @@ int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s)
     S.k_in = a.k_in;
     S.measured = a.measured;
     S.n_measured = a.n_measured;
+    S.key_stride = 0;
+    S.list_stride = a.n_chains;
+    for (int q = 0; q < MAXW; ++q) S.offsets[q] = offsets ? offsets[q] : a.offset_w;
     const int K = a.K;
     int64_t blocks = (a.n_src + TK_TILE - 1) / TK_TILE;
     if (blocks < 1) blocks = 1;
-    uint64_t *bufA = scratch, *bufB = scratch + (blocks + 1) * K;
+    const int64_t stride = (blocks + 1) * K;   // per workload, in each of the two buffers
+    uint64_t *bufA = scratch, *bufB = scratch + stride * n_batch;
     ProfScope ps(AT_K_TOPK, s);
-    topk_tile_kernel<<<(unsigned)blocks, TK_THREADS, 0, s>>>(S, K, bufA); at::note_launch();
+    topk_tile_kernel<<<dim3((unsigned)blocks, n_batch), TK_THREADS, 0, s>>>(S, K, bufA, stride); at::note_launch();
     AT_LAUNCH_CHECK("topk_tile_kernel");
     int64_t n = blocks * K;
     while (blocks > 1) {
-        TkSrc R{};
+        TkSrc R = S;
         R.mode = 2;
         R.keys = bufA;
         R.n = n;
+        R.key_stride = stride;
+        R.chain_list = nullptr;
+        R.n_measured = 0;
         blocks = (n + TK_TILE - 1) / TK_TILE;
-        topk_tile_kernel<<<(unsigned)blocks, TK_THREADS, 0, s>>>(R, K, bufB); at::note_launch();
+        topk_tile_kernel<<<dim3((unsigned)blocks, n_batch), TK_THREADS, 0, s>>>(R, K, bufB, stride); at::note_launch();
         AT_LAUNCH_CHECK("topk_tile_kernel(reduce)");
         n = blocks * K;
         uint64_t *t = bufA; bufA = bufB; bufB = t;
     }
-    topk_finish_kernel<<<1, 256, 0, s>>>(bufA, K, a.offset_w, a.out_idx, a.out_score, a.out_n); at::note_launch();
+    topk_finish_kernel<<<dim3(1, n_batch), 256, 0, s>>>(bufA, stride, K, S, a.out_idx, a.out_score, a.out_n);
+    at::note_launch();
     AT_LAUNCH_CHECK("topk_finish_kernel");
     return AT_OK;
 }
@@ -290,27 +325,28 @@ extern "C" int topk_merge(at_space sp, const uint64_t *d_in_idx, const float *d_
     if (n_measured > 0 && !d_measured_sorted) return at::fail(AT_EINVAL, "topk_merge: null measured list");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n_src = (int64_t)n_lists * k_in;
-    int rc = at::scratch_reserve(sp, at::topk_scratch_bytes(n_src, k_out), s);
+    const int nw = sp->host.n_w;
+    int rc = at::scratch_reserve(sp, at::topk_scratch_bytes(n_src, k_out, nw), s);
     if (rc) return rc;
-    for (int w = 0; w < sp->host.n_w; ++w) {
-        at::TkArgs a{};
-        a.mode = 1;
-        a.n_src = n_src;
-        a.w = w;
-        a.offset_w = sp->host.offset[w];
-        a.l_idx = d_in_idx;
-        a.l_score = d_in_score;
-        a.l_n = d_in_n;
-        a.n_w = sp->host.n_w;
-        a.k_in = k_in;
-        a.measured = d_measured_sorted;
-        a.n_measured = n_measured;
-        a.K = k_out;
-        a.out_idx = d_out_idx + (int64_t)w * k_out;
-        a.out_score = d_out_score + (int64_t)w * k_out;
-        a.out_n = d_out_n + w;
-        rc = at::topk_run(a, (uint64_t *)sp->d_scratch, s);
-        if (rc) return rc;
-    }
+    at::TkArgs a{};   // every workload in one batched pass (blockIdx.y = workload)
+    a.mode = 1;
+    a.n_src = n_src;
+    a.w = 0;
+    a.offset_w = sp->host.offset[0];
+    a.l_idx = d_in_idx;
+    a.l_score = d_in_score;
+    a.l_n = d_in_n;
+    a.n_w = nw;
+    a.k_in = k_in;
+    a.measured = d_measured_sorted;
+    a.n_measured = n_measured;
+    a.K = k_out;
+    a.out_idx = d_out_idx;
+    a.out_score = d_out_score;
+    a.out_n = d_out_n;
+    uint64_t offs[at::MAXW];
+    for (int q = 0; q < at::MAXW; ++q) offs[q] = q < nw ? sp->host.offset[q] : 0;
+    rc = at::topk_run(a, (uint64_t *)sp->d_scratch, s, nw, offs);
+    if (rc) return rc;
     return AT_OK;
 }

@@ -26,9 +26,11 @@ struct TkArgs {
     int32_t *out_n;
 };
 
-size_t topk_scratch_bytes(int64_t n_src, int K);
+size_t topk_scratch_bytes(int64_t n_src, int K, int n_batch = 1);
 // chain lists per workload: list[w * n_chains + j], j < cnt[w] (cnt zeroed by the caller)
 void topk_chain_lists(const uint16_t *chain_w, int64_t n_chains, int n_w, int32_t *list, int32_t *cnt, cudaStream_t s);
-int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s);
+// n_batch > 1: workloads a.w .. a.w + n_batch - 1 in one launch per pass, outputs in consecutive
+// rows; offsets[w] = each workload's global index offset (nullptr: a.offset_w for all)
+int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s, int n_batch = 1, const uint64_t *offsets = nullptr);
 
 }  // namespace at
