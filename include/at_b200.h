@@ -36,6 +36,13 @@
  *    the host before anything is launched; on error nothing is launched and
  *    at_last_error() returns a message (thread-local).  No C++ exception crosses
  *    the ABI.  CUDA launch failures return AT_ECUDA.
+ *  - Index errors found on the device ("errors: out-of-range index"): a
+ *    global index >= |S| passed to features_extract / features_knobs, a persistent chain
+ *    state or a chain workload outside its workload in sa_explore, a pool entry outside
+ *    `workload` in select_topk.  The kernel clamps the entry to a valid one (its outputs
+ *    for that entry are undefined) and raises the space's error word; the NEXT call on
+ *    that space returns AT_ERANGE without launching anything (and clears the word), or
+ *    space_check(sp, stream) synchronizes `stream` and reports it at once.
  *  - The library needs an sm_100a device (B200).  There is no CPU fallback.
  *  - Bit-exactness contract: indices, features, leaf slots,
  *    accept bits, top-k, selections, histograms and fitted trees are bit-identical
@@ -104,6 +111,9 @@ AT_API int space_create(const at_workload *w, int32_t n_workloads, at_space *out
 AT_API int space_info(at_space sp, uint64_t *size_total, int32_t *n_workloads, int32_t *n_features,
                uint64_t *offsets, int32_t *radices);
 AT_API int space_destroy(at_space sp);
+/* space_check -- synchronizes `stream`, then returns AT_ERANGE if a kernel of an earlier call on
+ * this space met an out-of-range index (see Conventions), else AT_OK.  Clears the error word. */
+AT_API int space_check(at_space sp, void *stream);
 
 /* features_extract -- for each global index d_idx[i], i < n: decode the knobs,
  * lower to the loop nest x = g(e, s) and write its 468 features as column i
@@ -112,8 +122,8 @@ AT_API int space_destroy(at_space sp);
  * bottom-up, per buffer touch/reuse/stride x3), 120 relation features
  * R_t = max_{k: touch_b(k) < 2^t} Z_k,{reuse_b, top-down}, total
  * iterations, 3 footprints, 2 zero pads.  Requires ld >= n and ld % 4 == 0.
- * An out-of-range index is not checked on the device (the caller owns d_idx);
- * columns of such indices are undefined.  n == 0 is a no-op. */
+ * An index >= |S| is detected on the device: its column is undefined and the next call on
+ * the space (or space_check) returns AT_ERANGE.  n == 0 is a no-op. */
 AT_API int features_extract(at_space sp, const uint64_t *d_idx, int64_t n, float *d_feat, int64_t ld,
                      void *stream);
 
@@ -285,6 +295,13 @@ AT_API int gbt_predict_acq(at_gbt g, const float *d_feat, int64_t n, int64_t ld,
  * fp32 rounding.  Host-side construction like gbt_create; *out is a new handle.  Errors:
  * AT_EMISMATCH (different n_features). */
 AT_API int gbt_concat(at_gbt a, at_gbt b, at_gbt *out);
+
+/* at_exp_det_eval -- d_out[i] = exp_det(the fp32 whose bits are first_bits + i), i < n (u32
+ * wrap-around).  exp_det is the deterministic fp32 exp of the Metropolis acceptance test (Alg. 1
+ * P:152-153) and of Eq. 2's sigmoid, reading Q22: clamps at -87 / 88, n = rint(a log2 e),
+ * two-step Cody-Waite reduction, degree-7 Horner polynomial with fma, times 2^n.  Exposed so that
+ * the device implementation can be compared with the oracle's on all 2^32 inputs. */
+AT_API int at_exp_det_eval(uint32_t first_bits, int64_t n, float *d_out, void *stream);
 
 /* ------------------------------------------------------------------ instrumentation
  * at_launch_count: kernels this library launched since load (bench "gpu_launches").

@@ -359,6 +359,13 @@ def exp_det_array(a):
     return np.array([lib().or_exp_det(C.c_float(float(v))) for v in a.ravel()], dtype=np.float32).reshape(a.shape)
 
 
+def exp_det_range(first_bits, n):
+    """exp_det of the n fp32 values with bit patterns first_bits, first_bits + 1, ... (C loop)."""
+    out = np.empty(n, np.float32)
+    lib().or_exp_det_range(C.c_uint32(first_bits), C.c_int64(n), _p(out, C.c_float))
+    return out
+
+
 def mulhi64(a, b):
     return int(lib().or_mulhi64(C.c_uint64(a), C.c_uint64(b)))
 

@@ -79,6 +79,12 @@ float or_exp_det(float a)
     return p * scale;
 }
 
+/* exp_det of the fp32 values whose bits are first_bits, first_bits + 1, ... (u32 wrap), n of them */
+void or_exp_det_range(uint32_t first_bits, int64_t n, float *out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = or_exp_det(f_from_bits(first_bits + (uint32_t)i));
+}
+
 /* ======================================================================
  * Schedule space S_e ("multi-level tiling on each loop axis, loop
  * ordering ... unrolling and vectorization"; templates Q3, knob order O2).
@@ -706,7 +712,9 @@ int or_select(const or_space_set *s, int w, const uint64_t *pool_idx, const floa
 {
     if (w < 0 || w >= s->n || b < 0) return -1;
     const or_space *sp = &s->sp[w];
-    int32_t n_rand = (int32_t)ceil((double)eps * (double)b);
+    /* Q26: ceil of the fp32 product eps * b (RN), so eps = 0.05f, b = 20 gives 1, not 2 */
+    float eb = eps * (float)b;
+    int32_t n_rand = (int32_t)ceilf(eb);
     if (n_rand > b) n_rand = b;
     int32_t n_g = b - n_rand;
     int32_t cnt = 0;

@@ -114,6 +114,7 @@ int  or_features(const or_space_set *s, const uint64_t *idx, int64_t n, float *o
 void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 uint64_t or_mulhi64(uint64_t a, uint64_t b);
 float or_exp_det(float a);
+void or_exp_det_range(uint32_t first_bits, int64_t n, float *out);
 
 /* ---- GBT inference ---- */
 float or_gbt_score(const or_gbt *m, const float *x, uint8_t *slots /* [T] or NULL */);

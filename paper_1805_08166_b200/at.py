@@ -79,6 +79,7 @@ def lib() -> C.CDLL:
         L.space_create.argtypes = [C.POINTER(Workload), i32, C.POINTER(vp)]
         L.space_info.argtypes = [vp, vp, vp, vp, vp, vp]
         L.space_destroy.argtypes = [vp]
+        L.space_check.argtypes = [vp, vp]
         L.features_extract.argtypes = [vp, vp, i64, vp, i64, vp]
         L.features_knobs.argtypes = [vp, vp, i64, vp, i64, vp]
         L.gbt_create.argtypes = [i32, i32, i32, vp, vp, vp, C.c_float, C.POINTER(vp)]
@@ -93,6 +94,7 @@ def lib() -> C.CDLL:
         L.topk_merge.argtypes = [vp, vp, vp, vp, i32, i32, vp, i64, i32, vp, vp, vp, vp]
         L.select_topk.argtypes = [vp, i32, vp, vp, i64, vp, i64, C.POINTER(SelectOpts), vp, vp, vp]
         L.gbt_fit_hist.argtypes = [vp, i64, i64, i32, vp, vp, i64, i64, C.POINTER(FitOpts), C.POINTER(vp), vp]
+        L.at_exp_det_eval.argtypes = [C.c_uint32, i64, vp, vp]
         L.at_prof_enable.argtypes = [C.c_int]
         L.at_prof_query.argtypes = [i32, vp, vp]
         _lib = L
@@ -166,6 +168,10 @@ class Space:
             self.close()
         except Exception:
             pass
+
+    def check(self, stream=None):
+        """Synchronize the stream and raise AT_ERANGE if an earlier call met an out-of-range index."""
+        _check(lib().space_check(self.h, _stream(stream)))
 
     def features(self, idx, out=None, ld=None, stream=None):
         """idx: int64 CUDA tensor of global indices -> SoA [468][ld] float32."""
@@ -393,6 +399,15 @@ def _view_i64(ptr, count, device):
     import torch
     with torch.cuda.device(device):
         return torch.as_tensor(_CudaArray(ptr, count), device=device)
+
+
+def exp_det_eval(first_bits, n, out=None, stream=None):
+    """Device exp_det (reading Q22) of the fp32 values with bits first_bits + i, i < n."""
+    import torch
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+    _check(lib().at_exp_det_eval(first_bits, n, _ptr(out), _stream(stream)))
+    return out
 
 
 def launch_count() -> int:

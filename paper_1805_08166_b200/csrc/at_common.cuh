@@ -161,7 +161,17 @@ struct SpaceDev {
     int32_t n_w;
     uint64_t offset[MAXW + 1];
     WlDev w[MAXW];
+    uint32_t *err;                // mapped host word: set by a kernel that met an out-of-range index
 };
+
+// an index outside the space (or a chain / pool entry outside its workload): the kernel clamps it
+// to a valid one and raises the space's error word, which the next call on the space (or
+// space_check) reports as AT_ERANGE
+__device__ __forceinline__ void flag_range(const SpaceDev *S)
+{
+    *(volatile uint32_t *)S->err = 1u;
+    __threadfence_system();
+}
 
 }  // namespace at
 
@@ -173,6 +183,7 @@ struct at_space_s {
     // lazily grown scratch for sa_explore / topk_merge
     void *d_scratch;
     size_t scratch_bytes;
+    uint32_t *h_err;              // mapped pinned word (device view in host.err); see flag_range
 };
 
 struct at_gbt_s {
@@ -194,4 +205,7 @@ struct at_gbt_s {
 
 namespace at {
 int scratch_reserve(at_space sp, size_t bytes, cudaStream_t s);
+// AT_ERANGE (and clears the word) if a kernel enqueued earlier on this space met an out-of-range
+// index and has already finished; AT_OK otherwise.  Never synchronizes.
+int take_range_error(at_space sp);
 }

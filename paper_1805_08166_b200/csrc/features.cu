@@ -34,7 +34,11 @@ __global__ void __launch_bounds__(FEAT_BLOCK) features_kernel(const SpaceDev *__
     for (int q = 1; q < nw; ++q)
         if (g >= S->offset[q]) w = q;
     const WlDev &W = S->w[w];
-    const uint32_t local = (uint32_t)(g - S->offset[w]);
+    uint32_t local = (uint32_t)(g - S->offset[w]);
+    if (g >= S->offset[nw]) {   // outside the space: clamped, reported as AT_ERANGE
+        flag_range(S);
+        local = 0;
+    }
     uint32_t ch[MAXKNOBS];
     GlobalSink sk{out, ld, i, stage, tid};
     switch (W.tmpl) {
@@ -97,7 +101,11 @@ __global__ void __launch_bounds__(256) knob_features_kernel(const SpaceDev *__re
     for (int q = 1; q < S->n_w; ++q)
         if (g >= S->offset[q]) w = q;
     const WlDev &W = S->w[w];
-    const uint32_t local = (uint32_t)(g - S->offset[w]);
+    uint32_t local = (uint32_t)(g - S->offset[w]);
+    if (g >= S->offset[S->n_w]) {   // outside the space: clamped, reported as AT_ERANGE
+        flag_range(S);
+        local = 0;
+    }
     uint32_t ch[MAXKNOBS];
     int c;
     switch (W.tmpl) {
@@ -113,6 +121,7 @@ __global__ void __launch_bounds__(256) knob_features_kernel(const SpaceDev *__re
 extern "C" int features_knobs(at_space sp, const uint64_t *d_idx, int64_t n, float *d_feat, int64_t ld, void *stream)
 {
     if (!sp) return at::fail(AT_EINVAL, "features_knobs: null space");
+    if (int rc = at::take_range_error(sp)) return rc;
     if (n < 0) return at::fail(AT_EINVAL, "features_knobs: n < 0");
     if (n == 0) return AT_OK;
     if (!d_idx || !d_feat) return at::fail(AT_EINVAL, "features_knobs: null buffer");
@@ -131,6 +140,7 @@ extern "C" int features_extract(at_space sp, const uint64_t *d_idx, int64_t n, f
                                 void *stream)
 {
     if (!sp) return at::fail(AT_EINVAL, "features_extract: null space");
+    if (int rc = at::take_range_error(sp)) return rc;
     if (n < 0) return at::fail(AT_EINVAL, "features_extract: n < 0");
     if (n == 0) return AT_OK;
     if (!d_idx || !d_feat) return at::fail(AT_EINVAL, "features_extract: null buffer");

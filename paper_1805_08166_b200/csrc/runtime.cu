@@ -97,9 +97,43 @@ int scratch_reserve(at_space sp, size_t bytes, cudaStream_t s)
     return AT_OK;
 }
 
+int take_range_error(at_space sp)
+{
+    if (sp->h_err && *(volatile uint32_t *)sp->h_err) {
+        *(volatile uint32_t *)sp->h_err = 0u;
+        return fail(AT_ERANGE, "an index outside the space (or outside its workload) was passed to an earlier call "
+                               "on this space; its outputs for that entry are undefined");
+    }
+    return AT_OK;
+}
+
+__global__ void exp_det_kernel(uint32_t first, int64_t n, float *__restrict__ out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = exp_det(__uint_as_float(first + (uint32_t)i));
+}
+
 }  // namespace at
 
 extern "C" {
+
+int at_exp_det_eval(uint32_t first_bits, int64_t n, float *d_out, void *stream)
+{
+    if (n < 0 || n > 0x100000000ll || (n > 0 && !d_out)) return at::fail(AT_EINVAL, "at_exp_det_eval: bad n / buffer");
+    if (n == 0) return AT_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    at::exp_det_kernel<<<148 * 8, 256, 0, s>>>(first_bits, n, d_out);
+    at::note_launch();
+    AT_LAUNCH_CHECK("exp_det_kernel");
+    return AT_OK;
+}
+
+int space_check(at_space sp, void *stream)
+{
+    if (!sp) return at::fail(AT_EINVAL, "space_check: null space");
+    AT_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return at::take_range_error(sp);
+}
 
 const char *at_last_error(void) { return at::g_err.c_str(); }
 

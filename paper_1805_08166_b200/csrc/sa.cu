@@ -183,6 +183,10 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     int tmpl = 0;
     if (owner) {
         if (live && P.chain_w) w = P.chain_w[c];
+        if (w >= P.S->n_w) {   // a chain outside the space's workloads: clamped, AT_ERANGE
+            flag_range(P.S);
+            w = 0;
+        }
         const WlDev &W = P.S->w[w];
         if (live) {
             if (P.init) {
@@ -190,6 +194,10 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
                 idx = W.offset + mulhi64((uint64_t)r.x | ((uint64_t)r.y << 32), (uint64_t)W.size);
             } else {
                 idx = P.chain_idx[c];
+                if (idx < W.offset || idx - W.offset >= (uint64_t)W.size) {   // not a state of workload w: AT_ERANGE
+                    flag_range(P.S);
+                    idx = W.offset;
+                }
             }
         } else {
             idx = W.offset;
@@ -410,6 +418,7 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
                           void *stream)
 {
     if (!sp || !g || !o) return at::fail(AT_EINVAL, "sa_explore: null handle");
+    if (int rc = at::take_range_error(sp)) return rc;
     if (!d_chain_idx || !d_chain_energy || (!o->d_temps && o->n_steps > 0) || !d_out_idx || !d_out_score || !d_out_n)
         return at::fail(AT_EINVAL, "sa_explore: null buffer");
     if (o->n_chains < 1 || o->n_steps < 0 || o->k_out < 1 || o->k_out > 1024 || n_measured < 0)

@@ -74,6 +74,11 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SpaceDev *__r
         s_idx[i] = gi;
         s_chosen[i] = 0;
         uint32_t local = (uint32_t)(gi - W.offset);
+        if (gi < W.offset || gi - W.offset >= W.size) {   // not in this workload: never picked, AT_ERANGE
+            flag_range(S);
+            s_chosen[i] = 1;
+            local = 0;
+        }
         for (int j = 0; j < MAXKNOBS; ++j) {
             if (j < nk) {
                 const uint32_t q = local / W.radix[j];
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SpaceDev *__r
     for (int i = tid; i < n_pool; i += SEL_THREADS) s_z[i] = ((double)pool_E[i] - s_mu) / s_sigma;
     __syncthreads();
 
-    int n_rand = (int)ceil((double)eps * (double)b);
+    int n_rand = (int)ceilf(__fmul_rn(eps, (float)b));   // Q26: ceil of the fp32 product
     if (n_rand > b) n_rand = b;
     const int n_g = b - n_rand;
     const int greedy = n_g < n_pool ? n_g : n_pool;
@@ -136,11 +141,13 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SpaceDev *__r
             Cand bb = s_red[0];
             for (int q = 1; q < SEL_THREADS / 32; ++q)
                 if (better(s_red[q], bb)) bb = s_red[q];
-            s_chosen[bb.i] = 1;
-            out[s_cnt++] = bb.idx;
-            for (int j = 0; j < nk; ++j) {
-                const uint32_t v = s_ch[bb.i][j];
-                s_cov[j][v >> 5] |= 1u << (v & 31);
+            if (bb.i >= 0) {   // (none left only when invalid pool entries were excluded)
+                s_chosen[bb.i] = 1;
+                out[s_cnt++] = bb.idx;
+                for (int j = 0; j < nk; ++j) {
+                    const uint32_t v = s_ch[bb.i][j];
+                    s_cov[j][v >> 5] |= 1u << (v & 31);
+                }
             }
         }
         __syncthreads();
@@ -181,6 +188,7 @@ extern "C" int select_topk(at_space sp, int32_t workload, const uint64_t *d_pool
                            const at_select_opts *o, uint64_t *d_out_idx, int32_t *d_out_n, void *stream)
 {
     if (!sp || !o || !d_out_idx || !d_out_n) return at::fail(AT_EINVAL, "select_topk: null pointer");
+    if (int rc = at::take_range_error(sp)) return rc;
     if (workload < 0 || workload >= sp->host.n_w) return at::fail(AT_ERANGE, "select_topk: workload out of range");
     if (n_pool < 0 || n_pool > at::SEL_MAXPOOL) return at::fail(AT_EUNSUPPORTED, "select_topk: pool must hold <= 1024");
     if (n_pool > 0 && (!d_pool_idx || !d_pool_score)) return at::fail(AT_EINVAL, "select_topk: null pool");

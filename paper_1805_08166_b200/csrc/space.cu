@@ -168,6 +168,7 @@ int space_create(const at_workload *w, int32_t n_workloads, at_space *out)
     sp->d_fact = nullptr;
     sp->d_scratch = nullptr;
     sp->scratch_bytes = 0;
+    sp->h_err = nullptr;
     Builder B;
     sp->host.n_w = n_workloads;
     uint64_t off = 0;
@@ -181,10 +182,20 @@ int space_create(const at_workload *w, int32_t n_workloads, at_space *out)
     sp->host.offset[n_workloads] = off;
     sp->total = off;
     if (B.fact.empty()) B.fact.push_back(0);
+    // the range-error word: pinned, mapped (kernels store to it; the host reads it without a sync)
+    if (cudaHostAlloc((void **)&sp->h_err, sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void **)&sp->host.err, sp->h_err, 0) != cudaSuccess) {
+        cudaGetLastError();
+        if (sp->h_err) cudaFreeHost(sp->h_err);
+        delete sp;
+        return at::fail(AT_ENOMEM, "space_create: mapped error word allocation failed");
+    }
+    *sp->h_err = 0u;
     if (cudaMalloc(&sp->d_space, sizeof(at::SpaceDev)) != cudaSuccess ||
         cudaMalloc(&sp->d_fact, B.fact.size() * sizeof(uint16_t)) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(sp->d_space);
+        cudaFreeHost(sp->h_err);
         delete sp;
         return at::fail(AT_ENOMEM, "space_create: device allocation failed");
     }
@@ -193,6 +204,7 @@ int space_create(const at_workload *w, int32_t n_workloads, at_space *out)
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
         cudaFree(sp->d_space);
         cudaFree(sp->d_fact);
+        cudaFreeHost(sp->h_err);
         delete sp;
         return at::cuda_fail(e1 != cudaSuccess ? e1 : e2, "space_create upload");
     }
@@ -222,6 +234,7 @@ int space_destroy(at_space sp)
     cudaFree(sp->d_space);
     cudaFree(sp->d_fact);
     if (sp->d_scratch) cudaFree(sp->d_scratch);
+    if (sp->h_err) cudaFreeHost(sp->h_err);
     delete sp;
     return AT_OK;
 }

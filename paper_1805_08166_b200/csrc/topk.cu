@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(TK_THREADS) topk_tile_kernel(TkSrc S, int K, u
             if (m) atomicAdd(&s_m, m);
             __syncthreads();
             const int mm = s_m;
+            __syncthreads();   // every warp has read s_m before thread 0 resets it
             if (mm == 0) break;
             lo = hi;
             hi += mm;
@@ -320,6 +321,7 @@ extern "C" int topk_merge(at_space sp, const uint64_t *d_in_idx, const float *d_
 {
     if (!sp || !d_in_idx || !d_in_score || !d_in_n || !d_out_idx || !d_out_score || !d_out_n)
         return at::fail(AT_EINVAL, "topk_merge: null pointer");
+    if (int rc = at::take_range_error(sp)) return rc;
     if (n_lists < 1 || k_in < 1 || k_out < 1 || k_out > 1024 || n_measured < 0)
         return at::fail(AT_EINVAL, "topk_merge: need n_lists, k_in >= 1 and 1 <= k_out <= 1024");
     if (n_measured > 0 && !d_measured_sorted) return at::fail(AT_EINVAL, "topk_merge: null measured list");

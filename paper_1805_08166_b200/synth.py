@@ -110,6 +110,23 @@ def temperatures(n_steps: int, t0: float, ratio: float = 0.05) -> np.ndarray:
     return (t0 * np.power(ratio, s / (n_steps - 1))).astype(np.float32)
 
 
+def energy_sigma(E) -> float:
+    """Reading Q21's T0: the population standard deviation of the chains' initial energies, fp64,
+    sequential in chain order (1.0 if it is 0, e.g. a constant model)."""
+    e = [float(x) for x in np.asarray(E, dtype=np.float32)]
+    if not e:
+        return 1.0
+    mu = 0.0
+    for x in e:
+        mu += x
+    mu /= len(e)
+    var = 0.0
+    for x in e:
+        var += (x - mu) * (x - mu)
+    sd = (var / len(e)) ** 0.5
+    return sd if sd > 0.0 else 1.0
+
+
 def energy_scale(n_trees: int) -> float:
     """Std of a sum of n_trees U(-0.1, 0.1) leaves: the T0 used with synthetic ensembles."""
     return float(0.2 / np.sqrt(12.0) * np.sqrt(n_trees))

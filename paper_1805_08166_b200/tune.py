@@ -70,12 +70,18 @@ class Tuner:
         self.state = TuneState(chain_idx=torch.zeros(cfg.n_chains, dtype=torch.int64, device="cuda"))
         self.round = 0
 
-    def _temps(self):
-        import torch
-        from .synth import energy_scale, temperatures
-        n_trees = self.model.n_trees // (self.acq["n_models"] if self.acq else 1)
-        t0 = energy_scale(n_trees)
-        return torch.from_numpy(temperatures(self.cfg.n_steps, t0, self.cfg.t_ratio)).cuda()
+    def _temps(self, meas):
+        """Reading Q21: geometric T0 -> t_ratio T0 with T0 = sigma of the round's initial chain energies
+        under the current f-hat (synth.energy_sigma).  The energies come from a 0-step sa_explore, which
+        scores the chain states and moves nothing; the 128 floats are read back (the round syncs for the
+        measurement anyway) so that the schedule is the same fp64 arithmetic on every replay."""
+        from .synth import energy_sigma, temperatures
+        at, torch, cfg, st = self.at, self.torch, self.cfg, self.state
+        empty = torch.empty(0, dtype=torch.float32, device=st.chain_idx.device)
+        r0 = at.sa_explore(self.space, self.model, st.chain_idx, empty, seed=cfg.seed, round_=self.round, k_out=1,
+                           measured=meas, init=self.round == 0, acq=self.acq)
+        t0 = energy_sigma(r0["chain_energy"].cpu().numpy())
+        return torch.from_numpy(temperatures(cfg.n_steps, t0, cfg.t_ratio)).cuda()
 
     def step(self):
         """One iteration of Algorithm 1; returns the selected global indices (numpy u64)."""
@@ -83,7 +89,7 @@ class Tuner:
         meas = None
         if st.measured:
             meas = torch.from_numpy(np.sort(np.array(st.measured, dtype=np.uint64)).view(np.int64)).cuda()
-        res = at.sa_explore(self.space, self.model, st.chain_idx, self._temps(), seed=cfg.seed, round_=self.round,
+        res = at.sa_explore(self.space, self.model, st.chain_idx, self._temps(meas), seed=cfg.seed, round_=self.round,
                             k_out=cfg.lam * cfg.b, measured=meas, init=self.round == 0, acq=self.acq)
         n_pool = int(res["out_n"][0])
         sel, n_sel = at.select_topk(self.space, 0, res["out_idx"][0, :n_pool].contiguous(),
@@ -94,11 +100,15 @@ class Tuner:
         st.measured += selected.tolist()
         st.costs += costs.tolist()
         st.history.append((selected, costs))
-        i = int(np.argmin(costs)) if len(costs) else -1
-        if i >= 0 and costs[i] < st.best_cost:
+        fin = np.where(np.isfinite(costs), costs, np.inf)
+        i = int(np.argmin(fin)) if len(costs) else -1
+        if i >= 0 and fin[i] < st.best_cost:
             st.best_cost, st.best_idx = float(costs[i]), int(selected[i])
-        # update f-hat using D (from scratch)
-        self.model, self.acq = self.refit()
+        # update f-hat using D (from scratch); failed measurements (non-finite cost) stay in D -- they
+        # are never proposed again -- but are left out of the fit
+        fit = self.refit()
+        if fit is not None:
+            self.model, self.acq = fit
         self.round += 1
         return selected
 
@@ -113,10 +123,14 @@ class Tuner:
     def refit(self):
         """update f-hat using D: one model, or K bootstrap models concatenated for the acquisition."""
         at, torch, cfg, st = self.at, self.torch, self.cfg, self.state
-        n = len(st.measured)
-        idx = torch.from_numpy(np.array(st.measured, dtype=np.uint64).view(np.int64)).cuda()
+        costs = np.array(st.costs, dtype=np.float32)
+        ok = np.isfinite(costs)
+        n = int(ok.sum())
+        if n < 2:          # nothing to rank yet: keep the current f-hat
+            return None
+        idx = torch.from_numpy(np.array(st.measured, dtype=np.uint64)[ok].view(np.int64)).cuda()
         X = self.space.features(idx)
-        c = torch.from_numpy(np.array(st.costs, dtype=np.float32)).cuda()
+        c = torch.from_numpy(costs[ok]).cuda()
         key = torch.zeros(n, dtype=torch.int16, device="cuda")
         if cfg.n_bootstrap < 2:
             return self._fit(X, n, c, key), None

@@ -873,6 +873,106 @@ def test_config5_sweep_sampled(at):
     assert_bits_equal(sl.cpu().numpy()[:, pick], esl, "sampled leaf slots")
 
 
+# ------------------------------------------------------------------ exp_det, boundary errors
+def test_exp_det_all_2_32_inputs_bit_identical(at):
+    """Reading Q22 (Metropolis acceptance, Alg. 1; Eq. 2's sigmoid): the device
+    exp_det equals the oracle's on every one of the 2^32 fp32 inputs (NaN outputs compared as NaN,
+    their payload is not part of the contract)."""
+    chunk = 1 << 27
+    out = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    bad = 0
+    for first in range(0, 1 << 32, chunk):
+        at.exp_det_eval(first, chunk, out=out)
+        g = out.cpu().numpy()
+        o = O.exp_det_range(first, chunk)
+        gb, ob = g.view(np.uint32), o.view(np.uint32)
+        diff = gb != ob
+        if diff.any():
+            diff &= ~(np.isnan(g) & np.isnan(o))
+            bad += int(diff.sum())
+            assert bad == 0, f"exp_det differs at bits {first + int(np.flatnonzero(diff)[0]):#010x}"
+
+
+def test_out_of_range_indices_report_erange(at):
+    """SPEC S:138-142 ("errors: out-of-range index"), include/at_b200.h conventions: an index >= |S|
+    in features_extract, a persistent chain state outside its workload or a chain workload >= n_w in
+    sa_explore, a pool entry outside `workload` in select_topk -> the next call on the space (or
+    space_check) returns AT_ERANGE; valid calls afterwards are unaffected."""
+    sp = at.Space([synth.MATMUL_512, synth.MATMUL_8])
+    n = sp.size()
+    idx = u64(np.array([0, n - 1, n, 5], np.uint64))
+    sp.features(idx)
+    with pytest.raises(at.ATError) as e:
+        sp.check()
+    assert e.value.code == -2
+    sp.features(idx[:2])
+    sp.check()                                        # cleared, and the valid call is clean
+    sp.features(idx)
+    torch.cuda.synchronize()
+    with pytest.raises(at.ATError) as e:              # reported by the NEXT call, which launches nothing
+        sp.features(idx[:2])
+    assert e.value.code == -2
+    ens = synth.ensemble(8, 3, seed=1)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    temps = torch.full((4,), 0.1, dtype=torch.float32, device="cuda")
+    # chain state of workload 1 claimed for workload 0
+    bad_state = u64(np.array([sp.offsets[1] + 3, 7], np.uint64))
+    cw = dev(np.array([0, 0], np.int16))
+    at.sa_explore(sp, g, bad_state, temps, seed=1, round_=0, k_out=4, chain_workload=cw)
+    with pytest.raises(at.ATError) as e:
+        sp.check()
+    assert e.value.code == -2
+    # chain workload >= n_w
+    at.sa_explore(sp, g, u64(np.array([1, 2], np.uint64)), temps, seed=1, round_=0, k_out=4,
+                  chain_workload=dev(np.array([0, 5], np.int16)))
+    with pytest.raises(at.ATError) as e:
+        sp.check()
+    assert e.value.code == -2
+    # select pool entry of another workload
+    pool = u64(np.array([1, 2, sp.offsets[1] + 1], np.uint64))
+    at.select_topk(sp, 0, pool, dev(np.array([0.1, 0.2, 0.3], np.float32)), b=2, eps=0.0, alpha=0.1, seed=1,
+                   round_=0)
+    with pytest.raises(at.ATError) as e:
+        sp.check()
+    assert e.value.code == -2
+    at.select_topk(sp, 0, pool[:2].contiguous(), dev(np.array([0.1, 0.2], np.float32)), b=2, eps=0.0, alpha=0.1,
+                   seed=1, round_=0)
+    sp.check()
+
+
+def test_topk_drops_measured_over_several_rounds(at):
+    """Alg. 1 P:152 / Q23: the distinct top-K excludes measured configurations even when the K best
+    keys hold many measured ones (the tile's measured-drop loop runs several rounds)."""
+    sp = at.Space([synth.MATMUL_8])
+    osp = O.OracleSpace([O.workload(**synth.MATMUL_8)])
+    ens = synth.ensemble(20, 5, seed=9)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    N = osp.size()
+    allidx = np.arange(N, dtype=np.uint64)
+    E = O.OracleGbt(**ens).predict(osp.features(allidx))
+    order = allidx[np.lexsort((allidx, E))]
+    for n_meas in (40, 200, 700):
+        meas = np.sort(order[:n_meas])   # the whole head of the ranking is measured
+        r = at.sa_explore(sp, g, u64(allidx), torch.empty(0, dtype=torch.float32, device="cuda"), seed=1,
+                          round_=0, k_out=64, measured=u64(meas), init=False)
+        k = int(r["out_n"][0])
+        assert k == 64
+        assert np.array_equal(host_u64(r["out_idx"][0][:k]), order[n_meas:n_meas + 64]), n_meas
+
+
+@pytest.mark.parametrize("b,want", [(20, 1), (64, 4), (100, 5)])
+def test_select_epsilon_count_matches_oracle(at, b, want):
+    """Q26: ceil(eps b) with eps b formed in fp32 (eps = 0.05): GPU selection == oracle selection."""
+    sp = at.Space([synth.CFG2B])
+    osp = O.OracleSpace([O.workload(**synth.CFG2B)])
+    idx = synth.uniform_indices(osp.size(), 2 * b, seed=b)
+    E = np.random.default_rng(b).random(2 * b).astype(np.float32)
+    o = np.lexsort((idx, E))
+    out, n = at.select_topk(sp, 0, u64(idx[o]), dev(E[o]), b=b, eps=0.05, alpha=0.1, seed=3, round_=2)
+    ref = osp.select(0, idx[o], E[o], b, 0.05, 0.1, 3, 2)
+    assert int(n) == b and np.array_equal(host_u64(out[:b]), ref)
+
+
 # ------------------------------------------------------------------ Algorithm 1 end to end
 def test_algorithm1_rounds_match_oracle(at):
     """Three rounds of Algorithm 1 (SA -> select -> measure -> refit, persistent chains) through the
@@ -892,7 +992,8 @@ def test_algorithm1_rounds_match_oracle(at):
     chains, measured, costs = None, [], []
     for r in range(3):
         sel_gpu = tuner.step()
-        temps = synth.temperatures(cfg.n_steps, synth.energy_scale(model.n_trees), cfg.t_ratio)
+        e0 = osp.sa_explore(model, cfg.n_chains, 0, cfg.seed, r, np.zeros(0, np.float32), chain_idx=chains)
+        temps = synth.temperatures(cfg.n_steps, synth.energy_sigma(e0["chain_energy"]), cfg.t_ratio)   # Q21
         res = osp.sa_explore(model, cfg.n_chains, cfg.n_steps, cfg.seed, r, temps, chain_idx=chains)
         chains = res["chain_idx"]
         (pi, pe), = osp.topk(res["visited_E"], res["visited_idx"], cfg.lam * cfg.b, measured=measured)
@@ -933,8 +1034,8 @@ def test_algorithm1_with_transfer_and_bootstrap_matches_oracle(at, objective, K,
     model, oacq, chains, measured, costs = oglob, None, None, [], []
     for r in range(2):
         sel_gpu = tuner.step()
-        T = (model[0] if isinstance(model, list) else model).n_trees
-        temps = synth.temperatures(cfg.n_steps, synth.energy_scale(T), cfg.t_ratio)
+        e0 = osp.sa_explore(model, cfg.n_chains, 0, cfg.seed, r, np.zeros(0, np.float32), chain_idx=chains, acq=oacq)
+        temps = synth.temperatures(cfg.n_steps, synth.energy_sigma(e0["chain_energy"]), cfg.t_ratio)   # Q21
         res = osp.sa_explore(model, cfg.n_chains, cfg.n_steps, cfg.seed, r, temps, chain_idx=chains, acq=oacq)
         chains = res["chain_idx"]
         (pi, pe), = osp.topk(res["visited_E"], res["visited_idx"], cfg.lam * cfg.b, measured=measured)

@@ -379,6 +379,125 @@ def test_sa_knob_frequencies_uniform():
     assert np.all(np.abs(cnt / cnt.sum() - 0.25) < 0.05 * 0.25 * 4)
 
 
+def _philox_words(seed, g, step, round_, tag):
+    """Philox4x32-10 words of counter (g, step, round, tag), key = seed (Q28; KAT-pinned above)."""
+    return O.philox([g, step, round_, tag], [seed & 0xFFFFFFFF, seed >> 32])
+
+
+def test_sa_metropolis_finite_temperature_decisions():
+    """Alg. 1 P:152-153 / P:187 at 0 < T < inf: every decision of every chain-step equals the
+    Metropolis rule written out independently here -- accept iff d = E' - E <= 0 or
+    u < exp(-d / T), with u = (word 2 >> 8) 2^-24 of Philox(g, s, round, SA_STEP) and exp from the
+    C library in fp64 (not exp_det).  Decisions within 1e-5 of the threshold are skipped (fp32 vs
+    fp64 rounding of exp); a sign error in -d/T, a wrong Philox word for u, or a strict/non-strict
+    mix-up of the d <= 0 branch fails here."""
+    sp, e, _ = _tiny()
+    seed, rnd, C, S = 0x1234_5678_9ABC, 3, 64, 60
+    temps = synth.temperatures(S, 0.08, 0.1)          # 0.08 -> 0.008, spans many acceptance rates
+    r = sp.sa_explore(e, C, S, seed=seed, round_=rnd, temps=temps, chain_id_base=1000)
+    n_up_acc = n_up_rej = n_skip = 0
+    for c in range(C):
+        E = np.float32(r["visited_E"][c, 0])
+        for st in range(S):
+            E2 = np.float32(r["visited_E"][c, st + 1])
+            d = np.float32(E2 - E)                     # fp32 RN difference, as the paper's energies are fp32
+            acc = (int(r["accept_bits"][c, st // 32]) >> (st % 32)) & 1
+            if d <= 0:
+                assert acc == 1, (c, st)
+            else:
+                u = (_philox_words(seed, 1000 + c, st, rnd, 1)[2] >> 8) * 2.0 ** -24
+                p = math.exp(-float(d) / float(temps[st]))
+                if abs(u - p) < 1e-5:
+                    n_skip += 1
+                else:
+                    assert acc == (1 if u < p else 0), (c, st, u, p)
+                    n_up_acc += acc
+                    n_up_rej += 1 - acc
+            if acc:
+                E = E2
+        assert r["chain_energy"][c] == E
+    assert n_up_acc > 100 and n_up_rej > 100 and n_skip < 10
+
+
+def test_sa_uphill_acceptance_frequency_is_boltzmann_factor():
+    """over many uphill proposals the number accepted equals sum exp(-d/T) within a
+    binomial 5-sigma band (the statistical form of the Metropolis rule)."""
+    sp, e, _ = _tiny()
+    T = 0.03
+    r = sp.sa_explore(e, 256, 80, seed=99, round_=0, temps=np.full(80, T, np.float32))
+    acc_n, p_sum, var = 0, 0.0, 0.0
+    for c in range(256):
+        E = r["visited_E"][c, 0]
+        for st in range(80):
+            E2 = r["visited_E"][c, st + 1]
+            a = (int(r["accept_bits"][c, st // 32]) >> (st % 32)) & 1
+            if E2 > E:
+                p = math.exp(-(float(E2) - float(E)) / T)
+                acc_n += a
+                p_sum += p
+                var += p * (1 - p)
+            if a:
+                E = E2
+    assert var > 100
+    assert abs(acc_n - p_sum) <= 5 * math.sqrt(var), (acc_n, p_sum, var)
+
+
+def test_sa_samples_the_boltzmann_distribution():
+    """Metropolis with a symmetric proposal (single-knob move uniform over the non-singleton knobs,
+    new value uniform among the others: S:151, Q20) has the stationary law pi(s) ~ exp(-f(s) / T)
+    (P:152-153).  On the 2,000-configuration matmul 8^3 space at fixed T, the final states of
+    3,000 independent chains match pi computed by exhaustive enumeration: chi-square over 10 energy
+    bins of equal pi mass (p > 1e-4) and the mean energy within 5 standard errors.  A sign error in
+    the acceptance exponent concentrates the chains on the worst configurations instead."""
+    from scipy.stats import chi2
+    sp, e, _ = _tiny()
+    N = sp.size()
+    allidx = np.arange(N, dtype=np.uint64)
+    E = e.predict(sp.features(allidx)).astype(np.float64)
+    T, C, S = 0.05, 3000, 150
+    r = sp.sa_explore(e, C, S, seed=11, round_=0, temps=np.full(S, T, np.float32))
+    fin = r["chain_idx"].astype(np.int64)
+    w = np.exp(-(E - E.min()) / T)
+    pi = w / w.sum()
+    order = np.argsort(E, kind="stable")
+    cum = np.cumsum(pi[order])
+    nb = 10
+    b_of = np.empty(N, np.int64)
+    b_of[order] = np.searchsorted(np.linspace(0, 1, nb + 1)[1:-1], cum - pi[order] / 2)
+    expect = np.array([pi[b_of == b].sum() for b in range(nb)]) * C
+    obs = np.bincount(b_of[fin], minlength=nb)
+    x2 = float(((obs - expect) ** 2 / expect).sum())
+    assert chi2.sf(x2, nb - 1) > 1e-4, (obs, expect.round(1), x2)
+    mean_pi = float((pi * E).sum())
+    sd_pi = math.sqrt(float((pi * (E - mean_pi) ** 2).sum()))
+    assert abs(E[fin].mean() - mean_pi) <= 5 * sd_pi / math.sqrt(C)
+
+
+def test_sa_annealing_concentrates_on_the_optimum_of_a_unimodal_energy():
+    """S:384 (the hill-climbing limit of SA, Alg. 1): on a unimodal energy, annealed chains
+    end at the optimum.  The energy is a hand-built depth-2 ensemble on the matmul 8^3 space: one
+    tree per loop i0, j0, k0, i1, j1 (rows 0-4 of the T_MM nest, length column 19 r) with penalty 1
+    for an extent < 2, 0 for extent 2, 1 for extent > 2 -- unimodal in every knob, minimum 0 exactly
+    at split_i = split_j = (2, 2, 2), split_k = (2, 4) (any unroll: 5 optimal configurations,
+    0.25 % of the space).  Annealed from T = 1 to 0.01 over 400 steps, >= 90 % of 512 chains end at
+    energy 0 (>= 90 % within the top 1 %); with the exponent's sign flipped they would climb."""
+    sp = space(synth.MATMUL_8)
+    rows = [0, 1, 2, 3, 4]
+    inf = np.float32(np.inf)
+    feat = np.array([[19 * r, 0, 19 * r] for r in rows], np.uint16)
+    thr = np.array([[1.5, inf, 2.5] for _ in rows], np.float32)
+    leaf = np.array([[1.0, 1.0, 0.0, 1.0] for _ in rows], np.float32)
+    e = O.OracleGbt(feat, thr, leaf)
+    N = sp.size()
+    E = e.predict(sp.features(np.arange(N, dtype=np.uint64)))
+    opt = np.flatnonzero(E == 0.0)
+    assert len(opt) == 5 and all(sp.decode(int(i))[:3] == sp.decode(int(opt[0]))[:3] for i in opt)
+    S = 400
+    r = sp.sa_explore(e, 512, S, seed=5, round_=1, temps=synth.temperatures(S, 1.0, 0.01))
+    assert np.mean(r["chain_energy"] == 0.0) >= 0.9
+    assert set(r["chain_idx"][r["chain_energy"] == 0.0].tolist()) <= set(opt.tolist())
+
+
 # ---------------------------------------------------------------- select (a8)
 def test_select_alpha0_eps0_is_plain_topb():
     sp = space(synth.CFG2A)
@@ -433,6 +552,46 @@ def test_select_greedy_vs_bruteforce_subsets():
         best = max(L(S) for S in itertools.combinations(range(8), 4))
         mine = L([list(idx).index(i) for i in got])
         assert mine >= (1 - 1 / math.e) * best - 1e-12
+
+
+def test_select_coverage_term_decides_at_the_hand_computed_threshold():
+    """Eq. 3: the coverage term counts distinct values per knob over the selected
+    set.  Pool of 3 on T_MM (4 knobs): A = (0,0,0,0) best, B = (0,1,0,0) (one knob differs from A),
+    C = (1,1,1,1) (all four differ).  After A is picked, B adds coverage 1 and C adds 4 (S:393's
+    example: {[1,2],[1,3]} covers |{1}| + |{2,3}| = 3 values -- A and B cover 4 + 1 = 5 here), so the
+    second greedy pick switches from B to C exactly when alpha (4 - 1) > z_C - z_B."""
+    sp = space(dict(kind=0, n=4, m=4, k=4))
+    A, B, Cc = (sp.encode(v) for v in ([0, 0, 0, 0], [0, 1, 0, 0], [1, 1, 1, 1]))
+    pool = np.array([A, B, Cc], np.uint64)
+    E = np.array([-1.0, 0.25, 0.5], np.float32)
+    Ed = E.astype(np.float64)
+    mu = (Ed[0] + Ed[1] + Ed[2]) / 3
+    sd = math.sqrt(((Ed[0] - mu) ** 2 + (Ed[1] - mu) ** 2 + (Ed[2] - mu) ** 2) / 3)
+    a_star = ((Ed[2] - mu) / sd - (Ed[1] - mu) / sd) / (4 - 1)
+    lo = sp.select(0, pool, E, b=2, eps=0.0, alpha=float(np.float32(a_star * 0.95)), seed=1, round_=0)
+    hi = sp.select(0, pool, E, b=2, eps=0.0, alpha=float(np.float32(a_star * 1.05)), seed=1, round_=0)
+    assert lo.tolist() == [A, B] and hi.tolist() == [A, Cc]
+    # first pick: every knob value is new for every candidate (coverage 4 each) -> lowest z wins
+    # even for a huge alpha
+    big = sp.select(0, pool, E, b=1, eps=0.0, alpha=1e6, seed=1, round_=0)
+    assert big.tolist() == [A]
+
+
+def test_select_epsilon_count_is_ceil_of_the_fp32_product():
+    """P:156, Q26: ceil(eps b) random picks with eps b formed in fp32 -- eps = 0.05 gives 1 of 20,
+    4 of 64 and 5 of 100 (not 2 / 6 from ceil of the widened 0.0500000007 b)."""
+    sp = space(synth.CFG2B)
+    for b, want in ((20, 1), (64, 4), (100, 5)):
+        n_pool = 2 * b
+        idx = synth.uniform_indices(sp.size(), n_pool, seed=b)
+        E = np.random.default_rng(b).random(n_pool).astype(np.float32)
+        order = np.lexsort((idx, E))
+        got = sp.select(0, idx[order], E[order], b=b, eps=0.05, alpha=0.0, seed=3, round_=0)
+        # alpha = 0: the greedy part is the plain top (b - n_rand) of the pool
+        n_g = b - want
+        assert got[:n_g].tolist() == idx[order[:n_g]].tolist()
+        assert got[n_g] != idx[order[n_g]]          # the next one is a random pick, not the pool's next
+        assert len(got) == b
 
 
 # ---------------------------------------------------------------- refit (a9)
