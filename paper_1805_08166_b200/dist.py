@@ -40,18 +40,43 @@ def chain_workloads(base: int, count: int, n_workloads: int, device) -> torch.Te
     return (c % n_workloads).to(torch.int16)
 
 
+def pack_lists(out_idx: torch.Tensor, out_score: torch.Tensor, out_n: torch.Tensor) -> torch.Tensor:
+    """One rank's [n_w][k] top-k lists as ONE int64 buffer (so the exchange is a single collective):
+    [n_w k global indices | n_w k score bits + n_w counts as int32 pairs]."""
+    nw, k = out_idx.shape
+    tail = torch.cat([out_score.reshape(-1).view(torch.int32), out_n.reshape(-1).to(torch.int32)])
+    if tail.numel() % 2:
+        tail = torch.cat([tail, tail.new_zeros(1)])
+    return torch.cat([out_idx.reshape(-1), tail.view(torch.int64)])
+
+
+def unpack_lists(buf: torch.Tensor, nw: int, k: int):
+    """[world][L] gathered buffers -> idx [world][nw][k] int64, score float32, n [world][nw] int32."""
+    world = buf.shape[0]
+    idx = buf[:, :nw * k].contiguous().view(world, nw, k)
+    tail = buf[:, nw * k:].contiguous().view(torch.int32)
+    score = tail[:, :nw * k].contiguous().view(torch.float32).view(world, nw, k)
+    n = tail[:, nw * k:nw * k + nw].contiguous()
+    return idx, score, n
+
+
 def gather_lists(out_idx: torch.Tensor, out_score: torch.Tensor, out_n: torch.Tensor, group=None):
-    """All-gather every rank's [n_w][k] top-k lists -> [world][n_w][k] (one collective per tensor)."""
+    """All-gather every rank's [n_w][k] top-k lists -> [world][n_w][k]: the lists are packed into one
+    int64 buffer and exchanged by ONE all_gather_into_tensor (NCCL over NVLink on the GPU box)."""
     rank, ws = world()
     if ws == 1:
         return out_idx[None], out_score[None], out_n[None]
-    gi = [torch.empty_like(out_idx) for _ in range(ws)]
-    gs = [torch.empty_like(out_score) for _ in range(ws)]
-    gn = [torch.empty_like(out_n) for _ in range(ws)]
-    dist.all_gather(gi, out_idx.contiguous(), group=group)
-    dist.all_gather(gs, out_score.contiguous(), group=group)
-    dist.all_gather(gn, out_n.contiguous(), group=group)
-    return torch.stack(gi), torch.stack(gs), torch.stack(gn)
+    nw, k = out_idx.shape
+    mine = pack_lists(out_idx, out_score, out_n)
+    allb = torch.empty(ws * mine.numel(), dtype=torch.int64, device=mine.device)
+    dist.all_gather_into_tensor(allb, mine, group=group)
+    return unpack_lists(allb.view(ws, -1), nw, k)
+
+
+def strong_slice(n_total: int, rank: int, world_size: int):
+    """Strong scaling: global chain ids [base, base + count) of this rank, contiguous."""
+    b, e = sample_slice(n_total, rank, world_size)
+    return b, e - b
 
 
 def make_allreduce(group=None):

@@ -90,6 +90,22 @@ def test_two_rank_topk_and_allreduce_equal_single_rank():
     assert [o[3] for o in out] == [(0, 501), (501, 1001)]
 
 
+def test_pack_unpack_roundtrip():
+    """The packed exchange buffer (one collective per round) carries indices, score bits (incl. -0.0,
+    inf) and counts unchanged, for even and odd n_w k."""
+    for nw, k in ((12, 128), (1, 3), (3, 5)):
+        g = np.random.default_rng(nw * k)
+        idx = torch.from_numpy(g.integers(0, 2 ** 62, size=(nw, k)).astype(np.int64))
+        sc = torch.from_numpy(g.standard_normal((nw, k)).astype(np.float32))
+        sc[0, 0] = -0.0
+        sc[-1, -1] = float("inf")
+        n = torch.from_numpy(g.integers(0, k + 1, size=nw).astype(np.int32))
+        buf = D.pack_lists(idx, sc, n)
+        i2, s2, n2 = D.unpack_lists(torch.stack([buf, buf]), nw, k)
+        assert torch.equal(i2[1], idx) and torch.equal(s2[0].view(torch.int32), sc.view(torch.int32))
+        assert torch.equal(n2[1], n)
+
+
 def test_partitions_cover_exactly():
     for n in (0, 1, 7, 1000, 100001):
         for ws in (1, 2, 3, 8):
@@ -97,5 +113,7 @@ def test_partitions_cover_exactly():
             assert sl[0][0] == 0 and sl[-1][1] == n
             assert all(sl[i][1] == sl[i + 1][0] for i in range(ws - 1))
     assert D.chain_slice(4096, 3) == (12288, 4096)
+    assert [D.strong_slice(65536, r, 8) for r in (0, 7)] == [(0, 8192), (57344, 8192)]
+    assert sum(D.strong_slice(65537, r, 3)[1] for r in range(3)) == 65537
     cw = D.chain_workloads(12, 13, 12, "cpu")
     assert cw.tolist() == [c % 12 for c in range(12, 25)]
