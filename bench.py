@@ -443,6 +443,16 @@ def other_configs(dev, stream, peaks):
     kg = torch.from_numpy(key.view(np.int16)).to(dev)
     ms = _events(stream, lambda: at.gbt_fit_hist(X, n, cost, kg, n_trees=100, depth=6), reps=3, warm=1)
     out["cfg4_refit"] = {"samples": n, "trees": 100, "depth": 6, "ms": round(ms, 2), "ms_per_tree": round(ms / 100, 3)}
+    # the multi-rank refit's per-rank compute: rank 0's work at R ranks (histograms over its 1/R sample slice,
+    # everything else replicated) with the exchange replaced by a no-op -- the numbers exclude communication
+    from paper_1805_08166_b200 import dist as D
+    per_rank = {}
+    for R in (2, 4, 8):
+        hr = D.sample_slice(n, 0, R)
+        per_rank[str(R)] = round(_events(stream, lambda: at.gbt_fit_hist(X, n, cost, kg, n_trees=100, depth=6,
+                                                                         hist_range=hr, allreduce=lambda t: None),
+                                         reps=2, warm=1), 2)
+    out["cfg4_refit"]["per_rank_ms_no_exchange"] = per_rank
     del X
     # config 5: 10^7 candidates (a n + c) mod |S_union| x 2000-tree d8, in chunks of 2^24 (features -> GBT)
     sp5 = at.Space(synth.ALL_RESNET)

@@ -357,7 +357,11 @@ def gbt_fit_hist(X, n, cost, group_key, *, n_trees=100, depth=6, max_bins=256, g
         def _cb(ptr, count, ctx, strm):
             try:
                 buf = _view_i64(ptr, count, X.device)
-                allreduce(buf)
+                # stream-ordered: the collective runs after the histogram kernels the library enqueued on
+                # its stream, and the library's next kernels on that stream run after it
+                st = torch.cuda.ExternalStream(strm, device=X.device) if strm else torch.cuda.default_stream(X.device)
+                with torch.cuda.stream(st):
+                    allreduce(buf)
                 return 0
             except Exception as e:  # noqa: BLE001 - reported through the status code
                 print("allreduce callback failed:", e, flush=True)

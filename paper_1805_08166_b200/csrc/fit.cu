@@ -905,7 +905,7 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
                                                              const int32_t *__restrict__ rowbase,
                                                              const int32_t *__restrict__ gbase,
                                                              const int32_t *__restrict__ nbk, int TB,
-                                                             int64_t *__restrict__ hist)
+                                                             int64_t *__restrict__ hist, int hb, int he)
 {
     extern __shared__ uint32_t sm[];
     if ((int)blockIdx.x >= *n_items) return;
@@ -929,11 +929,18 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
     const uint8_t *rows = binsR + R.byte_off + 4 * lane;
     for (int t0 = 0; it.y + warp + NW * t0 < it.z; t0 += 32) {
         const int pl = it.y + warp + NW * (t0 + lane);
-        const bool okl = pl < it.z;
-        const int il = okl ? (perm ? perm[pl] : pl) : 0;
+        const bool inseg = pl < it.z;
+        const int ip = inseg ? (perm ? perm[pl] : pl) : 0;
+        // multi-rank: this rank histograms only its own sample slice [hb, he) (the rest is all-reduced)
+        const bool okp = inseg && ip >= hb && ip < he;
+        const unsigned okm = __ballot_sync(0xFFFFFFFFu, okp);
+        const int cnt = (int)__popc(okm);
+        // compact the valid lanes to the front (lane k takes the k-th valid lane's sample)
+        const int src = lane < cnt ? (int)__fns(okm, 0u, lane + 1) : 0;
+        const int il = __shfl_sync(0xFFFFFFFFu, ip, src);
+        const bool okl = lane < cnt;
         const unsigned long long gvl = okl ? (unsigned long long)g[il] : 0ull;
         const unsigned long long hvl = okl ? (unsigned long long)h[il] : 0ull;
-        const int cnt = (int)__popc(__ballot_sync(0xFFFFFFFFu, okl));
         uint32_t w[SUB_NQW], wn[SUB_NQW];
         {
             const uint32_t *row = (const uint32_t *)(rows + (int64_t)__shfl_sync(0xFFFFFFFFu, il, 0) * FsP);
@@ -1004,16 +1011,17 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
 }
 
 // root items: chunks of [0, n) for node slot 0
-__global__ void sub_root_items_kernel(int n, int target, int4 *__restrict__ items, int32_t *__restrict__ n_items)
+__global__ void sub_root_items_kernel(int hb, int he, int target, int4 *__restrict__ items, int32_t *__restrict__ n_items)
 {
+    const int n = he - hb;   // this rank's samples (all of them on one rank)
     const int ch = max(64, (n + target - 1) / target);
     const int m = (n + ch - 1) / ch;
-    for (int b = threadIdx.x; b < m; b += blockDim.x) items[b] = make_int4(0, b * ch, min(n, (b + 1) * ch), 0);
+    for (int b = threadIdx.x; b < m; b += blockDim.x) items[b] = make_int4(0, hb + b * ch, hb + min(n, (b + 1) * ch), 0);
     if (threadIdx.x == 0) *n_items = m;
 }
 
 // root totals from the cells of the first splittable feature (its bins partition the samples),
-// the root segment, and (parity hook) the single cell of every constant feature
+// the root segment (this rank's n own samples), and (parity hook) the single cell of every constant feature
 __global__ void sub_root_tot_kernel(int64_t *__restrict__ hist, const int32_t *__restrict__ boff,
                                     const int32_t *__restrict__ flist, int F, int n, int fill_const,
                                     int64_t *__restrict__ tot, int32_t *__restrict__ seg_start,
@@ -1204,7 +1212,8 @@ __global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restric
 __device__ __forceinline__ void sub_worklist(int first, int nn, const int32_t *__restrict__ split_f,
                                              int32_t *__restrict__ cursor, int32_t *__restrict__ seg_start,
                                     int32_t *__restrict__ seg_cnt, int target, int4 *__restrict__ items,
-                                    int32_t *__restrict__ n_items, int4 *__restrict__ subs, int32_t *__restrict__ n_subs)
+                                    int32_t *__restrict__ n_items, int4 *__restrict__ subs, int32_t *__restrict__ n_subs,
+                                    int compact, const int64_t *__restrict__ tot)
 {
     __shared__ int s_cs[128], s_m0[129], s_s0[129], s_ch;
     const int q = threadIdx.x;
@@ -1220,9 +1229,13 @@ __device__ __forceinline__ void sub_worklist(int first, int nn, const int32_t *_
         seg_start[2 * nd + 2] = s0 + L;
         seg_cnt[2 * nd + 2] = Rc;
         alive = split_f[nd] >= 0;
-        small = L <= Rc ? 2 * nd + 1 : 2 * nd + 2;
-        st = L <= Rc ? s0 : s0 + L;
-        cs = L <= Rc ? L : Rc;
+        // the child to histogram: the one with fewer samples; with R ranks the counts are per rank, so the
+        // choice must come from replicated data instead -- the child with the smaller curvature sum H
+        // (global, from the all-reduced histograms), which is what the sample count stands in for
+        const bool left = compact ? tot[2 * (2 * nd + 1) + 1] <= tot[2 * (2 * nd + 2) + 1] : L <= Rc;
+        small = left ? 2 * nd + 1 : 2 * nd + 2;
+        st = left ? s0 : s0 + L;
+        cs = left ? L : Rc;
         s_cs[q] = alive ? cs : 0;
     }
     __syncthreads();
@@ -1247,7 +1260,10 @@ __device__ __forceinline__ void sub_worklist(int first, int nn, const int32_t *_
         const int ch = s_ch;
         int m = s_m0[q];
         subs[s_s0[q]] = make_int4(q, small - cfirst, big - cfirst, 0);
-        for (int o = 0; o < cs; o += ch) items[m++] = make_int4(small - cfirst, st + o, st + min(cs, o + ch), 0);
+        // compact (multi-rank): the smaller child of parent q goes to slot q of a dense [nn] buffer, the
+        // one that is all-reduced; else straight to its child slot
+        const int slot = compact ? q : small - cfirst;
+        for (int o = 0; o < cs; o += ch) items[m++] = make_int4(slot, st + o, st + min(cs, o + ch), 0);
     }
 }
 
@@ -1262,7 +1278,8 @@ __global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restr
                                                           int32_t *__restrict__ cursor, int32_t *__restrict__ node,
                                                           int32_t *__restrict__ perm, int target, int4 *__restrict__ items,
                                                           int32_t *__restrict__ n_items, int4 *__restrict__ subs,
-                                                          int32_t *__restrict__ n_subs, unsigned *__restrict__ done)
+                                                          int32_t *__restrict__ n_subs, unsigned *__restrict__ done,
+                                                          int compact, int64_t *__restrict__ tot, int hb, int he)
 {
     __shared__ int sc[256], sbase[256];
     const int tid = threadIdx.x;
@@ -1270,20 +1287,23 @@ __global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restr
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
     const bool ok = i < n;
+    // every sample moves to its child (the partition is replicated on all ranks); positions are kept for
+    // this rank's own samples [hb, he) only -- the ones it histograms
+    const bool own = ok && i >= hb && i < he;
     int nd = 0, slot = 0, r = 0, right = 0;
     if (ok) {
         nd = node[i];
         const int sf = split_f[nd];
         right = (sf >= 0 && (int)bins[(int64_t)sf * n + i] >= split_s[nd]) ? 1 : 0;
         slot = (nd - first) * 2 + right;
-        r = atomicAdd(&sc[slot], 1);
+        if (own) r = atomicAdd(&sc[slot], 1);
     }
     __syncthreads();
     for (int q = tid; q < 2 * nn; q += blockDim.x)
         if (sc[q]) sbase[q] = atomicAdd(&cursor[q], sc[q]);
     __syncthreads();
-    if (ok) {
-        node[i] = 2 * nd + 1 + right;
+    if (ok) node[i] = 2 * nd + 1 + right;
+    if (own) {
         const int o = sbase[slot] + r;
         perm[right ? seg_start[nd] + seg_cnt[nd] - 1 - o : seg_start[nd] + o] = (int32_t)i;
     }
@@ -1295,7 +1315,7 @@ __global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restr
     if (!s_last) return;
     __threadfence();
     sub_worklist(first, nn, split_f, cursor, seg_start, seg_cnt, target, items, n_items, subs,
-                 n_subs);
+                 n_subs, compact, tot);
     if (tid == 0) *done = 0u;
 }
 
@@ -1308,6 +1328,22 @@ __global__ void sub_subtract_kernel(const int64_t *__restrict__ parent, int64_t 
     const int64_t m = 2 * (int64_t)TB;
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x)
         child[s.z * m + c] = parent[s.x * m + c] - child[s.y * m + c];
+}
+
+// multi-rank: the all-reduced smaller children (dense slot q) -> both children: small = reduced,
+// large = parent - small (exact int64)
+__global__ void sub_expand_kernel(const int64_t *__restrict__ parent, const int64_t *__restrict__ small,
+                                  int64_t *__restrict__ child, int TB, const int4 *__restrict__ subs,
+                                  const int32_t *__restrict__ n_subs)
+{
+    if ((int)blockIdx.y >= *n_subs) return;
+    const int4 s = subs[blockIdx.y];
+    const int64_t m = 2 * (int64_t)TB;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = small[s.x * m + c];
+        child[s.y * m + c] = v;
+        child[s.z * m + c] = parent[s.x * m + c] - v;
+    }
 }
 
 // last level: every sample's leaf, prediction update in tree order
@@ -2332,9 +2368,13 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         return AT_OK;
     };
 
-    // single rank, larger n: histogram subtraction over node-contiguous positions (section 3b)
+    // larger n: histogram subtraction over node-contiguous positions (section 3b).  With R ranks every
+    // rank keeps the whole (replicated) partition and builds the smaller children's histograms over its
+    // own sample slice [hb, he) only; one int64 all-reduce per level (the dense smaller-children buffer,
+    // sized by the actual cut counts TB) makes them global, so every decision is replicated exactly.
     const char *sub_e = getenv("AT_FIT_SUB");   // "0" forces the plain level-by-level path
-    if ((!sub_e || atoi(sub_e) != 0) && !o->allreduce && n_split > 0) {
+    const bool multi = o->allreduce != nullptr;
+    if ((!sub_e || atoi(sub_e) != 0) && n_split > 0 && (!multi || n > FUSED_NMAX)) {
         // compact splittable features and the feature ranges whose bank columns fit a block's rows
         std::vector<int32_t> boff_h(F + 1), flist_h;
         for (int f = 0; f < F; ++f) {
@@ -2398,6 +2438,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             int64_t *tot = ws.get<int64_t>(2 * (size_t)(n_int + n_leaf));
             int64_t *hA = ws.get<int64_t>((size_t)max_nn * TB * 2);
             int64_t *hB = ws.get<int64_t>((size_t)max_nn * TB * 2);
+            int64_t *hS = multi ? ws.get<int64_t>((size_t)max_nn * TB * 2) : nullptr;   // dense smaller children
             // split entries: (feature, 32-split chunk), features ascending, chunks ascending
             std::vector<int32_t> ent_h;
             for (int k = 0; k < Fs; ++k) {
@@ -2443,7 +2484,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * max_nn, s));
             AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
             AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
-            sub_root_items_kernel<<<1, 256, 0, s>>>((int)n, target, root_items, root_n);
+            sub_root_items_kernel<<<1, 256, 0, s>>>((int)hb, (int)he, target, root_items, root_n);
             note_launch();
             auto enqueue_sub = [&](cudaStream_t s) -> int {
                 {
@@ -2466,10 +2507,14 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                     ProfScope ps(AT_K_FIT_HIST, s);
                     AT_CUDA_TRY(cudaMemsetAsync(hp, 0, sizeof(int64_t) * 2 * (size_t)TB, s));
                     sub_hist_kernel<<<dim3(max_items, NR), SUB_NT, hsm, s>>>(binsR, FsP, nullptr, g, h, root_items, root_n,
-                                                                             d_rng, d_rowbase, d_gbase, d_nbk, TB, hp);
+                                                                             d_rng, d_rowbase, d_gbase, d_nbk, TB, hp,
+                                                                             (int)hb, (int)he);
                     note_launch();
+                    AT_LAUNCH_CHECK("root histogram");
+                    if (multi && o->allreduce(hp, 2 * (int64_t)TB, o->ctx, stream))
+                        return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
                     const int want_h0 = o->d_hist0_out != nullptr;
-                    sub_root_tot_kernel<<<1, 256, 0, s>>>(hp, boff, flist, F, (int)n, want_h0, tot, seg_start, seg_cnt,
+                    sub_root_tot_kernel<<<1, 256, 0, s>>>(hp, boff, flist, F, (int)(he - hb), want_h0, tot, seg_start, seg_cnt,
                                                           d_tree); note_launch();
                     if (want_h0) {
                         hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hp, boff, F, B, o->d_hist0_out,
@@ -2493,15 +2538,39 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                         ProfScope ps(AT_K_FIT_SPLIT, s);
                         sub_scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, first, nn, seg_start,
                                                                         seg_cnt, cursor, node, perm, target, items, cnts,
-                                                                        subs, cnts + 1, done + 1);
+                                                                        subs, cnts + 1, done + 1, multi ? 1 : 0, tot,
+                                                                        (int)hb, (int)he);
                         note_launch();
                         AT_LAUNCH_CHECK("scatter");
+                    }
+                    if (multi) {
+                        {
+                            ProfScope ps(AT_K_FIT_HIST, s);
+                            AT_CUDA_TRY(cudaMemsetAsync(hS, 0, sizeof(int64_t) * 2 * (size_t)TB * nn, s));
+                            sub_hist_kernel<<<dim3(target + nn, NR), SUB_NT, hsm, s>>>(binsR, FsP, perm, g, h, items, cnts,
+                                                                                      d_rng, d_rowbase, d_gbase, d_nbk, TB,
+                                                                                      hS, (int)hb, (int)he);
+                            note_launch();
+                            AT_LAUNCH_CHECK("histograms");
+                        }
+                        if (o->allreduce(hS, 2 * (int64_t)TB * nn, o->ctx, stream))
+                            return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
+                        {
+                            ProfScope ps(AT_K_FIT_HIST, s);
+                            sub_expand_kernel<<<dim3(std::min<unsigned>(nblk(2 * (int64_t)TB, 256), 64), nn), 256, 0, s>>>(
+                                hp, hS, hc, TB, subs, cnts + 1);
+                            note_launch();
+                            AT_LAUNCH_CHECK("expand");
+                        }
+                        std::swap(hp, hc);
+                        continue;
                     }
                     {
                         ProfScope ps(AT_K_FIT_HIST, s);
                         AT_CUDA_TRY(cudaMemsetAsync(hc, 0, sizeof(int64_t) * 2 * (size_t)TB * 2 * nn, s));
                         sub_hist_kernel<<<dim3(target + nn, NR), SUB_NT, hsm, s>>>(binsR, FsP, perm, g, h, items, cnts,
-                                                                                  d_rng, d_rowbase, d_gbase, d_nbk, TB, hc);
+                                                                                  d_rng, d_rowbase, d_gbase, d_nbk, TB, hc,
+                                                                                  0, (int)n);
                         note_launch();
                         sub_subtract_kernel<<<dim3(std::min<unsigned>(nblk(2 * (int64_t)TB, 256), 64), nn), 256, 0, s>>>(
                             hp, hc, TB, subs, cnts + 1);
@@ -2524,8 +2593,15 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                 }
                 return AT_OK;
             };
-            const int rc = run_captured(enqueue_sub, o->n_trees);
-            if (rc) return rc;
+            if (multi) {   // host callbacks between levels: enqueued tree by tree (the tree index is on the device)
+                for (int t = 0; t < o->n_trees; ++t) {
+                    const int rc = enqueue_sub(s);
+                    if (rc) return rc;
+                }
+            } else {
+                const int rc = run_captured(enqueue_sub, o->n_trees);
+                if (rc) return rc;
+            }
             return finish();
         }
     }

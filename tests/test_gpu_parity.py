@@ -494,6 +494,72 @@ def test_fit_rank_invariance_two_emulated_ranks(at):
             assert_bits_equal(ex[k], single[k], f"rank {r} {k}")
 
 
+def _emulated_ranks(at, R, Xg, n, cg, kg, **kw):
+    """R ranks as R host threads + R streams on one GPU: each fits over its sample slice; the all-reduce is a
+    host barrier + a device sum (no kernel ever waits on another rank's kernel)."""
+    import threading
+    from paper_1805_08166_b200 import dist as D
+    bar = threading.Barrier(R)
+    bufs = [None] * R
+    streams = [torch.cuda.Stream() for _ in range(R)]
+    out = [None] * R
+    err = []
+
+    def make_ar(r):
+        def ar(t):
+            torch.cuda.current_stream().synchronize()
+            bufs[r] = t
+            bar.wait()
+            if r == 0:
+                s = bufs[0].clone()
+                for q in range(1, R):
+                    s += bufs[q]
+                for q in range(R):
+                    bufs[q].copy_(s)
+                torch.cuda.synchronize()
+            bar.wait()
+        return ar
+
+    def run(r):
+        try:
+            with torch.cuda.stream(streams[r]):
+                out[r] = at.gbt_fit_hist(Xg, n, cg, kg, hist_range=D.sample_slice(n, r, R), allreduce=make_ar(r),
+                                         stream=streams[r], **kw)
+                streams[r].synchronize()
+        except Exception as e:   # noqa: BLE001
+            err.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(R)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert not err, err
+    return out
+
+
+@pytest.mark.parametrize("n,R,trees,depth,nw", [(100000, 2, 3, 6, 9), (5000, 3, 4, 5, 3)])
+def test_fit_subtraction_path_rank_invariance(at, n, R, trees, depth, nw):
+    """Eq. 2: the multi-rank subtraction path -- every rank builds the smaller
+    children's histograms over its own sample slice, one int64 all-reduce per level -- gives the
+    bit-identical ensemble of the single-rank fit (emulated ranks, n > 2048)."""
+    wls = synth.ALL_DW[:nw]
+    sp = at.Space(wls)
+    key = synth.group_keys(n, nw, seed=n)
+    sizes = np.array([sp.size(w) for w in range(nw)], dtype=np.uint64)
+    loc = synth.uniform_indices(1 << 62, n, seed=n + 1) % sizes[key]
+    idx = loc + np.array(sp.offsets[:nw], dtype=np.uint64)[key]
+    Xg = sp.features(u64(idx))
+    c = synth.labels(Xg[:, :n].T.cpu().numpy(), seed=n + 2)
+    cg, kg = dev(c), dev(key.view(np.int16))
+    single = at.gbt_fit_hist(Xg, n, cg, kg, n_trees=trees, depth=depth).export()
+    torch.cuda.synchronize()
+    out = _emulated_ranks(at, R, Xg, n, cg, kg, n_trees=trees, depth=depth)
+    for r in range(R):
+        ex = out[r].export()
+        for k in ("feat", "thresh", "leaf"):
+            assert_bits_equal(ex[k], single[k], f"rank {r} {k}")
+
+
 FIT_PATHS = {"fused": {"AT_FIT_FUSED": "1"},                          # single launch (n <= 2048)
              "subtraction": {"AT_FIT_FUSED": "0"},                   # default above 2048
              "level-by-level": {"AT_FIT_FUSED": "0", "AT_FIT_SUB": "0"}}
