@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libautotvm_b200.so"
+LIB_PATH = PKG / "libautotvm_b200.so"   # tools may point this at an instrumented build before the first call
 NFEAT = 468
 
 AT_K = dict(features=0, predict=1, sa=2, topk=3, select=4, fit_prep=5, fit_grad=6, fit_hist=7, fit_split=8,

@@ -34,26 +34,30 @@ def _stale(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OBJ.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), lib: Path = None) -> Path:
+    """defines: extra -D flags for an instrumented variant (e.g. AT_SA_PHASE_TIMING), built into its own
+    object directory and `lib` path (tools only; the product library is the default build)."""
+    lib = LIB if lib is None else Path(lib)
+    obj = OBJ if not defines else OBJ.parent / ("obj_" + "_".join(d.lstrip("-D").lower() for d in defines))
+    obj.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "at_b200.h"]
     objs = []
     for src in SOURCES:
         s = CSRC / src
-        o = OBJ / (s.stem + ".o")
+        o = obj / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s, *headers, Path(__file__)]):
-            cmd = [NVCC, *FLAGS, "-c", str(s), "-o", str(o)]
+            cmd = [NVCC, *FLAGS, *defines, "-c", str(s), "-o", str(o)]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
                 print(" ".join(cmd), flush=True)
             subprocess.check_call(cmd)
-    if force or _stale(LIB, objs):
-        tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+    if force or _stale(lib, objs):
+        tmp = lib.with_suffix(f".so.tmp{os.getpid()}")
         subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp),
                                *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -423,7 +423,7 @@ __device__ __forceinline__ void sa_row(const WlDev &W, const SaLowering &L, int 
 // the extents of every loop of template TMPL for knob vector ch (one factor-table load per loop)
 template <int TMPL>
 __device__ __forceinline__ void sa_extents(const uint32_t (&foff)[6], const uint16_t *__restrict__ fact,
-                                           const uint32_t *ch, uint32_t *ext /* [MAXLOOPS][32] at the lane */)
+                                           const uint32_t *ch, uint16_t *ext /* [MAXLOOPS][32] at the lane */)
 {
     constexpr int NL = Tmpl<TMPL>::NL;
     const uint32_t p = TMPL == 1 ? ch[6] : TMPL == 2 ? ch[5] : 0u;
@@ -442,11 +442,11 @@ __device__ __forceinline__ void sa_extents(const uint32_t (&foff)[6], const uint
         ev[l] = __ldg(fact + fo + cha * (uint32_t)Lv + level);
     }
 #pragma unroll
-    for (int l = 0; l < NL; ++l) ext[l * 32] = ev[l];
+    for (int l = 0; l < NL; ++l) ext[l * 32] = (uint16_t)ev[l];   // factors are u16 (space tables)
 }
 
 template <int TMPL>
-__device__ __forceinline__ void sa_row_rel(const WlDev &W, const uint32_t *ext /* [l * 32] at the lane */,
+__device__ __forceinline__ void sa_row_rel(const WlDev &W, const uint16_t *ext /* [l * 32] at the lane */,
                                            const uint32_t *ch, int k, int lane, float *tile)
 {
     constexpr int NL = Tmpl<TMPL>::NL;

@@ -14,7 +14,7 @@ namespace at {
 
 constexpr int PRED_NW = 16;  // warps per block (tree slices); 32 candidates per tile
 
-TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes, bool rank)
+TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes, bool rank, int nbuf, int ring, int leaf_global)
 {
     TreeGeo G{};
     G.nodes = rank ? (const uint8_t *)g->d_rk_nodes : (const uint8_t *)g->d_nodes;
@@ -25,7 +25,8 @@ TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes, bool rank)
     G.D = g->depth;
     G.ni = (1 << g->depth) - 1;
     G.nl = 1 << g->depth;
-    const uint32_t per_tree = (uint32_t)G.ni * (uint32_t)G.nbytes + (uint32_t)G.nl * 4u;
+    const uint32_t per_tree = (uint32_t)G.ni * (uint32_t)G.nbytes + (leaf_global ? 0u : (uint32_t)G.nl * 4u);
+    G.leaf_global = leaf_global;
     int ch = (int)(buf_bytes / per_tree) / 2 * 2;   // even: chunk offsets and sizes stay 16-B aligned
     if (ch >= 32) ch = ch / 32 * 32;                 // whole 32-tree rounds: no idle walk slots
     if (ch < 2) ch = 2;
@@ -33,7 +34,9 @@ TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes, bool rank)
     G.CH = ch;
     G.NC = (G.T + ch - 1) / ch;
     G.chunk_bytes = (uint32_t)ch * per_tree;
-    G.resident = G.NC <= 2;
+    G.NBUF = nbuf;
+    G.ring = ring;
+    G.resident = G.NC <= nbuf;
     G.Tm = G.T;
     return G;
 }
@@ -119,7 +122,8 @@ __global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, flo
                     tl[g * tile_rows * 32 + f * 32 + lane] = ok[g] ? X[(int64_t)f * ld + cand0 + 32 * g] : (T)0;
             __syncthreads();
         }
-        walk_pass<PRED_NW, GRP, KM, RK>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part, slots,
+        walk_pass<PRED_NW, GRP, KM, RK>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part,
+                                        KM * 1024, slots,
                                     n, cand0, ok);
         if (KM == 1) {
             if (warp < GRP) {

@@ -27,35 +27,62 @@ struct TreeGeo {
     int CH;                 // trees per chunk (even: 16-B aligned bulk copies)
     int NC;                 // chunks per pass
     uint32_t chunk_bytes;   // CH * (ni * nbytes + nl * 4)
-    int resident;           // NC <= 2: loaded once, never re-streamed
+    int resident;           // NC <= NBUF: loaded once, never re-streamed
     int Tm;                 // trees per model (KM > 1: K equal models concatenated, gbt_predict_acq)
+    int NBUF;               // chunk buffers (2: double buffering; up to TS_MAXBUF in ring mode)
+    int ring;               // 0: a block barrier after every chunk; 1: no block barrier -- per-buffer
+                            // consumption counters, the last warp done with a chunk refills its buffer
+    int leaf_global;        // 1: chunks carry the nodes only; a walk's leaf is read from global memory
+                            // (L2) and added one batch later (walk_batch<..., LG>), so the tree buffers
+                            // hold 1.5x the trees of a depth-8 ensemble
 };
+constexpr int TS_MAXBUF = 4;
 
 constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // default per buffer (two buffers)
-TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes = TREE_BUF_BYTES, bool rank = false);
+#ifdef AT_SA_PHASE_TIMING
+__shared__ unsigned long long s_walk_prof[3 * 17];   // instrumented builds only (tools/sa_phases.py)
+#endif
+TreeGeo make_geo(const at_gbt_s *g, uint32_t buf_bytes = TREE_BUF_BYTES, bool rank = false, int nbuf = 2, int ring = 0,
+                 int leaf_global = 0);
+
+// leaves of the last walked batch, in flight from global memory (LG mode): added to the partial sums
+// when the next batch is done, before its own leaves -- ascending t per residue class, as in Q19
+template <int GRP, int NBMAX>
+struct LeafPend {
+    float v[GRP][NBMAX];
+    int j[NBMAX];
+    int n;
+};
 
 __device__ __forceinline__ void ts_issue(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint64_t c)
 {
-    const int k = (int)(c % (uint64_t)G.NC);
-    const int b = (int)(c & 1);
+    const int k = (int)((uint32_t)c % (uint32_t)G.NC);     // (32-bit: a 64-bit modulo is ~100 cycles)
+    const int b = (int)((uint32_t)c % (uint32_t)G.NBUF);
     const int t0 = k * G.CH;
     const int nt = min(G.CH, G.T_pad - t0);
     const uint32_t nb = (uint32_t)nt * G.ni * (uint32_t)G.nbytes, lb = (uint32_t)nt * G.nl * 4u;
     uint8_t *dst = bufs + (size_t)b * G.chunk_bytes;
+    if (G.leaf_global) {
+        mbar_arrive_expect_tx(&bar[b], nb);
+        bulk_g2s(dst, G.nodes + (int64_t)t0 * G.ni * G.nbytes, nb, &bar[b]);
+        return;
+    }
     mbar_arrive_expect_tx(&bar[b], nb + lb);
     bulk_g2s(dst, G.nodes + (int64_t)t0 * G.ni * G.nbytes, nb, &bar[b]);
     bulk_g2s(dst + (size_t)G.CH * G.ni * G.nbytes, G.leaf + (int64_t)t0 * G.nl, lb, &bar[b]);
 }
 
-// thread 0: initialise both barriers and start the first two chunks of the stream
+// thread 0: initialise the NBUF barriers (and, ring mode, the consumption counters that follow them
+// in `bar`) and start the first NBUF chunks of the stream
 __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64_t *bar)
 {
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int b = 0; b < G.NBUF; ++b) {
+            mbar_init(&bar[b], 1);
+            if (G.ring) ((unsigned *)(bar + G.NBUF))[b] = 0u;
+        }
         fence_proxy_async();
-        ts_issue(G, bufs, bar, 0);
-        if (G.NC > 1) ts_issue(G, bufs, bar, 1);
+        for (int b = 0; b < G.NBUF && b < G.NC; ++b) ts_issue(G, bufs, bar, (uint64_t)b);
     }
 }
 
@@ -63,11 +90,11 @@ __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64
 // GRP candidate groups at once: NB * GRP independent dependency chains.  RK: rank form -- 4-byte
 // nodes {k | tile byte offset of the feature << 16}, tiles of u16 feature ranks in pairs,
 // x < theta <=> rank < k.
-template <int NW, int GRP, int NB, int KM, bool RK = false>
+template <int NW, int GRP, int NB, int KM, bool RK = false, bool LG = false, int NBP = 1>
 __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf, int c0, int t0, const void *tile,
                                            int gstride, int lane, float (&p)[GRP][KM][32 / NW],
                                            uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand0,
-                                           const bool (&cand_ok)[GRP])
+                                           const bool (&cand_ok)[GRP], LeafPend<GRP, NBP> &pend)
 {
     constexpr int NQ = 32 / NW;
     constexpr uint32_t NBY = RK ? 4u : 8u;   // bytes per node
@@ -115,25 +142,49 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
             }
         }
     }
-    // leaves in ascending t: tree t adds to its residue class q = t mod 32, slot (q - warp) / NW = q / NW;
-    // with KM models of Tm trees, tree t = km Tm + u adds to model km's class u mod 32 (all trees of
-    // one (model, class) pair share t mod NW, so one warp owns it and sums it in ascending u)
+    if constexpr (LG) {
+        // the previous batch's leaves (loaded one batch ago) go first, then this batch's leaf loads are
+        // issued straight into the pending registers
 #pragma unroll
-    for (int jj = 0; jj < NB; ++jj) {
-        const int t = t0 + jj * NW;
-        int km = 0, u = t;
-        if (KM > 1) { km = t / G.Tm; u = t - km * G.Tm; }
-        const int j = (u & 31) / NW;
+        for (int jj = 0; jj < NBP; ++jj)
+            if (jj < pend.n)
 #pragma unroll
-        for (int g = 0; g < GRP; ++g) {
-            const int slot = (int)((a[g][jj] + add_l[jj]) >> (RK ? 2 : 3)) - nl;   // h = (a - tb) / NBY in [2^D, 2^(D+1))
-            const float lv = leaves[(t - c0) * nl + slot];
+                for (int g = 0; g < GRP; ++g)
 #pragma unroll
-            for (int m = 0; m < KM; ++m)
+                    for (int q = 0; q < NQ; ++q)
+                        if (q == pend.j[jj]) p[g][0][q] = __fadd_rn(p[g][0][q], pend.v[g][jj]);
 #pragma unroll
-                for (int q = 0; q < NQ; ++q)
-                    if (m == km && q == j) p[g][m][q] = __fadd_rn(p[g][m][q], lv);
-            if (slots && cand_ok[g]) slots[(int64_t)t * slot_ld + cand0 + 32 * g] = (uint8_t)slot;
+        for (int jj = 0; jj < NB; ++jj) {
+            const int t = t0 + jj * NW;
+            pend.j[jj] = (t & 31) / NW;
+#pragma unroll
+            for (int g = 0; g < GRP; ++g) {
+                const int slot = (int)((a[g][jj] + add_l[jj]) >> (RK ? 2 : 3)) - nl;
+                pend.v[g][jj] = __ldg(G.leaf + (int64_t)t * nl + slot);
+            }
+        }
+        pend.n = NB;
+    } else {
+        // leaves in ascending t: tree t adds to its residue class q = t mod 32, slot (q - warp) / NW = q / NW;
+        // with KM models of Tm trees, tree t = km Tm + u adds to model km's class u mod 32 (all trees of
+        // one (model, class) pair share t mod NW, so one warp owns it and sums it in ascending u)
+#pragma unroll
+        for (int jj = 0; jj < NB; ++jj) {
+            const int t = t0 + jj * NW;
+            int km = 0, u = t;
+            if (KM > 1) { km = t / G.Tm; u = t - km * G.Tm; }
+            const int j = (u & 31) / NW;
+#pragma unroll
+            for (int g = 0; g < GRP; ++g) {
+                const int slot = (int)((a[g][jj] + add_l[jj]) >> (RK ? 2 : 3)) - nl;   // h = (a - tb) / NBY in [2^D, 2^(D+1))
+                const float lv = leaves[(t - c0) * nl + slot];
+#pragma unroll
+                for (int m = 0; m < KM; ++m)
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        if (m == km && q == j) p[g][m][q] = __fadd_rn(p[g][m][q], lv);
+                if (slots && cand_ok[g]) slots[(int64_t)t * slot_ld + cand0 + 32 * g] = (uint8_t)slot;
+            }
         }
     }
 }
@@ -142,40 +193,51 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
 // in ascending order, in batches of up to 4 / GRP trees; no walk slot is spent on an absent tree,
 // whatever the chunk size.  GRP candidate groups of 32 (group g's tile at tile + g * gstride floats)
 // share every staged tree byte.
-template <int NW, int GRP, int KM, bool RK = false>
+template <int GRP, int KM>
+constexpr int walk_nbmax() { return GRP == 1 ? (KM == 1 ? 6 : 4) : 2; }
+
+template <int NW, int GRP, int KM, bool RK = false, bool LG = false>
 __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const void *tile, int gstride,
                                            int lane, int warp, float (&p)[GRP][KM][32 / NW], uint8_t *__restrict__ slots,
-                                           int64_t slot_ld, int64_t cand0, const bool (&cand_ok)[GRP])
+                                           int64_t slot_ld, int64_t cand0, const bool (&cand_ok)[GRP],
+                                           LeafPend<GRP, walk_nbmax<GRP, KM>()> &pend)
 {
-    constexpr int NBMAX = GRP == 1 ? (KM == 1 ? 6 : 4) : 2;
+    constexpr int NBMAX = walk_nbmax<GRP, KM>();
     const int c0 = k * G.CH;
     const int c1 = min(c0 + G.CH, G.T);
     int t0 = c0 + ((warp - c0) % NW + NW) % NW;
     for (; t0 + (NBMAX - 1) * NW < c1; t0 += NBMAX * NW)
-        walk_batch<NW, GRP, NBMAX, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, NBMAX, KM, RK, LG, NBMAX>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok,
+                                                      pend);
     int rest = t0 < c1 ? (c1 - 1 - t0) / NW + 1 : 0;   // warp-uniform, < NBMAX
     if (NBMAX > 4 && rest >= 4) {
-        walk_batch<NW, GRP, 4, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 4, KM, RK, LG, NBMAX>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok,
+                                                      pend);
         t0 += 4 * NW;
         rest -= 4;
     }
     if (NBMAX >= 4 && rest == 3)
-        walk_batch<NW, GRP, 3, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 3, KM, RK, LG, NBMAX>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok,
+                                                      pend);
     else if (rest >= 2)
-        walk_batch<NW, GRP, 2, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 2, KM, RK, LG, NBMAX>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok,
+                                                      pend);
     else if (rest == 1)
-        walk_batch<NW, GRP, 1, KM, RK>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok);
+        walk_batch<NW, GRP, 1, KM, RK, LG, NBMAX>(G, buf, c0, t0, tile, gstride, lane, p, slots, slot_ld, cand0, cand_ok,
+                                                      pend);
 }
 
 // One full pass over the ensemble.  `c` is the block-wide stream counter (identical in every
 // thread); `c_limit` the total number of chunks the kernel will consume.  Ends with group g's
-// partials in part[g * 1024 + q * 32 + lane] (KM models: part[((g KM + m) 32 + q) 32 + lane])
+// partials in part[g * pstride + q * 32 + lane] (KM models: part[g * pstride + (m 32 + q) 32 + lane])
 // and a __syncthreads.
-template <int NW, int GRP, int KM = 1, bool RK = false>
+// PW >= 0: warp PW is a producer only -- it walks nothing and issues the tree-chunk copies (the
+// issuing work, a proxy fence and two bulk copies, then never delays a walking warp)
+template <int NW, int GRP, int KM = 1, bool RK = false, bool LG = false, int PW = -1>
 __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph, uint64_t &c,
                                           uint64_t c_limit, const void *tile, int gstride, int lane, int warp,
-                                          float *part, uint8_t *__restrict__ slots, int64_t slot_ld, int64_t cand0,
-                                          const bool (&cand_ok)[GRP])
+                                          float *part, int pstride, uint8_t *__restrict__ slots, int64_t slot_ld,
+                                          int64_t cand0, const bool (&cand_ok)[GRP])
 {
     constexpr int NQ = 32 / NW;
     float p[GRP][KM][NQ];
@@ -185,32 +247,119 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
         for (int m = 0; m < KM; ++m)
 #pragma unroll
             for (int j = 0; j < NQ; ++j) p[g][m][j] = 0.0f;
+    LeafPend<GRP, walk_nbmax<GRP, KM>()> pend;
+    pend.n = 0;
+    const bool walker = PW < 0 || warp < PW;
     if (G.resident) {
-        for (int k = 0; k < G.NC; ++k)
-            walk_chunk<NW, GRP, KM, RK>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
-                                cand0, cand_ok);
+        for (int k = 0; k < G.NC && walker; ++k)
+            walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
+                                cand0, cand_ok, pend);
+    } else if (G.ring) {
+        // no block barrier per chunk: every warp waits for each chunk's data (so its phase bits stay
+        // exact), walks the trees of its residue class in it, and counts itself out; the last of the NW
+        // warps to leave chunk c refills that buffer with chunk c + NBUF.  Warps drift by up to NBUF - 1
+        // chunks, so one slow warp no longer stalls the other NW - 1 at every chunk.
+        unsigned *cnt = (unsigned *)(bar + G.NBUF);
+        if (!walker) {
+            // producer: chunk c's buffer is refilled with chunk c + NBUF once all NW walkers counted out
+            if (lane == 0)
+                for (int k = 0; k < G.NC; ++k, ++c) {
+                    const int b = (int)((uint32_t)c % (uint32_t)G.NBUF);
+                    const unsigned want = ((uint32_t)c / (uint32_t)G.NBUF + 1u) * (unsigned)NW;
+                    while (*(volatile unsigned *)&cnt[b] < want) {
+                    }
+                    if (c + G.NBUF < c_limit) {
+                        fence_proxy_async();
+                        ts_issue(G, bufs, bar, c + G.NBUF);
+                    }
+                }
+            else
+                c += G.NC;
+            c = __shfl_sync(0xFFFFFFFFu, c, 0);
+        } else {
+            for (int k = 0; k < G.NC; ++k, ++c) {
+                const int b = (int)((uint32_t)c % (uint32_t)G.NBUF);
+                mbar_wait(&bar[b], ph[b]);
+                ph[b] ^= 1u;
+                walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots,
+                                                slot_ld, cand0, cand_ok, pend);
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();   // this warp's reads of buffer b precede the refill
+                    if (PW >= 0) {
+                        atomicAdd(&cnt[b], 1u);
+                    } else {
+                        const unsigned old = atomicAdd(&cnt[b], 1u);
+                        if (old % NW == NW - 1 && c + G.NBUF < c_limit) {
+                            fence_proxy_async();
+                            ts_issue(G, bufs, bar, c + G.NBUF);
+                        }
+                    }
+                }
+            }
+        }
     } else {
         for (int k = 0; k < G.NC; ++k, ++c) {
             const int b = (int)(c & 1);
-            mbar_wait(&bar[b], ph[b]);
-            ph[b] ^= 1u;
-            walk_chunk<NW, GRP, KM, RK>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
-                                cand0, cand_ok);
+#ifdef AT_SA_PHASE_TIMING
+            long long q0 = clock64();
+#endif
+            if (PW < 0 || c == 0) {   // with a producer warp only the kernel's first chunk is waited for here
+                mbar_wait(&bar[b], ph[b]);
+                ph[b] ^= 1u;
+            }
+#ifdef AT_SA_PHASE_TIMING
+            long long q1 = clock64();
+#endif
+            if (walker) {
+                walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots,
+                                                slot_ld, cand0, cand_ok, pend);
+            } else if (c + 1 < c_limit) {
+                // the producer waits for the NEXT chunk before the block barrier, so the barrier itself
+                // publishes it: the walkers start it without an mbarrier wait of their own
+                const int b1 = (int)((c + 1) & 1);
+                mbar_wait(&bar[b1], ph[b1]);
+                ph[b1] ^= 1u;
+            }
+#ifdef AT_SA_PHASE_TIMING
+            long long q2 = clock64();
+#endif
             __syncthreads();   // every warp is done with buffer b
-            if (threadIdx.x == 0 && c + 2 < c_limit) {
+#ifdef AT_SA_PHASE_TIMING
+            if (lane == 0 && warp < 17) {
+                const long long q3 = clock64();
+                s_walk_prof[3 * warp] += q1 - q0;
+                s_walk_prof[3 * warp + 1] += q2 - q1;
+                s_walk_prof[3 * warp + 2] += q3 - q2;
+            }
+#endif
+            if ((PW < 0 ? threadIdx.x == 0 : (warp == PW && lane == 0)) && c + 2 < c_limit) {
                 fence_proxy_async();
                 ts_issue(G, bufs, bar, c + 2);
             }
         }
     }
+    if (LG) {   // the last batch's leaves
 #pragma unroll
-    for (int g = 0; g < GRP; ++g)
+        for (int jj = 0; jj < walk_nbmax<GRP, KM>(); ++jj)
+            if (jj < pend.n)
+#pragma unroll
+                for (int g = 0; g < GRP; ++g)
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        if (q == pend.j[jj]) p[g][0][q] = __fadd_rn(p[g][0][q], pend.v[g][jj]);
+    }
+    // a resident pass has no per-chunk barrier: every warp must be done reading the tile before the
+    // partials are written (sa_kernel keeps them in the tile's first columns)
+    if (G.resident) __syncthreads();
+#pragma unroll
+    for (int g = 0; g < GRP && walker; ++g)
 #pragma unroll
         for (int m = 0; m < KM; ++m) {
             // the warp's classes of model m: q = j NW + r, r = (warp - m Tm) mod NW
             const int r = KM == 1 ? warp : ((warp - (m * G.Tm) % NW) % NW + NW) % NW;
 #pragma unroll
-            for (int j = 0; j < NQ; ++j) part[((g * KM + m) * 32 + (r + j * NW)) * 32 + lane] = p[g][m][j];
+            for (int j = 0; j < NQ; ++j) part[g * pstride + (m * 32 + (r + j * NW)) * 32 + lane] = p[g][m][j];
         }
     __syncthreads();
 }
@@ -218,10 +367,8 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
 // resident ensembles: wait once for the initial load
 __device__ __forceinline__ void ts_wait_resident(const TreeGeo &G, uint64_t *bar)
 {
-    if (G.resident) {
-        mbar_wait(&bar[0], 0);
-        if (G.NC > 1) mbar_wait(&bar[1], 0);
-    }
+    if (G.resident)
+        for (int b = 0; b < G.NC; ++b) mbar_wait(&bar[b], 0);
 }
 
 // K bootstrap models scored at once (gbt_predict_acq): per-model canonical sums, then the acquisition

@@ -15,6 +15,9 @@
 #include "gbt.cuh"
 #include "topk.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace at {
 
 constexpr int SA_NW = 16;
@@ -92,21 +95,21 @@ struct SaParams {
 template <int GRP, int KM = 1>
 struct SaSmem {
     float tile[GRP][NFEAT * 32];
-    float part[GRP][KM * 32 * 32];
+    float part[GRP][KM > 1 ? KM * 32 * 32 : 1];   // KM = 1: the partials alias tile columns 0..31 (below)
     float fk[GRP][KM > 1 ? KM * 32 : 1];   // per-model energies (KM > 1)
     uint32_t chb[2][GRP][MAXKNOBS][32];   // proposal knob vectors, by step parity (owner-written)
     int32_t pjs[2][GRP][32];              // ... the move that made it (knob, -1: none) and the old value
     uint32_t pvs[2][GRP][32];
-    uint32_t extc[2][GRP][MAXLOOPS][32];  // loop extents of the next proposal for both outcomes of the
+    uint16_t extc[2][GRP][MAXLOOPS][32];  // loop extents of the next proposal for both outcomes of the
                                           // current step (0: accepted, 1: rejected), by helper warps
     uint32_t esel[GRP][32];               // which one the owner's decision selected
     uint32_t rnd[GRP][4][32];             // the next step's Philox words, precomputed by a helper warp
     int32_t w[GRP][32];
-    uint64_t bar[2];
+    uint64_t bar[2 * TS_MAXBUF];          // tree-chunk barriers, then (ring mode) consumption counters
 };
 
 template <int TM>
-__device__ __forceinline__ void sa_row_any(const WlDev &W, const uint32_t *ext, const uint32_t *ch, int k, int lane,
+__device__ __forceinline__ void sa_row_any(const WlDev &W, const uint16_t *ext, const uint32_t *ch, int k, int lane,
                                            float *tile)
 {
     if (TM >= 0) { sa_row_rel<TM < 0 ? 0 : TM>(W, ext, ch, k, lane, tile); return; }
@@ -119,7 +122,7 @@ __device__ __forceinline__ void sa_row_any(const WlDev &W, const uint32_t *ext, 
 
 template <int TM>
 __device__ __forceinline__ void sa_extents_any(int tmpl, const uint32_t (&foff)[6], const uint16_t *fact,
-                                               const uint32_t *ch, uint32_t *ext)
+                                               const uint32_t *ch, uint16_t *ext)
 {
     if (TM >= 0) { sa_extents<TM < 0 ? 0 : TM>(foff, fact, ch, ext); return; }
     switch (tmpl) {
@@ -134,21 +137,22 @@ __device__ __forceinline__ void sa_extents_any(int tmpl, const uint32_t (&foff)[
 template <int GRP>
 __device__ __forceinline__ void zero_relation(float (*tile)[NFEAT * 32], int lane, int warp)
 {
+    if (warp >= SA_NW) return;   // the producer warp
     for (int r = warp - GRP; r < GRP * 120; r += SA_NW - GRP) tile[r / 120][(342 + r % 120) * 32 + lane] = 0.0f;
 }
 
 // Block = GRP groups of 32 chains (lane = chain) x SA_NW warps.  Warp g owns group g's chain
 // state; every warp takes part in every group's feature phases and tree walk, so each tree byte
 // staged in shared memory serves 32 GRP chains.
-template <int GRP, int KM, int TM>
-__global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G)
+template <int GRP, int KM, int TM, bool LG = false>
+__global__ void __launch_bounds__((SA_NW + 1) * 32, 1) sa_kernel(SaParams P, TreeGeo G)
 {
     extern __shared__ __align__(128) unsigned char smraw[];
     SaSmem<GRP, KM> &sm = *(SaSmem<GRP, KM> *)smraw;
     uint8_t *bufs = smraw + ((sizeof(SaSmem<GRP, KM>) + 127) / 128) * 128;
     // the energy of group og's chains after a walk: f-hat, or the acquisition over the K models
     auto energy = [&](int og, int lane) -> float {
-        if (KM == 1) return gbt_combine(sm.part[og], lane, P.base);
+        if (KM == 1) return gbt_combine(&sm.tile[og][0], lane, P.base);   // partials in tile columns 0..31
         float mu, sd;
         return acquisition(P.Q, &sm.fk[og][lane], 32, mu, sd);
     };
@@ -169,6 +173,9 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     const int64_t per = (int64_t)P.n_steps + 1;
     const uint64_t c_limit = (uint64_t)G.NC * (uint64_t)per;
 
+#ifdef AT_SA_PHASE_TIMING
+    if (threadIdx.x < 3 * 17) s_walk_prof[threadIdx.x] = 0ull;
+#endif
     ts_start(G, bufs, sm.bar);
     // owner-warp state (registers): knob vector, index and energy of the lane's chain
     uint32_t ch[MAXKNOBS];
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         zero_relation<GRP>(sm.tile, lane, warp);
     }
     __syncthreads();
-    uint32_t ph[2] = {0u, 0u};
+    uint32_t ph[TS_MAXBUF] = {0u, 0u, 0u, 0u};
     uint64_t cs = 0;
     bool no_slots[GRP];
 #pragma unroll
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     // every warp computes its share of the features of all chains of the block
     auto features_phase = [&](int par) {
         // R) context rows and their relation deposits: items (group, row)
-        for (int it = warp; it < GRP * MAXLOOPS; it += SA_NW) {
+        for (int it = warp; it < GRP * MAXLOOPS && warp < SA_NW; it += SA_NW) {
             const int g = it / MAXLOOPS, k = it - g * MAXLOOPS;
             uint32_t chl[MAXKNOBS];
 #pragma unroll
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         t_rows += clock64() - t0;
 #endif
         // T) prefix max of the relation slots: items (group, buffer, pair)
-        for (int it = warp; it < GRP * 6; it += SA_NW) {
+        for (int it = warp; it < GRP * 6 && warp < SA_NW; it += SA_NW) {
             const int g = it / 6, r = it - g * 6;
             relation_prefix(sm.tile[g], lane, r >> 1, r & 1);
         }
@@ -299,7 +306,8 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
     features_phase(1);
     draw_next(0);
     ts_wait_resident(G, sm.bar);
-    walk_pass<SA_NW, GRP, KM>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp, &sm.part[0][0],
+    walk_pass<SA_NW, GRP, KM, false, LG, SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+                                              KM == 1 ? &sm.tile[0][0] : &sm.part[0][0], KM == 1 ? NFEAT * 32 : KM * 1024,
                           nullptr, 0, 0, no_slots);
     fold_models(warp, lane);
     if (!owner) zero_relation<GRP>(sm.tile, lane, warp);
@@ -353,8 +361,9 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
 #endif
-        walk_pass<SA_NW, GRP, KM>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
-                              &sm.part[0][0], nullptr, 0, 0, no_slots);
+        walk_pass<SA_NW, GRP, KM, false, LG, SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+                              KM == 1 ? &sm.tile[0][0] : &sm.part[0][0], KM == 1 ? NFEAT * 32 : KM * 1024, nullptr, 0,
+                              0, no_slots);
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_walk += t - t0; t0 = t; }
 #endif
@@ -401,13 +410,19 @@ __global__ void __launch_bounds__(SA_NW * 32, 1) sa_kernel(SaParams P, TreeGeo G
         printf("sa phases (cycles/step, block 0, GRP=%d T=%d NC=%d CH=%d): proposal+accept %lld features %lld (rows %lld) "
                "walk %lld\n", GRP, G.T, G.NC, G.CH, t_prop / max(P.n_steps, 1), t_feat / max(P.n_steps, 1),
                t_rows / max(P.n_steps, 1), t_walk / max(P.n_steps, 1));
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int w = 0; w < 17; ++w)
+            printf("  warp %2d per step: tree wait %llu walk %llu barrier+issue %llu\n", w,
+                   s_walk_prof[3 * w] / (P.n_steps + 1), s_walk_prof[3 * w + 1] / (P.n_steps + 1),
+                   s_walk_prof[3 * w + 2] / (P.n_steps + 1));
 #endif
 }
 
 template <int GRP, int KM = 1>
 size_t sa_smem_bytes(const TreeGeo &G)
 {
-    return ((sizeof(SaSmem<GRP, KM>) + 127) / 128) * 128 + 2 * (size_t)G.chunk_bytes;
+    return ((sizeof(SaSmem<GRP, KM>) + 127) / 128) * 128 + (size_t)G.NBUF * (size_t)G.chunk_bytes;
 }
 
 }  // namespace at
@@ -482,13 +497,38 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         AT_CUDA_TRY(cudaGetDevice(&dev));
         AT_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
+#ifdef AT_SA_PHASE_TIMING
+    constexpr size_t SMEM_MAX = 226 * 1024;   // room for the static profiling counters
+#else
     constexpr size_t SMEM_MAX = 227 * 1024;
-    // one group: the tree buffers take all the shared memory the group's state leaves (bigger chunks:
-    // more trees per warp per chunk, more independent walks in flight, fewer chunk barriers)
+#endif
+    // the tree buffers take all the shared memory the chain state leaves (bigger chunks: more trees per
+    // warp per chunk, more independent walks in flight, fewer chunk hand-offs).  A streamed ensemble
+    // uses NBUF buffers; ring mode drops the per-chunk block barrier (gbt.cuh walk_pass)
+    static int nbuf_env = -1, ring_env = -1, lg_env = -1;
+    if (nbuf_env < 0) {
+        const char *e1 = getenv("AT_SA_NBUF"), *e2 = getenv("AT_SA_RING"), *e3 = getenv("AT_SA_LG");
+        nbuf_env = e1 ? std::max(2, std::min(at::TS_MAXBUF, atoi(e1))) : 2;
+        ring_env = e2 ? (atoi(e2) != 0) : 0;
+        lg_env = e3 ? (atoi(e3) != 0) : 0;
+    }
+    auto geo = [&](size_t hdr) {
+        at::TreeGeo G0 = at::make_geo(g, (uint32_t)((SMEM_MAX - hdr) / 2));
+        if (G0.resident) return G0;
+        if (lg_env) {
+            // leaves from global memory: the buffers hold nodes only, chunks of a multiple of SA_NW trees
+            // (every warp walks the same number of trees per chunk)
+            const uint32_t nb = (uint32_t)((1 << g->depth) - 1) * 8u;
+            uint32_t per = (uint32_t)((SMEM_MAX - hdr) / nbuf_env) / nb;
+            if (per >= (uint32_t)at::SA_NW) per = per / at::SA_NW * at::SA_NW;
+            return at::make_geo(g, per * nb, false, nbuf_env, ring_env, 1);
+        }
+        return at::make_geo(g, (uint32_t)((SMEM_MAX - hdr) / nbuf_env), false, nbuf_env, ring_env);
+    };
     const size_t hdr1 = ((sizeof(at::SaSmem<1>) + 127) / 128) * 128;
-    at::TreeGeo G1 = at::make_geo(g, (uint32_t)((SMEM_MAX - hdr1) / 2));
+    at::TreeGeo G1 = geo(hdr1);
     const size_t hdr2 = ((sizeof(at::SaSmem<2>) + 127) / 128) * 128;
-    const at::TreeGeo G2 = at::make_geo(g, (uint32_t)((SMEM_MAX - hdr2) / 2));
+    const at::TreeGeo G2 = geo(hdr2);
     const bool use2 = !acq && !G1.resident && o->n_chains >= 2 * 64 * n_sm && at::sa_smem_bytes<2>(G2) <= SMEM_MAX;
     if (acq) {   // K models: 32 KB tree buffers leave room for the per-model partials
         G1 = at::make_geo(g, 32 * 1024);
@@ -505,9 +545,14 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     using KF = void (*)(at::SaParams, at::TreeGeo);
     const KF k1[4] = {at::sa_kernel<1, 1, -1>, at::sa_kernel<1, 1, 0>, at::sa_kernel<1, 1, 1>, at::sa_kernel<1, 1, 2>};
     const KF k2[4] = {at::sa_kernel<2, 1, -1>, at::sa_kernel<2, 1, 0>, at::sa_kernel<2, 1, 1>, at::sa_kernel<2, 1, 2>};
-    const KF kern = acq ? at::sa_kernel<1, 8, -1> : use2 ? k2[tm + 1] : k1[tm + 1];
-    static size_t attr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const int ai = acq ? 8 : (use2 ? 4 : 0) + tm + 1;
+    const KF k1l[4] = {at::sa_kernel<1, 1, -1, true>, at::sa_kernel<1, 1, 0, true>, at::sa_kernel<1, 1, 1, true>,
+                       at::sa_kernel<1, 1, 2, true>};
+    const KF k2l[4] = {at::sa_kernel<2, 1, -1, true>, at::sa_kernel<2, 1, 0, true>, at::sa_kernel<2, 1, 1, true>,
+                       at::sa_kernel<2, 1, 2, true>};
+    const bool lg = !acq && G.leaf_global;
+    const KF kern = acq ? at::sa_kernel<1, 8, -1> : use2 ? (lg ? k2l : k2)[tm + 1] : (lg ? k1l : k1)[tm + 1];
+    static size_t attr[17] = {0};
+    const int ai = acq ? 16 : (lg ? 8 : 0) + (use2 ? 4 : 0) + tm + 1;
     if (smem > attr[ai]) {
         AT_CUDA_TRY(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[ai] = smem;
@@ -516,7 +561,7 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         at::ProfScope ps(AT_K_SA, s);
         const int cpb = use2 ? 64 : 32;
         const unsigned blocks = (unsigned)((o->n_chains + cpb - 1) / cpb);
-        kern<<<blocks, at::SA_NW * 32, smem, s>>>(P, G);
+        kern<<<blocks, (at::SA_NW + 1) * 32, smem, s>>>(P, G);   // + the tree-stream producer warp
         at::note_launch();
         AT_LAUNCH_CHECK("sa_kernel");
     }
