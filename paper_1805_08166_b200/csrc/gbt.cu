@@ -73,7 +73,7 @@ __device__ __forceinline__ void tile_issue(const TileMap &tm, int64_t tile, T *d
 // the current walk (small, resident ensembles: HBM-bound).  GRP = 2: one buffer of 64 candidates,
 // so every streamed tree byte serves twice the candidates (large ensembles: L2-bound).
 template <int GRP, int KM, bool RK>
-__global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, float base, int F, int tile_rows,
+__global__ void __launch_bounds__((PRED_NW + 1) * 32, 1) predict_kernel(TreeGeo G, float base, int F, int tile_rows,
                                                                  const void *__restrict__ Xv, int64_t n, int64_t ld,
                                                                  float *__restrict__ score, uint8_t *__restrict__ slots,
                                                                  int use_bulk, const __grid_constant__ TileMap tm,
@@ -118,11 +118,11 @@ __global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, flo
             mbar_wait(&hd.tile_bar[tb], (uint32_t)((i / NBUF) & 1));
         } else {
             for (int g = 0; g < GRP; ++g)
-                for (int f = warp; f < F; f += PRED_NW)
+                for (int f = warp; f < F && warp < PRED_NW; f += PRED_NW)
                     tl[g * tile_rows * 32 + f * 32 + lane] = ok[g] ? X[(int64_t)f * ld + cand0 + 32 * g] : (T)0;
             __syncthreads();
         }
-        walk_pass<PRED_NW, GRP, KM, RK>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part,
+        walk_pass<PRED_NW, GRP, KM, RK, false, PRED_NW>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part,
                                         KM * 1024, slots,
                                     n, cand0, ok);
         if (KM == 1) {
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(PRED_NW * 32, 1) predict_kernel(TreeGeo G, flo
             }
         }
         __syncthreads();   // part[] and the tile buffer are free again
-        if (use_bulk && threadIdx.x == 0 && i + NBUF < my_tiles) {
+        if (use_bulk && warp == PRED_NW && lane == 0 && i + NBUF < my_tiles) {   // the producer warp
             fence_proxy_async();
             tile_issue<GRP>(tm, tile + NBUF * gridDim.x, tl, tile_rows, &hd.tile_bar[tb]);
         }
@@ -482,10 +482,10 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
             {
                 ProfScope ps(AT_K_PREDICT, s);
                 if (RGRP == 2)
-                    predict_kernel<2, 1, true><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
+                    predict_kernel<2, 1, true><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
                                                                                   d_score, d_leaf_slot, use_bulk, tm, Q);
                 else
-                    predict_kernel<4, 1, true><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
+                    predict_kernel<4, 1, true><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
                                                                                   d_score, d_leaf_slot, use_bulk, tm, Q);
                 note_launch();
                 AT_LAUNCH_CHECK("predict_kernel (rank form)");
@@ -542,13 +542,13 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
     if (acq) Q = *acq;
     ProfScope ps(AT_K_PREDICT, s);
     if (acq)
-        predict_kernel<1, 8, false><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+        predict_kernel<1, 8, false><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                 d_leaf_slot, use_bulk, tm, Q);
     else if (grp == 1)
-        predict_kernel<1, 1, false><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+        predict_kernel<1, 1, false><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                 d_leaf_slot, use_bulk, tm, Q);
     else
-        predict_kernel<2, 1, false><<<blocks, PRED_NW * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
+        predict_kernel<2, 1, false><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                 d_leaf_slot, use_bulk, tm, Q);
     note_launch();
     AT_LAUNCH_CHECK("predict_kernel");
