@@ -1552,7 +1552,7 @@ __device__ unsigned long long g_ft_work_max = 0ull, g_ft_grad_max = 0ull, g_ft_b
 #endif
 
 template <int EP, int NT>
-__global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ? 2 : 4)) fused_forest_kernel(FusedArgs A)
+__global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ? 3 : 4)) fused_forest_kernel(FusedArgs A)
 {
 #ifdef AT_FIT_TIMING
     unsigned long long ft[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer(), t_arr = 0;
