@@ -13,7 +13,8 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libautotvm_b200.so"   # tools may point this at an instrumented build before the first call
+# tools may point this at an instrumented build (AT_LIB=...; e.g. the -DAT_CHECKS variant) before the first call
+LIB_PATH = Path(os.environ.get("AT_LIB", str(PKG / "libautotvm_b200.so")))
 NFEAT = 468
 
 AT_K = dict(features=0, predict=1, sa=2, topk=3, select=4, fit_prep=5, fit_grad=6, fit_hist=7, fit_split=8,

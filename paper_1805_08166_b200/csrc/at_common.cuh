@@ -41,6 +41,23 @@ struct ProfScope {
     ~ProfScope() { prof_end(cls, s); }
 };
 
+// device-side bounds checks of the data-dependent indices (tools/checks_run.sh builds a variant with
+// -DAT_CHECKS and runs the GPU tests on it: compute-sanitizer is closed on the GPU pool)
+#ifdef AT_CHECKS
+#define AT_DCHECK(cond)                                                                                       \
+    do {                                                                                                      \
+        if (!(cond)) {                                                                                        \
+            printf("AT_CHECKS %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, #cond, (int)blockIdx.x, \
+                   (int)threadIdx.x);                                                                         \
+            __trap();                                                                                         \
+        }                                                                                                     \
+    } while (0)
+#else
+#define AT_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 // ---------------------------------------------------------------- constants
 constexpr int NFEAT = 468;
 constexpr int MAXLOOPS = 18;

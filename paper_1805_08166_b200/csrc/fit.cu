@@ -968,6 +968,7 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         c[j] = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
+                        AT_DCHECK(c[j] < P);
                         og[j] = atomicAdd(&glo[c[j]], gl);
                         oh[j] = atomicAdd(&hlo[c[j]], hl);
                     }
@@ -1804,6 +1805,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
                         int bv = 0, th = 1 << 30;
                         if (j < N) {
                             const int i = ord[j], q = nat[j], sf = T.decf[q];
+                            AT_DCHECK(i < N && q < 128);
                             iv[k] = i;
                             qv[k] = q;
                             if (sf >= 0) {

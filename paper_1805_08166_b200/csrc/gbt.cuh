@@ -136,6 +136,8 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
                     uint32_t nf, nt;
                     float x;
                     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g][jj]));
+                    AT_DCHECK(nf < (uint32_t)(gstride / 32));   // a feature row of the tile
+                    AT_DCHECK(((a[g][jj] + add_l[jj]) >> 3) >= 1u && ((a[g][jj] + add_l[jj]) >> 3) <= (uint32_t)ni);   // heap index
                     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile_lane + (nf << 7)));
                     a[g][jj] = 2u * a[g][jj] + (x < __uint_as_float(nt) ? add_l[jj] : add_r[jj]);
                 }
@@ -160,6 +162,7 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
 #pragma unroll
             for (int g = 0; g < GRP; ++g) {
                 const int slot = (int)((a[g][jj] + add_l[jj]) >> (RK ? 2 : 3)) - nl;
+                AT_DCHECK(slot >= 0 && slot < nl);
                 pend.v[g][jj] = __ldg(G.leaf + (int64_t)t * nl + slot);
             }
         }
@@ -177,6 +180,8 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
 #pragma unroll
             for (int g = 0; g < GRP; ++g) {
                 const int slot = (int)((a[g][jj] + add_l[jj]) >> (RK ? 2 : 3)) - nl;   // h = (a - tb) / NBY in [2^D, 2^(D+1))
+                AT_DCHECK(slot >= 0 && slot < nl);
+                AT_DCHECK(t - c0 >= 0 && t - c0 < G.CH);
                 const float lv = leaves[(t - c0) * nl + slot];
 #pragma unroll
                 for (int m = 0; m < KM; ++m)

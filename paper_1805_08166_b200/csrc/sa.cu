@@ -340,6 +340,7 @@ __global__ void __launch_bounds__((SA_NW + 1) * 32, 1) sa_kernel(SaParams P, Tre
                 for (int q = 0; q < MAXKNOBS; ++q) if (q == j) v = ch[q];
                 uint32_t v2 = __umulhi(r.y, W.radix[j] - 1u);
                 if (v2 >= v) v2 += 1;
+                AT_DCHECK(j < W.n_knobs && v < W.radix[j] && v2 < W.radix[j]);
                 idx2 = idx - (uint64_t)v * W.place[j] + (uint64_t)v2 * W.place[j];
                 pj = j;
                 pv = v;
