@@ -232,7 +232,12 @@ AT_API int select_topk(at_space sp, int32_t workload, const uint64_t *d_pool_idx
  * Writes the fitted ensemble to *out (a new handle); d_pred_out (nullable) [n] gets
  * the fit's final training predictions; d_hist0_out (nullable) [n_features][max_bins][2]
  * gets tree 0's root histogram (after the reduction).  Errors: AT_EEMPTY (n == 0),
- * AT_EINVAL (non-finite cost), AT_EUNSUPPORTED (depth > 8, max_bins > 256). */
+ * AT_EINVAL (non-finite cost), AT_EUNSUPPORTED (depth > 8, max_bins > 256, group key >= 1024).
+ * Host synchronization: a single-rank fit of n <= 2048 samples (one fused launch) reads every
+ * data-dependent size on the device and never blocks the host; its input errors (non-finite cost,
+ * group key >= 1024) travel with the returned model -- every later call on it (gbt_predict,
+ * sa_explore, gbt_export, gbt_concat, ...) returns AT_EINVAL.  Larger or multi-rank fits read the
+ * cut counts back once (the histogram layout is sized from them) and return those errors directly. */
 typedef int (*at_allreduce_i64_fn)(int64_t *d_buf, int64_t count, void *ctx, void *stream);
 
 typedef struct {

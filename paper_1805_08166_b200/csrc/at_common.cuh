@@ -218,6 +218,9 @@ struct at_gbt_s {
     int32_t *d_thr_off;
     float *d_thr_val;
     int32_t rk_state;
+    uint32_t *h_err;              // mapped word (fitted models): nonzero when the fit met a non-finite
+                                  // cost or a group key >= 1024; every later call on the model
+                                  // reports AT_EINVAL (gbt_fit_hist's small-fit path never syncs)
 };
 
 namespace at {
@@ -225,4 +228,6 @@ int scratch_reserve(at_space sp, size_t bytes, cudaStream_t s);
 // AT_ERANGE (and clears the word) if a kernel enqueued earlier on this space met an out-of-range
 // index and has already finished; AT_OK otherwise.  Never synchronizes.
 int take_range_error(at_space sp);
+// AT_EINVAL if the fit that produced g flagged bad input (see at_gbt_s::h_err); never synchronizes
+int model_error(at_gbt g);
 }

@@ -397,6 +397,14 @@ __global__ void bin_layout_kernel(const int32_t *__restrict__ ncuts, int F, int3
     info[0] = o;
     info[1] = mx;
     info[4] = nf;
+    if (nf == 0) flist[0] = 0;   // no feature can split: one block on feature 0 (no cut) keeps every node a leaf
+}
+
+// the fit's input flags (info[2]: 1 non-finite cost, 2 group key >= 1024) -> the model's mapped error word
+__global__ void fit_flag_kernel(const int32_t *__restrict__ info, uint32_t *err)
+{
+    *(volatile uint32_t *)err = (uint32_t)info[2];
+    __threadfence_system();
 }
 
 // Exact 64-bit add into shared memory with two native 32-bit atomics (sm_100a has no native 64-bit
@@ -1415,8 +1423,8 @@ struct FusedArgs {
     double lam, mcw, eta;
     unsigned *bar;
     int objective;              // AT_OBJ_RANK / AT_OBJ_REG
-    const int32_t *flist;       // the features that can split (ncuts > 0), ascending; nF of them
-    int nF;
+    const int32_t *flist;       // the features that can split (ncuts > 0), ascending; info[4] of them
+    const int32_t *info;        // device sizes of the fit prep: [2] input flags, [3] groups, [4] splittable features
 };
 
 __host__ __device__ inline int fused_ep(int N, int NT)
@@ -1573,7 +1581,13 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
 
     // blocks own the features that can split (constant ones never can: no cut), block b feature
     // flist[b] (and flist[b + G], ... when there are more than blocks)
-    const int G = gridDim.x, F = A.nF, D = A.D;
+    // the splittable-feature count and the group count come from the prep kernels on the device, so the
+    // host launches this kernel without reading them back (gbt_fit_hist never syncs on this path)
+    if (A.info[2] != 0) return;   // bad input: the model stays undefined, the fit's error word says so
+    // the launch is sized for every feature; blocks beyond the splittable ones leave before the first
+    // grid barrier, which then counts the G working blocks only
+    const int F = max(A.info[4], 1), G = min((int)gridDim.x, F), D = A.D, n_groups = A.info[3];
+    if ((int)blockIdx.x >= G) return;
     const int n_int = (1 << D) - 1, n_leaf = 1 << D;
     const bool resident = F <= G;
     unsigned epoch = 0;
@@ -1696,7 +1710,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
                 A.h[i] = hi;
             }
         }
-        for (int item = blockIdx.x; A.objective == AT_OBJ_RANK && item < A.n_groups * chunks; item += G) {
+        for (int item = blockIdx.x; A.objective == AT_OBJ_RANK && item < n_groups * chunks; item += G) {
             const int grp = item / chunks, a0 = (item - grp * chunks) * CM;
             if (tid == 0) {
                 int lo = 0, hi = FIT_MAXKEYS;   // largest w with gpre[w] <= grp
@@ -2201,7 +2215,11 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     float *t_leaf = ws.get<float>((size_t)o->n_trees * n_leaf);
     if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
 
-    // input checks + cuts + groups; one host sync reads back the sizes the launches need
+    // input checks + cuts + groups.  The small single-rank fit (one fused launch) reads every size it
+    // needs on the device and never synchronizes; the other paths read the sizes back once
+    const char *fused_e = getenv("AT_FIT_FUSED");   // "0" forces the level-by-level path
+    const int fused_env = fused_e ? atoi(fused_e) : 1;
+    const bool fused_path = fused_env && !o->allreduce && !o->d_hist0_out && n <= FUSED_NMAX;
     int info[8] = {0};
     std::vector<int32_t> ncuts_h(F);
     {
@@ -2227,14 +2245,17 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         else
             AT_CUDA_TRY(cudaMemsetAsync(pred, 0, sizeof(float) * n, s));
         AT_LAUNCH_CHECK("fit prep");
+    }
+    if (!fused_path) {
         AT_CUDA_TRY(cudaMemcpyAsync(info, d_info, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         AT_CUDA_TRY(cudaMemcpyAsync(ncuts_h.data(), ncuts, F * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         AT_CUDA_TRY(cudaStreamSynchronize(s));
+        if (info[2] == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
+        if (info[2] == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
     }
-    if (info[2] == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
-    if (info[2] == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
-    const int TB = info[0], max_nb = info[1], n_groups = info[3];
-    const int n_split = info[4];   // features with at least one cut
+    // (read back below for the paths that need them on the host)
+    int TB = info[0], max_nb = info[1], n_groups = info[3];
+    int n_split = info[4];   // features with at least one cut
     // the fitted ensemble handle (both paths)
     auto finish = [&]() -> int {
         // the fitted ensemble handle
@@ -2261,20 +2282,31 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         AT_CUDA_TRY(cudaMemcpyAsync(gm->d_leaf, t_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf,
                                     cudaMemcpyDeviceToDevice, s));
         if (o->d_pred_out) AT_CUDA_TRY(cudaMemcpyAsync(o->d_pred_out, pred, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+        if (fused_path) {   // input flags found on the device travel with the model (at_gbt_s::h_err)
+            if (cudaHostAlloc((void **)&gm->h_err, sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess) {
+                cudaGetLastError();
+                gm->h_err = nullptr;
+                gbt_destroy(gm);
+                return fail(AT_ENOMEM, "gbt_fit_hist: mapped error word allocation failed");
+            }
+            *gm->h_err = 0u;
+            uint32_t *d_err = nullptr;
+            AT_CUDA_TRY(cudaHostGetDevicePointer((void **)&d_err, gm->h_err, 0));
+            fit_flag_kernel<<<1, 1, 0, s>>>(d_info, d_err); note_launch();
+        }
         AT_LAUNCH_CHECK("fit finish");
         *out = gm;
         return AT_OK;
     };
 
-    // small single-rank fits: the whole forest in one cooperative launch (fused_forest_kernel)
-    const char *fused_e = getenv("AT_FIT_FUSED");   // "0" forces the level-by-level path
-    const int fused_env = fused_e ? atoi(fused_e) : 1;
-    if (fused_env && !o->allreduce && !o->d_hist0_out && n <= FUSED_NMAX) {
+    // small single-rank fits: the whole forest in one cooperative launch (fused_forest_kernel), sized for
+    // all F features (the splittable ones are known only on the device)
+    if (fused_path) {
         int dev = 0, nsm = 0, coop = 0, per = 0;
         AT_CUDA_TRY(cudaGetDevice(&dev));
         AT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         AT_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-        const int nF = std::max(n_split, 1);   // blocks own the splittable features
+        const int nF = F;   // an upper bound of the splittable features (blocks own them; the rest idle)
         // the kernel variant: 512 threads per block when every splittable feature still gets its own
         // resident block at 2 blocks / SM, else 256 threads (4 / SM)
         const void *fk = nullptr;
@@ -2297,12 +2329,14 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                 fused_attr[fslot] = fsm;
             }
             AT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fk, NT, fsm));
-            if (pass == 0 && per > 0 && nF <= per * nsm) break;
+            // 512 threads while they keep 2 blocks per SM (n <= 1024): 296 resident blocks hold the
+            // splittable features of typical databases (config 2: 284); the count itself is only known on
+            // the device, which falls back to blocks walking several features when it is larger
+            if (pass == 0 && per > 0 && (nF <= per * nsm || per >= 2)) break;
         }
         if (coop && per > 0) {
             // blocks for the splittable features only (all constant: one block on feature 0, which has no
             // cut, so every node stays a pass-through and the leaves are the node totals)
-            if (n_split == 0) AT_CUDA_TRY(cudaMemsetAsync(flist, 0, sizeof(int32_t), s));
             const int G = (int)std::min<int64_t>(nF, (int64_t)per * nsm);
             const bool resident = nF <= G;
             int32_t *klist = ws.get<int32_t>(n);
@@ -2318,8 +2352,8 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             AT_LAUNCH_CHECK("klist");
             FusedArgs fa;
             fa.bins = bins; fa.ncuts = ncuts; fa.cuts = cuts; fa.B = B;
-            fa.flist = flist; fa.nF = nF;
-            fa.n = (int)n; fa.F = F; fa.D = D; fa.n_trees = o->n_trees; fa.GS = GS; fa.n_groups = n_groups;
+            fa.flist = flist; fa.info = d_info;
+            fa.n = (int)n; fa.F = F; fa.D = D; fa.n_trees = o->n_trees; fa.GS = GS;
             fa.counts = counts; fa.woff = woff; fa.gpre = gpre; fa.klist = klist;
             float *pred2 = ws.get<float>(n);
             if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
@@ -2343,6 +2377,17 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         }
     }
 
+    if (fused_path) {   // no cooperative launch possible: the sizes are read back after all
+        AT_CUDA_TRY(cudaMemcpyAsync(info, d_info, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        AT_CUDA_TRY(cudaMemcpyAsync(ncuts_h.data(), ncuts, F * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        AT_CUDA_TRY(cudaStreamSynchronize(s));
+        if (info[2] == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
+        if (info[2] == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
+        TB = info[0];
+        max_nb = info[1];
+        n_groups = info[3];
+        n_split = info[4];
+    }
     // a single-rank fit has no host callback between levels: its launches are captured once into a
     // CUDA graph and launched as one unit (no host round trips for ~10 launches per level)
     auto run_captured = [&](auto &&enqueue, int reps) -> int {

@@ -219,6 +219,7 @@ int gbt_export(at_gbt g, uint16_t *feat, float *thresh, float *leaf, float *base
 {
     if (!g) return at::fail(AT_EINVAL, "gbt_export: null model");
     AT_CUDA_TRY(cudaStreamSynchronize(g->last));   // the fit that wrote it may run on a non-blocking stream
+    if (int rc = at::model_error(g)) return rc;
     const int64_t ni = (1 << g->depth) - 1, nl = 1 << g->depth;
     if (feat || thresh) {
         std::vector<uint2> nodes((size_t)g->n_trees * ni);
@@ -239,6 +240,10 @@ int gbt_export(at_gbt g, uint16_t *feat, float *thresh, float *leaf, float *base
 int gbt_concat(at_gbt a, at_gbt b, at_gbt *out)
 {
     if (!a || !b || !out) return at::fail(AT_EINVAL, "gbt_concat: null handle");
+    AT_CUDA_TRY(cudaStreamSynchronize(a->last));   // host-side construction from both models
+    AT_CUDA_TRY(cudaStreamSynchronize(b->last));
+    if (int rc = at::model_error(a)) return rc;
+    if (int rc = at::model_error(b)) return rc;
     if (a->n_features != b->n_features) return at::fail(AT_EMISMATCH, "gbt_concat: different n_features");
     const int D = std::max(a->depth, b->depth);
     const int64_t NI = (1 << D) - 1, NL = 1 << D;
@@ -273,6 +278,10 @@ int gbt_destroy(at_gbt g)
     if (g->d_rk_nodes) cudaFreeAsync(g->d_rk_nodes, g->last);
     if (g->d_thr_off) cudaFreeAsync(g->d_thr_off, g->last);
     if (g->d_thr_val) cudaFreeAsync(g->d_thr_val, g->last);
+    if (g->h_err) {   // mapped word the fit's last kernel writes: freed after the model's stream drains
+        cudaStreamSynchronize(g->last);
+        cudaFreeHost(g->h_err);
+    }
     delete g;
     return AT_OK;
 }
@@ -563,6 +572,7 @@ int gbt_predict(at_gbt g, const float *d_feat, int64_t n, int64_t ld, float *d_s
                 void *stream)
 {
     if (!g) return at::fail(AT_EINVAL, "gbt_predict: null model");
+    if (int rc = at::model_error(g)) return rc;
     if (n < 0) return at::fail(AT_EINVAL, "gbt_predict: n < 0");
     if (n == 0) return AT_OK;
     if (!d_feat || !d_score) return at::fail(AT_EINVAL, "gbt_predict: null buffer");
@@ -574,6 +584,7 @@ int gbt_predict_acq(at_gbt g, const float *d_feat, int64_t n, int64_t ld, const 
                     float *d_mean, float *d_std, void *stream)
 {
     if (!g || !o) return at::fail(AT_EINVAL, "gbt_predict_acq: null model / options");
+    if (int rc = at::model_error(g)) return rc;
     if (o->n_models < 1 || o->n_models > 8 || g->n_trees % o->n_models != 0)
         return at::fail(AT_EINVAL, "gbt_predict_acq: need 1 <= n_models <= 8 dividing n_trees");
     if (o->kind < AT_ACQ_MEAN || o->kind > AT_ACQ_EI) return at::fail(AT_EINVAL, "gbt_predict_acq: bad kind");

@@ -97,6 +97,15 @@ int scratch_reserve(at_space sp, size_t bytes, cudaStream_t s)
     return AT_OK;
 }
 
+int model_error(at_gbt g)
+{
+    if (g && g->h_err && *(volatile uint32_t *)g->h_err)
+        return fail(AT_EINVAL, *(volatile uint32_t *)g->h_err == 2u
+                                   ? "this model's fit met a group key >= 1024: the model is undefined"
+                                   : "this model's fit met a non-finite cost: the model is undefined");
+    return AT_OK;
+}
+
 int take_range_error(at_space sp)
 {
     if (sp->h_err && *(volatile uint32_t *)sp->h_err) {

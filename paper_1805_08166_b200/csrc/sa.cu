@@ -435,6 +435,7 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
 {
     if (!sp || !g || !o) return at::fail(AT_EINVAL, "sa_explore: null handle");
     if (int rc = at::take_range_error(sp)) return rc;
+    if (int rc = at::model_error(g)) return rc;
     if (!d_chain_idx || !d_chain_energy || (!o->d_temps && o->n_steps > 0) || !d_out_idx || !d_out_score || !d_out_n)
         return at::fail(AT_EINVAL, "sa_explore: null buffer");
     if (o->n_chains < 1 || o->n_steps < 0 || o->k_out < 1 || o->k_out > 1024 || n_measured < 0)

@@ -845,13 +845,56 @@ def test_knob_features_match_oracle(at, wls):
 
 
 def test_fit_errors(at):
+    """S:306 / header: n = 0 -> AT_EEMPTY at once.  A non-finite cost: a small fit (one fused launch, no
+    host sync) returns a model whose every later use reports AT_EINVAL; a large fit (reads its sizes
+    back) reports AT_EINVAL itself."""
     with pytest.raises(at.ATError) as e:
         at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 0, torch.zeros(4, device="cuda"),
                         torch.zeros(4, dtype=torch.int16, device="cuda"))
     assert e.value.code == -7
-    with pytest.raises(at.ATError):
-        c = torch.tensor([1.0, float("nan"), 2.0, 3.0], device="cuda")
-        at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 4, c, torch.zeros(4, dtype=torch.int16, device="cuda"))
+    c = torch.tensor([1.0, float("nan"), 2.0, 3.0], device="cuda")
+    X = torch.zeros((468, 4), device="cuda")
+    m = at.gbt_fit_hist(X, 4, c, torch.zeros(4, dtype=torch.int16, device="cuda"))
+    for use in (lambda: m.export(), lambda: m.predict(X, n=4)):
+        with pytest.raises(at.ATError) as e:
+            use()
+        assert e.value.code == -1
+    n = 3000
+    cb = torch.ones(n, device="cuda")
+    cb[7] = float("inf")
+    with pytest.raises(at.ATError) as e:
+        at.gbt_fit_hist(torch.rand((468, n), device="cuda"), n, cb, torch.zeros(n, dtype=torch.int16, device="cuda"))
+    assert e.value.code == -1
+
+
+def test_small_fit_does_not_block_the_host(at):
+    """8(b) "every call is stream-ordered and asynchronous": a fit enqueued behind a long kernel returns to
+    the host before that kernel finishes (the fused path sizes its launch on the device), and its model is
+    the oracle's."""
+    import time
+    sp = at.Space(synth.ALL_RESNET)
+    ens = synth.ensemble(1000, 8, seed=1805)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    n_ch = 65536
+    temps = torch.from_numpy(synth.temperatures(40, synth.energy_scale(1000))).cuda()
+    cw = dev((np.arange(n_ch) % 12).astype(np.int16))
+    osp, idx, Xo, c, key = fit_inputs(800, [synth.CFG2A], seed=21)
+    Xg = at.Space([synth.CFG2A]).features(u64(idx))
+    cg, kg = dev(c), dev(key.view(np.int16))
+    at.gbt_fit_hist(Xg, 800, cg, kg, n_trees=2, depth=3)   # warm (workspace, attributes)
+    torch.cuda.synchronize()
+    at.sa_explore(sp, g, torch.zeros(n_ch, dtype=torch.int64, device="cuda"), temps, seed=1, round_=0, k_out=8,
+                  chain_workload=cw, init=True)            # ~15 ms of device work
+    t0 = time.perf_counter()
+    m = at.gbt_fit_hist(Xg, 800, cg, kg, n_trees=5, depth=5)
+    dt = time.perf_counter() - t0
+    busy = not torch.cuda.current_stream().query()
+    torch.cuda.synchronize()
+    assert busy, f"the stream drained during the fit call ({dt * 1e3:.2f} ms)"
+    ref = O.fit_hist(Xo, c, key, n_trees=5, depth=5)
+    ex = m.export()
+    for k in ("feat", "thresh", "leaf"):
+        assert_bits_equal(ex[k], ref[k], f"model {k}")
 
 
 # ------------------------------------------------------------------ full-size configurations, sampled
