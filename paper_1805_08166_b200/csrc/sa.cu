@@ -491,8 +491,6 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         P.Q.best = acq->best;
         for (int k = 0; k < 8; ++k) P.Q.base[k] = k < acq->n_models ? acq->model_base[k] : 0.0f;
     }
-    // two 32-chain groups per block when there are enough chains to fill the SMs twice over and the
-    // ensemble streams (each streamed tree byte then serves 64 chains); otherwise one group
     static int n_sm = 0;
     if (!n_sm) {
         int dev = 0;
@@ -531,7 +529,16 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     at::TreeGeo G1 = geo(hdr1);
     const size_t hdr2 = ((sizeof(at::SaSmem<2>) + 127) / 128) * 128;
     const at::TreeGeo G2 = geo(hdr2);
-    const bool use2 = !acq && !G1.resident && o->n_chains >= 2 * 64 * n_sm && at::sa_smem_bytes<2>(G2) <= SMEM_MAX;
+    static int grp_env = -1;
+    if (grp_env < 0) {
+        const char *e = getenv("AT_SA_GRP");   // 1 / 2 force the group count (measurement knob)
+        grp_env = e ? atoi(e) : 0;
+    }
+    const bool fit2 = !acq && !G1.resident && at::sa_smem_bytes<2>(G2) <= SMEM_MAX;
+    // two 32-chain groups per block (every streamed tree byte serves 64 chains) as soon as they still occupy
+    // ~85 % of the SMs in one wave: measured on config 3, 8192 chains (128 blocks) run 1.55x faster with two
+    // groups than with one (256 blocks), 4096 chains (64 blocks) 1.24x slower
+    const bool use2 = grp_env == 2 ? fit2 : grp_env == 1 ? false : fit2 && (int64_t)o->n_chains * 20 >= (int64_t)64 * n_sm * 17;
     if (acq) {   // K models: 32 KB tree buffers leave room for the per-model partials
         G1 = at::make_geo(g, 32 * 1024);
         G1.Tm = g->n_trees / acq->n_models;

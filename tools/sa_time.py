@@ -7,8 +7,9 @@ from paper_1805_08166_b200 import at, build, synth
 build.build(); torch.cuda.set_device(0)
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+C3 = int(os.environ.get("SA_CHAINS", "65536"))
 if cfg == "cfg3":
-    wls, T, D, C, cw = synth.ALL_RESNET, 1000, 8, 65536, torch.from_numpy((np.arange(65536) % 12).astype(np.int16)).cuda()
+    wls, T, D, C, cw = synth.ALL_RESNET, 1000, 8, C3, torch.from_numpy((np.arange(C3) % 12).astype(np.int16)).cuda()
 else:
     wls, T, D, C, cw = [synth.CFG2A], 500, 6, 4096, None
 sp = at.Space(wls)
@@ -28,6 +29,6 @@ for rep in range(3):
     ts.append(a.elapsed_time(b))
     assert torch.equal(r["accept_bits"], ref_bits)
 ms = min(ts)
-print(json.dumps({"cfg": cfg, "nbuf": os.environ.get("AT_SA_NBUF"), "ring": os.environ.get("AT_SA_RING"), "lg": os.environ.get("AT_SA_LG"),
+print(json.dumps({"cfg": cfg, "nbuf": os.environ.get("AT_SA_NBUF"), "ring": os.environ.get("AT_SA_RING"), "lg": os.environ.get("AT_SA_LG"), "grp": os.environ.get("AT_SA_GRP"), "chains": C,
                   "ms": round(ms, 3), "chain_steps_per_s": round(C * (steps + 1) / ms * 1e3, 1),
                   "accept_digest": int(ref_bits.sum().item())}))
