@@ -35,7 +35,27 @@ struct TreeGeo {
     int leaf_global;        // 1: chunks carry the nodes only; a walk's leaf is read from global memory
                             // (L2) and added one batch later (walk_batch<..., LG>), so the tree buffers
                             // hold 1.5x the trees of a depth-8 ensemble
+    int NP;                 // > 1: NP independent tree pipelines (walk_pass): warp group p of NW / NP warps
+                            // streams its own slices of CH = NW / NP trees through its own two buffers,
+                            // with full / empty mbarriers and no block barrier; NC counts slices
 };
+
+// stream uses per pass (the unit of the stream counter c): chunks, or each pipeline's slices
+__host__ __device__ inline int ts_uses_per_pass(const TreeGeo &G) { return G.NP > 1 ? G.NC / G.NP : G.NC; }
+
+// pipeline q's use v of the stream: slice (v mod per) NP + q of pass v / per into slot 2q + (v & 1)
+__device__ __forceinline__ void ts_issue_slice(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, int q, uint64_t v)
+{
+    const uint32_t per = (uint32_t)(G.NC / G.NP);
+    const int s = (int)((uint32_t)v % per) * G.NP + q;
+    const int slot = 2 * q + (int)(v & 1);
+    const int t0 = s * G.CH;
+    const uint32_t nb = (uint32_t)G.CH * G.ni * (uint32_t)G.nbytes, lb = (uint32_t)G.CH * G.nl * 4u;
+    uint8_t *dst = bufs + (size_t)slot * G.chunk_bytes;
+    mbar_arrive_expect_tx(&bar[slot], nb + lb);
+    bulk_g2s(dst, G.nodes + (int64_t)t0 * G.ni * G.nbytes, nb, &bar[slot]);
+    bulk_g2s(dst + (size_t)G.CH * G.ni * G.nbytes, G.leaf + (int64_t)t0 * G.nl, lb, &bar[slot]);
+}
 constexpr int TS_MAXBUF = 4;
 
 constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // default per buffer (two buffers)
@@ -77,6 +97,18 @@ __device__ __forceinline__ void ts_issue(const TreeGeo &G, uint8_t *bufs, uint64
 __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64_t *bar)
 {
     if (threadIdx.x == 0) {
+        if (G.NP > 1) {   // full[2 NP] (one arrival + tx), then empty[2 NP] (one arrival per walker warp)
+            for (int b = 0; b < 2 * G.NP; ++b) {
+                mbar_init(&bar[b], 1);
+                mbar_init(&bar[2 * G.NP + b], 16 / G.NP);
+            }
+            fence_proxy_async();
+            for (int q = 0; q < G.NP; ++q) {
+                ts_issue_slice(G, bufs, bar, q, 0);
+                ts_issue_slice(G, bufs, bar, q, 1);
+            }
+            return;
+        }
         for (int b = 0; b < G.NBUF; ++b) {
             mbar_init(&bar[b], 1);
             if (G.ring) ((unsigned *)(bar + G.NBUF))[b] = 0u;
@@ -255,7 +287,38 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
     LeafPend<GRP, walk_nbmax<GRP, KM>()> pend;
     pend.n = 0;
     const bool walker = PW < 0 || warp < PW;
-    if (G.resident) {
+    if (PW >= 0 && G.NP > 1) {
+        // NP independent pipelines, no block barrier: warp group p (NW / NP warps) walks its slices -- each
+        // warp one tree per slice -- waiting on the slot's full barrier and counting out on its empty
+        // barrier; lane q of the producer warp refills pipeline q's slot as soon as its walkers are out.
+        // The groups drift apart, so one group's fill / drain overlaps another's steady walk.
+        const int per = G.NC / G.NP;
+        if (walker) {
+            const int pp = warp / (NW / G.NP);
+            for (int kk = 0; kk < per; ++kk, ++c) {
+                const int slot = 2 * pp + (int)(c & 1);
+                mbar_wait(&bar[slot], (uint32_t)((c >> 1) & 1));
+                walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)slot * G.chunk_bytes, kk * G.NP + pp, tile, gstride,
+                                                lane, warp, p, slots, slot_ld, cand0, cand_ok, pend);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar[2 * G.NP + slot]);
+            }
+        } else {
+            if (lane < G.NP) {
+                uint64_t u = c;
+                for (int kk = 0; kk < per; ++kk, ++u) {
+                    const int slot = 2 * lane + (int)(u & 1);
+                    mbar_wait(&bar[2 * G.NP + slot], (uint32_t)((u >> 1) & 1));
+                    if (u + 2 < c_limit) {
+                        fence_proxy_async();
+                        ts_issue_slice(G, bufs, bar, lane, u + 2);
+                    }
+                }
+            }
+            __syncwarp();
+            c += per;
+        }
+    } else if (G.resident) {
         for (int k = 0; k < G.NC && walker; ++k)
             walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)k * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots, slot_ld,
                                 cand0, cand_ok, pend);
@@ -356,7 +419,7 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
     }
     // a resident pass has no per-chunk barrier: every warp must be done reading the tile before the
     // partials are written (sa_kernel keeps them in the tile's first columns)
-    if (G.resident) __syncthreads();
+    if (G.resident || G.NP > 1) __syncthreads();
 #pragma unroll
     for (int g = 0; g < GRP && walker; ++g)
 #pragma unroll

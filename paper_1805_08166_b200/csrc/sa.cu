@@ -105,7 +105,8 @@ struct SaSmem {
     uint32_t esel[GRP][32];               // which one the owner's decision selected
     uint32_t rnd[GRP][4][32];             // the next step's Philox words, precomputed by a helper warp
     int32_t w[GRP][32];
-    uint64_t bar[2 * TS_MAXBUF];          // tree-chunk barriers, then (ring mode) consumption counters
+    uint64_t bar[4 * TS_MAXBUF];          // tree-chunk barriers, then (ring mode) consumption counters; NP
+                                          // pipelines: full[2 NP] then empty[2 NP]
 };
 
 template <int TM>
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__((SA_NW + 1) * 32, 1) sa_kernel(SaParams P, Tre
     const int c = blockIdx.x * 32 * GRP + og * 32 + lane;  // the owner's chain
     const bool live = owner && c < P.n_chains;
     const int64_t per = (int64_t)P.n_steps + 1;
-    const uint64_t c_limit = (uint64_t)G.NC * (uint64_t)per;
+    const uint64_t c_limit = (uint64_t)ts_uses_per_pass(G) * (uint64_t)per;
 
 #ifdef AT_SA_PHASE_TIMING
     if (threadIdx.x < 3 * 17) s_walk_prof[threadIdx.x] = 0ull;
@@ -505,9 +506,12 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     // the tree buffers take all the shared memory the chain state leaves (bigger chunks: more trees per
     // warp per chunk, more independent walks in flight, fewer chunk hand-offs).  A streamed ensemble
     // uses NBUF buffers; ring mode drops the per-chunk block barrier (gbt.cuh walk_pass)
-    static int nbuf_env = -1, ring_env = -1, lg_env = -1;
+    static int nbuf_env = -1, ring_env = -1, lg_env = -1, np_env = -1;
     if (nbuf_env < 0) {
         const char *e1 = getenv("AT_SA_NBUF"), *e2 = getenv("AT_SA_RING"), *e3 = getenv("AT_SA_LG");
+        const char *e4 = getenv("AT_SA_NP");
+        np_env = e4 ? atoi(e4) : 0;
+        if (np_env != 2 && np_env != 4) np_env = 0;
         nbuf_env = e1 ? std::max(2, std::min(at::TS_MAXBUF, atoi(e1))) : 2;
         ring_env = e2 ? (atoi(e2) != 0) : 0;
         lg_env = e3 ? (atoi(e3) != 0) : 0;
@@ -515,6 +519,20 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     auto geo = [&](size_t hdr) {
         at::TreeGeo G0 = at::make_geo(g, (uint32_t)((SMEM_MAX - hdr) / 2));
         if (G0.resident) return G0;
+        if (np_env) {
+            // NP pipelines of SA_NW / NP warps, each with two slices of SA_NW / NP trees
+            const uint32_t per_tree = (uint32_t)((1 << g->depth) - 1) * 8u + (uint32_t)(1 << g->depth) * 4u;
+            const int chs = at::SA_NW / np_env;
+            if ((size_t)2 * np_env * chs * per_tree <= SMEM_MAX - hdr) {
+                at::TreeGeo Gp = at::make_geo(g, (uint32_t)chs * per_tree, false, 2 * np_env, 0);
+                Gp.CH = chs;
+                Gp.NC = g->t_pad / chs;
+                Gp.chunk_bytes = (uint32_t)chs * per_tree;
+                Gp.resident = 0;
+                Gp.NP = np_env;
+                return Gp;
+            }
+        }
         if (lg_env) {
             // leaves from global memory: the buffers hold nodes only, chunks of a multiple of SA_NW trees
             // (every warp walks the same number of trees per chunk)

@@ -1,4 +1,5 @@
-for cfg in cfg3 cfg2; do
-  timeout 300 python tools/sa_time.py $cfg 100 2>&1 | tail -1
+for np in 0 2 4; do
+  AT_SA_NP=$np timeout 300 python tools/sa_time.py cfg3 100 2>&1 | tail -1
 done
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+AT_SA_NP=2 SA_CHAINS=8192 timeout 300 python tools/sa_time.py cfg3 100 2>&1 | tail -1
+AT_SA_NP=2 timeout 300 python tools/sa_time.py cfg2 100 2>&1 | tail -1
