@@ -10,7 +10,8 @@ One STEP = one exploration round of Algorithm 1 over the whole hot p
     decision (a2-a6);
   * per workload the distinct top lambda b = 128 of the visited set, measured configs excluded
     (a7); with N > 1: ONE all-gather of the packed per-rank lists (NCCL over NVLink) + topk_merge;
-  * select_topk for each of the 12 workloads: b = 64, eps = 0.05, alpha = 0.1 (a8);
+  * select_topk for each of the 12 workloads (one select_topk_batch launch): b = 64, eps = 0.05,
+    alpha = 0.1 (a8);
   * refit: features_extract of the measured database D (|D| = 12 x 128 synthetic measured configs,
     pairs within a workload) + gbt_fit_hist, 100 trees, depth 6, rank loss (a9), replicated on
     every rank (bit-identical, no communication: at this |D| a per-level histogram all-reduce
@@ -190,8 +191,9 @@ class Config3:
         if self.world > 1:
             gi, gs, gn = D.gather_lists(oi, osc, on)
             oi, osc, on = at.topk_merge(self.space, gi, gs, gn, K_POOL, measured=meas)
-        sels = [at.select_topk(self.space, w, oi[w], osc[w], b=B, eps=EPS, alpha=ALPHA, seed=SEED, round_=r,
-                               measured=meas)[0] for w in range(NW)]
+        sel, _ = at.select_topk_batch(self.space, oi, osc, on, b=B, eps=EPS, alpha=ALPHA, seed=SEED, round_=r,
+                                      measured=meas)   # the 12 workloads' selections in one launch
+        sels = list(sel)
         XD = self.space.features(d_idx)
         fit = at.gbt_fit_hist(XD, D_SIZE, cost, self.gkey, n_trees=FIT_TREES, depth=FIT_DEPTH)
         self.last = (oi, osc, on, sels, fit)

@@ -217,6 +217,16 @@ AT_API int select_topk(at_space sp, int32_t workload, const uint64_t *d_pool_idx
                 int64_t n_pool, const uint64_t *d_measured_sorted, int64_t n_measured,
                 const at_select_opts *o, uint64_t *d_out_idx, int32_t *d_out_n, void *stream);
 
+/* select_topk_batch -- select_topk for workloads w0 .. w0 + n_w - 1 in ONE launch (one block per
+ * workload), each from its own pool: pool q at d_pool_idx / d_pool_score + q * pool_stride with
+ * d_pool_n[q] valid entries (device counts, e.g. the out_n of sa_explore / topk_merge; NULL ->
+ * n_pool_max each).  Results d_out_idx [n_w][b], d_out_n [n_w]; bit-identical to n_w select_topk calls
+ * with the same options. */
+AT_API int select_topk_batch(at_space sp, int32_t w0, int32_t n_w, const uint64_t *d_pool_idx,
+                             const float *d_pool_score, int64_t pool_stride, const int32_t *d_pool_n,
+                             int64_t n_pool_max, const uint64_t *d_measured_sorted, int64_t n_measured,
+                             const at_select_opts *o, uint64_t *d_out_idx, int32_t *d_out_n, void *stream);
+
 /* ------------------------------------------------------------------ model update
  * gbt_fit_hist -- histogram GBT under the pairwise rank loss (Eq. 2), refit
  * from scratch (readings Q16, Q17, Q34-Q37): cuts per feature (<= max_bins-1),

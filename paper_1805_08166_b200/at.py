@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
         L.sa_explore.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.POINTER(SaOpts), vp, vp, vp, vp]
         L.topk_merge.argtypes = [vp, vp, vp, vp, i32, i32, vp, i64, i32, vp, vp, vp, vp]
         L.select_topk.argtypes = [vp, i32, vp, vp, i64, vp, i64, C.POINTER(SelectOpts), vp, vp, vp]
+        L.select_topk_batch.argtypes = [vp, i32, i32, vp, vp, i64, vp, i64, vp, i64, C.POINTER(SelectOpts), vp, vp, vp]
         L.gbt_fit_hist.argtypes = [vp, i64, i64, i32, vp, vp, i64, i64, C.POINTER(FitOpts), C.POINTER(vp), vp]
         L.at_exp_det_eval.argtypes = [C.c_uint32, i64, vp, vp]
         L.at_prof_enable.argtypes = [C.c_int]
@@ -337,6 +338,23 @@ def select_topk(space: Space, workload_id, pool_idx, pool_score, *, b, eps, alph
     _check(lib().select_topk(space.h, workload_id, _u64(pool_idx), _ptr(pool_score), pool_idx.numel(),
                              _ptr(measured) if nm else None, nm, C.byref(o), _ptr(out), _ptr(out_n),
                              _stream(stream)))
+    return out, out_n
+
+
+def select_topk_batch(space: Space, pool_idx, pool_score, pool_n=None, *, b, eps, alpha, seed, round_, w0=0,
+                      measured=None, stream=None):
+    """Every workload's selection in one launch: pool_idx / pool_score [n_w][k] (e.g. sa_explore's out_idx /
+    out_score), pool_n [n_w] int32 device counts (or None: all k) -> (out [n_w][b], out_n [n_w])."""
+    import torch
+    n_w, k = pool_idx.shape
+    dev = pool_idx.device
+    o = SelectOpts(b, eps, alpha, seed, round_)
+    out = torch.empty((n_w, max(b, 1)), dtype=torch.int64, device=dev)
+    out_n = torch.empty(n_w, dtype=torch.int32, device=dev)
+    nm = 0 if measured is None else measured.numel()
+    _check(lib().select_topk_batch(space.h, w0, n_w, _u64(pool_idx), _ptr(pool_score), k,
+                                   _ptr(pool_n) if pool_n is not None else None, k, _ptr(measured) if nm else None, nm,
+                                   C.byref(o), _ptr(out), _ptr(out_n), _stream(stream)))
     return out, out_n
 
 

@@ -50,13 +50,15 @@ __device__ __forceinline__ int64_t lower_bound(const uint64_t *a, int64_t n, uin
     return lo;
 }
 
-__global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SpaceDev *__restrict__ S, int w,
+__global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SpaceDev *__restrict__ S, int w0,
                                                             const uint64_t *__restrict__ pool_idx,
-                                                            const float *__restrict__ pool_E, int n_pool,
+                                                            const float *__restrict__ pool_E, int n_pool_max,
+                                                            int64_t pool_stride, const int32_t *__restrict__ d_pool_n,
                                                             const uint64_t *__restrict__ measured,
                                                             int64_t n_measured, int b, float eps, float alpha,
                                                             uint64_t seed, uint32_t round,
-                                                            uint64_t *__restrict__ out, int32_t *__restrict__ out_n)
+                                                            uint64_t *__restrict__ out, int64_t out_stride,
+                                                            int32_t *__restrict__ out_n)
 {
     __shared__ uint64_t s_idx[SEL_MAXPOOL];
     __shared__ double s_z[SEL_MAXPOOL];
@@ -67,6 +69,15 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SpaceDev *__r
     __shared__ double s_mu, s_sigma;
     __shared__ int s_cnt;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // block q selects for workload w0 + q from its own pool (select_topk_batch: one launch for every
+    // workload; select_topk: one block)
+    const int q = blockIdx.x, w = w0 + q;
+    pool_idx += (int64_t)q * pool_stride;
+    pool_E += (int64_t)q * pool_stride;
+    out += (int64_t)q * out_stride;
+    out_n += q;
+    int n_pool = n_pool_max;
+    if (d_pool_n) n_pool = max(0, min(n_pool_max, d_pool_n[q]));
     const WlDev &W = S->w[w];
     const int nk = W.n_knobs;
     for (int i = tid; i < n_pool; i += SEL_THREADS) {
@@ -199,9 +210,36 @@ extern "C" int select_topk(at_space sp, int32_t workload, const uint64_t *d_pool
             return at::fail(AT_EUNSUPPORTED, "select_topk: knob radix > 288");
     cudaStream_t s = (cudaStream_t)stream;
     at::ProfScope ps(AT_K_SELECT, s);
-    at::select_kernel<<<1, at::SEL_THREADS, 0, s>>>(sp->d_space, workload, d_pool_idx, d_pool_score, (int)n_pool,
-                                                    d_measured_sorted, n_measured, o->b, o->eps, o->alpha, o->seed,
-                                                    o->round, d_out_idx, d_out_n); at::note_launch();
+    at::select_kernel<<<1, at::SEL_THREADS, 0, s>>>(sp->d_space, workload, d_pool_idx, d_pool_score, (int)n_pool, 0,
+                                                    nullptr, d_measured_sorted, n_measured, o->b, o->eps, o->alpha,
+                                                    o->seed, o->round, d_out_idx, 0, d_out_n); at::note_launch();
     AT_LAUNCH_CHECK("select_kernel");
+    return AT_OK;
+}
+
+extern "C" int select_topk_batch(at_space sp, int32_t w0, int32_t n_w, const uint64_t *d_pool_idx,
+                                 const float *d_pool_score, int64_t pool_stride, const int32_t *d_pool_n,
+                                 int64_t n_pool_max, const uint64_t *d_measured_sorted, int64_t n_measured,
+                                 const at_select_opts *o, uint64_t *d_out_idx, int32_t *d_out_n, void *stream)
+{
+    if (!sp || !o || !d_out_idx || !d_out_n) return at::fail(AT_EINVAL, "select_topk_batch: null pointer");
+    if (int rc = at::take_range_error(sp)) return rc;
+    if (n_w < 1 || w0 < 0 || w0 + n_w > sp->host.n_w) return at::fail(AT_ERANGE, "select_topk_batch: workloads out of range");
+    if (n_pool_max < 0 || n_pool_max > at::SEL_MAXPOOL) return at::fail(AT_EUNSUPPORTED, "select_topk_batch: pools must hold <= 1024");
+    if (pool_stride < n_pool_max) return at::fail(AT_EMISMATCH, "select_topk_batch: pool_stride < n_pool_max");
+    if (n_pool_max > 0 && (!d_pool_idx || !d_pool_score)) return at::fail(AT_EINVAL, "select_topk_batch: null pools");
+    if (o->b < 0 || !(o->eps >= 0.0f && o->eps <= 1.0f)) return at::fail(AT_EINVAL, "select_topk_batch: need b >= 0, 0 <= eps <= 1");
+    if (n_measured < 0 || (n_measured > 0 && !d_measured_sorted)) return at::fail(AT_EINVAL, "select_topk_batch: bad measured list");
+    for (int q = w0; q < w0 + n_w; ++q)
+        for (int j = 0; j < sp->host.w[q].n_knobs; ++j)
+            if (sp->host.w[q].radix[j] > 32 * at::COV_WORDS)
+                return at::fail(AT_EUNSUPPORTED, "select_topk_batch: knob radix > 288");
+    cudaStream_t s = (cudaStream_t)stream;
+    at::ProfScope ps(AT_K_SELECT, s);
+    at::select_kernel<<<n_w, at::SEL_THREADS, 0, s>>>(sp->d_space, w0, d_pool_idx, d_pool_score, (int)n_pool_max,
+                                                      pool_stride, d_pool_n, d_measured_sorted, n_measured, o->b, o->eps,
+                                                      o->alpha, o->seed, o->round, d_out_idx, o->b > 0 ? o->b : 1, d_out_n);
+    at::note_launch();
+    AT_LAUNCH_CHECK("select_kernel (batch)");
     return AT_OK;
 }

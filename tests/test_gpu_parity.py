@@ -1069,6 +1069,35 @@ def test_topk_drops_measured_over_several_rounds(at):
         assert np.array_equal(host_u64(r["out_idx"][0][:k]), order[n_meas:n_meas + 64]), n_meas
 
 
+def test_select_batch_equals_single_calls_and_oracle(at):
+    """select_topk_batch (one launch, one block per workload, pools with device counts) == select_topk per
+    workload == the oracle, on the 12-workload union with measured exclusions and a short pool."""
+    sp = at.Space(synth.ALL_RESNET)
+    osp = O.OracleSpace([O.workload(**w) for w in synth.ALL_RESNET])
+    k = 40
+    rng = np.random.default_rng(5)
+    idx = np.zeros((12, k), np.uint64)
+    sc = np.zeros((12, k), np.float32)
+    for w in range(12):
+        i = synth.uniform_indices(osp.size(w), k, seed=100 + w, offset=osp.offset(w))
+        e = rng.random(k).astype(np.float32)
+        o = np.lexsort((i, e))
+        idx[w], sc[w] = i[o], e[o]
+    cnt = np.full(12, k, np.int32)
+    cnt[3] = 7                                              # a short pool
+    meas = np.sort(np.concatenate([idx[w, :2] for w in range(0, 12, 2)]))
+    out, on = at.select_topk_batch(sp, u64(idx), dev(sc), dev(cnt), b=16, eps=0.25, alpha=0.1, seed=9, round_=3,
+                                   measured=u64(meas))
+    for w in range(12):
+        n = int(on[w])
+        single, sn = at.select_topk(sp, w, u64(idx[w, :cnt[w]]), dev(sc[w, :cnt[w]]), b=16, eps=0.25, alpha=0.1,
+                                    seed=9, round_=3, measured=u64(meas))
+        assert n == int(sn) == 16
+        assert np.array_equal(host_u64(out[w][:n]), host_u64(single[:n]))
+        ref = osp.select(w, idx[w, :cnt[w]], sc[w, :cnt[w]], 16, 0.25, 0.1, 9, 3, measured=meas)
+        assert np.array_equal(host_u64(out[w][:n]), ref), w
+
+
 @pytest.mark.parametrize("b,want", [(20, 1), (64, 4), (100, 5)])
 def test_select_epsilon_count_matches_oracle(at, b, want):
     """Q26: ceil(eps b) with eps b formed in fp32 (eps = 0.05): GPU selection == oracle selection."""
