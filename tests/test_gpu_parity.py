@@ -1111,6 +1111,43 @@ def test_select_epsilon_count_matches_oracle(at, b, want):
     assert int(n) == b and np.array_equal(host_u64(out[:b]), ref)
 
 
+def test_rank_split_pack_gather_merge_equals_single_rank(at):
+    """The bench's multi-GPU exchange without NCCL: config-3 chains split contiguously over R emulated
+    ranks (each its own sa_explore with its global chain-id base), every rank's per-workload top-k packed
+    into one int64 buffer (dist.pack_lists), the R buffers stacked as all_gather_into_tensor lays them out,
+    unpacked and merged by topk_merge == one sa_explore over all chains; then select_topk_batch on the
+    merged pools == on the single-rank pools ("a batch of parallel Markov chains")."""
+    from paper_1805_08166_b200 import dist as D
+    sp = at.Space(synth.ALL_RESNET)
+    ens = synth.ensemble(200, 8, seed=44)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    n, steps, K = 6000, 12, 32
+    temps = dev(synth.temperatures(steps, synth.energy_scale(200)))
+    meas = u64(np.sort(synth.uniform_indices(sp.size(), 300, seed=5)))
+    cw_all = D.chain_workloads(0, n, 12, "cuda")
+    one = at.sa_explore(sp, g, torch.zeros(n, dtype=torch.int64, device="cuda"), temps, seed=3, round_=1, k_out=K,
+                        chain_workload=cw_all, measured=meas, init=True)
+    for R in (2, 3, 8):
+        bufs = []
+        for r in range(R):
+            base, cnt = D.strong_slice(n, r, R)
+            res = at.sa_explore(sp, g, torch.zeros(cnt, dtype=torch.int64, device="cuda"), temps, seed=3, round_=1,
+                                k_out=K, chain_workload=D.chain_workloads(base, cnt, 12, "cuda"), measured=meas,
+                                init=True, chain_id_base=base)
+            bufs.append(D.pack_lists(res["out_idx"], res["out_score"], res["out_n"]))
+        gi, gs, gn = D.unpack_lists(torch.stack(bufs), 12, K)
+        mi, ms, mn = at.topk_merge(sp, gi, gs, gn, K, measured=meas)
+        assert torch.equal(mn, one["out_n"]), R
+        for w in range(12):
+            k = int(mn[w])
+            assert torch.equal(mi[w][:k], one["out_idx"][w][:k]), (R, w)
+            assert torch.equal(ms[w][:k].view(torch.int32), one["out_score"][w][:k].view(torch.int32)), (R, w)
+        s1, n1 = at.select_topk_batch(sp, mi, ms, mn, b=16, eps=0.05, alpha=0.1, seed=3, round_=1, measured=meas)
+        s0, n0 = at.select_topk_batch(sp, one["out_idx"], one["out_score"], one["out_n"], b=16, eps=0.05, alpha=0.1,
+                                      seed=3, round_=1, measured=meas)
+        assert torch.equal(n1, n0) and torch.equal(s1, s0), R
+
+
 # ------------------------------------------------------------------ Algorithm 1 end to end
 def test_algorithm1_rounds_match_oracle(at):
     """Three rounds of Algorithm 1 (SA -> select -> measure -> refit, persistent chains) through the
