@@ -304,7 +304,7 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
                 if (lane == 0) mbar_arrive(&bar[2 * G.NP + slot]);
             }
         } else {
-            if (lane < G.NP) {
+            if (warp == PW && lane < G.NP) {
                 uint64_t u = c;
                 for (int kk = 0; kk < per; ++kk, ++u) {
                     const int slot = 2 * lane + (int)(u & 1);
@@ -382,7 +382,7 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
             if (walker) {
                 walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots,
                                                 slot_ld, cand0, cand_ok, pend);
-            } else if (c + 1 < c_limit) {
+            } else if (warp == PW && c + 1 < c_limit) {
                 // the producer waits for the NEXT chunk before the block barrier, so the barrier itself
                 // publishes it: the walkers start it without an mbarrier wait of their own
                 const int b1 = (int)((c + 1) & 1);

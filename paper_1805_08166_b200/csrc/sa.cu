@@ -20,7 +20,9 @@
 
 namespace at {
 
-constexpr int SA_NW = 16;
+constexpr int SA_NW = 16;      // walker warps
+constexpr int SA_NWARPS = 17;  // + the tree-stream producer warp, which also takes feature-phase items (an 18th
+                               // warp, so that the 2 x 18 row items take two rounds, measured no faster)
 
 struct TileSink {
     float *tile;
@@ -146,7 +148,7 @@ __device__ __forceinline__ void zero_relation(float (*tile)[NFEAT * 32], int lan
 // state; every warp takes part in every group's feature phases and tree walk, so each tree byte
 // staged in shared memory serves 32 GRP chains.
 template <int GRP, int KM, int TM, bool LG = false>
-__global__ void __launch_bounds__((SA_NW + 1) * 32, 1) sa_kernel(SaParams P, TreeGeo G)
+__global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeGeo G)
 {
     extern __shared__ __align__(128) unsigned char smraw[];
     SaSmem<GRP, KM> &sm = *(SaSmem<GRP, KM> *)smraw;
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__((SA_NW + 1) * 32, 1) sa_kernel(SaParams P, Tre
     // every warp computes its share of the features of all chains of the block
     auto features_phase = [&](int par) {
         // R) context rows and their relation deposits: items (group, row)
-        for (int it = warp; it < GRP * MAXLOOPS && warp < SA_NW; it += SA_NW) {
+        for (int it = warp; it < GRP * MAXLOOPS; it += SA_NWARPS) {
             const int g = it / MAXLOOPS, k = it - g * MAXLOOPS;
             uint32_t chl[MAXKNOBS];
 #pragma unroll
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__((SA_NW + 1) * 32, 1) sa_kernel(SaParams P, Tre
         t_rows += clock64() - t0;
 #endif
         // T) prefix max of the relation slots: items (group, buffer, pair)
-        for (int it = warp; it < GRP * 6 && warp < SA_NW; it += SA_NW) {
+        for (int it = warp; it < GRP * 6; it += SA_NWARPS) {
             const int g = it / 6, r = it - g * 6;
             relation_prefix(sm.tile[g], lane, r >> 1, r & 1);
         }
@@ -588,7 +590,7 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         at::ProfScope ps(AT_K_SA, s);
         const int cpb = use2 ? 64 : 32;
         const unsigned blocks = (unsigned)((o->n_chains + cpb - 1) / cpb);
-        kern<<<blocks, (at::SA_NW + 1) * 32, smem, s>>>(P, G);   // + the tree-stream producer warp
+        kern<<<blocks, at::SA_NWARPS * 32, smem, s>>>(P, G);   // 16 walkers + the producer
         at::note_launch();
         AT_LAUNCH_CHECK("sa_kernel");
     }
