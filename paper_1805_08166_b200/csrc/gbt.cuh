@@ -226,6 +226,49 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
     }
 }
 
+// A chunk of exactly NW trees (one per warp: tree c0 + warp), fp32 nodes, compile-time depth D: the
+// walk of the SA kernel's streamed depth-6..8 chunks without walk_chunk's batch dispatch and with the
+// level loop unrolled (the per-chunk setup was ~15 % of the kernel's stall samples); sums exactly as
+// walk_batch<NB = 1> does (tree t adds its leaf to class t mod 32 in ascending t).
+template <int NW, int GRP, int D>
+__device__ __forceinline__ void walk_one(const TreeGeo &G, const uint8_t *buf, int c0, const float *tile, int gstride,
+                                         int lane, int warp, float (&p)[GRP][1][32 / NW])
+{
+    constexpr int NQ = 32 / NW;
+    constexpr int ni = (1 << D) - 1, nl = 1 << D;
+    const int t = c0 + warp;
+    if (t >= G.T) return;
+    const uint32_t tb = (uint32_t)__cvta_generic_to_shared(buf) + (uint32_t)warp * (uint32_t)(ni * 8) - 8u;
+    const uint32_t add_l = 0u - tb, add_r = 8u - tb;
+    const uint32_t tile0 = (uint32_t)__cvta_generic_to_shared(tile + lane);
+    uint32_t a[GRP];
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) a[g] = tb + 8u;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) {
+            uint32_t nf, nt;
+            float x;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g]));
+            AT_DCHECK(nf < (uint32_t)(gstride / 32));
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)(g * gstride * 4) + (nf << 7)));
+            a[g] = 2u * a[g] + (x < __uint_as_float(nt) ? add_l : add_r);
+        }
+    }
+    const float *leaves = (const float *)(buf + (size_t)G.CH * ni * 8);
+    const int j = (t & 31) / NW;
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) {
+        const int slot = (int)((a[g] + add_l) >> 3) - nl;
+        AT_DCHECK(slot >= 0 && slot < nl);
+        const float lv = leaves[warp * nl + slot];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if (q == j) p[g][0][q] = __fadd_rn(p[g][0][q], lv);
+    }
+}
+
 // Walk one staged chunk [c0, c1): every warp takes the trees of its residue classes (t = warp mod NW)
 // in ascending order, in batches of up to 4 / GRP trees; no walk slot is spent on an absent tree,
 // whatever the chunk size.  GRP candidate groups of 32 (group g's tile at tile + g * gstride floats)
@@ -380,8 +423,25 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
             long long q1 = clock64();
 #endif
             if (walker) {
-                walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p, slots,
-                                                slot_ld, cand0, cand_ok, pend);
+                // one tree per warp (the SA kernel's chunks): the specialised walk for depths 6 .. 8
+                uint8_t *cb = bufs + (size_t)b * G.chunk_bytes;
+                bool done = false;
+                if constexpr (PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG) {   // (GRP = 1 chunks hold more trees)
+                    if (G.CH == NW && slots == nullptr) {
+                        done = true;
+                        if (G.D == 8)
+                            walk_one<NW, GRP, 8>(G, cb, k * NW, (const float *)tile, gstride, lane, warp, p);
+                        else if (G.D == 7)
+                            walk_one<NW, GRP, 7>(G, cb, k * NW, (const float *)tile, gstride, lane, warp, p);
+                        else if (G.D == 6)
+                            walk_one<NW, GRP, 6>(G, cb, k * NW, (const float *)tile, gstride, lane, warp, p);
+                        else
+                            done = false;
+                    }
+                }
+                if (!done)
+                    walk_chunk<NW, GRP, KM, RK, LG>(G, cb, k, tile, gstride, lane, warp, p, slots, slot_ld, cand0,
+                                                    cand_ok, pend);
             } else if (warp == PW && c + 1 < c_limit) {
                 // the producer waits for the NEXT chunk before the block barrier, so the barrier itself
                 // publishes it: the walkers start it without an mbarrier wait of their own

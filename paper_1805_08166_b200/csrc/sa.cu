@@ -21,8 +21,8 @@
 namespace at {
 
 constexpr int SA_NW = 16;      // walker warps
-constexpr int SA_NWARPS = 17;  // + the tree-stream producer warp, which also takes feature-phase items (an 18th
-                               // warp, so that the 2 x 18 row items take two rounds, measured no faster)
+constexpr int SA_NWARPS = 17;  // + the tree-stream producer warp (feature-phase items stay with the walkers:
+                               // giving the producer some, or an 18th warp, measured no faster)
 
 struct TileSink {
     float *tile;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeG
     // every warp computes its share of the features of all chains of the block
     auto features_phase = [&](int par) {
         // R) context rows and their relation deposits: items (group, row)
-        for (int it = warp; it < GRP * MAXLOOPS; it += SA_NWARPS) {
+        for (int it = warp; it < GRP * MAXLOOPS && warp < SA_NW; it += SA_NW) {
             const int g = it / MAXLOOPS, k = it - g * MAXLOOPS;
             uint32_t chl[MAXKNOBS];
 #pragma unroll
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeG
         t_rows += clock64() - t0;
 #endif
         // T) prefix max of the relation slots: items (group, buffer, pair)
-        for (int it = warp; it < GRP * 6; it += SA_NWARPS) {
+        for (int it = warp; it < GRP * 6 && warp < SA_NW; it += SA_NW) {
             const int g = it / 6, r = it - g * 6;
             relation_prefix(sm.tile[g], lane, r >> 1, r & 1);
         }
