@@ -226,46 +226,75 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
     }
 }
 
-// A chunk of exactly NW trees (one per warp: tree c0 + warp), fp32 nodes, compile-time depth D: the
-// walk of the SA kernel's streamed depth-6..8 chunks without walk_chunk's batch dispatch and with the
-// level loop unrolled (the per-chunk setup was ~15 % of the kernel's stall samples); sums exactly as
-// walk_batch<NB = 1> does (tree t adds its leaf to class t mod 32 in ascending t).
-template <int NW, int GRP, int D>
-__device__ __forceinline__ void walk_one(const TreeGeo &G, const uint8_t *buf, int c0, const float *tile, int gstride,
-                                         int lane, int warp, float (&p)[GRP][1][32 / NW])
+// One pass over a streamed ensemble whose chunks hold exactly NW trees (one per walker warp: tree
+// NW k + warp of chunk k), fp32 nodes, compile-time depth D, with a producer warp PW: the SA kernel's
+// depth-6..8 walk.  Everything that does not change from chunk to chunk -- the warp's tree base in
+// either buffer, its leaf row, the lane's tile address, the depth dispatch -- is computed once per
+// pass, so a chunk starts walking right after the barrier (the per-chunk setup of the generic
+// walk_chunk was ~25 % of the kernel's stall samples).  Sums exactly as walk_batch<NB = 1> does: tree
+// t adds its leaf to class t mod 32 in ascending t.
+template <int NW, int GRP, int D, int PW>
+__device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph,
+                                                uint64_t &c, uint64_t c_limit, const float *tile, int gstride,
+                                                int lane, int warp, float (&p)[GRP][1][32 / NW])
 {
     constexpr int NQ = 32 / NW;
-    constexpr int ni = (1 << D) - 1, nl = 1 << D;
-    const int t = c0 + warp;
-    if (t >= G.T) return;
-    const uint32_t tb = (uint32_t)__cvta_generic_to_shared(buf) + (uint32_t)warp * (uint32_t)(ni * 8) - 8u;
-    const uint32_t add_l = 0u - tb, add_r = 8u - tb;
+    constexpr uint32_t ni = (1u << D) - 1u, nl = 1u << D;
+    const bool walker = warp < PW;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(bufs);
+    const uint32_t tbw = sb + (uint32_t)warp * ni * 8u - 8u;                       // + buffer offset
+    const uint32_t lfw = sb + (uint32_t)G.CH * ni * 8u + (uint32_t)warp * nl * 4u;  // + buffer offset
     const uint32_t tile0 = (uint32_t)__cvta_generic_to_shared(tile + lane);
-    uint32_t a[GRP];
-#pragma unroll
-    for (int g = 0; g < GRP; ++g) a[g] = tb + 8u;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-#pragma unroll
-        for (int g = 0; g < GRP; ++g) {
-            uint32_t nf, nt;
-            float x;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g]));
-            AT_DCHECK(nf < (uint32_t)(gstride / 32));
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)(g * gstride * 4) + (nf << 7)));
-            a[g] = 2u * a[g] + (x < __uint_as_float(nt) ? add_l : add_r);
+    const uint32_t gbytes = (uint32_t)gstride * 4u;
+    const int T = G.T, NC = G.NC;
+    const uint32_t cbytes = G.chunk_bytes;
+    for (int k = 0; k < NC; ++k, ++c) {
+        const uint32_t boff = (c & 1) ? cbytes : 0u;
+        if (c == 0) {   // the kernel's first chunk; later ones are waited for by the producer (below)
+            mbar_wait(&bar[0], ph[0]);
+            ph[0] ^= 1u;
         }
-    }
-    const float *leaves = (const float *)(buf + (size_t)G.CH * ni * 8);
-    const int j = (t & 31) / NW;
+        const int t = k * NW + warp;
+        if (walker && t < T) {
+            const uint32_t tb = tbw + boff;
+            const uint32_t add_l = 0u - tb, add_r = 8u - tb;
+            uint32_t a[GRP];
 #pragma unroll
-    for (int g = 0; g < GRP; ++g) {
-        const int slot = (int)((a[g] + add_l) >> 3) - nl;
-        AT_DCHECK(slot >= 0 && slot < nl);
-        const float lv = leaves[warp * nl + slot];
+            for (int g = 0; g < GRP; ++g) a[g] = tb + 8u;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-            if (q == j) p[g][0][q] = __fadd_rn(p[g][0][q], lv);
+            for (int d = 0; d < D; ++d) {
+#pragma unroll
+                for (int g = 0; g < GRP; ++g) {
+                    uint32_t nf, nt;
+                    float x;
+                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g]));
+                    AT_DCHECK(nf < (uint32_t)(gstride / 32));
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
+                    a[g] = 2u * a[g] + (x < __uint_as_float(nt) ? add_l : add_r);
+                }
+            }
+            const int j = (t & 31) / NW;
+#pragma unroll
+            for (int g = 0; g < GRP; ++g) {
+                const uint32_t slot = ((a[g] + add_l) >> 3) - nl;
+                AT_DCHECK(slot < nl);
+                float lv;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lv) : "r"(lfw + boff + slot * 4u));
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    if (q == j) p[g][0][q] = __fadd_rn(p[g][0][q], lv);
+            }
+        } else if (warp == PW && c + 1 < c_limit) {
+            // the producer waits for the NEXT chunk before the block barrier, so the barrier publishes it
+            const int b1 = (int)((c + 1) & 1);
+            mbar_wait(&bar[b1], ph[b1]);
+            ph[b1] ^= 1u;
+        }
+        __syncthreads();   // every warp is done with this chunk's buffer
+        if (warp == PW && lane == 0 && c + 2 < c_limit) {
+            fence_proxy_async();
+            ts_issue(G, bufs, bar, c + 2);
+        }
     }
 }
 
@@ -330,6 +359,9 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
     LeafPend<GRP, walk_nbmax<GRP, KM>()> pend;
     pend.n = 0;
     const bool walker = PW < 0 || warp < PW;
+    // the SA kernel's streamed chunks of one tree per walker warp (two chain groups, depth 6..8)
+    const bool stream_one = PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG && !G.resident && !G.ring && G.NP <= 1 &&
+                            G.CH == NW && slots == nullptr && G.D >= 6 && G.D <= 8;
     if (PW >= 0 && G.NP > 1) {
         // NP independent pipelines, no block barrier: warp group p (NW / NP warps) walks its slices -- each
         // warp one tree per slice -- waiting on the slot's full barrier and counting out on its empty
@@ -409,6 +441,16 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
                 }
             }
         }
+    } else if (stream_one) {
+        if constexpr (PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG) {
+            const float *tf = (const float *)tile;
+            if (G.D == 8)
+                walk_stream_one<NW, GRP, 8, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
+            else if (G.D == 7)
+                walk_stream_one<NW, GRP, 7, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
+            else
+                walk_stream_one<NW, GRP, 6, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
+        }
     } else {
         for (int k = 0; k < G.NC; ++k, ++c) {
             const int b = (int)(c & 1);
@@ -423,25 +465,8 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
             long long q1 = clock64();
 #endif
             if (walker) {
-                // one tree per warp (the SA kernel's chunks): the specialised walk for depths 6 .. 8
-                uint8_t *cb = bufs + (size_t)b * G.chunk_bytes;
-                bool done = false;
-                if constexpr (PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG) {   // (GRP = 1 chunks hold more trees)
-                    if (G.CH == NW && slots == nullptr) {
-                        done = true;
-                        if (G.D == 8)
-                            walk_one<NW, GRP, 8>(G, cb, k * NW, (const float *)tile, gstride, lane, warp, p);
-                        else if (G.D == 7)
-                            walk_one<NW, GRP, 7>(G, cb, k * NW, (const float *)tile, gstride, lane, warp, p);
-                        else if (G.D == 6)
-                            walk_one<NW, GRP, 6>(G, cb, k * NW, (const float *)tile, gstride, lane, warp, p);
-                        else
-                            done = false;
-                    }
-                }
-                if (!done)
-                    walk_chunk<NW, GRP, KM, RK, LG>(G, cb, k, tile, gstride, lane, warp, p, slots, slot_ld, cand0,
-                                                    cand_ok, pend);
+                walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p,
+                                                slots, slot_ld, cand0, cand_ok, pend);
             } else if (warp == PW && c + 1 < c_limit) {
                 // the producer waits for the NEXT chunk before the block barrier, so the barrier itself
                 // publishes it: the walkers start it without an mbarrier wait of their own
