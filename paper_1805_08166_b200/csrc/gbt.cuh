@@ -248,21 +248,34 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
     const uint32_t gbytes = (uint32_t)gstride * 4u;
     const int T = G.T, NC = G.NC;
     const uint32_t cbytes = G.chunk_bytes;
-    for (int k = 0; k < NC; ++k, ++c) {
-        const uint32_t boff = (c & 1) ? cbytes : 0u;
-        if (c == 0) {   // the kernel's first chunk; later ones are waited for by the producer (below)
+    // 32-bit stream counters (c_limit < 2^32) and running per-chunk values: no 64-bit or multiply in the
+    // chunk loop's critical path
+    uint32_t cc = (uint32_t)c;
+    const uint32_t climit = (uint32_t)c_limit;
+    uint32_t boff = (cc & 1u) ? cbytes : 0u;
+    int t = warp;
+    for (int k = 0; k < NC; ++k, ++cc, t += NW, boff ^= cbytes) {
+        if (cc == 0u) {   // the kernel's first chunk; later ones are waited for by the producer (below)
             mbar_wait(&bar[0], ph[0]);
             ph[0] ^= 1u;
         }
-        const int t = k * NW + warp;
         if (walker && t < T) {
             const uint32_t tb = tbw + boff;
             const uint32_t add_l = 0u - tb, add_r = 8u - tb;
             uint32_t a[GRP];
+            {   // the root: one node load serves every group
+                uint32_t nf, nt;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(tb + 8u));
+                AT_DCHECK(nf < (uint32_t)(gstride / 32));
 #pragma unroll
-            for (int g = 0; g < GRP; ++g) a[g] = tb + 8u;
+                for (int g = 0; g < GRP; ++g) {
+                    float x;
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
+                    a[g] = 2u * (tb + 8u) + (x < __uint_as_float(nt) ? add_l : add_r);
+                }
+            }
 #pragma unroll
-            for (int d = 0; d < D; ++d) {
+            for (int d = 1; d < D; ++d) {
 #pragma unroll
                 for (int g = 0; g < GRP; ++g) {
                     uint32_t nf, nt;
@@ -284,18 +297,19 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
                 for (int q = 0; q < NQ; ++q)
                     if (q == j) p[g][0][q] = __fadd_rn(p[g][0][q], lv);
             }
-        } else if (warp == PW && c + 1 < c_limit) {
+        } else if (warp == PW && cc + 1u < climit) {
             // the producer waits for the NEXT chunk before the block barrier, so the barrier publishes it
-            const int b1 = (int)((c + 1) & 1);
+            const int b1 = (int)((cc + 1u) & 1u);
             mbar_wait(&bar[b1], ph[b1]);
             ph[b1] ^= 1u;
         }
         __syncthreads();   // every warp is done with this chunk's buffer
-        if (warp == PW && lane == 0 && c + 2 < c_limit) {
+        if (warp == PW && lane == 0 && cc + 2u < climit) {
             fence_proxy_async();
-            ts_issue(G, bufs, bar, c + 2);
+            ts_issue(G, bufs, bar, (uint64_t)cc + 2u);
         }
     }
+    c = cc;
 }
 
 // Walk one staged chunk [c0, c1): every warp takes the trees of its residue classes (t = warp mod NW)
