@@ -457,13 +457,17 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     // chain lists per workload (multi-workload spaces): the top-k then reads only a workload's own keys
     const bool lists = d_chain_workload && sp->host.n_w > 1;
     const size_t list_bytes = lists ? (((size_t)sp->host.n_w * o->n_chains + at::MAXW) * sizeof(int32_t) + 255) / 256 * 256 : 0;
-    int rc = at::scratch_reserve(sp, key_bytes + list_bytes + at::topk_scratch_bytes(n_keys, o->k_out, lists ? sp->host.n_w : 1),
-                                 s);
+    const int nbt = lists ? sp->host.n_w : 1;
+    const size_t tk_bytes = (at::topk_scratch_bytes(n_keys, o->k_out, nbt) + 255) / 256 * 256;
+    const size_t fast_bytes = at::topk_fast_scratch_bytes(nbt) + 256;
+    int rc = at::scratch_reserve(sp, key_bytes + list_bytes + tk_bytes + fast_bytes, s);
     if (rc) return rc;
     uint64_t *keys = (uint64_t *)sp->d_scratch;
     int32_t *chain_list = lists ? (int32_t *)((char *)sp->d_scratch + key_bytes) : nullptr;
     int32_t *list_n = lists ? chain_list + (size_t)sp->host.n_w * o->n_chains : nullptr;
     uint64_t *tkbuf = (uint64_t *)((char *)sp->d_scratch + key_bytes + list_bytes);
+    uint8_t *fastbuf = (uint8_t *)sp->d_scratch + key_bytes + list_bytes + tk_bytes;
+    int32_t *fb = (int32_t *)(fastbuf + at::topk_fast_scratch_bytes(nbt));   // [nbt] fall-back flags
 
     at::SaParams P{};
     P.S = sp->d_space;
@@ -624,7 +628,18 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
         }
         uint64_t offs[at::MAXW];
         for (int q = 0; q < at::MAXW; ++q) offs[q] = q < sp->host.n_w ? sp->host.offset[q] : 0;
-        rc = at::topk_run(a, tkbuf, s, nb, offs);
+        // the threshold fast path settles (almost) every workload; the exact tile reduction then runs only
+        // for the rows it flagged (AT_TOPK_FAST=0: the tile reduction alone)
+        static int fast_env = -1;
+        if (fast_env < 0) {
+            const char *e = getenv("AT_TOPK_FAST");
+            fast_env = e ? atoi(e) : 1;
+        }
+        if (fast_env) {
+            rc = at::topk_fast(a, nb, offs, per, fastbuf, fb, s);
+            if (rc) return rc;
+        }
+        rc = at::topk_run(a, tkbuf, s, nb, offs, fast_env ? fb : nullptr);
         if (rc) return rc;
     }
     return AT_OK;

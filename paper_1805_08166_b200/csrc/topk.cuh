@@ -31,6 +31,12 @@ size_t topk_scratch_bytes(int64_t n_src, int K, int n_batch = 1);
 void topk_chain_lists(const uint16_t *chain_w, int64_t n_chains, int n_w, int32_t *list, int32_t *cnt, cudaStream_t s);
 // n_batch > 1: workloads a.w .. a.w + n_batch - 1 in one launch per pass, outputs in consecutive
 // rows; offsets[w] = each workload's global index offset (nullptr: a.offset_w for all)
-int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s, int n_batch = 1, const uint64_t *offsets = nullptr);
+int topk_run(const TkArgs &a, uint64_t *scratch, cudaStream_t s, int n_batch = 1, const uint64_t *offsets = nullptr,
+             const int32_t *fb = nullptr);
+// threshold fast path for SA keys (mode 0): settles most workloads in 4 short launches; a row it cannot
+// settle gets fb[y] = 1, and topk_run(..., fb) then reduces that row alone (the others return at once)
+size_t topk_fast_scratch_bytes(int n_batch);
+int topk_fast(const TkArgs &a, int n_batch, const uint64_t *offsets, int64_t per, uint8_t *scratch, int32_t *fb,
+              cudaStream_t s);
 
 }  // namespace at

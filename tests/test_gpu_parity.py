@@ -1098,6 +1098,43 @@ def test_select_batch_equals_single_calls_and_oracle(at):
         assert np.array_equal(host_u64(out[w][:n]), ref), w
 
 
+def test_topk_fast_path_and_its_fallback(at):
+    """Alg. 1 P:152 / Q23 through the top-k threshold fast path: (1) a long run on the 2,000-config matmul
+    space, where 4096 greedy chains pile onto a few local minima -- the candidates below the threshold
+    are mostly duplicates, so the fast path must hand the workload to the exact tile reduction; (2) a
+    12-workload union with measured configurations, settled by the fast path.  Both == the oracle."""
+    sp = at.Space([synth.MATMUL_8])
+    osp = O.OracleSpace([O.workload(**synth.MATMUL_8)])
+    ens = synth.ensemble(30, 5, seed=12)
+    n, steps = 4096, 40
+    temps = np.zeros(steps, np.float32)
+    r = at.sa_explore(sp, at.Gbt(ens["feat"], ens["thresh"], ens["leaf"]), torch.zeros(n, dtype=torch.int64, device="cuda"),
+                      dev(temps), seed=4, round_=0, k_out=64, init=True, visited=True)
+    (oi, oE), = osp.topk(r["visited_E"].cpu().numpy().ravel(), host_u64(r["visited_idx"]).ravel(), 64)
+    k = int(r["out_n"][0])
+    assert k == len(oi)
+    assert np.array_equal(host_u64(r["out_idx"][0][:k]), oi)
+    assert_bits_equal(r["out_score"][0][:k].cpu().numpy(), oE, "scores")
+    # union with measured configurations
+    ens2 = synth.ensemble(60, 6, seed=13)
+    n2, st2 = 3000, 30
+    cw = (np.arange(n2) % 12).astype(np.uint16)
+    sp2 = at.Space(synth.ALL_RESNET)
+    osp2 = O.OracleSpace([O.workload(**w) for w in synth.ALL_RESNET])
+    t2 = synth.temperatures(st2, synth.energy_scale(60))
+    g2 = at.Gbt(ens2["feat"], ens2["thresh"], ens2["leaf"])
+    r0 = at.sa_explore(sp2, g2, torch.zeros(n2, dtype=torch.int64, device="cuda"), dev(t2), seed=6, round_=0, k_out=32,
+                       chain_workload=dev(cw.view(np.int16)), init=True)
+    meas = np.sort(np.concatenate([host_u64(r0["out_idx"][w][:10]) for w in range(12)]))
+    r2 = at.sa_explore(sp2, g2, torch.zeros(n2, dtype=torch.int64, device="cuda"), dev(t2), seed=6, round_=0, k_out=32,
+                       chain_workload=dev(cw.view(np.int16)), init=True, measured=u64(meas), visited=True)
+    tops = osp2.topk(r2["visited_E"].cpu().numpy().ravel(), host_u64(r2["visited_idx"]).ravel(), 32, measured=meas)
+    for w, (oi2, oE2) in enumerate(tops):
+        k2 = int(r2["out_n"][w])
+        assert k2 == len(oi2)
+        assert np.array_equal(host_u64(r2["out_idx"][w][:k2]), oi2), w
+
+
 @pytest.mark.parametrize("b,want", [(20, 1), (64, 4), (100, 5)])
 def test_select_epsilon_count_matches_oracle(at, b, want):
     """Q26: ceil(eps b) with eps b formed in fp32 (eps = 0.05): GPU selection == oracle selection."""
