@@ -312,6 +312,91 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
     c = cc;
 }
 
+// The rank-form counterpart for gbt_predict's streamed depth-6..8 ensembles: chunks of TPW NW trees,
+// TPW trees per walker warp (tree NW (TPW k + jj) + warp, jj < TPW), walked for GRP candidate groups
+// at once (TPW GRP independent chains), 4-byte nodes {k | tile byte offset << 16} against u16
+// feature ranks (x < theta <=> rank < k).  Per-pass constants hoisted as in walk_stream_one; leaves
+// added in ascending t per residue class (jj ascending = t ascending).
+template <int NW, int GRP, int D, int PW, int TPW>
+__device__ __forceinline__ void walk_stream_rank(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph,
+                                                 uint64_t &c, uint64_t c_limit, const uint32_t *tile, int gstride,
+                                                 int lane, int warp, float (&p)[GRP][1][32 / NW])
+{
+    constexpr int NQ = 32 / NW;
+    constexpr uint32_t ni = (1u << D) - 1u, nl = 1u << D;
+    const bool walker = warp < PW;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(bufs);
+    const uint32_t tbw = sb + (uint32_t)warp * ni * 4u - 4u;                       // + buffer + jj NW trees
+    const uint32_t lfw = sb + (uint32_t)G.CH * ni * 4u + (uint32_t)warp * nl * 4u;  // + buffer + jj NW leaf rows
+    const uint32_t tile0 = (uint32_t)__cvta_generic_to_shared(tile + lane);
+    const uint32_t gbytes = (uint32_t)gstride * 4u;
+    const int T = G.T, NC = G.NC;
+    const uint32_t cbytes = G.chunk_bytes;
+    uint32_t cc = (uint32_t)c;
+    const uint32_t climit = (uint32_t)c_limit;
+    uint32_t boff = (cc & 1u) ? cbytes : 0u;
+    int t = warp;
+    for (int k = 0; k < NC; ++k, ++cc, t += TPW * NW, boff ^= cbytes) {
+        if (cc == 0u) {
+            mbar_wait(&bar[0], ph[0]);
+            ph[0] ^= 1u;
+        }
+        if (walker && t < T) {
+            uint32_t a[TPW][GRP], add_l[TPW], add_r[TPW];
+#pragma unroll
+            for (int jj = 0; jj < TPW; ++jj) {
+                const uint32_t tb = tbw + boff + (uint32_t)(jj * NW) * ni * 4u;
+                add_l[jj] = 0u - tb;
+                add_r[jj] = 4u - tb;
+#pragma unroll
+                for (int g = 0; g < GRP; ++g) a[jj][g] = tb + 4u;
+            }
+            const bool two = TPW > 1 && t + NW < T;   // warp-uniform: the chunk's second tree exists
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+#pragma unroll
+                for (int jj = 0; jj < TPW; ++jj) {
+                    if (jj > 0 && !two) break;
+#pragma unroll
+                    for (int g = 0; g < GRP; ++g) {
+                        uint32_t nd, x;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nd) : "r"(a[jj][g]));
+                        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nd >> 16)));
+                        a[jj][g] = 2u * a[jj][g] + (x < (nd & 0xFFFFu) ? add_l[jj] : add_r[jj]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < TPW; ++jj) {
+                if (jj > 0 && !two) break;
+                const int j = ((t + jj * NW) & 31) / NW;
+#pragma unroll
+                for (int g = 0; g < GRP; ++g) {
+                    const uint32_t slot = ((a[jj][g] + add_l[jj]) >> 2) - nl;
+                    AT_DCHECK(slot < nl);
+                    float lv;
+                    asm volatile("ld.shared.f32 %0, [%1];"
+                                 : "=f"(lv)
+                                 : "r"(lfw + boff + (uint32_t)(jj * NW) * nl * 4u + slot * 4u));
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        if (q == j) p[g][0][q] = __fadd_rn(p[g][0][q], lv);
+                }
+            }
+        } else if (warp == PW && cc + 1u < climit) {
+            const int b1 = (int)((cc + 1u) & 1u);
+            mbar_wait(&bar[b1], ph[b1]);
+            ph[b1] ^= 1u;
+        }
+        __syncthreads();
+        if (warp == PW && lane == 0 && cc + 2u < climit) {
+            fence_proxy_async();
+            ts_issue(G, bufs, bar, (uint64_t)cc + 2u);
+        }
+    }
+    c = cc;
+}
+
 // Walk one staged chunk [c0, c1): every warp takes the trees of its residue classes (t = warp mod NW)
 // in ascending order, in batches of up to 4 / GRP trees; no walk slot is spent on an absent tree,
 // whatever the chunk size.  GRP candidate groups of 32 (group g's tile at tile + g * gstride floats)
@@ -374,6 +459,9 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
     pend.n = 0;
     const bool walker = PW < 0 || warp < PW;
     // the SA kernel's streamed chunks of one tree per walker warp (two chain groups, depth 6..8)
+    // gbt_predict's streamed rank-form depth-7/8 chunks of NW or 2 NW trees
+    const bool stream_rank = PW >= 0 && KM == 1 && RK && !LG && !G.resident && !G.ring && G.NP <= 1 &&
+                             (G.CH == NW || G.CH == 2 * NW) && slots == nullptr && G.D >= 7 && G.D <= 8;
     const bool stream_one = PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG && !G.resident && !G.ring && G.NP <= 1 &&
                             G.CH == NW && slots == nullptr && G.D >= 6 && G.D <= 8;
     if (PW >= 0 && G.NP > 1) {
@@ -454,6 +542,19 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
                     }
                 }
             }
+        }
+    } else if (stream_rank) {
+        if constexpr (PW >= 0 && KM == 1 && RK && !LG) {
+            const uint32_t *tu = (const uint32_t *)tile;
+            const int tpw = G.CH / NW;
+            if (G.D == 8 && tpw == 2)
+                walk_stream_rank<NW, GRP, 8, PW, 2>(G, bufs, bar, ph, c, c_limit, tu, gstride, lane, warp, p);
+            else if (G.D == 8)
+                walk_stream_rank<NW, GRP, 8, PW, 1>(G, bufs, bar, ph, c, c_limit, tu, gstride, lane, warp, p);
+            else if (G.D == 7 && tpw == 2)
+                walk_stream_rank<NW, GRP, 7, PW, 2>(G, bufs, bar, ph, c, c_limit, tu, gstride, lane, warp, p);
+            else
+                walk_stream_rank<NW, GRP, 7, PW, 1>(G, bufs, bar, ph, c, c_limit, tu, gstride, lane, warp, p);
         }
     } else if (stream_one) {
         if constexpr (PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG) {
