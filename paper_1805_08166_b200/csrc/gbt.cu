@@ -434,10 +434,16 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
     // the rank tables are built (once) from the model as its last writer left it, then this stream owns it
     const int rk_ok = want_rk ? build_rank_form(g) : 0;
     g->last = s;
-    // AT_RK_GRP: candidate groups per tile (2: 32-tree chunks, default; 4: 16-tree chunks -- the same
-    // walks in flight per warp, half the tiles: equal at 10^7+ candidates, worse balanced below)
+    // candidate groups per tile: 4 (16-tree chunks: every streamed tree byte serves 128 candidates) when
+    // there are >= 8 tiles per SM to balance, else 2 (32-tree chunks); with the streamed rank walk
+    // (walk_stream_rank) 4 groups run config 5 at 10^7 candidates 1.18x faster.  AT_RK_GRP=2|4 forces it
     const char *rg_e = getenv("AT_RK_GRP");
-    const int RGRP = rg_e && atoi(rg_e) == 4 ? 4 : 2;
+    int nsm_rk = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm_rk, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int RGRP = rg_e ? (atoi(rg_e) == 4 ? 4 : 2) : (n >= (int64_t)nsm_rk * 8 * 128 ? 4 : 2);
     if (want_rk && rk_ok == 1) {
         const int P = (F + 1) / 2;   // u32 rank pairs per candidate
         const int pn_box = (P + 255) / 256, pbox_rows = (P + pn_box - 1) / pn_box, ptile_rows = pn_box * pbox_rows;
