@@ -35,6 +35,8 @@ struct TreeGeo {
     int leaf_global;        // 1: chunks carry the nodes only; a walk's leaf is read from global memory
                             // (L2) and added one batch later (walk_batch<..., LG>), so the tree buffers
                             // hold 1.5x the trees of a depth-8 ensemble
+    int eb;                 // 1 (walk_stream_one only): no chunk barrier -- walkers wait on the chunk's full
+                            // mbarrier and count out on its empty mbarrier; the producer refills after it
     int NP;                 // > 1: NP independent tree pipelines (walk_pass): warp group p of NW / NP warps
                             // streams its own slices of CH = NW / NP trees through its own two buffers,
                             // with full / empty mbarriers and no block barrier; NC counts slices
@@ -112,6 +114,7 @@ __device__ __forceinline__ void ts_start(const TreeGeo &G, uint8_t *bufs, uint64
         for (int b = 0; b < G.NBUF; ++b) {
             mbar_init(&bar[b], 1);
             if (G.ring) ((unsigned *)(bar + G.NBUF))[b] = 0u;
+            if (G.eb) mbar_init(&bar[G.NBUF + b], 16);   // empty: one arrival per walker warp
         }
         fence_proxy_async();
         for (int b = 0; b < G.NBUF && b < G.NC; ++b) ts_issue(G, bufs, bar, (uint64_t)b);
@@ -254,6 +257,63 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
     const uint32_t climit = (uint32_t)c_limit;
     uint32_t boff = (cc & 1u) ? cbytes : 0u;
     int t = warp;
+    if (G.eb) {
+        // no chunk barrier: walkers wait on the chunk's full barrier and count out on its empty barrier;
+        // the producer refills a buffer as soon as all walkers left it
+        for (int k = 0; k < NC; ++k, ++cc, t += NW, boff ^= cbytes) {
+            const int b = (int)(cc & 1u);
+            const uint32_t par = (cc >> 1) & 1u;
+            if (walker) {
+                mbar_wait(&bar[b], par);
+                if (t < T) {
+                    const uint32_t tb = tbw + boff;
+                    const uint32_t add_l = 0u - tb, add_r = 8u - tb;
+                    uint32_t a[GRP];
+                    {
+                        uint32_t nf, nt;
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(tb + 8u));
+#pragma unroll
+                        for (int g = 0; g < GRP; ++g) {
+                            float x;
+                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
+                            a[g] = 2u * (tb + 8u) + (x < __uint_as_float(nt) ? add_l : add_r);
+                        }
+                    }
+#pragma unroll
+                    for (int d = 1; d < D; ++d) {
+#pragma unroll
+                        for (int g = 0; g < GRP; ++g) {
+                            uint32_t nf, nt;
+                            float x;
+                            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g]));
+                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
+                            a[g] = 2u * a[g] + (x < __uint_as_float(nt) ? add_l : add_r);
+                        }
+                    }
+                    const int j = (t & 31) / NW;
+#pragma unroll
+                    for (int g = 0; g < GRP; ++g) {
+                        const uint32_t slot = ((a[g] + add_l) >> 3) - nl;
+                        float lv;
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lv) : "r"(lfw + boff + slot * 4u));
+#pragma unroll
+                        for (int q = 0; q < NQ; ++q)
+                            if (q == j) p[g][0][q] = __fadd_rn(p[g][0][q], lv);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar[2 + b]);
+            } else if (warp == PW && lane == 0) {
+                mbar_wait(&bar[2 + b], par);   // every walker left chunk cc
+                if (cc + 2u < climit) {
+                    fence_proxy_async();
+                    ts_issue(G, bufs, bar, (uint64_t)cc + 2u);
+                }
+            }
+        }
+        c = cc;
+        return;
+    }
     for (int k = 0; k < NC; ++k, ++cc, t += NW, boff ^= cbytes) {
         if (cc == 0u) {   // the kernel's first chunk; later ones are waited for by the producer (below)
             mbar_wait(&bar[0], ph[0]);
@@ -619,7 +679,7 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
     }
     // a resident pass has no per-chunk barrier: every warp must be done reading the tile before the
     // partials are written (sa_kernel keeps them in the tile's first columns)
-    if (G.resident || G.NP > 1) __syncthreads();
+    if (G.resident || G.NP > 1 || G.eb) __syncthreads();
 #pragma unroll
     for (int g = 0; g < GRP && walker; ++g)
 #pragma unroll

@@ -552,7 +552,13 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     const size_t hdr1 = ((sizeof(at::SaSmem<1>) + 127) / 128) * 128;
     at::TreeGeo G1 = geo(hdr1);
     const size_t hdr2 = ((sizeof(at::SaSmem<2>) + 127) / 128) * 128;
-    const at::TreeGeo G2 = geo(hdr2);
+    at::TreeGeo G2 = geo(hdr2);
+    static int eb_env = -1;
+    if (eb_env < 0) {
+        const char *e = getenv("AT_SA_EB");
+        eb_env = e ? atoi(e) : 1;
+    }
+    if (eb_env && G2.CH == at::SA_NW && !G2.resident && !G2.ring && G2.NP <= 1 && !G2.leaf_global) G2.eb = 1;
     static int grp_env = -1;
     if (grp_env < 0) {
         const char *e = getenv("AT_SA_GRP");   // 1 / 2 force the group count (measurement knob)

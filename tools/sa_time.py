@@ -29,6 +29,6 @@ for rep in range(3):
     ts.append(a.elapsed_time(b))
     assert torch.equal(r["accept_bits"], ref_bits)
 ms = min(ts)
-print(json.dumps({"cfg": cfg, "nbuf": os.environ.get("AT_SA_NBUF"), "ring": os.environ.get("AT_SA_RING"), "lg": os.environ.get("AT_SA_LG"), "grp": os.environ.get("AT_SA_GRP"), "np": os.environ.get("AT_SA_NP"), "chains": C,
+print(json.dumps({"cfg": cfg, "nbuf": os.environ.get("AT_SA_NBUF"), "ring": os.environ.get("AT_SA_RING"), "lg": os.environ.get("AT_SA_LG"), "grp": os.environ.get("AT_SA_GRP"), "np": os.environ.get("AT_SA_NP"), "eb": os.environ.get("AT_SA_EB"), "chains": C,
                   "ms": round(ms, 3), "chain_steps_per_s": round(C * (steps + 1) / ms * 1e3, 1),
                   "accept_digest": int(ref_bits.sum().item())}))
