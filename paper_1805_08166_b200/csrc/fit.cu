@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(256) grads_kernel(const int32_t *__restrict__ 
     float *sp = sc + group_size;
     __shared__ int s_w;
     const int b = blockIdx.x;
+    if (b >= gprefix[FIT_MAXKEYS]) return;   // grids sized by an upper bound of the group count
     if (threadIdx.x == 0) {
         int lo = 0, hi = FIT_MAXKEYS;   // largest w with gprefix[w] <= b
         while (hi - lo > 1) {
@@ -875,12 +876,89 @@ struct SubRange {
     int k_lo, nf, rows, byte_off;
 };
 
+// the subtraction path's layout, computed on the device from the cut counts (sub_layout_kernel), so a
+// single-rank fit never reads them back: every launch is sized by an upper bound and reads these
+struct SubDev {
+    int Fs, FsP, NR, max_rows, NE, TB, target;
+};
+
+// one block (thread 0 after the inverse table's reset): the splittable features' bank-column rows (stripes of 32 features while every column
+// fits SUB_ROWS), the ranges, the row-byte inverse table, the split entries (feature, 32-split chunk)
+// -- the same greedy layout the host used to compute.  With no splittable feature, feature 0 (one bin)
+// stands in, so the root totals still come out of its histogram and every node stays a leaf.
+__global__ void sub_layout_kernel(const int32_t *__restrict__ ncuts, const int32_t *__restrict__ boff, int F,
+                                  int32_t *__restrict__ flist, int32_t *__restrict__ rowbase,
+                                  int32_t *__restrict__ gbase, int32_t *__restrict__ nbk, int32_t *__restrict__ inv,
+                                  int FsP_max, SubRange *__restrict__ rng, int32_t *__restrict__ ent_f,
+                                  int32_t *__restrict__ ent_c, int nsm, SubDev *__restrict__ L)
+{
+    for (int b = threadIdx.x; b < FsP_max; b += blockDim.x) inv[b] = -1;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    int Fs = 0;
+    for (int f = 0; f < F; ++f)
+        if (ncuts[f] > 0) flist[Fs++] = f;
+    if (Fs == 0) {
+        flist[0] = 0;
+        Fs = 1;
+    }
+    for (int k = 0; k < Fs; ++k) {
+        gbase[k] = boff[flist[k]];
+        nbk[k] = ncuts[flist[k]] + 1;
+    }
+    int FsP = 0, NR = 0, max_rows = 0;
+    for (int k = 0; k < Fs;) {
+        int col[32];
+        for (int l = 0; l < 32; ++l) col[l] = 0;
+        int nf = 0;
+        while (k + nf < Fs && nf < 128 * SUB_NQW) {
+            const int m = min(32, Fs - (k + nf));
+            bool fits = true;
+            for (int l = 0; l < m; ++l) fits = fits && col[l] + nbk[k + nf + l] <= SUB_ROWS;
+            if (!fits && nf > 0) break;
+            for (int l = 0; l < m; ++l) {
+                rowbase[k + nf + l] = col[l];
+                col[l] += nbk[k + nf + l];
+            }
+            nf += m;
+        }
+        int rows = 0;
+        for (int l = 0; l < 32; ++l) rows = max(rows, col[l]);
+        rng[NR] = SubRange{k, nf, rows, FsP};
+        ++NR;
+        max_rows = max(max_rows, rows);
+        FsP += 128 * ((nf + 127) / 128);
+        k += nf;
+    }
+    for (int r0 = 0; r0 < NR; ++r0) {
+        const SubRange R = rng[r0];
+        for (int r = 0; r < R.nf; ++r) inv[R.byte_off + 128 * (r / 128) + 4 * (r % 32) + (r % 128) / 32] = R.k_lo + r;
+    }
+    int NE = 0;
+    for (int k = 0; k < Fs; ++k) {
+        const int nchk = max(1, (ncuts[flist[k]] + 31) / 32);
+        for (int c = 0; c < nchk; ++c, ++NE) {
+            ent_f[NE] = flist[k];
+            ent_c[NE] = c;
+        }
+    }
+    L->Fs = Fs;
+    L->FsP = FsP;
+    L->NR = NR;
+    L->max_rows = max_rows;
+    L->NE = NE;
+    L->TB = boff[F];
+    L->target = max(1, nsm / NR);
+}
+
 // bins [F][n] (column-major) -> binsR [n][FsP] in the ranges' byte order (inv[b] = compact feature
 // at row byte b, -1 = padding)
 __global__ void rowbins_kernel(const uint8_t *__restrict__ bins, int64_t n, const int32_t *__restrict__ flist,
-                               const int32_t *__restrict__ inv, int FsP, uint8_t *__restrict__ binsR)
+                               const int32_t *__restrict__ inv, const SubDev *__restrict__ L, uint8_t *__restrict__ binsR)
 {
     __shared__ uint8_t t[32][33];
+    const int FsP = L->FsP;
+    if ((int)blockIdx.y * 32 >= FsP) return;   // grid sized by an upper bound
     const int64_t i0 = (int64_t)blockIdx.x * 32;
     const int b0 = blockIdx.y * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -903,7 +981,8 @@ __global__ void rowbins_kernel(const uint8_t *__restrict__ bins, int64_t n, cons
 // it.y + w + NW t (balanced to within one sample), 32 of them per batch (one coalesced load of their
 // sample ids and gradients), then walks them with the next sample's row words in flight while the
 // current one's atomics issue.
-__global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__restrict__ binsR, int FsP,
+__global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__restrict__ binsR,
+                                                             const SubDev *__restrict__ L,
                                                              const int32_t *__restrict__ perm,
                                                              const int64_t *__restrict__ g,
                                                              const int64_t *__restrict__ h,
@@ -912,116 +991,123 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
                                                              const SubRange *__restrict__ ranges,
                                                              const int32_t *__restrict__ rowbase,
                                                              const int32_t *__restrict__ gbase,
-                                                             const int32_t *__restrict__ nbk, int TB,
+                                                             const int32_t *__restrict__ nbk,
                                                              int64_t *__restrict__ hist, int hb, int he)
 {
     extern __shared__ uint32_t sm[];
-    if ((int)blockIdx.x >= *n_items) return;
-    const SubRange R = ranges[blockIdx.y];
-    const int4 it = items[blockIdx.x];
-    const int P = (R.rows + 1) * 32;   // + a trash row: empty slots (padding bytes are 0) add there
-    uint32_t *glo = sm, *ghi = sm + P, *hlo = sm + 2 * P, *hhi = sm + 3 * P;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = SUB_NT / 32;
-    for (int q = tid; q < 4 * P; q += SUB_NT) sm[q] = 0u;
-    const int nqw = (R.nf + 127) >> 7;
-    int rb[SUB_NQW][4];
+    const int FsP = L->FsP, TB = L->TB, NR = L->NR;
+    const int n_wu = *n_items * NR;   // work units (item, range); a persistent grid of one block per SM
+    for (int wu = blockIdx.x; wu < n_wu; wu += gridDim.x) {
+        const SubRange R = ranges[wu % NR];
+        const int4 it = items[wu / NR];
+        const int P = (R.rows + 1) * 32;   // + a trash row: empty slots (padding bytes are 0) add there
+        uint32_t *glo = sm, *ghi = sm + P, *hlo = sm + 2 * P, *hhi = sm + 3 * P;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        constexpr int NW = SUB_NT / 32;
+        for (int q = tid; q < 4 * P; q += SUB_NT) sm[q] = 0u;
+        const int nqw = (R.nf + 127) >> 7;
+        int rb[SUB_NQW][4];
 #pragma unroll
-    for (int u = 0; u < SUB_NQW; ++u)
+        for (int u = 0; u < SUB_NQW; ++u)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int r = 128 * u + 32 * j + lane;
-            rb[u][j] = (r < R.nf ? rowbase[R.k_lo + r] : R.rows) * 32 + lane;
-        }
-    __syncthreads();
-    const uint8_t *rows = binsR + R.byte_off + 4 * lane;
-    for (int t0 = 0; it.y + warp + NW * t0 < it.z; t0 += 32) {
-        const int pl = it.y + warp + NW * (t0 + lane);
-        const bool inseg = pl < it.z;
-        const int ip = inseg ? (perm ? perm[pl] : pl) : 0;
-        // multi-rank: this rank histograms only its own sample slice [hb, he) (the rest is all-reduced)
-        const bool okp = inseg && ip >= hb && ip < he;
-        const unsigned okm = __ballot_sync(0xFFFFFFFFu, okp);
-        const int cnt = (int)__popc(okm);
-        // compact the valid lanes to the front (lane k takes the k-th valid lane's sample)
-        const int src = lane < cnt ? (int)__fns(okm, 0u, lane + 1) : 0;
-        const int il = __shfl_sync(0xFFFFFFFFu, ip, src);
-        const bool okl = lane < cnt;
-        const unsigned long long gvl = okl ? (unsigned long long)g[il] : 0ull;
-        const unsigned long long hvl = okl ? (unsigned long long)h[il] : 0ull;
-        uint32_t w[SUB_NQW], wn[SUB_NQW];
-        {
-            const uint32_t *row = (const uint32_t *)(rows + (int64_t)__shfl_sync(0xFFFFFFFFu, il, 0) * FsP);
-#pragma unroll
-            for (int u = 0; u < SUB_NQW; ++u) w[u] = u < nqw ? row[32 * u] : 0u;
-        }
-        for (int sI = 0; sI < cnt; ++sI) {
-            const int inext = __shfl_sync(0xFFFFFFFFu, il, (sI + 1) & 31);
-            if (sI + 1 < cnt) {
-                const uint32_t *row = (const uint32_t *)(rows + (int64_t)inext * FsP);
-#pragma unroll
-                for (int u = 0; u < SUB_NQW; ++u) wn[u] = u < nqw ? row[32 * u] : 0u;
+            for (int j = 0; j < 4; ++j) {
+                const int r = 128 * u + 32 * j + lane;
+                rb[u][j] = (r < R.nf ? rowbase[R.k_lo + r] : R.rows) * 32 + lane;
             }
-            const unsigned long long gv = __shfl_sync(0xFFFFFFFFu, gvl, sI);
-            const unsigned long long hv = __shfl_sync(0xFFFFFFFFu, hvl, sI);
-            if ((gv | hv) != 0ull) {   // warp-uniform: a zero-gradient sample contributes nothing
-                const uint32_t gl = (uint32_t)gv, gh = (uint32_t)(gv >> 32), hl = (uint32_t)hv, hh = (uint32_t)(hv >> 32);
+        __syncthreads();
+        const uint8_t *rows = binsR + R.byte_off + 4 * lane;
+        for (int t0 = 0; it.y + warp + NW * t0 < it.z; t0 += 32) {
+            const int pl = it.y + warp + NW * (t0 + lane);
+            const bool inseg = pl < it.z;
+            const int ip = inseg ? (perm ? perm[pl] : pl) : 0;
+            // multi-rank: this rank histograms only its own sample slice [hb, he) (the rest is all-reduced)
+            const bool okp = inseg && ip >= hb && ip < he;
+            const unsigned okm = __ballot_sync(0xFFFFFFFFu, okp);
+            const int cnt = (int)__popc(okm);
+            // compact the valid lanes to the front (lane k takes the k-th valid lane's sample)
+            const int src = lane < cnt ? (int)__fns(okm, 0u, lane + 1) : 0;
+            const int il = __shfl_sync(0xFFFFFFFFu, ip, src);
+            const bool okl = lane < cnt;
+            const unsigned long long gvl = okl ? (unsigned long long)g[il] : 0ull;
+            const unsigned long long hvl = okl ? (unsigned long long)h[il] : 0ull;
+            uint32_t w[SUB_NQW], wn[SUB_NQW];
+            {
+                const uint32_t *row = (const uint32_t *)(rows + (int64_t)__shfl_sync(0xFFFFFFFFu, il, 0) * FsP);
 #pragma unroll
-                for (int u = 0; u < SUB_NQW; ++u) {
-                    if (u >= nqw) break;
-                    // the 8 low-word atomics of the 4 slots first (their returns in flight together), then
-                    // the 8 high words with their carries
-                    int c[4];
-                    uint32_t og[4], oh[4];
+                for (int u = 0; u < SUB_NQW; ++u) w[u] = u < nqw ? row[32 * u] : 0u;
+            }
+            for (int sI = 0; sI < cnt; ++sI) {
+                const int inext = __shfl_sync(0xFFFFFFFFu, il, (sI + 1) & 31);
+                if (sI + 1 < cnt) {
+                    const uint32_t *row = (const uint32_t *)(rows + (int64_t)inext * FsP);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        c[j] = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
-                        AT_DCHECK(c[j] < P);
-                        og[j] = atomicAdd(&glo[c[j]], gl);
-                        oh[j] = atomicAdd(&hlo[c[j]], hl);
-                    }
+                    for (int u = 0; u < SUB_NQW; ++u) wn[u] = u < nqw ? row[32 * u] : 0u;
+                }
+                const unsigned long long gv = __shfl_sync(0xFFFFFFFFu, gvl, sI);
+                const unsigned long long hv = __shfl_sync(0xFFFFFFFFu, hvl, sI);
+                if ((gv | hv) != 0ull) {   // warp-uniform: a zero-gradient sample contributes nothing
+                    const uint32_t gl = (uint32_t)gv, gh = (uint32_t)(gv >> 32), hl = (uint32_t)hv, hh = (uint32_t)(hv >> 32);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        atomicAdd(&ghi[c[j]], gh + ((og[j] + gl < og[j]) ? 1u : 0u));   // exact modular 64-bit sums
-                        atomicAdd(&hhi[c[j]], hh + ((oh[j] + hl < oh[j]) ? 1u : 0u));
+                    for (int u = 0; u < SUB_NQW; ++u) {
+                        if (u >= nqw) break;
+                        // the 8 low-word atomics of the 4 slots first (their returns in flight together), then
+                        // the 8 high words with their carries
+                        int c[4];
+                        uint32_t og[4], oh[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            c[j] = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
+                            AT_DCHECK(c[j] < P);
+                            og[j] = atomicAdd(&glo[c[j]], gl);
+                            oh[j] = atomicAdd(&hlo[c[j]], hl);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            atomicAdd(&ghi[c[j]], gh + ((og[j] + gl < og[j]) ? 1u : 0u));   // exact modular 64-bit sums
+                            atomicAdd(&hhi[c[j]], hh + ((oh[j] + hl < oh[j]) ? 1u : 0u));
+                        }
                     }
                 }
-            }
 #pragma unroll
-            for (int u = 0; u < SUB_NQW; ++u) w[u] = wn[u];
+                for (int u = 0; u < SUB_NQW; ++u) w[u] = wn[u];
+            }
         }
-    }
-    __syncthreads();
-    // flush: lane = bank column, a warp walks a band of rows; each lane tracks the feature of its
-    // column that holds the current row
-    const int band = (R.rows + NW - 1) / NW;
-    const int row0 = warp * band, row1 = min(R.rows, row0 + band);
-    if (row0 >= row1) return;
-    int r = lane;   // this column's features: lane, lane + 32, ...
-    while (r < R.nf && rowbase[R.k_lo + r] + nbk[R.k_lo + r] <= row0) r += 32;
-    int rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF, rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
-    int cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
-    unsigned long long *hn = (unsigned long long *)(hist + (int64_t)it.x * TB * 2);
-    for (int row = row0; row < row1; ++row) {
-        if (row >= rend) {
-            r += 32;
-            rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF;
-            rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
-            cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
+        __syncthreads();
+        // flush: lane = bank column, a warp walks a band of rows; each lane tracks the feature of its
+        // column that holds the current row
+        const int band = (R.rows + NW - 1) / NW;
+        const int row0 = warp * band, row1 = min(R.rows, row0 + band);
+        if (row0 < row1) {
+            int r = lane;   // this column's features: lane, lane + 32, ...
+            while (r < R.nf && rowbase[R.k_lo + r] + nbk[R.k_lo + r] <= row0) r += 32;
+            int rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF, rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
+            int cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
+            unsigned long long *hn = (unsigned long long *)(hist + (int64_t)it.x * TB * 2);
+            for (int row = row0; row < row1; ++row) {
+                if (row >= rend) {
+                    r += 32;
+                    rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF;
+                    rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
+                    cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
+                }
+                if (row < rbase) continue;
+                const int a = row * 32 + lane;
+                const unsigned long long G = (unsigned long long)glo[a] | ((unsigned long long)ghi[a] << 32);
+                const unsigned long long H = (unsigned long long)hlo[a] | ((unsigned long long)hhi[a] << 32);
+                const int64_t cell = (int64_t)(cbase + row - rbase) * 2;
+                if (G) atomicAdd(&hn[cell], G);
+                if (H) atomicAdd(&hn[cell + 1], H);
+            }
         }
-        if (row < rbase) continue;
-        const int a = row * 32 + lane;
-        const unsigned long long G = (unsigned long long)glo[a] | ((unsigned long long)ghi[a] << 32);
-        const unsigned long long H = (unsigned long long)hlo[a] | ((unsigned long long)hhi[a] << 32);
-        const int64_t cell = (int64_t)(cbase + row - rbase) * 2;
-        if (G) atomicAdd(&hn[cell], G);
-        if (H) atomicAdd(&hn[cell + 1], H);
+        __syncthreads();   // the shared histogram is zeroed again by the next unit
     }
 }
 
 // root items: chunks of [0, n) for node slot 0
-__global__ void sub_root_items_kernel(int hb, int he, int target, int4 *__restrict__ items, int32_t *__restrict__ n_items)
+__global__ void sub_root_items_kernel(int hb, int he, const SubDev *__restrict__ L, int4 *__restrict__ items,
+                                      int32_t *__restrict__ n_items)
 {
+    const int target = L->target;
     const int n = he - hb;   // this rank's samples (all of them on one rank)
     const int ch = max(64, (n + target - 1) / target);
     const int m = (n + ch - 1) / ch;
@@ -1177,8 +1263,8 @@ __device__ __forceinline__ SplitBest scan_chunk(const int64_t *hf, int nb, int c
 __global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restrict__ hist,
                                                         const int32_t *__restrict__ boff,
                                                         const int32_t *__restrict__ ent_f,
-                                                        const int32_t *__restrict__ ent_c, int NE, int TB, int first,
-                                                        int nn, int64_t *__restrict__ tot, double lam,
+                                                        const int32_t *__restrict__ ent_c, const SubDev *__restrict__ L,
+                                                        int first, int nn, int64_t *__restrict__ tot, double lam,
                                                         double mcw, uint8_t *__restrict__ dead,
                                                         double *__restrict__ best_gain, int32_t *__restrict__ best_s,
                                                         const float *__restrict__ cuts, int B,
@@ -1188,6 +1274,7 @@ __global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restric
                                                         unsigned *__restrict__ done)
 {
     const int lane = threadIdx.x & 31;
+    const int NE = L->NE, TB = L->TB;
     const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (gw >= nn * NE) return;
     const int q = gw / NE, j = gw - q * NE;
@@ -1285,7 +1372,8 @@ __global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restr
                                                           int32_t *__restrict__ seg_start,
                                                           int32_t *__restrict__ seg_cnt,
                                                           int32_t *__restrict__ cursor, int32_t *__restrict__ node,
-                                                          int32_t *__restrict__ perm, int target, int4 *__restrict__ items,
+                                                          int32_t *__restrict__ perm, const SubDev *__restrict__ L,
+                                                          int4 *__restrict__ items,
                                                           int32_t *__restrict__ n_items, int4 *__restrict__ subs,
                                                           int32_t *__restrict__ n_subs, unsigned *__restrict__ done,
                                                           int compact, int64_t *__restrict__ tot, int hb, int he)
@@ -1323,15 +1411,17 @@ __global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restr
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    sub_worklist(first, nn, split_f, cursor, seg_start, seg_cnt, target, items, n_items, subs,
+    sub_worklist(first, nn, split_f, cursor, seg_start, seg_cnt, L->target, items, n_items, subs,
                  n_subs, compact, tot);
     if (tid == 0) *done = 0u;
 }
 
 // larger child = parent - smaller child, every cell (exact int64)
-__global__ void sub_subtract_kernel(const int64_t *__restrict__ parent, int64_t *__restrict__ child, int TB,
-                                    const int4 *__restrict__ subs, const int32_t *__restrict__ n_subs)
+__global__ void sub_subtract_kernel(const int64_t *__restrict__ parent, int64_t *__restrict__ child,
+                                    const SubDev *__restrict__ L, const int4 *__restrict__ subs,
+                                    const int32_t *__restrict__ n_subs)
 {
+    const int TB = L->TB;
     if ((int)blockIdx.y >= *n_subs) return;
     const int4 s = subs[blockIdx.y];
     const int64_t m = 2 * (int64_t)TB;
@@ -1342,9 +1432,10 @@ __global__ void sub_subtract_kernel(const int64_t *__restrict__ parent, int64_t 
 // multi-rank: the all-reduced smaller children (dense slot q) -> both children: small = reduced,
 // large = parent - small (exact int64)
 __global__ void sub_expand_kernel(const int64_t *__restrict__ parent, const int64_t *__restrict__ small,
-                                  int64_t *__restrict__ child, int TB, const int4 *__restrict__ subs,
+                                  int64_t *__restrict__ child, const SubDev *__restrict__ L, const int4 *__restrict__ subs,
                                   const int32_t *__restrict__ n_subs)
 {
+    const int TB = L->TB;
     if ((int)blockIdx.y >= *n_subs) return;
     const int4 s = subs[blockIdx.y];
     const int64_t m = 2 * (int64_t)TB;
@@ -1353,6 +1444,15 @@ __global__ void sub_expand_kernel(const int64_t *__restrict__ parent, const int6
         child[s.y * m + c] = v;
         child[s.z * m + c] = parent[s.x * m + c] - v;
     }
+}
+
+// zero 2 TB mult int64 cells (TB read on the device; 16-B stores)
+__global__ void sub_zero_kernel(int64_t *__restrict__ p, const SubDev *__restrict__ L, int mult)
+{
+    const int64_t m = (int64_t)L->TB * mult;   // pairs of cells
+    longlong2 *q = (longlong2 *)p;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x)
+        q[c] = make_longlong2(0, 0);
 }
 
 // last level: every sample's leaf, prediction update in tree order
@@ -2215,11 +2315,18 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     float *t_leaf = ws.get<float>((size_t)o->n_trees * n_leaf);
     if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
 
-    // input checks + cuts + groups.  The small single-rank fit (one fused launch) reads every size it
-    // needs on the device and never synchronizes; the other paths read the sizes back once
+    // input checks + cuts + groups.  A single-rank fit (one fused launch for n <= FUSED_NMAX, else the
+    // subtraction path laid out on the device) reads every size it needs on the device and never
+    // synchronizes; the multi-rank and level-by-level paths read the sizes back once
     const char *fused_e = getenv("AT_FIT_FUSED");   // "0" forces the level-by-level path
     const int fused_env = fused_e ? atoi(fused_e) : 1;
     const bool fused_path = fused_env && !o->allreduce && !o->d_hist0_out && n <= FUSED_NMAX;
+    const char *sub_e = getenv("AT_FIT_SUB");   // "0" forces the plain level-by-level path
+    const bool multi = o->allreduce != nullptr;
+    // histogram subtraction (section 3b) for larger n (any n with AT_FIT_FUSED=0 on one rank); F bounded
+    // so every feature range fits SUB_MAXR (nbk <= 256 < SUB_ROWS keeps every stripe in a block's rows)
+    const bool sub_path = (!sub_e || atoi(sub_e) != 0) && (!multi || n > FUSED_NMAX) && F <= 32 * SUB_MAXR;
+    bool synced = !(fused_path || (sub_path && !multi));
     int info[8] = {0};
     std::vector<int32_t> ncuts_h(F);
     {
@@ -2246,7 +2353,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             AT_CUDA_TRY(cudaMemsetAsync(pred, 0, sizeof(float) * n, s));
         AT_LAUNCH_CHECK("fit prep");
     }
-    if (!fused_path) {
+    if (synced) {
         AT_CUDA_TRY(cudaMemcpyAsync(info, d_info, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         AT_CUDA_TRY(cudaMemcpyAsync(ncuts_h.data(), ncuts, F * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         AT_CUDA_TRY(cudaStreamSynchronize(s));
@@ -2255,7 +2362,6 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
     }
     // (read back below for the paths that need them on the host)
     int TB = info[0], max_nb = info[1], n_groups = info[3];
-    int n_split = info[4];   // features with at least one cut
     // the fitted ensemble handle (both paths)
     auto finish = [&]() -> int {
         // the fitted ensemble handle
@@ -2282,7 +2388,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         AT_CUDA_TRY(cudaMemcpyAsync(gm->d_leaf, t_leaf, sizeof(float) * (size_t)o->n_trees * n_leaf,
                                     cudaMemcpyDeviceToDevice, s));
         if (o->d_pred_out) AT_CUDA_TRY(cudaMemcpyAsync(o->d_pred_out, pred, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
-        if (fused_path) {   // input flags found on the device travel with the model (at_gbt_s::h_err)
+        if (!synced) {   // input flags found on the device travel with the model (at_gbt_s::h_err)
             if (cudaHostAlloc((void **)&gm->h_err, sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess) {
                 cudaGetLastError();
                 gm->h_err = nullptr;
@@ -2377,16 +2483,16 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         }
     }
 
-    if (fused_path) {   // no cooperative launch possible: the sizes are read back after all
+    if (fused_path && !sub_path) {   // no cooperative launch possible: the sizes are read back after all
         AT_CUDA_TRY(cudaMemcpyAsync(info, d_info, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         AT_CUDA_TRY(cudaMemcpyAsync(ncuts_h.data(), ncuts, F * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         AT_CUDA_TRY(cudaStreamSynchronize(s));
+        synced = true;
         if (info[2] == 1) return fail(AT_EINVAL, "gbt_fit_hist: non-finite cost");
         if (info[2] == 2) return fail(AT_EUNSUPPORTED, "gbt_fit_hist: group key >= 1024");
         TB = info[0];
         max_nb = info[1];
         n_groups = info[3];
-        n_split = info[4];
     }
     // a single-rank fit has no host callback between levels: its launches are captured once into a
     // CUDA graph and launched as one unit (no host round trips for ~10 launches per level)
@@ -2415,242 +2521,182 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         return AT_OK;
     };
 
-    // larger n: histogram subtraction over node-contiguous positions (section 3b).  With R ranks every
-    // rank keeps the whole (replicated) partition and builds the smaller children's histograms over its
-    // own sample slice [hb, he) only; one int64 all-reduce per level (the dense smaller-children buffer,
-    // sized by the actual cut counts TB) makes them global, so every decision is replicated exactly.
-    const char *sub_e = getenv("AT_FIT_SUB");   // "0" forces the plain level-by-level path
-    const bool multi = o->allreduce != nullptr;
-    if ((!sub_e || atoi(sub_e) != 0) && n_split > 0 && (!multi || n > FUSED_NMAX)) {
-        // compact splittable features and the feature ranges whose bank columns fit a block's rows
-        std::vector<int32_t> boff_h(F + 1), flist_h;
-        for (int f = 0; f < F; ++f) {
-            boff_h[f + 1] = boff_h[f] + ncuts_h[f] + 1;
-            if (ncuts_h[f] > 0) flist_h.push_back(f);
+    // histogram subtraction over node-contiguous positions (section 3b).  The layout (splittable
+    // features, bank-column stripes, split entries, TB) is computed on the device by sub_layout_kernel and
+    // every launch below is sized by an upper bound of it, so one rank never reads anything back.  With R
+    // ranks every rank keeps the whole (replicated) partition and builds the smaller children's histograms
+    // over its own sample slice [hb, he) only; one int64 all-reduce per level (the dense smaller-children
+    // buffer, sized by the cut counts TB read back above) makes them global, so every decision is
+    // replicated exactly.
+    if (sub_path) {
+        int dev = 0, nsm = 0;
+        AT_CUDA_TRY(cudaGetDevice(&dev));
+        AT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const int NR_max = (F + 31) / 32;                     // a range holds >= min(32, rest) features
+        const int FsP_max = F + 128 * NR_max;                 // each range's bytes padded to 128
+        const int NE_max = F * std::max(1, (B + 30) / 32);    // (feature, 32-split chunk) entries
+        const int64_t TB_cap = synced ? (int64_t)TB : (int64_t)F * B;
+        const int max_items = nsm + max_nn + 1;               // target (<= nsm) root chunks, + nn per level
+        uint8_t *binsR = ws.get<uint8_t>((size_t)n * FsP_max);
+        int32_t *perm = ws.get<int32_t>(n);
+        int32_t *d_tab = ws.get<int32_t>(3 * (size_t)F + FsP_max);   // rowbase, gbase, nbk, inv
+        SubRange *d_rng = ws.get<SubRange>(NR_max);
+        SubDev *d_L = ws.get<SubDev>(1);
+        int32_t *d_ent = ws.get<int32_t>(2 * (size_t)NE_max);   // [feature of entry][chunk of entry]
+        int4 *items = ws.get<int4>(max_items);
+        int4 *subs = ws.get<int4>(max_nn + 1);
+        int32_t *cnts = ws.get<int32_t>(4);   // [0] n_items, [1] n_subs
+        int32_t *cursor = ws.get<int32_t>(2 * max_nn);
+        int32_t *seg_start = ws.get<int32_t>(n_int + n_leaf);
+        int32_t *seg_cnt = ws.get<int32_t>(n_int + n_leaf);
+        int64_t *tot = ws.get<int64_t>(2 * (size_t)(n_int + n_leaf));
+        int64_t *hA = ws.get<int64_t>((size_t)max_nn * TB_cap * 2);
+        int64_t *hB = ws.get<int64_t>((size_t)max_nn * TB_cap * 2);
+        int64_t *hS = multi ? ws.get<int64_t>((size_t)max_nn * TB * 2) : nullptr;   // dense smaller children
+        double *bg = ws.get<double>((size_t)max_nn * NE_max);
+        int32_t *bs = ws.get<int32_t>((size_t)max_nn * NE_max);
+        int32_t *d_tree = ws.get<int32_t>(1);
+        int4 *root_items = ws.get<int4>(max_items);
+        int32_t *root_n = ws.get<int32_t>(4);
+        unsigned *done = ws.get<unsigned>(2 + max_nn);   // last-block counter of the scatter, per-node split counters
+        if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+        int32_t *d_rowbase = d_tab, *d_gbase = d_tab + F, *d_nbk = d_tab + 2 * F, *d_inv = d_tab + 3 * F;
+        sub_layout_kernel<<<1, 256, 0, s>>>(ncuts, boff, F, flist, d_rowbase, d_gbase, d_nbk, d_inv, FsP_max, d_rng,
+                                            d_ent, d_ent + NE_max, nsm, d_L);
+        note_launch();
+        rowbins_kernel<<<dim3(nblk(n, 32), nblk(FsP_max, 32)), dim3(32, 8), 0, s>>>(bins, n, flist, d_inv, d_L, binsR);
+        note_launch();
+        AT_LAUNCH_CHECK("layout/rowbins");
+        const size_t hsm = (size_t)4 * 32 * (SUB_ROWS + 1) * sizeof(uint32_t);
+        static size_t sub_attr = 0;
+        if (sub_attr < hsm) {
+            AT_CUDA_TRY(cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+            sub_attr = hsm;
         }
-        const int Fs = (int)flist_h.size();
-        std::vector<int32_t> rowbase_h(Fs), gbase_h(Fs), nbk_h(Fs);
-        for (int k = 0; k < Fs; ++k) {
-            gbase_h[k] = boff_h[flist_h[k]];
-            nbk_h[k] = ncuts_h[flist_h[k]] + 1;
-        }
-        std::vector<SubRange> rng;
-        int FsP = 0;
-        for (int k = 0; k < Fs;) {
-            // add stripes of 32 features (one per bank column) while every column fits
-            int col[32] = {0};
-            int nf = 0;
-            while (k + nf < Fs && nf < 128 * SUB_NQW) {
-                int trial[32];
-                std::copy(col, col + 32, trial);
-                const int m = std::min(32, Fs - (k + nf));
-                bool fits = true;
-                for (int l = 0; l < m; ++l) {
-                    trial[l] += nbk_h[k + nf + l];
-                    fits = fits && trial[l] <= SUB_ROWS;
-                }
-                if (!fits && nf > 0) break;
-                for (int l = 0; l < m; ++l) rowbase_h[k + nf + l] = col[l];
-                std::copy(trial, trial + 32, col);
-                nf += m;
-            }
-            const int rows = *std::max_element(col, col + 32);
-            rng.push_back(SubRange{k, nf, rows, FsP});
-            FsP += 128 * ((nf + 127) / 128);
-            k += nf;
-        }
-        const int NR = (int)rng.size();
-        int max_rows = 0;
-        for (const SubRange &r : rng) max_rows = std::max(max_rows, r.rows);
-        std::vector<int32_t> inv_h(FsP, -1);
-        for (const SubRange &R : rng)
-            for (int r = 0; r < R.nf; ++r)
-                inv_h[R.byte_off + 128 * (r / 128) + 4 * (r % 32) + (r % 128) / 32] = R.k_lo + r;
-        if (NR <= SUB_MAXR && max_rows <= SUB_ROWS) {
-            int dev = 0, nsm = 0;
-            AT_CUDA_TRY(cudaGetDevice(&dev));
-            AT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-            const int target = std::max(1, nsm / NR);   // one wave of 1 block / SM
-            const int max_items = target + max_nn + 1;
-            uint8_t *binsR = ws.get<uint8_t>((size_t)n * FsP);
-            int32_t *perm = ws.get<int32_t>(n);
-            int32_t *d_tab = ws.get<int32_t>(3 * (size_t)Fs + FsP);   // rowbase, gbase, nbk, inv
-            SubRange *d_rng = ws.get<SubRange>(NR);
-            int4 *items = ws.get<int4>(max_items);
-            int4 *subs = ws.get<int4>(max_nn + 1);
-            int32_t *cnts = ws.get<int32_t>(4);   // [0] n_items, [1] n_subs
-            int32_t *cursor = ws.get<int32_t>(2 * max_nn);
-            int32_t *seg_start = ws.get<int32_t>(n_int + n_leaf);
-            int32_t *seg_cnt = ws.get<int32_t>(n_int + n_leaf);
-            int64_t *tot = ws.get<int64_t>(2 * (size_t)(n_int + n_leaf));
-            int64_t *hA = ws.get<int64_t>((size_t)max_nn * TB * 2);
-            int64_t *hB = ws.get<int64_t>((size_t)max_nn * TB * 2);
-            int64_t *hS = multi ? ws.get<int64_t>((size_t)max_nn * TB * 2) : nullptr;   // dense smaller children
-            // split entries: (feature, 32-split chunk), features ascending, chunks ascending
-            std::vector<int32_t> ent_h;
-            for (int k = 0; k < Fs; ++k) {
-                const int nchk = std::max(1, (ncuts_h[flist_h[k]] + 31) / 32);
-                for (int c = 0; c < nchk; ++c) ent_h.push_back(flist_h[k]);
-            }
-            const int NE = (int)ent_h.size();
-            for (int k = 0, j = 0; k < Fs; ++k) {
-                const int nchk = std::max(1, (ncuts_h[flist_h[k]] + 31) / 32);
-                for (int c = 0; c < nchk; ++c, ++j) ent_h.push_back(c);
-            }
-            int32_t *d_ent = ws.get<int32_t>(2 * (size_t)NE);   // [feature of entry][chunk of entry]
-            double *bg = ws.get<double>((size_t)max_nn * NE);
-            int32_t *bs = ws.get<int32_t>((size_t)max_nn * NE);
-            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
-            std::vector<int32_t> tab(rowbase_h);
-            tab.insert(tab.end(), gbase_h.begin(), gbase_h.end());
-            tab.insert(tab.end(), nbk_h.begin(), nbk_h.end());
-            tab.insert(tab.end(), inv_h.begin(), inv_h.end());
-            AT_CUDA_TRY(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-            AT_CUDA_TRY(cudaMemcpyAsync(d_rng, rng.data(), NR * sizeof(SubRange), cudaMemcpyHostToDevice, s));
-            AT_CUDA_TRY(cudaMemcpyAsync(d_ent, ent_h.data(), ent_h.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-            const int32_t *d_rowbase = d_tab, *d_gbase = d_tab + Fs, *d_nbk = d_tab + 2 * Fs, *d_inv = d_tab + 3 * Fs;
-            rowbins_kernel<<<dim3(nblk(n, 32), nblk(FsP, 32)), dim3(32, 8), 0, s>>>(bins, n, flist, d_inv, FsP, binsR);
-            note_launch();
-            AT_LAUNCH_CHECK("rowbins");
-            const size_t hsm = (size_t)4 * 32 * (max_rows + 1) * sizeof(uint32_t);
-            static size_t sub_attr = 0;
-            if (sub_attr < hsm) {
-                AT_CUDA_TRY(cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-                sub_attr = hsm;
-            }
-            // one tree is captured once and its graph launched n_trees times: the tree index lives on the
-            // device (d_tree, advanced by the graph's last node), so the host cost per fit is one capture
-            int32_t *d_tree = ws.get<int32_t>(1);
-            int4 *root_items = ws.get<int4>(max_items);
-            int32_t *root_n = ws.get<int32_t>(4);
-            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
-            unsigned *done = ws.get<unsigned>(2 + max_nn);   // last-block counter of the scatter, per-node split counters
-            if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
-            AT_CUDA_TRY(cudaMemsetAsync(d_tree, 0, sizeof(int32_t), s));
-            AT_CUDA_TRY(cudaMemsetAsync(done, 0, (2 + max_nn) * sizeof(unsigned), s));
-            AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * max_nn, s));
-            AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
-            AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
-            sub_root_items_kernel<<<1, 256, 0, s>>>((int)hb, (int)he, target, root_items, root_n);
-            note_launch();
-            auto enqueue_sub = [&](cudaStream_t s) -> int {
-                {
-                    ProfScope ps(AT_K_FIT_GRAD, s);
-                    if (o->objective == AT_OBJ_REG) {
-                        reg_grads_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, pred, n, g, h); note_launch();
-                    } else {
-                        positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, 0u,
-                                                                      member, d_tree); note_launch();
-                        if (n_groups > 0) {
-                            grads_kernel<<<n_groups, 256, (size_t)GS * 2 * sizeof(float), s>>>(member, counts, woff, gpre,
-                                                                                                GS, d_cost, pred, g, h);
-                            note_launch();
-                        }
+        // one tree is captured once and its graph launched n_trees times: the tree index lives on the
+        // device (d_tree, advanced by the graph's last node), so the host cost per fit is one capture
+        AT_CUDA_TRY(cudaMemsetAsync(d_tree, 0, sizeof(int32_t), s));
+        AT_CUDA_TRY(cudaMemsetAsync(done, 0, (2 + max_nn) * sizeof(unsigned), s));
+        AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * max_nn, s));
+        AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
+        AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
+        sub_root_items_kernel<<<1, 256, 0, s>>>((int)hb, (int)he, d_L, root_items, root_n);
+        note_launch();
+        // group count bounded by n / GS + one partial group per present key
+        const int grad_grid = synced ? n_groups : (int)(n / GS + std::min<int64_t>(n, FIT_MAXKEYS));
+        const unsigned zgrid = 2 * (unsigned)nsm;
+        auto enqueue_sub = [&](cudaStream_t s) -> int {
+            {
+                ProfScope ps(AT_K_FIT_GRAD, s);
+                if (o->objective == AT_OBJ_REG) {
+                    reg_grads_kernel<<<nblk(n, 256), 256, 0, s>>>(d_cost, pred, n, g, h); note_launch();
+                } else {
+                    positions_kernel<<<nblk(n, 256), 256, 0, s>>>(d_group_key, rank, counts, woff, n, o->seed, 0u,
+                                                                  member, d_tree); note_launch();
+                    if (grad_grid > 0) {
+                        grads_kernel<<<grad_grid, 256, (size_t)GS * 2 * sizeof(float), s>>>(member, counts, woff, gpre,
+                                                                                            GS, d_cost, pred, g, h);
+                        note_launch();
                     }
-                    AT_LAUNCH_CHECK("fit gradients");
                 }
-                int64_t *hp = hA, *hc = hB;   // node[] and dead[] were zeroed by the previous tree (or below)
-                {
-                    ProfScope ps(AT_K_FIT_HIST, s);
-                    AT_CUDA_TRY(cudaMemsetAsync(hp, 0, sizeof(int64_t) * 2 * (size_t)TB, s));
-                    sub_hist_kernel<<<dim3(max_items, NR), SUB_NT, hsm, s>>>(binsR, FsP, nullptr, g, h, root_items, root_n,
-                                                                             d_rng, d_rowbase, d_gbase, d_nbk, TB, hp,
-                                                                             (int)hb, (int)he);
+                AT_LAUNCH_CHECK("fit gradients");
+            }
+            int64_t *hp = hA, *hc = hB;   // node[] and dead[] were zeroed by the previous tree (or below)
+            {
+                ProfScope ps(AT_K_FIT_HIST, s);
+                sub_zero_kernel<<<zgrid, 256, 0, s>>>(hp, d_L, 1); note_launch();
+                sub_hist_kernel<<<nsm, SUB_NT, hsm, s>>>(binsR, d_L, nullptr, g, h, root_items, root_n, d_rng, d_rowbase,
+                                                         d_gbase, d_nbk, hp, (int)hb, (int)he);
+                note_launch();
+                AT_LAUNCH_CHECK("root histogram");
+                if (multi && o->allreduce(hp, 2 * (int64_t)TB, o->ctx, stream))
+                    return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
+                const int want_h0 = o->d_hist0_out != nullptr;
+                sub_root_tot_kernel<<<1, 256, 0, s>>>(hp, boff, flist, F, (int)(he - hb), want_h0, tot, seg_start, seg_cnt,
+                                                      d_tree); note_launch();
+                if (want_h0) {
+                    hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hp, boff, F, B, o->d_hist0_out,
+                                                                                 d_tree);
                     note_launch();
-                    AT_LAUNCH_CHECK("root histogram");
-                    if (multi && o->allreduce(hp, 2 * (int64_t)TB, o->ctx, stream))
-                        return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
-                    const int want_h0 = o->d_hist0_out != nullptr;
-                    sub_root_tot_kernel<<<1, 256, 0, s>>>(hp, boff, flist, F, (int)(he - hb), want_h0, tot, seg_start, seg_cnt,
-                                                          d_tree); note_launch();
-                    if (want_h0) {
-                        hist0_expand_kernel<<<nblk((int64_t)F * B, 256), 256, 0, s>>>(hp, boff, F, B, o->d_hist0_out,
-                                                                                     d_tree);
-                        note_launch();
-                    }
-                    AT_LAUNCH_CHECK("root histogram");
                 }
-                for (int d = 0; d < D; ++d) {
-                    const int first = (1 << d) - 1, nn = 1 << d;
-                    {
-                        ProfScope ps(AT_K_FIT_SPLIT, s);
-                        sub_split_kernel<<<nblk((int64_t)nn * NE, 8), 256, 0, s>>>(
-                            hp, boff, d_ent, d_ent + NE, NE, TB, first, nn, tot, lam, mcw, dead, bg, bs, cuts, B, split_f,
-                            split_s, t_feat, t_thr, n_int, d_tree, done + 2);
-                        note_launch();
-                        AT_LAUNCH_CHECK("split/decide");
-                    }
-                    if (d == D - 1) break;
-                    {
-                        ProfScope ps(AT_K_FIT_SPLIT, s);
-                        sub_scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, first, nn, seg_start,
-                                                                        seg_cnt, cursor, node, perm, target, items, cnts,
-                                                                        subs, cnts + 1, done + 1, multi ? 1 : 0, tot,
-                                                                        (int)hb, (int)he);
-                        note_launch();
-                        AT_LAUNCH_CHECK("scatter");
-                    }
-                    if (multi) {
-                        {
-                            ProfScope ps(AT_K_FIT_HIST, s);
-                            AT_CUDA_TRY(cudaMemsetAsync(hS, 0, sizeof(int64_t) * 2 * (size_t)TB * nn, s));
-                            sub_hist_kernel<<<dim3(target + nn, NR), SUB_NT, hsm, s>>>(binsR, FsP, perm, g, h, items, cnts,
-                                                                                      d_rng, d_rowbase, d_gbase, d_nbk, TB,
-                                                                                      hS, (int)hb, (int)he);
-                            note_launch();
-                            AT_LAUNCH_CHECK("histograms");
-                        }
-                        if (o->allreduce(hS, 2 * (int64_t)TB * nn, o->ctx, stream))
-                            return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
-                        {
-                            ProfScope ps(AT_K_FIT_HIST, s);
-                            sub_expand_kernel<<<dim3(std::min<unsigned>(nblk(2 * (int64_t)TB, 256), 64), nn), 256, 0, s>>>(
-                                hp, hS, hc, TB, subs, cnts + 1);
-                            note_launch();
-                            AT_LAUNCH_CHECK("expand");
-                        }
-                        std::swap(hp, hc);
-                        continue;
-                    }
+                AT_LAUNCH_CHECK("root histogram");
+            }
+            for (int d = 0; d < D; ++d) {
+                const int first = (1 << d) - 1, nn = 1 << d;
+                {
+                    ProfScope ps(AT_K_FIT_SPLIT, s);
+                    sub_split_kernel<<<nblk((int64_t)nn * NE_max, 8), 256, 0, s>>>(
+                        hp, boff, d_ent, d_ent + NE_max, d_L, first, nn, tot, lam, mcw, dead, bg, bs, cuts, B, split_f,
+                        split_s, t_feat, t_thr, n_int, d_tree, done + 2);
+                    note_launch();
+                    AT_LAUNCH_CHECK("split/decide");
+                }
+                if (d == D - 1) break;
+                {
+                    ProfScope ps(AT_K_FIT_SPLIT, s);
+                    sub_scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, first, nn, seg_start,
+                                                                    seg_cnt, cursor, node, perm, d_L, items, cnts,
+                                                                    subs, cnts + 1, done + 1, multi ? 1 : 0, tot,
+                                                                    (int)hb, (int)he);
+                    note_launch();
+                    AT_LAUNCH_CHECK("scatter");
+                }
+                if (multi) {
                     {
                         ProfScope ps(AT_K_FIT_HIST, s);
-                        AT_CUDA_TRY(cudaMemsetAsync(hc, 0, sizeof(int64_t) * 2 * (size_t)TB * 2 * nn, s));
-                        sub_hist_kernel<<<dim3(target + nn, NR), SUB_NT, hsm, s>>>(binsR, FsP, perm, g, h, items, cnts,
-                                                                                  d_rng, d_rowbase, d_gbase, d_nbk, TB, hc,
-                                                                                  0, (int)n);
-                        note_launch();
-                        sub_subtract_kernel<<<dim3(std::min<unsigned>(nblk(2 * (int64_t)TB, 256), 64), nn), 256, 0, s>>>(
-                            hp, hc, TB, subs, cnts + 1);
+                        AT_CUDA_TRY(cudaMemsetAsync(hS, 0, sizeof(int64_t) * 2 * (size_t)TB * nn, s));
+                        sub_hist_kernel<<<nsm, SUB_NT, hsm, s>>>(binsR, d_L, perm, g, h, items, cnts, d_rng, d_rowbase,
+                                                                 d_gbase, d_nbk, hS, (int)hb, (int)he);
                         note_launch();
                         AT_LAUNCH_CHECK("histograms");
                     }
+                    if (o->allreduce(hS, 2 * (int64_t)TB * nn, o->ctx, stream))
+                        return fail(AT_ECUDA, "gbt_fit_hist: allreduce callback failed");
+                    {
+                        ProfScope ps(AT_K_FIT_HIST, s);
+                        sub_expand_kernel<<<dim3(64, nn), 256, 0, s>>>(hp, hS, hc, d_L, subs, cnts + 1);
+                        note_launch();
+                        AT_LAUNCH_CHECK("expand");
+                    }
                     std::swap(hp, hc);
+                    continue;
                 }
                 {
-                    ProfScope ps(AT_K_FIT_UPDATE, s);
-                    sub_leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(tot + 2 * (size_t)n_int, n_leaf, eta, lam, t_leaf,
-                                                                      d_tree, dead, n_int + n_leaf);
+                    ProfScope ps(AT_K_FIT_HIST, s);
+                    sub_zero_kernel<<<zgrid, 256, 0, s>>>(hc, d_L, 2 * nn); note_launch();
+                    sub_hist_kernel<<<nsm, SUB_NT, hsm, s>>>(binsR, d_L, perm, g, h, items, cnts, d_rng, d_rowbase,
+                                                             d_gbase, d_nbk, hc, 0, (int)n);
                     note_launch();
-                    sub_final_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, node, split_f, split_s, n_int, t_leaf, pred,
-                                                                  d_tree);
+                    sub_subtract_kernel<<<dim3(64, nn), 256, 0, s>>>(hp, hc, d_L, subs, cnts + 1);
                     note_launch();
-                    sub_tree_next_kernel<<<1, 1, 0, s>>>(d_tree);
-                    note_launch();
-                    AT_LAUNCH_CHECK("leaf/pred update");
+                    AT_LAUNCH_CHECK("histograms");
                 }
-                return AT_OK;
-            };
-            if (multi) {   // host callbacks between levels: enqueued tree by tree (the tree index is on the device)
-                for (int t = 0; t < o->n_trees; ++t) {
-                    const int rc = enqueue_sub(s);
-                    if (rc) return rc;
-                }
-            } else {
-                const int rc = run_captured(enqueue_sub, o->n_trees);
+                std::swap(hp, hc);
+            }
+            {
+                ProfScope ps(AT_K_FIT_UPDATE, s);
+                sub_leaf_kernel<<<nblk(n_leaf, 256), 256, 0, s>>>(tot + 2 * (size_t)n_int, n_leaf, eta, lam, t_leaf,
+                                                                  d_tree, dead, n_int + n_leaf);
+                note_launch();
+                sub_final_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, node, split_f, split_s, n_int, t_leaf, pred,
+                                                              d_tree);
+                note_launch();
+                sub_tree_next_kernel<<<1, 1, 0, s>>>(d_tree);
+                note_launch();
+                AT_LAUNCH_CHECK("leaf/pred update");
+            }
+            return AT_OK;
+        };
+        if (multi) {   // host callbacks between levels: enqueued tree by tree (the tree index is on the device)
+            for (int t = 0; t < o->n_trees; ++t) {
+                const int rc = enqueue_sub(s);
                 if (rc) return rc;
             }
-            return finish();
+        } else {
+            const int rc = run_captured(enqueue_sub, o->n_trees);
+            if (rc) return rc;
         }
+        return finish();
     }
 
     int64_t *hist = ws.get<int64_t>((size_t)max_nn * TB * 2);

@@ -648,6 +648,20 @@ def test_fit_subtraction_many_feature_ranges(at):
     _check_paths(_fit_paths(at, Xg, n, c, key, paths=("subtraction", "level-by-level"), n_trees=2, depth=6), ref)
 
 
+def test_fit_subtraction_no_splittable_feature(at):
+    """Every feature constant (no cut anywhere) on the subtraction path: its device layout lets feature 0
+    (one bin) stand in, so the root totals still come from a histogram and every node is a pass-through
+    (threshold +inf, leaves = the Newton step of the totals), as the oracle builds it."""
+    n = 3000
+    rng = np.random.default_rng(5)
+    X = np.full((n, 468), 2.0, np.float32)
+    c = (1.0 + rng.random(n)).astype(np.float32)
+    key = (np.arange(n) % 4).astype(np.uint16)
+    ref = O.fit_hist(X, c, key, n_trees=2, depth=4)
+    Xg = dev(np.ascontiguousarray(X.T))
+    _check_paths(_fit_paths(at, Xg, n, c, key, paths=("subtraction", "level-by-level"), n_trees=2, depth=4), ref)
+
+
 def test_fit_subtraction_large_gradients(at):
     """Regression on costs of order 10^4: |g| = 2 |f - c| 2^32 reaches 2^46, so the 64-bit histogram sums
     need their carries (low word -> high word) at every level."""
@@ -845,9 +859,9 @@ def test_knob_features_match_oracle(at, wls):
 
 
 def test_fit_errors(at):
-    """S:306 / header: n = 0 -> AT_EEMPTY at once.  A non-finite cost: a small fit (one fused launch, no
-    host sync) returns a model whose every later use reports AT_EINVAL; a large fit (reads its sizes
-    back) reports AT_EINVAL itself."""
+    """S:306 / header: n = 0 -> AT_EEMPTY at once.  A non-finite cost: a single-rank fit (fused launch or
+    device-laid-out subtraction path, no host sync) returns a model whose every later use reports
+    AT_EINVAL; the level-by-level path (AT_FIT_SUB=0, reads its sizes back) reports AT_EINVAL itself."""
     with pytest.raises(at.ATError) as e:
         at.gbt_fit_hist(torch.zeros((468, 4), device="cuda"), 0, torch.zeros(4, device="cuda"),
                         torch.zeros(4, dtype=torch.int16, device="cuda"))
@@ -862,15 +876,26 @@ def test_fit_errors(at):
     n = 3000
     cb = torch.ones(n, device="cuda")
     cb[7] = float("inf")
-    with pytest.raises(at.ATError) as e:
-        at.gbt_fit_hist(torch.rand((468, n), device="cuda"), n, cb, torch.zeros(n, dtype=torch.int16, device="cuda"))
-    assert e.value.code == -1
+    Xb = torch.rand((468, n), device="cuda")
+    m = at.gbt_fit_hist(Xb, n, cb, torch.zeros(n, dtype=torch.int16, device="cuda"))
+    for use in (lambda: m.export(), lambda: m.predict(Xb, n=n)):
+        with pytest.raises(at.ATError) as e:
+            use()
+        assert e.value.code == -1
+    os.environ["AT_FIT_SUB"] = "0"
+    try:
+        with pytest.raises(at.ATError) as e:
+            at.gbt_fit_hist(Xb, n, cb, torch.zeros(n, dtype=torch.int16, device="cuda"))
+        assert e.value.code == -1
+    finally:
+        del os.environ["AT_FIT_SUB"]
 
 
-def test_small_fit_does_not_block_the_host(at):
-    """8(b) "every call is stream-ordered and asynchronous": a fit enqueued behind a long kernel returns to
-    the host before that kernel finishes (the fused path sizes its launch on the device), and its model is
-    the oracle's."""
+@pytest.mark.parametrize("n_fit", [800, 4000])
+def test_fit_does_not_block_the_host(at, n_fit):
+    """8(b) "every call is stream-ordered and asynchronous": a single-rank fit enqueued behind a long kernel
+    returns to the host before that kernel finishes (the fused path, n = 800, and the subtraction path,
+    n = 4000, size their launches on the device), and its model is the oracle's."""
     import time
     sp = at.Space(synth.ALL_RESNET)
     ens = synth.ensemble(1000, 8, seed=1805)
@@ -878,15 +903,15 @@ def test_small_fit_does_not_block_the_host(at):
     n_ch = 65536
     temps = torch.from_numpy(synth.temperatures(40, synth.energy_scale(1000))).cuda()
     cw = dev((np.arange(n_ch) % 12).astype(np.int16))
-    osp, idx, Xo, c, key = fit_inputs(800, [synth.CFG2A], seed=21)
+    osp, idx, Xo, c, key = fit_inputs(n_fit, [synth.CFG2A], seed=21)
     Xg = at.Space([synth.CFG2A]).features(u64(idx))
     cg, kg = dev(c), dev(key.view(np.int16))
-    at.gbt_fit_hist(Xg, 800, cg, kg, n_trees=2, depth=3)   # warm (workspace, attributes)
+    at.gbt_fit_hist(Xg, n_fit, cg, kg, n_trees=2, depth=3)   # warm (workspace, attributes)
     torch.cuda.synchronize()
     at.sa_explore(sp, g, torch.zeros(n_ch, dtype=torch.int64, device="cuda"), temps, seed=1, round_=0, k_out=8,
                   chain_workload=cw, init=True)            # ~15 ms of device work
     t0 = time.perf_counter()
-    m = at.gbt_fit_hist(Xg, 800, cg, kg, n_trees=5, depth=5)
+    m = at.gbt_fit_hist(Xg, n_fit, cg, kg, n_trees=5, depth=5)
     dt = time.perf_counter() - t0
     busy = not torch.cuda.current_stream().query()
     torch.cuda.synchronize()

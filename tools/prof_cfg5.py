@@ -12,7 +12,7 @@ build.build()
 sp = at.Space(synth.ALL_RESNET)
 ens = synth.ensemble(2000, 8, seed=1805)
 g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
-n = 1 << 16
+n = 1 << 20
 idx = torch.from_numpy(synth.sweep_indices(sp.size(), 0, n).view(np.int64)).cuda()
 X = sp.features(idx)
 for _ in range(2):
