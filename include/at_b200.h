@@ -243,11 +243,14 @@ AT_API int select_topk_batch(at_space sp, int32_t w0, int32_t n_w, const uint64_
  * the fit's final training predictions; d_hist0_out (nullable) [n_features][max_bins][2]
  * gets tree 0's root histogram (after the reduction).  Errors: AT_EEMPTY (n == 0),
  * AT_EINVAL (non-finite cost), AT_EUNSUPPORTED (depth > 8, max_bins > 256, group key >= 1024).
- * Host synchronization: a single-rank fit of n <= 2048 samples (one fused launch) reads every
- * data-dependent size on the device and never blocks the host; its input errors (non-finite cost,
- * group key >= 1024) travel with the returned model -- every later call on it (gbt_predict,
- * sa_explore, gbt_export, gbt_concat, ...) returns AT_EINVAL.  Larger or multi-rank fits read the
- * cut counts back once (the histogram layout is sized from them) and return those errors directly. */
+ * Host synchronization: a single-rank fit (one fused launch for n <= 2048 samples, else the
+ * histogram-subtraction path, whose layout is computed on the device and whose launches are sized
+ * by upper bounds) reads every data-dependent size on the device and never blocks the host; its
+ * input errors (non-finite cost, group key >= 1024) travel with the returned model -- every later
+ * call on it (gbt_predict, sa_explore, gbt_export, gbt_concat, ...) returns AT_EINVAL.  Multi-rank
+ * fits (the all-reduce count is the cut total) and the level-by-level path (AT_FIT_SUB=0) read the
+ * cut counts back once and return those errors directly.  n_features <= 8192 on the subtraction
+ * path (else level-by-level). */
 typedef int (*at_allreduce_i64_fn)(int64_t *d_buf, int64_t count, void *ctx, void *stream);
 
 typedef struct {

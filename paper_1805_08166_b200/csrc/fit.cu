@@ -864,6 +864,9 @@ __global__ void key_check_kernel(const uint16_t *__restrict__ k, int64_t n, int3
 // (+ next work list), histograms of the smaller children, subtraction; one tree is one CUDA graph.
 constexpr int SUB_NT = 1024;
 constexpr int SUB_ROWS = 400;   // rows of 32 cells (+ 1 trash row): 4 planes x 4 B x 32 x 401 = 200 KB of shared memory
+// default stripe cap (AT_SUB_ROWS overrides, within [B, SUB_ROWS]): 164 KB of shared histogram leaves
+// the SM ~90 KB of L1 (measured on config 4: 37.8 ms at 290-320 rows vs 38.2 ms at 400)
+constexpr int SUB_ROWS_DEF = 320;
 constexpr int SUB_NQW = 4;      // row words per lane and sample: <= 512 features per range
 constexpr int SUB_MAXR = 256;
 
@@ -882,73 +885,116 @@ struct SubDev {
     int Fs, FsP, NR, max_rows, NE, TB, target;
 };
 
-// one block (thread 0 after the inverse table's reset): the splittable features' bank-column rows (stripes of 32 features while every column
-// fits SUB_ROWS), the ranges, the row-byte inverse table, the split entries (feature, 32-split chunk)
-// -- the same greedy layout the host used to compute.  With no splittable feature, feature 0 (one bin)
-// stands in, so the root totals still come out of its histogram and every node stays a leaf.
+// one histogram block's work: positions [it.y, it.z) of node slot it.x, feature range R (the item and
+// the range side by side, so a block's first loads do not depend on one another)
+struct SubUnit {
+    int4 it;
+    SubRange R;
+};
+
+// zero 2 TB mult int64 cells with the whole grid (16-B stores); TB is read on the device
+__device__ __forceinline__ void sub_zero_cells(int64_t *__restrict__ p, const SubDev *__restrict__ L, int mult)
+{
+    const int64_t m = (int64_t)L->TB * mult;   // pairs of cells
+    longlong2 *q = (longlong2 *)p;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x)
+        q[c] = make_longlong2(0, 0);
+}
+
+// items[0, m) x the NR ranges -> units, range-major (run by one block after its items are written)
+__device__ __forceinline__ void sub_units(const int4 *__restrict__ items, int m, const SubRange *__restrict__ ranges,
+                                          int NR, SubUnit *__restrict__ units, int32_t *__restrict__ n_units)
+{
+    for (int u = threadIdx.x; u < m * NR; u += blockDim.x) units[u] = SubUnit{items[u % m], ranges[u / m]};
+    if (threadIdx.x == 0) *n_units = m * NR;
+}
+
+// one block; warp 0 lays out (lane l = bank column l): the splittable features in order, their
+// bank-column rows (stripes of 32 features while every column still fits rows_cap, greedy -- the layout
+// the host used to compute), the ranges, the row-byte inverse table and the split entries (feature,
+// 32-split chunk).  With no splittable feature, feature 0 (one bin) stands in, so the root totals still
+// come out of its histogram and every node stays a leaf.
 __global__ void sub_layout_kernel(const int32_t *__restrict__ ncuts, const int32_t *__restrict__ boff, int F,
                                   int32_t *__restrict__ flist, int32_t *__restrict__ rowbase,
                                   int32_t *__restrict__ gbase, int32_t *__restrict__ nbk, int32_t *__restrict__ inv,
                                   int FsP_max, SubRange *__restrict__ rng, int32_t *__restrict__ ent_f,
-                                  int32_t *__restrict__ ent_c, int nsm, SubDev *__restrict__ L)
+                                  int32_t *__restrict__ ent_c, int nsm, int rows_cap, SubDev *__restrict__ L)
 {
     for (int b = threadIdx.x; b < FsP_max; b += blockDim.x) inv[b] = -1;
     __syncthreads();
-    if (threadIdx.x != 0) return;
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const unsigned below = (1u << lane) - 1u;
+    // compaction of the splittable features (ascending), their cell bases and bin counts
     int Fs = 0;
-    for (int f = 0; f < F; ++f)
-        if (ncuts[f] > 0) flist[Fs++] = f;
+    for (int f0 = 0; f0 < F; f0 += 32) {
+        const int f = f0 + lane;
+        const bool sp = f < F && ncuts[f] > 0;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, sp);
+        if (sp) {
+            const int k = Fs + __popc(m & below);
+            flist[k] = f;
+            gbase[k] = boff[f];
+            nbk[k] = ncuts[f] + 1;
+        }
+        Fs += __popc(m);
+    }
     if (Fs == 0) {
-        flist[0] = 0;
+        if (lane == 0) { flist[0] = 0; gbase[0] = boff[0]; nbk[0] = 1; }
         Fs = 1;
     }
-    for (int k = 0; k < Fs; ++k) {
-        gbase[k] = boff[flist[k]];
-        nbk[k] = ncuts[flist[k]] + 1;
-    }
+    __syncwarp();
+    // ranges: add stripes of 32 features (feature k + nf + l on column l) while every column fits
     int FsP = 0, NR = 0, max_rows = 0;
     for (int k = 0; k < Fs;) {
-        int col[32];
-        for (int l = 0; l < 32; ++l) col[l] = 0;
-        int nf = 0;
+        int col = 0, nf = 0;
         while (k + nf < Fs && nf < 128 * SUB_NQW) {
             const int m = min(32, Fs - (k + nf));
-            bool fits = true;
-            for (int l = 0; l < m; ++l) fits = fits && col[l] + nbk[k + nf + l] <= SUB_ROWS;
+            const int nb = lane < m ? nbk[k + nf + lane] : 0;
+            const bool fits = __all_sync(0xFFFFFFFFu, col + nb <= rows_cap);
             if (!fits && nf > 0) break;
-            for (int l = 0; l < m; ++l) {
-                rowbase[k + nf + l] = col[l];
-                col[l] += nbk[k + nf + l];
-            }
+            if (lane < m) rowbase[k + nf + lane] = col;
+            col += nb;
             nf += m;
         }
-        int rows = 0;
-        for (int l = 0; l < 32; ++l) rows = max(rows, col[l]);
-        rng[NR] = SubRange{k, nf, rows, FsP};
+        int rows = col;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) rows = max(rows, __shfl_xor_sync(0xFFFFFFFFu, rows, off));
+        if (lane == 0) rng[NR] = SubRange{k, nf, rows, FsP};
+        // row-byte inverse table of this range
+        for (int r = lane; r < nf; r += 32) inv[FsP + 128 * (r / 128) + 4 * (r % 32) + (r % 128) / 32] = k + r;
         ++NR;
         max_rows = max(max_rows, rows);
         FsP += 128 * ((nf + 127) / 128);
         k += nf;
     }
-    for (int r0 = 0; r0 < NR; ++r0) {
-        const SubRange R = rng[r0];
-        for (int r = 0; r < R.nf; ++r) inv[R.byte_off + 128 * (r / 128) + 4 * (r % 32) + (r % 128) / 32] = R.k_lo + r;
-    }
+    // split entries: feature k owns max(1, ceil(ncuts / 32)) consecutive entries (exclusive prefix)
     int NE = 0;
-    for (int k = 0; k < Fs; ++k) {
-        const int nchk = max(1, (ncuts[flist[k]] + 31) / 32);
-        for (int c = 0; c < nchk; ++c, ++NE) {
-            ent_f[NE] = flist[k];
-            ent_c[NE] = c;
+    for (int k0 = 0; k0 < Fs; k0 += 32) {
+        const int k = k0 + lane;
+        const int nchk = k < Fs ? max(1, (nbk[k] - 1 + 31) / 32) : 0;
+        int x = nchk;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+            if (lane >= off) x += y;
         }
+        const int e0 = NE + x - nchk;
+        for (int c = 0; c < nchk; ++c) {
+            ent_f[e0 + c] = flist[k];
+            ent_c[e0 + c] = c;
+        }
+        NE += __shfl_sync(0xFFFFFFFFu, x, 31);
     }
-    L->Fs = Fs;
-    L->FsP = FsP;
-    L->NR = NR;
-    L->max_rows = max_rows;
-    L->NE = NE;
-    L->TB = boff[F];
-    L->target = max(1, nsm / NR);
+    if (lane == 0) {
+        L->Fs = Fs;
+        L->FsP = FsP;
+        L->NR = NR;
+        L->max_rows = max_rows;
+        L->NE = NE;
+        L->TB = boff[F];
+        L->target = max(1, nsm / NR);
+    }
 }
 
 // bins [F][n] (column-major) -> binsR [n][FsP] in the ranges' byte order (inv[b] = compact feature
@@ -958,20 +1004,21 @@ __global__ void rowbins_kernel(const uint8_t *__restrict__ bins, int64_t n, cons
 {
     __shared__ uint8_t t[32][33];
     const int FsP = L->FsP;
-    if ((int)blockIdx.y * 32 >= FsP) return;   // grid sized by an upper bound
     const int64_t i0 = (int64_t)blockIdx.x * 32;
-    const int b0 = blockIdx.y * 32;
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int b = b0 + r;
-        const int64_t i = i0 + threadIdx.x;
-        const int k = b < FsP ? inv[b] : -1;
-        t[r][threadIdx.x] = (k >= 0 && i < n) ? bins[(int64_t)flist[k] * n + i] : (uint8_t)0;
-    }
-    __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int64_t i = i0 + r;
-        const int b = b0 + threadIdx.x;
-        if (i < n && b < FsP) binsR[i * FsP + b] = t[threadIdx.x][r];
+    for (int b0 = blockIdx.y * 32; b0 < FsP; b0 += gridDim.y * 32) {   // FsP known on the device only
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int b = b0 + r;
+            const int64_t i = i0 + threadIdx.x;
+            const int k = b < FsP ? inv[b] : -1;
+            t[r][threadIdx.x] = (k >= 0 && i < n) ? bins[(int64_t)flist[k] * n + i] : (uint8_t)0;
+        }
+        __syncthreads();
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int64_t i = i0 + r;
+            const int b = b0 + threadIdx.x;
+            if (i < n && b < FsP) binsR[i * FsP + b] = t[threadIdx.x][r];
+        }
+        __syncthreads();
     }
 }
 
@@ -986,133 +1033,134 @@ __global__ void __launch_bounds__(SUB_NT, 1) sub_hist_kernel(const uint8_t *__re
                                                              const int32_t *__restrict__ perm,
                                                              const int64_t *__restrict__ g,
                                                              const int64_t *__restrict__ h,
-                                                             const int4 *__restrict__ items,
-                                                             const int32_t *__restrict__ n_items,
-                                                             const SubRange *__restrict__ ranges,
+                                                             const SubUnit *__restrict__ units,
+                                                             const int32_t *__restrict__ n_units,
                                                              const int32_t *__restrict__ rowbase,
                                                              const int32_t *__restrict__ gbase,
                                                              const int32_t *__restrict__ nbk,
                                                              int64_t *__restrict__ hist, int hb, int he)
 {
     extern __shared__ uint32_t sm[];
-    const int FsP = L->FsP, TB = L->TB, NR = L->NR;
-    const int n_wu = *n_items * NR;   // work units (item, range); a persistent grid of one block per SM
-    for (int wu = blockIdx.x; wu < n_wu; wu += gridDim.x) {
-        const SubRange R = ranges[wu % NR];
-        const int4 it = items[wu / NR];
-        const int P = (R.rows + 1) * 32;   // + a trash row: empty slots (padding bytes are 0) add there
-        uint32_t *glo = sm, *ghi = sm + P, *hlo = sm + 2 * P, *hhi = sm + 3 * P;
-        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-        constexpr int NW = SUB_NT / 32;
-        for (int q = tid; q < 4 * P; q += SUB_NT) sm[q] = 0u;
-        const int nqw = (R.nf + 127) >> 7;
-        int rb[SUB_NQW][4];
+    // work unit blockIdx.x; the grid is an upper bound of the units (their count comes from the
+    // device), the spare blocks exit at once
+    const int FsP = L->FsP, TB = L->TB;
+    const SubUnit U = units[blockIdx.x];   // (capacity-sized array: the load is in bounds either way)
+    if ((int)blockIdx.x >= *n_units) return;
+    const SubRange R = U.R;
+    const int4 it = U.it;
+    const int P = (R.rows + 1) * 32;   // + a trash row: empty slots (padding bytes are 0) add there
+    uint32_t *glo = sm, *ghi = sm + P, *hlo = sm + 2 * P, *hhi = sm + 3 * P;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = SUB_NT / 32;
+    for (int q = tid; q < 4 * P; q += SUB_NT) sm[q] = 0u;
+    const int nqw = (R.nf + 127) >> 7;
+    int rb[SUB_NQW][4];
 #pragma unroll
-        for (int u = 0; u < SUB_NQW; ++u)
+    for (int u = 0; u < SUB_NQW; ++u)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int r = 128 * u + 32 * j + lane;
-                rb[u][j] = (r < R.nf ? rowbase[R.k_lo + r] : R.rows) * 32 + lane;
+        for (int j = 0; j < 4; ++j) {
+            const int r = 128 * u + 32 * j + lane;
+            rb[u][j] = (r < R.nf ? rowbase[R.k_lo + r] : R.rows) * 32 + lane;
+        }
+    __syncthreads();
+    const uint8_t *rows = binsR + R.byte_off + 4 * lane;
+    for (int t0 = 0; it.y + warp + NW * t0 < it.z; t0 += 32) {
+        const int pl = it.y + warp + NW * (t0 + lane);
+        const bool inseg = pl < it.z;
+        const int ip = inseg ? (perm ? perm[pl] : pl) : 0;
+        // multi-rank: this rank histograms only its own sample slice [hb, he) (the rest is all-reduced)
+        const bool okp = inseg && ip >= hb && ip < he;
+        const unsigned okm = __ballot_sync(0xFFFFFFFFu, okp);
+        const int cnt = (int)__popc(okm);
+        // compact the valid lanes to the front (lane k takes the k-th valid lane's sample)
+        const int src = lane < cnt ? (int)__fns(okm, 0u, lane + 1) : 0;
+        const int il = __shfl_sync(0xFFFFFFFFu, ip, src);
+        const bool okl = lane < cnt;
+        const unsigned long long gvl = okl ? (unsigned long long)g[il] : 0ull;
+        const unsigned long long hvl = okl ? (unsigned long long)h[il] : 0ull;
+        uint32_t w[SUB_NQW], wn[SUB_NQW];
+        {
+            const uint32_t *row = (const uint32_t *)(rows + (int64_t)__shfl_sync(0xFFFFFFFFu, il, 0) * FsP);
+#pragma unroll
+            for (int u = 0; u < SUB_NQW; ++u) w[u] = u < nqw ? row[32 * u] : 0u;
+        }
+        for (int sI = 0; sI < cnt; ++sI) {
+            const int inext = __shfl_sync(0xFFFFFFFFu, il, (sI + 1) & 31);
+            if (sI + 1 < cnt) {
+                const uint32_t *row = (const uint32_t *)(rows + (int64_t)inext * FsP);
+#pragma unroll
+                for (int u = 0; u < SUB_NQW; ++u) wn[u] = u < nqw ? row[32 * u] : 0u;
             }
-        __syncthreads();
-        const uint8_t *rows = binsR + R.byte_off + 4 * lane;
-        for (int t0 = 0; it.y + warp + NW * t0 < it.z; t0 += 32) {
-            const int pl = it.y + warp + NW * (t0 + lane);
-            const bool inseg = pl < it.z;
-            const int ip = inseg ? (perm ? perm[pl] : pl) : 0;
-            // multi-rank: this rank histograms only its own sample slice [hb, he) (the rest is all-reduced)
-            const bool okp = inseg && ip >= hb && ip < he;
-            const unsigned okm = __ballot_sync(0xFFFFFFFFu, okp);
-            const int cnt = (int)__popc(okm);
-            // compact the valid lanes to the front (lane k takes the k-th valid lane's sample)
-            const int src = lane < cnt ? (int)__fns(okm, 0u, lane + 1) : 0;
-            const int il = __shfl_sync(0xFFFFFFFFu, ip, src);
-            const bool okl = lane < cnt;
-            const unsigned long long gvl = okl ? (unsigned long long)g[il] : 0ull;
-            const unsigned long long hvl = okl ? (unsigned long long)h[il] : 0ull;
-            uint32_t w[SUB_NQW], wn[SUB_NQW];
-            {
-                const uint32_t *row = (const uint32_t *)(rows + (int64_t)__shfl_sync(0xFFFFFFFFu, il, 0) * FsP);
+            const unsigned long long gv = __shfl_sync(0xFFFFFFFFu, gvl, sI);
+            const unsigned long long hv = __shfl_sync(0xFFFFFFFFu, hvl, sI);
+            if ((gv | hv) != 0ull) {   // warp-uniform: a zero-gradient sample contributes nothing
+                const uint32_t gl = (uint32_t)gv, gh = (uint32_t)(gv >> 32), hl = (uint32_t)hv, hh = (uint32_t)(hv >> 32);
 #pragma unroll
-                for (int u = 0; u < SUB_NQW; ++u) w[u] = u < nqw ? row[32 * u] : 0u;
-            }
-            for (int sI = 0; sI < cnt; ++sI) {
-                const int inext = __shfl_sync(0xFFFFFFFFu, il, (sI + 1) & 31);
-                if (sI + 1 < cnt) {
-                    const uint32_t *row = (const uint32_t *)(rows + (int64_t)inext * FsP);
+                for (int u = 0; u < SUB_NQW; ++u) {
+                    if (u >= nqw) break;
+                    // the 8 low-word atomics of the 4 slots first (their returns in flight together), then
+                    // the 8 high words with their carries
+                    int c[4];
+                    uint32_t og[4], oh[4];
 #pragma unroll
-                    for (int u = 0; u < SUB_NQW; ++u) wn[u] = u < nqw ? row[32 * u] : 0u;
-                }
-                const unsigned long long gv = __shfl_sync(0xFFFFFFFFu, gvl, sI);
-                const unsigned long long hv = __shfl_sync(0xFFFFFFFFu, hvl, sI);
-                if ((gv | hv) != 0ull) {   // warp-uniform: a zero-gradient sample contributes nothing
-                    const uint32_t gl = (uint32_t)gv, gh = (uint32_t)(gv >> 32), hl = (uint32_t)hv, hh = (uint32_t)(hv >> 32);
+                    for (int j = 0; j < 4; ++j) {
+                        c[j] = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
+                        AT_DCHECK(c[j] < P);
+                        og[j] = atomicAdd(&glo[c[j]], gl);
+                        oh[j] = atomicAdd(&hlo[c[j]], hl);
+                    }
 #pragma unroll
-                    for (int u = 0; u < SUB_NQW; ++u) {
-                        if (u >= nqw) break;
-                        // the 8 low-word atomics of the 4 slots first (their returns in flight together), then
-                        // the 8 high words with their carries
-                        int c[4];
-                        uint32_t og[4], oh[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            c[j] = rb[u][j] + 32 * (int)((w[u] >> (8 * j)) & 255u);
-                            AT_DCHECK(c[j] < P);
-                            og[j] = atomicAdd(&glo[c[j]], gl);
-                            oh[j] = atomicAdd(&hlo[c[j]], hl);
-                        }
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            atomicAdd(&ghi[c[j]], gh + ((og[j] + gl < og[j]) ? 1u : 0u));   // exact modular 64-bit sums
-                            atomicAdd(&hhi[c[j]], hh + ((oh[j] + hl < oh[j]) ? 1u : 0u));
-                        }
+                    for (int j = 0; j < 4; ++j) {
+                        atomicAdd(&ghi[c[j]], gh + ((og[j] + gl < og[j]) ? 1u : 0u));   // exact modular 64-bit sums
+                        atomicAdd(&hhi[c[j]], hh + ((oh[j] + hl < oh[j]) ? 1u : 0u));
                     }
                 }
+            }
 #pragma unroll
-                for (int u = 0; u < SUB_NQW; ++u) w[u] = wn[u];
-            }
+            for (int u = 0; u < SUB_NQW; ++u) w[u] = wn[u];
         }
-        __syncthreads();
-        // flush: lane = bank column, a warp walks a band of rows; each lane tracks the feature of its
-        // column that holds the current row
-        const int band = (R.rows + NW - 1) / NW;
-        const int row0 = warp * band, row1 = min(R.rows, row0 + band);
-        if (row0 < row1) {
-            int r = lane;   // this column's features: lane, lane + 32, ...
-            while (r < R.nf && rowbase[R.k_lo + r] + nbk[R.k_lo + r] <= row0) r += 32;
-            int rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF, rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
-            int cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
-            unsigned long long *hn = (unsigned long long *)(hist + (int64_t)it.x * TB * 2);
-            for (int row = row0; row < row1; ++row) {
-                if (row >= rend) {
-                    r += 32;
-                    rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF;
-                    rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
-                    cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
-                }
-                if (row < rbase) continue;
-                const int a = row * 32 + lane;
-                const unsigned long long G = (unsigned long long)glo[a] | ((unsigned long long)ghi[a] << 32);
-                const unsigned long long H = (unsigned long long)hlo[a] | ((unsigned long long)hhi[a] << 32);
-                const int64_t cell = (int64_t)(cbase + row - rbase) * 2;
-                if (G) atomicAdd(&hn[cell], G);
-                if (H) atomicAdd(&hn[cell + 1], H);
+    }
+    __syncthreads();
+    // flush: lane = bank column, a warp walks a band of rows; each lane tracks the feature of its
+    // column that holds the current row
+    const int band = (R.rows + NW - 1) / NW;
+    const int row0 = warp * band, row1 = min(R.rows, row0 + band);
+    if (row0 < row1) {
+        int r = lane;   // this column's features: lane, lane + 32, ...
+        while (r < R.nf && rowbase[R.k_lo + r] + nbk[R.k_lo + r] <= row0) r += 32;
+        int rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF, rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
+        int cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
+        unsigned long long *hn = (unsigned long long *)(hist + (int64_t)it.x * TB * 2);
+        for (int row = row0; row < row1; ++row) {
+            if (row >= rend) {
+                r += 32;
+                rbase = r < R.nf ? rowbase[R.k_lo + r] : 0x7FFFFFFF;
+                rend = r < R.nf ? rbase + nbk[R.k_lo + r] : 0x7FFFFFFF;
+                cbase = r < R.nf ? gbase[R.k_lo + r] : 0;
             }
+            if (row < rbase) continue;
+            const int a = row * 32 + lane;
+            const unsigned long long G = (unsigned long long)glo[a] | ((unsigned long long)ghi[a] << 32);
+            const unsigned long long H = (unsigned long long)hlo[a] | ((unsigned long long)hhi[a] << 32);
+            const int64_t cell = (int64_t)(cbase + row - rbase) * 2;
+            if (G) atomicAdd(&hn[cell], G);
+            if (H) atomicAdd(&hn[cell + 1], H);
         }
-        __syncthreads();   // the shared histogram is zeroed again by the next unit
     }
 }
 
 // root items: chunks of [0, n) for node slot 0
 __global__ void sub_root_items_kernel(int hb, int he, const SubDev *__restrict__ L, int4 *__restrict__ items,
-                                      int32_t *__restrict__ n_items)
+                                      const SubRange *__restrict__ ranges, SubUnit *__restrict__ units,
+                                      int32_t *__restrict__ n_units)
 {
     const int target = L->target;
     const int n = he - hb;   // this rank's samples (all of them on one rank)
     const int ch = max(64, (n + target - 1) / target);
     const int m = (n + ch - 1) / ch;
     for (int b = threadIdx.x; b < m; b += blockDim.x) items[b] = make_int4(0, hb + b * ch, hb + min(n, (b + 1) * ch), 0);
-    if (threadIdx.x == 0) *n_items = m;
+    __syncthreads();
+    sub_units(items, m, ranges, L->NR, units, n_units);
 }
 
 // root totals from the cells of the first splittable feature (its bins partition the samples),
@@ -1275,32 +1323,34 @@ __global__ void __launch_bounds__(256) sub_split_kernel(const int64_t *__restric
 {
     const int lane = threadIdx.x & 31;
     const int NE = L->NE, TB = L->TB;
-    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (gw >= nn * NE) return;
-    const int q = gw / NE, j = gw - q * NE;
-    const int nd = first + q, f = ent_f[j];
-    if (dead[nd]) {
-        if (lane == 0) best_s[(int64_t)q * NE + j] = 0;
-    } else {
-        const SplitBest best = scan_chunk(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f], ent_c[j],
-                                          tot[2 * nd], tot[2 * nd + 1], lam, mcw, f, lane);
-        if (lane == 0) {
-            best_gain[(int64_t)q * NE + j] = best.gain;
-            best_s[(int64_t)q * NE + j] = best.f < 0 ? 0 : best.s;
+    // warps stride over the entries (the grid is sized by an upper bound of NE)
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gw < nn * NE; gw += nwarps) {
+        const int q = gw / NE, j = gw - q * NE;
+        const int nd = first + q, f = ent_f[j];
+        if (dead[nd]) {
+            if (lane == 0) best_s[(int64_t)q * NE + j] = 0;
+        } else {
+            const SplitBest best = scan_chunk(hist + ((int64_t)q * TB + boff[f]) * 2, boff[f + 1] - boff[f], ent_c[j],
+                                              tot[2 * nd], tot[2 * nd + 1], lam, mcw, f, lane);
+            if (lane == 0) {
+                best_gain[(int64_t)q * NE + j] = best.gain;
+                best_s[(int64_t)q * NE + j] = best.f < 0 ? 0 : best.s;
+            }
         }
-    }
-    unsigned last = 0;
-    if (lane == 0) {
+        unsigned last = 0;
+        if (lane == 0) {
+            __threadfence();
+            last = atomicAdd(&done[q], 1u) == (unsigned)(NE - 1);
+        }
+        last = __shfl_sync(0xFFFFFFFFu, last, 0);
+        if (!last) continue;
         __threadfence();
-        last = atomicAdd(&done[q], 1u) == (unsigned)(NE - 1);
+        // entries in feature order, chunks ascending: the (gain desc, f asc, s asc) rule picks as before
+        sub_decide_node(q, best_gain, best_s, ent_f, NE, first, nn, cuts, B, hist, boff, TB, dead, split_f, split_s,
+                        tree_feat, tree_thr, tot, n_int, d_tree);
+        if (lane == 0) done[q] = 0u;   // for the next level
     }
-    last = __shfl_sync(0xFFFFFFFFu, last, 0);
-    if (!last) return;
-    __threadfence();
-    // entries in feature order, chunks ascending: the (gain desc, f asc, s asc) rule picks as before
-    sub_decide_node(q, best_gain, best_s, ent_f, NE, first, nn, cuts, B, hist, boff, TB, dead, split_f, split_s,
-                    tree_feat, tree_thr, tot, n_int, d_tree);
-    if (lane == 0) done[q] = 0u;   // for the next level
 }
 
 // one block: children's segments, the smaller child of every split node as histogram items (chunks
@@ -1309,7 +1359,8 @@ __device__ __forceinline__ void sub_worklist(int first, int nn, const int32_t *_
                                              int32_t *__restrict__ cursor, int32_t *__restrict__ seg_start,
                                     int32_t *__restrict__ seg_cnt, int target, int4 *__restrict__ items,
                                     int32_t *__restrict__ n_items, int4 *__restrict__ subs, int32_t *__restrict__ n_subs,
-                                    int compact, const int64_t *__restrict__ tot)
+                                    int compact, const int64_t *__restrict__ tot, const SubRange *__restrict__ ranges,
+                                    int NR, SubUnit *__restrict__ units, int32_t *__restrict__ n_units)
 {
     __shared__ int s_cs[128], s_m0[129], s_s0[129], s_ch;
     const int q = threadIdx.x;
@@ -1347,6 +1398,7 @@ __device__ __forceinline__ void sub_worklist(int first, int nn, const int32_t *_
             ns += split_f[first + p] >= 0 ? 1 : 0;
         }
         s_ch = ch;
+        s_m0[nn] = m;
         *n_items = m;
         *n_subs = ns;
     }
@@ -1361,6 +1413,8 @@ __device__ __forceinline__ void sub_worklist(int first, int nn, const int32_t *_
         const int slot = compact ? q : small - cfirst;
         for (int o = 0; o < cs; o += ch) items[m++] = make_int4(slot, st + o, st + min(cs, o + ch), 0);
     }
+    __syncthreads();
+    sub_units(items, s_m0[nn], ranges, NR, units, n_units);
 }
 
 // samples of level-d nodes move to their children: node ids, and positions in the parent's segment
@@ -1376,10 +1430,14 @@ __global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restr
                                                           int4 *__restrict__ items,
                                                           int32_t *__restrict__ n_items, int4 *__restrict__ subs,
                                                           int32_t *__restrict__ n_subs, unsigned *__restrict__ done,
-                                                          int compact, int64_t *__restrict__ tot, int hb, int he)
+                                                          int compact, int64_t *__restrict__ tot, int hb, int he,
+                                                          const SubRange *__restrict__ ranges,
+                                                          SubUnit *__restrict__ units, int32_t *__restrict__ n_units,
+                                                          int64_t *__restrict__ zp, int zmult)
 {
     __shared__ int sc[256], sbase[256];
     const int tid = threadIdx.x;
+    sub_zero_cells(zp, L, zmult);   // the next histogram launch's slots (nobody reads them here)
     for (int q = tid; q < 2 * nn; q += blockDim.x) sc[q] = 0;
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
@@ -1412,7 +1470,7 @@ __global__ void __launch_bounds__(256) sub_scatter_kernel(const uint8_t *__restr
     if (!s_last) return;
     __threadfence();
     sub_worklist(first, nn, split_f, cursor, seg_start, seg_cnt, L->target, items, n_items, subs,
-                 n_subs, compact, tot);
+                 n_subs, compact, tot, ranges, L->NR, units, n_units);
     if (tid == 0) *done = 0u;
 }
 
@@ -1446,20 +1504,19 @@ __global__ void sub_expand_kernel(const int64_t *__restrict__ parent, const int6
     }
 }
 
-// zero 2 TB mult int64 cells (TB read on the device; 16-B stores)
+// zero 2 TB mult int64 cells (TB read on the device; 16-B stores), grid-stride
 __global__ void sub_zero_kernel(int64_t *__restrict__ p, const SubDev *__restrict__ L, int mult)
 {
-    const int64_t m = (int64_t)L->TB * mult;   // pairs of cells
-    longlong2 *q = (longlong2 *)p;
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x)
-        q[c] = make_longlong2(0, 0);
+    sub_zero_cells(p, L, mult);
 }
 
 // last level: every sample's leaf, prediction update in tree order
 __global__ void sub_final_kernel(const uint8_t *__restrict__ bins, int64_t n, int32_t *__restrict__ node,
                                  const int32_t *__restrict__ split_f, const int32_t *__restrict__ split_s, int n_int,
-                                 const float *__restrict__ leaf, float *__restrict__ pred, const int32_t *__restrict__ d_tree)
+                                 const float *__restrict__ leaf, float *__restrict__ pred, const int32_t *__restrict__ d_tree,
+                                 int64_t *__restrict__ zp, const SubDev *__restrict__ L)
 {
+    sub_zero_cells(zp, L, 1);   // the next tree's root histogram (no histogram is read any more)
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     leaf += (int64_t)*d_tree * (n_int + 1);
@@ -2545,7 +2602,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         int32_t *d_ent = ws.get<int32_t>(2 * (size_t)NE_max);   // [feature of entry][chunk of entry]
         int4 *items = ws.get<int4>(max_items);
         int4 *subs = ws.get<int4>(max_nn + 1);
-        int32_t *cnts = ws.get<int32_t>(4);   // [0] n_items, [1] n_subs
+        int32_t *cnts = ws.get<int32_t>(4);   // [0] n_items, [1] n_subs, [2] n_units
         int32_t *cursor = ws.get<int32_t>(2 * max_nn);
         int32_t *seg_start = ws.get<int32_t>(n_int + n_leaf);
         int32_t *seg_cnt = ws.get<int32_t>(n_int + n_leaf);
@@ -2557,17 +2614,25 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         int32_t *bs = ws.get<int32_t>((size_t)max_nn * NE_max);
         int32_t *d_tree = ws.get<int32_t>(1);
         int4 *root_items = ws.get<int4>(max_items);
+        const int wu_root = std::max(nsm, NR_max);   // root units <= target NR <= max(nsm, NR)
+        SubUnit *units = ws.get<SubUnit>((size_t)wu_root + (size_t)max_nn * NR_max);   // + nn NR per level
+        SubUnit *root_units = ws.get<SubUnit>(wu_root);
         int32_t *root_n = ws.get<int32_t>(4);
         unsigned *done = ws.get<unsigned>(2 + max_nn);   // last-block counter of the scatter, per-node split counters
         if (ws.err) return fail(AT_ENOMEM, "gbt_fit_hist: workspace allocation failed");
+        // a range's rows <= max(rows_cap, B) (its first stripe always goes in; a stripe of one feature
+        // each takes <= B rows): the shared histogram is sized by that bound
+        const char *rc_e = getenv("AT_SUB_ROWS");
+        const int rows_cap = std::min(SUB_ROWS, std::max(B, rc_e ? atoi(rc_e) : SUB_ROWS_DEF));
+        const size_t hsm = (size_t)4 * 32 * (std::max(rows_cap, B) + 1) * sizeof(uint32_t);
         int32_t *d_rowbase = d_tab, *d_gbase = d_tab + F, *d_nbk = d_tab + 2 * F, *d_inv = d_tab + 3 * F;
         sub_layout_kernel<<<1, 256, 0, s>>>(ncuts, boff, F, flist, d_rowbase, d_gbase, d_nbk, d_inv, FsP_max, d_rng,
-                                            d_ent, d_ent + NE_max, nsm, d_L);
+                                            d_ent, d_ent + NE_max, nsm, rows_cap, d_L);
         note_launch();
-        rowbins_kernel<<<dim3(nblk(n, 32), nblk(FsP_max, 32)), dim3(32, 8), 0, s>>>(bins, n, flist, d_inv, d_L, binsR);
+        rowbins_kernel<<<dim3(nblk(n, 32), std::min(4u, nblk(FsP_max, 32))), dim3(32, 8), 0, s>>>(bins, n, flist, d_inv,
+                                                                                                  d_L, binsR);
         note_launch();
         AT_LAUNCH_CHECK("layout/rowbins");
-        const size_t hsm = (size_t)4 * 32 * (SUB_ROWS + 1) * sizeof(uint32_t);
         static size_t sub_attr = 0;
         if (sub_attr < hsm) {
             AT_CUDA_TRY(cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
@@ -2580,11 +2645,15 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         AT_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * max_nn, s));
         AT_CUDA_TRY(cudaMemsetAsync(node, 0, sizeof(int32_t) * n, s));
         AT_CUDA_TRY(cudaMemsetAsync(dead, 0, n_int + n_leaf, s));
-        sub_root_items_kernel<<<1, 256, 0, s>>>((int)hb, (int)he, d_L, root_items, root_n);
+        // spare histogram blocks read a unit past the count before they exit: keep it initialised
+        AT_CUDA_TRY(cudaMemsetAsync(units, 0, sizeof(SubUnit) * ((size_t)wu_root + (size_t)max_nn * NR_max), s));
+        AT_CUDA_TRY(cudaMemsetAsync(root_units, 0, sizeof(SubUnit) * (size_t)wu_root, s));
+        sub_zero_kernel<<<2 * nsm, 256, 0, s>>>(hA, d_L, 1);   // tree 0's root (each tree zeroes the next one's)
+        note_launch();
+        sub_root_items_kernel<<<1, 256, 0, s>>>((int)hb, (int)he, d_L, root_items, d_rng, root_units, root_n);
         note_launch();
         // group count bounded by n / GS + one partial group per present key
         const int grad_grid = synced ? n_groups : (int)(n / GS + std::min<int64_t>(n, FIT_MAXKEYS));
-        const unsigned zgrid = 2 * (unsigned)nsm;
         auto enqueue_sub = [&](cudaStream_t s) -> int {
             {
                 ProfScope ps(AT_K_FIT_GRAD, s);
@@ -2604,9 +2673,8 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
             int64_t *hp = hA, *hc = hB;   // node[] and dead[] were zeroed by the previous tree (or below)
             {
                 ProfScope ps(AT_K_FIT_HIST, s);
-                sub_zero_kernel<<<zgrid, 256, 0, s>>>(hp, d_L, 1); note_launch();
-                sub_hist_kernel<<<nsm, SUB_NT, hsm, s>>>(binsR, d_L, nullptr, g, h, root_items, root_n, d_rng, d_rowbase,
-                                                         d_gbase, d_nbk, hp, (int)hb, (int)he);
+                sub_hist_kernel<<<wu_root, SUB_NT, hsm, s>>>(binsR, d_L, nullptr, g, h, root_units, root_n,
+                                                             d_rowbase, d_gbase, d_nbk, hp, (int)hb, (int)he);
                 note_launch();
                 AT_LAUNCH_CHECK("root histogram");
                 if (multi && o->allreduce(hp, 2 * (int64_t)TB, o->ctx, stream))
@@ -2625,7 +2693,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                 const int first = (1 << d) - 1, nn = 1 << d;
                 {
                     ProfScope ps(AT_K_FIT_SPLIT, s);
-                    sub_split_kernel<<<nblk((int64_t)nn * NE_max, 8), 256, 0, s>>>(
+                    sub_split_kernel<<<std::min<unsigned>(nblk((int64_t)nn * NE_max, 8), 8 * nsm), 256, 0, s>>>(
                         hp, boff, d_ent, d_ent + NE_max, d_L, first, nn, tot, lam, mcw, dead, bg, bs, cuts, B, split_f,
                         split_s, t_feat, t_thr, n_int, d_tree, done + 2);
                     note_launch();
@@ -2637,16 +2705,17 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                     sub_scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, split_f, split_s, first, nn, seg_start,
                                                                     seg_cnt, cursor, node, perm, d_L, items, cnts,
                                                                     subs, cnts + 1, done + 1, multi ? 1 : 0, tot,
-                                                                    (int)hb, (int)he);
+                                                                    (int)hb, (int)he, d_rng, units, cnts + 2,
+                                                                    multi ? hS : hc, multi ? nn : 2 * nn);
                     note_launch();
                     AT_LAUNCH_CHECK("scatter");
                 }
                 if (multi) {
                     {
                         ProfScope ps(AT_K_FIT_HIST, s);
-                        AT_CUDA_TRY(cudaMemsetAsync(hS, 0, sizeof(int64_t) * 2 * (size_t)TB * nn, s));
-                        sub_hist_kernel<<<nsm, SUB_NT, hsm, s>>>(binsR, d_L, perm, g, h, items, cnts, d_rng, d_rowbase,
-                                                                 d_gbase, d_nbk, hS, (int)hb, (int)he);
+                        sub_hist_kernel<<<wu_root + nn * NR_max, SUB_NT, hsm, s>>>(binsR, d_L, perm, g, h, units, cnts + 2,
+                                                                                   d_rowbase, d_gbase, d_nbk, hS,
+                                                                                   (int)hb, (int)he);
                         note_launch();
                         AT_LAUNCH_CHECK("histograms");
                     }
@@ -2663,9 +2732,8 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                 }
                 {
                     ProfScope ps(AT_K_FIT_HIST, s);
-                    sub_zero_kernel<<<zgrid, 256, 0, s>>>(hc, d_L, 2 * nn); note_launch();
-                    sub_hist_kernel<<<nsm, SUB_NT, hsm, s>>>(binsR, d_L, perm, g, h, items, cnts, d_rng, d_rowbase,
-                                                             d_gbase, d_nbk, hc, 0, (int)n);
+                    sub_hist_kernel<<<wu_root + nn * NR_max, SUB_NT, hsm, s>>>(binsR, d_L, perm, g, h, units, cnts + 2,
+                                                                               d_rowbase, d_gbase, d_nbk, hc, 0, (int)n);
                     note_launch();
                     sub_subtract_kernel<<<dim3(64, nn), 256, 0, s>>>(hp, hc, d_L, subs, cnts + 1);
                     note_launch();
@@ -2679,7 +2747,7 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
                                                                   d_tree, dead, n_int + n_leaf);
                 note_launch();
                 sub_final_kernel<<<nblk(n, 256), 256, 0, s>>>(bins, n, node, split_f, split_s, n_int, t_leaf, pred,
-                                                              d_tree);
+                                                              d_tree, hA, d_L);
                 note_launch();
                 sub_tree_next_kernel<<<1, 1, 0, s>>>(d_tree);
                 note_launch();
