@@ -498,21 +498,36 @@ def other_configs(dev, stream, peaks):
     sp5 = at.Space(synth.ALL_RESNET)
     ens = synth.ensemble(2000, 8, seed=SEED)
     g5 = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
-    n5, chunk = 10 ** 7, 1 << 22
+    n5, chunk = 10 ** 8, 1 << 24   # north_star's 10^8 sweep, 2^24-candidate chunks (31 GB feature buffer)
     idx5 = torch.from_numpy(synth.sweep_indices(sp5.size(), 0, n5).view(np.int64)).to(dev)
     X5 = torch.empty((468, chunk), dtype=torch.float32, device=dev)
     s5 = torch.empty(n5, dtype=torch.float32, device=dev)
+    spans = [(c0, min(n5, c0 + chunk)) for c0 in range(0, n5, chunk)]
+
+    def feats():
+        for c0, c1 in spans:
+            sp5.features(idx5[c0:c1], out=X5, ld=chunk)
+
+    def preds():   # every chunk scored from the last chunk's features: the same work per call
+        for c0, c1 in spans:
+            g5.predict(X5, n=c1 - c0, out=s5[c0:c1])
 
     def run5():
-        for c0 in range(0, n5, chunk):
-            c1 = min(n5, c0 + chunk)
+        for c0, c1 in spans:
             sp5.features(idx5[c0:c1], out=X5, ld=chunk)
             g5.predict(X5, n=c1 - c0, out=s5[c0:c1])
 
     ms5 = _events(stream, run5, reps=1, warm=1)
-    out["cfg5_sweep_1e7"] = {"candidates": n5, "trees": 2000, "depth": 8, "ms": round(ms5, 2),
+    ms5f = _events(stream, feats, reps=1, warm=0)
+    ms5p = _events(stream, preds, reps=1, warm=0)
+    out["cfg5_sweep_1e8"] = {"candidates": n5, "trees": 2000, "depth": 8, "ms": round(ms5, 2),
                              "cand_per_s": round(n5 / (ms5 / 1e3), 1),
+                             "features_extract_ms": round(ms5f, 2),
+                             "gbt_predict_ms": round(ms5p, 2),
+                             "gbt_predict_cand_per_s": round(n5 / (ms5p / 1e3), 1),
+                             "gbt_predict_Gnode_steps_per_s": round(n5 * 16000 / (ms5p / 1e3) / 1e9, 1),
                              "Gnode_steps_per_s": round(n5 * 16000 / (ms5 / 1e3) / 1e9, 1)}
+    del X5, idx5, s5
     return out
 
 
