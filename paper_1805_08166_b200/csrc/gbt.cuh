@@ -59,6 +59,9 @@ __device__ __forceinline__ void ts_issue_slice(const TreeGeo &G, uint8_t *bufs, 
     bulk_g2s(dst + (size_t)G.CH * G.ni * G.nbytes, G.leaf + (int64_t)t0 * G.nl, lb, &bar[slot]);
 }
 constexpr int TS_MAXBUF = 4;
+#ifndef AT_SA_SPEC
+#define AT_SA_SPEC 1   // speculative levels of the eb walk: 1 = the root's children + the leaf pair (measured best)
+#endif
 
 constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // default per buffer (two buffers)
 #ifdef AT_SA_PHASE_TIMING
@@ -84,6 +87,11 @@ __device__ __forceinline__ void ts_issue(const TreeGeo &G, uint8_t *bufs, uint64
     const int nt = min(G.CH, G.T_pad - t0);
     const uint32_t nb = (uint32_t)nt * G.ni * (uint32_t)G.nbytes, lb = (uint32_t)nt * G.nl * 4u;
     uint8_t *dst = bufs + (size_t)b * G.chunk_bytes;
+#ifdef AT_SA_NOSTREAM
+    // experiment only (tools): after the first buffers, complete the chunk without copying -- the walk
+    // then reuses stale trees, which isolates the cost of the L2 -> shared stream
+    if (c >= (uint64_t)G.NBUF) { mbar_arrive(&bar[b]); return; }
+#endif
     if (G.leaf_global) {
         mbar_arrive_expect_tx(&bar[b], nb);
         bulk_g2s(dst, G.nodes + (int64_t)t0 * G.ni * G.nbytes, nb, &bar[b]);
@@ -266,36 +274,77 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
             if (walker) {
                 mbar_wait(&bar[b], par);
                 if (t < T) {
+                    // Speculative descent: on the top SPEC levels a node's two children (adjacent in the
+                    // heap) are loaded beside its feature value, so the dependent chain per level is one
+                    // shared load instead of two; the last level loads its two leaves (one 8-B pair)
+                    // beside the feature.  Same comparisons, same leaves: bit-identical to the plain walk.
+                    constexpr int SPEC = D - 1 < AT_SA_SPEC ? D - 1 : AT_SA_SPEC;
                     const uint32_t tb = tbw + boff;
                     const uint32_t add_l = 0u - tb, add_r = 8u - tb;
-                    uint32_t a[GRP];
-                    {
-                        uint32_t nf, nt;
-                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(tb + 8u));
+                    uint32_t a[GRP], cf[GRP], ct[GRP];   // current node: address, feature, threshold bits
+                    {   // the root and its two children: one load each serves every group
+                        uint32_t rf, rt, lf, lt, qf, qt;
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(rf), "=r"(rt) : "r"(tb + 8u));
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lf), "=r"(lt) : "r"(tb + 16u));
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(qf), "=r"(qt) : "r"(tb + 24u));
 #pragma unroll
                         for (int g = 0; g < GRP; ++g) {
                             float x;
-                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
-                            a[g] = 2u * (tb + 8u) + (x < __uint_as_float(nt) ? add_l : add_r);
+                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (rf << 7)));
+                            const bool c = x < __uint_as_float(rt);
+                            a[g] = c ? tb + 16u : tb + 24u;
+                            cf[g] = c ? lf : qf;
+                            ct[g] = c ? lt : qt;
                         }
                     }
 #pragma unroll
-                    for (int d = 1; d < D; ++d) {
+                    for (int d = 1; d < SPEC; ++d) {
 #pragma unroll
                         for (int g = 0; g < GRP; ++g) {
-                            uint32_t nf, nt;
+                            const uint32_t la = 2u * a[g] + add_l;
+                            uint32_t lf, lt, qf, qt;
                             float x;
-                            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g]));
-                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
-                            a[g] = 2u * a[g] + (x < __uint_as_float(nt) ? add_l : add_r);
+                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (cf[g] << 7)));
+                            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lf), "=r"(lt) : "r"(la));
+                            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(qf), "=r"(qt) : "r"(la + 8u));
+                            const bool c = x < __uint_as_float(ct[g]);
+                            a[g] = c ? la : la + 8u;
+                            cf[g] = c ? lf : qf;
+                            ct[g] = c ? lt : qt;
                         }
                     }
+                    // a[g] is a level-SPEC node with its data in (cf, ct)
+                    if constexpr (SPEC < D - 1) {
+#pragma unroll
+                        for (int g = 0; g < GRP; ++g) {
+                            float x;
+                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (cf[g] << 7)));
+                            a[g] = 2u * a[g] + (x < __uint_as_float(ct[g]) ? add_l : add_r);
+                        }
+#pragma unroll
+                        for (int d = SPEC + 1; d < D - 1; ++d) {
+#pragma unroll
+                            for (int g = 0; g < GRP; ++g) {
+                                uint32_t nf, nt;
+                                float x;
+                                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g]));
+                                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
+                                a[g] = 2u * a[g] + (x < __uint_as_float(nt) ? add_l : add_r);
+                            }
+                        }
+#pragma unroll
+                        for (int g = 0; g < GRP; ++g)
+                            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cf[g]), "=r"(ct[g]) : "r"(a[g]));
+                    }
+                    // last level: its feature value and its two leaves (slots 2 idx + 2 - 2^D, + 1) together
                     const int j = (t & 31) / NW;
 #pragma unroll
                     for (int g = 0; g < GRP; ++g) {
-                        const uint32_t slot = ((a[g] + add_l) >> 3) - nl;
-                        float lv;
-                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lv) : "r"(lfw + boff + slot * 4u));
+                        const uint32_t slot = ((a[g] + add_l) >> 2) - nl;
+                        float x, lL, lR;
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (cf[g] << 7)));
+                        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(lL), "=f"(lR) : "r"(lfw + boff + slot * 4u));
+                        const float lv = x < __uint_as_float(ct[g]) ? lL : lR;
 #pragma unroll
                         for (int q = 0; q < NQ; ++q)
                             if (q == j) p[g][0][q] = __fadd_rn(p[g][0][q], lv);
