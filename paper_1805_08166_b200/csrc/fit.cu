@@ -2030,6 +2030,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
                         if (j < N) { iv[k] = ord[j]; qv[k] = nat[j]; }
                     }
                 }
+                FT_MARK(5);   // (instrumented builds: partition)
                 // prefix sums of (g, h) in this order; node bases and totals
                 long long pg[EP], ph[EP];
                 int qb[EP];   // node << 8 | bin of each owned position
@@ -2070,6 +2071,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
                     }
                 }
                 __syncthreads();
+                FT_MARK(6);   // (prefix sums)
                 // every run end of every node: the split s = b + 1 (left = bins <= b), fp64 gain in
                 // the oracle's operation order
                 unsigned long long gk[EP];
@@ -2118,6 +2120,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
                     if (gk[k] && gk[k] == (((unsigned long long)T.nbh[(qb[k] >> 8)] << 32) | T.nbl[(qb[k] >> 8)]))
                         atomicMin(&T.nms[(qb[k] >> 8)], (unsigned)((qb[k] & 0xFF) + 1));
                 __syncthreads();
+                FT_MARK(7);   // (gains + per-node shared maxima)
                 for (int q = tid; q < nn; q += NT) {
                     const unsigned long long gb = ((unsigned long long)T.nbh[q] << 32) | T.nbl[q];
                     if (gb)
@@ -2224,15 +2227,19 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
 #ifdef AT_FIT_TIMING
     FT_MARK(4);
     if (threadIdx.x == 0) {
-        atomicMax(&g_ft_work_max, ft[2]);
+        atomicMax(&g_ft_work_max, ft[2] + ft[5] + ft[6] + ft[7]);
         atomicMax(&g_ft_grad_max, ft[0]);
         __threadfence();
     }
     if (blockIdx.x == 0 && threadIdx.x == 0)
         printf("fused forest ns/tree (block 0, G=%d): grads %llu gsync %llu | levels: work %llu sync %llu | "
                "decide+leaves %llu | max over blocks: grads %llu work %llu (from earlier-finishing blocks)\n", G,
-               ft[0] / A.n_trees, ft[1] / A.n_trees, ft[2] / A.n_trees, ft[3] / A.n_trees, ft[4] / A.n_trees,
+               ft[0] / A.n_trees, ft[1] / A.n_trees, ft[2] / A.n_trees + ft[5] / A.n_trees + ft[6] / A.n_trees +
+               ft[7] / A.n_trees, ft[3] / A.n_trees, ft[4] / A.n_trees,
                g_ft_grad_max / A.n_trees, g_ft_work_max / A.n_trees);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("level work split (ns/tree): partition %llu prefix %llu gains+maxima %llu slot+store %llu\n",
+               ft[5] / A.n_trees, ft[6] / A.n_trees, ft[7] / A.n_trees, ft[2] / A.n_trees);
     if (blockIdx.x == 0 && threadIdx.x == 0)
         printf("barrier (last arriver: arrival -> release seen): %llu ns avg over %llu\n",
                g_ft_bar_n ? g_ft_bar_ns / g_ft_bar_n : 0ull, g_ft_bar_n);

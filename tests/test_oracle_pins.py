@@ -152,6 +152,15 @@ def test_appendix_c_matmul_example():
           sp.factors(0, 2).index(tuple(s["k"])), [1, 2, 4, 8, 16].index(gold["unroll"])]
     _check_rows(sp, ch, gold, 8)
     x = sp.features([sp.encode(ch)])[0]
+    # the feature vector's row blocks (Appendix A: 19 columns per loop -- length, the
+    # annotation one-hot, top-down, bottom-up, then (touch, reuse, stride) of C, A, B) hold the golden rows
+    for k, g in enumerate(gold["rows"]):
+        z = x[19 * k: 19 * k + 19]
+        assert [z[0], z[8], z[9]] == g[:3], gold["loops"][k]
+        assert list(z[10:19]) == g[3:12], gold["loops"][k]
+        hot = [0.0] * 7
+        hot[ANN[gold["annotations"][k]]] = 1.0
+        assert list(z[1:8]) == hot, gold["loops"][k]
     rel = gold["relation_t1_6"]
     for b, name in enumerate("CAB"):
         assert list(x[342 + 40 * b: 342 + 40 * b + 6]) == rel[f"{name}_reuse"]
@@ -686,6 +695,41 @@ def test_fit_root_split_equals_exact_greedy():
     for slot, m in ((0, left), (1, ~left)):
         w = -0.1 * (G[m].sum() / (H[m].sum() + lam))
         assert out["leaf"][0, slot] == pytest.approx(w, rel=1e-6)
+
+
+def test_fit_min_gain_is_lambda_regularised():
+    """Q37's gain G_L^2/(H_L+lam) + G_R^2/(H_R+lam) - G^2/(H+lam) decides whether the root splits at all.
+    Regression loss (g = 2 (f - c), h = 2), one feature x = (0, 0, 1, 1), lam = 1: for costs
+    (1, 1, 1 + d, 1 + d) the gain is positive iff (1 + (1+d)^2)/5 > (2+d)^2/9, i.e. d > 1 (by hand);
+    d = 1.5 splits (leaves -G_L/(H_L+lam) = 0.8 and 10/5 = 2.0 at eta = 1), d = 0.5 does not (a
+    pass-through root, threshold +inf, left leaf -G/(H+lam) = 10/9)."""
+    X = np.array([[0.0], [0.0], [1.0], [1.0]], np.float32)
+    key = np.zeros(4, np.uint16)
+    out = O.fit_hist(X, np.array([1, 1, 2.5, 2.5], np.float32), key, n_trees=1, depth=1, eta=1.0, lam=1.0,
+                     min_child_weight=1.0, objective="reg")
+    assert out["feat"][0, 0] == 0 and out["thresh"][0, 0] == 1.0
+    assert out["leaf"][0].tolist() == pytest.approx([0.8, 2.0], rel=1e-6)
+    out = O.fit_hist(X, np.array([1, 1, 1.5, 1.5], np.float32), key, n_trees=1, depth=1, eta=1.0, lam=1.0,
+                     min_child_weight=1.0, objective="reg")
+    assert np.isinf(out["thresh"][0, 0])
+    assert out["leaf"][0, 0] == pytest.approx(10.0 / 9.0, rel=1e-6)
+
+
+def test_fit_min_child_weight_and_tie_rule():
+    """Q37: a split needs H_L, H_R >= min_child_weight; equal gains go to the lower feature (then the lower
+    split).  Regression loss (h = 2 per sample), x = (0, 0, 0, 1), costs (0, 0, 0, 10): the only split
+    leaves H_R = 2, so min_child_weight 3 forbids it and 1 allows it (its gain 400/3 - 400/9 > 0 by hand).
+    Two identical columns give two equal gains: feature 0 wins."""
+    key = np.zeros(4, np.uint16)
+    X = np.array([[0.0], [0.0], [0.0], [1.0]], np.float32)
+    c = np.array([0, 0, 0, 10], np.float32)
+    kw = dict(n_trees=1, depth=1, eta=1.0, lam=1.0, objective="reg")
+    assert np.isinf(O.fit_hist(X, c, key, min_child_weight=3.0, **kw)["thresh"][0, 0])
+    out = O.fit_hist(X, c, key, min_child_weight=1.0, **kw)
+    assert out["feat"][0, 0] == 0 and out["thresh"][0, 0] == 1.0
+    X2 = np.array([[0.0, 0.0], [0.0, 0.0], [1.0, 1.0], [1.0, 1.0]], np.float32)
+    out = O.fit_hist(X2, np.array([1, 1, 2.5, 2.5], np.float32), key, min_child_weight=1.0, **kw)
+    assert out["feat"][0, 0] == 0 and out["thresh"][0, 0] == 1.0
 
 
 def test_fit_reduces_rank_loss():
