@@ -986,6 +986,7 @@ __global__ void sub_layout_kernel(const int32_t *__restrict__ ncuts, const int32
         }
         NE += __shfl_sync(0xFFFFFFFFu, x, 31);
     }
+    AT_DCHECK(FsP <= FsP_max);
     if (lane == 0) {
         L->Fs = Fs;
         L->FsP = FsP;
