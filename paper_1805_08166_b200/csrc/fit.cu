@@ -1722,7 +1722,7 @@ template <int EP, int NT>
 __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ? 3 : 4)) fused_forest_kernel(FusedArgs A)
 {
 #ifdef AT_FIT_TIMING
-    unsigned long long ft[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer(), t_arr = 0;
+    unsigned long long ft[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, ft_last = gtimer(), t_arr = 0;
 #endif
     extern __shared__ __align__(16) unsigned char fsm[];
     const int N = A.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2107,6 +2107,10 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
                         if (gain > 0.0) gk[k] = (unsigned long long)__double_as_longlong(gain);
                     }
                 }
+#ifdef AT_FIT_TIMING
+                __syncthreads();   // (instrumented builds: the gains alone)
+                FT_MARK(8);
+#endif
                 // per-node max: gain high word, low word, then the lowest s among equal gains
 #pragma unroll
                 for (int k = 0; k < EP; ++k)
@@ -2228,7 +2232,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
 #ifdef AT_FIT_TIMING
     FT_MARK(4);
     if (threadIdx.x == 0) {
-        atomicMax(&g_ft_work_max, ft[2] + ft[5] + ft[6] + ft[7]);
+        atomicMax(&g_ft_work_max, ft[2] + ft[5] + ft[6] + ft[7] + ft[8]);
         atomicMax(&g_ft_grad_max, ft[0]);
         __threadfence();
     }
@@ -2236,11 +2240,11 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
         printf("fused forest ns/tree (block 0, G=%d): grads %llu gsync %llu | levels: work %llu sync %llu | "
                "decide+leaves %llu | max over blocks: grads %llu work %llu (from earlier-finishing blocks)\n", G,
                ft[0] / A.n_trees, ft[1] / A.n_trees, ft[2] / A.n_trees + ft[5] / A.n_trees + ft[6] / A.n_trees +
-               ft[7] / A.n_trees, ft[3] / A.n_trees, ft[4] / A.n_trees,
+               ft[7] / A.n_trees + ft[8] / A.n_trees, ft[3] / A.n_trees, ft[4] / A.n_trees,
                g_ft_grad_max / A.n_trees, g_ft_work_max / A.n_trees);
     if (blockIdx.x == 0 && threadIdx.x == 0)
-        printf("level work split (ns/tree): partition %llu prefix %llu gains+maxima %llu slot+store %llu\n",
-               ft[5] / A.n_trees, ft[6] / A.n_trees, ft[7] / A.n_trees, ft[2] / A.n_trees);
+        printf("level work split (ns/tree): partition %llu prefix %llu gains %llu maxima %llu slot+store %llu\n",
+               ft[5] / A.n_trees, ft[6] / A.n_trees, ft[8] / A.n_trees, ft[7] / A.n_trees, ft[2] / A.n_trees);
     if (blockIdx.x == 0 && threadIdx.x == 0)
         printf("barrier (last arriver: arrival -> release seen): %llu ns avg over %llu\n",
                g_ft_bar_n ? g_ft_bar_ns / g_ft_bar_n : 0ull, g_ft_bar_n);
