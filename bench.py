@@ -158,6 +158,7 @@ class Config3:
         from paper_1805_08166_b200 import at, synth
         from paper_1805_08166_b200 import dist as D
         self.at, self.world = at, world
+        self.grouped = torch.distributed.is_initialized()   # the exchange runs whenever a group exists
         self.space = at.Space(synth.ALL_RESNET)
         ens = synth.ensemble(T_TREES, DEPTH, seed=SEED)
         self.model = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
@@ -188,7 +189,7 @@ class Config3:
                             chain_workload=self.cw, measured=meas, init=self.first, chain_id_base=self.base)
         self.first = False
         oi, osc, on = res["out_idx"], res["out_score"], res["out_n"]
-        if self.world > 1:
+        if self.grouped:
             gi, gs, gn = D.gather_lists(oi, osc, on)
             oi, osc, on = at.topk_merge(self.space, gi, gs, gn, K_POOL, measured=meas)
         sel, _ = at.select_topk_batch(self.space, oi, osc, on, b=B, eps=EPS, alpha=ALPHA, seed=SEED, round_=r,
@@ -226,8 +227,13 @@ def run_ours(args):
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    grouped = world > 1 or args.dist
+    if grouped:
+        # --dist at N = 1: a one-rank NCCL group, so the N > 1 code path (all-gather, merge, max-over-ranks,
+        # the candidate split) runs and can be checked on one GPU
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     stream = torch.cuda.current_stream()
     peaks = _peaks()
     c3 = Config3(rank, world, dev)
@@ -242,7 +248,7 @@ def run_ours(args):
     at.prof_enable(True)
     launches0 = at.launch_count()
     evs = []
-    if world > 1:
+    if grouped:
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
@@ -254,7 +260,7 @@ def run_ours(args):
             e1.record(stream)
             evs.append((e0, e1))
         torch.cuda.synchronize()
-        if world > 1:
+        if grouped:
             dist.barrier()
     launches = at.launch_count() - launches0
     at.prof_enable(False)
@@ -268,7 +274,7 @@ def run_ours(args):
 
     roofline = sa_roofline(prof, sum(step_ms), c3.cnt, peaks)
     extra = {}
-    if world == 1 and not args.quick:
+    if not grouped and not args.quick:
         extra["e2e"] = run_e2e(args, c3, dev, stream, world)
         extra["config2_round"] = config2_round(dev, stream)
         extra["configs"] = other_configs(dev, stream, peaks)
@@ -288,11 +294,11 @@ def run_ours(args):
     for k in ("config2_round", "configs", "cfg5_split"):
         if k in extra:
             out[k] = extra[k]
-    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):
+    if rank == 0 and not grouped and not (args.no_cpu_baseline or args.quick):
         out["cpu_baseline"] = cpu_baseline()
     if rank == 0:
-        print(json.dumps(out), flush=True)
-    if world > 1:
+        print(json.dumps(out), file=_JSON_OUT, flush=True)
+    if grouped:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -391,7 +397,7 @@ def cfg5_split(rank, world, dev, stream, n=10 ** 7, chunk=1 << 22):
 
     run()
     torch.cuda.synchronize()
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.barrier()
     a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
@@ -642,19 +648,36 @@ def run_reference(args):
                                    f"|D|={D_SIZE}; single-threaded C oracle", "cpu": _cpu_model()},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    print(json.dumps(out), file=_JSON_OUT, flush=True)
 
 
-def _self_launch(args):
-    """--gpus N > 1 outside torchrun: start N ranks on this node (127.0.0.1) and pass their output on."""
+def _free_port() -> int:
     import socket
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
+    return port
+
+
+def _self_launch(args):
+    """--gpus N > 1 outside torchrun: start N ranks on this node (127.0.0.1) and pass their output on."""
+    port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd)
+
+
+_JSON_OUT = sys.stdout
+
+
+def _claim_stdout():
+    """stdout carries exactly one JSON line: keep a private handle on it and point fd 1 at stderr, so
+    anything else a library prints there (NCCL's version banner, warnings) cannot interleave."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
 
 
 def main():
@@ -664,10 +687,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="N = 1: run the N > 1 code path in a one-rank NCCL group")
     ap.add_argument("--quick", action="store_true", help="timed steps only (no e2e / extra configs / cpu baseline): for ncu")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         raise SystemExit(_self_launch(args))
+    _claim_stdout()
     if args.impl == "reference":
         run_reference(args)
     else:

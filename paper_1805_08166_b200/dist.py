@@ -22,6 +22,12 @@ def world():
     return 0, 1
 
 
+def _grouped() -> bool:
+    """A process group exists (of any size, 1 included): the collectives below then always run, so the
+    NCCL path is exercised even on one GPU."""
+    return dist.is_available() and dist.is_initialized()
+
+
 def chain_slice(n_per_rank: int, rank: int):
     """Global chain-id base and count of this rank (weak scaling: n_per_rank chains per GPU)."""
     return rank * n_per_rank, n_per_rank
@@ -64,7 +70,7 @@ def gather_lists(out_idx: torch.Tensor, out_score: torch.Tensor, out_n: torch.Te
     """All-gather every rank's [n_w][k] top-k lists -> [world][n_w][k]: the lists are packed into one
     int64 buffer and exchanged by ONE all_gather_into_tensor (NCCL over NVLink on the GPU box)."""
     rank, ws = world()
-    if ws == 1:
+    if not _grouped():
         return out_idx[None], out_score[None], out_n[None]
     nw, k = out_idx.shape
     mine = pack_lists(out_idx, out_score, out_n)
@@ -88,8 +94,7 @@ def make_allreduce(group=None):
 
 
 def max_over_ranks(x: float, device=None) -> float:
-    rank, ws = world()
-    if ws == 1:
+    if not _grouped():
         return x
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -97,8 +102,7 @@ def max_over_ranks(x: float, device=None) -> float:
 
 
 def sum_over_ranks(x: float, device=None) -> float:
-    rank, ws = world()
-    if ws == 1:
+    if not _grouped():
         return x
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)

@@ -1324,3 +1324,48 @@ def test_fused_scoring_is_sa_with_zero_steps(at):
         k = int(r["out_n"][wl])
         assert_bits_equal(host_u64(r["out_idx"][wl][:k]), idx[m][order][:k], f"workload {wl} top-k")
 
+
+
+# ------------------------------------------------------------------ NCCL plumbing on the GPU (world size 1)
+def test_nccl_world1_gather_merge_and_allreduce_fit(at):
+    """The bench's NCCL code path on one B200: a world-size-1 NCCL process group, so the packed
+    all_gather_into_tensor of the per-workload top-k lists, topk_merge of the gathered lists, the
+    histogram all-reduce of the multi-rank subtraction refit (NCCL on the library's stream through the
+    callback) and the max-over-ranks timing reduction all run through NCCL; each equals the group-free
+    result bit for bit (with one rank every collective is the identity)."""
+    import socket
+    import torch.distributed as tdist
+    from paper_1805_08166_b200 import dist as D
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sp = at.Space(synth.ALL_RESNET)
+    ens = synth.ensemble(100, 8, seed=45)
+    g = at.Gbt(ens["feat"], ens["thresh"], ens["leaf"])
+    n, steps, K = 2400, 8, 24
+    temps = dev(synth.temperatures(steps, synth.energy_scale(100)))
+    one = at.sa_explore(sp, g, torch.zeros(n, dtype=torch.int64, device="cuda"), temps, seed=4, round_=0, k_out=K,
+                        chain_workload=D.chain_workloads(0, n, 12, "cuda"), init=True)
+    osp, idx, Xo, c, key = fit_inputs(3000, [synth.CFG2A, synth.CFG2B], seed=46)
+    Xg = at.Space([synth.CFG2A, synth.CFG2B]).features(u64(idx))
+    cg, kg = dev(c), dev(key.view(np.int16))
+    ref = at.gbt_fit_hist(Xg, 3000, cg, kg, n_trees=4, depth=5).export()
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        gi, gs, gn = D.gather_lists(one["out_idx"], one["out_score"], one["out_n"])
+        assert gi.shape == (1, 12, K)
+        mi, ms, mn = at.topk_merge(sp, gi, gs, gn, K)
+        assert torch.equal(mn, one["out_n"])
+        for w in range(12):
+            k = int(mn[w])
+            assert torch.equal(mi[w][:k], one["out_idx"][w][:k])
+            assert torch.equal(ms[w][:k].view(torch.int32), one["out_score"][w][:k].view(torch.int32))
+        m = at.gbt_fit_hist(Xg, 3000, cg, kg, n_trees=4, depth=5, hist_range=(0, 3000), allreduce=D.make_allreduce())
+        ex = m.export()
+        for k in ("feat", "thresh", "leaf"):
+            assert_bits_equal(ex[k], ref[k], f"NCCL-reduced fit {k}")
+        assert D.max_over_ranks(1.5, torch.device("cuda", 0)) == 1.5
+    finally:
+        tdist.destroy_process_group()
