@@ -2487,18 +2487,34 @@ extern "C" int gbt_fit_hist(const float *d_feat, int64_t n, int64_t ld, int32_t 
         const void *fk = nullptr;
         int NT = 512, fep = 1;
         size_t fsm = 0;
-        static size_t fused_attr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        static size_t fused_attr[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        static int trim_env = -1;
+        if (trim_env < 0) {
+            const char *e = getenv("AT_FIT_NT_TRIM");   // "0": keep 256 threads at 8 positions each
+            trim_env = e ? atoi(e) : 1;
+        }
         for (int pass = 0; pass < 2; ++pass) {
             NT = pass == 0 ? 512 : 256;
             fep = fused_ep((int)n, NT);
             fsm = fused_smem_bytes((int)n, GS);
+            int fslot = (pass == 0 ? 0 : 4) + (fep == 1 ? 0 : fep == 2 ? 1 : fep == 4 ? 2 : 3);
             if (NT == 512)
                 fk = fep == 1 ? (const void *)fused_forest_kernel<1, 512> : fep == 2 ? (const void *)fused_forest_kernel<2, 512>
                    : (const void *)fused_forest_kernel<4, 512>;
             else
                 fk = fep == 1   ? (const void *)fused_forest_kernel<1, 256> : fep == 2 ? (const void *)fused_forest_kernel<2, 256>
                    : fep == 4 ? (const void *)fused_forest_kernel<4, 256> : (const void *)fused_forest_kernel<8, 256>;
-            const int fslot = (pass == 0 ? 0 : 4) + (fep == 1 ? 0 : fep == 2 ? 1 : fep == 4 ? 2 : 3);
+            if (NT == 256 && fep == 8 && trim_env) {
+                // 8 positions per thread: only ceil(n / 256) warps hold positions (1536 -> 6 of 8); drop the
+                // idle warps, whose block barriers and scans are pure overhead
+                const int nt = (int)((n + 255) / 256) * 32;
+                if (nt < 256) {
+                    NT = nt;
+                    fk = nt == 160 ? (const void *)fused_forest_kernel<8, 160> : nt == 192 ? (const void *)fused_forest_kernel<8, 192>
+                       : (const void *)fused_forest_kernel<8, 224>;
+                    fslot = 8 + (nt / 32 - 5);
+                }
+            }
             if (fused_attr[fslot] < fsm) {
                 AT_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
                 fused_attr[fslot] = fsm;

@@ -592,7 +592,10 @@ def _check_paths(outs, ref, keys=("feat", "thresh", "leaf", "pred")):
                                                   (333, synth.ALL_DW[:5], 4, 3, 2),
                                                   (1000, [synth.MATMUL_512], 3, 5, 1024),
                                                   (1, [synth.CFG2A], 2, 4, 64),
-                                                  (37, [synth.CFG2A, synth.CFG2B], 3, 1, 8)])
+                                                  (37, [synth.CFG2A, synth.CFG2B], 3, 1, 8),
+                                                  (1536, synth.ALL_RESNET, 3, 6, 64),       # config 3's |D|: 192 threads
+                                                  (1100, synth.ALL_DW[:3], 2, 5, 64),       # 160 threads
+                                                  (1700, synth.ALL_RESNET[:6], 2, 6, 128)])  # 224 threads
 def test_fit_fused_forest_matches_oracle(at, n, wls, trees, depth, gs):
     osp, idx, X, c, key = fit_inputs(n, wls, seed=n + depth)
     ref = O.fit_hist(X, c, key, n_trees=trees, depth=depth, group_size=gs)
