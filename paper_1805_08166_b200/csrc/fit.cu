@@ -1713,6 +1713,10 @@ __device__ __forceinline__ unsigned long long gtimer()
     return t;
 }
 __device__ unsigned long long g_ft_work_max = 0ull, g_ft_grad_max = 0ull, g_ft_bar_ns = 0ull, g_ft_bar_n = 0ull;
+#ifndef AT_FIT_BLOCKS_DUMP
+#define AT_FIT_BLOCKS_DUMP 0
+#endif
+constexpr bool getenv_blocks_dump = AT_FIT_BLOCKS_DUMP;   // per-block work lines (tools/fit_blocks.py)
 #define FT_MARK(k) do { if (threadIdx.x == 0) { unsigned long long _t = gtimer(); ft[k] += _t - ft_last; ft_last = _t; } } while (0)
 #else
 #define FT_MARK(k) do {} while (0)
@@ -2231,6 +2235,13 @@ __global__ void __launch_bounds__(NT, NT == 512 ? (EP >= 4 ? 1 : 2) : (EP >= 8 ?
     }
 #ifdef AT_FIT_TIMING
     FT_MARK(4);
+    if (threadIdx.x == 0 && getenv_blocks_dump) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        printf("FTBLK %d %u %d %d %llu %llu\n", (int)blockIdx.x, smid, __ldg(A.flist + blockIdx.x),
+               A.ncuts[__ldg(A.flist + blockIdx.x)], (ft[2] + ft[5] + ft[6] + ft[7] + ft[8]) / A.n_trees,
+               ft[8] / A.n_trees);
+    }
     if (threadIdx.x == 0) {
         atomicMax(&g_ft_work_max, ft[2] + ft[5] + ft[6] + ft[7] + ft[8]);
         atomicMax(&g_ft_grad_max, ft[0]);
