@@ -651,6 +651,28 @@ def test_fit_subtraction_many_feature_ranges(at):
     _check_paths(_fit_paths(at, Xg, n, c, key, paths=("subtraction", "level-by-level"), n_trees=2, depth=6), ref)
 
 
+@pytest.mark.parametrize("F,kind", [(1, "quantile"), (1, "constant"), (33, "mixed"), (2, "binary")])
+def test_fit_subtraction_few_features(at, F, kind):
+    """Edge layouts of the device-computed subtraction path (one feature range, a single stripe of 1-2
+    features, one column past a stripe, a lone constant feature) against the oracle, n = 2500, depth 7."""
+    n = 2500
+    rng = np.random.default_rng(F * 7 + len(kind))
+    if kind == "quantile":
+        X = (rng.random((n, F)) * 1e3).astype(np.float32)           # > 256 unique values: 255 cuts
+    elif kind == "constant":
+        X = np.full((n, F), 4.0, np.float32)
+    elif kind == "binary":
+        X = rng.integers(0, 2, (n, F)).astype(np.float32)
+    else:
+        X = rng.integers(0, 300, (n, F)).astype(np.float32)
+        X[:, 5] = 1.0
+    c = (1.0 + rng.random(n) + (X[:, 0] if kind != "constant" else 0) / 500).astype(np.float32)
+    key = (np.arange(n) % 3).astype(np.uint16)
+    ref = O.fit_hist(X, c, key, n_trees=2, depth=7)
+    Xg = dev(np.ascontiguousarray(X.T))
+    _check_paths(_fit_paths(at, Xg, n, c, key, paths=("subtraction",), n_trees=2, depth=7), ref)
+
+
 def test_fit_subtraction_no_splittable_feature(at):
     """Every feature constant (no cut anywhere) on the subtraction path: its device layout lets feature 0
     (one bin) stand in, so the root totals still come from a histogram and every node is a pass-through
