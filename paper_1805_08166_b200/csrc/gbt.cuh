@@ -318,8 +318,9 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
 #pragma unroll
                         for (int g = 0; g < GRP; ++g) {
                             float x;
+                            const uint32_t al = 2u * a[g] + add_l;   // both children's addresses off the chain
                             asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (cf[g] << 7)));
-                            a[g] = 2u * a[g] + (x < __uint_as_float(ct[g]) ? add_l : add_r);
+                            a[g] = x < __uint_as_float(ct[g]) ? al : al + 8u;
                         }
 #pragma unroll
                         for (int d = SPEC + 1; d < D - 1; ++d) {
@@ -327,9 +328,10 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
                             for (int g = 0; g < GRP; ++g) {
                                 uint32_t nf, nt;
                                 float x;
+                                const uint32_t al = 2u * a[g] + add_l;
                                 asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g]));
                                 asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
-                                a[g] = 2u * a[g] + (x < __uint_as_float(nt) ? add_l : add_r);
+                                a[g] = x < __uint_as_float(nt) ? al : al + 8u;
                             }
                         }
 #pragma unroll
@@ -389,10 +391,11 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
                 for (int g = 0; g < GRP; ++g) {
                     uint32_t nf, nt;
                     float x;
+                    const uint32_t al = 2u * a[g] + add_l;   // both children's addresses off the chain
                     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nf), "=r"(nt) : "r"(a[g]));
                     AT_DCHECK(nf < (uint32_t)(gstride / 32));
                     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nf << 7)));
-                    a[g] = 2u * a[g] + (x < __uint_as_float(nt) ? add_l : add_r);
+                    a[g] = x < __uint_as_float(nt) ? al : al + 8u;
                 }
             }
             const int j = (t & 31) / NW;
@@ -471,7 +474,8 @@ __device__ __forceinline__ void walk_stream_rank(const TreeGeo &G, uint8_t *bufs
                         uint32_t nd, x;
                         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nd) : "r"(a[jj][g]));
                         asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nd >> 16)));
-                        a[jj][g] = 2u * a[jj][g] + (x < (nd & 0xFFFFu) ? add_l[jj] : add_r[jj]);
+                        const uint32_t al = 2u * a[jj][g] + add_l[jj];
+                        a[jj][g] = x < (nd & 0xFFFFu) ? al : al + 4u;
                     }
                 }
             }
