@@ -537,7 +537,7 @@ def _emulated_ranks(at, R, Xg, n, cg, kg, **kw):
     return out
 
 
-@pytest.mark.parametrize("n,R,trees,depth,nw", [(100000, 2, 3, 6, 9), (5000, 3, 4, 5, 3)])
+@pytest.mark.parametrize("n,R,trees,depth,nw", [(100000, 2, 3, 6, 9), (5000, 3, 4, 5, 3), (20000, 8, 2, 7, 9)])
 def test_fit_subtraction_path_rank_invariance(at, n, R, trees, depth, nw):
     """Eq. 2: the multi-rank subtraction path -- every rank builds the smaller
     children's histograms over its own sample slice, one int64 all-reduce per level -- gives the
