@@ -280,7 +280,7 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
                     // beside the feature.  Same comparisons, same leaves: bit-identical to the plain walk.
                     constexpr int SPEC = D - 1 < AT_SA_SPEC ? D - 1 : AT_SA_SPEC;
                     const uint32_t tb = tbw + boff;
-                    const uint32_t add_l = 0u - tb, add_r = 8u - tb;
+                    const uint32_t add_l = 0u - tb;   // (the right child is the left one + 8 bytes)
                     uint32_t a[GRP], cf[GRP], ct[GRP];   // current node: address, feature, threshold bits
                     {   // the root and its two children: one load each serves every group
                         uint32_t rf, rt, lf, lt, qf, qt;
@@ -454,12 +454,11 @@ __device__ __forceinline__ void walk_stream_rank(const TreeGeo &G, uint8_t *bufs
             ph[0] ^= 1u;
         }
         if (walker && t < T) {
-            uint32_t a[TPW][GRP], add_l[TPW], add_r[TPW];
+            uint32_t a[TPW][GRP], add_l[TPW];   // (right child = left + 4 bytes)
 #pragma unroll
             for (int jj = 0; jj < TPW; ++jj) {
                 const uint32_t tb = tbw + boff + (uint32_t)(jj * NW) * ni * 4u;
                 add_l[jj] = 0u - tb;
-                add_r[jj] = 4u - tb;
 #pragma unroll
                 for (int g = 0; g < GRP; ++g) a[jj][g] = tb + 4u;
             }
