@@ -553,7 +553,9 @@ __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf,
 // and a __syncthreads.
 // PW >= 0: warp PW is a producer only -- it walks nothing and issues the tree-chunk copies (the
 // issuing work, a proxy fence and two bulk copies, then never delays a walking warp)
-template <int NW, int GRP, int KM = 1, bool RK = false, bool LG = false, int PW = -1>
+// SO: the caller guarantees the stream_one geometry (sa_kernel's specialised variant): only that walk is
+// compiled in, so the hot loop is register-allocated and scheduled on its own
+template <int NW, int GRP, int KM = 1, bool RK = false, bool LG = false, int PW = -1, bool SO = false>
 __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph, uint64_t &c,
                                           uint64_t c_limit, const void *tile, int gstride, int lane, int warp,
                                           float *part, int pstride, uint8_t *__restrict__ slots, int64_t slot_ld,
@@ -576,7 +578,16 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
                              (G.CH == NW || G.CH == 2 * NW) && slots == nullptr && G.D >= 7 && G.D <= 8;
     const bool stream_one = PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG && !G.resident && !G.ring && G.NP <= 1 &&
                             G.CH == NW && slots == nullptr && G.D >= 6 && G.D <= 8;
-    if (PW >= 0 && G.NP > 1) {
+    if constexpr (SO) {
+        static_assert(PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG, "SO: the stream_one geometry only");
+        const float *tf = (const float *)tile;
+        if (G.D == 8)
+            walk_stream_one<NW, GRP, 8, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
+        else if (G.D == 7)
+            walk_stream_one<NW, GRP, 7, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
+        else
+            walk_stream_one<NW, GRP, 6, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
+    } else if (PW >= 0 && G.NP > 1) {
         // NP independent pipelines, no block barrier: warp group p (NW / NP warps) walks its slices -- each
         // warp one tree per slice -- waiting on the slot's full barrier and counting out on its empty
         // barrier; lane q of the producer warp refills pipeline q's slot as soon as its walkers are out.

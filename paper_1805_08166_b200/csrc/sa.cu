@@ -147,7 +147,7 @@ __device__ __forceinline__ void zero_relation(float (*tile)[NFEAT * 32], int lan
 // Block = GRP groups of 32 chains (lane = chain) x SA_NW warps.  Warp g owns group g's chain
 // state; every warp takes part in every group's feature phases and tree walk, so each tree byte
 // staged in shared memory serves 32 GRP chains.
-template <int GRP, int KM, int TM, bool LG = false>
+template <int GRP, int KM, int TM, bool LG = false, bool SO = false>
 __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeGeo G)
 {
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeG
     features_phase(1);
     draw_next(0);
     ts_wait_resident(G, sm.bar);
-    walk_pass<SA_NW, GRP, KM, false, LG, SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+    walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, SO>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
                                               KM == 1 ? &sm.tile[0][0] : &sm.part[0][0], KM == 1 ? NFEAT * 32 : KM * 1024,
                           nullptr, 0, 0, no_slots);
     fold_models(warp, lane);
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeG
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
 #endif
-        walk_pass<SA_NW, GRP, KM, false, LG, SA_NW>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+        walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, SO>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
                               KM == 1 ? &sm.tile[0][0] : &sm.part[0][0], KM == 1 ? NFEAT * 32 : KM * 1024, nullptr, 0,
                               0, no_slots);
 #ifdef AT_SA_PHASE_TIMING
@@ -588,10 +588,20 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
                        at::sa_kernel<1, 1, 2, true>};
     const KF k2l[4] = {at::sa_kernel<2, 1, -1, true>, at::sa_kernel<2, 1, 0, true>, at::sa_kernel<2, 1, 1, true>,
                        at::sa_kernel<2, 1, 2, true>};
+    // the one-tree-per-warp streamed pass (the config-3 geometry): a variant with only that walk compiled in
+    const KF k2s[4] = {at::sa_kernel<2, 1, -1, false, true>, at::sa_kernel<2, 1, 0, false, true>,
+                       at::sa_kernel<2, 1, 1, false, true>, at::sa_kernel<2, 1, 2, false, true>};
     const bool lg = !acq && G.leaf_global;
-    const KF kern = acq ? at::sa_kernel<1, 8, -1> : use2 ? (lg ? k2l : k2)[tm + 1] : (lg ? k1l : k1)[tm + 1];
-    static size_t attr[17] = {0};
-    const int ai = acq ? 16 : (lg ? 8 : 0) + (use2 ? 4 : 0) + tm + 1;
+    static int so_env = -1;
+    if (so_env < 0) {
+        const char *e = getenv("AT_SA_SO");   // "0": the generic kernel (measurement knob)
+        so_env = e ? atoi(e) : 1;
+    }
+    const bool so = so_env && !acq && use2 && !lg && G.CH == at::SA_NW && !G.resident && !G.ring && G.NP <= 1 &&
+                    G.D >= 6 && G.D <= 8;
+    const KF kern = acq ? at::sa_kernel<1, 8, -1> : so ? k2s[tm + 1] : use2 ? (lg ? k2l : k2)[tm + 1] : (lg ? k1l : k1)[tm + 1];
+    static size_t attr[21] = {0};
+    const int ai = acq ? 16 : so ? 17 + tm + 1 : (lg ? 8 : 0) + (use2 ? 4 : 0) + tm + 1;
     if (smem > attr[ai]) {
         AT_CUDA_TRY(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[ai] = smem;
