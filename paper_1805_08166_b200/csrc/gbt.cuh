@@ -182,7 +182,8 @@ __device__ __forceinline__ void walk_batch(const TreeGeo &G, const uint8_t *buf,
                     AT_DCHECK(nf < (uint32_t)(gstride / 32));   // a feature row of the tile
                     AT_DCHECK(((a[g][jj] + add_l[jj]) >> 3) >= 1u && ((a[g][jj] + add_l[jj]) >> 3) <= (uint32_t)ni);   // heap index
                     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(tile_lane + (nf << 7)));
-                    a[g][jj] = 2u * a[g][jj] + (x < __uint_as_float(nt) ? add_l[jj] : add_r[jj]);
+                    const uint32_t al = 2u * a[g][jj] + add_l[jj];
+                    a[g][jj] = x < __uint_as_float(nt) ? al : al + NBY;
                 }
             }
         }
@@ -514,7 +515,7 @@ __device__ __forceinline__ void walk_stream_rank(const TreeGeo &G, uint8_t *bufs
 // whatever the chunk size.  GRP candidate groups of 32 (group g's tile at tile + g * gstride floats)
 // share every staged tree byte.
 template <int GRP, int KM>
-constexpr int walk_nbmax() { return GRP == 1 ? (KM == 1 ? 6 : 4) : 2; }
+constexpr int walk_nbmax() { return GRP == 1 ? (KM == 1 ? 6 : 4) : (GRP == 2 && KM == 1 ? 4 : 2); }
 
 template <int NW, int GRP, int KM, bool RK = false, bool LG = false>
 __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf, int k, const void *tile, int gstride,
