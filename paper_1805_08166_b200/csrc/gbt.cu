@@ -72,7 +72,7 @@ __device__ __forceinline__ void tile_issue(const TileMap &tm, int64_t tile, T *d
 // 2-D TMA (tensor map over X[F][ld]).  GRP = 1: two tile buffers, the next tile's HBM read overlaps
 // the current walk (small, resident ensembles: HBM-bound).  GRP = 2: one buffer of 64 candidates,
 // so every streamed tree byte serves twice the candidates (large ensembles: L2-bound).
-template <int GRP, int KM, bool RK>
+template <int GRP, int KM, bool RK, int ONLY = 0>
 __global__ void __launch_bounds__((PRED_NW + 1) * 32, 1) predict_kernel(TreeGeo G, float base, int F, int tile_rows,
                                                                  const void *__restrict__ Xv, int64_t n, int64_t ld,
                                                                  float *__restrict__ score, uint8_t *__restrict__ slots,
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__((PRED_NW + 1) * 32, 1) predict_kernel(TreeGeo 
                     tl[g * tile_rows * 32 + f * 32 + lane] = ok[g] ? X[(int64_t)f * ld + cand0 + 32 * g] : (T)0;
             __syncthreads();
         }
-        walk_pass<PRED_NW, GRP, KM, RK, false, PRED_NW>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part,
+        walk_pass<PRED_NW, GRP, KM, RK, false, PRED_NW, ONLY>(G, bufs, hd.tree_bar, ph, c, c_limit, tl, tile_rows * 32, lane, warp, part,
                                         KM * 1024, slots,
                                     n, cand0, ok);
         if (KM == 1) {
@@ -452,11 +452,17 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
         const size_t smem = 128 + (size_t)RGRP * 32 * 32 * sizeof(float) + (size_t)RGRP * ptile_rows * 32 * 4 +
                             tree_smem_bytes(G);
         if (!G.resident && smem <= SMEM_MAX) {
-            const void *rk_kern = RGRP == 2 ? (const void *)predict_kernel<2, 1, true> : (const void *)predict_kernel<4, 1, true>;
-            static size_t rk_attr[2] = {0, 0};
-            if (smem > rk_attr[RGRP == 2]) {
+            // the streamed rank pass only (no leaf slots, 16- or 32-tree chunks of depth 7-8 trees): a kernel
+            // variant with only that walk compiled in
+            const bool sr = !d_leaf_slot && !G.ring && G.NP <= 1 && (G.CH == PRED_NW || G.CH == 2 * PRED_NW) &&
+                            G.D >= 7 && G.D <= 8;
+            const void *rk_kern = RGRP == 2 ? (sr ? (const void *)predict_kernel<2, 1, true, 2> : (const void *)predict_kernel<2, 1, true>)
+                                            : (sr ? (const void *)predict_kernel<4, 1, true, 2> : (const void *)predict_kernel<4, 1, true>);
+            static size_t rk_attr[4] = {0, 0, 0, 0};
+            const int rai = (RGRP == 2) + 2 * sr;
+            if (smem > rk_attr[rai]) {
                 AT_CUDA_TRY(cudaFuncSetAttribute(rk_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                rk_attr[RGRP == 2] = smem;
+                rk_attr[rai] = smem;
             }
             pool_keep();   // the rank tiles below are stream-ordered scratch
             const int64_t ldr = (n + 3) / 4 * 4;   // 16-B rows for the tensor map
@@ -496,12 +502,15 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
             AcqArgs Q{};
             {
                 ProfScope ps(AT_K_PREDICT, s);
-                if (RGRP == 2)
-                    predict_kernel<2, 1, true><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
-                                                                                  d_score, d_leaf_slot, use_bulk, tm, Q);
-                else
-                    predict_kernel<4, 1, true><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr,
-                                                                                  d_score, d_leaf_slot, use_bulk, tm, Q);
+#define AT_RK_LAUNCH(GR, ON)                                                                                          \
+    predict_kernel<GR, 1, true, ON><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, P, ptile_rows, Xr, n, ldr, d_score, \
+                                                                          d_leaf_slot, use_bulk, tm, Q)
+                if (RGRP == 2) {
+                    if (sr) AT_RK_LAUNCH(2, 2); else AT_RK_LAUNCH(2, 0);
+                } else {
+                    if (sr) AT_RK_LAUNCH(4, 2); else AT_RK_LAUNCH(4, 0);
+                }
+#undef AT_RK_LAUNCH
                 note_launch();
                 AT_LAUNCH_CHECK("predict_kernel (rank form)");
             }

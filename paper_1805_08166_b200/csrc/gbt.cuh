@@ -554,9 +554,9 @@ __device__ __forceinline__ void walk_chunk(const TreeGeo &G, const uint8_t *buf,
 // and a __syncthreads.
 // PW >= 0: warp PW is a producer only -- it walks nothing and issues the tree-chunk copies (the
 // issuing work, a proxy fence and two bulk copies, then never delays a walking warp)
-// SO: the caller guarantees the stream_one geometry (sa_kernel's specialised variant): only that walk is
-// compiled in, so the hot loop is register-allocated and scheduled on its own
-template <int NW, int GRP, int KM = 1, bool RK = false, bool LG = false, int PW = -1, bool SO = false>
+// ONLY = 1 / 2: the caller guarantees the stream_one (sa_kernel) / stream_rank (gbt_predict rank form)
+// geometry and only that walk is compiled in, so the hot loop is register-allocated and scheduled on its own
+template <int NW, int GRP, int KM = 1, bool RK = false, bool LG = false, int PW = -1, int ONLY = 0>
 __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint64_t *bar, uint32_t *ph, uint64_t &c,
                                           uint64_t c_limit, const void *tile, int gstride, int lane, int warp,
                                           float *part, int pstride, uint8_t *__restrict__ slots, int64_t slot_ld,
@@ -579,8 +579,8 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
                              (G.CH == NW || G.CH == 2 * NW) && slots == nullptr && G.D >= 7 && G.D <= 8;
     const bool stream_one = PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG && !G.resident && !G.ring && G.NP <= 1 &&
                             G.CH == NW && slots == nullptr && G.D >= 6 && G.D <= 8;
-    if constexpr (SO) {
-        static_assert(PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG, "SO: the stream_one geometry only");
+    if constexpr (ONLY == 1) {
+        static_assert(PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG, "ONLY = 1: the stream_one geometry");
         const float *tf = (const float *)tile;
         if (G.D == 8)
             walk_stream_one<NW, GRP, 8, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
@@ -588,6 +588,18 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
             walk_stream_one<NW, GRP, 7, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
         else
             walk_stream_one<NW, GRP, 6, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
+    } else if constexpr (ONLY == 2) {
+        static_assert(PW >= 0 && KM == 1 && RK && !LG, "ONLY = 2: the stream_rank geometry");
+        const uint32_t *tu = (const uint32_t *)tile;
+        const int tpw = G.CH / NW;
+        if (G.D == 8 && tpw == 2)
+            walk_stream_rank<NW, GRP, 8, PW, 2>(G, bufs, bar, ph, c, c_limit, tu, gstride, lane, warp, p);
+        else if (G.D == 8)
+            walk_stream_rank<NW, GRP, 8, PW, 1>(G, bufs, bar, ph, c, c_limit, tu, gstride, lane, warp, p);
+        else if (G.D == 7 && tpw == 2)
+            walk_stream_rank<NW, GRP, 7, PW, 2>(G, bufs, bar, ph, c, c_limit, tu, gstride, lane, warp, p);
+        else
+            walk_stream_rank<NW, GRP, 7, PW, 1>(G, bufs, bar, ph, c, c_limit, tu, gstride, lane, warp, p);
     } else if (PW >= 0 && G.NP > 1) {
         // NP independent pipelines, no block barrier: warp group p (NW / NP warps) walks its slices -- each
         // warp one tree per slice -- waiting on the slot's full barrier and counting out on its empty

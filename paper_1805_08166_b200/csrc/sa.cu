@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeG
     features_phase(1);
     draw_next(0);
     ts_wait_resident(G, sm.bar);
-    walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, SO>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+    walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, SO ? 1 : 0>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
                                               KM == 1 ? &sm.tile[0][0] : &sm.part[0][0], KM == 1 ? NFEAT * 32 : KM * 1024,
                           nullptr, 0, 0, no_slots);
     fold_models(warp, lane);
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeG
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
 #endif
-        walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, SO>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+        walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, SO ? 1 : 0>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
                               KM == 1 ? &sm.tile[0][0] : &sm.part[0][0], KM == 1 ? NFEAT * 32 : KM * 1024, nullptr, 0,
                               0, no_slots);
 #ifdef AT_SA_PHASE_TIMING
