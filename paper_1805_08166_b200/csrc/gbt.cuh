@@ -456,16 +456,24 @@ __device__ __forceinline__ void walk_stream_rank(const TreeGeo &G, uint8_t *bufs
         }
         if (walker && t < T) {
             uint32_t a[TPW][GRP], add_l[TPW];   // (right child = left + 4 bytes)
+            const bool two = TPW > 1 && t + NW < T;   // warp-uniform: the chunk's second tree exists
 #pragma unroll
             for (int jj = 0; jj < TPW; ++jj) {
                 const uint32_t tb = tbw + boff + (uint32_t)(jj * NW) * ni * 4u;
                 add_l[jj] = 0u - tb;
+                if (jj > 0 && !two) break;
+                uint32_t nd;   // the root: one node load serves every group
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nd) : "r"(tb + 4u));
+                const uint32_t al = 2u * (tb + 4u) + add_l[jj];
 #pragma unroll
-                for (int g = 0; g < GRP; ++g) a[jj][g] = tb + 4u;
+                for (int g = 0; g < GRP; ++g) {
+                    uint32_t x;
+                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nd >> 16)));
+                    a[jj][g] = x < (nd & 0xFFFFu) ? al : al + 4u;
+                }
             }
-            const bool two = TPW > 1 && t + NW < T;   // warp-uniform: the chunk's second tree exists
 #pragma unroll
-            for (int d = 0; d < D; ++d) {
+            for (int d = 1; d < D; ++d) {
 #pragma unroll
                 for (int jj = 0; jj < TPW; ++jj) {
                     if (jj > 0 && !two) break;
