@@ -529,10 +529,14 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
     const int grp = (!acq && !G.resident && smem_for(2) <= SMEM_MAX) ? 2 : 1;
     const size_t smem = smem_for(grp);
     if (smem > SMEM_MAX) return fail(AT_EUNSUPPORTED, "gbt_predict: too many features for the smem tiles");
+    // two groups on the generic streamed pass (a chunk barrier every chunk): a variant with only that walk
+    const bool gen = !acq && grp == 2 && !G.resident && !G.ring && G.NP <= 1 &&
+                     !(G.CH == PRED_NW && !d_leaf_slot && G.D >= 6 && G.D <= 8);
     const void *kern = acq ? (const void *)predict_kernel<1, 8, false>
-                     : grp == 1 ? (const void *)predict_kernel<1, 1, false> : (const void *)predict_kernel<2, 1, false>;
-    static size_t attr[3] = {0, 0, 0};
-    const int ai = acq ? 2 : grp - 1;
+                     : grp == 1 ? (const void *)predict_kernel<1, 1, false>
+                     : gen ? (const void *)predict_kernel<2, 1, false, 3> : (const void *)predict_kernel<2, 1, false>;
+    static size_t attr[4] = {0, 0, 0, 0};
+    const int ai = acq ? 2 : gen ? 3 : grp - 1;
     if (smem > attr[ai]) {
         AT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[ai] = smem;
@@ -571,6 +575,9 @@ static int predict_launch(at_gbt g, const float *d_feat, int64_t n, int64_t ld, 
     else if (grp == 1)
         predict_kernel<1, 1, false><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                 d_leaf_slot, use_bulk, tm, Q);
+    else if (gen)
+        predict_kernel<2, 1, false, 3><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld,
+                                                                   d_score, d_leaf_slot, use_bulk, tm, Q);
     else
         predict_kernel<2, 1, false><<<blocks, (PRED_NW + 1) * 32, smem, s>>>(G, g->base, F, tile_rows, d_feat, n, ld, d_score,
                                                                 d_leaf_slot, use_bulk, tm, Q);

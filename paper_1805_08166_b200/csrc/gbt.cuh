@@ -587,6 +587,48 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
                              (G.CH == NW || G.CH == 2 * NW) && slots == nullptr && G.D >= 7 && G.D <= 8;
     const bool stream_one = PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG && !G.resident && !G.ring && G.NP <= 1 &&
                             G.CH == NW && slots == nullptr && G.D >= 6 && G.D <= 8;
+    // the generic streamed pass: a block barrier after every chunk (ONLY = 3 compiles this one alone)
+    auto generic_pass = [&]() {
+        for (int k = 0; k < G.NC; ++k, ++c) {
+            const int b = (int)(c & 1);
+#ifdef AT_SA_PHASE_TIMING
+            long long q0 = clock64();
+#endif
+            if (PW < 0 || c == 0) {   // with a producer warp only the kernel's first chunk is waited for here
+                mbar_wait(&bar[b], ph[b]);
+                ph[b] ^= 1u;
+            }
+#ifdef AT_SA_PHASE_TIMING
+            long long q1 = clock64();
+#endif
+            if (walker) {
+                walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p,
+                                                slots, slot_ld, cand0, cand_ok, pend);
+            } else if (warp == PW && c + 1 < c_limit) {
+                // the producer waits for the NEXT chunk before the block barrier, so the barrier itself
+                // publishes it: the walkers start it without an mbarrier wait of their own
+                const int b1 = (int)((c + 1) & 1);
+                mbar_wait(&bar[b1], ph[b1]);
+                ph[b1] ^= 1u;
+            }
+#ifdef AT_SA_PHASE_TIMING
+            long long q2 = clock64();
+#endif
+            __syncthreads();   // every warp is done with buffer b
+#ifdef AT_SA_PHASE_TIMING
+            if (lane == 0 && warp < 17) {
+                const long long q3 = clock64();
+                s_walk_prof[3 * warp] += q1 - q0;
+                s_walk_prof[3 * warp + 1] += q2 - q1;
+                s_walk_prof[3 * warp + 2] += q3 - q2;
+            }
+#endif
+            if ((PW < 0 ? threadIdx.x == 0 : (warp == PW && lane == 0)) && c + 2 < c_limit) {
+                fence_proxy_async();
+                ts_issue(G, bufs, bar, c + 2);
+            }
+        }
+    };
     if constexpr (ONLY == 1) {
         static_assert(PW >= 0 && GRP == 2 && KM == 1 && !RK && !LG, "ONLY = 1: the stream_one geometry");
         const float *tf = (const float *)tile;
@@ -596,6 +638,8 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
             walk_stream_one<NW, GRP, 7, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
         else
             walk_stream_one<NW, GRP, 6, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
+    } else if constexpr (ONLY == 3) {
+        generic_pass();
     } else if constexpr (ONLY == 2) {
         static_assert(PW >= 0 && KM == 1 && RK && !LG, "ONLY = 2: the stream_rank geometry");
         const uint32_t *tu = (const uint32_t *)tile;
@@ -711,45 +755,7 @@ __device__ __forceinline__ void walk_pass(const TreeGeo &G, uint8_t *bufs, uint6
                 walk_stream_one<NW, GRP, 6, PW>(G, bufs, bar, ph, c, c_limit, tf, gstride, lane, warp, p);
         }
     } else {
-        for (int k = 0; k < G.NC; ++k, ++c) {
-            const int b = (int)(c & 1);
-#ifdef AT_SA_PHASE_TIMING
-            long long q0 = clock64();
-#endif
-            if (PW < 0 || c == 0) {   // with a producer warp only the kernel's first chunk is waited for here
-                mbar_wait(&bar[b], ph[b]);
-                ph[b] ^= 1u;
-            }
-#ifdef AT_SA_PHASE_TIMING
-            long long q1 = clock64();
-#endif
-            if (walker) {
-                walk_chunk<NW, GRP, KM, RK, LG>(G, bufs + (size_t)b * G.chunk_bytes, k, tile, gstride, lane, warp, p,
-                                                slots, slot_ld, cand0, cand_ok, pend);
-            } else if (warp == PW && c + 1 < c_limit) {
-                // the producer waits for the NEXT chunk before the block barrier, so the barrier itself
-                // publishes it: the walkers start it without an mbarrier wait of their own
-                const int b1 = (int)((c + 1) & 1);
-                mbar_wait(&bar[b1], ph[b1]);
-                ph[b1] ^= 1u;
-            }
-#ifdef AT_SA_PHASE_TIMING
-            long long q2 = clock64();
-#endif
-            __syncthreads();   // every warp is done with buffer b
-#ifdef AT_SA_PHASE_TIMING
-            if (lane == 0 && warp < 17) {
-                const long long q3 = clock64();
-                s_walk_prof[3 * warp] += q1 - q0;
-                s_walk_prof[3 * warp + 1] += q2 - q1;
-                s_walk_prof[3 * warp + 2] += q3 - q2;
-            }
-#endif
-            if ((PW < 0 ? threadIdx.x == 0 : (warp == PW && lane == 0)) && c + 2 < c_limit) {
-                fence_proxy_async();
-                ts_issue(G, bufs, bar, c + 2);
-            }
-        }
+        generic_pass();
     }
     if (LG) {   // the last batch's leaves
 #pragma unroll
