@@ -147,7 +147,7 @@ __device__ __forceinline__ void zero_relation(float (*tile)[NFEAT * 32], int lan
 // Block = GRP groups of 32 chains (lane = chain) x SA_NW warps.  Warp g owns group g's chain
 // state; every warp takes part in every group's feature phases and tree walk, so each tree byte
 // staged in shared memory serves 32 GRP chains.
-template <int GRP, int KM, int TM, bool LG = false, bool SO = false>
+template <int GRP, int KM, int TM, bool LG = false, int ONLY = 0>
 __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeGeo G)
 {
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeG
     features_phase(1);
     draw_next(0);
     ts_wait_resident(G, sm.bar);
-    walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, SO ? 1 : 0>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+    walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, ONLY>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
                                               KM == 1 ? &sm.tile[0][0] : &sm.part[0][0], KM == 1 ? NFEAT * 32 : KM * 1024,
                           nullptr, 0, 0, no_slots);
     fold_models(warp, lane);
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(SA_NWARPS * 32, 1) sa_kernel(SaParams P, TreeG
 #ifdef AT_SA_PHASE_TIMING
         { long long t = clock64(); t_feat += t - t0; t0 = t; }
 #endif
-        walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, SO ? 1 : 0>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
+        walk_pass<SA_NW, GRP, KM, false, LG, SA_NW, ONLY>(G, bufs, sm.bar, ph, cs, c_limit, &sm.tile[0][0], NFEAT * 32, lane, warp,
                               KM == 1 ? &sm.tile[0][0] : &sm.part[0][0], KM == 1 ? NFEAT * 32 : KM * 1024, nullptr, 0,
                               0, no_slots);
 #ifdef AT_SA_PHASE_TIMING
@@ -589,8 +589,11 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     const KF k2l[4] = {at::sa_kernel<2, 1, -1, true>, at::sa_kernel<2, 1, 0, true>, at::sa_kernel<2, 1, 1, true>,
                        at::sa_kernel<2, 1, 2, true>};
     // the one-tree-per-warp streamed pass (the config-3 geometry): a variant with only that walk compiled in
-    const KF k2s[4] = {at::sa_kernel<2, 1, -1, false, true>, at::sa_kernel<2, 1, 0, false, true>,
-                       at::sa_kernel<2, 1, 1, false, true>, at::sa_kernel<2, 1, 2, false, true>};
+    const KF k2s[4] = {at::sa_kernel<2, 1, -1, false, 1>, at::sa_kernel<2, 1, 0, false, 1>,
+                       at::sa_kernel<2, 1, 1, false, 1>, at::sa_kernel<2, 1, 2, false, 1>};
+    // one group on the generic streamed pass (config 2): likewise, only that walk compiled in
+    const KF k1g[4] = {at::sa_kernel<1, 1, -1, false, 3>, at::sa_kernel<1, 1, 0, false, 3>,
+                       at::sa_kernel<1, 1, 1, false, 3>, at::sa_kernel<1, 1, 2, false, 3>};
     const bool lg = !acq && G.leaf_global;
     static int so_env = -1;
     if (so_env < 0) {
@@ -599,9 +602,11 @@ extern "C" int sa_explore(at_space sp, at_gbt g, uint64_t *d_chain_idx, float *d
     }
     const bool so = so_env && !acq && use2 && !lg && G.CH == at::SA_NW && !G.resident && !G.ring && G.NP <= 1 &&
                     G.D >= 6 && G.D <= 8;
-    const KF kern = acq ? at::sa_kernel<1, 8, -1> : so ? k2s[tm + 1] : use2 ? (lg ? k2l : k2)[tm + 1] : (lg ? k1l : k1)[tm + 1];
-    static size_t attr[21] = {0};
-    const int ai = acq ? 16 : so ? 17 + tm + 1 : (lg ? 8 : 0) + (use2 ? 4 : 0) + tm + 1;
+    const bool gen1 = so_env && !acq && !use2 && !lg && !G.resident && !G.ring && G.NP <= 1;
+    const KF kern = acq ? at::sa_kernel<1, 8, -1> : so ? k2s[tm + 1] : gen1 ? k1g[tm + 1]
+                  : use2 ? (lg ? k2l : k2)[tm + 1] : (lg ? k1l : k1)[tm + 1];
+    static size_t attr[25] = {0};
+    const int ai = acq ? 16 : so ? 17 + tm + 1 : gen1 ? 21 + tm + 1 : (lg ? 8 : 0) + (use2 ? 4 : 0) + tm + 1;
     if (smem > attr[ai]) {
         AT_CUDA_TRY(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[ai] = smem;
