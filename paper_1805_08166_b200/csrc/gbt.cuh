@@ -425,6 +425,20 @@ __device__ __forceinline__ void walk_stream_one(const TreeGeo &G, uint8_t *bufs,
     c = cc;
 }
 
+// x < (nd & 0xFFFF) for u16 ranks, as one fp16 compare of the low halves: ranks and node ranks are at
+// most 257 (positive fp16 subnormals, ordered like their integers; the compare keeps subnormals) and a
+// NaN feature's rank 0xFFFF is an fp16 NaN, which compares false -- as 0xFFFF < k does.  Returns
+// lt ? al : al + step without a separate mask of nd.
+__device__ __forceinline__ uint32_t rank_step(uint32_t x, uint32_t nd, uint32_t al, uint32_t step)
+{
+    uint32_t r;
+    asm("{\n.reg .b16 xl, xh, kl, kh;\n.reg .pred p;\nmov.b32 {xl, xh}, %1;\nmov.b32 {kl, kh}, %2;\n"
+        "setp.lt.f16 p, xl, kl;\nadd.u32 %0, %3, %4;\n@p mov.u32 %0, %3;\n}"
+        : "=r"(r)
+        : "r"(x), "r"(nd), "r"(al), "r"(step));
+    return r;
+}
+
 // The rank-form counterpart for gbt_predict's streamed depth-6..8 ensembles: chunks of TPW NW trees,
 // TPW trees per walker warp (tree NW (TPW k + jj) + warp, jj < TPW), walked for GRP candidate groups
 // at once (TPW GRP independent chains), 4-byte nodes {k | tile byte offset << 16} against u16
@@ -469,7 +483,7 @@ __device__ __forceinline__ void walk_stream_rank(const TreeGeo &G, uint8_t *bufs
                 for (int g = 0; g < GRP; ++g) {
                     uint32_t x;
                     asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nd >> 16)));
-                    a[jj][g] = x < (nd & 0xFFFFu) ? al : al + 4u;
+                    a[jj][g] = rank_step(x, nd, al, 4u);
                 }
             }
 #pragma unroll
@@ -483,7 +497,7 @@ __device__ __forceinline__ void walk_stream_rank(const TreeGeo &G, uint8_t *bufs
                         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nd) : "r"(a[jj][g]));
                         asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(tile0 + (uint32_t)g * gbytes + (nd >> 16)));
                         const uint32_t al = 2u * a[jj][g] + add_l[jj];
-                        a[jj][g] = x < (nd & 0xFFFFu) ? al : al + 4u;
+                        a[jj][g] = rank_step(x, nd, al, 4u);
                     }
                 }
             }

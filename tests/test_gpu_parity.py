@@ -168,6 +168,45 @@ def test_predict_rank_form_edge_values(at, T, D):
     assert_bits_equal(outs[0][0][fin], es, "scores vs oracle")
 
 
+@pytest.mark.parametrize("rk_grp", ["2", "4"])
+def test_predict_rank_streamed_pass_edge_values(at, rk_grp):
+    """The streamed rank pass (no leaf slots asked for: the predict_kernel<..., ONLY = 2> variant, 2 or 4
+    candidate groups) on the edge values of the test above plus one feature with 256 distinct thresholds
+    (ranks up to 256) and NaN features (rank 0xFFFF, which must go right): scores equal the fp32 walk's
+    and, on finite candidates, the oracle's."""
+    rng = np.random.default_rng(77)
+    T, D = 300, 8
+    ens = synth.ensemble(T, D, seed=78)
+    th, feat = ens["thresh"], ens["feat"]
+    feat[:, 1:40] = 3                                                   # feature 3: 256 distinct thresholds
+    th[:, 1:40] = rng.choice(np.arange(256, dtype=np.float32) * 0.5, size=(T, 39))
+    th[rng.random(th.shape) < 0.02] = np.float32(np.inf)
+    th[rng.random(th.shape) < 0.02] = np.float32(-np.inf)
+    th[rng.random(th.shape) < 0.02] = np.float32(-0.0)
+    n = 5000
+    X = np.power(2.0, rng.integers(0, 42, size=(468, n)) / 2.0).astype(np.float32)
+    X[3] = rng.integers(-2, 260, size=n).astype(np.float32) * 0.5      # every rank of feature 3
+    m = rng.random(X.shape)
+    X[m < 0.01] = np.float32(-0.0)
+    X[(m >= 0.01) & (m < 0.02)] = np.float32(np.inf)
+    X[(m >= 0.02) & (m < 0.03)] = np.float32(-np.inf)
+    X[(m >= 0.03) & (m < 0.04)] = np.float32(np.nan)
+    Xg = dev(np.ascontiguousarray(X))
+    g = at.Gbt(feat, th, ens["leaf"], base=0.25)
+    outs = []
+    for env in ("1", "0"):
+        os.environ.update(AT_PREDICT_RANK=env, AT_RK_GRP=rk_grp)
+        try:
+            outs.append(g.predict(Xg, n=n).cpu().numpy())
+        finally:
+            os.environ.pop("AT_PREDICT_RANK", None)
+            os.environ.pop("AT_RK_GRP", None)
+    assert_bits_equal(outs[0], outs[1], "scores (rank pass vs fp32 walk)")
+    fin = np.all(np.isfinite(X), axis=0)
+    es = O.OracleGbt(feat, th, ens["leaf"], base=0.25).predict(np.ascontiguousarray(X[:, fin].T))
+    assert_bits_equal(outs[0][fin], es, "scores vs oracle")
+
+
 def test_predict_rank_form_odd_feature_count(at):
     """F = 7 (the last rank pair has one feature), depth 8, 200 streamed trees; rank vs fp32 vs oracle."""
     rng = np.random.default_rng(5)
