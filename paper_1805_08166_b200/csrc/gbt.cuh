@@ -62,6 +62,7 @@ constexpr int TS_MAXBUF = 4;
 #ifndef AT_SA_SPEC
 #define AT_SA_SPEC 1   // speculative levels of the eb walk: 1 = the root's children + the leaf pair (measured best)
 #endif
+static_assert(AT_SA_SPEC >= 1, "the eb walk's root step always loads the root's children");
 
 constexpr uint32_t TREE_BUF_BYTES = 48 * 1024;   // default per buffer (two buffers)
 #ifdef AT_SA_PHASE_TIMING
